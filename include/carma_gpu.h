@@ -1,0 +1,248 @@
+/* carma_gpu.h — C ABI of the B200-native CARMA hot path.
+ *
+ * Drop-in boundary for the two stages of the reference's data-parallel path
+ * (see DESIGN.md §2 and INTEGRATION.md). Plain pointers and sizes only; no
+ * C++ or torch types cross this boundary. Every call returns a
+ * carma_status; carma_last_error() gives the thread-local message. No
+ * exception crosses the boundary and there is no CPU fallback: without a
+ * usable sm_100 device every compute entry point fails with
+ * CARMA_ERR_CUDA.
+ *
+ * Stage 1 — GPUMemNet (the reference's k-NN memory-bin classifier):
+ *   carma_knn_*    replaces LearnedEstimator::predict / predict_scalar
+ *                  (proj/include/carma/estimators.hpp:115, src/estimators.cpp:438-475)
+ *                  and estimate_learned (estimators.hpp:140-142,
+ *                  src/estimators.cpp:540-551), batched; a handle holds one
+ *                  model per ModelFamily like Manager::set_learned_estimators
+ *                  (manager.hpp:77) so rows route by family (manager.cpp:91-97).
+ * Stage 2 — placement scoring and trace replay:
+ *   carma_pick_batch   replaces Manager::eligible_gpus + map_task
+ *                      (manager.hpp:82-86, src/manager.cpp:109-245) for a batch of
+ *                      independent decisions on GPU snapshots.
+ *   carma_replay_*     replaces run_simulation's event loop for many
+ *                      independent traces (runner.hpp:49, src/runner.cpp:40-147;
+ *                      World::run/step/place/finish world.hpp:73-90; the Manager
+ *                      pipeline manager.cpp:247-357) and the per-trace part of
+ *                      compute_report (metrics.cpp:16-70) — the engine under
+ *                      run_sweep (runner.hpp:72).
+ */
+#ifndef CARMA_GPU_H
+#define CARMA_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum carma_status {
+    CARMA_OK = 0,
+    CARMA_ERR_INVALID = 1,     /* bad argument / ConfigError, NonPositiveRange, EmptyDataset */
+    CARMA_ERR_CUDA = 2,        /* no device, launch or copy failure */
+    CARMA_ERR_OVERFLOW = 3,    /* a trace exceeded every state capacity tier */
+    CARMA_ERR_FAMILY = 4,      /* FamilyMismatch: no model for a requested family */
+    CARMA_ERR_UNSUPPORTED = 5, /* a config outside the kernel's domain (e.g. MIG) */
+    CARMA_ERR_INCOMPLETE = 6   /* IncompleteRun: a trace could not finish */
+} carma_status;
+
+const char* carma_last_error(void);
+int carma_version(void);
+/* Number of usable sm_100 devices (0 when none). */
+int carma_device_count(void);
+
+/* ------------------------------------------------------------ stage 1 */
+
+#define CARMA_FEATURE_DIMS 19
+#define CARMA_MAX_K 32
+#define CARMA_FAMILIES 3 /* ModelFamily: 0 MLP, 1 CNN, 2 Transformer (task.hpp:30) */
+
+/* The FeatureVector summary a prediction consumes (task.hpp:89-100):
+ * tallies, activation (cos, sin) and the first / middle / last layer tuples
+ * (kind code, activations, params) that scalar_features reads
+ * (estimators.cpp:317-342). has_layers = 0 leaves dims 9..17 at zero. */
+typedef struct carma_feature_row {
+    uint64_t n_linear, n_batchnorm, n_dropout, n_conv;
+    uint64_t batch_size, total_params, total_activations;
+    double act_cos, act_sin;
+    int32_t kind[3];
+    int32_t has_layers;
+    uint64_t tuple_acts[3];
+    uint64_t tuple_params[3];
+} carma_feature_row; /* 136 bytes */
+
+typedef struct carma_knn carma_knn;
+
+/* Row formats accepted by carma_knn_predict_device. */
+#define CARMA_ROWS_FEATURES 0 /* carma_feature_row[q] */
+#define CARMA_ROWS_SCALAR 1   /* double[q][19] raw scalar features */
+
+carma_status carma_knn_create(int device, carma_knn** out);
+carma_status carma_knn_destroy(carma_knn* h);
+/* Installs the model of one family: min/max bounds, the n normalised training
+ * points (row-major n x 19, training order) and their labels, as produced by
+ * train_learned_estimator (estimators.cpp:344-395). */
+carma_status carma_knn_set_model(carma_knn* h, int32_t family, const double* lo,
+                                 const double* hi, const double* points,
+                                 const int32_t* labels, uint64_t n, uint32_t k,
+                                 uint64_t bucket_range);
+
+/* Host-buffer batch predict (the drop-in for estimate_learned over q rows).
+ * family: per-row family (nullable: every row is default_family).
+ * bucket_out[i] = LearnedEstimator::predict; bytes_out[i] = (bucket+1)*range.
+ * Rows whose family has no model get bucket -1 and bytes UINT64_MAX
+ * (FamilyMismatch -> no estimate, manager.cpp:99-105). Either output may be
+ * NULL. H2D, compute and D2H are pipelined in chunks on the handle's
+ * streams. */
+carma_status carma_knn_predict(carma_knn* h, const carma_feature_row* rows,
+                               const int8_t* family, int32_t default_family, uint64_t q,
+                               int32_t* bucket_out, uint64_t* bytes_out);
+/* Same over raw 19-feature rows (predict_scalar). */
+carma_status carma_knn_predict_scalar(carma_knn* h, const double* raw, const int8_t* family,
+                                      int32_t default_family, uint64_t q,
+                                      int32_t* bucket_out, uint64_t* bytes_out);
+/* Device-resident predict: all pointers are device pointers on the handle's
+ * device; runs on `stream` (a cudaStream_t, NULL = the handle's stream).
+ * topk_d2 / topk_idx (nullable, q x k) receive the k nearest (d2, training
+ * index) pairs in ascending (d2, index) order for parity checks. */
+carma_status carma_knn_predict_device(carma_knn* h, const void* rows, int32_t format,
+                                      const int8_t* family, int32_t default_family,
+                                      uint64_t q, int32_t* bucket_out, uint64_t* bytes_out,
+                                      double* topk_d2, int64_t* topk_idx, void* stream);
+/* Kernel statistics of the last predict: launches and the number of (query,
+ * point) distance evaluations performed. */
+carma_status carma_knn_last_stats(carma_knn* h, uint64_t* launches, uint64_t* evaluations);
+
+/* ------------------------------------------------------------ stage 2 */
+
+#define CARMA_POLICY_EXCLUSIVE 0 /* manager.hpp:15 */
+#define CARMA_POLICY_RR 1
+#define CARMA_POLICY_MAGM 2
+#define CARMA_POLICY_LUG 3
+#define CARMA_POLICY_MUG 4
+#define CARMA_MODE_STREAMS 0 /* gpu.hpp:14 */
+#define CARMA_MODE_MPS 1
+#define CARMA_MODE_MIG 2 /* not supported by the replay kernel */
+#define CARMA_NO_ESTIMATE UINT64_MAX
+#define CARMA_MAX_GPUS 64
+
+/* PolicyConfig (manager.hpp:29-37) + SimConstants (memory_model.hpp:11-29). */
+typedef struct carma_replay_config {
+    int32_t policy;
+    int32_t mode;
+    int32_t gpu_count;
+    int32_t rr_apply_preconditions;
+    double max_smact;
+    uint64_t min_free; /* PreconditionSet::min_free_mem; 0 == unset */
+    double monitor_window;
+    uint64_t gpu_capacity;
+    uint64_t alloc_block;
+    double p_idle_w, p_max_w, p_boost_w, boost_threshold;
+    double oom_startup_delay;
+} carma_replay_config;
+
+/* One materialised task (TaskSpec, task.hpp:63-80) as the replay sees it. */
+typedef struct carma_task {
+    double submit;     /* submit_time */
+    double work;       /* total_work() = epochs * nominal_epoch_time */
+    double demand;     /* smact_demand */
+    uint64_t true_mem; /* true_mem_bytes */
+    uint64_t estimate; /* make_estimate(task).bytes, CARMA_NO_ESTIMATE for none */
+    uint32_t gpus;     /* gpus_requested */
+    uint32_t rank;     /* rank of the task id in std::string order within its trace */
+} carma_task;          /* 48 bytes */
+
+/* TaskTiming (manager.hpp:39-46) + TaskRun placement (world.hpp:32-44). */
+typedef struct carma_task_result {
+    double first_attempt;  /* dispatch_attempts.front(), -1 when none */
+    double final_dispatch; /* -1 when never placed */
+    double complete;       /* -1 when never completed */
+    double first_crash;    /* crash_times.front(), -1 when none */
+    double last_crash;     /* crash_times.back(), -1 when none */
+    double executed;       /* TaskRun::executed_integral */
+    uint32_t attempts;     /* dispatch_attempts.size() */
+    uint32_t ooms;         /* TaskTiming::oom_count */
+    int16_t gpu[2];        /* TaskRun::gpu_ids, -1 padded */
+    uint32_t reserved;
+} carma_task_result; /* 64 bytes */
+
+/* RunReport scalars (metrics.hpp:44-57) + replay counters. */
+typedef struct carma_trace_result {
+    double trace_total_time;
+    double avg_wait, avg_exec, avg_jct;
+    double energy_mj;
+    double first_submit, last_complete;
+    double end_time; /* World::now() when the queue ran dry */
+    int32_t oom_count;
+    int32_t status;  /* carma_status of this trace */
+    uint64_t events; /* World::step pops */
+} carma_trace_result; /* 80 bytes */
+
+typedef struct carma_gpu_result {
+    double energy_j;   /* after the overshoot correction (runner.cpp:117-120) */
+    double mean_smact; /* windowed_smact(last_complete, span) (runner.cpp:135-137) */
+    uint64_t peak_used;
+    uint64_t smact_steps; /* size of the SMACT step history */
+} carma_gpu_result;      /* 32 bytes */
+
+/* A replay job: one trace under one config. Task results of job j are laid
+ * out at sum_{i<j} n_tasks(job_i); GPU results at sum_{i<j} gpu_count(job_i). */
+typedef struct carma_replay_job {
+    uint32_t trace;
+    uint32_t config;
+} carma_replay_job;
+
+typedef struct carma_replay_plan carma_replay_plan;
+
+/* Uploads configs, tasks (trace t = tasks[trace_offsets[t] .. trace_offsets[t+1]))
+ * and jobs to `device`. want_task_results = 0 skips per-task outputs. */
+carma_status carma_replay_plan_create(int device, const carma_replay_config* configs,
+                                      uint32_t n_configs, const carma_task* tasks,
+                                      const uint64_t* trace_offsets, uint32_t n_traces,
+                                      const carma_replay_job* jobs, uint32_t n_jobs,
+                                      int32_t want_task_results, carma_replay_plan** out);
+/* Overrides every task's estimate with a device array (one u64 per task, same
+ * indexing as `tasks`), e.g. the bytes_out of carma_knn_predict_device. */
+carma_status carma_replay_plan_set_estimates_device(carma_replay_plan* p, const uint64_t* est);
+/* Runs all jobs on the device (inputs resident). stream: cudaStream_t or NULL. */
+carma_status carma_replay_plan_run(carma_replay_plan* p, void* stream);
+carma_status carma_replay_plan_results(carma_replay_plan* p, carma_task_result* tasks,
+                                       carma_trace_result* traces, carma_gpu_result* gpus);
+/* Kernel launches of the last run and the state tier each job finished in. */
+carma_status carma_replay_plan_stats(carma_replay_plan* p, uint64_t* launches,
+                                     uint64_t* retried_jobs);
+carma_status carma_replay_plan_destroy(carma_replay_plan* p);
+
+/* One-shot host API: create + run + results + destroy (the run_sweep engine). */
+carma_status carma_replay_batch(int device, const carma_replay_config* configs,
+                                uint32_t n_configs, const carma_task* tasks,
+                                const uint64_t* trace_offsets, uint32_t n_traces,
+                                const carma_replay_job* jobs, uint32_t n_jobs,
+                                carma_task_result* task_results,
+                                carma_trace_result* trace_results,
+                                carma_gpu_result* gpu_results);
+
+/* --- batched placement scoring (eligible_gpus + map_task) --- */
+typedef struct carma_gpu_view {
+    uint64_t total_free;   /* GpuDevice::total_free() */
+    double windowed_smact; /* windowed_smact(now, monitor_window) */
+    int32_t idle;          /* no residents */
+    int32_t reserved;
+} carma_gpu_view;
+
+typedef struct carma_pick_request {
+    uint64_t estimate; /* CARMA_NO_ESTIMATE for none */
+    uint32_t want;     /* gpus_requested (1 or 2) */
+    int32_t from_recovery;
+} carma_pick_request;
+
+/* n decisions over n x n_gpus views (row-major), each with its own RR cursor
+ * (in/out). out_gpus is n x 2 (-1 padded; {-1,-1} = defer). Host buffers. */
+carma_status carma_pick_batch(int device, const carma_replay_config* cfg,
+                              const carma_gpu_view* views, uint32_t n_gpus,
+                              const carma_pick_request* reqs, uint64_t n,
+                              int32_t* rr_cursor, int32_t* out_gpus);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CARMA_GPU_H */

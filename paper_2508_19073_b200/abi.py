@@ -1,0 +1,167 @@
+"""ctypes binding of include/carma_gpu.h and include/carma_host.h.
+
+Loads the in-tree ``libcarma_b200.so`` (built by ``__graft_entry__.build()``
+or ``make -C paper_2508_19073_b200/csrc``). There is no fallback: if the
+library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_uint32, c_uint64, c_void_p
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcarma_b200.so")
+
+CARMA_OK = 0
+STATUS_NAMES = {
+    0: "OK", 1: "INVALID", 2: "CUDA", 3: "OVERFLOW", 4: "FAMILY", 5: "UNSUPPORTED", 6: "INCOMPLETE",
+}
+
+POLICY = {"exclusive": 0, "rr": 1, "magm": 2, "lug": 3, "mug": 4}
+MODE = {"streams": 0, "mps": 1, "mig": 2}
+FAMILY = {"mlp": 0, "cnn": 1, "transformer": 2}
+ESTIMATOR = {"none": 0, "oracle": 1, "analytical": 2, "static_graph": 3, "learned": 4}
+MIX = {"t90": 0, "t60": 1}
+NO_ESTIMATE = np.uint64(0xFFFFFFFFFFFFFFFF)
+ROWS_FEATURES, ROWS_SCALAR = 0, 1
+GiB = 1 << 30
+MiB = 1 << 20
+
+feature_row_dtype = np.dtype([
+    ("n_linear", "<u8"), ("n_batchnorm", "<u8"), ("n_dropout", "<u8"), ("n_conv", "<u8"),
+    ("batch_size", "<u8"), ("total_params", "<u8"), ("total_activations", "<u8"),
+    ("act_cos", "<f8"), ("act_sin", "<f8"), ("kind", "<i4", (3,)), ("has_layers", "<i4"),
+    ("tuple_acts", "<u8", (3,)), ("tuple_params", "<u8", (3,)),
+], align=True)
+
+replay_config_dtype = np.dtype([
+    ("policy", "<i4"), ("mode", "<i4"), ("gpu_count", "<i4"), ("rr_apply_preconditions", "<i4"),
+    ("max_smact", "<f8"), ("min_free", "<u8"), ("monitor_window", "<f8"),
+    ("gpu_capacity", "<u8"), ("alloc_block", "<u8"),
+    ("p_idle_w", "<f8"), ("p_max_w", "<f8"), ("p_boost_w", "<f8"), ("boost_threshold", "<f8"),
+    ("oom_startup_delay", "<f8"),
+], align=True)
+
+task_dtype = np.dtype([
+    ("submit", "<f8"), ("work", "<f8"), ("demand", "<f8"), ("true_mem", "<u8"),
+    ("estimate", "<u8"), ("gpus", "<u4"), ("rank", "<u4"),
+], align=True)
+
+task_result_dtype = np.dtype([
+    ("first_attempt", "<f8"), ("final_dispatch", "<f8"), ("complete", "<f8"),
+    ("first_crash", "<f8"), ("last_crash", "<f8"), ("executed", "<f8"),
+    ("attempts", "<u4"), ("ooms", "<u4"), ("gpu", "<i2", (2,)), ("reserved", "<u4"),
+], align=True)
+
+trace_result_dtype = np.dtype([
+    ("trace_total_time", "<f8"), ("avg_wait", "<f8"), ("avg_exec", "<f8"), ("avg_jct", "<f8"),
+    ("energy_mj", "<f8"), ("first_submit", "<f8"), ("last_complete", "<f8"), ("end_time", "<f8"),
+    ("oom_count", "<i4"), ("status", "<i4"), ("events", "<u8"),
+], align=True)
+
+gpu_result_dtype = np.dtype([
+    ("energy_j", "<f8"), ("mean_smact", "<f8"), ("peak_used", "<u8"), ("smact_steps", "<u8"),
+], align=True)
+
+job_dtype = np.dtype([("trace", "<u4"), ("config", "<u4")], align=True)
+
+gpu_view_dtype = np.dtype([
+    ("total_free", "<u8"), ("windowed_smact", "<f8"), ("idle", "<i4"), ("reserved", "<i4"),
+], align=True)
+
+pick_request_dtype = np.dtype([
+    ("estimate", "<u8"), ("want", "<u4"), ("from_recovery", "<i4"),
+], align=True)
+
+assert feature_row_dtype.itemsize == 136
+assert replay_config_dtype.itemsize == 96
+assert task_dtype.itemsize == 48
+assert task_result_dtype.itemsize == 64
+assert trace_result_dtype.itemsize == 80
+assert gpu_result_dtype.itemsize == 32
+assert gpu_view_dtype.itemsize == 24
+assert pick_request_dtype.itemsize == 16
+
+P = c_void_p  # every array crosses as a raw pointer
+
+# name -> (restype, argtypes); mirrors the two headers exactly.
+SIGNATURES = {
+    # carma_gpu.h
+    "carma_last_error": (c_char_p, []),
+    "carma_version": (c_int, []),
+    "carma_device_count": (c_int, []),
+    "carma_knn_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "carma_knn_destroy": (c_int, [c_void_p]),
+    "carma_knn_set_model": (c_int, [c_void_p, c_int32, P, P, P, P, c_uint64, c_uint32, c_uint64]),
+    "carma_knn_predict": (c_int, [c_void_p, P, P, c_int32, c_uint64, P, P]),
+    "carma_knn_predict_scalar": (c_int, [c_void_p, P, P, c_int32, c_uint64, P, P]),
+    "carma_knn_predict_device": (c_int, [c_void_p, P, c_int32, P, c_int32, c_uint64, P, P, P, P, c_void_p]),
+    "carma_knn_last_stats": (c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64)]),
+    "carma_replay_plan_create": (c_int, [c_int, P, c_uint32, P, P, c_uint32, P, c_uint32, c_int32,
+                                         POINTER(c_void_p)]),
+    "carma_replay_plan_set_estimates_device": (c_int, [c_void_p, P]),
+    "carma_replay_plan_run": (c_int, [c_void_p, c_void_p]),
+    "carma_replay_plan_results": (c_int, [c_void_p, P, P, P]),
+    "carma_replay_plan_stats": (c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64)]),
+    "carma_replay_plan_destroy": (c_int, [c_void_p]),
+    "carma_replay_batch": (c_int, [c_int, P, c_uint32, P, P, c_uint32, P, c_uint32, P, P, P]),
+    "carma_pick_batch": (c_int, [c_int, P, P, c_uint32, P, c_uint64, P, P]),
+    # carma_host.h
+    "carma_host_catalog_size": (c_int, []),
+    "carma_host_catalog_entry": (c_int, [c_int, c_char_p, c_int, P, P, P, P]),
+    "carma_host_generate_trace": (c_int, [c_int32, c_uint64, P, P, P, c_uint64, POINTER(c_uint64)]),
+    "carma_host_generate_uniform_trace": (c_int, [c_uint64, c_double, c_uint64, P, P, P]),
+    "carma_host_save_trace": (c_int, [c_char_p, c_uint64, c_char_p, P, P, P, c_uint64]),
+    "carma_host_load_trace": (c_int, [c_char_p, P, P, P, c_uint64, POINTER(c_uint64)]),
+    "carma_host_materialize": (c_int, [P, P, P, c_uint64, P, P, P]),
+    "carma_host_estimates": (c_int, [c_int32, c_uint64, P, c_uint64, P]),
+    "carma_host_dataset": (c_int, [c_int32, c_uint64, c_uint64, P, P, P]),
+    "carma_host_fit": (c_int, [c_int32, c_uint64, c_uint64, c_uint32, P, P, P, P, c_uint64,
+                               POINTER(c_uint64), POINTER(c_uint64), P, POINTER(c_uint64)]),
+    "carma_host_scalar_features": (c_int, [P, c_uint64, P]),
+}
+
+
+class CarmaError(RuntimeError):
+    """A non-OK carma_status; .status holds the code (reference: CarmaError, errors.hpp:12)."""
+
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int) -> None:
+    if status != CARMA_OK:
+        raise CarmaError(status, lib.carma_last_error().decode(errors="replace"))
+
+
+def ptr(a) -> int | None:
+    """Raw data pointer of a numpy array / torch tensor (None passes NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays crossing the C ABI must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    if isinstance(a, int):
+        return a
+    raise TypeError(f"cannot pass {type(a)} across the C ABI")

@@ -1,0 +1,497 @@
+"""Reference-shaped host API over the C ABI.
+
+Mirrors the parts of the reference's public C++ API that sit on the hot path
+(names follow proj/include/carma/*.hpp):
+
+* ``generate_synthetic_dataset`` / ``train_learned_estimator`` /
+  ``LearnedEstimator.predict`` / ``estimate_learned``  (estimators.hpp:98-142)
+* ``generate_trace`` / ``materialize_trace`` / ``save_trace`` / ``load_trace``
+  (traces.hpp:42-62)
+* ``PolicyConfig`` / ``SimConstants`` / ``RunConfig`` / ``run_simulation`` /
+  ``run_sweep`` (manager.hpp:29-37, memory_model.hpp:11-29, runner.hpp:18-72)
+* ``pick_batch``: batched ``Manager::eligible_gpus`` + ``map_task``
+  (manager.hpp:82-86)
+
+Everything numeric runs in libcarma_b200.so: the k-NN and the replay on the
+GPU, trace/dataset provisioning in its host C++ half. Errors surface as
+:class:`abi.CarmaError` (the reference's CarmaError family).
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+from typing import Dict, Iterable, List, Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from .abi import check, lib, ptr
+
+# ----------------------------------------------------------------- catalog
+
+
+@dataclasses.dataclass(frozen=True)
+class CatalogEntry:
+    key: str
+    family: int
+    gpus: int
+    batch: int
+    mem_gib: float
+
+
+def builtin_catalog() -> List[CatalogEntry]:
+    out = []
+    for i in range(lib.carma_host_catalog_size()):
+        key = ctypes.create_string_buffer(96)
+        fam, gpus, batch, mem = ctypes.c_int32(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_double()
+        check(lib.carma_host_catalog_entry(i, key, 96, ctypes.addressof(fam), ctypes.addressof(gpus),
+                                           ctypes.addressof(batch), ctypes.addressof(mem)))
+        out.append(CatalogEntry(key.value.decode(), fam.value, gpus.value, batch.value, mem.value))
+    return out
+
+
+# ------------------------------------------------------------------ traces
+
+
+@dataclasses.dataclass
+class Trace:
+    """TraceFile (traces.hpp:43-52): rows of (submit_s, catalog index, epochs)."""
+
+    submit: np.ndarray
+    entry: np.ndarray
+    epochs: np.ndarray
+    seed: int = 0
+    mix: str = ""
+
+    def __len__(self) -> int:
+        return len(self.submit)
+
+
+def generate_trace(mix: str, seed: int) -> Trace:
+    cap = 128
+    sub = np.zeros(cap, np.float64)
+    ent = np.zeros(cap, np.int32)
+    ep = np.zeros(cap, np.uint64)
+    n = ctypes.c_uint64()
+    check(lib.carma_host_generate_trace(abi.MIX[mix], seed, ptr(sub), ptr(ent), ptr(ep), cap, ctypes.byref(n)))
+    k = n.value
+    return Trace(sub[:k].copy(), ent[:k].copy(), ep[:k].copy(), seed, mix)
+
+
+def generate_uniform_trace(n: int, mean_gap: float, seed: int) -> Trace:
+    sub = np.zeros(n, np.float64)
+    ent = np.zeros(n, np.int32)
+    ep = np.zeros(n, np.uint64)
+    check(lib.carma_host_generate_uniform_trace(n, mean_gap, seed, ptr(sub), ptr(ent), ptr(ep)))
+    return Trace(sub, ent, ep, seed, "uniform")
+
+
+def save_trace(trace: Trace, path: str) -> None:
+    check(lib.carma_host_save_trace(path.encode(), trace.seed, trace.mix.encode(), ptr(trace.submit),
+                                    ptr(trace.entry), ptr(trace.epochs), len(trace)))
+
+
+def load_trace(path: str) -> Trace:
+    n = ctypes.c_uint64()
+    check(lib.carma_host_load_trace(path.encode(), None, None, None, 0, ctypes.byref(n)))
+    sub = np.zeros(n.value, np.float64)
+    ent = np.zeros(n.value, np.int32)
+    ep = np.zeros(n.value, np.uint64)
+    check(lib.carma_host_load_trace(path.encode(), ptr(sub), ptr(ent), ptr(ep), n.value, ctypes.byref(n)))
+    return Trace(sub, ent, ep)
+
+
+@dataclasses.dataclass
+class Materialized:
+    tasks: np.ndarray      # task_dtype
+    features: np.ndarray   # feature_row_dtype
+    family: np.ndarray     # int8
+    entry: np.ndarray      # int32 catalog index
+
+
+def materialize_trace(trace: Trace) -> Materialized:
+    n = len(trace)
+    tasks = np.zeros(n, abi.task_dtype)
+    feats = np.zeros(n, abi.feature_row_dtype)
+    fam = np.zeros(n, np.int8)
+    check(lib.carma_host_materialize(ptr(trace.submit), ptr(trace.entry), ptr(trace.epochs), n, ptr(tasks),
+                                     ptr(feats), ptr(fam)))
+    return Materialized(tasks, feats, fam, trace.entry.copy())
+
+
+def set_persona_estimates(m: Materialized, estimator: str, safety_margin: int = 2 * abi.GiB) -> None:
+    """oracle / analytical / static_graph / none into m.tasks['estimate'] (manager.cpp:80-107)."""
+    check(lib.carma_host_estimates(abi.ESTIMATOR[estimator], safety_margin, ptr(m.entry), len(m.tasks),
+                                   ptr(m.tasks)))
+
+
+# ---------------------------------------------------------------- datasets
+
+
+@dataclasses.dataclass
+class EstimatorDataset:
+    rows: np.ndarray     # feature_row_dtype
+    bucket: np.ndarray   # int32
+    mem: np.ndarray      # uint64
+    family: int
+    seed: int
+
+    @property
+    def bucket_range(self) -> int:
+        return abi.GiB if self.family == 0 else 8 * abi.GiB
+
+
+def generate_synthetic_dataset(family: int, n: int, seed: int) -> EstimatorDataset:
+    rows = np.zeros(n, abi.feature_row_dtype)
+    b = np.zeros(n, np.int32)
+    m = np.zeros(n, np.uint64)
+    check(lib.carma_host_dataset(family, n, seed, ptr(rows), ptr(b), ptr(m)))
+    return EstimatorDataset(rows, b, m, family, seed)
+
+
+def scalar_features(rows: np.ndarray) -> np.ndarray:
+    out = np.zeros((len(rows), 19), np.float64)
+    rows = np.ascontiguousarray(rows)
+    check(lib.carma_host_scalar_features(ptr(rows), len(rows), ptr(out)))
+    return out
+
+
+@dataclasses.dataclass
+class HoldoutReport:
+    accuracy: float = 0.0
+    macro_f1: float = 0.0
+    train_size: int = 0
+    holdout_size: int = 0
+    underestimate_rate: float = 0.0
+
+
+@dataclasses.dataclass
+class KnnModel:
+    family: int
+    k: int
+    bucket_range: int
+    lo: np.ndarray
+    hi: np.ndarray
+    points: np.ndarray   # n x 19 normalised
+    labels: np.ndarray   # int32
+    holdout_rows: np.ndarray
+    seed: int = 0
+
+
+def fit_knn(family: int, samples: int, seed: int, k: int = 5) -> KnnModel:
+    lo = np.zeros(19)
+    hi = np.zeros(19)
+    pts = np.zeros((samples, 19))
+    lab = np.zeros(samples, np.int32)
+    hold = np.zeros(samples, np.uint64)
+    n, br, nh = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib.carma_host_fit(family, samples, seed, k, ptr(lo), ptr(hi), ptr(pts), ptr(lab), samples,
+                             ctypes.byref(n), ctypes.byref(br), ptr(hold), ctypes.byref(nh)))
+    return KnnModel(family, k, br.value, lo, hi, pts[: n.value].copy(), lab[: n.value].copy(),
+                    hold[: nh.value].astype(np.int64), seed)
+
+
+class GpuKnn:
+    """A device-resident bank of k-NN models, one per family (the drop-in for
+    Manager::set_learned_estimators + estimate_learned, manager.cpp:91-97)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = ctypes.c_void_p()
+        check(lib.carma_knn_create(device, ctypes.byref(h)))
+        self._h = h
+        self.models: Dict[int, KnnModel] = {}
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def set_model(self, m: KnnModel) -> None:
+        pts = np.ascontiguousarray(m.points, np.float64)
+        check(lib.carma_knn_set_model(self._h, m.family, ptr(m.lo), ptr(m.hi), ptr(pts), ptr(m.labels), len(m.labels),
+                                      m.k, m.bucket_range))
+        self.models[m.family] = m
+
+    def predict(self, rows: np.ndarray, family=None, default_family: Optional[int] = None):
+        """Buckets and upper-edge bytes for feature rows (or raw n x 19 scalar rows)."""
+        q = len(rows)
+        bucket = np.zeros(q, np.int32)
+        nbytes = np.zeros(q, np.uint64)
+        fam = None if family is None else np.ascontiguousarray(family, np.int8)
+        dflt = default_family if default_family is not None else next(iter(self.models))
+        rows = np.ascontiguousarray(rows)
+        if rows.dtype == abi.feature_row_dtype:
+            check(lib.carma_knn_predict(self._h, ptr(rows), ptr(fam), dflt, q, ptr(bucket), ptr(nbytes)))
+        else:
+            rows = np.ascontiguousarray(rows, np.float64)
+            check(lib.carma_knn_predict_scalar(self._h, ptr(rows), ptr(fam), dflt, q, ptr(bucket), ptr(nbytes)))
+        return bucket, nbytes
+
+    def last_stats(self):
+        la, ev = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.carma_knn_last_stats(self._h, ctypes.byref(la), ctypes.byref(ev)))
+        return la.value, ev.value
+
+    def close(self) -> None:
+        if self._h:
+            lib.carma_knn_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LearnedEstimator:
+    """train_learned_estimator's product (estimators.hpp:108-133) on the GPU."""
+
+    def __init__(self, model: KnnModel, knn: GpuKnn, holdout: HoldoutReport):
+        self.model = model
+        self.knn = knn
+        self.holdout = holdout
+
+    @property
+    def family(self) -> int:
+        return self.model.family
+
+    @property
+    def bucket_range(self) -> int:
+        return self.model.bucket_range
+
+    def predict(self, rows: np.ndarray) -> np.ndarray:
+        return self.knn.predict(rows, default_family=self.model.family)[0]
+
+
+def train_learned_estimator(family: int, samples: int, seed: int, k: int = 5, device: int = 0,
+                            knn: Optional[GpuKnn] = None) -> LearnedEstimator:
+    """Fit on generate_synthetic_dataset(family, samples, seed) and score the
+    30% holdout with the GPU predict (estimators.cpp:344-436)."""
+    m = fit_knn(family, samples, seed, k)
+    knn = knn or GpuKnn(device)
+    knn.set_model(m)
+    ds = generate_synthetic_dataset(family, samples, seed)
+    rep = HoldoutReport(train_size=len(m.labels), holdout_size=len(m.holdout_rows))
+    if len(m.holdout_rows):
+        rows = ds.rows[m.holdout_rows]
+        pred, nbytes = knn.predict(rows, default_family=family)
+        gold = ds.bucket[m.holdout_rows]
+        rep.accuracy = float(np.count_nonzero(pred == gold)) / len(gold)
+        rep.underestimate_rate = float(np.count_nonzero(nbytes < ds.mem[m.holdout_rows])) / len(gold)
+        f1 = 0.0
+        classes = 0
+        for label in sorted(set(pred.tolist()) | set(gold.tolist())):
+            tp = float(np.count_nonzero((pred == label) & (gold == label)))
+            fp = float(np.count_nonzero((pred == label) & (gold != label)))
+            fn = float(np.count_nonzero((pred != label) & (gold == label)))
+            if tp + fn == 0:
+                continue
+            prec = tp / (tp + fp) if tp + fp > 0 else 0.0
+            rec = tp / (tp + fn)
+            f1 += 2 * prec * rec / (prec + rec) if prec + rec > 0 else 0.0
+            classes += 1
+        rep.macro_f1 = f1 / classes if classes else 0.0
+    return LearnedEstimator(m, knn, rep)
+
+
+# ---------------------------------------------------------------- replay
+
+
+@dataclasses.dataclass
+class SimConstants:
+    gpu_capacity: int = 40 * abi.GiB
+    gpu_count: int = 4
+    alloc_block: int = 512 * abi.MiB
+    p_idle_w: float = 55.0
+    p_max_w: float = 400.0
+    p_boost_w: float = 30.0
+    boost_threshold: float = 0.9
+    oom_startup_delay: float = 5.0
+
+
+@dataclasses.dataclass
+class PolicyConfig:
+    policy: str = "magm"
+    max_smact: float = 0.80
+    min_free_mem: Optional[int] = None
+    safety_margin: int = 2 * abi.GiB
+    estimator: str = "none"
+    collocation_mode: str = "mps"
+    monitor_window: float = 60.0
+    rr_apply_preconditions: bool = False
+
+
+def make_config(policy: PolicyConfig, consts: SimConstants) -> np.ndarray:
+    c = np.zeros(1, abi.replay_config_dtype)
+    c["policy"] = abi.POLICY[policy.policy]
+    c["mode"] = abi.MODE[policy.collocation_mode]
+    c["gpu_count"] = consts.gpu_count
+    c["rr_apply_preconditions"] = int(policy.rr_apply_preconditions)
+    c["max_smact"] = policy.max_smact
+    c["min_free"] = policy.min_free_mem or 0
+    c["monitor_window"] = policy.monitor_window
+    c["gpu_capacity"] = consts.gpu_capacity
+    c["alloc_block"] = consts.alloc_block
+    c["p_idle_w"] = consts.p_idle_w
+    c["p_max_w"] = consts.p_max_w
+    c["p_boost_w"] = consts.p_boost_w
+    c["boost_threshold"] = consts.boost_threshold
+    c["oom_startup_delay"] = consts.oom_startup_delay
+    return c
+
+
+@dataclasses.dataclass
+class ReplayResult:
+    tasks: np.ndarray     # task_result_dtype, per job concatenated
+    traces: np.ndarray    # trace_result_dtype, per job
+    gpus: np.ndarray      # gpu_result_dtype, per job concatenated
+    task_offsets: np.ndarray
+    gpu_offsets: np.ndarray
+
+    def job_tasks(self, j: int) -> np.ndarray:
+        return self.tasks[self.task_offsets[j]: self.task_offsets[j + 1]]
+
+    def job_gpus(self, j: int) -> np.ndarray:
+        return self.gpus[self.gpu_offsets[j]: self.gpu_offsets[j + 1]]
+
+
+class ReplayPlan:
+    """Device-resident replay jobs (carma_replay_plan_*)."""
+
+    def __init__(self, configs: np.ndarray, tasks: np.ndarray, trace_offsets: np.ndarray, jobs: np.ndarray,
+                 device: int = 0, want_task_results: bool = True):
+        self.configs = np.ascontiguousarray(configs, abi.replay_config_dtype)
+        self.tasks = np.ascontiguousarray(tasks, abi.task_dtype)
+        self.trace_offsets = np.ascontiguousarray(trace_offsets, np.uint64)
+        self.jobs = np.ascontiguousarray(jobs, abi.job_dtype)
+        h = ctypes.c_void_p()
+        check(lib.carma_replay_plan_create(device, ptr(self.configs), len(self.configs), ptr(self.tasks),
+                                           ptr(self.trace_offsets), len(self.trace_offsets) - 1, ptr(self.jobs),
+                                           len(self.jobs), int(want_task_results), ctypes.byref(h)))
+        self._h = h
+        n_t = np.diff(self.trace_offsets.astype(np.int64))[self.jobs["trace"]]
+        n_g = self.configs["gpu_count"][self.jobs["config"]].astype(np.int64)
+        self.task_offsets = np.concatenate([[0], np.cumsum(n_t)])
+        self.gpu_offsets = np.concatenate([[0], np.cumsum(n_g)])
+
+    def set_estimates_device(self, dev_ptr: int) -> None:
+        check(lib.carma_replay_plan_set_estimates_device(self._h, dev_ptr))
+
+    def run(self, stream: int = 0) -> None:
+        check(lib.carma_replay_plan_run(self._h, stream or None))
+
+    def results(self, tasks: bool = True) -> ReplayResult:
+        tr = np.zeros(int(self.task_offsets[-1]) if tasks else 0, abi.task_result_dtype)
+        jr = np.zeros(len(self.jobs), abi.trace_result_dtype)
+        gr = np.zeros(int(self.gpu_offsets[-1]), abi.gpu_result_dtype)
+        check(lib.carma_replay_plan_results(self._h, ptr(tr) if tasks else None, ptr(jr), ptr(gr)))
+        return ReplayResult(tr, jr, gr, self.task_offsets, self.gpu_offsets)
+
+    def stats(self):
+        la, rt = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.carma_replay_plan_stats(self._h, ctypes.byref(la), ctypes.byref(rt)))
+        return la.value, rt.value
+
+    def close(self) -> None:
+        if self._h:
+            lib.carma_replay_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def replay(configs: np.ndarray, task_lists: Sequence[np.ndarray], jobs: Iterable = None,
+           device: int = 0) -> ReplayResult:
+    """One-shot batch replay: traces = task_lists, jobs = [(trace, config)] (default: all x all)."""
+    offs = np.concatenate([[0], np.cumsum([len(t) for t in task_lists])]).astype(np.uint64)
+    tasks = np.concatenate(task_lists) if len(task_lists) > 1 else np.ascontiguousarray(task_lists[0])
+    if jobs is None:
+        jobs = [(t, c) for c in range(len(configs)) for t in range(len(task_lists))]
+    jarr = np.array(list(jobs), dtype=np.uint32).reshape(-1, 2)
+    j = np.zeros(len(jarr), abi.job_dtype)
+    j["trace"] = jarr[:, 0]
+    j["config"] = jarr[:, 1]
+    plan = ReplayPlan(configs, tasks, offs, j, device)
+    try:
+        plan.run()
+        res = plan.results()
+    finally:
+        plan.close()
+    bad = res.traces["status"] != 0
+    if bad.any():
+        st = int(res.traces["status"][bad][0])
+        raise abi.CarmaError(abi.CARMA_OK + (3 if st < 0 else st),
+                             f"{int(bad.sum())} job(s) failed (first status {st})")
+    return res
+
+
+# ----------------------------------------------------------------- runner
+
+
+@dataclasses.dataclass
+class RunConfig:
+    """runner.hpp:18-40 (trace source, policy, constants, estimator provisioning)."""
+
+    mix: Optional[str] = "t90"
+    trace_seed: int = 1
+    trace_path: Optional[str] = None
+    policy: PolicyConfig = dataclasses.field(default_factory=PolicyConfig)
+    constants: SimConstants = dataclasses.field(default_factory=SimConstants)
+    estimator_seed: int = 11
+    estimator_k: int = 5
+    estimator_samples: int = 4000
+
+
+def provision_estimates(rc: RunConfig, m: Materialized, device: int = 0,
+                        knn: Optional[GpuKnn] = None) -> None:
+    """make_estimate for every task (manager.cpp:80-107); learned via the GPU k-NN bank
+    trained like provision_estimators (runner.cpp:17-38)."""
+    est = rc.policy.estimator
+    if est != "learned":
+        set_persona_estimates(m, est, rc.policy.safety_margin)
+        return
+    knn = knn or GpuKnn(device)
+    for fam in sorted(set(m.family.tolist())):
+        if fam not in knn.models:
+            seed = rc.estimator_seed + fam * 101
+            knn.set_model(fit_knn(fam, rc.estimator_samples, seed, rc.estimator_k))
+    _, nbytes = knn.predict(m.features, family=m.family)
+    m.tasks["estimate"] = nbytes
+
+
+def run_simulation(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None):
+    """Replays one trace on the GPU; returns (trace result, task results, gpu results)."""
+    trace = load_trace(rc.trace_path) if rc.trace_path else generate_trace(rc.mix, rc.trace_seed)
+    m = materialize_trace(trace)
+    provision_estimates(rc, m, device, knn)
+    res = replay(make_config(rc.policy, rc.constants), [m.tasks], device=device)
+    return res.traces[0], res.job_tasks(0), res.job_gpus(0)
+
+
+def median(values) -> float:
+    """runner.cpp:149-155"""
+    v = sorted(values)
+    n = len(v)
+    if n == 0:
+        return 0.0
+    return v[n // 2] if n % 2 else 0.5 * (v[n // 2 - 1] + v[n // 2])
+
+
+# ------------------------------------------------------------------ pick
+
+
+def pick_batch(cfg: np.ndarray, views: np.ndarray, reqs: np.ndarray, rr_cursor: np.ndarray, device: int = 0):
+    """Batched eligible_gpus + map_task: views (n x G gpu_view), reqs (n pick_request)."""
+    n, g = views.shape
+    views = np.ascontiguousarray(views, abi.gpu_view_dtype)
+    reqs = np.ascontiguousarray(reqs, abi.pick_request_dtype)
+    cur = np.ascontiguousarray(rr_cursor, np.int32).copy()
+    out = np.zeros((n, 2), np.int32)
+    check(lib.carma_pick_batch(device, ptr(cfg), ptr(views), g, ptr(reqs), n, ptr(cur), ptr(out)))
+    return out, cur

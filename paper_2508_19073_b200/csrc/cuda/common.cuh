@@ -1,0 +1,91 @@
+// Shared device/host helpers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../host/status.hpp"
+
+namespace carma_b200 {
+
+#define CARMA_CUDA(call)                                                                  \
+    do {                                                                                  \
+        cudaError_t err__ = (call);                                                       \
+        if (err__ != cudaSuccess)                                                         \
+            throw ::carma_b200::CudaFailure(std::string(#call) + ": " +                  \
+                                            cudaGetErrorString(err__));                   \
+    } while (0)
+
+// Throws unless `device` is a usable sm_100 device. No CPU fallback exists:
+// every compute entry point calls this first.
+void require_device(int device);
+
+// RAII device buffer (grow-only).
+struct DeviceBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t want) {
+        if (want <= bytes) return;
+        release();
+        if (want == 0) return;
+        CARMA_CUDA(cudaMalloc(&ptr, want));
+        bytes = want;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(ptr);
+    }
+    ~DeviceBuffer() { release(); }
+};
+
+// RAII pinned host buffer (grow-only).
+struct PinnedBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t want) {
+        if (want <= bytes) return;
+        release();
+        if (want == 0) return;
+        CARMA_CUDA(cudaMallocHost(&ptr, want));
+        bytes = want;
+    }
+    void release() {
+        if (ptr) cudaFreeHost(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(ptr);
+    }
+    ~PinnedBuffer() { release(); }
+};
+
+// Scoped device switch.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CARMA_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) CARMA_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+bool is_pinned(const void* p);
+
+inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 1u << 20) {
+    uint64_t g = (n + block - 1) / block;
+    if (g == 0) g = 1;
+    return static_cast<unsigned>(g < cap ? g : cap);
+}
+
+}  // namespace carma_b200

@@ -1,0 +1,697 @@
+// Stage 1 — GPUMemNet (the reference's k-NN memory-bin classifier) on sm_100a.
+//
+// Semantics: LearnedEstimator::predict_scalar + estimate_learned
+// (proj/src/estimators.cpp:438-475, :540-551), bit-exact:
+//   q[d]  = hi>lo ? (raw-lo)/(hi-lo) : 0                    (:439-441)
+//   d2    = sum_{d=0..18} diff_d^2 in dim order, diff_18 *= 64 (:445-457)
+//   top-k = k smallest (d2, training index) pairs              (:460-462)
+//   vote  = most votes, ties to the larger bucket             (:463-474)
+//   bytes = (bucket + 1) * bucket_range                        (:540-551)
+// Built with --fmad=false: every sub/mul/add is rounded separately, as in
+// the reference's FMA-free x86-64 build.
+//
+// Algorithm (exact, not approximate). Because every term is >= 0 and
+// rounding is monotone, a point's computed d2 is >= its own last term
+// t18 = fl(fl(64*fl(p18-q18))^2). Training points are stored sorted by p18,
+// so t18 grows monotonically walking outward from q18's position; a side can
+// be abandoned as soon as its next t18 exceeds the current k-th best d2 —
+// every point beyond it provably cannot enter the top-k, ties included.
+// Queries are bucketed by (family, position of q18 in the sorted model) so a
+// warp holds 32 queries with nearly identical search windows; the warp walks
+// one common frontier and every lane evaluates the same point, so model
+// reads are warp-uniform broadcasts from L1. Per query the work drops from
+// N = 2800 to the window size (~150-300 points).
+//
+// Pipeline per batch (all on one stream):
+//   knn_keys     featurise dim 18, normalise, binary-search -> (bin, pos); CTA histograms
+//   scan_matrix  exclusive scan of the [bin][cta] histogram matrix
+//   knn_scatter  counting-sort scatter of row ids into bin order
+//   knn_search   warp-per-32-queries frontier search + fused vote/bucket/bytes epilogue
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <vector>
+
+#include "../../../include/carma_gpu.h"
+#include "common.cuh"
+
+namespace carma_b200 {
+namespace {
+
+constexpr int kDims = 19;
+constexpr int kStride = 20;  // doubles per stored point (160 B, 16-B aligned)
+constexpr int kMaxK = 16;
+constexpr uint32_t kInvalidBin = 0xffffffffu;
+constexpr int kScatterCtas = 296;  // 2 per SM on a 148-SM B200
+constexpr int kMaxBins = 4096;
+
+struct ModelDev {
+    const double* pts;    // N x 20, sorted by (p18, original index)
+    const double* key18;  // N, pts[i][18]
+    const int32_t* orig;  // N, original training index
+    const int32_t* label_by_orig;
+    uint64_t n;
+    uint64_t bucket_range;
+    uint32_t k;
+    uint32_t bin_base;
+    uint32_t bin_shift;
+    int32_t present;
+    double lo[kDims];
+    double hi[kDims];
+};
+
+struct KnnParams {
+    ModelDev m[CARMA_FAMILIES];
+    const void* rows;
+    int32_t format;
+    const int8_t* family;
+    int32_t default_family;
+    uint64_t q;
+};
+
+__device__ __forceinline__ double u2d(uint64_t v) { return __ull2double_rn(v); }
+
+// scalar_features dim d of a feature row (estimators.cpp:317-342).
+__device__ __forceinline__ void featurize(const carma_feature_row& r, double* raw) {
+    raw[0] = u2d(r.n_linear);
+    raw[1] = u2d(r.n_batchnorm);
+    raw[2] = u2d(r.n_dropout);
+    raw[3] = u2d(r.n_conv);
+    raw[4] = u2d(r.batch_size);
+    raw[5] = u2d(r.total_params);
+    raw[6] = u2d(r.total_activations);
+    raw[7] = r.act_cos;
+    raw[8] = r.act_sin;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const bool h = r.has_layers != 0;
+        raw[9 + 3 * k] = h ? static_cast<double>(r.kind[k]) : 0.0;
+        raw[10 + 3 * k] = h ? u2d(r.tuple_acts[k]) : 0.0;
+        raw[11 + 3 * k] = h ? u2d(r.tuple_params[k]) : 0.0;
+    }
+    raw[18] = __dadd_rn(__dmul_rn(16.0, raw[5]), __dmul_rn(__dmul_rn(4.0, raw[4]), raw[6]));
+}
+
+__device__ __forceinline__ double raw18_of(const KnnParams& p, uint64_t i) {
+    if (p.format == CARMA_ROWS_SCALAR) return static_cast<const double*>(p.rows)[i * kDims + 18];
+    const carma_feature_row& r = static_cast<const carma_feature_row*>(p.rows)[i];
+    return __dadd_rn(__dmul_rn(16.0, u2d(r.total_params)),
+                     __dmul_rn(__dmul_rn(4.0, u2d(r.batch_size)), u2d(r.total_activations)));
+}
+
+__device__ __forceinline__ double normalize(double raw, double lo, double hi) {
+    return hi > lo ? __ddiv_rn(__dsub_rn(raw, lo), __dsub_rn(hi, lo)) : 0.0;
+}
+
+__device__ __forceinline__ int family_of(const KnnParams& p, uint64_t i) {
+    const int f = p.family ? static_cast<int>(p.family[i]) : p.default_family;
+    return (f >= 0 && f < CARMA_FAMILIES && p.m[f].present) ? f : -1;
+}
+
+// first index with key18[i] >= x
+__device__ __forceinline__ uint32_t lower_bound(const double* key, uint64_t n, double x) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (__ldg(key + mid) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return static_cast<uint32_t>(lo);
+}
+
+// Pass 1: bin and start position per row; per-CTA histogram -> hist[bin][cta].
+__global__ void knn_keys(KnnParams p, uint32_t n_bins, uint32_t* __restrict__ qbin,
+                         uint32_t* __restrict__ qpos, uint32_t* __restrict__ hist) {
+    extern __shared__ uint32_t sh[];
+    for (uint32_t b = threadIdx.x; b < n_bins; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    const uint64_t per = (p.q + gridDim.x - 1) / gridDim.x;
+    const uint64_t beg = per * blockIdx.x;
+    const uint64_t end = min(p.q, beg + per);
+    for (uint64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+        const int f = family_of(p, i);
+        uint32_t bin = kInvalidBin, pos = 0;
+        if (f >= 0) {
+            const ModelDev& m = p.m[f];
+            const double q18 = normalize(raw18_of(p, i), m.lo[18], m.hi[18]);
+            pos = lower_bound(m.key18, m.n, q18);
+            bin = m.bin_base + (pos >> m.bin_shift);
+        }
+        const uint32_t b = bin == kInvalidBin ? n_bins - 1 : bin;
+        qbin[i] = b;
+        qpos[i] = pos;
+        atomicAdd(&sh[b], 1u);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < n_bins; b += blockDim.x)
+        hist[static_cast<uint64_t>(b) * gridDim.x + blockIdx.x] = sh[b];
+}
+
+// Exclusive scan of n u32 values by one CTA of 1024 threads.
+__global__ void scan_matrix(uint32_t* __restrict__ v, uint64_t n) {
+    __shared__ uint32_t part[1024];
+    const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint64_t beg = per * threadIdx.x, end = min(n, beg + per);
+    uint32_t s = 0;
+    for (uint64_t i = beg; i < end; ++i) s += v[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (unsigned off = 1; off < blockDim.x; off <<= 1) {
+        const uint32_t add = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+        __syncthreads();
+        part[threadIdx.x] += add;
+        __syncthreads();
+    }
+    uint32_t run = part[threadIdx.x] - s;
+    for (uint64_t i = beg; i < end; ++i) {
+        const uint32_t x = v[i];
+        v[i] = run;
+        run += x;
+    }
+}
+
+// Pass 2: scatter row ids into bin order (same CTA tiling as knn_keys).
+__global__ void knn_scatter(uint64_t q, uint32_t n_bins, const uint32_t* __restrict__ qbin,
+                            const uint32_t* __restrict__ base, uint32_t* __restrict__ perm) {
+    extern __shared__ uint32_t sh[];
+    for (uint32_t b = threadIdx.x; b < n_bins; b += blockDim.x)
+        sh[b] = base[static_cast<uint64_t>(b) * gridDim.x + blockIdx.x];
+    __syncthreads();
+    const uint64_t per = (q + gridDim.x - 1) / gridDim.x;
+    const uint64_t beg = per * blockIdx.x;
+    const uint64_t end = min(q, beg + per);
+    for (uint64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+        const uint32_t slot = atomicAdd(&sh[qbin[i]], 1u);
+        perm[slot] = static_cast<uint32_t>(i);
+    }
+}
+
+// k best (d2, training index) pairs, ascending, register resident. For a
+// runtime k < K the first K-k slots hold (-inf, INT_MIN) sentinels that never
+// move, so the k-th best is always slot K-1 (static register indexing).
+template <int K>
+struct TopK {
+    double d[K];
+    int32_t id[K];
+    __device__ __forceinline__ void init(int k) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const bool sentinel = j < K - k;
+            d[j] = __longlong_as_double(sentinel ? 0xfff0000000000000ll : 0x7ff0000000000000ll);
+            id[j] = sentinel ? static_cast<int32_t>(0x80000000u) : 0x7fffffff;
+        }
+    }
+    __device__ __forceinline__ double kth() const { return d[K - 1]; }
+    __device__ __forceinline__ void insert(double d2, int32_t oi) {
+        if (!(d2 < d[K - 1] || (d2 == d[K - 1] && oi < id[K - 1]))) return;
+        bool placed = false;
+#pragma unroll
+        for (int j = K - 1; j >= 0; --j) {
+            if (placed) continue;
+            const bool prev_greater =
+                j > 0 && (d[j - 1] > d2 || (d[j - 1] == d2 && id[j - 1] > oi));
+            if (prev_greater) {
+                d[j] = d[j - 1];
+                id[j] = id[j - 1];
+            } else {
+                d[j] = d2;
+                id[j] = oi;
+                placed = true;
+            }
+        }
+    }
+};
+
+__device__ __forceinline__ double t18_of(double key, double q18) {
+    const double diff = __dmul_rn(__dsub_rn(key, q18), 64.0);
+    return __dmul_rn(diff, diff);
+}
+
+template <int K>
+__global__ void __launch_bounds__(128)
+    knn_search(KnnParams p, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ qpos,
+               int32_t* __restrict__ bucket_out, uint64_t* __restrict__ bytes_out,
+               double* __restrict__ topk_d2, int64_t* __restrict__ topk_idx,
+               unsigned long long* __restrict__ evals) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long my_evals = 0;
+
+    for (uint64_t w = warp; w * 32 < p.q; w += n_warps) {
+        const uint64_t slot = w * 32 + lane;
+        const bool live = slot < p.q;
+        const uint32_t row = live ? perm[slot] : 0;
+        const int fam = live ? family_of(p, row) : -1;
+        if (live && fam < 0) {  // FamilyMismatch -> no estimate
+            if (bucket_out) bucket_out[row] = -1;
+            if (bytes_out) bytes_out[row] = ~0ull;
+        }
+        unsigned pending = __ballot_sync(0xffffffffu, fam >= 0);
+        while (pending) {
+            const int f = __shfl_sync(0xffffffffu, fam, __ffs(pending) - 1);
+            const bool mine = fam == f && ((pending >> lane) & 1u);
+            const unsigned members = __ballot_sync(0xffffffffu, mine);
+            pending &= ~members;
+            const ModelDev& m = p.m[f];
+            const int k = static_cast<int>(m.k < K ? m.k : K);
+
+            // Query in registers (normalised), same arithmetic as estimators.cpp:439-441.
+            double q[kDims];
+            if (mine) {
+                double raw[kDims];
+                if (p.format == CARMA_ROWS_SCALAR) {
+                    const double* r = static_cast<const double*>(p.rows) + static_cast<uint64_t>(row) * kDims;
+#pragma unroll
+                    for (int d = 0; d < kDims; ++d) raw[d] = r[d];
+                } else {
+                    featurize(static_cast<const carma_feature_row*>(p.rows)[row], raw);
+                }
+#pragma unroll
+                for (int d = 0; d < kDims; ++d) q[d] = normalize(raw[d], m.lo[d], m.hi[d]);
+            } else {
+#pragma unroll
+                for (int d = 0; d < kDims; ++d) q[d] = 0.0;
+            }
+            TopK<K> top;
+            top.init(k);
+
+            // Common frontier: evaluated range [L, R), started at the middle
+            // member's position. A lane's own position pos may differ from the
+            // start, so its per-side lower bound is t18 of the next point only
+            // when that side moves away from pos; otherwise it is t_in, the
+            // minimum t18 around pos (t18 decreases toward pos, then grows).
+            unsigned mm = members;
+            for (int j = (__popc(members) - 1) / 2; j > 0; --j) mm &= mm - 1;
+            const int mid_lane = __ffs(mm) - 1;
+            const int64_t n = static_cast<int64_t>(m.n);
+            const int64_t pos = live ? static_cast<int64_t>(qpos[row]) : 0;
+            const int64_t start = __shfl_sync(0xffffffffu, pos, mid_lane);
+            int64_t L = start, R = start;
+            const double inf = __longlong_as_double(0x7ff0000000000000ll);
+            const double t_in = fmin(pos > 0 ? t18_of(__ldg(m.key18 + pos - 1), q[18]) : inf,
+                                     pos < n ? t18_of(__ldg(m.key18 + pos), q[18]) : inf);
+            double tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q[18]) : t_in) : inf;
+            double tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q[18]) : t_in) : inf;
+            uint64_t steps = 0;
+            for (;;) {
+                const double kth = top.kth();
+                const bool need_l = mine && L > 0 && tl <= kth;
+                const bool need_r = mine && R < n && tr <= kth;
+                const unsigned bl = __ballot_sync(0xffffffffu, need_l);
+                const unsigned br = __ballot_sync(0xffffffffu, need_r);
+                if ((bl | br) == 0) break;
+                // Best-first for the representative lane, else whichever side is wanted.
+                const double rl = __shfl_sync(0xffffffffu, need_l ? tl : inf, mid_lane);
+                const double rr = __shfl_sync(0xffffffffu, need_r ? tr : inf, mid_lane);
+                const bool go_left = bl != 0 && (br == 0 || rl <= rr);
+                const int64_t i = go_left ? --L : R++;
+                const double2* pt = reinterpret_cast<const double2*>(m.pts + i * kStride);
+                double d2 = 0.0;
+#pragma unroll
+                for (int h = 0; h < 9; ++h) {
+                    const double2 v = __ldg(pt + h);
+                    const double a = __dsub_rn(v.x, q[2 * h]);
+                    d2 = __dadd_rn(d2, __dmul_rn(a, a));
+                    const double b = __dsub_rn(v.y, q[2 * h + 1]);
+                    d2 = __dadd_rn(d2, __dmul_rn(b, b));
+                }
+                {
+                    const double v = __ldg(m.pts + i * kStride + 18);
+                    const double a = __dmul_rn(__dsub_rn(v, q[18]), 64.0);
+                    d2 = __dadd_rn(d2, __dmul_rn(a, a));
+                }
+                const int32_t oi = __ldg(m.orig + i);
+                if (mine) top.insert(d2, oi);
+                if (go_left) tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q[18]) : t_in) : inf;
+                else tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q[18]) : t_in) : inf;
+                ++steps;
+            }
+            my_evals += steps * static_cast<unsigned long long>(__popc(members));
+
+            if (mine) {
+                // Vote over the kk = min(k, n) neighbours (estimators.cpp:463-474):
+                // real entries are slots [K-k, K) whose id is a training index.
+                int best = 0, best_votes = 0;
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    if (a < K - k || top.id[a] == 0x7fffffff) continue;
+                    const int la = __ldg(m.label_by_orig + top.id[a]);
+                    int votes = 0;
+#pragma unroll
+                    for (int b = 0; b < K; ++b)
+                        if (b >= K - k && top.id[b] != 0x7fffffff && __ldg(m.label_by_orig + top.id[b]) == la)
+                            ++votes;
+                    if (votes > best_votes || (votes == best_votes && la > best)) {
+                        best = la;
+                        best_votes = votes;
+                    }
+                }
+                if (bucket_out) bucket_out[row] = best;
+                if (bytes_out) bytes_out[row] = (static_cast<uint64_t>(best) + 1ull) * m.bucket_range;
+                if (topk_d2 || topk_idx) {
+#pragma unroll
+                    for (int a = 0; a < K; ++a) {
+                        if (a < K - k) continue;
+                        const uint64_t o = static_cast<uint64_t>(row) * m.k + (a - (K - k));
+                        const bool real = top.id[a] != 0x7fffffff;
+                        if (topk_d2) topk_d2[o] = real ? top.d[a] : inf;
+                        if (topk_idx) topk_idx[o] = real ? top.id[a] : -1;
+                    }
+                }
+            }
+        }
+    }
+    if (evals && lane == 0 && my_evals) atomicAdd(evals, my_evals);
+}
+
+struct HostModel {
+    DeviceBuffer pts, key18, orig, label_by_orig;
+    uint64_t n = 0;
+    uint64_t bucket_range = 0;
+    uint32_t k = 0;
+    double lo[kDims], hi[kDims];
+    bool present = false;
+};
+
+}  // namespace
+
+struct KnnHandle {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t pipe[2] = {nullptr, nullptr};
+    HostModel model[CARMA_FAMILIES];
+    struct Scratch {
+        DeviceBuffer rows, family, qbin, qpos, perm, hist, bucket, bytes;
+        PinnedBuffer stage_rows, stage_family;
+    } scratch[2];
+    DeviceBuffer evals;
+    uint64_t last_launches = 0, last_evals = 0;
+    std::mutex mu;
+};
+
+namespace {
+
+KnnParams make_params(const KnnHandle& h, uint32_t* n_bins) {
+    KnnParams p{};
+    uint32_t base = 0;
+    for (int f = 0; f < CARMA_FAMILIES; ++f) {
+        const HostModel& hm = h.model[f];
+        ModelDev& m = p.m[f];
+        m.present = hm.present ? 1 : 0;
+        if (!hm.present) continue;
+        m.pts = hm.pts.as<double>();
+        m.key18 = hm.key18.as<double>();
+        m.orig = hm.orig.as<int32_t>();
+        m.label_by_orig = hm.label_by_orig.as<int32_t>();
+        m.n = hm.n;
+        m.bucket_range = hm.bucket_range;
+        m.k = hm.k;
+        std::memcpy(m.lo, hm.lo, sizeof(m.lo));
+        std::memcpy(m.hi, hm.hi, sizeof(m.hi));
+        uint32_t shift = 0;
+        while (((hm.n + (1ull << shift) - 1) >> shift) > (kMaxBins / CARMA_FAMILIES) - 1) ++shift;
+        m.bin_shift = shift;
+        m.bin_base = base;
+        base += static_cast<uint32_t>((hm.n >> shift) + 1);
+    }
+    *n_bins = base + 1;  // + invalid-family bin
+    return p;
+}
+
+int max_k(const KnnHandle& h) {
+    uint32_t k = 1;
+    for (const auto& m : h.model)
+        if (m.present) k = std::max(k, m.k);
+    return static_cast<int>(k);
+}
+
+void launch_search(const KnnParams& p, int kmax, const uint32_t* perm, const uint32_t* qpos,
+                   int32_t* bucket, uint64_t* bytes, double* d2, int64_t* idx,
+                   unsigned long long* evals, cudaStream_t s) {
+    const uint64_t warps = (p.q + 31) / 32;
+    const unsigned block = 128;
+    const unsigned grid = grid_for(warps * 32, block, 148u * 64u);
+    if (kmax <= 5)
+        knn_search<5><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+    else if (kmax <= 8)
+        knn_search<8><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+    else
+        knn_search<kMaxK><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+}
+
+// Runs the 4-kernel pipeline on device-resident rows.
+uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, int32_t format,
+                      const int8_t* family, int32_t default_family, uint64_t q,
+                      int32_t* bucket, uint64_t* bytes, double* d2, int64_t* idx,
+                      unsigned long long* evals, cudaStream_t s) {
+    uint32_t n_bins = 0;
+    KnnParams p = make_params(h, &n_bins);
+    p.rows = rows;
+    p.format = format;
+    p.family = family;
+    p.default_family = default_family;
+    p.q = q;
+    const unsigned ctas = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(kScatterCtas, (q + 4095) / 4096)));
+    sc.qbin.ensure(q * 4);
+    sc.qpos.ensure(q * 4);
+    sc.perm.ensure(q * 4);
+    sc.hist.ensure(static_cast<size_t>(n_bins) * ctas * 4);
+    const size_t shmem = n_bins * 4;
+    knn_keys<<<ctas, 512, shmem, s>>>(p, n_bins, sc.qbin.as<uint32_t>(), sc.qpos.as<uint32_t>(),
+                                      sc.hist.as<uint32_t>());
+    scan_matrix<<<1, 1024, 0, s>>>(sc.hist.as<uint32_t>(), static_cast<uint64_t>(n_bins) * ctas);
+    knn_scatter<<<ctas, 512, shmem, s>>>(q, n_bins, sc.qbin.as<uint32_t>(), sc.hist.as<uint32_t>(),
+                                         sc.perm.as<uint32_t>());
+    launch_search(p, max_k(h), sc.perm.as<uint32_t>(), sc.qpos.as<uint32_t>(), bucket, bytes, d2, idx,
+                  evals, s);
+    CARMA_CUDA(cudaGetLastError());
+    return 4;
+}
+
+void check_ready(const KnnHandle* h) {
+    if (!h) throw InvalidArg("null handle");
+    bool any = false;
+    for (const auto& m : h->model) any |= m.present;
+    if (!any) throw CarmaFailure(CARMA_ERR_FAMILY, "no model installed");
+}
+
+carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int32_t format,
+                          const int8_t* family, int32_t default_family, uint64_t q,
+                          int32_t* bucket_out, uint64_t* bytes_out) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        check_ready(h);
+        if (q == 0) return;
+        if (!rows) throw InvalidArg("rows is null");
+        std::lock_guard<std::mutex> lock(h->mu);
+        DeviceGuard g(h->device);
+        const uint64_t chunk = 1ull << 20;
+        const bool rows_pinned = is_pinned(rows);
+        const bool fam_pinned = !family || is_pinned(family);
+        const bool out_pinned = (!bucket_out || is_pinned(bucket_out)) && (!bytes_out || is_pinned(bytes_out));
+        h->evals.ensure(8);
+        CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 8, h->pipe[0]));
+        CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
+        uint64_t launches = 0;
+        const uint64_t n_chunks = (q + chunk - 1) / chunk;
+        for (uint64_t c = 0; c < n_chunks; ++c) {
+            KnnHandle::Scratch& sc = h->scratch[c & 1];
+            cudaStream_t s = h->pipe[c & 1];
+            const uint64_t beg = c * chunk, cnt = std::min(chunk, q - beg);
+            const char* src = static_cast<const char*>(rows) + beg * row_bytes;
+            sc.rows.ensure(chunk * row_bytes);
+            sc.bucket.ensure(chunk * 4);
+            sc.bytes.ensure(chunk * 8);
+            if (family) sc.family.ensure(chunk);
+            if (!rows_pinned || !fam_pinned) {
+                // Stage through pinned memory; wait until this buffer's previous
+                // chunk has been consumed.
+                CARMA_CUDA(cudaStreamSynchronize(s));
+                sc.stage_rows.ensure(chunk * row_bytes);
+                std::memcpy(sc.stage_rows.ptr, src, cnt * row_bytes);
+                src = sc.stage_rows.as<char>();
+                if (family) {
+                    sc.stage_family.ensure(chunk);
+                    std::memcpy(sc.stage_family.ptr, family + beg, cnt);
+                }
+            }
+            CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, src, cnt * row_bytes, cudaMemcpyHostToDevice, s));
+            if (family)
+                CARMA_CUDA(cudaMemcpyAsync(sc.family.ptr,
+                                           (!rows_pinned || !fam_pinned) ? sc.stage_family.as<int8_t>() : family + beg,
+                                           cnt, cudaMemcpyHostToDevice, s));
+            launches += run_pipeline(*h, sc, sc.rows.ptr, format, family ? sc.family.as<int8_t>() : nullptr,
+                                     default_family, cnt, sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(),
+                                     nullptr, nullptr, h->evals.as<unsigned long long>(), s);
+            if (out_pinned) {
+                if (bucket_out)
+                    CARMA_CUDA(cudaMemcpyAsync(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost, s));
+                if (bytes_out)
+                    CARMA_CUDA(cudaMemcpyAsync(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost, s));
+            } else {
+                CARMA_CUDA(cudaStreamSynchronize(s));
+                if (bucket_out)
+                    CARMA_CUDA(cudaMemcpy(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost));
+                if (bytes_out)
+                    CARMA_CUDA(cudaMemcpy(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost));
+            }
+        }
+        CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
+        CARMA_CUDA(cudaStreamSynchronize(h->pipe[1]));
+        unsigned long long ev = 0;
+        CARMA_CUDA(cudaMemcpy(&ev, h->evals.ptr, 8, cudaMemcpyDeviceToHost));
+        h->last_launches = launches;
+        h->last_evals = ev;
+    });
+}
+
+}  // namespace
+}  // namespace carma_b200
+
+using namespace carma_b200;
+
+extern "C" {
+
+carma_status carma_knn_create(int device, carma_knn** out) {
+    return guarded([&] {
+        if (!out) throw InvalidArg("out is null");
+        require_device(device);
+        DeviceGuard g(device);
+        auto* h = new KnnHandle();
+        h->device = device;
+        CARMA_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CARMA_CUDA(cudaStreamCreateWithFlags(&h->pipe[0], cudaStreamNonBlocking));
+        CARMA_CUDA(cudaStreamCreateWithFlags(&h->pipe[1], cudaStreamNonBlocking));
+        *out = reinterpret_cast<carma_knn*>(h);
+    });
+}
+
+carma_status carma_knn_destroy(carma_knn* hh) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        if (!h) return;
+        {
+            DeviceGuard g(h->device);
+            cudaStreamSynchronize(h->stream);
+            cudaStreamSynchronize(h->pipe[0]);
+            cudaStreamSynchronize(h->pipe[1]);
+            for (auto& m : h->model) {
+                m.pts.release();
+                m.key18.release();
+                m.orig.release();
+                m.label_by_orig.release();
+            }
+            for (auto& sc : h->scratch) {
+                sc.rows.release(); sc.family.release(); sc.qbin.release(); sc.qpos.release();
+                sc.perm.release(); sc.hist.release(); sc.bucket.release(); sc.bytes.release();
+                sc.stage_rows.release(); sc.stage_family.release();
+            }
+            h->evals.release();
+            cudaStreamDestroy(h->stream);
+            cudaStreamDestroy(h->pipe[0]);
+            cudaStreamDestroy(h->pipe[1]);
+        }
+        delete h;
+    });
+}
+
+carma_status carma_knn_set_model(carma_knn* hh, int32_t family, const double* lo, const double* hi,
+                                 const double* points, const int32_t* labels, uint64_t n,
+                                 uint32_t k, uint64_t bucket_range) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        if (!h) throw InvalidArg("null handle");
+        if (family < 0 || family >= CARMA_FAMILIES) throw InvalidArg("unknown family");
+        if (n == 0) throw InvalidArg("EmptyDataset: model has no points");
+        if (n > 0x7fffffffull) throw InvalidArg("model too large");
+        if (k < 1) throw InvalidArg("k must be >= 1");
+        if (k > kMaxK) throw Unsupported("k > 16 is not supported by the GPU kernel");
+        if (bucket_range == 0) throw InvalidArg("NonPositiveRange: bucket range must be > 0");
+        if (!lo || !hi || !points || !labels) throw InvalidArg("null model array");
+        std::lock_guard<std::mutex> lock(h->mu);
+        DeviceGuard g(h->device);
+        // Sort by (p18, original index): the search order (see file header).
+        std::vector<int32_t> order(n);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+            return points[static_cast<uint64_t>(a) * kDims + 18] < points[static_cast<uint64_t>(b) * kDims + 18];
+        });
+        std::vector<double> pts(n * kStride, 0.0), key(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            const double* src = points + static_cast<uint64_t>(order[i]) * kDims;
+            std::memcpy(&pts[i * kStride], src, sizeof(double) * kDims);
+            key[i] = src[18];
+        }
+        HostModel& m = h->model[family];
+        m.pts.ensure(n * kStride * 8);
+        m.key18.ensure(n * 8);
+        m.orig.ensure(n * 4);
+        m.label_by_orig.ensure(n * 4);
+        CARMA_CUDA(cudaMemcpy(m.pts.ptr, pts.data(), n * kStride * 8, cudaMemcpyHostToDevice));
+        CARMA_CUDA(cudaMemcpy(m.key18.ptr, key.data(), n * 8, cudaMemcpyHostToDevice));
+        CARMA_CUDA(cudaMemcpy(m.orig.ptr, order.data(), n * 4, cudaMemcpyHostToDevice));
+        CARMA_CUDA(cudaMemcpy(m.label_by_orig.ptr, labels, n * 4, cudaMemcpyHostToDevice));
+        m.n = n;
+        m.k = k;
+        m.bucket_range = bucket_range;
+        std::memcpy(m.lo, lo, sizeof(m.lo));
+        std::memcpy(m.hi, hi, sizeof(m.hi));
+        m.present = true;
+    });
+}
+
+carma_status carma_knn_predict(carma_knn* h, const carma_feature_row* rows, const int8_t* family,
+                               int32_t default_family, uint64_t q, int32_t* bucket_out,
+                               uint64_t* bytes_out) {
+    return predict_host(h, rows, sizeof(carma_feature_row), CARMA_ROWS_FEATURES, family, default_family,
+                        q, bucket_out, bytes_out);
+}
+
+carma_status carma_knn_predict_scalar(carma_knn* h, const double* raw, const int8_t* family,
+                                      int32_t default_family, uint64_t q, int32_t* bucket_out,
+                                      uint64_t* bytes_out) {
+    return predict_host(h, raw, sizeof(double) * kDims, CARMA_ROWS_SCALAR, family, default_family, q,
+                        bucket_out, bytes_out);
+}
+
+carma_status carma_knn_predict_device(carma_knn* hh, const void* rows, int32_t format,
+                                      const int8_t* family, int32_t default_family, uint64_t q,
+                                      int32_t* bucket_out, uint64_t* bytes_out, double* topk_d2,
+                                      int64_t* topk_idx, void* stream) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        check_ready(h);
+        if (format != CARMA_ROWS_FEATURES && format != CARMA_ROWS_SCALAR) throw InvalidArg("unknown row format");
+        if (q == 0) return;
+        if (!rows) throw InvalidArg("rows is null");
+        std::lock_guard<std::mutex> lock(h->mu);
+        DeviceGuard g(h->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        h->evals.ensure(8);
+        CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 8, s));
+        h->last_launches = run_pipeline(*h, h->scratch[0], rows, format, family, default_family, q,
+                                        bucket_out, bytes_out, topk_d2, topk_idx,
+                                        h->evals.as<unsigned long long>(), s);
+    });
+}
+
+carma_status carma_knn_last_stats(carma_knn* hh, uint64_t* launches, uint64_t* evaluations) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        if (!h) throw InvalidArg("null handle");
+        DeviceGuard g(h->device);
+        unsigned long long ev = 0;
+        if (h->evals.ptr) {
+            CARMA_CUDA(cudaDeviceSynchronize());
+            CARMA_CUDA(cudaMemcpy(&ev, h->evals.ptr, 8, cudaMemcpyDeviceToHost));
+        }
+        if (launches) *launches = h->last_launches;
+        if (evaluations) *evaluations = ev;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+"""ctypes bindings of the test oracles (test infrastructure only).
+
+* ``oracle``  — oracle/build/liboracle.so: the CPU restatement (always buildable).
+* ``ref``     — oracle/_ref/libcarma_ref.so: the UNMODIFIED reference library +
+                marshalling shim; present when built here (needs /root/reference)
+                or shipped prebuilt to the GPU box.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_uint32, c_uint64, c_void_p
+
+import numpy as np
+
+from paper_2508_19073_b200 import abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "build", "liboracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libcarma_ref.so")
+P = c_void_p
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def load_oracle() -> ctypes.CDLL:
+    if not os.path.exists(ORACLE_SO):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "oracle"], check=True,
+                       stdout=subprocess.DEVNULL)
+    lib = ctypes.CDLL(ORACLE_SO)
+    lib.oracle_knn_predict.restype = c_int
+    lib.oracle_knn_predict.argtypes = [P, P, P, P, c_uint64, c_uint32, c_uint64, P, c_uint64, P, P, P, P]
+    lib.oracle_replay.restype = c_int
+    lib.oracle_replay.argtypes = [P, P, c_uint32, P, P, P]
+    lib.oracle_pick.restype = c_int
+    lib.oracle_pick.argtypes = [P, P, c_uint32, P, P, P]
+    return lib
+
+
+def load_ref():
+    if not os.path.exists(REF_SO):
+        return None
+    lib = ctypes.CDLL(REF_SO)
+    lib.ref_last_error.restype = c_char_p
+    lib.ref_train.argtypes = [c_int, c_uint64, c_uint64, c_uint64, c_char_p, P, P, P, P, c_uint64,
+                              POINTER(c_uint64), POINTER(c_uint64), P]
+    lib.ref_dataset.argtypes = [c_int, c_uint64, c_uint64, P, P, P]
+    lib.ref_dataset_fv.argtypes = [c_int, c_uint64, c_uint64, P, P, P, P, P]
+    lib.ref_predict_dataset.argtypes = [c_int, c_uint64, c_uint64, c_uint64, c_uint64, c_uint64, P, P]
+    lib.ref_bench_predict.restype = c_double
+    lib.ref_bench_predict.argtypes = [c_int, c_uint64, c_uint64, c_uint64, c_uint64, c_uint64, c_int, c_int,
+                                      POINTER(c_uint64)]
+    lib.ref_gen_trace.argtypes = [c_int, c_uint64, P, P, P, c_uint64, POINTER(c_uint64)]
+    lib.ref_save_trace.argtypes = [c_char_p, c_uint64, c_char_p, P, P, P, c_uint64]
+    lib.ref_materialize.argtypes = [c_char_p, c_uint64, P, P, P, P, P, P, P, P, P, c_int, POINTER(c_uint64)]
+    lib.ref_run.argtypes = [P, c_int, c_uint64, c_char_p, P, c_uint64, P, P, P, P]
+    lib.ref_bench_sweep.restype = c_double
+    lib.ref_bench_sweep.argtypes = [P, c_int, c_uint64, c_uint64, P, c_int, c_int, POINTER(c_uint64),
+                                    POINTER(c_double)]
+    return lib
+
+
+ref_config_dtype = np.dtype([
+    ("policy", "<i4"), ("estimator", "<i4"), ("mode", "<i4"), ("rr_apply_preconditions", "<i4"),
+    ("max_smact", "<f8"), ("has_min_free", "<i4"), ("min_free", "<u8"), ("safety_margin", "<u8"),
+    ("monitor_window", "<f8"), ("gpu_count", "<i4"), ("gpu_capacity", "<u8"), ("alloc_block", "<u8"),
+    ("estimator_seed", "<u8"), ("estimator_k", "<u8"), ("estimator_samples", "<u8"),
+], align=True)
+
+ref_task_out_dtype = np.dtype([
+    ("submit", "<f8"), ("first_attempt", "<f8"), ("final_dispatch", "<f8"), ("complete", "<f8"),
+    ("first_crash", "<f8"), ("last_crash", "<f8"), ("executed", "<f8"), ("n_attempts", "<u4"),
+    ("ooms", "<u4"), ("gpu0", "<i4"), ("gpu1", "<i4"),
+], align=True)
+
+ref_trace_out_dtype = np.dtype([
+    ("trace_total_time", "<f8"), ("avg_wait", "<f8"), ("avg_exec", "<f8"), ("avg_jct", "<f8"),
+    ("energy_mj", "<f8"), ("last_complete", "<f8"), ("first_submit", "<f8"), ("oom_count", "<i4"),
+    ("n_tasks", "<i4"),
+], align=True)
+
+
+def ref_config(policy="magm", estimator="none", mode="mps", rr_pre=False, max_smact=0.8, min_free=None,
+               margin=2 * abi.GiB, window=60.0, gpu_count=4, capacity=40 * abi.GiB, block=512 * abi.MiB,
+               est_seed=11, est_k=5, est_samples=4000):
+    c = np.zeros(1, ref_config_dtype)
+    c["policy"] = abi.POLICY[policy]
+    c["estimator"] = abi.ESTIMATOR[estimator]
+    c["mode"] = abi.MODE[mode]
+    c["rr_apply_preconditions"] = int(rr_pre)
+    c["max_smact"] = max_smact
+    c["has_min_free"] = int(min_free is not None)
+    c["min_free"] = min_free or 0
+    c["safety_margin"] = margin
+    c["monitor_window"] = window
+    c["gpu_count"] = gpu_count
+    c["gpu_capacity"] = capacity
+    c["alloc_block"] = block
+    c["estimator_seed"] = est_seed
+    c["estimator_k"] = est_k
+    c["estimator_samples"] = est_samples
+    return c
+
+
+def replay_config_from(c):
+    """The carma_replay_config equivalent of a ref config row."""
+    r = np.zeros(1, abi.replay_config_dtype)
+    for f in ("policy", "mode", "gpu_count", "rr_apply_preconditions", "max_smact", "monitor_window",
+              "gpu_capacity", "alloc_block"):
+        r[f] = c[f]
+    r["min_free"] = c["min_free"] if c["has_min_free"][0] else 0
+    r["p_idle_w"], r["p_max_w"], r["p_boost_w"], r["boost_threshold"] = 55.0, 400.0, 30.0, 0.9
+    r["oom_startup_delay"] = 5.0
+    return r
+
+
+def ref_run(ref, cfg, mix=None, seed=1, path=None, cap=1 << 20):
+    tout = np.zeros(cap, ref_task_out_dtype)
+    rout = np.zeros(1, ref_trace_out_dtype)
+    g = int(cfg["gpu_count"][0])
+    ge = np.zeros(g)
+    gs = np.zeros(g)
+    gp = np.zeros(g, np.uint64)
+    rc = ref.ref_run(_ptr(cfg), abi.MIX[mix] if mix else -1, seed, path.encode() if path else None,
+                     _ptr(tout), cap, _ptr(rout), _ptr(ge), _ptr(gs), _ptr(gp))
+    if rc != 0:
+        raise RuntimeError(ref.ref_last_error().decode())
+    n = int(rout["n_tasks"][0])
+    return tout[:n], rout[0], ge, gs, gp
+
+
+def oracle_replay(olib, cfg, tasks):
+    n = len(tasks)
+    tout = np.zeros(n, abi.task_result_dtype)
+    tr = np.zeros(1, abi.trace_result_dtype)
+    g = np.zeros(int(cfg["gpu_count"][0]), abi.gpu_result_dtype)
+    tasks = np.ascontiguousarray(tasks)
+    rc = olib.oracle_replay(_ptr(cfg), _ptr(tasks), n, _ptr(tout), _ptr(tr), _ptr(g))
+    return rc, tout, tr[0], g
+
+
+def oracle_predict(olib, m, raw, k=None):
+    raw = np.ascontiguousarray(raw, np.float64)
+    q = len(raw)
+    k = k or m.k
+    b = np.zeros(q, np.int32)
+    by = np.zeros(q, np.uint64)
+    d2 = np.zeros((q, k))
+    idx = np.zeros((q, k), np.int64)
+    pts = np.ascontiguousarray(m.points)
+    rc = olib.oracle_knn_predict(_ptr(m.lo), _ptr(m.hi), _ptr(pts), _ptr(m.labels), len(m.labels), k,
+                                 m.bucket_range, _ptr(raw), q, _ptr(b), _ptr(by), _ptr(d2), _ptr(idx))
+    assert rc == 0
+    return b, by, d2, idx
