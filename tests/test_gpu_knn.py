@@ -1,0 +1,143 @@
+"""Stage 1 parity on the GPU: carma_knn_* vs the oracle restatement of
+LearnedEstimator::predict_scalar (estimators.cpp:438-475). Bit-exact: buckets,
+bytes, and the k nearest (d2, training index) pairs."""
+import numpy as np
+import pytest
+
+import paper_2508_19073_b200 as cb
+from paper_2508_19073_b200 import abi
+from oracle_bind import oracle_predict
+
+pytestmark = pytest.mark.gpu
+
+FAMILIES = [(0, 11, 12345), (1, 112, 2024), (2, 213, 2025)]
+
+
+def _device_predict(knn, rows, family=None, default_family=0, k=5, fmt=abi.ROWS_FEATURES):
+    import torch
+
+    q = len(rows)
+    raw = torch.from_numpy(np.ascontiguousarray(rows).view(np.uint8).reshape(-1)).cuda()
+    fam = None if family is None else torch.from_numpy(np.ascontiguousarray(family, np.int8)).cuda()
+    b = torch.empty(q, dtype=torch.int32, device="cuda")
+    by = torch.empty(q, dtype=torch.int64, device="cuda")
+    d2 = torch.empty(q * k, dtype=torch.float64, device="cuda")
+    idx = torch.empty(q * k, dtype=torch.int64, device="cuda")
+    abi.check(abi.lib.carma_knn_predict_device(knn.handle, raw.data_ptr(), fmt,
+                                               None if fam is None else fam.data_ptr(), default_family, q,
+                                               b.data_ptr(), by.data_ptr(), d2.data_ptr(), idx.data_ptr(), None))
+    torch.cuda.synchronize()
+    return (b.cpu().numpy(), by.cpu().numpy().view(np.uint64), d2.cpu().numpy().reshape(q, k),
+            idx.cpu().numpy().reshape(q, k))
+
+
+@pytest.fixture(scope="module")
+def models():
+    return {f: cb.fit_knn(f, 4000, s, 5) for f, s, _ in FAMILIES}
+
+
+@pytest.mark.parametrize("fam,seed,qseed", FAMILIES)
+def test_knn_matches_oracle_bit_exact(gpu, olib, models, fam, seed, qseed):
+    m = models[fam]
+    knn = cb.GpuKnn(gpu)
+    knn.set_model(m)
+    ds = cb.generate_synthetic_dataset(fam, 4096, qseed)
+    raw = cb.scalar_features(ds.rows)
+    ob, oby, od2, oidx = oracle_predict(olib, m, raw)
+    b, by = knn.predict(ds.rows, default_family=fam)
+    assert np.array_equal(b, ob)
+    assert np.array_equal(by, oby)
+    gb, gby, gd2, gidx = _device_predict(knn, ds.rows, default_family=fam)
+    assert np.array_equal(gb, ob)
+    assert np.array_equal(gd2.view(np.uint64), od2.view(np.uint64))  # same IEEE bits
+    assert np.array_equal(gidx, oidx)
+    # raw 19-feature rows (predict_scalar) give the same answer
+    sb, sby = knn.predict(raw, default_family=fam)
+    assert np.array_equal(sb, ob)
+    launches, evals = knn.last_stats()
+    assert launches >= 4 and 0 < evals < 4096 * len(m.labels)
+
+
+def test_bank_routes_by_family_and_flags_mismatch(gpu, olib, models):
+    knn = cb.GpuKnn(gpu)
+    knn.set_model(models[1])
+    knn.set_model(models[2])  # no MLP model: family 0 rows -> no estimate
+    rows, fams, want_b = [], [], []
+    for f, _, qs in FAMILIES:
+        ds = cb.generate_synthetic_dataset(f, 700, qs + 1)
+        rows.append(ds.rows)
+        fams.append(np.full(700, f, np.int8))
+        if f == 0:
+            want_b.append(np.full(700, -1, np.int32))
+        else:
+            want_b.append(oracle_predict(olib, models[f], cb.scalar_features(ds.rows))[0])
+    rows = np.concatenate(rows)
+    fams = np.concatenate(fams)
+    want_b = np.concatenate(want_b)
+    perm = np.random.default_rng(5).permutation(len(rows))
+    b, by = knn.predict(rows[perm], family=fams[perm])
+    assert np.array_equal(b, want_b[perm])
+    assert np.all(by[fams[perm] == 0] == np.uint64(0xFFFFFFFFFFFFFFFF))
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
+def test_knn_k_variants_and_vote_ties(gpu, olib, k):
+    m = cb.fit_knn(1, 1500, 77, k)
+    knn = cb.GpuKnn(gpu)
+    knn.set_model(m)
+    ds = cb.generate_synthetic_dataset(1, 2000, 99)
+    raw = cb.scalar_features(ds.rows)
+    ob, oby, od2, oidx = oracle_predict(olib, m, raw)
+    gb, gby, gd2, gidx = _device_predict(knn, ds.rows, default_family=1, k=k)
+    assert np.array_equal(gb, ob)
+    assert np.array_equal(gd2.view(np.uint64), od2.view(np.uint64))
+    assert np.array_equal(gidx, oidx)
+
+
+def test_knn_degenerate_models_ties_and_outliers(gpu, olib):
+    rng = np.random.default_rng(3)
+    # Duplicated points -> exact d2 ties broken by training index; k > n.
+    n = 7
+    pts = np.repeat(rng.random((3, 19)), [3, 2, 2], axis=0)[:n]
+    pts[:, 5] = 0.0
+    lo = np.zeros(19)
+    hi = np.ones(19)
+    hi[5] = 0.0  # a constant feature (hi == lo -> normalised to 0)
+    labels = np.array([4, 4, 1, 2, 2, 3, 0], np.int32)
+    for k in (3, 5, 9, 16):
+        m = cb.KnnModel(1, k, 8 * abi.GiB, lo, hi, pts.copy(), labels, np.zeros(0, np.int64))
+        knn = cb.GpuKnn(gpu)
+        knn.set_model(m)
+        q = np.concatenate([pts, rng.random((200, 19)) * 3 - 1, np.full((1, 19), 1e12), np.zeros((1, 19))])
+        ob, oby, od2, oidx = oracle_predict(olib, m, q, k=k)
+        gb, gby, gd2, gidx = _device_predict(knn, q, default_family=1, k=k, fmt=abi.ROWS_SCALAR)
+        assert np.array_equal(gb, ob)
+        kk = min(k, n)
+        assert np.array_equal(gd2[:, :kk].view(np.uint64), od2[:, :kk].view(np.uint64))
+        assert np.array_equal(gidx[:, :kk], oidx[:, :kk])
+
+
+def test_knn_empty_and_single(gpu, models):
+    knn = cb.GpuKnn(gpu)
+    knn.set_model(models[0])
+    b, by = knn.predict(np.zeros(0, abi.feature_row_dtype), default_family=0)
+    assert len(b) == 0
+    ds = cb.generate_synthetic_dataset(0, 1, 5)
+    b, _ = knn.predict(ds.rows, default_family=0)
+    assert b.shape == (1,)
+
+
+def test_knn_large_batch_subsample_parity(gpu, olib, models):
+    """1M rows through the chunked host pipeline; a 3000-row sample vs the oracle,
+    and determinism of the whole output."""
+    ds = cb.generate_synthetic_dataset(2, 50_000, 31)
+    rows = np.tile(ds.rows, 20)
+    knn = cb.GpuKnn(gpu)
+    knn.set_model(models[2])
+    b1, by1 = knn.predict(rows, default_family=2)
+    b2, _ = knn.predict(rows, default_family=2)
+    assert np.array_equal(b1, b2)
+    assert np.array_equal(b1.reshape(20, -1), np.broadcast_to(b1[:50_000], (20, 50_000)))
+    sel = np.random.default_rng(0).choice(50_000, 3000, replace=False)
+    ob, _, _, _ = oracle_predict(olib, models[2], cb.scalar_features(ds.rows[sel]))
+    assert np.array_equal(b1[sel], ob)

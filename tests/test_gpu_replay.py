@@ -1,0 +1,158 @@
+"""Stage 2 parity on the GPU: carma_replay_* vs the oracle restatement of
+run_simulation (world.cpp / manager.cpp / gpu.cpp / runner.cpp / metrics.cpp).
+Every output field is compared bit-for-bit: per task (attempts, dispatch,
+completion, crash times, OOMs, GPU ids, executed work), per GPU (energy,
+mean SMACT, peak memory, step count) and per trace (report scalars, events)."""
+import numpy as np
+import pytest
+
+import paper_2508_19073_b200 as cb
+from paper_2508_19073_b200 import abi
+from oracle_bind import oracle_predict, oracle_replay
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg_of(policy="magm", mode="mps", gpu_count=4, max_smact=0.8, min_free=None, window=60.0, rr_pre=False,
+           capacity=40 * abi.GiB):
+    return cb.make_config(cb.PolicyConfig(policy=policy, collocation_mode=mode, max_smact=max_smact,
+                                          min_free_mem=min_free, monitor_window=window,
+                                          rr_apply_preconditions=rr_pre),
+                          cb.SimConstants(gpu_count=gpu_count, gpu_capacity=capacity))
+
+
+def learned_estimates(olib, m, models):
+    raw = cb.scalar_features(m.features)
+    est = np.zeros(len(m.tasks), np.uint64)
+    for f in set(m.family.tolist()):
+        sel = m.family == f
+        est[sel] = oracle_predict(olib, models[f], raw[sel])[1]
+    return est
+
+
+@pytest.fixture(scope="module")
+def models():
+    return {f: cb.fit_knn(f, 4000, 11 + 101 * f, 5) for f in range(3)}
+
+
+def check_jobs(olib, res, cfgs, task_lists, jobs):
+    for j, (t, c) in enumerate(jobs):
+        cfg = cfgs[c: c + 1]
+        rc, ot, otr, og = oracle_replay(olib, cfg, task_lists[t])
+        assert rc == 0
+        gt = res.job_tasks(j)
+        assert gt.tobytes() == ot.tobytes(), f"job {j} task results differ"
+        assert res.traces[j: j + 1].tobytes() == np.array([otr]).tobytes(), f"job {j} report differs"
+        assert res.job_gpus(j).tobytes() == og.tobytes(), f"job {j} gpu results differ"
+
+
+def test_replay_policies_mixes_estimators(gpu, olib, models):
+    """t90/t60 seeds 1..6 x {exclusive, rr, magm, lug, mug} x estimator personas."""
+    task_lists = []
+    for mix in ("t90", "t60"):
+        for seed in range(1, 7):
+            for est in ("none", "oracle", "learned", "static_graph"):
+                m = cb.materialize_trace(cb.generate_trace(mix, seed))
+                if est == "learned":
+                    m.tasks["estimate"] = learned_estimates(olib, m, models)
+                else:
+                    cb.set_persona_estimates(m, est)
+                task_lists.append(m.tasks)
+    cfgs = np.concatenate([cfg_of(p) for p in ("exclusive", "rr", "magm", "lug", "mug")] +
+                          [cfg_of("rr", rr_pre=True), cfg_of("magm", min_free=2 * abi.GiB),
+                           cfg_of("magm", max_smact=1.0, mode="streams"), cfg_of("rr", mode="streams")])
+    jobs = [(t, c) for c in range(len(cfgs)) for t in range(len(task_lists))]
+    res = cb.replay(cfgs, task_lists, jobs)
+    check_jobs(olib, res, cfgs, task_lists, jobs)
+
+
+@pytest.mark.parametrize("gpus,window", [(8, 60.0), (2, 5.0), (16, 5.0), (64, 5.0)])
+def test_replay_gpu_counts_and_windows(gpu, olib, models, gpus, window):
+    task_lists = []
+    for seed in (1, 2, 3):
+        m = cb.materialize_trace(cb.generate_trace("t90", seed))
+        m.tasks["estimate"] = learned_estimates(olib, m, models)
+        task_lists.append(m.tasks)
+    cfgs = np.concatenate([cfg_of(p, gpu_count=gpus, window=window) for p in ("magm", "lug", "rr", "exclusive")])
+    jobs = [(t, c) for c in range(len(cfgs)) for t in range(len(task_lists))]
+    res = cb.replay(cfgs, task_lists, jobs)
+    check_jobs(olib, res, cfgs, task_lists, jobs)
+
+
+def test_replay_large_trace_many_gpus(gpu, olib):
+    """A 4000-task uniform-catalog trace on 64 GPUs (ids beyond t999 exercise
+    the lexicographic rank order) — runs in the global-memory state tier."""
+    tr = cb.generate_uniform_trace(4000, 3.0, 7)
+    m = cb.materialize_trace(tr)
+    cb.set_persona_estimates(m, "oracle")
+    cfgs = np.concatenate([cfg_of("magm", gpu_count=64, window=5.0), cfg_of("rr", gpu_count=64, window=5.0)])
+    jobs = [(0, 0), (0, 1)]
+    res = cb.replay(cfgs, [m.tasks], jobs)
+    check_jobs(olib, res, cfgs, [m.tasks], jobs)
+    assert not np.array_equal(m.tasks["rank"], np.arange(4000))
+
+
+def test_replay_overflow_tier_escalation(gpu, olib):
+    """RR without preconditions on 80 GiB GPUs stacks > 24 residents per GPU:
+    the shared-memory tier overflows and the job re-runs in the global tier."""
+    tr = cb.generate_uniform_trace(600, 1.0, 11)
+    m = cb.materialize_trace(tr)
+    cfg = cfg_of("rr", gpu_count=2, capacity=80 * abi.GiB, window=1.0)
+    offs = np.array([0, len(m.tasks)], np.uint64)
+    jobs = np.zeros(1, abi.job_dtype)
+    plan = cb.ReplayPlan(cfg, m.tasks, offs, jobs)
+    plan.run()
+    res = plan.results()
+    launches, retried = plan.stats()
+    check_jobs(olib, res, cfg, [m.tasks], [(0, 0)])
+    assert res.traces["status"][0] == 0
+
+
+def test_replay_deterministic_and_resident(gpu, olib):
+    task_lists = [cb.materialize_trace(cb.generate_trace("t90", s)).tasks for s in range(1, 65)]
+    cfgs = np.concatenate([cfg_of(p) for p in ("exclusive", "rr", "magm", "lug")])
+    offs = np.concatenate([[0], np.cumsum([len(t) for t in task_lists])]).astype(np.uint64)
+    jobs = np.zeros(len(task_lists) * 4, abi.job_dtype)
+    jobs["trace"] = np.tile(np.arange(len(task_lists)), 4)
+    jobs["config"] = np.repeat(np.arange(4), len(task_lists))
+    plan = cb.ReplayPlan(cfgs, np.concatenate(task_lists), offs, jobs)
+    plan.run()
+    r1 = plan.results()
+    plan.run()
+    r2 = plan.results()
+    assert r1.tasks.tobytes() == r2.tasks.tobytes()
+    assert r1.traces.tobytes() == r2.traces.tobytes()
+    for j in range(0, len(jobs), 37):
+        t, c = int(jobs["trace"][j]), int(jobs["config"][j])
+        rc, ot, otr, og = oracle_replay(olib, cfgs[c: c + 1], task_lists[t])
+        assert r1.job_tasks(j).tobytes() == ot.tobytes()
+
+
+def test_pick_batch_matches_oracle(gpu, olib):
+    rng = np.random.default_rng(1)
+    for g in (1, 3, 4, 8, 17, 32, 64):
+        n = 3000
+        views = np.zeros((n, g), abi.gpu_view_dtype)
+        views["total_free"] = rng.integers(0, 81, (n, g)).astype(np.uint64) * (512 * abi.MiB)
+        views["total_free"][:, ::3] = 20 * abi.GiB  # ties
+        views["windowed_smact"] = np.round(rng.random((n, g)), 1)
+        views["idle"] = rng.random((n, g)) < 0.3
+        reqs = np.zeros(n, abi.pick_request_dtype)
+        reqs["estimate"] = np.where(rng.random(n) < 0.3, abi.NO_ESTIMATE,
+                                    rng.integers(0, 45, n).astype(np.uint64) * abi.GiB)
+        reqs["want"] = np.where(rng.random(n) < 0.2, 2, 1).astype(np.uint32)
+        if g == 1:
+            reqs["want"] = 1
+        reqs["from_recovery"] = rng.random(n) < 0.1
+        cursor = rng.integers(0, g, n).astype(np.int32)
+        for policy in ("exclusive", "rr", "magm", "lug", "mug"):
+            for rr_pre in (False, True):
+                cfg = cfg_of(policy, gpu_count=g, min_free=abi.GiB, rr_pre=rr_pre)
+                out, cur = cb.pick_batch(cfg, views, reqs, cursor)
+                for i in range(0, n, 7):
+                    oc = np.array([cursor[i]], np.int32)
+                    oo = np.zeros(2, np.int32)
+                    olib.oracle_pick(cfg.ctypes.data, views[i].ctypes.data, g, reqs[i: i + 1].ctypes.data,
+                                     oc.ctypes.data, oo.ctypes.data)
+                    assert out[i].tolist() == oo.tolist(), (g, policy, i)
+                    assert cur[i] == oc[0]
