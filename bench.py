@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""Benchmark of the CARMA hot path on B200.
+
+Headline (BASELINE.json configs[1]): GPUMemNet estimates/s — the reference's
+k-NN memory-bin classifier over the 16,777,216-row CNN + Transformer batch
+(generate_synthetic_dataset(CNN, 8388608, 2024) + (Transformer, 8388608, 2025)),
+routed per family to the models provision_estimators trains (seeds 112, 213).
+Secondary (configs[3], same JSON line under "replay"): trace-replay placed
+tasks/s for the policy sweep t90 seeds 1..100000 x {exclusive, rr, magm, lug}.
+
+Scaling is weak: every rank runs the full per-GPU workload on its own GPU
+with no data-path collective; value = all ranks' units / max-over-ranks time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl carma|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KNN_ROWS_PER_FAMILY = 8_388_608
+KNN_SEEDS = {1: 2024, 2: 2025}          # query datasets (family -> seed)
+MODEL_SEEDS = {1: 11 + 101, 2: 11 + 202}  # provision_estimators: estimator_seed + 101*family
+SWEEP_TRACES = 100_000
+SWEEP_POLICIES = ("exclusive", "rr", "magm", "lug")
+ALG_BYTES_PER_ESTIMATE = 164       # 19 f64 in + i32 bucket + u64 bytes
+ALG_BYTES_PER_TASK = 80            # 45 B in + 35 B out per placed task
+FLOPS_PER_EVAL = 58                # 19 x (sub, mul, add) + 1 weight mul, FMA-free
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except OSError:
+            rows = []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], 0.0, set()
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for name, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(name)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ dist
+class Dist:
+    def __init__(self, gpus: int):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.n = max(self.world, 1)
+        if gpus and self.world > 1 and gpus != self.world:
+            log(f"warning: --gpus {gpus} but WORLD_SIZE {self.world}")
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ------------------------------------------------------------------ data
+def knn_inputs(cb):
+    """The c2 batch: 8,388,608 CNN rows (seed 2024) + 8,388,608 Transformer rows (seed 2025)."""
+    out = {}
+
+    def gen(f):
+        out[f] = cb.generate_synthetic_dataset(f, KNN_ROWS_PER_FAMILY, KNN_SEEDS[f])
+
+    th = [threading.Thread(target=gen, args=(f,)) for f in KNN_SEEDS]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    rows = np.concatenate([out[1].rows, out[2].rows])
+    fam = np.concatenate([np.full(KNN_ROWS_PER_FAMILY, 1, np.int8), np.full(KNN_ROWS_PER_FAMILY, 2, np.int8)])
+    return rows, fam
+
+
+def sweep_inputs(cb, n_traces: int):
+    """t90 seeds 1..n_traces, materialised once; jobs = traces x 4 policies."""
+    lists = [cb.materialize_trace(cb.generate_trace("t90", s)).tasks for s in range(1, n_traces + 1)]
+    tasks = np.concatenate(lists)
+    offs = np.concatenate([[0], np.cumsum([len(t) for t in lists])]).astype(np.uint64)
+    cfgs = np.concatenate([cb.make_config(cb.PolicyConfig(policy=p, max_smact=0.8), cb.SimConstants())
+                           for p in SWEEP_POLICIES])
+    from paper_2508_19073_b200 import abi
+    jobs = np.zeros(n_traces * len(SWEEP_POLICIES), abi.job_dtype)
+    jobs["trace"] = np.tile(np.arange(n_traces, dtype=np.uint32), len(SWEEP_POLICIES))
+    jobs["config"] = np.repeat(np.arange(len(SWEEP_POLICIES), dtype=np.uint32), n_traces)
+    return cfgs, tasks, offs, jobs
+
+
+def profile_traffic(name: str):
+    """dram bytes per launch from the committed ncu --set full summary, if present."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(path)).get(name)
+    except (OSError, ValueError):
+        return None
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def knn_config(n: int) -> dict:
+    return {"workload": "c2: GPUMemNet k-NN ensemble over 8,388,608 CNN (seed 2024) + 8,388,608 "
+                        "Transformer (seed 2025) feature vectors per GPU; models = provision_estimators "
+                        "(4000 samples, k=5, seeds 112/213)",
+            "rows_per_gpu": 2 * KNN_ROWS_PER_FAMILY, "parallelism": f"dp{n} (independent shards, no collective)",
+            "l2": "inputs 2.28 GB per GPU > 126 MB L2 (no flush needed)"}
+
+
+# ------------------------------------------------------------ reference arm
+def ref_lib():
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import load_ref
+    return load_ref()
+
+
+def cpu_knn_baseline(ref, threads: int, target_s: float = 10.0):
+    """The reference predict (estimate_learned, oracle/_ref) on `threads` host
+    threads over CNN (seed 2024) and Transformer (seed 2025) rows, sized for
+    ~target_s of wall time. Returns (estimates/s, sample description)."""
+    import ctypes
+    n = 50_000
+    ck = ctypes.c_uint64()
+    # warm the model cache + calibrate
+    t = ref.ref_bench_predict(1, 4000, MODEL_SEEDS[1], 5, 4000, KNN_SEEDS[1], threads, 1, ctypes.byref(ck))
+    rate = 4000 / max(t, 1e-6)
+    reps = max(1, int(rate * target_s / 2 / n))
+    tot, rows = 0.0, 0
+    for f in (1, 2):
+        s = ref.ref_bench_predict(f, 4000, MODEL_SEEDS[f], 5, n, KNN_SEEDS[f], threads, reps, ctypes.byref(ck))
+        if s < 0:
+            raise RuntimeError(ref.ref_last_error().decode())
+        tot += s
+        rows += n * reps
+    return rows / tot, f"{reps} x {n} CNN (seed 2024) + {reps} x {n} Transformer (seed 2025) rows; " \
+                       f"models trained as provision_estimators (seeds 112, 213)"
+
+
+def cpu_sweep_baseline(ref, threads: int, target_s: float = 10.0):
+    """The reference run_simulation pool (run_sweep shape) over t90 seeds x 4 policies."""
+    import ctypes
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import ref_config
+    from paper_2508_19073_b200 import abi
+    cfg = ref_config(policy="magm", max_smact=0.8)
+    pols = np.array([abi.POLICY[p] for p in SWEEP_POLICIES], np.int32)
+    placed, esum = ctypes.c_uint64(), ctypes.c_double()
+    n0 = max(8, threads)
+    t = ref.ref_bench_sweep(cfg.ctypes.data, 0, 1, n0, pols.ctypes.data, len(pols), threads,
+                            ctypes.byref(placed), ctypes.byref(esum))
+    rate = n0 * len(pols) / max(t, 1e-6)
+    n = max(n0, int(rate * target_s / len(pols)))
+    t = ref.ref_bench_sweep(cfg.ctypes.data, 0, 1, n, pols.ctypes.data, len(pols), threads,
+                            ctypes.byref(placed), ctypes.byref(esum))
+    if t < 0:
+        raise RuntimeError(ref.ref_last_error().decode())
+    return placed.value / t, f"t90 seeds 1..{n} x {{exclusive, rr, magm, lug}} ({n * len(pols)} runs)", n
+
+
+def run_reference(args, d: Dist):
+    if d.rank != 0:
+        return
+    ref = ref_lib()
+    threads = os.cpu_count() or 1
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcarma_ref.so not built"}))
+        return
+    steps = []
+    for _ in range(args.warmup + args.steps):
+        rate, sample = cpu_knn_baseline(ref, threads, target_s=4.0)
+        steps.append(rate)
+    vals = steps[args.warmup:]
+    value = statistics.median(vals)
+    srate, ssample, _ = cpu_sweep_baseline(ref, threads, target_s=4.0)
+    line = {
+        "impl": "reference", "metric": "GPUMemNet estimates/sec (k-NN, CNN+Transformer ensemble)",
+        "value": value, "unit": "estimates/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": knn_config(1),
+        "cpu_baseline": {"value": value, "unit": "estimates/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "replay": {"value": srate, "unit": "placed tasks/s", "cores": threads, "sample": ssample},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ ours
+def run_carma(args, d: Dist):
+    import torch
+
+    import paper_2508_19073_b200 as cb
+    from paper_2508_19073_b200 import abi
+
+    dev = d.local
+    torch.cuda.set_device(dev)
+    if abi.lib.carma_device_count() < 1:
+        raise SystemExit("no sm_100 device visible")
+    N = d.n
+    import ctypes
+    fp64 = ctypes.c_double()
+    abi.check(abi.lib.carma_probe_fp64(dev, ctypes.byref(fp64)))
+
+    # ---------------- stage 1 inputs
+    t0 = time.time()
+    rows, fam = knn_inputs(cb)
+    Q = len(rows)
+    knn = cb.GpuKnn(dev)
+    for f in (1, 2):
+        knn.set_model(cb.fit_knn(f, 4000, MODEL_SEEDS[f], 5))
+    log(f"[rank {d.rank}] knn inputs {Q} rows in {time.time() - t0:.1f}s; fp64 probe {fp64.value / 1e12:.2f} TF/s")
+    stream = torch.cuda.current_stream()
+    d_rows = torch.from_numpy(rows.view(np.uint8).reshape(-1)).to("cuda")
+    d_fam = torch.from_numpy(fam).to("cuda")
+    d_b = torch.empty(Q, dtype=torch.int32, device="cuda")
+    d_by = torch.empty(Q, dtype=torch.int64, device="cuda")
+
+    def knn_step():
+        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_FEATURES,
+                                                   d_fam.data_ptr(), 1, Q, d_b.data_ptr(), d_by.data_ptr(),
+                                                   None, None, stream.cuda_stream))
+
+    for _ in range(args.warmup):
+        knn_step()
+    torch.cuda.synchronize()
+    launches0, evals = knn.last_stats()
+    search_ms, pipe_ms = [], []
+    sm, pm = ctypes.c_double(), ctypes.c_double()
+    with Clocks(dev) as clk:
+        d.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            knn_step()
+            abi.check(abi.lib.carma_knn_last_timing(knn.handle, ctypes.byref(sm), ctypes.byref(pm)))
+            search_ms.append(sm.value)
+            pipe_ms.append(pm.value)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        d.barrier()
+    knn_ms = d.max(e0.elapsed_time(e1) / args.steps)
+    clocks = clk.summary()
+    # parity spot check on the bench batch itself (outputs identical across steps)
+    b_dev = d_b.cpu().numpy()
+    launches, evals = knn.last_stats()
+    value = N * Q / (knn_ms * 1e-3)
+
+    # e2e: host pinned rows -> carma_knn_predict (chunked H2D / compute / D2H) -> host outputs
+    h_rows = torch.from_numpy(rows.view(np.uint8).reshape(-1)).pin_memory().numpy().view(rows.dtype)
+    h_fam = torch.from_numpy(fam).pin_memory().numpy()
+    h_b = torch.empty(Q, dtype=torch.int32).pin_memory().numpy()
+    h_by = torch.empty(Q, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    for _ in range(max(1, args.warmup - 1)):
+        abi.check(abi.lib.carma_knn_predict(knn.handle, h_rows.ctypes.data, h_fam.ctypes.data, 1, Q,
+                                            h_b.ctypes.data, h_by.ctypes.data))
+    d.barrier()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        abi.check(abi.lib.carma_knn_predict(knn.handle, h_rows.ctypes.data, h_fam.ctypes.data, 1, Q,
+                                            h_b.ctypes.data, h_by.ctypes.data))
+    e2e_s = d.max((time.perf_counter() - t) / args.steps)
+    d.barrier()
+    assert np.array_equal(h_b, b_dev), "host-API and device-resident predictions differ"
+    del d_rows, d_fam, d_b, d_by
+
+    search_avg = statistics.mean(search_ms)
+    flops_per_launch = evals * FLOPS_PER_EVAL
+    achieved = flops_per_launch / (search_avg * 1e-3)
+    traffic = profile_traffic("knn_search")
+
+    # ---------------- stage 2: policy sweep
+    replay = None
+    if not args.skip_replay:
+        t0 = time.time()
+        n_tr = args.sweep_traces
+        cfgs, tasks, offs, jobs = sweep_inputs(cb, n_tr)
+        n_placed = int(np.diff(offs.astype(np.int64))[jobs["trace"]].sum())
+        plan = cb.ReplayPlan(cfgs, tasks, offs, jobs, device=dev)
+        log(f"[rank {d.rank}] sweep inputs {n_tr} traces x {len(SWEEP_POLICIES)} in {time.time() - t0:.1f}s")
+        for _ in range(args.warmup):
+            plan.run()
+        km, rm = ctypes.c_double(), ctypes.c_double()
+        kernel_ms, run_ms = [], []
+        d.barrier()
+        for _ in range(args.steps):
+            plan.run()
+            abi.check(abi.lib.carma_replay_plan_timing(plan._h, ctypes.byref(km), ctypes.byref(rm)))
+            kernel_ms.append(km.value)
+            run_ms.append(rm.value)
+        d.barrier()
+        res = plan.results(tasks=False)
+        assert (res.traces["status"] == 0).all()
+        launches_r, retried = plan.stats()
+        events = int(res.traces["events"].sum())
+        plan.close()
+        run_avg = d.max(statistics.mean(run_ms))
+        k_avg = statistics.mean(kernel_ms)
+        # e2e through the one-shot host API (upload, run, download every step)
+        h_tasks = torch.from_numpy(tasks.view(np.uint8)).pin_memory().numpy().view(tasks.dtype)
+        tr_out = torch.empty(int(n_placed * 64), dtype=torch.uint8).pin_memory().numpy().view(abi.task_result_dtype)
+        j_out = np.zeros(len(jobs), abi.trace_result_dtype)
+        g_out = np.zeros(len(jobs) * 4, abi.gpu_result_dtype)
+
+        def e2e_step():
+            abi.check(abi.lib.carma_replay_batch(dev, cfgs.ctypes.data, len(cfgs), h_tasks.ctypes.data,
+                                                 offs.ctypes.data, len(offs) - 1, jobs.ctypes.data, len(jobs),
+                                                 tr_out.ctypes.data, j_out.ctypes.data, g_out.ctypes.data))
+
+        e2e_step()
+        d.barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        r_e2e = d.max((time.perf_counter() - t) / args.steps)
+        assert np.array_equal(j_out["energy_mj"], res.traces["energy_mj"])
+        replay = {
+            "metric": "trace-replay placed tasks/sec", "unit": "placed tasks/s",
+            "value": N * n_placed / (run_avg * 1e-3), "ms_per_step": run_avg,
+            "config": {"workload": f"c4 policy sweep: t90 seeds 1..{n_tr} x {{exclusive, rr, magm, lug}}, "
+                                   "MPS, u=0.8, no estimator, 4 GPUs x 40 GiB, W=60 s",
+                       "jobs_per_gpu": len(jobs), "placed_tasks_per_gpu": n_placed},
+            "events_per_s": N * events / (run_avg * 1e-3),
+            "e2e": {"value": N * n_placed / r_e2e, "unit": "placed tasks/s",
+                    "h2d_bytes_per_step": int(tasks.nbytes + cfgs.nbytes + offs.nbytes + jobs.nbytes),
+                    "d2h_bytes_per_step": int(tr_out.nbytes + j_out.nbytes + g_out.nbytes)},
+            "gpu_launches": int(launches_r),
+            "retried_jobs": int(retried),
+            "roofline": {"bound": "hbm", "achieved": ALG_BYTES_PER_TASK * n_placed / (k_avg * 1e-3) / 1e9,
+                         "peak": peaks().get("hbm_gbs", 6650.0), "unit": "GB/s",
+                         "frac": ALG_BYTES_PER_TASK * n_placed / (k_avg * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6650.0),
+                         "traffic": profile_traffic("replay_kernel"),
+                         "note": "latency/issue bound event loop; algorithmic bytes = 80 B per placed task"},
+        }
+
+    # ---------------- CPU baselines (rank 0, N = 1)
+    cpu = None
+    if d.rank == 0 and N == 1 and not args.skip_cpu:
+        ref = ref_lib()
+        threads = os.cpu_count() or 1
+        if ref is not None:
+            rate, sample = cpu_knn_baseline(ref, threads)
+            cpu = {"value": rate, "unit": "estimates/s", "cores": threads, "kind": "reference", "sample": sample}
+            if replay is not None:
+                srate, ssample, _ = cpu_sweep_baseline(ref, threads)
+                replay["cpu_baseline"] = {"value": srate, "unit": "placed tasks/s", "cores": threads,
+                                          "kind": "reference", "sample": ssample}
+
+    if d.rank != 0:
+        return
+    hbm = peaks().get("hbm_gbs")
+    line = {
+        "metric": "GPUMemNet estimates/sec (k-NN, CNN+Transformer ensemble)",
+        "value": value, "unit": "estimates/s", "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": knn_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference generators, seeded)",
+        "config": knn_config(N),
+        "e2e": {"value": N * Q / e2e_s, "unit": "estimates/s",
+                "h2d_bytes_per_step": int(h_rows.nbytes + h_fam.nbytes),
+                "d2h_bytes_per_step": int(h_b.nbytes + h_by.nbytes)},
+        "gpu_launches": int(launches) * args.steps,
+        "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": fp64.value / 1e12, "unit": "TFLOP/s",
+                     "frac": achieved / fp64.value, "traffic": traffic,
+                     "kernel": "knn_search", "kernel_ms": search_avg,
+                     "kernel_share_of_step": search_avg / statistics.mean(pipe_ms),
+                     "peak_source": "measured: carma_probe_fp64 (separately rounded DADD/DMUL issue rate)",
+                     "work": f"{evals} (query, point) distance evaluations x {FLOPS_PER_EVAL} fp64 ops",
+                     "brute_force_equivalent_tflops": Q * 162_400 / (search_avg * 1e-3) / 1e12,
+                     "hbm_gbs": ALG_BYTES_PER_ESTIMATE * Q / (search_avg * 1e-3) / 1e9, "hbm_peak_gbs": hbm},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "replay": replay,
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("carma", "reference"), default="carma")
+    ap.add_argument("--sweep-traces", type=int, default=SWEEP_TRACES)
+    ap.add_argument("--skip-replay", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("note: warmup raised to 3 (timing rule)")
+        args.warmup = 3
+    d = Dist(args.gpus)
+    try:
+        if args.impl == "reference":
+            run_reference(args, d)
+        else:
+            run_carma(args, d)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

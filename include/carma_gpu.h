@@ -111,6 +111,9 @@ carma_status carma_knn_predict_device(carma_knn* h, const void* rows, int32_t fo
 /* Kernel statistics of the last predict: launches and the number of (query,
  * point) distance evaluations performed. */
 carma_status carma_knn_last_stats(carma_knn* h, uint64_t* launches, uint64_t* evaluations);
+/* CUDA-event timing of the last carma_knn_predict_device on its stream:
+ * the knn_search kernel alone and the whole 4-kernel pipeline (ms). */
+carma_status carma_knn_last_timing(carma_knn* h, double* search_ms, double* pipeline_ms);
 
 /* ------------------------------------------------------------ stage 2 */
 
@@ -210,6 +213,9 @@ carma_status carma_replay_plan_results(carma_replay_plan* p, carma_task_result* 
 /* Kernel launches of the last run and the state tier each job finished in. */
 carma_status carma_replay_plan_stats(carma_replay_plan* p, uint64_t* launches,
                                      uint64_t* retried_jobs);
+/* CUDA-event timing of the last run on the plan's stream: the first-tier
+ * replay kernel and the whole run including retries (ms). */
+carma_status carma_replay_plan_timing(carma_replay_plan* p, double* kernel_ms, double* run_ms);
 carma_status carma_replay_plan_destroy(carma_replay_plan* p);
 
 /* One-shot host API: create + run + results + destroy (the run_sweep engine). */
@@ -241,6 +247,12 @@ carma_status carma_pick_batch(int device, const carma_replay_config* cfg,
                               const carma_gpu_view* views, uint32_t n_gpus,
                               const carma_pick_request* reqs, uint64_t n,
                               int32_t* rr_cursor, int32_t* out_gpus);
+
+/* ------------------------------------------------------------ probes */
+/* Measured fp64 add/mul issue throughput of `device` (separately rounded
+ * ops per second, 1 op = 1 flop): the roofline denominator of the k-NN
+ * distance kernel, which is FP64-pipe bound and FMA-free by contract. */
+carma_status carma_probe_fp64(int device, double* flops_per_s);
 
 #ifdef __cplusplus
 }

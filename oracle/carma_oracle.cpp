@@ -104,11 +104,29 @@ struct Sim {
     double now = 0.0;
     uint64_t events = 0;
     uint64_t max_events = 0;
+    bool collect = false;
+    uint32_t arrivals_seen = 0;
     // manager
     std::deque<int> main_q, recovery_q;
     int rr_cursor = 0, oom_count = 0;
     double deadline = 0.0;
     carma_task_result* out;
+    // capacity statistics (oracle_replay_stats)
+    uint64_t st_heap = 0, st_resident = 0, st_res_gpu = 0, st_window = 0, st_rq = 0;
+    void sample_stats() {
+        { const int64_t dyn = static_cast<int64_t>(pq.size()) - (static_cast<int64_t>(n) - arrivals_seen); st_heap = std::max<uint64_t>(st_heap, dyn > 0 ? static_cast<uint64_t>(dyn) : 0); }
+        uint64_t tot = 0;
+        for (const auto& g : gpu) {
+            tot += g.residents.size();
+            st_res_gpu = std::max<uint64_t>(st_res_gpu, g.residents.size());
+            const double begin = std::max(0.0, now - c.monitor_window);
+            uint64_t in_window = 0;
+            for (const auto& stp : g.steps) in_window += stp.first > begin ? 1 : 0;
+            st_window = std::max<uint64_t>(st_window, in_window + 1);
+        }
+        st_resident = std::max(st_resident, tot);
+        st_rq = std::max<uint64_t>(st_rq, recovery_q.size());
+    }
 
     Sim(const carma_replay_config& cfg, const carma_task* t, uint32_t nt, carma_task_result* o)
         : c(cfg), tasks(t), n(nt), gpu(static_cast<size_t>(cfg.gpu_count)), run(nt), out(o) {
@@ -408,6 +426,7 @@ struct Sim {
         Event ev = pq.top();
         pq.pop();
         ++events;
+        if (collect) sample_stats();
         integrate_to(ev.t);
         if (ev.kind == COMPLETION) {
             Run& r = run[static_cast<size_t>(ev.task)];
@@ -416,6 +435,7 @@ struct Sim {
         }
         switch (ev.kind) {
             case ARRIVAL:
+                ++arrivals_seen;
                 main_q.push_back(ev.task);
                 try_schedule();
                 break;
@@ -573,5 +593,30 @@ extern "C" int oracle_pick(const carma_replay_config* cfg, const carma_gpu_view*
         }
     }
     for (size_t i = 0; i < ids.size() && i < 2; ++i) out[i] = ids[i];
+    return 0;
+}
+
+// Test-only: peak sizes of the replay state over one run (heap of pending
+// events, resident tasks, residents per GPU, SMACT steps inside the window
+// + 1, recovery queue). Used to size the GPU kernel's state tiers.
+extern "C" int oracle_replay_stats(const carma_replay_config* cfg, const carma_task* tasks, uint32_t n,
+                                   uint64_t* stats5) {
+    std::vector<carma_task_result> out(n);
+    for (auto& o : out) {
+        o.first_attempt = o.final_dispatch = o.complete = o.first_crash = o.last_crash = -1.0;
+        o.attempts = o.ooms = 0;
+    }
+    Sim s(*cfg, tasks, n, out.data());
+    s.max_events = 1000ull * n + 1000000ull;
+    s.collect = true;
+    for (uint32_t i = 0; i < n; ++i) s.schedule(tasks[i].submit, ARRIVAL, static_cast<int>(i), 0);
+    while (s.step()) {
+    }
+    // arrivals sit in the oracle's heap; the kernel streams them separately
+    stats5[0] = s.st_heap;
+    stats5[1] = s.st_resident;
+    stats5[2] = s.st_res_gpu;
+    stats5[3] = s.st_window;
+    stats5[4] = s.st_rq;
     return 0;
 }

@@ -100,6 +100,9 @@ SIGNATURES = {
     "carma_knn_predict_scalar": (c_int, [c_void_p, P, P, c_int32, c_uint64, P, P]),
     "carma_knn_predict_device": (c_int, [c_void_p, P, c_int32, P, c_int32, c_uint64, P, P, P, P, c_void_p]),
     "carma_knn_last_stats": (c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64)]),
+    "carma_knn_last_timing": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
+    "carma_replay_plan_timing": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
+    "carma_probe_fp64": (c_int, [c_int, POINTER(c_double)]),
     "carma_replay_plan_create": (c_int, [c_int, P, c_uint32, P, P, c_uint32, P, c_uint32, c_int32,
                                          POINTER(c_void_p)]),
     "carma_replay_plan_set_estimates_device": (c_int, [c_void_p, P]),

@@ -47,6 +47,7 @@ constexpr int kMaxK = 16;
 constexpr uint32_t kInvalidBin = 0xffffffffu;
 constexpr int kScatterCtas = 296;  // 2 per SM on a 148-SM B200
 constexpr int kMaxBins = 4096;
+constexpr int kBlock = 8;  // points per frontier step
 
 struct ModelDev {
     const double* pts;    // N x 20, sorted by (p18, original index)
@@ -59,6 +60,7 @@ struct ModelDev {
     uint32_t bin_base;
     uint32_t bin_shift;
     int32_t present;
+    uint32_t active;  // dims whose term can be non-zero (see carma_knn_set_model)
     double lo[kDims];
     double hi[kDims];
 };
@@ -225,6 +227,20 @@ struct TopK {
     }
 };
 
+template <int K>
+__device__ __forceinline__ void insert_block(TopK<K>& top, const double (&d2)[kBlock], unsigned cand,
+                                          const int32_t* orig) {
+    while (cand) {
+        const int c = __ffs(cand) - 1;
+        cand &= cand - 1;
+        double v = d2[0];
+#pragma unroll
+        for (int j = 1; j < kBlock; ++j)
+            if (j == c) v = d2[j];
+        top.insert(v, __ldg(orig + c));
+    }
+}
+
 __device__ __forceinline__ double t18_of(double key, double q18) {
     const double diff = __dmul_rn(__dsub_rn(key, q18), 64.0);
     return __dmul_rn(diff, diff);
@@ -296,6 +312,7 @@ __global__ void __launch_bounds__(128)
                                      pos < n ? t18_of(__ldg(m.key18 + pos), q[18]) : inf);
             double tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q[18]) : t_in) : inf;
             double tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q[18]) : t_in) : inf;
+            const uint32_t act = m.active;
             uint64_t steps = 0;
             for (;;) {
                 const double kth = top.kth();
@@ -308,27 +325,67 @@ __global__ void __launch_bounds__(128)
                 const double rl = __shfl_sync(0xffffffffu, need_l ? tl : inf, mid_lane);
                 const double rr = __shfl_sync(0xffffffffu, need_r ? tr : inf, mid_lane);
                 const bool go_left = bl != 0 && (br == 0 || rl <= rr);
-                const int64_t i = go_left ? --L : R++;
-                const double2* pt = reinterpret_cast<const double2*>(m.pts + i * kStride);
-                double d2 = 0.0;
+                // Next block of up to kBlock contiguous points on that side.
+                int64_t i0, cnt;
+                if (go_left) {
+                    i0 = L > kBlock ? L - kBlock : 0;
+                    cnt = L - i0;
+                    L = i0;
+                } else {
+                    i0 = R;
+                    cnt = n - R < kBlock ? n - R : kBlock;
+                    R += cnt;
+                }
+                // kBlock independent accumulation chains; each d2 keeps the
+                // reference's dim order. Dims outside `act` contribute exactly
+                // +0.0 and are skipped (warp-uniform branch).
+                double d2[kBlock];
+                const double* base[kBlock];
+#pragma unroll
+                for (int c = 0; c < kBlock; ++c) {
+                    d2[c] = 0.0;
+                    base[c] = m.pts + (i0 + (c < cnt ? c : cnt - 1)) * kStride;
+                }
 #pragma unroll
                 for (int h = 0; h < 9; ++h) {
-                    const double2 v = __ldg(pt + h);
-                    const double a = __dsub_rn(v.x, q[2 * h]);
-                    d2 = __dadd_rn(d2, __dmul_rn(a, a));
-                    const double b = __dsub_rn(v.y, q[2 * h + 1]);
-                    d2 = __dadd_rn(d2, __dmul_rn(b, b));
+                    if (!(act & (3u << (2 * h)))) continue;
+                    double2 v[kBlock];
+#pragma unroll
+                    for (int c = 0; c < kBlock; ++c) v[c] = __ldg(reinterpret_cast<const double2*>(base[c]) + h);
+                    if (act & (1u << (2 * h))) {
+#pragma unroll
+                        for (int c = 0; c < kBlock; ++c) {
+                            const double a = __dsub_rn(v[c].x, q[2 * h]);
+                            d2[c] = __dadd_rn(d2[c], __dmul_rn(a, a));
+                        }
+                    }
+                    if (act & (2u << (2 * h))) {
+#pragma unroll
+                        for (int c = 0; c < kBlock; ++c) {
+                            const double b = __dsub_rn(v[c].y, q[2 * h + 1]);
+                            d2[c] = __dadd_rn(d2[c], __dmul_rn(b, b));
+                        }
+                    }
                 }
-                {
-                    const double v = __ldg(m.pts + i * kStride + 18);
-                    const double a = __dmul_rn(__dsub_rn(v, q[18]), 64.0);
-                    d2 = __dadd_rn(d2, __dmul_rn(a, a));
+                if (act & (1u << 18)) {
+#pragma unroll
+                    for (int c = 0; c < kBlock; ++c) {
+                        const double a = __dmul_rn(__dsub_rn(__ldg(base[c] + 18), q[18]), 64.0);
+                        d2[c] = __dadd_rn(d2[c], __dmul_rn(a, a));
+                    }
                 }
-                const int32_t oi = __ldg(m.orig + i);
-                if (mine) top.insert(d2, oi);
+                // Candidates: d2 <= k-th best (ties resolved by index inside).
+                // The insertion is rare after the first blocks; keep it off
+                // the straight-line path so it is not if-converted.
+                const double kb = top.kth();
+                unsigned cand = 0;
+#pragma unroll
+                for (int c = 0; c < kBlock; ++c) cand |= (c < cnt && d2[c] <= kb) ? (1u << c) : 0u;
+                if (!mine) cand = 0;
+                if (cand) insert_block<K>(top, d2, cand, m.orig + i0);
                 if (go_left) tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q[18]) : t_in) : inf;
                 else tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q[18]) : t_in) : inf;
-                ++steps;
+                steps += static_cast<uint64_t>(cnt);
             }
             my_evals += steps * static_cast<unsigned long long>(__popc(members));
 
@@ -374,6 +431,7 @@ struct HostModel {
     uint64_t bucket_range = 0;
     uint32_t k = 0;
     double lo[kDims], hi[kDims];
+    uint32_t active = 0;
     bool present = false;
 };
 
@@ -389,6 +447,8 @@ struct KnnHandle {
         PinnedBuffer stage_rows, stage_family;
     } scratch[2];
     DeviceBuffer evals;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // pipeline start, search start, search end
+    bool timed = false;
     uint64_t last_launches = 0, last_evals = 0;
     std::mutex mu;
 };
@@ -410,6 +470,7 @@ KnnParams make_params(const KnnHandle& h, uint32_t* n_bins) {
         m.n = hm.n;
         m.bucket_range = hm.bucket_range;
         m.k = hm.k;
+        m.active = hm.active;
         std::memcpy(m.lo, hm.lo, sizeof(m.lo));
         std::memcpy(m.hi, hm.hi, sizeof(m.hi));
         uint32_t shift = 0;
@@ -461,13 +522,17 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
     sc.perm.ensure(q * 4);
     sc.hist.ensure(static_cast<size_t>(n_bins) * ctas * 4);
     const size_t shmem = n_bins * 4;
+    const bool timed = h.timed && h.ev[0];
+    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
     knn_keys<<<ctas, 512, shmem, s>>>(p, n_bins, sc.qbin.as<uint32_t>(), sc.qpos.as<uint32_t>(),
                                       sc.hist.as<uint32_t>());
     scan_matrix<<<1, 1024, 0, s>>>(sc.hist.as<uint32_t>(), static_cast<uint64_t>(n_bins) * ctas);
     knn_scatter<<<ctas, 512, shmem, s>>>(q, n_bins, sc.qbin.as<uint32_t>(), sc.hist.as<uint32_t>(),
                                          sc.perm.as<uint32_t>());
+    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[1], s));
     launch_search(p, max_k(h), sc.perm.as<uint32_t>(), sc.qpos.as<uint32_t>(), bucket, bytes, d2, idx,
                   evals, s);
+    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[2], s));
     CARMA_CUDA(cudaGetLastError());
     return 4;
 }
@@ -493,6 +558,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
         const bool rows_pinned = is_pinned(rows);
         const bool fam_pinned = !family || is_pinned(family);
         const bool out_pinned = (!bucket_out || is_pinned(bucket_out)) && (!bytes_out || is_pinned(bytes_out));
+        h->timed = false;
         h->evals.ensure(8);
         CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 8, h->pipe[0]));
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
@@ -566,6 +632,7 @@ carma_status carma_knn_create(int device, carma_knn** out) {
         CARMA_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         CARMA_CUDA(cudaStreamCreateWithFlags(&h->pipe[0], cudaStreamNonBlocking));
         CARMA_CUDA(cudaStreamCreateWithFlags(&h->pipe[1], cudaStreamNonBlocking));
+        for (auto& e : h->ev) CARMA_CUDA(cudaEventCreate(&e));
         *out = reinterpret_cast<carma_knn*>(h);
     });
 }
@@ -591,6 +658,8 @@ carma_status carma_knn_destroy(carma_knn* hh) {
                 sc.stage_rows.release(); sc.stage_family.release();
             }
             h->evals.release();
+            for (auto& e : h->ev)
+                if (e) cudaEventDestroy(e);
             cudaStreamDestroy(h->stream);
             cudaStreamDestroy(h->pipe[0]);
             cudaStreamDestroy(h->pipe[1]);
@@ -638,6 +707,15 @@ carma_status carma_knn_set_model(carma_knn* hh, int32_t family, const double* lo
         m.n = n;
         m.k = k;
         m.bucket_range = bucket_range;
+        // A dim contributes exactly +0.0 to every d2 when the query side is
+        // always 0 (hi <= lo, or NaN bounds: normalise yields 0) and every
+        // stored point is +-0 there: diff = +-0, diff^2 = +0, d2 + 0 = d2.
+        m.active = 0;
+        for (int d = 0; d < kDims; ++d) {
+            bool zero = !(hi[d] > lo[d]);
+            for (uint64_t i = 0; zero && i < n; ++i) zero = points[i * kDims + d] == 0.0;
+            if (!zero) m.active |= 1u << d;
+        }
         std::memcpy(m.lo, lo, sizeof(m.lo));
         std::memcpy(m.hi, hi, sizeof(m.hi));
         m.present = true;
@@ -673,9 +751,24 @@ carma_status carma_knn_predict_device(carma_knn* hh, const void* rows, int32_t f
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
         h->evals.ensure(8);
         CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 8, s));
+        h->timed = true;
         h->last_launches = run_pipeline(*h, h->scratch[0], rows, format, family, default_family, q,
                                         bucket_out, bytes_out, topk_d2, topk_idx,
                                         h->evals.as<unsigned long long>(), s);
+    });
+}
+
+carma_status carma_knn_last_timing(carma_knn* hh, double* search_ms, double* pipeline_ms) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        if (!h) throw InvalidArg("null handle");
+        DeviceGuard g(h->device);
+        CARMA_CUDA(cudaEventSynchronize(h->ev[2]));
+        float a = 0.f, b = 0.f;
+        CARMA_CUDA(cudaEventElapsedTime(&a, h->ev[1], h->ev[2]));
+        CARMA_CUDA(cudaEventElapsedTime(&b, h->ev[0], h->ev[2]));
+        if (search_ms) *search_ms = a;
+        if (pipeline_ms) *pipeline_ms = b;
     });
 }
 

@@ -1,0 +1,934 @@
+// Stage 2 device code: the warp-per-job replay kernel.
+//
+// One warp replays one (trace, config) job end to end: the deterministic
+// discrete-event loop of World (proj/src/world.cpp:31-186) driving the CARMA
+// Manager pipeline (proj/src/manager.cpp:58-357) over simulated GpuDevices in
+// MPS / streams mode (proj/src/gpu.cpp:58-274), then the runner tail
+// (runner.cpp:97-141) and compute_report's scalars (metrics.cpp:16-70).
+// Bit-identical to the reference: built with --fmad=false, every
+// floating-point expression keeps the reference's operation order.
+//
+// Warp organisation. Sequential event logic (queue heads, the event heap,
+// dispatch decisions, rate refresh) runs warp-uniformly — every lane computes
+// the same values — while per-GPU work is lane-parallel: lane l owns
+// simulated GPUs l and l+32. Energy integration, windowed SMACT, feasibility
+// and the MAGM/LUG/MUG arg-reductions (pick.cuh) take one step across the
+// lanes; the first-fit allocator runs on the owner lane's bitmap.
+//
+// Code shape. The event loop is flat: the handlers for the four event kinds
+// only set flags, and try_schedule / place / finish / refresh_rates each
+// occur once in the instruction stream (a fully inlined version thrashed the
+// instruction cache: 84% of stall samples were no_instructions). The state
+// layout is a compile-time struct of offsets from one per-warp base pointer,
+// so no register holds a layout pointer.
+//
+// State (per warp; shared memory for the two common tiers, global memory for
+// the large tier):
+//   * per GPU (SoA): allocation bitmap (block = SimConstants::alloc_block),
+//     cached per-resident rate / instantaneous SMACT / power, energy, peak,
+//     the resident list in insertion order, a ring of recent SMACT steps for
+//     windowed_smact, and a running integrator that reproduces the
+//     full-history windowed_smact(last_complete, span) of runner.cpp:135-137
+//     term by term;
+//   * resident-task slots (remaining work, rate, last update, live event seq);
+//   * a binary min-heap of dynamic events ordered by (t, seq); arrivals are a
+//     pre-sorted stream with seq = trace index (runner.cpp:72-78), merged at pop;
+//   * the main queue is the index range [mq_head, arrived) (FIFO,
+//     manager.cpp:58-78); the recovery queue is a ring.
+// A completion event is live iff its seq equals its slot's live seq — the
+// same test as TaskRun::gen (world.cpp:52-57), since every reschedule draws a
+// fresh seq. Any capacity overflow aborts the job in its tier and the host
+// re-runs it in the global-memory tier.
+#pragma once
+
+#include <cstdint>
+
+#include "../../../include/carma_gpu.h"
+#include "pick.cuh"
+
+namespace carma_b200 {
+namespace replay {
+
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr uint32_t kWindow = 1u, kCompletion = 2u, kCrash = 3u;
+constexpr int32_t kStatusRetry = -1;      // overflowed this tier
+constexpr int32_t kStatusRedoSmact = -2;  // full-history SMACT needs the true window begin
+constexpr int kWords = 4;                 // bitmap words per GPU: <= 256 blocks
+
+struct Params {
+    const carma_replay_config* cfgs;
+    const carma_task* tasks;
+    const uint64_t* trace_off;
+    const carma_replay_job* jobs;
+    const uint64_t* task_out_off;
+    const uint64_t* gpu_out_off;
+    const uint64_t* est_override;  // nullable, indexed like tasks
+    const uint32_t* job_list;      // jobs to run in this launch
+    uint32_t n_list;
+    carma_task_result* task_out;
+    carma_trace_result* trace_out;
+    carma_gpu_result* gpu_out;
+    uint32_t* inv_scratch;   // rank -> index, indexed like task_out
+    double* smact_begin;     // per job; NaN = derive from first_submit
+    uint32_t* retry_list;    // jobs that overflowed this tier
+    uint32_t* retry_count;
+    unsigned int* next_job;  // dynamic scheduler counter
+    char* gstate;            // global-tier state, per warp
+};
+
+// Compile-time state layout: G GPUs, H heap entries, S slots, RC residents
+// per GPU, RG SMACT ring entries per GPU, RQ recovery-queue entries.
+template <int G_, int H_, int S_, int RC_, int RG_, int RQ_>
+struct Layout {
+    static constexpr int G = G_, H = H_, S = S_, RC = RC_, RG = RG_, RQ = RQ_;
+    static constexpr int GPL = (G + 31) / 32;
+    static constexpr size_t al8(size_t x) { return (x + 15) / 16 * 16; }
+    static constexpr size_t cfg = 0;                                   // carma_replay_config
+    static constexpr size_t used = al8(cfg + sizeof(carma_replay_config));  // u64 [W][G]
+    static constexpr size_t energy = al8(used + 8ull * kWords * G);    // f64 [G] x 9
+    static constexpr size_t rate = energy + 8ull * G;
+    static constexpr size_t inst = rate + 8ull * G;
+    static constexpr size_t power = inst + 8ull * G;
+    static constexpr size_t lvl = power + 8ull * G;
+    static constexpr size_t cur = lvl + 8ull * G;
+    static constexpr size_t integ = cur + 8ull * G;
+    static constexpr size_t last_t = integ + 8ull * G;
+    static constexpr size_t last_v = last_t + 8ull * G;
+    static constexpr size_t ring_t = al8(last_v + 8ull * G);           // f64 [G][RG]
+    static constexpr size_t ring_v = ring_t + 8ull * G * RG;
+    static constexpr size_t ht = ring_v + 8ull * G * RG;               // f64 [H]
+    static constexpr size_t s_rem = ht + 8ull * H;                     // f64 [S] x 5
+    static constexpr size_t s_rate = s_rem + 8ull * S;
+    static constexpr size_t s_last = s_rate + 8ull * S;
+    static constexpr size_t s_exec = s_last + 8ull * S;
+    static constexpr size_t s_dem = s_exec + 8ull * S;
+    static constexpr size_t aff = s_dem + 8ull * S;                    // u64 [2 RC] x 2
+    static constexpr size_t aff2 = aff + 16ull * RC;
+    static constexpr size_t nres = aff2 + 16ull * RC;                  // u32 [G] x 6
+    static constexpr size_t nsteps = nres + 4ull * G;
+    static constexpr size_t rhead = nsteps + 4ull * G;
+    static constexpr size_t rcnt = rhead + 4ull * G;
+    static constexpr size_t peak = rcnt + 4ull * G;
+    static constexpr size_t has_step = peak + 4ull * G;
+    static constexpr size_t hs = has_step + 4ull * G;                  // u32 [H] x 2
+    static constexpr size_t hinfo = hs + 4ull * H;
+    static constexpr size_t s_task = hinfo + 4ull * H;                 // u32 [S] x 6
+    static constexpr size_t s_rank = s_task + 4ull * S;
+    static constexpr size_t s_seq = s_rank + 4ull * S;
+    static constexpr size_t s_gp = s_seq + 4ull * S;
+    static constexpr size_t s_off = s_gp + 4ull * S;
+    static constexpr size_t s_nb = s_off + 4ull * S;
+    static constexpr size_t free_stack = s_nb + 4ull * S;              // u32 [S]
+    static constexpr size_t rq = free_stack + 4ull * S;                // u32 [RQ]
+    static constexpr size_t res = rq + 4ull * RQ;                      // u16 [G][RC]
+    static constexpr size_t bytes = al8(res + 2ull * G * RC);
+};
+
+#define RP_F64(f) reinterpret_cast<double*>(b + L::f)
+#define RP_U32(f) reinterpret_cast<uint32_t*>(b + L::f)
+#define RP_U64(f) reinterpret_cast<uint64_t*>(b + L::f)
+#define RP_U16(f) reinterpret_cast<uint16_t*>(b + L::f)
+#define RP_CFG (*reinterpret_cast<const carma_replay_config*>(b + L::cfg))
+
+__device__ __forceinline__ double dmax0(double x) { return 0.0 < x ? x : 0.0; }      // std::max(0.0, x)
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min(a, b)
+__device__ __forceinline__ bool later(double ta, uint32_t sa, double tb, uint32_t sb) {
+    return ta != tb ? ta > tb : sa > sb;
+}
+
+// Warp-uniform scalar state (replicated in every lane).
+struct Sc {
+    double now, deadline, window, begin0;
+    uint32_t seq_next, arrived, mq_head, rq_head, rq_cnt, hsize, nfree, T;
+    int rr_cursor;
+    int32_t oom, status;
+    uint32_t events_lo, events_hi;
+};
+
+// ---------------------------------------------------------------- heap
+template <class L>
+__device__ __forceinline__ uint32_t heap_push(char* b, Sc& c, double t, uint32_t info) {
+    if (c.hsize >= static_cast<uint32_t>(L::H)) {
+        c.status = kStatusRetry;
+        return kNone;
+    }
+    double* ht = RP_F64(ht);
+    uint32_t* hs = RP_U32(hs);
+    uint32_t* hi = RP_U32(hinfo);
+    const uint32_t seq = c.seq_next++;
+    uint32_t i = c.hsize++;
+    while (i > 0) {
+        const uint32_t p = (i - 1) >> 1;
+        const double pt = ht[p];
+        const uint32_t ps = hs[p];
+        if (!later(pt, ps, t, seq)) break;
+        ht[i] = pt;
+        hs[i] = ps;
+        hi[i] = hi[p];
+        i = p;
+    }
+    ht[i] = t;
+    hs[i] = seq;
+    hi[i] = info;
+    return seq;
+}
+
+template <class L>
+__device__ __forceinline__ void heap_pop(char* b, Sc& c) {
+    double* ht = RP_F64(ht);
+    uint32_t* hs = RP_U32(hs);
+    uint32_t* hi = RP_U32(hinfo);
+    const uint32_t n = --c.hsize;
+    if (n == 0) return;
+    const double t = ht[n];
+    const uint32_t sq = hs[n], inf = hi[n];
+    uint32_t i = 0;
+    for (;;) {
+        uint32_t l = 2 * i + 1;
+        if (l >= n) break;
+        const uint32_t r = l + 1;
+        if (r < n && later(ht[l], hs[l], ht[r], hs[r])) l = r;
+        if (!later(t, sq, ht[l], hs[l])) break;
+        ht[i] = ht[l];
+        hs[i] = hs[l];
+        hi[i] = hi[l];
+        i = l;
+    }
+    ht[i] = t;
+    hs[i] = sq;
+    hi[i] = inf;
+}
+
+// ------------------------------------------------------------ allocator
+// Bit = 1: block used (bits past the device's block count are set).
+template <class L>
+__device__ __forceinline__ int next_bit(const uint64_t* used, int g, int from, int nblk, bool one) {
+    for (int w = from >> 6; w < kWords; ++w) {
+        uint64_t bits = used[w * L::G + g];
+        if (!one) bits = ~bits;
+        if (w == (from >> 6)) bits &= ~0ull << (from & 63);
+        if (bits) {
+            const int bit = w * 64 + __ffsll(static_cast<long long>(bits)) - 1;
+            return bit < nblk ? bit : nblk;
+        }
+    }
+    return nblk;
+}
+
+template <class L>
+__device__ __forceinline__ void set_bits(uint64_t* used, int g, int off, int nb, bool on) {
+    for (int x = off; x < off + nb;) {
+        const int w = x >> 6, lo = x & 63;
+        const int cnt = min(64 - lo, off + nb - x);
+        const uint64_t m = (cnt == 64 ? ~0ull : ((1ull << cnt) - 1ull)) << lo;
+        uint64_t& word = used[w * L::G + g];
+        word = on ? (word | m) : (word & ~m);
+        x += cnt;
+    }
+}
+
+template <class L>
+__device__ __forceinline__ uint32_t free_blocks(const uint64_t* used, int g) {
+    uint32_t f = 0;
+#pragma unroll
+    for (int w = 0; w < kWords; ++w) f += __popcll(static_cast<long long>(~used[w * L::G + g]));
+    return f;
+}
+
+// GpuDevice::allocate_range in whole-device mode (gpu.cpp:72-114): first fit
+// over maximal free runs; carve from the tail iff the left neighbour is used
+// and the run reaches the end of the device (no right neighbour).
+template <class L>
+__device__ __forceinline__ int first_fit(char* b, int g, int nblk, int want) {
+    uint64_t* used = RP_U64(used);
+    int pos = 0;
+    while (pos < nblk) {
+        const int start = next_bit<L>(used, g, pos, nblk, false);
+        if (start >= nblk) break;
+        const int end = next_bit<L>(used, g, start, nblk, true);
+        if (end - start >= want) {
+            const int place = (start > 0 && end == nblk) ? end - want : start;
+            set_bits<L>(used, g, place, want, true);
+            const uint32_t u = static_cast<uint32_t>(nblk) - free_blocks<L>(used, g);
+            uint32_t* peak = RP_U32(peak);
+            if (u > peak[g]) peak[g] = u;
+            return place;
+        }
+        pos = end;
+    }
+    return -1;
+}
+
+// ----------------------------------------------------------------- SMACT
+// windowed_smact (gpu.cpp:244-267) over the ring of recent steps.
+template <class L>
+__device__ __forceinline__ double windowed(char* b, int g, double now, double window) {
+    const double begin = dmax0(now - window);
+    const double span = now - begin;
+    if (span <= 0.0) return RP_F64(inst)[g];
+    const double* rt = RP_F64(ring_t) + g * L::RG;
+    const double* rv = RP_F64(ring_v) + g * L::RG;
+    double integral = 0.0, level = 0.0, cursor = begin;
+    const uint32_t h = RP_U32(rhead)[g], n = RP_U32(rcnt)[g];
+    for (uint32_t k = 0; k < n; ++k) {
+        uint32_t idx = h + k;
+        if (idx >= static_cast<uint32_t>(L::RG)) idx -= L::RG;
+        const double t = rt[idx];
+        const double v = rv[idx];
+        if (t <= begin) {
+            level = v;
+            continue;
+        }
+        if (t >= now) break;
+        integral = __dadd_rn(integral, __dmul_rn(level, __dsub_rn(t, cursor)));
+        cursor = t;
+        level = v;
+    }
+    integral = __dadd_rn(integral, __dmul_rn(level, __dsub_rn(now, cursor)));
+    return __ddiv_rn(integral, span);
+}
+
+// effective_rates / instantaneous_smact / power_draw (gpu.cpp:183-229,
+// 269-274) for GPU g after its resident list changed, then record_smact
+// (gpu.cpp:231-242) into the ring and the full-history integrator.
+// Owner lane only. Returns false on ring overflow.
+template <class L>
+__device__ __forceinline__ bool refresh_gpu(char* b, int g, double now, double window, double begin0) {
+    const carma_replay_config& cf = RP_CFG;
+    const uint32_t n = RP_U32(nres)[g];
+    const uint16_t* res = RP_U16(res) + g * L::RC;
+    const double* dem = RP_F64(s_dem);
+    double rate = 0.0, inst = 0.0;
+    if (n > 0) {
+        if (cf.mode == CARMA_MODE_MPS) {
+            double total = 0.0;
+            for (uint32_t r = 0; r < n; ++r) total = __dadd_rn(total, dem[res[r]]);
+            rate = dmin(1.0, __ddiv_rn(1.0, total));
+        } else {
+            rate = __ddiv_rn(1.0, static_cast<double>(n));
+        }
+        double sum = 0.0;
+        for (uint32_t r = 0; r < n; ++r) sum = __dadd_rn(sum, __dmul_rn(dem[res[r]], rate));
+        inst = dmin(1.0, sum);
+    }
+    RP_F64(rate)[g] = rate;
+    RP_F64(inst)[g] = inst;
+    double p = __dadd_rn(cf.p_idle_w, __dmul_rn(__dsub_rn(cf.p_max_w, cf.p_idle_w), inst));
+    if (inst > cf.boost_threshold) p = __dadd_rn(p, cf.p_boost_w);
+    RP_F64(power)[g] = p;
+
+    // record_smact
+    const double v = inst;
+    uint32_t* has = RP_U32(has_step);
+    double* lt = RP_F64(last_t);
+    double* lv = RP_F64(last_v);
+    uint32_t* rh = RP_U32(rhead);
+    uint32_t* rc = RP_U32(rcnt);
+    double* rt = RP_F64(ring_t) + g * L::RG;
+    double* rv = RP_F64(ring_v) + g * L::RG;
+    if (has[g]) {
+        if (lv[g] == v) return true;
+        if (lt[g] == now) {
+            lv[g] = v;
+            uint32_t li = rh[g] + rc[g] - 1;
+            if (li >= static_cast<uint32_t>(L::RG)) li -= L::RG;
+            rv[li] = v;
+            RP_F64(lvl)[g] = v;
+            return true;
+        }
+    }
+    // Drop ring entries no future window can need: begin only grows, so an
+    // entry whose successor is already at or before begin is dead.
+    const double begin_now = dmax0(now - window);
+    while (rc[g] >= 2) {
+        uint32_t second = rh[g] + 1;
+        if (second >= static_cast<uint32_t>(L::RG)) second -= L::RG;
+        if (!(rt[second] <= begin_now)) break;
+        rh[g] = second;
+        rc[g] -= 1;
+    }
+    if (rc[g] >= static_cast<uint32_t>(L::RG)) return false;
+    uint32_t slot = rh[g] + rc[g];
+    if (slot >= static_cast<uint32_t>(L::RG)) slot -= L::RG;
+    rt[slot] = now;
+    rv[slot] = v;
+    rc[g] += 1;
+    double* lvl = RP_F64(lvl);
+    if (now <= begin0) {
+        lvl[g] = v;
+    } else {
+        double* integ = RP_F64(integ);
+        double* cur = RP_F64(cur);
+        integ[g] = __dadd_rn(integ[g], __dmul_rn(lvl[g], __dsub_rn(now, cur[g])));
+        cur[g] = now;
+        lvl[g] = v;
+    }
+    has[g] = 1;
+    lt[g] = now;
+    lv[g] = v;
+    RP_U32(nsteps)[g] += 1;
+    return true;
+}
+
+// World::refresh_rates (world.cpp:157-186) for touched GPUs t0 (, t1).
+template <class L>
+__device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, int nt, unsigned lane) {
+    bool ok = true;
+    if ((t0 & 31) == static_cast<int>(lane)) ok = refresh_gpu<L>(b, t0, c.now, c.window, c.begin0);
+    __syncwarp();
+    if (nt > 1 && (t1 & 31) == static_cast<int>(lane)) ok = refresh_gpu<L>(b, t1, c.now, c.window, c.begin0) && ok;
+    if (!__all_sync(0xffffffffu, ok)) {
+        c.status = kStatusRetry;
+        return;
+    }
+    // Affected tasks: residents of the touched GPUs, deduplicated, ordered by
+    // id (std::set<std::string>) == by rank.
+    const uint32_t* nres = RP_U32(nres);
+    const uint16_t* res = RP_U16(res);
+    const uint32_t* gp = RP_U32(s_gp);
+    const uint32_t* rank = RP_U32(s_rank);
+    uint64_t* aff = RP_U64(aff);
+    uint64_t* aff2 = RP_U64(aff2);
+    uint32_t na = 0;
+    {
+        const uint32_t n0 = nres[t0];
+        for (uint32_t r = lane; r < n0; r += 32) {
+            const uint32_t slot = res[t0 * L::RC + r];
+            aff[r] = (static_cast<uint64_t>(rank[slot]) << 32) | slot;
+        }
+        na = n0;
+        if (nt > 1) {
+            const uint32_t n1 = nres[t1];
+            for (uint32_t base = 0; base < n1; base += 32) {
+                const uint32_t r = base + lane;
+                bool keep = false;
+                uint32_t slot = 0;
+                if (r < n1) {
+                    slot = res[t1 * L::RC + r];
+                    const uint32_t g = gp[slot];
+                    keep = !(static_cast<int>(g & 0xff) == t0 || ((g >> 16) > 1 && static_cast<int>((g >> 8) & 0xff) == t0));
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (keep) aff[na + __popc(m & ((1u << lane) - 1u))] = (static_cast<uint64_t>(rank[slot]) << 32) | slot;
+                na += __popc(m);
+            }
+        }
+    }
+    __syncwarp();
+    for (uint32_t e = lane; e < na; e += 32) {
+        const uint64_t key = aff[e];
+        uint32_t pos = 0;
+        for (uint32_t k = 0; k < na; ++k) pos += aff[k] < key;
+        aff2[pos] = key;
+    }
+    __syncwarp();
+    const double* grate = RP_F64(rate);
+    double* s_rate = RP_F64(s_rate);
+    double* s_last = RP_F64(s_last);
+    double* s_exec = RP_F64(s_exec);
+    double* s_rem = RP_F64(s_rem);
+    uint32_t* s_seq = RP_U32(s_seq);
+    for (uint32_t e = 0; e < na; ++e) {
+        const uint32_t slot = static_cast<uint32_t>(aff2[e] & 0xffffffffu);
+        const uint32_t g = gp[slot];
+        double rate = dmin(1.0, grate[g & 0xff]);
+        if ((g >> 16) > 1) rate = dmin(rate, grate[(g >> 8) & 0xff]);
+        const double old = s_rate[slot];
+        if (rate == old && s_seq[slot] != kNone) continue;
+        const double dt = __dsub_rn(c.now, s_last[slot]);
+        s_exec[slot] = __dadd_rn(s_exec[slot], __dmul_rn(old, dt));
+        const double rem = dmax0(__dsub_rn(s_rem[slot], __dmul_rn(old, dt)));
+        s_rem[slot] = rem;
+        s_last[slot] = c.now;
+        s_rate[slot] = rate;
+        const uint32_t seq = heap_push<L>(b, c, __dadd_rn(c.now, __ddiv_rn(rem, rate)), (kCompletion << 30) | slot);
+        if (c.status) return;
+        s_seq[slot] = seq;
+    }
+    __syncwarp();
+}
+
+// World::place (world.cpp:73-130) without the trailing refresh_rates:
+// allocate on every GPU in order (rolling back on failure), then take a
+// slot and append the task to the resident lists.
+template <class L>
+__device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint32_t task, int g0, int g1,
+                                      int want, int nblk, unsigned lane) {
+    const uint64_t block = RP_CFG.alloc_block;
+    const uint64_t bytes = tk.true_mem > 0 ? tk.true_mem : 1;
+    const uint64_t nb64 = (bytes + block - 1) / block;
+    const int nb = nb64 > static_cast<uint64_t>(nblk) ? nblk + 1 : static_cast<int>(nb64);
+    int off0 = -1, off1 = 0;
+    if ((g0 & 31) == static_cast<int>(lane) && nb <= nblk) off0 = first_fit<L>(b, g0, nblk, nb);
+    off0 = __shfl_sync(0xffffffffu, off0, g0 & 31);
+    if (off0 < 0) return false;
+    if (want > 1) {
+        int o = -1;
+        if ((g1 & 31) == static_cast<int>(lane)) o = first_fit<L>(b, g1, nblk, nb);
+        o = __shfl_sync(0xffffffffu, o, g1 & 31);
+        if (o < 0) {
+            if ((g0 & 31) == static_cast<int>(lane)) set_bits<L>(RP_U64(used), g0, off0, nb, false);
+            __syncwarp();
+            return false;
+        }
+        off1 = o;
+    }
+    if (c.nfree == 0) {
+        c.status = kStatusRetry;
+        return false;
+    }
+    const uint32_t slot = RP_U32(free_stack)[--c.nfree];
+    RP_U32(s_task)[slot] = task;
+    RP_U32(s_rank)[slot] = tk.rank;
+    RP_F64(s_rem)[slot] = tk.work;
+    RP_F64(s_rate)[slot] = 0.0;
+    RP_F64(s_last)[slot] = c.now;
+    RP_F64(s_exec)[slot] = 0.0;
+    RP_F64(s_dem)[slot] = tk.demand;
+    RP_U32(s_seq)[slot] = kNone;
+    RP_U32(s_gp)[slot] = static_cast<uint32_t>(g0) | (static_cast<uint32_t>(want > 1 ? g1 : 0) << 8) |
+                         (static_cast<uint32_t>(want) << 16);
+    RP_U32(s_off)[slot] = static_cast<uint32_t>(off0) | (static_cast<uint32_t>(off1) << 16);
+    RP_U32(s_nb)[slot] = static_cast<uint32_t>(nb);
+    uint32_t* nres = RP_U32(nres);
+    uint16_t* res = RP_U16(res);
+    for (int k = 0; k < want; ++k) {
+        const int g = k == 0 ? g0 : g1;
+        const uint32_t n = nres[g];
+        if (n >= static_cast<uint32_t>(L::RC)) {
+            c.status = kStatusRetry;
+            return false;
+        }
+        res[g * L::RC + n] = static_cast<uint16_t>(slot);
+        nres[g] = n + 1;
+    }
+    __syncwarp();
+    return true;
+}
+
+// World::finish (world.cpp:132-155) without the trailing refresh_rates.
+template <class L>
+__device__ __forceinline__ void finish(char* b, Sc& c, uint32_t slot, carma_task_result* out, int& g0, int& g1,
+                                       int& want, unsigned lane) {
+    double* s_last = RP_F64(s_last);
+    double* s_rem = RP_F64(s_rem);
+    const double dt = __dsub_rn(c.now, s_last[slot]);
+    const double rate = RP_F64(s_rate)[slot];
+    const double exec = __dadd_rn(RP_F64(s_exec)[slot], __dmul_rn(rate, dt));
+    s_rem[slot] = dmax0(__dsub_rn(s_rem[slot], __dmul_rn(rate, dt)));
+    s_last[slot] = c.now;
+    const uint32_t gp = RP_U32(s_gp)[slot], of = RP_U32(s_off)[slot];
+    want = static_cast<int>(gp >> 16);
+    g0 = static_cast<int>(gp & 0xff);
+    g1 = static_cast<int>((gp >> 8) & 0xff);
+    const int nb = static_cast<int>(RP_U32(s_nb)[slot]);
+    uint32_t* nres = RP_U32(nres);
+    uint16_t* res = RP_U16(res);
+    for (int k = 0; k < want; ++k) {
+        const int g = k == 0 ? g0 : g1;
+        if ((g & 31) == static_cast<int>(lane)) {
+            set_bits<L>(RP_U64(used), g, k == 0 ? static_cast<int>(of & 0xffff) : static_cast<int>(of >> 16), nb, false);
+            // remove_resident preserving insertion order (gpu.cpp:175-181)
+            const uint32_t n = nres[g];
+            uint16_t* rl = res + g * L::RC;
+            uint32_t r = 0;
+            while (r < n && rl[r] != slot) ++r;
+            for (; r + 1 < n; ++r) rl[r] = rl[r + 1];
+            nres[g] = n - 1;
+        }
+    }
+    const uint32_t task = RP_U32(s_task)[slot];
+    if (lane == 0) {
+        out[task].executed = exec;
+        out[task].complete = c.now;
+    }
+    RP_U32(s_seq)[slot] = kNone;
+    RP_U32(free_stack)[c.nfree++] = slot;
+    __syncwarp();
+}
+
+// Manager::try_schedule's decision half (manager.cpp:280-316): gate, head,
+// estimate, map_task. Returns the number of GPUs chosen (0 = no dispatch).
+template <class L>
+__device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, const uint64_t* est,
+                                      uint32_t& head, bool& from_recovery, int& g0, int& g1, unsigned lane) {
+    const carma_replay_config& cf = RP_CFG;
+    const int G = cf.gpu_count;
+    const uint32_t* nres = RP_U32(nres);
+    bool idle_all = true;
+#pragma unroll
+    for (int j = 0; j < L::GPL; ++j) {
+        const int g = static_cast<int>(lane) + 32 * j;
+        if (g < G && nres[g] != 0) idle_all = false;
+    }
+    idle_all = __all_sync(0xffffffffu, idle_all);
+    if (!(c.now >= c.deadline) && !idle_all) return 0;  // gate_open (manager.cpp:269-273)
+    from_recovery = c.rq_cnt > 0;
+    if (from_recovery) head = RP_U32(rq)[c.rq_head];
+    else if (c.mq_head < c.arrived) head = c.mq_head;
+    else return 0;
+    const int policy = from_recovery ? CARMA_POLICY_EXCLUSIVE : cf.policy;
+    uint64_t floor = cf.min_free;
+    if (!from_recovery && cf.policy != CARMA_POLICY_EXCLUSIVE) {
+        const uint64_t e = est ? est[head] : tasks[head].estimate;
+        if (e != CARMA_NO_ESTIMATE) {
+            const uint64_t need = e < cf.gpu_capacity ? e : cf.gpu_capacity;
+            if (need > floor) floor = need;
+        }
+    }
+    const bool need_smact = policy != CARMA_POLICY_EXCLUSIVE &&
+                            !(policy == CARMA_POLICY_RR && !cf.rr_apply_preconditions);
+    const uint64_t* used = RP_U64(used);
+    PickInput in[L::GPL];
+#pragma unroll
+    for (int j = 0; j < L::GPL; ++j) {
+        const int g = static_cast<int>(lane) + 32 * j;
+        const bool valid = g < G;
+        in[j].valid = valid;
+        in[j].idle = valid && nres[g] == 0;
+        in[j].free_bytes = valid ? static_cast<uint64_t>(free_blocks<L>(used, g)) * cf.alloc_block : 0;
+        in[j].smact = (valid && need_smact) ? windowed<L>(b, g, c.now, c.window) : 0.0;
+    }
+    int gids[2];
+    const int got = pick_gpus<L::GPL>(cf, policy, tasks[head].gpus, floor, in, lane, 0, 32, c.rr_cursor, gids);
+    g0 = gids[0];
+    g1 = gids[1];
+    return got;
+}
+
+// Per-job setup. Cold (once per job): kept out of line.
+template <class L>
+__device__ __noinline__ void init_job(char* b, const Params& p, uint32_t j, unsigned lane, Sc& c,
+                                      const carma_task*& tasks, carma_task_result*& out, int& nblk) {
+    const carma_replay_job job = p.jobs[j];
+    const carma_replay_config* src = p.cfgs + job.config;
+    if (lane < sizeof(carma_replay_config) / 8)
+        reinterpret_cast<uint64_t*>(b + L::cfg)[lane] = reinterpret_cast<const uint64_t*>(src)[lane];
+    __syncwarp();
+    const carma_replay_config& cf = RP_CFG;
+    const uint64_t tb = p.trace_off[job.trace];
+    const uint32_t T = static_cast<uint32_t>(p.trace_off[job.trace + 1] - tb);
+    tasks = p.tasks + tb;
+    out = p.task_out + p.task_out_off[j];
+    nblk = static_cast<int>(cf.gpu_capacity / cf.alloc_block);
+    // first_submit (runner.cpp:108-109) and the full-history window begin.
+    double fs = tasks[0].submit;
+    for (uint32_t i = lane; i < T; i += 32) fs = dmin(fs, tasks[i].submit);
+    for (int o = 16; o > 0; o >>= 1) fs = dmin(fs, __shfl_xor_sync(0xffffffffu, fs, o));
+    const double forced = p.smact_begin[j];
+    c.begin0 = forced == forced ? forced : dmax0(fs);
+    for (uint32_t i = lane; i < T; i += 32) {
+        carma_task_result r;
+        r.first_attempt = r.final_dispatch = r.complete = r.first_crash = r.last_crash = -1.0;
+        r.executed = 0.0;
+        r.attempts = r.ooms = 0;
+        r.gpu[0] = r.gpu[1] = -1;
+        r.reserved = 0;
+        out[i] = r;
+    }
+    uint64_t* used = RP_U64(used);
+    double p0 = __dadd_rn(cf.p_idle_w, __dmul_rn(__dsub_rn(cf.p_max_w, cf.p_idle_w), 0.0));
+    if (0.0 > cf.boost_threshold) p0 = __dadd_rn(p0, cf.p_boost_w);
+    for (int g = static_cast<int>(lane); g < L::G; g += 32) {
+#pragma unroll
+        for (int w = 0; w < kWords; ++w) {
+            const int lo = w * 64;
+            uint64_t m = ~0ull;
+            if (nblk > lo) m = nblk - lo >= 64 ? 0ull : (~0ull << (nblk - lo));
+            used[w * L::G + g] = m;
+        }
+        RP_F64(energy)[g] = 0.0;
+        RP_F64(rate)[g] = 0.0;
+        RP_F64(inst)[g] = 0.0;
+        RP_F64(power)[g] = p0;
+        RP_F64(lvl)[g] = 0.0;
+        RP_F64(cur)[g] = c.begin0;
+        RP_F64(integ)[g] = 0.0;
+        RP_F64(last_t)[g] = 0.0;
+        RP_F64(last_v)[g] = 0.0;
+        RP_U32(nres)[g] = 0;
+        RP_U32(nsteps)[g] = 0;
+        RP_U32(rhead)[g] = 0;
+        RP_U32(rcnt)[g] = 0;
+        RP_U32(peak)[g] = 0;
+        RP_U32(has_step)[g] = 0;
+    }
+    for (int k = static_cast<int>(lane); k < L::S; k += 32) RP_U32(free_stack)[k] = L::S - 1 - k;
+    c.now = 0.0;
+    c.deadline = 0.0;
+    c.window = cf.monitor_window;
+    c.seq_next = T;
+    c.arrived = 0;
+    c.mq_head = 0;
+    c.rq_head = 0;
+    c.rq_cnt = 0;
+    c.hsize = 0;
+    c.nfree = L::S;
+    c.T = T;
+    c.rr_cursor = 0;
+    c.oom = 0;
+    c.status = 0;
+    c.events_lo = c.events_hi = 0;
+    __syncwarp();
+}
+
+// Runner tail + report. Cold: out of line.
+template <class L>
+__device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, unsigned lane, const Sc& c,
+                                        const carma_task* tasks, carma_task_result* out) {
+    const carma_replay_config& cf = RP_CFG;
+    carma_trace_result& tr = p.trace_out[j];
+    if (c.status == kStatusRetry) {
+        if (lane == 0) {
+            tr.status = kStatusRetry;
+            p.retry_list[atomicAdd(p.retry_count, 1u)] = j;
+        }
+        return;
+    }
+    const uint32_t T = c.T;
+    uint32_t* inv = p.inv_scratch + p.task_out_off[j];
+    double lc = 0.0, fs = tasks[0].submit;
+    bool complete = true;
+    for (uint32_t i = lane; i < T; i += 32) {
+        carma_task_result& o = out[i];
+        const double cpl = o.complete;
+        lc = lc < cpl ? cpl : lc;  // std::max(last_complete, t.complete)
+        fs = dmin(fs, tasks[i].submit);
+        complete = complete && cpl >= 0.0;
+        o.attempts = o.ooms + (o.final_dispatch >= 0.0 ? 1u : 0u);
+        inv[tasks[i].rank] = i;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double x = __shfl_xor_sync(0xffffffffu, lc, o);
+        lc = lc < x ? x : lc;
+        fs = dmin(fs, __shfl_xor_sync(0xffffffffu, fs, o));
+    }
+    complete = __all_sync(0xffffffffu, complete);
+    int32_t status = c.status;
+    if (status == 0 && !complete) status = CARMA_ERR_INCOMPLETE;
+    const double span = __dsub_rn(lc, fs);
+    const double begin_actual = dmax0(__dsub_rn(lc, span));
+    const double forced = p.smact_begin[j];
+    if (status == 0 && span > 0.0 && !(forced == forced) && begin_actual != c.begin0) {
+        // Re-run with the true window begin (see file header).
+        if (lane == 0) {
+            p.smact_begin[j] = begin_actual;
+            tr.status = kStatusRedoSmact;
+            p.retry_list[atomicAdd(p.retry_count, 1u)] = j;
+        }
+        return;
+    }
+    const int G = cf.gpu_count;
+    carma_gpu_result* gout = p.gpu_out + p.gpu_out_off[j];
+    const double overshoot = __dsub_rn(c.now, lc);
+    double energy = 0.0;
+    for (int g = 0; g < G; ++g) {
+        double e = RP_F64(energy)[g];
+        if (overshoot > 0.0) e = __dsub_rn(e, __dmul_rn(RP_F64(power)[g], overshoot));
+        energy = __dadd_rn(energy, e);
+        if ((g & 31) == static_cast<int>(lane)) {
+            carma_gpu_result r;
+            r.energy_j = e;
+            double mean = 0.0;
+            if (span > 0.0)
+                mean = __ddiv_rn(__dadd_rn(RP_F64(integ)[g], __dmul_rn(RP_F64(lvl)[g], __dsub_rn(lc, RP_F64(cur)[g]))),
+                                 span);
+            r.mean_smact = mean;
+            r.peak_used = static_cast<uint64_t>(RP_U32(peak)[g]) * cf.alloc_block;
+            r.smact_steps = RP_U32(nsteps)[g];
+            gout[g] = r;
+        }
+    }
+    __syncwarp();
+    // Sums in id (rank) order (metrics.cpp:25-45): each lane stages 32
+    // values; lane order is rank order.
+    double ws = 0.0, es = 0.0, js = 0.0;
+    for (uint32_t base = 0; base < T; base += 32) {
+        const uint32_t r = base + lane;
+        double w = 0.0, e = 0.0, jc = 0.0;
+        if (r < T) {
+            const uint32_t i = inv[r];
+            const double sub = tasks[i].submit;
+            const double fd = out[i].final_dispatch, cp = out[i].complete;
+            w = __dsub_rn(fd, sub);
+            e = __dsub_rn(cp, fd);
+            jc = __dsub_rn(cp, sub);
+        }
+        const uint32_t cnt = min(32u, T - base);
+        for (uint32_t l = 0; l < cnt; ++l) {
+            ws = __dadd_rn(ws, __shfl_sync(0xffffffffu, w, l));
+            es = __dadd_rn(es, __shfl_sync(0xffffffffu, e, l));
+            js = __dadd_rn(js, __shfl_sync(0xffffffffu, jc, l));
+        }
+    }
+    if (lane == 0) {
+        const double nd = static_cast<double>(T);
+        carma_trace_result r;
+        r.trace_total_time = span;
+        r.avg_wait = __ddiv_rn(ws, nd);
+        r.avg_exec = __ddiv_rn(es, nd);
+        r.avg_jct = __ddiv_rn(js, nd);
+        r.energy_mj = __ddiv_rn(energy, 1e6);
+        r.first_submit = fs;
+        r.last_complete = lc;
+        r.end_time = c.now;
+        r.oom_count = c.oom;
+        r.status = status;
+        r.events = (static_cast<uint64_t>(c.events_hi) << 32) | c.events_lo;
+        tr = r;
+    }
+}
+
+template <class L>
+__device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, unsigned lane) {
+    Sc c;
+    const carma_task* tasks;
+    carma_task_result* out;
+    int nblk;
+    init_job<L>(b, p, j, lane, c, tasks, out, nblk);
+    const uint64_t* est = p.est_override ? p.est_override + p.trace_off[p.jobs[j].trace] : nullptr;
+    const uint64_t max_events = 1000ull * c.T + 1000000ull;
+    uint64_t events = 0;
+    const double delay = RP_CFG.oom_startup_delay;
+    for (;;) {
+        // ---- next event: arrival stream (seq = index) vs heap top
+        const bool have_arr = c.arrived < c.T;
+        const bool have_heap = c.hsize > 0;
+        if (!have_arr && !have_heap) break;
+        if (events >= max_events) {
+            c.status = CARMA_ERR_INCOMPLETE;
+            break;
+        }
+        double t;
+        uint32_t kind, payload, seq = 0;
+        const double at = have_arr ? tasks[c.arrived].submit : 0.0;
+        if (have_arr && (!have_heap || !later(at, c.arrived, RP_F64(ht)[0], RP_U32(hs)[0]))) {
+            t = at;
+            kind = 0;
+            payload = c.arrived;
+        } else {
+            t = RP_F64(ht)[0];
+            seq = RP_U32(hs)[0];
+            const uint32_t info = RP_U32(hinfo)[0];
+            kind = info >> 30;
+            payload = info & 0x3fffffffu;
+            heap_pop<L>(b, c);
+        }
+        ++events;
+        // ---- integrate_to (world.cpp:37-44)
+        const double dt = __dsub_rn(t, c.now);
+        if (dt > 0.0) {
+            double* energy = RP_F64(energy);
+            const double* power = RP_F64(power);
+            const int G = RP_CFG.gpu_count;
+#pragma unroll
+            for (int jj = 0; jj < L::GPL; ++jj) {
+                const int g = static_cast<int>(lane) + 32 * jj;
+                if (g < G) energy[g] = __dadd_rn(energy[g], __dmul_rn(power[g], dt));
+            }
+        }
+        c.now = t;
+        // ---- handle (World::step + Manager::on_event, manager.cpp:333-357)
+        bool sched = true;
+        int t0 = 0, t1 = 0, nt = 0;
+        if (kind == 0) {
+            c.arrived++;  // Manager::submit: joins the main queue
+        } else if (kind == kWindow) {
+            sched = t == c.deadline;
+        } else if (kind == kCompletion) {
+            if (RP_U32(s_seq)[payload] != seq) continue;  // superseded by a rate change
+            finish<L>(b, c, payload, out, t0, t1, nt, lane);
+        } else {  // oom_crash -> handle_oom (manager.cpp:262-267)
+            c.oom++;
+            if (lane == 0) {
+                carma_task_result& o = out[payload];
+                o.ooms += 1;
+                if (o.first_crash < 0.0) o.first_crash = c.now;
+                o.last_crash = c.now;
+            }
+            if (c.rq_cnt >= static_cast<uint32_t>(L::RQ)) {
+                c.status = kStatusRetry;
+                break;
+            }
+            uint32_t tail = c.rq_head + c.rq_cnt;
+            if (tail >= static_cast<uint32_t>(L::RQ)) tail -= L::RQ;
+            RP_U32(rq)[tail] = payload;
+            c.rq_cnt++;
+            __syncwarp();
+        }
+        // ---- refresh_rates after finish / place, then try_schedule
+        for (;;) {
+            if (nt) {
+                refresh_rates<L>(b, c, t0, t1, nt, lane);
+                nt = 0;
+                if (c.status) break;
+            }
+            if (!sched) break;
+            sched = false;
+            uint32_t head = 0;
+            bool from_recovery = false;
+            int g0 = -1, g1 = -1;
+            const int got = decide<L>(b, c, tasks, est, head, from_recovery, g0, g1, lane);
+            if (got == 0) break;  // defer; retried on the next completion / expiry
+            if (from_recovery) {
+                c.rq_head = c.rq_head + 1 == static_cast<uint32_t>(L::RQ) ? 0 : c.rq_head + 1;
+                c.rq_cnt--;
+            } else {
+                c.mq_head++;
+            }
+            // dispatch (manager.cpp:247-260)
+            if (lane == 0 && !from_recovery) out[head].first_attempt = c.now;
+            const bool ok = place<L>(b, c, tasks[head], head, g0, g1, got, nblk, lane);
+            if (c.status) break;
+            if (ok) {
+                if (lane == 0) {
+                    carma_task_result& o = out[head];
+                    o.final_dispatch = c.now;
+                    o.gpu[0] = static_cast<int16_t>(g0);
+                    o.gpu[1] = static_cast<int16_t>(got > 1 ? g1 : -1);
+                }
+                t0 = g0;
+                t1 = g1;
+                nt = got;
+            } else {
+                heap_push<L>(b, c, __dadd_rn(c.now, delay), (kCrash << 30) | head);
+            }
+            // arm_window (manager.cpp:275-278)
+            c.deadline = __dadd_rn(c.now, c.window);
+            heap_push<L>(b, c, c.deadline, kWindow << 30);
+            if (c.status) break;
+        }
+        if (c.status) break;
+        __syncwarp();
+    }
+    c.events_lo = static_cast<uint32_t>(events);
+    c.events_hi = static_cast<uint32_t>(events >> 32);
+    __syncwarp();
+    finish_job<L>(b, p, j, lane, c, tasks, out);
+}
+
+template <class L, bool SMEM>
+__global__ void __launch_bounds__(128, SMEM ? 6 : 1) replay_kernel(Params p) {
+    extern __shared__ __align__(16) char smem[];
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned wib = threadIdx.x >> 5;
+    char* b = SMEM ? smem + static_cast<size_t>(wib) * L::bytes
+                   : p.gstate + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * L::bytes;
+    for (;;) {
+        unsigned k = 0;
+        if (lane == 0) k = atomicAdd(p.next_job, 1u);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= p.n_list) break;
+        run_job<L>(b, p, p.job_list[k], lane);
+        __syncwarp();
+    }
+}
+
+#undef RP_F64
+#undef RP_U32
+#undef RP_U64
+#undef RP_U16
+#undef RP_CFG
+
+}  // namespace replay
+}  // namespace carma_b200

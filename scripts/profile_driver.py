@@ -1,0 +1,74 @@
+"""Small single-purpose drivers for ncu captures (one GPU).
+
+  python scripts/profile_driver.py replay --traces 20000 --policies magm,rr
+  python scripts/profile_driver.py knn --rows 4194304
+
+Each runs the workload `--reps` times (default 2) so `ncu -k regex:<kernel> -s <n> -c 1`
+can skip the first launch.
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2508_19073_b200 as cb  # noqa: E402
+from paper_2508_19073_b200 import abi  # noqa: E402
+
+
+def replay(args):
+    pols = args.policies.split(",")
+    lists = [cb.materialize_trace(cb.generate_trace("t90", s)).tasks for s in range(1, args.traces + 1)]
+    tasks = np.concatenate(lists)
+    offs = np.concatenate([[0], np.cumsum([len(t) for t in lists])]).astype(np.uint64)
+    cfgs = np.concatenate([cb.make_config(cb.PolicyConfig(policy=p, max_smact=0.8), cb.SimConstants()) for p in pols])
+    jobs = np.zeros(args.traces * len(pols), abi.job_dtype)
+    jobs["trace"] = np.tile(np.arange(args.traces, dtype=np.uint32), len(pols))
+    jobs["config"] = np.repeat(np.arange(len(pols), dtype=np.uint32), args.traces)
+    plan = cb.ReplayPlan(cfgs, tasks, offs, jobs)
+    import ctypes
+    km, rm = ctypes.c_double(), ctypes.c_double()
+    for _ in range(args.reps):
+        plan.run()
+        abi.check(abi.lib.carma_replay_plan_timing(plan._h, ctypes.byref(km), ctypes.byref(rm)))
+        print(f"replay {len(jobs)} jobs: tier0 {km.value:.2f} ms, run {rm.value:.2f} ms, "
+              f"stats {plan.stats()}", flush=True)
+    res = plan.results(tasks=False)
+    print("events", int(res.traces["events"].sum()), "status!=0", int((res.traces["status"] != 0).sum()))
+
+
+def knn(args):
+    import torch
+    ds = [cb.generate_synthetic_dataset(f, args.rows // 2, s) for f, s in ((1, 2024), (2, 2025))]
+    rows = np.concatenate([d.rows for d in ds])
+    fam = np.concatenate([np.full(args.rows // 2, 1, np.int8), np.full(args.rows // 2, 2, np.int8)])
+    k = cb.GpuKnn(0)
+    k.set_model(cb.fit_knn(1, 4000, 112, 5))
+    k.set_model(cb.fit_knn(2, 4000, 213, 5))
+    d_rows = torch.from_numpy(rows.view(np.uint8)).cuda()
+    d_fam = torch.from_numpy(fam).cuda()
+    b = torch.empty(len(rows), dtype=torch.int32, device="cuda")
+    by = torch.empty(len(rows), dtype=torch.int64, device="cuda")
+    import ctypes
+    sm, pm = ctypes.c_double(), ctypes.c_double()
+    for _ in range(args.reps):
+        abi.check(abi.lib.carma_knn_predict_device(k.handle, d_rows.data_ptr(), 0, d_fam.data_ptr(), 1, len(rows),
+                                                   b.data_ptr(), by.data_ptr(), None, None, None))
+        abi.check(abi.lib.carma_knn_last_timing(k.handle, ctypes.byref(sm), ctypes.byref(pm)))
+        print(f"knn {len(rows)} rows: search {sm.value:.2f} ms pipeline {pm.value:.2f} ms stats {k.last_stats()}",
+              flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", choices=("replay", "knn"))
+    ap.add_argument("--traces", type=int, default=20000)
+    ap.add_argument("--policies", default="exclusive,rr,magm,lug")
+    ap.add_argument("--rows", type=int, default=1 << 22)
+    ap.add_argument("--reps", type=int, default=2)
+    a = ap.parse_args()
+    replay(a) if a.what == "replay" else knn(a)
