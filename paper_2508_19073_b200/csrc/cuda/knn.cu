@@ -247,17 +247,23 @@ __device__ __forceinline__ double t18_of(double key, double q18) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
     knn_search(KnnParams p, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ qpos,
                int32_t* __restrict__ bucket_out, uint64_t* __restrict__ bytes_out,
                double* __restrict__ topk_d2, int64_t* __restrict__ topk_idx,
                unsigned long long* __restrict__ evals) {
     const unsigned lane = threadIdx.x & 31;
-    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    // Each CTA walks one contiguous range of the bin-sorted queries (its
+    // warps interleaved), so an SM's warps search neighbouring regions of the
+    // model and the points stay L1-resident.
+    const uint64_t total_w = (p.q + 31) / 32;
+    const uint64_t per_cta = (total_w + gridDim.x - 1) / gridDim.x;
+    const uint64_t w_beg = per_cta * blockIdx.x;
+    const uint64_t w_end = min(total_w, w_beg + per_cta);
+    const unsigned wpc = blockDim.x >> 5;
     unsigned long long my_evals = 0;
 
-    for (uint64_t w = warp; w * 32 < p.q; w += n_warps) {
+    for (uint64_t w = w_beg + (threadIdx.x >> 5); w < w_end; w += wpc) {
         const uint64_t slot = w * 32 + lane;
         const bool live = slot < p.q;
         const uint32_t row = live ? perm[slot] : 0;
@@ -325,33 +331,35 @@ __global__ void __launch_bounds__(128)
                 const double rl = __shfl_sync(0xffffffffu, need_l ? tl : inf, mid_lane);
                 const double rr = __shfl_sync(0xffffffffu, need_r ? tr : inf, mid_lane);
                 const bool go_left = bl != 0 && (br == 0 || rl <= rr);
-                // Next block of up to kBlock contiguous points on that side.
-                int64_t i0, cnt;
+                // Next block of kBlock contiguous points on that side. The
+                // stored model is padded by kBlock points at both ends, so a
+                // block never leaves the allocation; slots outside [0, n) are
+                // evaluated but never inserted.
+                int64_t s0;
+                unsigned valid;
                 if (go_left) {
-                    i0 = L > kBlock ? L - kBlock : 0;
-                    cnt = L - i0;
-                    L = i0;
+                    s0 = L - kBlock;
+                    valid = L >= kBlock ? 0xffu : (0xffu << (kBlock - L)) & 0xffu;
+                    L = L > kBlock ? L - kBlock : 0;
                 } else {
-                    i0 = R;
-                    cnt = n - R < kBlock ? n - R : kBlock;
-                    R += cnt;
+                    s0 = R;
+                    valid = n - R >= kBlock ? 0xffu : (1u << (n - R)) - 1u;
+                    R = n - R > kBlock ? R + kBlock : n;
                 }
+                const int64_t cnt = __popc(valid);
                 // kBlock independent accumulation chains; each d2 keeps the
                 // reference's dim order. Dims outside `act` contribute exactly
                 // +0.0 and are skipped (warp-uniform branch).
                 double d2[kBlock];
-                const double* base[kBlock];
+                const double* blk = m.pts + s0 * kStride;
 #pragma unroll
-                for (int c = 0; c < kBlock; ++c) {
-                    d2[c] = 0.0;
-                    base[c] = m.pts + (i0 + (c < cnt ? c : cnt - 1)) * kStride;
-                }
+                for (int c = 0; c < kBlock; ++c) d2[c] = 0.0;
 #pragma unroll
                 for (int h = 0; h < 9; ++h) {
                     if (!(act & (3u << (2 * h)))) continue;
                     double2 v[kBlock];
 #pragma unroll
-                    for (int c = 0; c < kBlock; ++c) v[c] = __ldg(reinterpret_cast<const double2*>(base[c]) + h);
+                    for (int c = 0; c < kBlock; ++c) v[c] = __ldg(reinterpret_cast<const double2*>(blk + c * kStride) + h);
                     if (act & (1u << (2 * h))) {
 #pragma unroll
                         for (int c = 0; c < kBlock; ++c) {
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(128)
                 if (act & (1u << 18)) {
 #pragma unroll
                     for (int c = 0; c < kBlock; ++c) {
-                        const double a = __dmul_rn(__dsub_rn(__ldg(base[c] + 18), q[18]), 64.0);
+                        const double a = __dmul_rn(__dsub_rn(__ldg(blk + c * kStride + 18), q[18]), 64.0);
                         d2[c] = __dadd_rn(d2[c], __dmul_rn(a, a));
                     }
                 }
@@ -380,9 +388,10 @@ __global__ void __launch_bounds__(128)
                 const double kb = top.kth();
                 unsigned cand = 0;
 #pragma unroll
-                for (int c = 0; c < kBlock; ++c) cand |= (c < cnt && d2[c] <= kb) ? (1u << c) : 0u;
+                for (int c = 0; c < kBlock; ++c) cand |= (d2[c] <= kb) ? (1u << c) : 0u;
+                cand &= valid;
                 if (!mine) cand = 0;
-                if (cand) insert_block<K>(top, d2, cand, m.orig + i0);
+                if (cand) insert_block<K>(top, d2, cand, m.orig + s0);
                 if (go_left) tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q[18]) : t_in) : inf;
                 else tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q[18]) : t_in) : inf;
                 steps += static_cast<uint64_t>(cnt);
@@ -463,7 +472,7 @@ KnnParams make_params(const KnnHandle& h, uint32_t* n_bins) {
         ModelDev& m = p.m[f];
         m.present = hm.present ? 1 : 0;
         if (!hm.present) continue;
-        m.pts = hm.pts.as<double>();
+        m.pts = hm.pts.as<double>() + kBlock * kStride;
         m.key18 = hm.key18.as<double>();
         m.orig = hm.orig.as<int32_t>();
         m.label_by_orig = hm.label_by_orig.as<int32_t>();
@@ -495,7 +504,9 @@ void launch_search(const KnnParams& p, int kmax, const uint32_t* perm, const uin
                    unsigned long long* evals, cudaStream_t s) {
     const uint64_t warps = (p.q + 31) / 32;
     const unsigned block = 128;
-    const unsigned grid = grid_for(warps * 32, block, 148u * 64u);
+    // ~16 CTAs per SM over the run (4 resident): small contiguous chunks keep
+    // the tail short while each CTA stays in one region of the model.
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, 148u * 16u)));
     if (kmax <= 5)
         knn_search<5><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
     else if (kmax <= 8)
@@ -689,18 +700,19 @@ carma_status carma_knn_set_model(carma_knn* hh, int32_t family, const double* lo
         std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
             return points[static_cast<uint64_t>(a) * kDims + 18] < points[static_cast<uint64_t>(b) * kDims + 18];
         });
-        std::vector<double> pts(n * kStride, 0.0), key(n);
+        // kBlock padding points on both sides (never inserted; see knn_search)
+        std::vector<double> pts((n + 2 * kBlock) * kStride, 0.0), key(n);
         for (uint64_t i = 0; i < n; ++i) {
             const double* src = points + static_cast<uint64_t>(order[i]) * kDims;
-            std::memcpy(&pts[i * kStride], src, sizeof(double) * kDims);
+            std::memcpy(&pts[(i + kBlock) * kStride], src, sizeof(double) * kDims);
             key[i] = src[18];
         }
         HostModel& m = h->model[family];
-        m.pts.ensure(n * kStride * 8);
+        m.pts.ensure((n + 2 * kBlock) * kStride * 8);
         m.key18.ensure(n * 8);
         m.orig.ensure(n * 4);
         m.label_by_orig.ensure(n * 4);
-        CARMA_CUDA(cudaMemcpy(m.pts.ptr, pts.data(), n * kStride * 8, cudaMemcpyHostToDevice));
+        CARMA_CUDA(cudaMemcpy(m.pts.ptr, pts.data(), (n + 2 * kBlock) * kStride * 8, cudaMemcpyHostToDevice));
         CARMA_CUDA(cudaMemcpy(m.key18.ptr, key.data(), n * 8, cudaMemcpyHostToDevice));
         CARMA_CUDA(cudaMemcpy(m.orig.ptr, order.data(), n * 4, cudaMemcpyHostToDevice));
         CARMA_CUDA(cudaMemcpy(m.label_by_orig.ptr, labels, n * 4, cudaMemcpyHostToDevice));

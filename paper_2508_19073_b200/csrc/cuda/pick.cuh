@@ -27,57 +27,47 @@ __device__ __forceinline__ unsigned group_bits(unsigned ballot, unsigned base, u
     return width == 32 ? ballot : (ballot >> base) & ((1u << width) - 1u);
 }
 
-// Argmax of (free desc, id asc) / argmin|argmax of (smact, id asc) over the
-// lane's candidates, then across the group.
+// Orderable 64-bit key of a double: same order as <, +0 == -0.
+__device__ __forceinline__ uint64_t dkey(double x) {
+    if (x == 0.0) x = 0.0;
+    const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// The policy's sort key as "larger is better" (manager.cpp:217-224):
+// MAGM total_free descending, LUG windowed SMACT ascending, MUG descending.
+__device__ __forceinline__ uint64_t policy_key(int policy, const PickInput& in) {
+    if (policy == CARMA_POLICY_MAGM) return in.free_bytes;
+    const uint64_t k = dkey(in.smact);
+    return policy == CARMA_POLICY_LUG ? ~k : k;
+}
+
+// Arg-best of (key desc, id asc) over the lane's candidates, then across the
+// group (stable_sort by key with ties to the lowest id). -1 when none.
 template <int GPL>
 __device__ __forceinline__ int arg_best(int policy, const PickInput (&in)[GPL], const bool (&cand)[GPL],
                                         unsigned lane_in_group, unsigned width) {
-    // best key per lane: (valid, value, id)
-    bool have = false;
-    uint64_t bf = 0;
-    double bs = 0.0;
-    int bid = 0x7fffffff;
+    uint64_t bk = 0;
+    int bid = 0x7fffffff;  // sentinel: loses to every real candidate
 #pragma unroll
     for (int j = 0; j < GPL; ++j) {
-        if (!cand[j]) continue;
+        const uint64_t k = policy_key(policy, in[j]);
         const int id = static_cast<int>(lane_in_group + j * width);
-        bool better;
-        if (!have) better = true;
-        else if (policy == CARMA_POLICY_MAGM)
-            better = in[j].free_bytes > bf || (in[j].free_bytes == bf && id < bid);
-        else if (policy == CARMA_POLICY_LUG)
-            better = in[j].smact < bs || (in[j].smact == bs && id < bid);
-        else
-            better = in[j].smact > bs || (in[j].smact == bs && id < bid);
-        if (better) {
-            have = true;
-            bf = in[j].free_bytes;
-            bs = in[j].smact;
+        if (cand[j] && (k > bk || (k == bk && id < bid))) {
+            bk = k;
             bid = id;
         }
     }
+#pragma unroll 1
     for (unsigned off = 1; off < width; off <<= 1) {
-        const bool oh = __shfl_xor_sync(0xffffffffu, have, off, width);
-        const uint64_t of = __shfl_xor_sync(0xffffffffu, bf, off, width);
-        const double os = __shfl_xor_sync(0xffffffffu, bs, off, width);
+        const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off, width);
         const int oid = __shfl_xor_sync(0xffffffffu, bid, off, width);
-        bool take;
-        if (!oh) take = false;
-        else if (!have) take = true;
-        else if (policy == CARMA_POLICY_MAGM)
-            take = of > bf || (of == bf && oid < bid);
-        else if (policy == CARMA_POLICY_LUG)
-            take = os < bs || (os == bs && oid < bid);
-        else
-            take = os > bs || (os == bs && oid < bid);
-        if (take) {
-            have = true;
-            bf = of;
-            bs = os;
+        if (ok > bk || (ok == bk && oid < bid)) {
+            bk = ok;
             bid = oid;
         }
     }
-    return have ? bid : -1;
+    return bid == 0x7fffffff ? -1 : bid;
 }
 
 // One decision. policy is the effective policy (exclusive for recovery tasks).
@@ -110,17 +100,18 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
     const bool sorted = policy == CARMA_POLICY_MAGM || policy == CARMA_POLICY_LUG || policy == CARMA_POLICY_MUG;
     // MAGM / LUG / MUG: stable sort by key then id == repeated arg-best.
     int best[2] = {-1, -1};
-    if (__any_sync(0xffffffffu, ok && sorted)) {
-        bool cand[GPL];
+    const int rounds = __any_sync(0xffffffffu, ok && sorted && want > 1) ? 2
+                       : (__any_sync(0xffffffffu, ok && sorted) ? 1 : 0);
+    bool cand[GPL];
 #pragma unroll
-        for (int j = 0; j < GPL; ++j) cand[j] = el[j];
-        best[0] = arg_best<GPL>(policy, in, cand, lane_in_group, width);
-        if (__any_sync(0xffffffffu, ok && sorted && want > 1)) {
+    for (int j = 0; j < GPL; ++j) cand[j] = el[j];
+#pragma unroll 1
+    for (int r = 0; r < rounds; ++r) {
+        const int g = arg_best<GPL>(policy, in, cand, lane_in_group, width);
+        best[r] = g;
 #pragma unroll
-            for (int j = 0; j < GPL; ++j)
-                if (static_cast<int>(lane_in_group + j * width) == best[0]) cand[j] = false;
-            best[1] = arg_best<GPL>(policy, in, cand, lane_in_group, width);
-        }
+        for (int j = 0; j < GPL; ++j)
+            if (static_cast<int>(lane_in_group + j * width) == g) cand[j] = false;
     }
     if (!ok) return 0;
     if (sorted) {

@@ -74,9 +74,9 @@ struct ReplayPlan {
     uint32_t n_traces = 0;
     uint64_t n_tasks = 0, n_task_out = 0, n_gpu_out = 0;
     int max_g = 1;
-    uint32_t class_count[2] = {0, 0};
-    int class_max_g[2] = {1, 1};
-    std::vector<uint32_t> class_list;  // jobs ordered light class first, then heavy
+    uint32_t class_count[3] = {0, 0, 0};
+    int class_max_g[3] = {1, 1, 1};
+    std::vector<uint32_t> class_list;  // jobs ordered: light, heavy, global-only
     DeviceBuffer d_cfgs, d_tasks, d_trace_off, d_jobs, d_task_off, d_gpu_off, d_list, d_task_out,
         d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate;
     const uint64_t* est_override = nullptr;
@@ -93,9 +93,9 @@ using replay::Layout;
 // at <= 34 pending events and 8 residents; RR without preconditions stacks
 // up to 34 residents (11 per GPU) and ~200 pending events (stale completion
 // events stay queued: they are energy-integration breakpoints).
-template <int G> using LightL = Layout<G, 64, 32, 16, 16, 16>;
-template <int G> using HeavyL = Layout<G, 320, 64, 32, 16, 16>;
-using GlobalL = Layout<64, 8192, 2048, 256, 256, 4096>;
+template <int G> using LightL = Layout<G, 64, 32, 16, 16, 16, 2>;
+template <int G> using HeavyL = Layout<G, 320, 64, 32, 16, 16, 2>;
+using GlobalL = Layout<64, 8192, 2048, 256, 256, 4096, 4>;
 
 // Configs whose policy can stack tasks without utilisation preconditions.
 bool heavy_config(const carma_replay_config& c) {
@@ -112,7 +112,7 @@ void validate_config(const carma_replay_config& c) {
     if (c.alloc_block == 0) throw Unsupported("alloc_block = 0 is not supported");
     if (c.gpu_capacity % c.alloc_block != 0)
         throw Unsupported("gpu_capacity must be a multiple of alloc_block");
-    if (c.gpu_capacity / c.alloc_block > 64ull * replay::kWords)
+    if (c.gpu_capacity / c.alloc_block > 64ull * replay::kMaxWords)
         throw Unsupported("more than 256 allocation blocks per GPU");
 }
 
@@ -204,10 +204,16 @@ void run_plan(ReplayPlan& pl) {
     if (r0) CARMA_CUDA(cudaMemcpy(ids.data(), retry, r0 * 4, cudaMemcpyDeviceToHost));
     if (total > r0)
         CARMA_CUDA(cudaMemcpy(ids.data() + r0, retry + pl.class_count[0], (total - r0) * 4, cudaMemcpyDeviceToHost));
-    // Overflowed or begin-corrected jobs re-run in the global-memory tier (at
-    // most twice: a begin correction can follow an overflow).
+    // jobs that only fit the global tier
+    const uint32_t gbeg = pl.class_count[0] + pl.class_count[1];
+    ids.insert(ids.end(), pl.class_list.begin() + gbeg, pl.class_list.end());
+    pl.retried = total;  // jobs that overflowed a shared-memory tier
+    total = static_cast<uint32_t>(ids.size());
+    const bool list_dirty = total > 0;
+    // Overflowed, global-only or begin-corrected jobs run in the global-memory
+    // tier (at most twice: a begin correction can follow an overflow).
     for (int round = 0; round < 2 && total > 0; ++round) {
-        pl.retried += total;
+        if (round > 0) pl.retried += total;
         CARMA_CUDA(cudaMemcpy(list, ids.data(), total * 4, cudaMemcpyHostToDevice));
         launch_tier(pl, p, list, total, 2, pl.max_g, counters, retry);
         uint32_t nr = 0;
@@ -218,7 +224,7 @@ void run_plan(ReplayPlan& pl) {
         if (total) CARMA_CUDA(cudaMemcpy(ids.data(), retry, total * 4, cudaMemcpyDeviceToHost));
     }
     CARMA_CUDA(cudaEventRecord(pl.ev[2], pl.stream));
-    if (pl.retried) CARMA_CUDA(cudaMemcpy(list, pl.class_list.data(), n * 4, cudaMemcpyHostToDevice));
+    if (list_dirty) CARMA_CUDA(cudaMemcpy(list, pl.class_list.data(), n * 4, cudaMemcpyHostToDevice));
 }
 
 }  // namespace
@@ -286,10 +292,12 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
             up(pl->d_task_off, task_off.data(), n_jobs * sizeof(uint64_t));
             up(pl->d_gpu_off, gpu_off.data(), n_jobs * sizeof(uint64_t));
             std::vector<uint32_t> list(2 * static_cast<size_t>(n_jobs));
-            for (int cls = 0; cls < 2; ++cls)
+            for (int cls = 0; cls < 3; ++cls)
                 for (uint32_t i = 0; i < n_jobs; ++i) {
                     const carma_replay_config& c = configs[jobs[i].config];
-                    if (static_cast<int>(heavy_config(c)) != cls) continue;
+                    // > 128 allocation blocks: the shared-memory layouts hold 2 bitmap words
+                    const int jc = c.gpu_capacity / c.alloc_block > 128 ? 2 : static_cast<int>(heavy_config(c));
+                    if (jc != cls) continue;
                     pl->class_list.push_back(i);
                     pl->class_count[cls]++;
                     pl->class_max_g[cls] = std::max(pl->class_max_g[cls], c.gpu_count);

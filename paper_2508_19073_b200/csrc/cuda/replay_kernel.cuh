@@ -53,7 +53,7 @@ constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kWindow = 1u, kCompletion = 2u, kCrash = 3u;
 constexpr int32_t kStatusRetry = -1;      // overflowed this tier
 constexpr int32_t kStatusRedoSmact = -2;  // full-history SMACT needs the true window begin
-constexpr int kWords = 4;                 // bitmap words per GPU: <= 256 blocks
+constexpr int kMaxWords = 4;              // bitmap words per GPU: <= 256 blocks
 
 struct Params {
     const carma_replay_config* cfgs;
@@ -78,14 +78,14 @@ struct Params {
 
 // Compile-time state layout: G GPUs, H heap entries, S slots, RC residents
 // per GPU, RG SMACT ring entries per GPU, RQ recovery-queue entries.
-template <int G_, int H_, int S_, int RC_, int RG_, int RQ_>
+template <int G_, int H_, int S_, int RC_, int RG_, int RQ_, int W_>
 struct Layout {
-    static constexpr int G = G_, H = H_, S = S_, RC = RC_, RG = RG_, RQ = RQ_;
+    static constexpr int G = G_, H = H_, S = S_, RC = RC_, RG = RG_, RQ = RQ_, W = W_;
     static constexpr int GPL = (G + 31) / 32;
     static constexpr size_t al8(size_t x) { return (x + 15) / 16 * 16; }
     static constexpr size_t cfg = 0;                                   // carma_replay_config
     static constexpr size_t used = al8(cfg + sizeof(carma_replay_config));  // u64 [W][G]
-    static constexpr size_t energy = al8(used + 8ull * kWords * G);    // f64 [G] x 9
+    static constexpr size_t energy = al8(used + 8ull * W * G);    // f64 [G] x 9
     static constexpr size_t rate = energy + 8ull * G;
     static constexpr size_t inst = rate + 8ull * G;
     static constexpr size_t power = inst + 8ull * G;
@@ -203,7 +203,7 @@ __device__ __forceinline__ void heap_pop(char* b, Sc& c) {
 // Bit = 1: block used (bits past the device's block count are set).
 template <class L>
 __device__ __forceinline__ int next_bit(const uint64_t* used, int g, int from, int nblk, bool one) {
-    for (int w = from >> 6; w < kWords; ++w) {
+    for (int w = from >> 6; w < L::W; ++w) {
         uint64_t bits = used[w * L::G + g];
         if (!one) bits = ~bits;
         if (w == (from >> 6)) bits &= ~0ull << (from & 63);
@@ -231,7 +231,7 @@ template <class L>
 __device__ __forceinline__ uint32_t free_blocks(const uint64_t* used, int g) {
     uint32_t f = 0;
 #pragma unroll
-    for (int w = 0; w < kWords; ++w) f += __popcll(static_cast<long long>(~used[w * L::G + g]));
+    for (int w = 0; w < L::W; ++w) f += __popcll(static_cast<long long>(~used[w * L::G + g]));
     return f;
 }
 
@@ -374,9 +374,11 @@ __device__ __forceinline__ bool refresh_gpu(char* b, int g, double now, double w
 template <class L>
 __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, int nt, unsigned lane) {
     bool ok = true;
-    if ((t0 & 31) == static_cast<int>(lane)) ok = refresh_gpu<L>(b, t0, c.now, c.window, c.begin0);
-    __syncwarp();
-    if (nt > 1 && (t1 & 31) == static_cast<int>(lane)) ok = refresh_gpu<L>(b, t1, c.now, c.window, c.begin0) && ok;
+#pragma unroll 1
+    for (int k = 0; k < nt; ++k) {
+        const int g = k == 0 ? t0 : t1;
+        if ((g & 31) == static_cast<int>(lane)) ok = refresh_gpu<L>(b, g, c.now, c.window, c.begin0) && ok;
+    }
     if (!__all_sync(0xffffffffu, ok)) {
         c.status = kStatusRetry;
         return;
@@ -631,7 +633,7 @@ __device__ __noinline__ void init_job(char* b, const Params& p, uint32_t j, unsi
     if (0.0 > cf.boost_threshold) p0 = __dadd_rn(p0, cf.p_boost_w);
     for (int g = static_cast<int>(lane); g < L::G; g += 32) {
 #pragma unroll
-        for (int w = 0; w < kWords; ++w) {
+        for (int w = 0; w < L::W; ++w) {
             const int lo = w * 64;
             uint64_t m = ~0ull;
             if (nblk > lo) m = nblk - lo >= 64 ? 0ull : (~0ull << (nblk - lo));
@@ -890,12 +892,15 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
                 t0 = g0;
                 t1 = g1;
                 nt = got;
-            } else {
-                heap_push<L>(b, c, __dadd_rn(c.now, delay), (kCrash << 30) | head);
             }
-            // arm_window (manager.cpp:275-278)
+            // crash (on failure, manager.cpp:251-256) then arm_window
+            // (manager.cpp:275-278): one push site for both.
             c.deadline = __dadd_rn(c.now, c.window);
-            heap_push<L>(b, c, c.deadline, kWindow << 30);
+#pragma unroll 1
+            for (int e = ok ? 1 : 0; e < 2; ++e) {
+                if (e == 0) heap_push<L>(b, c, __dadd_rn(c.now, delay), (kCrash << 30) | head);
+                else heap_push<L>(b, c, c.deadline, kWindow << 30);
+            }
             if (c.status) break;
         }
         if (c.status) break;
