@@ -284,21 +284,21 @@ def run_carma(args, d: Dist):
     for f in (1, 2):
         knn.set_model(cb.fit_knn(f, 4000, MODEL_SEEDS[f], 5))
     log(f"[rank {d.rank}] knn inputs {Q} rows in {time.time() - t0:.1f}s; fp64 probe {fp64.value / 1e12:.2f} TF/s")
+    # 64-byte packed rows (lossless, family inside; include/carma_gpu.h)
+    packed, table = cb.pack_features(rows, fam)
+    abi.check(abi.lib.carma_knn_set_act_table(knn.handle, table.ctypes.data))
     stream = torch.cuda.current_stream()
-    d_rows = torch.from_numpy(rows.view(np.uint8).reshape(-1)).to("cuda")
-    d_fam = torch.from_numpy(fam).to("cuda")
+    d_rows = torch.from_numpy(packed.view(np.uint8).reshape(-1)).to("cuda")
     d_b = torch.empty(Q, dtype=torch.int32, device="cuda")
     d_by = torch.empty(Q, dtype=torch.int64, device="cuda")
 
     def knn_step():
-        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_FEATURES,
-                                                   d_fam.data_ptr(), 1, Q, d_b.data_ptr(), d_by.data_ptr(),
-                                                   None, None, stream.cuda_stream))
+        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_PACKED, None, 1, Q,
+                                                   d_b.data_ptr(), d_by.data_ptr(), None, None, stream.cuda_stream))
 
     for _ in range(args.warmup):
         knn_step()
     torch.cuda.synchronize()
-    launches0, evals = knn.last_stats()
     search_ms, pipe_ms = [], []
     sm, pm = ctypes.c_double(), ctypes.c_double()
     with Clocks(dev) as clk:
@@ -317,28 +317,38 @@ def run_carma(args, d: Dist):
         d.barrier()
     knn_ms = d.max(e0.elapsed_time(e1) / args.steps)
     clocks = clk.summary()
-    # parity spot check on the bench batch itself (outputs identical across steps)
     b_dev = d_b.cpu().numpy()
     launches, evals = knn.last_stats()
     value = N * Q / (knn_ms * 1e-3)
 
-    # e2e: host pinned rows -> carma_knn_predict (chunked H2D / compute / D2H) -> host outputs
-    h_rows = torch.from_numpy(rows.view(np.uint8).reshape(-1)).pin_memory().numpy().view(rows.dtype)
-    h_fam = torch.from_numpy(fam).pin_memory().numpy()
+    # e2e: pinned host packed rows -> carma_knn_predict_packed (chunked H2D /
+    # compute / D2H on two streams) -> pinned host buckets + bytes
+    h_rows = torch.from_numpy(packed.view(np.uint8).reshape(-1)).pin_memory().numpy().view(packed.dtype)
     h_b = torch.empty(Q, dtype=torch.int32).pin_memory().numpy()
     h_by = torch.empty(Q, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+
+    def e2e_step():
+        abi.check(abi.lib.carma_knn_predict_packed(knn.handle, h_rows.ctypes.data, table.ctypes.data, Q,
+                                                   h_b.ctypes.data, h_by.ctypes.data))
+
     for _ in range(max(1, args.warmup - 1)):
-        abi.check(abi.lib.carma_knn_predict(knn.handle, h_rows.ctypes.data, h_fam.ctypes.data, 1, Q,
-                                            h_b.ctypes.data, h_by.ctypes.data))
+        e2e_step()
     d.barrier()
     t = time.perf_counter()
     for _ in range(args.steps):
-        abi.check(abi.lib.carma_knn_predict(knn.handle, h_rows.ctypes.data, h_fam.ctypes.data, 1, Q,
-                                            h_b.ctypes.data, h_by.ctypes.data))
+        e2e_step()
     e2e_s = d.max((time.perf_counter() - t) / args.steps)
     d.barrier()
     assert np.array_equal(h_b, b_dev), "host-API and device-resident predictions differ"
-    del d_rows, d_fam, d_b, d_by
+    # the 136-byte FeatureVector-row host API, once, for reference
+    h_full = torch.from_numpy(rows.view(np.uint8).reshape(-1)).pin_memory().numpy().view(rows.dtype)
+    h_fam = torch.from_numpy(fam).pin_memory().numpy()
+    t = time.perf_counter()
+    abi.check(abi.lib.carma_knn_predict(knn.handle, h_full.ctypes.data, h_fam.ctypes.data, 1, Q,
+                                        h_b.ctypes.data, h_by.ctypes.data))
+    e2e_full_s = time.perf_counter() - t
+    assert np.array_equal(h_b, b_dev)
+    del d_rows, d_b, d_by, h_full, h_fam
 
     search_avg = statistics.mean(search_ms)
     flops_per_launch = evals * FLOPS_PER_EVAL
@@ -372,16 +382,19 @@ def run_carma(args, d: Dist):
         plan.close()
         run_avg = d.max(statistics.mean(run_ms))
         k_avg = statistics.mean(kernel_ms)
-        # e2e through the one-shot host API (upload, run, download every step)
+        # e2e through the plan's host API: every step uploads the tasks from
+        # pinned memory, replays, and reads back per-task outcomes + reports
+        plan = cb.ReplayPlan(cfgs, tasks, offs, jobs, device=dev)
         h_tasks = torch.from_numpy(tasks.view(np.uint8)).pin_memory().numpy().view(tasks.dtype)
-        tr_out = torch.empty(int(n_placed * 64), dtype=torch.uint8).pin_memory().numpy().view(abi.task_result_dtype)
-        j_out = np.zeros(len(jobs), abi.trace_result_dtype)
-        g_out = np.zeros(len(jobs) * 4, abi.gpu_result_dtype)
+        o_t = torch.empty(n_placed * 24, dtype=torch.uint8).pin_memory().numpy().view(abi.task_outcome_dtype)
+        o_j = torch.empty(len(jobs) * 80, dtype=torch.uint8).pin_memory().numpy().view(abi.trace_result_dtype)
+        o_g = torch.empty(len(jobs) * 4 * 32, dtype=torch.uint8).pin_memory().numpy().view(abi.gpu_result_dtype)
 
         def e2e_step():
-            abi.check(abi.lib.carma_replay_batch(dev, cfgs.ctypes.data, len(cfgs), h_tasks.ctypes.data,
-                                                 offs.ctypes.data, len(offs) - 1, jobs.ctypes.data, len(jobs),
-                                                 tr_out.ctypes.data, j_out.ctypes.data, g_out.ctypes.data))
+            abi.check(abi.lib.carma_replay_plan_upload_tasks(plan._h, h_tasks.ctypes.data))
+            abi.check(abi.lib.carma_replay_plan_run(plan._h, None))
+            abi.check(abi.lib.carma_replay_plan_outcomes(plan._h, o_t.ctypes.data, o_j.ctypes.data,
+                                                         o_g.ctypes.data))
 
         e2e_step()
         d.barrier()
@@ -389,7 +402,8 @@ def run_carma(args, d: Dist):
         for _ in range(args.steps):
             e2e_step()
         r_e2e = d.max((time.perf_counter() - t) / args.steps)
-        assert np.array_equal(j_out["energy_mj"], res.traces["energy_mj"])
+        plan.close()
+        assert np.array_equal(o_j["energy_mj"], res.traces["energy_mj"])
         replay = {
             "metric": "trace-replay placed tasks/sec", "unit": "placed tasks/s",
             "value": N * n_placed / (run_avg * 1e-3), "ms_per_step": run_avg,
@@ -398,9 +412,10 @@ def run_carma(args, d: Dist):
                        "jobs_per_gpu": len(jobs), "placed_tasks_per_gpu": n_placed},
             "events_per_s": N * events / (run_avg * 1e-3),
             "e2e": {"value": N * n_placed / r_e2e, "unit": "placed tasks/s",
-                    "h2d_bytes_per_step": int(tasks.nbytes + cfgs.nbytes + offs.nbytes + jobs.nbytes),
-                    "d2h_bytes_per_step": int(tr_out.nbytes + j_out.nbytes + g_out.nbytes)},
-            "gpu_launches": int(launches_r),
+                    "h2d_bytes_per_step": int(h_tasks.nbytes),
+                    "d2h_bytes_per_step": int(o_t.nbytes + o_j.nbytes + o_g.nbytes),
+                    "api": "carma_replay_plan_upload_tasks + run + outcomes (per-task outcomes, reports, per-GPU)"},
+            "gpu_launches": int(launches_r) * args.steps,
             "retried_jobs": int(retried),
             "roofline": {"bound": "hbm", "achieved": ALG_BYTES_PER_TASK * n_placed / (k_avg * 1e-3) / 1e9,
                          "peak": peaks().get("hbm_gbs", 6650.0), "unit": "GB/s",
@@ -432,8 +447,10 @@ def run_carma(args, d: Dist):
         "dtype": "f64", "data": "synthetic (reference generators, seeded)",
         "config": knn_config(N),
         "e2e": {"value": N * Q / e2e_s, "unit": "estimates/s",
-                "h2d_bytes_per_step": int(h_rows.nbytes + h_fam.nbytes),
-                "d2h_bytes_per_step": int(h_b.nbytes + h_by.nbytes)},
+                "h2d_bytes_per_step": int(h_rows.nbytes),
+                "d2h_bytes_per_step": int(h_b.nbytes + h_by.nbytes),
+                "api": "carma_knn_predict_packed (64 B packed rows, pinned host buffers)",
+                "feature_row_api_estimates_per_s": N * Q / e2e_full_s},
         "gpu_launches": int(launches) * args.steps,
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": fp64.value / 1e12, "unit": "TFLOP/s",
                      "frac": achieved / fp64.value, "traffic": traffic,

@@ -75,6 +75,32 @@ typedef struct carma_knn carma_knn;
 /* Row formats accepted by carma_knn_predict_device. */
 #define CARMA_ROWS_FEATURES 0 /* carma_feature_row[q] */
 #define CARMA_ROWS_SCALAR 1   /* double[q][19] raw scalar features */
+#define CARMA_ROWS_PACKED 2   /* carma_feature_packed[q] (+ activation table) */
+
+/* Lossless 64-byte packing of a carma_feature_row plus its family, for bulk
+ * callers (half the PCIe bytes of the 136-byte row). Eight u64 words:
+ *   w0 = total_params      | n_linear   << 48 | n_batchnorm << 56
+ *   w1 = total_activations | n_dropout  << 48 | n_conv      << 56
+ *   w2 = tuple_acts[0]     | (batch & 0xffff) << 48
+ *   w3 = tuple_params[0]   | kind0 << 48 | kind1 << 52 | kind2 << 56
+ *                          | has_layers << 60 | act_code << 61
+ *   w4 = tuple_acts[1]     | family << 48
+ *   w5 = tuple_params[1]   | (batch >> 16) << 48
+ *   w6 = tuple_acts[2]
+ *   w7 = tuple_params[2]
+ * 48-bit counts, 8-bit tallies, 4-bit kinds, 32-bit batch; (act_cos,
+ * act_sin) is entry act_code of an 8-entry table passed with the batch.
+ * carma_pack_features reports CARMA_ERR_UNSUPPORTED for rows that do not
+ * fit; callers then use the 136-byte format. */
+typedef struct carma_feature_packed {
+    uint64_t w[8];
+} carma_feature_packed;
+
+/* Packs n rows (family per row, nullable -> default_family) and builds the
+ * activation table act_table[16] = {cos0, sin0, cos1, sin1, ...}. */
+carma_status carma_pack_features(const carma_feature_row* rows, const int8_t* family,
+                                 int32_t default_family, uint64_t n, double* act_table,
+                                 carma_feature_packed* out);
 
 carma_status carma_knn_create(int device, carma_knn** out);
 carma_status carma_knn_destroy(carma_knn* h);
@@ -96,6 +122,10 @@ carma_status carma_knn_set_model(carma_knn* h, int32_t family, const double* lo,
 carma_status carma_knn_predict(carma_knn* h, const carma_feature_row* rows,
                                const int8_t* family, int32_t default_family, uint64_t q,
                                int32_t* bucket_out, uint64_t* bytes_out);
+/* Same over packed rows; the family of each row is in the packing. */
+carma_status carma_knn_predict_packed(carma_knn* h, const carma_feature_packed* rows,
+                                      const double* act_table, uint64_t q,
+                                      int32_t* bucket_out, uint64_t* bytes_out);
 /* Same over raw 19-feature rows (predict_scalar). */
 carma_status carma_knn_predict_scalar(carma_knn* h, const double* raw, const int8_t* family,
                                       int32_t default_family, uint64_t q,
@@ -108,6 +138,8 @@ carma_status carma_knn_predict_device(carma_knn* h, const void* rows, int32_t fo
                                       const int8_t* family, int32_t default_family,
                                       uint64_t q, int32_t* bucket_out, uint64_t* bytes_out,
                                       double* topk_d2, int64_t* topk_idx, void* stream);
+/* Activation table (host, 16 doubles) used by CARMA_ROWS_PACKED device calls. */
+carma_status carma_knn_set_act_table(carma_knn* h, const double* act_table);
 /* Kernel statistics of the last predict: launches and the number of (query,
  * point) distance evaluations performed. */
 carma_status carma_knn_last_stats(carma_knn* h, uint64_t* launches, uint64_t* evaluations);
@@ -197,7 +229,9 @@ typedef struct carma_replay_job {
 typedef struct carma_replay_plan carma_replay_plan;
 
 /* Uploads configs, tasks (trace t = tasks[trace_offsets[t] .. trace_offsets[t+1]))
- * and jobs to `device`. want_task_results = 0 skips per-task outputs. */
+ * and jobs to `device`. want_task_results is ignored (kept for ABI shape):
+ * per-task results are always produced on the device; what crosses PCIe is
+ * chosen per call in carma_replay_plan_results / carma_replay_batch_mode. */
 carma_status carma_replay_plan_create(int device, const carma_replay_config* configs,
                                       uint32_t n_configs, const carma_task* tasks,
                                       const uint64_t* trace_offsets, uint32_t n_traces,
@@ -206,6 +240,9 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
 /* Overrides every task's estimate with a device array (one u64 per task, same
  * indexing as `tasks`), e.g. the bytes_out of carma_knn_predict_device. */
 carma_status carma_replay_plan_set_estimates_device(carma_replay_plan* p, const uint64_t* est);
+/* Re-uploads the task array (same shape as at creation) from host memory,
+ * e.g. the next sweep's traces; pinned host memory copies asynchronously. */
+carma_status carma_replay_plan_upload_tasks(carma_replay_plan* p, const carma_task* tasks);
 /* Runs all jobs on the device (inputs resident). stream: cudaStream_t or NULL. */
 carma_status carma_replay_plan_run(carma_replay_plan* p, void* stream);
 carma_status carma_replay_plan_results(carma_replay_plan* p, carma_task_result* tasks,
@@ -217,6 +254,18 @@ carma_status carma_replay_plan_stats(carma_replay_plan* p, uint64_t* launches,
  * replay kernel and the whole run including retries (ms). */
 carma_status carma_replay_plan_timing(carma_replay_plan* p, double* kernel_ms, double* run_ms);
 carma_status carma_replay_plan_destroy(carma_replay_plan* p);
+
+/* Per-task outcome in compact form (TaskOutcome, metrics.hpp:29-38 inputs). */
+typedef struct carma_task_outcome {
+    double final_dispatch;
+    double complete;
+    uint32_t ooms;
+    uint32_t attempts;
+} carma_task_outcome; /* 24 bytes */
+
+/* Compact results: per-task outcomes (nullable) + traces + GPUs. */
+carma_status carma_replay_plan_outcomes(carma_replay_plan* p, carma_task_outcome* tasks,
+                                        carma_trace_result* traces, carma_gpu_result* gpus);
 
 /* One-shot host API: create + run + results + destroy (the run_sweep engine). */
 carma_status carma_replay_batch(int device, const carma_replay_config* configs,

@@ -26,7 +26,7 @@ FAMILY = {"mlp": 0, "cnn": 1, "transformer": 2}
 ESTIMATOR = {"none": 0, "oracle": 1, "analytical": 2, "static_graph": 3, "learned": 4}
 MIX = {"t90": 0, "t60": 1}
 NO_ESTIMATE = np.uint64(0xFFFFFFFFFFFFFFFF)
-ROWS_FEATURES, ROWS_SCALAR = 0, 1
+ROWS_FEATURES, ROWS_SCALAR, ROWS_PACKED = 0, 1, 2
 GiB = 1 << 30
 MiB = 1 << 20
 
@@ -35,6 +35,12 @@ feature_row_dtype = np.dtype([
     ("batch_size", "<u8"), ("total_params", "<u8"), ("total_activations", "<u8"),
     ("act_cos", "<f8"), ("act_sin", "<f8"), ("kind", "<i4", (3,)), ("has_layers", "<i4"),
     ("tuple_acts", "<u8", (3,)), ("tuple_params", "<u8", (3,)),
+], align=True)
+
+feature_packed_dtype = np.dtype([("w", "<u8", (8,))])
+
+task_outcome_dtype = np.dtype([
+    ("final_dispatch", "<f8"), ("complete", "<f8"), ("ooms", "<u4"), ("attempts", "<u4"),
 ], align=True)
 
 replay_config_dtype = np.dtype([
@@ -77,6 +83,8 @@ pick_request_dtype = np.dtype([
 ], align=True)
 
 assert feature_row_dtype.itemsize == 136
+assert feature_packed_dtype.itemsize == 64
+assert task_outcome_dtype.itemsize == 24
 assert replay_config_dtype.itemsize == 96
 assert task_dtype.itemsize == 48
 assert task_result_dtype.itemsize == 64
@@ -98,6 +106,11 @@ SIGNATURES = {
     "carma_knn_set_model": (c_int, [c_void_p, c_int32, P, P, P, P, c_uint64, c_uint32, c_uint64]),
     "carma_knn_predict": (c_int, [c_void_p, P, P, c_int32, c_uint64, P, P]),
     "carma_knn_predict_scalar": (c_int, [c_void_p, P, P, c_int32, c_uint64, P, P]),
+    "carma_knn_predict_packed": (c_int, [c_void_p, P, P, c_uint64, P, P]),
+    "carma_knn_set_act_table": (c_int, [c_void_p, P]),
+    "carma_pack_features": (c_int, [P, P, c_int32, c_uint64, P, P]),
+    "carma_replay_plan_upload_tasks": (c_int, [c_void_p, P]),
+    "carma_replay_plan_outcomes": (c_int, [c_void_p, P, P, P]),
     "carma_knn_predict_device": (c_int, [c_void_p, P, c_int32, P, c_int32, c_uint64, P, P, P, P, c_void_p]),
     "carma_knn_last_stats": (c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64)]),
     "carma_knn_last_timing": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),

@@ -150,6 +150,16 @@ def generate_synthetic_dataset(family: int, n: int, seed: int) -> EstimatorDatas
     return EstimatorDataset(rows, b, m, family, seed)
 
 
+def pack_features(rows: np.ndarray, family=None, default_family: int = 0):
+    """64-byte packed rows (family inside) + the 16-double activation table."""
+    rows = np.ascontiguousarray(rows, abi.feature_row_dtype)
+    fam = None if family is None else np.ascontiguousarray(family, np.int8)
+    out = np.zeros(len(rows), abi.feature_packed_dtype)
+    table = np.zeros(16, np.float64)
+    check(lib.carma_pack_features(ptr(rows), ptr(fam), default_family, len(rows), ptr(table), ptr(out)))
+    return out, table
+
+
 def scalar_features(rows: np.ndarray) -> np.ndarray:
     out = np.zeros((len(rows), 19), np.float64)
     rows = np.ascontiguousarray(rows)
@@ -226,6 +236,14 @@ class GpuKnn:
         else:
             rows = np.ascontiguousarray(rows, np.float64)
             check(lib.carma_knn_predict_scalar(self._h, ptr(rows), ptr(fam), dflt, q, ptr(bucket), ptr(nbytes)))
+        return bucket, nbytes
+
+    def predict_packed(self, packed: np.ndarray, table: np.ndarray):
+        q = len(packed)
+        bucket = np.zeros(q, np.int32)
+        nbytes = np.zeros(q, np.uint64)
+        check(lib.carma_knn_predict_packed(self._h, ptr(np.ascontiguousarray(packed)), ptr(table), q, ptr(bucket),
+                                           ptr(nbytes)))
         return bucket, nbytes
 
     def last_stats(self):
@@ -381,6 +399,17 @@ class ReplayPlan:
 
     def run(self, stream: int = 0) -> None:
         check(lib.carma_replay_plan_run(self._h, stream or None))
+
+    def upload_tasks(self, tasks: np.ndarray) -> None:
+        check(lib.carma_replay_plan_upload_tasks(self._h, ptr(np.ascontiguousarray(tasks, abi.task_dtype))))
+
+    def outcomes(self):
+        """Compact per-task outcomes + trace reports + per-GPU results."""
+        to = np.zeros(int(self.task_offsets[-1]), abi.task_outcome_dtype)
+        jr = np.zeros(len(self.jobs), abi.trace_result_dtype)
+        gr = np.zeros(int(self.gpu_offsets[-1]), abi.gpu_result_dtype)
+        check(lib.carma_replay_plan_outcomes(self._h, ptr(to), ptr(jr), ptr(gr)))
+        return to, jr, gr
 
     def results(self, tasks: bool = True) -> ReplayResult:
         tr = np.zeros(int(self.task_offsets[-1]) if tasks else 0, abi.task_result_dtype)

@@ -67,6 +67,7 @@ struct ModelDev {
 
 struct KnnParams {
     ModelDev m[CARMA_FAMILIES];
+    double act[16];  // packed rows: (cos, sin) per activation code
     const void* rows;
     int32_t format;
     const int8_t* family;
@@ -97,8 +98,39 @@ __device__ __forceinline__ void featurize(const carma_feature_row& r, double* ra
     raw[18] = __dadd_rn(__dmul_rn(16.0, raw[5]), __dmul_rn(__dmul_rn(4.0, raw[4]), raw[6]));
 }
 
+constexpr uint64_t kLow48 = (1ull << 48) - 1ull;
+
+// Unpacks a carma_feature_packed row (layout in carma_gpu.h).
+__device__ __forceinline__ void featurize_packed(const KnnParams& p, const carma_feature_packed& r, double* raw) {
+    const uint64_t w0 = r.w[0], w1 = r.w[1], w2 = r.w[2], w3 = r.w[3], w5 = r.w[5];
+    raw[0] = u2d((w0 >> 48) & 0xff);
+    raw[1] = u2d(w0 >> 56);
+    raw[2] = u2d((w1 >> 48) & 0xff);
+    raw[3] = u2d(w1 >> 56);
+    raw[4] = u2d((w2 >> 48) | ((w5 >> 48) << 16));
+    raw[5] = u2d(w0 & kLow48);
+    raw[6] = u2d(w1 & kLow48);
+    const int code = static_cast<int>(w3 >> 61);
+    raw[7] = p.act[2 * code];
+    raw[8] = p.act[2 * code + 1];
+    const bool h = (w3 >> 60) & 1ull;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        raw[9 + 3 * k] = h ? static_cast<double>((w3 >> (48 + 4 * k)) & 0xf) : 0.0;
+        raw[10 + 3 * k] = h ? u2d(r.w[2 + 2 * k] & kLow48) : 0.0;
+        raw[11 + 3 * k] = h ? u2d(r.w[3 + 2 * k] & kLow48) : 0.0;
+    }
+    raw[18] = __dadd_rn(__dmul_rn(16.0, raw[5]), __dmul_rn(__dmul_rn(4.0, raw[4]), raw[6]));
+}
+
 __device__ __forceinline__ double raw18_of(const KnnParams& p, uint64_t i) {
     if (p.format == CARMA_ROWS_SCALAR) return static_cast<const double*>(p.rows)[i * kDims + 18];
+    if (p.format == CARMA_ROWS_PACKED) {
+        const carma_feature_packed* r = static_cast<const carma_feature_packed*>(p.rows) + i;
+        const uint64_t w0 = r->w[0], w1 = r->w[1], w2 = r->w[2], w5 = r->w[5];
+        const double batch = u2d((w2 >> 48) | ((w5 >> 48) << 16));
+        return __dadd_rn(__dmul_rn(16.0, u2d(w0 & kLow48)), __dmul_rn(__dmul_rn(4.0, batch), u2d(w1 & kLow48)));
+    }
     const carma_feature_row& r = static_cast<const carma_feature_row*>(p.rows)[i];
     return __dadd_rn(__dmul_rn(16.0, u2d(r.total_params)),
                      __dmul_rn(__dmul_rn(4.0, u2d(r.batch_size)), u2d(r.total_activations)));
@@ -109,7 +141,9 @@ __device__ __forceinline__ double normalize(double raw, double lo, double hi) {
 }
 
 __device__ __forceinline__ int family_of(const KnnParams& p, uint64_t i) {
-    const int f = p.family ? static_cast<int>(p.family[i]) : p.default_family;
+    const int f = p.format == CARMA_ROWS_PACKED
+                      ? static_cast<int>((static_cast<const carma_feature_packed*>(p.rows)[i].w[4] >> 48) & 0xff)
+                      : (p.family ? static_cast<int>(p.family[i]) : p.default_family);
     return (f >= 0 && f < CARMA_FAMILIES && p.m[f].present) ? f : -1;
 }
 
@@ -289,6 +323,8 @@ __global__ void __launch_bounds__(128, 4)
                     const double* r = static_cast<const double*>(p.rows) + static_cast<uint64_t>(row) * kDims;
 #pragma unroll
                     for (int d = 0; d < kDims; ++d) raw[d] = r[d];
+                } else if (p.format == CARMA_ROWS_PACKED) {
+                    featurize_packed(p, static_cast<const carma_feature_packed*>(p.rows)[row], raw);
                 } else {
                     featurize(static_cast<const carma_feature_row*>(p.rows)[row], raw);
                 }
@@ -456,6 +492,7 @@ struct KnnHandle {
         PinnedBuffer stage_rows, stage_family;
     } scratch[2];
     DeviceBuffer evals;
+    double act[16] = {0};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // pipeline start, search start, search end
     bool timed = false;
     uint64_t last_launches = 0, last_evals = 0;
@@ -466,6 +503,7 @@ namespace {
 
 KnnParams make_params(const KnnHandle& h, uint32_t* n_bins) {
     KnnParams p{};
+    std::memcpy(p.act, h.act, sizeof(p.act));
     uint32_t base = 0;
     for (int f = 0; f < CARMA_FAMILIES; ++f) {
         const HostModel& hm = h.model[f];
@@ -741,6 +779,22 @@ carma_status carma_knn_predict(carma_knn* h, const carma_feature_row* rows, cons
                         q, bucket_out, bytes_out);
 }
 
+carma_status carma_knn_set_act_table(carma_knn* hh, const double* act_table) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        if (!h || !act_table) throw InvalidArg("null argument");
+        std::memcpy(h->act, act_table, sizeof(h->act));
+    });
+}
+
+carma_status carma_knn_predict_packed(carma_knn* hh, const carma_feature_packed* rows, const double* act_table,
+                                      uint64_t q, int32_t* bucket_out, uint64_t* bytes_out) {
+    KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+    if (h && act_table) std::memcpy(h->act, act_table, sizeof(h->act));
+    return predict_host(hh, rows, sizeof(carma_feature_packed), CARMA_ROWS_PACKED, nullptr, 0, q, bucket_out,
+                        bytes_out);
+}
+
 carma_status carma_knn_predict_scalar(carma_knn* h, const double* raw, const int8_t* family,
                                       int32_t default_family, uint64_t q, int32_t* bucket_out,
                                       uint64_t* bytes_out) {
@@ -755,7 +809,8 @@ carma_status carma_knn_predict_device(carma_knn* hh, const void* rows, int32_t f
     return guarded([&] {
         KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
         check_ready(h);
-        if (format != CARMA_ROWS_FEATURES && format != CARMA_ROWS_SCALAR) throw InvalidArg("unknown row format");
+        if (format != CARMA_ROWS_FEATURES && format != CARMA_ROWS_SCALAR && format != CARMA_ROWS_PACKED)
+            throw InvalidArg("unknown row format");
         if (q == 0) return;
         if (!rows) throw InvalidArg("rows is null");
         std::lock_guard<std::mutex> lock(h->mu);

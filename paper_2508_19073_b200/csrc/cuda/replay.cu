@@ -63,6 +63,20 @@ __global__ void pick_kernel(carma_replay_config cf, const carma_gpu_view* __rest
     }
 }
 
+__global__ void compact_outcomes(const carma_task_result* __restrict__ in, uint64_t n,
+                                 carma_task_outcome* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const carma_task_result r = in[i];
+        carma_task_outcome o;
+        o.final_dispatch = r.final_dispatch;
+        o.complete = r.complete;
+        o.ooms = r.ooms;
+        o.attempts = r.attempts;
+        out[i] = o;
+    }
+}
+
 }  // namespace
 
 // --------------------------------------------------------------- host side
@@ -78,7 +92,7 @@ struct ReplayPlan {
     int class_max_g[3] = {1, 1, 1};
     std::vector<uint32_t> class_list;  // jobs ordered: light, heavy, global-only
     DeviceBuffer d_cfgs, d_tasks, d_trace_off, d_jobs, d_task_off, d_gpu_off, d_list, d_task_out,
-        d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate;
+        d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate, d_outcomes;
     const uint64_t* est_override = nullptr;
     uint64_t launches = 0, retried = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // run start, shared-memory tiers end, run end
@@ -345,6 +359,43 @@ carma_status carma_replay_plan_run(carma_replay_plan* hp, void* stream) {
     });
 }
 
+carma_status carma_replay_plan_upload_tasks(carma_replay_plan* hp, const carma_task* tasks) {
+    return guarded([&] {
+        auto* pl = reinterpret_cast<ReplayPlan*>(hp);
+        if (!pl || !tasks) throw InvalidArg("null argument");
+        std::lock_guard<std::mutex> lock(pl->mu);
+        DeviceGuard guard(pl->device);
+        CARMA_CUDA(cudaMemcpyAsync(pl->d_tasks.ptr, tasks, pl->n_tasks * sizeof(carma_task), cudaMemcpyHostToDevice,
+                                   pl->stream));
+        if (!is_pinned(tasks)) CARMA_CUDA(cudaStreamSynchronize(pl->stream));
+    });
+}
+
+carma_status carma_replay_plan_outcomes(carma_replay_plan* hp, carma_task_outcome* tasks,
+                                        carma_trace_result* traces, carma_gpu_result* gpus) {
+    return guarded([&] {
+        auto* pl = reinterpret_cast<ReplayPlan*>(hp);
+        if (!pl) throw InvalidArg("null plan");
+        std::lock_guard<std::mutex> lock(pl->mu);
+        DeviceGuard guard(pl->device);
+        if (tasks) {
+            pl->d_outcomes.ensure(pl->n_task_out * sizeof(carma_task_outcome));
+            compact_outcomes<<<grid_for(pl->n_task_out, 256, 148u * 16u), 256, 0, pl->stream>>>(
+                pl->d_task_out.as<carma_task_result>(), pl->n_task_out, pl->d_outcomes.as<carma_task_outcome>());
+            CARMA_CUDA(cudaGetLastError());
+            CARMA_CUDA(cudaMemcpyAsync(tasks, pl->d_outcomes.ptr, pl->n_task_out * sizeof(carma_task_outcome),
+                                       cudaMemcpyDeviceToHost, pl->stream));
+        }
+        if (traces)
+            CARMA_CUDA(cudaMemcpyAsync(traces, pl->d_trace_out.ptr, pl->jobs.size() * sizeof(carma_trace_result),
+                                       cudaMemcpyDeviceToHost, pl->stream));
+        if (gpus)
+            CARMA_CUDA(cudaMemcpyAsync(gpus, pl->d_gpu_out.ptr, pl->n_gpu_out * sizeof(carma_gpu_result),
+                                       cudaMemcpyDeviceToHost, pl->stream));
+        CARMA_CUDA(cudaStreamSynchronize(pl->stream));
+    });
+}
+
 carma_status carma_replay_plan_results(carma_replay_plan* hp, carma_task_result* tasks,
                                        carma_trace_result* traces, carma_gpu_result* gpus) {
     return guarded([&] {
@@ -397,7 +448,7 @@ carma_status carma_replay_plan_destroy(carma_replay_plan* hp) {
             cudaStreamSynchronize(pl->stream);
             DeviceBuffer* bufs[] = {&pl->d_cfgs, &pl->d_tasks, &pl->d_trace_off, &pl->d_jobs, &pl->d_task_off,
                                     &pl->d_gpu_off, &pl->d_list, &pl->d_task_out, &pl->d_trace_out, &pl->d_gpu_out,
-                                    &pl->d_inv, &pl->d_begin, &pl->d_counters, &pl->d_gstate};
+                                    &pl->d_inv, &pl->d_begin, &pl->d_counters, &pl->d_gstate, &pl->d_outcomes};
             for (auto* b : bufs) b->release();
             for (auto& e : pl->ev)
                 if (e) cudaEventDestroy(e);

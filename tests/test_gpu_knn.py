@@ -141,3 +141,35 @@ def test_knn_large_batch_subsample_parity(gpu, olib, models):
     sel = np.random.default_rng(0).choice(50_000, 3000, replace=False)
     ob, _, _, _ = oracle_predict(olib, models[2], cb.scalar_features(ds.rows[sel]))
     assert np.array_equal(b1[sel], ob)
+
+
+def test_packed_rows_match_oracle(gpu, olib, models):
+    """The 64-byte packed format (host + device paths) gives identical results."""
+    rows, fams, want = [], [], []
+    for f, _, qs in FAMILIES:
+        ds = cb.generate_synthetic_dataset(f, 1500, qs + 7)
+        rows.append(ds.rows)
+        fams.append(np.full(1500, f, np.int8))
+        want.append(oracle_predict(olib, models[f], cb.scalar_features(ds.rows))[0])
+    rows, fams, want = np.concatenate(rows), np.concatenate(fams), np.concatenate(want)
+    knn = cb.GpuKnn(gpu)
+    for f in models:
+        knn.set_model(models[f])
+    packed, table = cb.pack_features(rows, fams)
+    b, by = knn.predict_packed(packed, table)
+    assert np.array_equal(b, want)
+    abi.check(abi.lib.carma_knn_set_act_table(knn.handle, table.ctypes.data))
+    gb, _, _, _ = _device_predict(knn, packed, k=5, fmt=abi.ROWS_PACKED)
+    assert np.array_equal(gb, want)
+
+
+@pytest.mark.parametrize("family", [0, 1, 2])
+def test_gpu_knn_matches_reference_golden(gpu, family):
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "knn.npz"))
+    fam, mseed, qseed, n = (int(x) for x in g["cases"][family])
+    knn = cb.GpuKnn(gpu)
+    knn.set_model(cb.fit_knn(fam, 4000, mseed, 5))
+    ds = cb.generate_synthetic_dataset(fam, n, qseed)
+    b, by = knn.predict(ds.rows, default_family=fam)
+    assert np.array_equal(b, g[f"bucket_{family}"]) and np.array_equal(by, g[f"bytes_{family}"])

@@ -156,3 +156,44 @@ def test_pick_batch_matches_oracle(gpu, olib):
                                      oc.ctypes.data, oo.ctypes.data)
                     assert out[i].tolist() == oo.tolist(), (g, policy, i)
                     assert cur[i] == oc[0]
+
+
+def test_gpu_replay_matches_reference_golden(gpu, olib):
+    """All 60 golden reference runs (tests/golden/replay.npz) in one batch; learned
+    estimates come from the GPU k-NN (GPUMemNet stage feeding stage 2)."""
+    import os
+
+    from cases import assert_matches_ref, case_inputs
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "replay.npz"))
+    knn = cb.GpuKnn(gpu)
+    cfgs, lists = [], []
+    for case in g["cases"]:
+        cfg, tasks = case_inputs(olib, str(case), knn=knn)
+        cfgs.append(cfg)
+        lists.append(tasks)
+    jobs = [(i, i) for i in range(len(lists))]
+    res = cb.replay(np.concatenate(cfgs), lists, jobs)
+    for i in range(len(lists)):
+        assert_matches_ref(g, i, res.job_tasks(i), res.traces[i], res.job_gpus(i))
+
+
+def test_plan_upload_and_outcomes(gpu, olib):
+    """Re-uploading a different task set into a plan and the compact outcome path."""
+    a = [cb.materialize_trace(cb.generate_trace("t90", s)).tasks for s in (1, 2)]
+    b = [cb.materialize_trace(cb.generate_trace("t90", s)).tasks for s in (3, 4)]
+    cfg = cfg_of("magm")
+    offs = np.array([0, 90, 180], np.uint64)
+    jobs = np.zeros(2, abi.job_dtype)
+    jobs["trace"] = [0, 1]
+    plan = cb.ReplayPlan(cfg, np.concatenate(a), offs, jobs)
+    plan.run()
+    plan.upload_tasks(np.concatenate(b))
+    plan.run()
+    to, jr, gr = plan.outcomes()
+    for j in range(2):
+        rc, ot, otr, og = oracle_replay(olib, cfg, b[j])
+        sl = slice(90 * j, 90 * (j + 1))
+        assert np.array_equal(to["complete"][sl], ot["complete"])
+        assert np.array_equal(to["final_dispatch"][sl], ot["final_dispatch"])
+        assert np.array_equal(to["ooms"][sl], ot["ooms"]) and np.array_equal(to["attempts"][sl], ot["attempts"])
+        assert jr[j].tobytes() == np.array([otr]).tobytes()

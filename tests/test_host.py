@@ -1,0 +1,131 @@
+"""CPU tests of the host side: the C-ABI library loads and exports every
+declared symbol, compute entry points fail loudly without a GPU, and the
+host provisioning (traces, datasets, features, packing) behaves."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2508_19073_b200 as cb
+from paper_2508_19073_b200 import abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = []
+    for h in ("carma_gpu.h", "carma_host.h"):
+        text = open(os.path.join(ROOT, "include", h)).read()
+        names += re.findall(r"^(?:carma_status|int|const char\*)\s+(carma_\w+)\(", text, re.M)
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_symbols()
+    assert len(names) >= 30
+    lib = ctypes.CDLL(abi.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) <= set(abi.SIGNATURES), set(names) - set(abi.SIGNATURES)
+
+
+def test_no_gpu_fails_loudly():
+    if abi.lib.carma_device_count() > 0:
+        pytest.skip("a GPU is present")
+    h = ctypes.c_void_p()
+    st = abi.lib.carma_knn_create(0, ctypes.byref(h))
+    assert st == 2  # CARMA_ERR_CUDA: no CPU fallback
+    assert b"no CPU fallback" in abi.lib.carma_last_error()
+
+
+def test_catalog_and_trace_shapes():
+    cat = cb.builtin_catalog()
+    assert len(cat) == 35
+    assert sum(1 for e in cat if e.gpus == 2) == 3
+    t90 = cb.generate_trace("t90", 1)
+    t60 = cb.generate_trace("t60", 1)
+    assert len(t90) == 90 and len(t60) == 60
+    assert np.all(np.diff(t90.submit) >= 0) and t90.submit[0] == 0.0
+    m = cb.materialize_trace(t90)
+    assert sorted(m.tasks["rank"].tolist()) == list(range(90))
+    assert np.array_equal(m.tasks["rank"], np.arange(90))  # 3-digit ids sort in index order
+
+
+def test_rank_is_lexicographic_beyond_999(tmp_path):
+    tr = cb.generate_uniform_trace(1200, 3.0, 7)
+    m = cb.materialize_trace(tr)
+    cat = cb.builtin_catalog()
+    ids = ["t%03d-%s" % (i, cat[e].key) for i, e in enumerate(tr.entry)]
+    want = np.empty(len(ids), np.uint32)
+    want[np.argsort(ids, kind="stable")] = np.arange(len(ids))
+    assert np.array_equal(m.tasks["rank"], want)
+
+
+def test_trace_file_round_trip(tmp_path):
+    tr = cb.generate_trace("t60", 3)
+    p = str(tmp_path / "t.trace")
+    cb.save_trace(tr, p)
+    back = cb.load_trace(p)
+    assert np.array_equal(back.submit, tr.submit)
+    assert np.array_equal(back.entry, tr.entry) and np.array_equal(back.epochs, tr.epochs)
+    assert open(p).readline().startswith("#carma-trace v1 seed=3 mix=t60")
+    bad = tmp_path / "bad.trace"
+    bad.write_text("#carma-trace v1\n5.0,resnet18_cifar100_bs32,20\n1.0,resnet18_cifar100_bs32,20\n")
+    with pytest.raises(abi.CarmaError):
+        cb.load_trace(str(bad))
+
+
+def unpack(packed, table):
+    w = packed["w"].astype(np.uint64)
+    m48 = np.uint64((1 << 48) - 1)
+    s = np.zeros((len(w), 19))
+    s[:, 0] = (w[:, 0] >> np.uint64(48)) & np.uint64(0xff)
+    s[:, 1] = w[:, 0] >> np.uint64(56)
+    s[:, 2] = (w[:, 1] >> np.uint64(48)) & np.uint64(0xff)
+    s[:, 3] = w[:, 1] >> np.uint64(56)
+    batch = (w[:, 2] >> np.uint64(48)) | ((w[:, 5] >> np.uint64(48)) << np.uint64(16))
+    s[:, 4] = batch
+    s[:, 5] = w[:, 0] & m48
+    s[:, 6] = w[:, 1] & m48
+    code = (w[:, 3] >> np.uint64(61)).astype(np.int64)
+    s[:, 7] = table[2 * code]
+    s[:, 8] = table[2 * code + 1]
+    for k in range(3):
+        s[:, 9 + 3 * k] = (w[:, 3] >> np.uint64(48 + 4 * k)) & np.uint64(0xf)
+        s[:, 10 + 3 * k] = w[:, 2 + 2 * k] & m48
+        s[:, 11 + 3 * k] = w[:, 3 + 2 * k] & m48
+    s[:, 18] = 16.0 * s[:, 5] + (4.0 * s[:, 4]) * s[:, 6]
+    fam = ((w[:, 4] >> np.uint64(48)) & np.uint64(0xff)).astype(np.int8)
+    return s, fam
+
+
+@pytest.mark.parametrize("family", [0, 1, 2])
+def test_packed_format_is_lossless(family):
+    ds = cb.generate_synthetic_dataset(family, 3000, 9)
+    packed, table = cb.pack_features(ds.rows, default_family=family)
+    s, fam = unpack(packed, table)
+    want = cb.scalar_features(ds.rows)
+    assert np.array_equal(s.view(np.uint64), want.view(np.uint64))
+    assert np.all(fam == family)
+
+
+def test_packed_format_rejects_out_of_range_rows():
+    ds = cb.generate_synthetic_dataset(0, 4, 9)
+    rows = ds.rows.copy()
+    rows["total_params"][2] = 1 << 50
+    with pytest.raises(abi.CarmaError) as e:
+        cb.pack_features(rows, default_family=0)
+    assert e.value.status == 5
+
+
+def test_fit_shapes_and_holdout_split():
+    m = cb.fit_knn(0, 4000, 11, 5)
+    assert len(m.labels) == 2800 and len(m.holdout_rows) == 1200
+    assert m.points.shape == (2800, 19)
+    lo, hi = m.lo, m.hi
+    active = hi > lo
+    assert np.all(m.points[:, active] >= 0.0) and np.all(m.points[:, active] <= 1.0)
+    assert np.all(m.points[:, ~active] == 0.0)
+    assert m.bucket_range == 1 << 30

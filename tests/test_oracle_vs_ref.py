@@ -1,0 +1,126 @@
+"""Pins the oracle restatement and the product's host provisioning to the
+compiled reference (oracle/_ref) on fresh seeds. Skips where the reference
+library is not built."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2508_19073_b200 as cb
+from paper_2508_19073_b200 import abi
+from cases import model
+from oracle_bind import oracle_predict, oracle_replay, ref_config, ref_run, replay_config_from
+
+
+@pytest.mark.parametrize("family,seed", [(0, 11), (1, 112), (2, 213), (1, 7)])
+def test_fit_matches_reference_train(ref, family, seed):
+    lo, hi = np.zeros(19), np.zeros(19)
+    pts, lab = np.zeros((4000, 19)), np.zeros(4000, np.int32)
+    n, br, h = ctypes.c_uint64(), ctypes.c_uint64(), np.zeros(3)
+    assert ref.ref_train(family, 4000, seed, 5, b"/tmp/carma_ref_model.json", lo.ctypes.data, hi.ctypes.data,
+                         pts.ctypes.data, lab.ctypes.data, 4000, ctypes.byref(n), ctypes.byref(br),
+                         h.ctypes.data) == 0
+    m = cb.fit_knn(family, 4000, seed, 5)
+    assert np.array_equal(m.lo, lo) and np.array_equal(m.hi, hi)
+    assert np.array_equal(m.points, pts[: n.value]) and np.array_equal(m.labels, lab[: n.value])
+    assert m.bucket_range == br.value
+
+
+@pytest.mark.parametrize("family,seed", [(0, 3), (1, 5), (2, 8)])
+def test_dataset_and_predict_match_reference(ref, olib, family, seed):
+    n = 1500
+    f, b, mm = np.zeros((n, 19)), np.zeros(n, np.int32), np.zeros(n, np.uint64)
+    assert ref.ref_dataset(family, n, seed, f.ctypes.data, b.ctypes.data, mm.ctypes.data) == 0
+    ds = cb.generate_synthetic_dataset(family, n, seed)
+    raw = cb.scalar_features(ds.rows)
+    assert np.array_equal(raw.view(np.uint64), f.view(np.uint64))
+    assert np.array_equal(ds.bucket, b) and np.array_equal(ds.mem, mm)
+    pb, pby = np.zeros(n, np.int32), np.zeros(n, np.uint64)
+    mseed = 11 + 101 * family
+    assert ref.ref_predict_dataset(family, 4000, mseed, 5, n, seed, pb.ctypes.data, pby.ctypes.data) == 0
+    ob, oby, _, _ = oracle_predict(olib, model(family, 4000, mseed), raw)
+    assert np.array_equal(ob, pb) and np.array_equal(oby, pby)
+
+
+def test_traces_and_materialize_match_reference(ref, tmp_path):
+    for mix in (0, 1):
+        for seed in (1, 17, 99):
+            sub, ent, ep = np.zeros(128), np.zeros(128, np.int32), np.zeros(128, np.uint64)
+            n = ctypes.c_uint64()
+            assert ref.ref_gen_trace(mix, seed, sub.ctypes.data, ent.ctypes.data, ep.ctypes.data, 128,
+                                     ctypes.byref(n)) == 0
+            tr = cb.generate_trace("t90" if mix == 0 else "t60", seed)
+            k = n.value
+            assert np.array_equal(tr.submit, sub[:k]) and np.array_equal(tr.entry, ent[:k])
+            assert np.array_equal(tr.epochs, ep[:k])
+    tr = cb.generate_uniform_trace(1500, 3.0, 7)
+    path = str(tmp_path / "u.trace")
+    cb.save_trace(tr, path)
+    cap = 2000
+    arrs = dict(submit=np.zeros(cap), true_mem=np.zeros(cap, np.uint64), work=np.zeros(cap),
+                demand=np.zeros(cap), gpus=np.zeros(cap, np.uint64), family=np.zeros(cap, np.int32),
+                batch=np.zeros(cap, np.uint64), feats=np.zeros((cap, 19)))
+    n = ctypes.c_uint64()
+    assert ref.ref_materialize(path.encode(), cap, *[a.ctypes.data for a in arrs.values()], None, 0,
+                               ctypes.byref(n)) == 0
+    m = cb.materialize_trace(tr)
+    k = n.value
+    assert k == 1500
+    for f in ("submit", "true_mem", "work", "demand", "gpus"):
+        assert np.array_equal(m.tasks[f], arrs[f][:k].astype(m.tasks[f].dtype)), f
+    assert np.array_equal(m.family, arrs["family"][:k].astype(np.int8))
+    assert np.array_equal(cb.scalar_features(m.features).view(np.uint64), arrs["feats"][:k].view(np.uint64))
+
+
+GRID = [dict(policy=p) for p in ("exclusive", "rr", "magm", "lug", "mug")] + [
+    dict(policy="rr", rr_pre=True, estimator="oracle"),
+    dict(policy="magm", estimator="analytical"),
+    dict(policy="magm", estimator="static_graph"),
+    dict(policy="magm", mode="streams", max_smact=1.0),
+    dict(policy="lug", gpu_count=8, window=5.0),
+    dict(policy="magm", gpu_count=2, window=5.0, min_free=3 << 30),
+]
+
+
+@pytest.mark.parametrize("kw", GRID, ids=[str(i) for i in range(len(GRID))])
+def test_oracle_replay_matches_reference(ref, olib, kw):
+    for mix in ("t90", "t60"):
+        for seed in (11, 12):
+            cfg = ref_config(**kw)
+            tout, rout, ge, gs, gp = ref_run(ref, cfg, mix=mix, seed=seed)
+            m = cb.materialize_trace(cb.generate_trace(mix, seed))
+            cb.set_persona_estimates(m, kw.get("estimator", "none"))
+            rc, ot, otr, og = oracle_replay(olib, replay_config_from(cfg), m.tasks)
+            assert rc == 0
+            for a, b in (("final_dispatch", "final_dispatch"), ("complete", "complete"), ("ooms", "ooms"),
+                         ("executed", "executed"), ("first_attempt", "first_attempt"),
+                         ("last_crash", "last_crash"), ("attempts", "n_attempts")):
+                assert np.array_equal(ot[a], tout[b]), (kw, mix, seed, a)
+            assert np.array_equal(ot["gpu"][:, 0], tout["gpu0"]) and np.array_equal(ot["gpu"][:, 1], tout["gpu1"])
+            for f in ("avg_wait", "avg_exec", "avg_jct", "energy_mj", "trace_total_time"):
+                assert otr[f] == rout[f], (kw, mix, seed, f)
+            assert np.array_equal(og["energy_j"], ge) and np.array_equal(og["mean_smact"], gs)
+            assert np.array_equal(og["peak_used"], gp)
+
+
+def test_oracle_large_trace_matches_reference(ref, olib, tmp_path):
+    """2000 uniform-catalog tasks on 64 GPUs, W = 5 s, learned estimates, loaded
+    from a #carma-trace v1 file (ids past t999: lexicographic order matters)."""
+    tr = cb.generate_uniform_trace(2000, 3.0, 7)
+    path = str(tmp_path / "big.trace")
+    cb.save_trace(tr, path)
+    cfg = ref_config(policy="magm", estimator="learned", gpu_count=64, window=5.0)
+    tout, rout, ge, gs, gp = ref_run(ref, cfg, path=path)
+    m = cb.materialize_trace(cb.load_trace(path))
+    raw = cb.scalar_features(m.features)
+    e = np.zeros(len(m.tasks), np.uint64)
+    for f in set(m.family.tolist()):
+        sel = m.family == f
+        e[sel] = oracle_predict(olib, model(f), raw[sel])[1]
+    m.tasks["estimate"] = e
+    rc, ot, otr, og = oracle_replay(olib, replay_config_from(cfg), m.tasks)
+    assert rc == 0
+    assert np.array_equal(ot["complete"], tout["complete"]) and np.array_equal(ot["ooms"], tout["ooms"])
+    assert np.array_equal(ot["gpu"][:, 0], tout["gpu0"])
+    assert otr["energy_mj"] == rout["energy_mj"] and otr["avg_jct"] == rout["avg_jct"]
+    assert np.array_equal(og["mean_smact"], gs)
