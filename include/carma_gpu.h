@@ -140,9 +140,16 @@ carma_status carma_knn_predict_device(carma_knn* h, const void* rows, int32_t fo
                                       double* topk_d2, int64_t* topk_idx, void* stream);
 /* Activation table (host, 16 doubles) used by CARMA_ROWS_PACKED device calls. */
 carma_status carma_knn_set_act_table(carma_knn* h, const double* act_table);
-/* Kernel statistics of the last predict: launches and the number of (query,
- * point) distance evaluations performed. */
+/* Kernel statistics of the last predict: launches and the number of exact
+ * fp64 (query, point) distance evaluations performed. */
 carma_status carma_knn_last_stats(carma_knn* h, uint64_t* launches, uint64_t* evaluations);
+/* Same, plus the fp32 pre-filter evaluations (0 on the exact-only path). */
+carma_status carma_knn_last_work(carma_knn* h, uint64_t* launches, uint64_t* fp64_evals,
+                                 uint64_t* fp32_evals);
+/* Search path: 0 auto (fp32 pre-filter whenever every installed model has
+ * <= 16 active dims), 1 exact fp64 blocks only, 2 fp32 pre-filter. Both
+ * paths return identical, exact results. */
+carma_status carma_knn_set_path(carma_knn* h, int32_t path);
 /* CUDA-event timing of the last carma_knn_predict_device on its stream:
  * the knn_search kernel alone and the whole 4-kernel pipeline (ms). */
 carma_status carma_knn_last_timing(carma_knn* h, double* search_ms, double* pipeline_ms);

@@ -113,6 +113,8 @@ SIGNATURES = {
     "carma_replay_plan_outcomes": (c_int, [c_void_p, P, P, P]),
     "carma_knn_predict_device": (c_int, [c_void_p, P, c_int32, P, c_int32, c_uint64, P, P, P, P, c_void_p]),
     "carma_knn_last_stats": (c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64)]),
+    "carma_knn_last_work": (c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64), POINTER(c_uint64)]),
+    "carma_knn_set_path": (c_int, [c_void_p, c_int32]),
     "carma_knn_last_timing": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "carma_replay_plan_timing": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "carma_probe_fp64": (c_int, [c_int, POINTER(c_double)]),

@@ -24,7 +24,7 @@
 //
 // Pipeline per batch (all on one stream):
 //   knn_keys     featurise dim 18, normalise, binary-search -> (bin, pos); CTA histograms
-//   scan_matrix  exclusive scan of the [bin][cta] histogram matrix
+//   bin_totals / scan_bins / bin_offsets  exclusive scan of the [bin][cta] histogram
 //   knn_scatter  counting-sort scatter of row ids into bin order
 //   knn_search   warp-per-32-queries frontier search + fused vote/bucket/bytes epilogue
 
@@ -48,6 +48,8 @@ constexpr uint32_t kInvalidBin = 0xffffffffu;
 constexpr int kScatterCtas = 296;  // 2 per SM on a 148-SM B200
 constexpr int kMaxBins = 4096;
 constexpr int kBlock = 8;  // points per frontier step
+constexpr int kF32Dims = 16;  // fp32 pre-filter: active dims per point
+constexpr int kCandCap = 16;  // fp32 pre-filter: candidate buffer per lane
 
 struct ModelDev {
     const double* pts;    // N x 20, sorted by (p18, original index)
@@ -61,6 +63,10 @@ struct ModelDev {
     uint32_t bin_shift;
     int32_t present;
     uint32_t active;  // dims whose term can be non-zero (see carma_knn_set_model)
+    int32_t f32_ok;   // fp32 pre-filter usable: <= 16 active dims, |points| <= 1e15
+    const float* ptsf;  // (N + 2 kBlock) x 16: fl32(w * p[a_j]) for the active dims a_j
+    double pmax[kF32Dims];  // max |p[a_j]| over the model
+    uint8_t adim[kF32Dims]; // active dim a_j (0xff: padding)
     double lo[kDims];
     double hi[kDims];
 };
@@ -186,13 +192,26 @@ __global__ void knn_keys(KnnParams p, uint32_t n_bins, uint32_t* __restrict__ qb
         hist[static_cast<uint64_t>(b) * gridDim.x + blockIdx.x] = sh[b];
 }
 
-// Exclusive scan of n u32 values by one CTA of 1024 threads.
-__global__ void scan_matrix(uint32_t* __restrict__ v, uint64_t n) {
-    __shared__ uint32_t part[1024];
-    const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
-    const uint64_t beg = per * threadIdx.x, end = min(n, beg + per);
+// Exclusive scan of the [bin][cta] histogram matrix in three small steps:
+// per-bin totals (warp per bin), a one-CTA scan of the bin totals, then a
+// warp-level scan over each bin's CTAs.
+__global__ void bin_totals(const uint32_t* __restrict__ hist, uint32_t n_bins, uint32_t n_ctas,
+                           uint32_t* __restrict__ tot) {
+    const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = threadIdx.x & 31;
+    if (b >= n_bins) return;
     uint32_t s = 0;
-    for (uint64_t i = beg; i < end; ++i) s += v[i];
+    for (uint32_t c = lane; c < n_ctas; c += 32) s += hist[static_cast<uint64_t>(b) * n_ctas + c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) tot[b] = s;
+}
+
+__global__ void scan_bins(uint32_t* __restrict__ v, uint32_t n) {
+    __shared__ uint32_t part[1024];
+    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t beg = per * threadIdx.x, end = min(n, beg + per);
+    uint32_t s = 0;
+    for (uint32_t i = beg; i < end; ++i) s += v[i];
     part[threadIdx.x] = s;
     __syncthreads();
     for (unsigned off = 1; off < blockDim.x; off <<= 1) {
@@ -202,10 +221,30 @@ __global__ void scan_matrix(uint32_t* __restrict__ v, uint64_t n) {
         __syncthreads();
     }
     uint32_t run = part[threadIdx.x] - s;
-    for (uint64_t i = beg; i < end; ++i) {
+    for (uint32_t i = beg; i < end; ++i) {
         const uint32_t x = v[i];
         v[i] = run;
         run += x;
+    }
+}
+
+__global__ void bin_offsets(uint32_t* __restrict__ hist, uint32_t n_bins, uint32_t n_ctas,
+                            const uint32_t* __restrict__ base) {
+    const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = threadIdx.x & 31;
+    if (b >= n_bins) return;
+    uint32_t run = base[b];
+    uint32_t* row = hist + static_cast<uint64_t>(b) * n_ctas;
+    for (uint32_t c0 = 0; c0 < n_ctas; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        const uint32_t x = c < n_ctas ? row[c] : 0;
+        uint32_t incl = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= static_cast<unsigned>(o)) incl += y;
+        }
+        if (c < n_ctas) row[c] = run + incl - x;
+        run += __shfl_sync(0xffffffffu, incl, 31);
     }
 }
 
@@ -470,8 +509,380 @@ __global__ void __launch_bounds__(128, 4)
     if (evals && lane == 0 && my_evals) atomicAdd(evals, my_evals);
 }
 
+// ------------------------------------------------------------------------
+// knn_search_f32: the same exact search with an fp32 pre-filter.
+//
+// Phase A walks the frontier in blocks of 8 points exactly like knn_search,
+// but evaluates each point in fp32 (one FADD + FFMA per active dim, from a
+// compact fp32 copy of the model). With a = the fp32 difference vector and
+// b = the real weighted difference vector, every component satisfies
+// |a_j - b_j| <= eps_j = 2u(1+u) w_j (pmax_j + |q_j|)  (u = 2^-24: two input
+// conversions + one rounded subtraction), so ||a - b|| <= eta and
+//   LB = (sqrt(sf/(1+g)) - eta)^2 (1-g64)  <=  d2_fp64  <=
+//   UB = (sqrt(sf/(1-g)) + eta)^2 (1+g64)
+// where sf is the FFMA-accumulated sum (relative error g = 17u) and g64
+// bounds the reference's own fp64 rounding. A point can enter the exact
+// top-k only if LB <= kth, tested without a sqrt as sf <= T_lb(kth). kth is
+// an upper bound of the exact k-th best: the k-th smallest UB seen so far,
+// or the exact k-th best after a flush. Surviving candidates are buffered per
+// lane and evaluated exactly in fp64 (reference arithmetic) in phase B,
+// which also runs whenever a lane's buffer fills. Queries whose magnitudes
+// could overflow fp32 (|q| > 1e15 or NaN) never filter (eta = inf) and so
+// are evaluated exactly on every visited point.
+// ------------------------------------------------------------------------
+
+// Bound arithmetic in fp32 with directed rounding (every step rounds toward
+// the safe side). Constants: g = 17 u (FFMA accumulation of 16 terms),
+// g64 = 64 * 2^-53 (the reference's own fp64 rounding of d2), each folded
+// into a factor that dominates it.
+struct F32Bounds {
+    static constexpr float up_g = 1.0f + 0x1.0p-19f;     // >= (1 + g)
+    static constexpr float dn_g = 1.0f - 0x1.0p-19f;     // <= (1 - g)
+    static constexpr float up_g64 = 1.0f + 0x1.0p-22f;   // >= 1/(1 - g64), (1 + g64)
+    static constexpr float dn_g64 = 1.0f - 0x1.0p-22f;   // <= 1/(1 + g64)
+};
+
+// Largest sf that may still hold a candidate: sf <= (1+g)(sqrt(kth/(1-g64)) + eta)^2.
+__device__ __forceinline__ float t_lb(float kth, float eta) {
+    const float r = __fadd_ru(__fsqrt_ru(__fmul_ru(kth, F32Bounds::up_g64)), eta);
+    return __fmul_ru(__fmul_ru(r, r), F32Bounds::up_g);  // inf stays inf
+}
+
+// sf below which a point's UB may improve the UB top-k:
+// sf < (1-g)(sqrt(kth_ub/(1+g64)) - eta)^2; -1 when impossible.
+__device__ __forceinline__ float t_ub(float kth_ub, float eta) {
+    const float r = __fsub_rd(__fsqrt_rd(__fmul_rd(kth_ub, F32Bounds::dn_g64)), eta);
+    if (!(r > 0.0f)) return -1.0f;
+    return __fmul_rd(__fmul_rd(r, r), F32Bounds::dn_g);
+}
+
+// UB = (sqrt(sf/(1-g)) + eta)^2 (1+g64), rounded up.
+__device__ __forceinline__ float ub_of(float sf, float eta) {
+    const float r = __fadd_ru(__fsqrt_ru(__fmul_ru(sf, F32Bounds::up_g)), eta);
+    return __fmul_ru(__fmul_ru(r, r), F32Bounds::up_g64);
+}
+
+// Exact reference d2 (estimators.cpp:445-457) of point s against q in shared memory.
+__device__ __forceinline__ double exact_d2(const double* pt, const double* qs) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int h = 0; h < 9; ++h) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(pt) + h);
+        const double a = __dsub_rn(v.x, qs[2 * h]);
+        d2 = __dadd_rn(d2, __dmul_rn(a, a));
+        const double b = __dsub_rn(v.y, qs[2 * h + 1]);
+        d2 = __dadd_rn(d2, __dmul_rn(b, b));
+    }
+    const double a = __dmul_rn(__dsub_rn(__ldg(pt + 18), qs[18]), 64.0);
+    return __dadd_rn(d2, __dmul_rn(a, a));
+}
+
+template <int K>
+__global__ void __launch_bounds__(128, 4)
+    knn_search_f32(KnnParams p, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ qpos,
+                   int32_t* __restrict__ bucket_out, uint64_t* __restrict__ bytes_out,
+                   double* __restrict__ topk_d2, int64_t* __restrict__ topk_idx,
+                   unsigned long long* __restrict__ evals) {
+    __shared__ double qsh[128][kDims + 1];
+    __shared__ uint32_t cbuf_i[128][kCandCap];
+    __shared__ float cbuf_s[128][kCandCap];
+    const unsigned lane = threadIdx.x & 31;
+    double* qs = qsh[threadIdx.x];
+    uint32_t* ci = cbuf_i[threadIdx.x];
+    float* cs = cbuf_s[threadIdx.x];
+    const uint64_t total_w = (p.q + 31) / 32;
+    const uint64_t per_cta = (total_w + gridDim.x - 1) / gridDim.x;
+    const uint64_t w_beg = per_cta * blockIdx.x;
+    const uint64_t w_end = min(total_w, w_beg + per_cta);
+    const unsigned wpc = blockDim.x >> 5;
+    unsigned long long my_visits = 0, my_exact = 0;
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+
+    for (uint64_t w = w_beg + (threadIdx.x >> 5); w < w_end; w += wpc) {
+        const uint64_t slot = w * 32 + lane;
+        const bool live = slot < p.q;
+        const uint32_t row = live ? perm[slot] : 0;
+        const int fam = live ? family_of(p, row) : -1;
+        if (live && fam < 0) {  // FamilyMismatch -> no estimate
+            if (bucket_out) bucket_out[row] = -1;
+            if (bytes_out) bytes_out[row] = ~0ull;
+        }
+        unsigned pending = __ballot_sync(0xffffffffu, fam >= 0);
+        while (pending) {
+            const int f = __shfl_sync(0xffffffffu, fam, __ffs(pending) - 1);
+            const bool mine = fam == f && ((pending >> lane) & 1u);
+            const unsigned members = __ballot_sync(0xffffffffu, mine);
+            pending &= ~members;
+            const ModelDev& m = p.m[f];
+            const int k = static_cast<int>(m.k < K ? m.k : K);
+
+            // Query: exact fp64 normalisation (estimators.cpp:439-441) into
+            // shared memory, plus the fp32 copy of the active dims and eta.
+            float qf[kF32Dims];
+            double eta = 0.0;
+            double q18 = 0.0;
+            {
+                double raw[kDims];
+                if (mine) {
+                    if (p.format == CARMA_ROWS_SCALAR) {
+                        const double* r = static_cast<const double*>(p.rows) + static_cast<uint64_t>(row) * kDims;
+#pragma unroll
+                        for (int d = 0; d < kDims; ++d) raw[d] = r[d];
+                    } else if (p.format == CARMA_ROWS_PACKED) {
+                        featurize_packed(p, static_cast<const carma_feature_packed*>(p.rows)[row], raw);
+                    } else {
+                        featurize(static_cast<const carma_feature_row*>(p.rows)[row], raw);
+                    }
+                } else {
+#pragma unroll
+                    for (int d = 0; d < kDims; ++d) raw[d] = 0.0;
+                }
+                double qmax = 0.0;
+#pragma unroll
+                for (int d = 0; d < kDims; ++d) {
+                    const double v = mine ? normalize(raw[d], m.lo[d], m.hi[d]) : 0.0;
+                    qs[d] = v;
+                    const double av = fabs(v);
+                    qmax = (av > qmax || av != av) ? av : qmax;
+                }
+                q18 = qs[18];
+                double e2 = 0.0;
+#pragma unroll
+                for (int j = 0; j < kF32Dims; ++j) {
+                    const int a = m.adim[j];
+                    const double w = a == 18 ? 64.0 : 1.0;
+                    const double qa = a < kDims ? qs[a] : 0.0;
+                    qf[j] = a < kDims ? __double2float_rn(w * qa) : 0.0f;
+                    const double ej = a < kDims ? 2.0 * 0x1.0p-24 * (1.0 + 0x1.0p-24) * w * (m.pmax[j] + fabs(qa)) + 0x1.0p-140
+                                                : 0.0;
+                    e2 += ej * ej;
+                }
+                eta = sqrt(e2) * (1.0 + 0x1.0p-40);
+                if (!(qmax <= 1e15)) eta = inf;  // huge or NaN query: exact on every point
+            }
+
+            TopK<K> top;
+            top.init(k);
+            // k smallest UB values (float), same sentinel layout as TopK
+            float ubv[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) ubv[j] = j < K - k ? -1.0f : __int_as_float(0x7f800000);
+            double kth = inf;  // filter bound: >= the exact k-th best
+            const float etaf = __double2float_ru(eta);
+            float T_lb = t_lb(__int_as_float(0x7f800000), etaf), T_ub = t_ub(__int_as_float(0x7f800000), etaf);
+            int cnt = 0;
+
+            unsigned mm = members;
+            for (int j = (__popc(members) - 1) / 2; j > 0; --j) mm &= mm - 1;
+            const int mid_lane = __ffs(mm) - 1;
+            const int64_t n = static_cast<int64_t>(m.n);
+            const int64_t pos = live ? static_cast<int64_t>(qpos[row]) : 0;
+            const int64_t start = __shfl_sync(0xffffffffu, pos, mid_lane);
+            int64_t L = start, R = start;
+            const double t_in = fmin(pos > 0 ? t18_of(__ldg(m.key18 + pos - 1), q18) : inf,
+                                     pos < n ? t18_of(__ldg(m.key18 + pos), q18) : inf);
+            double tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q18) : t_in) : inf;
+            double tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q18) : t_in) : inf;
+            uint64_t visits = 0, exact = 0;
+
+            // Phase B: exact fp64 evaluation of the buffered candidates that
+            // still pass the (possibly tightened) bound, then tighten kth.
+            auto flush = [&]() {
+                for (;;) {
+                    const bool have = cnt > 0;
+                    if (!__any_sync(0xffffffffu, have)) break;
+                    if (have) {
+                        --cnt;
+                        if (cs[cnt] <= T_lb) {
+                            const uint32_t sidx = ci[cnt];
+                            const double d2 = exact_d2(m.pts + static_cast<int64_t>(sidx) * kStride, qs);
+                            top.insert(d2, __ldg(m.orig + sidx));
+                            ++exact;
+                        }
+                    }
+                }
+                const double kx = top.kth();
+                if (kx < kth) {
+                    kth = kx;
+                    T_lb = t_lb(__double2float_ru(kth), etaf);
+                }
+            };
+
+            for (;;) {
+                const bool need_l = mine && L > 0 && tl <= kth;
+                const bool need_r = mine && R < n && tr <= kth;
+                const unsigned bl = __ballot_sync(0xffffffffu, need_l);
+                const unsigned br = __ballot_sync(0xffffffffu, need_r);
+                if ((bl | br) == 0) break;
+                const double rl = __shfl_sync(0xffffffffu, need_l ? tl : inf, mid_lane);
+                const double rr = __shfl_sync(0xffffffffu, need_r ? tr : inf, mid_lane);
+                const bool go_left = bl != 0 && (br == 0 || rl <= rr);
+                int64_t s0;
+                unsigned valid;
+                if (go_left) {
+                    s0 = L - kBlock;
+                    valid = L >= kBlock ? 0xffu : (0xffu << (kBlock - L)) & 0xffu;
+                    L = L > kBlock ? L - kBlock : 0;
+                } else {
+                    s0 = R;
+                    valid = n - R >= kBlock ? 0xffu : (1u << (n - R)) - 1u;
+                    R = n - R > kBlock ? R + kBlock : n;
+                }
+                // Phase A: fp32 sums for the block's 8 points.
+                float sf[kBlock];
+                const float4* blk = reinterpret_cast<const float4*>(m.ptsf + s0 * kF32Dims);
+#pragma unroll
+                for (int c = 0; c < kBlock; ++c) sf[c] = 0.0f;
+#pragma unroll
+                for (int h = 0; h < kF32Dims / 4; ++h) {
+                    float4 v[kBlock];
+#pragma unroll
+                    for (int c = 0; c < kBlock; ++c) v[c] = __ldg(blk + c * (kF32Dims / 4) + h);
+#pragma unroll
+                    for (int c = 0; c < kBlock; ++c) {
+                        float d = v[c].x - qf[4 * h];
+                        sf[c] = fmaf(d, d, sf[c]);
+                        d = v[c].y - qf[4 * h + 1];
+                        sf[c] = fmaf(d, d, sf[c]);
+                        d = v[c].z - qf[4 * h + 2];
+                        sf[c] = fmaf(d, d, sf[c]);
+                        d = v[c].w - qf[4 * h + 3];
+                        sf[c] = fmaf(d, d, sf[c]);
+                    }
+                }
+                unsigned cand = 0, upd = 0;
+#pragma unroll
+                for (int c = 0; c < kBlock; ++c) {
+                    cand |= (sf[c] <= T_lb) ? (1u << c) : 0u;
+                    upd |= (sf[c] < T_ub) ? (1u << c) : 0u;
+                }
+                cand &= valid;
+                upd &= valid;
+                if (!mine) cand = upd = 0;
+                visits += static_cast<uint64_t>(__popc(valid));
+                if (upd) {  // rare: a point whose UB may improve the UB top-k
+                    while (upd) {
+                        const int c = __ffs(upd) - 1;
+                        upd &= upd - 1;
+                        float v = sf[0];
+#pragma unroll
+                        for (int j = 1; j < kBlock; ++j)
+                            if (j == c) v = sf[j];
+                        const float ub = ub_of(v, etaf);
+                        if (ub < ubv[K - 1]) {
+                            bool placed = false;
+#pragma unroll
+                            for (int j = K - 1; j >= 0; --j) {
+                                if (placed) continue;
+                                if (j > 0 && ubv[j - 1] > ub) {
+                                    ubv[j] = ubv[j - 1];
+                                } else {
+                                    ubv[j] = ub;
+                                    placed = true;
+                                }
+                            }
+                        }
+                    }
+                    const float kub = ubv[K - 1];
+                    T_ub = t_ub(kub, etaf);
+                    if (static_cast<double>(kub) < kth) {
+                        kth = static_cast<double>(kub);
+                        T_lb = t_lb(kub, etaf);
+                    }
+                    cand &= 0xffu;
+#pragma unroll
+                    for (int c = 0; c < kBlock; ++c)
+                        if (!(sf[c] <= T_lb)) cand &= ~(1u << c);
+                }
+                // Buffer the candidates; flush (warp-wide) when a lane is full.
+                bool full = false;
+                while (cand) {
+                    const int c = __ffs(cand) - 1;
+                    cand &= cand - 1;
+                    float v = sf[0];
+#pragma unroll
+                    for (int j = 1; j < kBlock; ++j)
+                        if (j == c) v = sf[j];
+                    ci[cnt] = static_cast<uint32_t>(s0 + c);
+                    cs[cnt] = v;
+                    ++cnt;
+                    if (cnt == kCandCap) {
+                        full = true;
+                        break;
+                    }
+                }
+                // a full lane may still hold unbuffered candidates of this block
+                if (__any_sync(0xffffffffu, full)) {
+                    flush();
+                    while (cand) {
+                        const int c = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        float v = sf[0];
+#pragma unroll
+                        for (int j = 1; j < kBlock; ++j)
+                            if (j == c) v = sf[j];
+                        if (v <= T_lb) {
+                            ci[cnt] = static_cast<uint32_t>(s0 + c);
+                            cs[cnt] = v;
+                            ++cnt;
+                        }
+                    }
+                }
+                if (go_left) tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q18) : t_in) : inf;
+                else tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q18) : t_in) : inf;
+            }
+            flush();
+            my_visits += visits;
+            my_exact += exact;
+
+            if (mine) {
+                int best = 0, best_votes = 0;
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    if (a < K - k || top.id[a] == 0x7fffffff) continue;
+                    const int la = __ldg(m.label_by_orig + top.id[a]);
+                    int votes = 0;
+#pragma unroll
+                    for (int b = 0; b < K; ++b)
+                        if (b >= K - k && top.id[b] != 0x7fffffff && __ldg(m.label_by_orig + top.id[b]) == la)
+                            ++votes;
+                    if (votes > best_votes || (votes == best_votes && la > best)) {
+                        best = la;
+                        best_votes = votes;
+                    }
+                }
+                if (bucket_out) bucket_out[row] = best;
+                if (bytes_out) bytes_out[row] = (static_cast<uint64_t>(best) + 1ull) * m.bucket_range;
+                if (topk_d2 || topk_idx) {
+#pragma unroll
+                    for (int a = 0; a < K; ++a) {
+                        if (a < K - k) continue;
+                        const uint64_t o = static_cast<uint64_t>(row) * m.k + (a - (K - k));
+                        const bool real = top.id[a] != 0x7fffffff;
+                        if (topk_d2) topk_d2[o] = real ? top.d[a] : inf;
+                        if (topk_idx) topk_idx[o] = real ? top.id[a] : -1;
+                    }
+                }
+            }
+        }
+    }
+    if (evals) {
+        for (int o = 16; o > 0; o >>= 1) {
+            my_visits += __shfl_xor_sync(0xffffffffu, my_visits, o);
+            my_exact += __shfl_xor_sync(0xffffffffu, my_exact, o);
+        }
+        if (lane == 0) {
+            atomicAdd(evals, my_exact);
+            atomicAdd(evals + 1, my_visits);
+        }
+    }
+}
+
 struct HostModel {
-    DeviceBuffer pts, key18, orig, label_by_orig;
+    DeviceBuffer pts, ptsf, key18, orig, label_by_orig;
+    bool f32_ok = false;
+    double pmax[kF32Dims] = {0};
+    uint8_t adim[kF32Dims] = {0};
     uint64_t n = 0;
     uint64_t bucket_range = 0;
     uint32_t k = 0;
@@ -488,11 +899,13 @@ struct KnnHandle {
     cudaStream_t pipe[2] = {nullptr, nullptr};
     HostModel model[CARMA_FAMILIES];
     struct Scratch {
-        DeviceBuffer rows, family, qbin, qpos, perm, hist, bucket, bytes;
+        DeviceBuffer rows, family, qbin, qpos, perm, hist, tot, bucket, bytes;
         PinnedBuffer stage_rows, stage_family;
     } scratch[2];
     DeviceBuffer evals;
     double act[16] = {0};
+    int path = 0;  // 0 auto (fp32 pre-filter when every model allows it), 1 exact fp64 blocks, 2 fp32 pre-filter
+    uint64_t last_visits = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // pipeline start, search start, search end
     bool timed = false;
     uint64_t last_launches = 0, last_evals = 0;
@@ -518,6 +931,10 @@ KnnParams make_params(const KnnHandle& h, uint32_t* n_bins) {
         m.bucket_range = hm.bucket_range;
         m.k = hm.k;
         m.active = hm.active;
+        m.f32_ok = hm.f32_ok ? 1 : 0;
+        m.ptsf = hm.f32_ok ? hm.ptsf.as<float>() + kBlock * kF32Dims : nullptr;
+        std::memcpy(m.pmax, hm.pmax, sizeof(m.pmax));
+        std::memcpy(m.adim, hm.adim, sizeof(m.adim));
         std::memcpy(m.lo, hm.lo, sizeof(m.lo));
         std::memcpy(m.hi, hm.hi, sizeof(m.hi));
         uint32_t shift = 0;
@@ -537,20 +954,38 @@ int max_k(const KnnHandle& h) {
     return static_cast<int>(k);
 }
 
-void launch_search(const KnnParams& p, int kmax, const uint32_t* perm, const uint32_t* qpos,
-                   int32_t* bucket, uint64_t* bytes, double* d2, int64_t* idx,
-                   unsigned long long* evals, cudaStream_t s) {
+void launch_search(const KnnParams& p, int kmax, bool f32, const uint32_t* perm, const uint32_t* qpos,
+                   int32_t* bucket, uint64_t* bytes, double* d2, int64_t* idx, unsigned long long* evals,
+                   cudaStream_t s) {
     const uint64_t warps = (p.q + 31) / 32;
     const unsigned block = 128;
     // ~16 CTAs per SM over the run (4 resident): small contiguous chunks keep
     // the tail short while each CTA stays in one region of the model.
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, 148u * 16u)));
-    if (kmax <= 5)
-        knn_search<5><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
-    else if (kmax <= 8)
-        knn_search<8><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
-    else
-        knn_search<kMaxK><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+    if (f32) {
+        if (kmax <= 5)
+            knn_search_f32<5><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+        else if (kmax <= 8)
+            knn_search_f32<8><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+        else
+            knn_search_f32<kMaxK><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+    } else {
+        if (kmax <= 5)
+            knn_search<5><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+        else if (kmax <= 8)
+            knn_search<8><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+        else
+            knn_search<kMaxK><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+    }
+}
+
+bool use_f32(const KnnHandle& h) {
+    if (h.path == 1) return false;
+    bool ok = true;
+    for (const auto& m : h.model)
+        if (m.present) ok = ok && m.f32_ok;
+    if (h.path == 2 && !ok) throw Unsupported("fp32 pre-filter requested but a model has > 16 active dims");
+    return ok;
 }
 
 // Runs the 4-kernel pipeline on device-resident rows.
@@ -575,15 +1010,18 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
     knn_keys<<<ctas, 512, shmem, s>>>(p, n_bins, sc.qbin.as<uint32_t>(), sc.qpos.as<uint32_t>(),
                                       sc.hist.as<uint32_t>());
-    scan_matrix<<<1, 1024, 0, s>>>(sc.hist.as<uint32_t>(), static_cast<uint64_t>(n_bins) * ctas);
+    sc.tot.ensure(n_bins * 4);
+    bin_totals<<<(n_bins + 7) / 8, 256, 0, s>>>(sc.hist.as<uint32_t>(), n_bins, ctas, sc.tot.as<uint32_t>());
+    scan_bins<<<1, 1024, 0, s>>>(sc.tot.as<uint32_t>(), n_bins);
+    bin_offsets<<<(n_bins + 7) / 8, 256, 0, s>>>(sc.hist.as<uint32_t>(), n_bins, ctas, sc.tot.as<uint32_t>());
     knn_scatter<<<ctas, 512, shmem, s>>>(q, n_bins, sc.qbin.as<uint32_t>(), sc.hist.as<uint32_t>(),
                                          sc.perm.as<uint32_t>());
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[1], s));
-    launch_search(p, max_k(h), sc.perm.as<uint32_t>(), sc.qpos.as<uint32_t>(), bucket, bytes, d2, idx,
-                  evals, s);
+    launch_search(p, max_k(h), use_f32(h), sc.perm.as<uint32_t>(), sc.qpos.as<uint32_t>(), bucket, bytes, d2,
+                  idx, evals, s);
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[2], s));
     CARMA_CUDA(cudaGetLastError());
-    return 4;
+    return 6;
 }
 
 void check_ready(const KnnHandle* h) {
@@ -608,8 +1046,8 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
         const bool fam_pinned = !family || is_pinned(family);
         const bool out_pinned = (!bucket_out || is_pinned(bucket_out)) && (!bytes_out || is_pinned(bytes_out));
         h->timed = false;
-        h->evals.ensure(8);
-        CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 8, h->pipe[0]));
+        h->evals.ensure(16);
+        CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 16, h->pipe[0]));
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
         uint64_t launches = 0;
         const uint64_t n_chunks = (q + chunk - 1) / chunk;
@@ -657,10 +1095,11 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
         }
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[1]));
-        unsigned long long ev = 0;
-        CARMA_CUDA(cudaMemcpy(&ev, h->evals.ptr, 8, cudaMemcpyDeviceToHost));
+        unsigned long long ev[2] = {0, 0};
+        CARMA_CUDA(cudaMemcpy(ev, h->evals.ptr, 16, cudaMemcpyDeviceToHost));
         h->last_launches = launches;
-        h->last_evals = ev;
+        h->last_evals = ev[0];
+        h->last_visits = ev[1];
     });
 }
 
@@ -697,13 +1136,14 @@ carma_status carma_knn_destroy(carma_knn* hh) {
             cudaStreamSynchronize(h->pipe[1]);
             for (auto& m : h->model) {
                 m.pts.release();
+                m.ptsf.release();
                 m.key18.release();
                 m.orig.release();
                 m.label_by_orig.release();
             }
             for (auto& sc : h->scratch) {
                 sc.rows.release(); sc.family.release(); sc.qbin.release(); sc.qpos.release();
-                sc.perm.release(); sc.hist.release(); sc.bucket.release(); sc.bytes.release();
+                sc.perm.release(); sc.hist.release(); sc.tot.release(); sc.bucket.release(); sc.bytes.release();
                 sc.stage_rows.release(); sc.stage_family.release();
             }
             h->evals.release();
@@ -746,6 +1186,45 @@ carma_status carma_knn_set_model(carma_knn* hh, int32_t family, const double* lo
             key[i] = src[18];
         }
         HostModel& m = h->model[family];
+        // fp32 pre-filter copy: fl32(w * p) of the active dims (w = 64 for dim 18)
+        {
+            int ad = 0;
+            uint32_t act = 0;
+            bool small = true;
+            for (int d = 0; d < kDims; ++d) {
+                bool zero = !(hi[d] > lo[d]);
+                for (uint64_t i = 0; zero && i < n; ++i) zero = points[i * kDims + d] == 0.0;
+                if (!zero) act |= 1u << d;
+            }
+            for (int j = 0; j < kF32Dims; ++j) {
+                m.adim[j] = 0xff;
+                m.pmax[j] = 0.0;
+            }
+            for (int d = 0; d < kDims; ++d)
+                if (act & (1u << d)) {
+                    if (ad < kF32Dims) {
+                        m.adim[ad] = static_cast<uint8_t>(d);
+                        double pm = 0.0;
+                        for (uint64_t i = 0; i < n; ++i) pm = std::max(pm, std::fabs(points[i * kDims + d]));
+                        small = small && pm <= 1e15 && pm == pm;
+                        m.pmax[ad] = pm;
+                    }
+                    ++ad;
+                }
+            m.f32_ok = ad <= kF32Dims && small;
+            if (m.f32_ok) {
+                std::vector<float> pf((n + 2 * kBlock) * kF32Dims, 0.0f);
+                for (uint64_t i = 0; i < n; ++i) {
+                    const double* src = points + static_cast<uint64_t>(order[i]) * kDims;
+                    for (int j = 0; j < ad; ++j) {
+                        const int d = m.adim[j];
+                        pf[(i + kBlock) * kF32Dims + j] = static_cast<float>(d == 18 ? 64.0 * src[d] : src[d]);
+                    }
+                }
+                m.ptsf.ensure(pf.size() * 4);
+                CARMA_CUDA(cudaMemcpy(m.ptsf.ptr, pf.data(), pf.size() * 4, cudaMemcpyHostToDevice));
+            }
+        }
         m.pts.ensure((n + 2 * kBlock) * kStride * 8);
         m.key18.ensure(n * 8);
         m.orig.ensure(n * 4);
@@ -816,8 +1295,8 @@ carma_status carma_knn_predict_device(carma_knn* hh, const void* rows, int32_t f
         std::lock_guard<std::mutex> lock(h->mu);
         DeviceGuard g(h->device);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
-        h->evals.ensure(8);
-        CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 8, s));
+        h->evals.ensure(16);
+        CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 16, s));
         h->timed = true;
         h->last_launches = run_pipeline(*h, h->scratch[0], rows, format, family, default_family, q,
                                         bucket_out, bytes_out, topk_d2, topk_idx,
@@ -840,17 +1319,34 @@ carma_status carma_knn_last_timing(carma_knn* hh, double* search_ms, double* pip
 }
 
 carma_status carma_knn_last_stats(carma_knn* hh, uint64_t* launches, uint64_t* evaluations) {
+    uint64_t visits = 0;
+    return carma_knn_last_work(hh, launches, evaluations, &visits);
+}
+
+carma_status carma_knn_last_work(carma_knn* hh, uint64_t* launches, uint64_t* fp64_evals, uint64_t* fp32_evals) {
     return guarded([&] {
         KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
         if (!h) throw InvalidArg("null handle");
         DeviceGuard g(h->device);
-        unsigned long long ev = 0;
+        unsigned long long ev[2] = {0, 0};
         if (h->evals.ptr) {
             CARMA_CUDA(cudaDeviceSynchronize());
-            CARMA_CUDA(cudaMemcpy(&ev, h->evals.ptr, 8, cudaMemcpyDeviceToHost));
+            CARMA_CUDA(cudaMemcpy(ev, h->evals.ptr, 16, cudaMemcpyDeviceToHost));
         }
+        const bool f32 = use_f32(*h);
         if (launches) *launches = h->last_launches;
-        if (evaluations) *evaluations = ev;
+        // the exact kernel counts every (query, point) evaluation in ev[0]
+        if (fp64_evals) *fp64_evals = ev[0];
+        if (fp32_evals) *fp32_evals = f32 ? ev[1] : 0;
+    });
+}
+
+carma_status carma_knn_set_path(carma_knn* hh, int32_t path) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        if (!h) throw InvalidArg("null handle");
+        if (path < 0 || path > 2) throw InvalidArg("path must be 0 (auto), 1 (exact fp64) or 2 (fp32 pre-filter)");
+        h->path = path;
     });
 }
 

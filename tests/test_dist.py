@@ -1,0 +1,70 @@
+"""The N>1 path on CPU: world_size-2 gloo process group; sharding + gather must
+equal the single-process result (the replay/k-NN shard runners are replaced
+by the oracle, since there is no GPU here)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2508_19073_b200.dist import balanced_shards, run_sharded
+
+
+def test_balanced_shards_cover_and_balance():
+    w = np.random.default_rng(0).integers(50, 130, 1000)
+    for world in (1, 2, 3, 8):
+        sh = balanced_shards(w, world)
+        assert sh[0][0] == 0 and sh[-1][1] == len(w)
+        assert all(a[1] == b[0] for a, b in zip(sh, sh[1:]))
+        loads = [w[b:e].sum() for b, e in sh]
+        assert max(loads) - min(loads) <= 2 * w.max()
+    assert balanced_shards([], 4) == [(0, 0)] * 4
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import paper_2508_19073_b200 as cb
+    from oracle_bind import load_oracle, oracle_replay
+
+    olib = load_oracle()
+    lists = [cb.materialize_trace(cb.generate_trace("t90", s)).tasks for s in range(1, 13)]
+    cfg = cb.make_config(cb.PolicyConfig(policy="magm"), cb.SimConstants())
+
+    def shard(b, e):
+        from paper_2508_19073_b200 import abi
+        out = np.zeros(e - b, abi.trace_result_dtype)
+        for k, t in enumerate(range(b, e)):
+            out[k] = oracle_replay(olib, cfg, lists[t])[2]
+        return out
+
+    res = run_sharded(len(lists), [len(t) for t in lists], shard, rank, world, dist)
+    if rank == 0:
+        np.save(out_path, res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_sweep_equals_single_process(tmp_path, olib):
+    out = str(tmp_path / "res.npy")
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    import paper_2508_19073_b200 as cb
+    from oracle_bind import oracle_replay
+    cfg = cb.make_config(cb.PolicyConfig(policy="magm"), cb.SimConstants())
+    want = np.concatenate([[oracle_replay(olib, cfg, cb.materialize_trace(cb.generate_trace("t90", s)).tasks)[2]]
+                           for s in range(1, 13)])
+    assert got.tobytes() == want.tobytes()

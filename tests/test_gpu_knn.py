@@ -36,11 +36,13 @@ def models():
     return {f: cb.fit_knn(f, 4000, s, 5) for f, s, _ in FAMILIES}
 
 
+@pytest.mark.parametrize("path", [1, 2], ids=["exact-fp64", "fp32-prefilter"])
 @pytest.mark.parametrize("fam,seed,qseed", FAMILIES)
-def test_knn_matches_oracle_bit_exact(gpu, olib, models, fam, seed, qseed):
+def test_knn_matches_oracle_bit_exact(gpu, olib, models, fam, seed, qseed, path):
     m = models[fam]
     knn = cb.GpuKnn(gpu)
     knn.set_model(m)
+    abi.check(abi.lib.carma_knn_set_path(knn.handle, path))
     ds = cb.generate_synthetic_dataset(fam, 4096, qseed)
     raw = cb.scalar_features(ds.rows)
     ob, oby, od2, oidx = oracle_predict(olib, m, raw)
@@ -80,11 +82,13 @@ def test_bank_routes_by_family_and_flags_mismatch(gpu, olib, models):
     assert np.all(by[fams[perm] == 0] == np.uint64(0xFFFFFFFFFFFFFFFF))
 
 
+@pytest.mark.parametrize("path", [1, 2], ids=["exact-fp64", "fp32-prefilter"])
 @pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
-def test_knn_k_variants_and_vote_ties(gpu, olib, k):
+def test_knn_k_variants_and_vote_ties(gpu, olib, k, path):
     m = cb.fit_knn(1, 1500, 77, k)
     knn = cb.GpuKnn(gpu)
     knn.set_model(m)
+    abi.check(abi.lib.carma_knn_set_path(knn.handle, path))
     ds = cb.generate_synthetic_dataset(1, 2000, 99)
     raw = cb.scalar_features(ds.rows)
     ob, oby, od2, oidx = oracle_predict(olib, m, raw)
@@ -173,3 +177,47 @@ def test_gpu_knn_matches_reference_golden(gpu, family):
     ds = cb.generate_synthetic_dataset(fam, n, qseed)
     b, by = knn.predict(ds.rows, default_family=fam)
     assert np.array_equal(b, g[f"bucket_{family}"]) and np.array_equal(by, g[f"bytes_{family}"])
+
+
+@pytest.mark.parametrize("path", [1, 2], ids=["exact-fp64", "fp32-prefilter"])
+def test_knn_outlier_queries_and_near_ties(gpu, olib, models, path):
+    """Queries far outside the training range (fp32 filter loses precision or
+    would overflow -> exact fallback), duplicated training points (exact d2
+    ties) and queries sitting exactly on training points."""
+    m = models[1]
+    pts = m.points.copy()
+    pts[100:140] = pts[60:100]  # exact duplicates -> ties broken by index
+    mm = cb.KnnModel(1, 5, m.bucket_range, m.lo, m.hi, pts, m.labels, m.holdout_rows)
+    knn = cb.GpuKnn(gpu)
+    knn.set_model(mm)
+    abi.check(abi.lib.carma_knn_set_path(knn.handle, path))
+    rng = np.random.default_rng(11)
+    raw = cb.scalar_features(cb.generate_synthetic_dataset(1, 600, 4).rows)
+    span = np.where(m.hi > m.lo, m.hi - m.lo, 1.0)
+    on_pts = pts[55:105] * span + m.lo  # de-normalised training points
+    huge = raw[:40].copy()
+    huge[:, 5] *= 1e9
+    huge[:10, 18] = 1e40
+    q = np.concatenate([raw, on_pts, huge, raw[:20] * (1 + 1e-12)])
+    ob, oby, od2, oidx = oracle_predict(olib, mm, q)
+    gb, gby, gd2, gidx = _device_predict(knn, q, default_family=1, k=5, fmt=abi.ROWS_SCALAR)
+    assert np.array_equal(gb, ob)
+    assert np.array_equal(gd2.view(np.uint64), od2.view(np.uint64))
+    assert np.array_equal(gidx, oidx)
+
+
+def test_fp32_prefilter_cuts_fp64_work(gpu, models):
+    knn = cb.GpuKnn(gpu)
+    knn.set_model(models[2])
+    ds = cb.generate_synthetic_dataset(2, 20000, 77)
+    import ctypes
+    la, e64, e32 = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    abi.check(abi.lib.carma_knn_set_path(knn.handle, 1))
+    b1, _ = knn.predict(ds.rows, default_family=2)
+    abi.check(abi.lib.carma_knn_last_work(knn.handle, ctypes.byref(la), ctypes.byref(e64), ctypes.byref(e32)))
+    exact_only = e64.value
+    abi.check(abi.lib.carma_knn_set_path(knn.handle, 2))
+    b2, _ = knn.predict(ds.rows, default_family=2)
+    abi.check(abi.lib.carma_knn_last_work(knn.handle, ctypes.byref(la), ctypes.byref(e64), ctypes.byref(e32)))
+    assert np.array_equal(b1, b2)
+    assert e32.value > 0 and e64.value * 4 < exact_only, (e64.value, e32.value, exact_only)
