@@ -503,6 +503,40 @@ def run_simulation(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None)
     return res.traces[0], res.job_tasks(0), res.job_gpus(0)
 
 
+class FusedReplay:
+    """Estimator-in-the-loop replay (BASELINE c5): the GPUMemNet k-NN pre-pass
+    over every arrival writes each task's estimate on the device, and the
+    replay reads it there (carma_replay_plan_set_estimates_device) — the
+    estimate is a pure function of the task, so a pre-pass gives the bins
+    make_estimate computes on every dispatch attempt (manager.cpp:292-294)."""
+
+    def __init__(self, m: "Materialized", cfg: np.ndarray, knn: GpuKnn, device: int = 0):
+        import torch
+        self.m, self.cfg, self.knn, self.device = m, cfg, knn, device
+        self.packed, self.table = pack_features(m.features, m.family)
+        abi.check(lib.carma_knn_set_act_table(knn.handle, ptr(self.table)))
+        self.d_rows = torch.from_numpy(self.packed.view(np.uint8).reshape(-1)).to(f"cuda:{device}")
+        self.d_bucket = torch.empty(len(m.tasks), dtype=torch.int32, device=f"cuda:{device}")
+        self.d_bytes = torch.empty(len(m.tasks), dtype=torch.int64, device=f"cuda:{device}")
+        jobs = np.zeros(1, abi.job_dtype)
+        self.plan = ReplayPlan(cfg, m.tasks, np.array([0, len(m.tasks)], np.uint64), jobs, device)
+        self.plan.set_estimates_device(self.d_bytes.data_ptr())
+
+    def run(self) -> None:
+        import torch
+        s = torch.cuda.current_stream(self.device)
+        check(lib.carma_knn_predict_device(self.knn.handle, self.d_rows.data_ptr(), abi.ROWS_PACKED, None, 0,
+                                           len(self.m.tasks), self.d_bucket.data_ptr(), self.d_bytes.data_ptr(),
+                                           None, None, s.cuda_stream))
+        self.plan.run(s.cuda_stream)
+
+    def results(self) -> ReplayResult:
+        return self.plan.results()
+
+    def close(self) -> None:
+        self.plan.close()
+
+
 def median(values) -> float:
     """runner.cpp:149-155"""
     v = sorted(values)

@@ -88,6 +88,7 @@ struct ReplayPlan {
     uint32_t n_traces = 0;
     uint64_t n_tasks = 0, n_task_out = 0, n_gpu_out = 0;
     int max_g = 1;
+    int max_blocks = 1;
     uint32_t class_count[3] = {0, 0, 0};
     int class_max_g[3] = {1, 1, 1};
     std::vector<uint32_t> class_list;  // jobs ordered: light, heavy, global-only
@@ -109,6 +110,9 @@ using replay::Layout;
 // events stay queued: they are energy-integration breakpoints).
 template <int G> using LightL = Layout<G, 64, 32, 16, 16, 16, 2>;
 template <int G> using HeavyL = Layout<G, 320, 64, 32, 16, 16, 2>;
+// Large shared-memory tier for long traces on many GPUs (c5: 10^6 tasks on
+// 64 GPUs peaks at 128 residents and ~215 pending events): one warp per CTA.
+using LargeL = Layout<64, 1024, 256, 32, 16, 128, 2>;
 using GlobalL = Layout<64, 8192, 2048, 256, 256, 4096, 4>;
 
 // Configs whose policy can stack tasks without utilisation preconditions.
@@ -131,18 +135,17 @@ void validate_config(const carma_replay_config& c) {
 }
 
 template <class L, bool SMEM>
-void launch(ReplayPlan& pl, replay::Params p, int sms) {
+void launch(ReplayPlan& pl, replay::Params p, int sms, int warps_per_cta = 4) {
     auto kern = replay::replay_kernel<L, SMEM>;
     if (SMEM) {
-        const int warps_per_cta = 4;
         const size_t shmem = L::bytes * warps_per_cta;
         CARMA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shmem)));
         int per_sm = 0;
-        CARMA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, shmem));
+        CARMA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta, shmem));
         if (per_sm < 1) throw Unsupported("replay state does not fit in shared memory");
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
             static_cast<uint64_t>(per_sm) * sms, (p.n_list + warps_per_cta - 1) / warps_per_cta));
-        kern<<<grid, 128, shmem, pl.stream>>>(p);
+        kern<<<grid, 32 * warps_per_cta, shmem, pl.stream>>>(p);
     } else {
         const unsigned warps = static_cast<unsigned>(std::min<uint64_t>(p.n_list, static_cast<uint64_t>(sms) * 2));
         const unsigned grid = (warps + 3) / 4;
@@ -163,7 +166,8 @@ void launch_shared(ReplayPlan& pl, const replay::Params& p, int max_g, int sms) 
     else launch<LL<64>, true>(pl, p, sms);
 }
 
-// tier 0 = light shared-memory layout, 1 = heavy shared-memory, 2 = global memory
+// tier 0 = light shared-memory layout, 1 = heavy shared-memory, 2 = global
+// memory, 3 = large shared-memory (one warp per CTA)
 void launch_tier(ReplayPlan& pl, const replay::Params& base, const uint32_t* list_dev, uint32_t n_list, int tier,
                  int max_g, uint32_t* counters, uint32_t* retry_base) {
     replay::Params p = base;
@@ -177,6 +181,7 @@ void launch_tier(ReplayPlan& pl, const replay::Params& base, const uint32_t* lis
     CARMA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl.device));
     if (tier == 0) launch_shared<LightL>(pl, p, max_g, sms);
     else if (tier == 1) launch_shared<HeavyL>(pl, p, max_g, sms);
+    else if (tier == 3) launch<LargeL, true>(pl, p, sms, 1);
     else launch<GlobalL, false>(pl, p, sms);
 }
 
@@ -224,12 +229,14 @@ void run_plan(ReplayPlan& pl) {
     pl.retried = total;  // jobs that overflowed a shared-memory tier
     total = static_cast<uint32_t>(ids.size());
     const bool list_dirty = total > 0;
-    // Overflowed, global-only or begin-corrected jobs run in the global-memory
-    // tier (at most twice: a begin correction can follow an overflow).
-    for (int round = 0; round < 2 && total > 0; ++round) {
+    // Overflowed, global-only or begin-corrected jobs: the large shared-memory
+    // tier first, then the global-memory tier (a begin correction can follow
+    // an overflow, so up to three rounds).
+    for (int round = 0; round < 3 && total > 0; ++round) {
         if (round > 0) pl.retried += total;
         CARMA_CUDA(cudaMemcpy(list, ids.data(), total * 4, cudaMemcpyHostToDevice));
-        launch_tier(pl, p, list, total, 2, pl.max_g, counters, retry);
+        const bool large_ok = round == 0 && pl.max_blocks <= 128;
+        launch_tier(pl, p, list, total, large_ok ? 3 : 2, pl.max_g, counters, retry);
         uint32_t nr = 0;
         CARMA_CUDA(cudaMemcpyAsync(&nr, counters + 1, 4, cudaMemcpyDeviceToHost, pl.stream));
         CARMA_CUDA(cudaStreamSynchronize(pl.stream));
@@ -268,6 +275,7 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
             for (const auto& c : pl->cfgs) {
                 validate_config(c);
                 pl->max_g = std::max(pl->max_g, c.gpu_count);
+                pl->max_blocks = std::max(pl->max_blocks, static_cast<int>(c.gpu_capacity / c.alloc_block));
             }
             for (uint32_t t = 0; t < n_traces; ++t) {
                 if (trace_offsets[t + 1] <= trace_offsets[t]) throw InvalidArg("ConfigError: trace contains no tasks");

@@ -63,12 +63,36 @@ def knn(args):
               flush=True)
 
 
+def fused(args):
+    import ctypes
+    m = cb.materialize_trace(cb.generate_uniform_trace(args.tasks, 3.0, 7))
+    cfg = cb.make_config(cb.PolicyConfig(policy="magm", max_smact=0.8, monitor_window=5.0),
+                         cb.SimConstants(gpu_count=64))
+    knn = cb.GpuKnn(0)
+    for f in (1, 2):
+        knn.set_model(cb.fit_knn(f, 4000, 11 + 101 * f, 5))
+    fr = cb.FusedReplay(m, cfg, knn, 0)
+    import torch
+    for _ in range(args.reps):
+        t = time.perf_counter()
+        fr.run()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        km, rm = ctypes.c_double(), ctypes.c_double()
+        abi.check(abi.lib.carma_replay_plan_timing(fr.plan._h, ctypes.byref(km), ctypes.byref(rm)))
+        print(f"fused {args.tasks} tasks: wall {dt * 1e3:.1f} ms, replay run {rm.value:.1f} ms "
+              f"(tier0 {km.value:.1f}), stats {fr.plan.stats()}", flush=True)
+    r = fr.results().traces[0]
+    print("oom", r["oom_count"], "events", r["events"], "makespan", r["trace_total_time"], "status", r["status"])
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=("replay", "knn"))
+    ap.add_argument("what", choices=("replay", "knn", "fused"))
+    ap.add_argument("--tasks", type=int, default=1_000_000)
     ap.add_argument("--traces", type=int, default=20000)
     ap.add_argument("--policies", default="exclusive,rr,magm,lug")
     ap.add_argument("--rows", type=int, default=1 << 22)
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
-    replay(a) if a.what == "replay" else knn(a)
+    {"replay": replay, "knn": knn, "fused": fused}[a.what](a)

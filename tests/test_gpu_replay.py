@@ -197,3 +197,35 @@ def test_plan_upload_and_outcomes(gpu, olib):
         assert np.array_equal(to["final_dispatch"][sl], ot["final_dispatch"])
         assert np.array_equal(to["ooms"][sl], ot["ooms"]) and np.array_equal(to["attempts"][sl], ot["attempts"])
         assert jr[j].tobytes() == np.array([otr]).tobytes()
+
+
+@pytest.mark.parametrize("estimator", ["learned", "none"])
+def test_fused_c5_prefix_matches_oracle(gpu, olib, estimator):
+    """BASELINE c5 shape on a 20k-task prefix: uniform catalog, 3 s mean gaps,
+    64 GPUs, MAGM u=0.8, W=5 s; learned estimates from the on-device k-NN
+    pre-pass feed the replay without leaving the GPU."""
+    from cases import model
+    m = cb.materialize_trace(cb.generate_uniform_trace(20000, 3.0, 7))
+    cfg = cfg_of("magm", gpu_count=64, window=5.0)
+    knn = cb.GpuKnn(gpu)
+    for f in (1, 2):
+        knn.set_model(model(f))
+    want_tasks = m.tasks.copy()
+    if estimator == "learned":
+        raw = cb.scalar_features(m.features)
+        e = np.zeros(len(m.tasks), np.uint64)
+        for f in set(m.family.tolist()):
+            sel = m.family == f
+            e[sel] = oracle_predict(olib, model(f), raw[sel])[1]
+        want_tasks["estimate"] = e
+        fused = cb.FusedReplay(m, cfg, knn, gpu)
+        fused.run()
+        res = fused.results()
+        fused.close()
+    else:
+        res = cb.replay(cfg, [m.tasks])
+    rc, ot, otr, og = oracle_replay(olib, cfg, want_tasks)
+    assert rc == 0
+    assert res.job_tasks(0).tobytes() == ot.tobytes()
+    assert res.traces[0:1].tobytes() == np.array([otr]).tobytes()
+    assert res.job_gpus(0).tobytes() == og.tobytes()
