@@ -232,6 +232,23 @@ def cpu_sweep_baseline(ref, threads: int, target_s: float = 10.0):
     return placed.value / t, f"t90 seeds 1..{n} x {{exclusive, rr, magm, lug}} ({n * len(pols)} runs)", n
 
 
+def cpu_fused_baseline(ref, n_tasks: int):
+    """One reference run_simulation (single-threaded by design, runner.cpp:40)
+    on the first n_tasks rows of the c5 trace, loaded from a #carma-trace v1
+    file, learned estimator provisioned in-process as the reference does."""
+    import paper_2508_19073_b200 as cb
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import ref_config, ref_run
+    path = os.path.join(tempfile.mkdtemp(), "c5_prefix.trace")
+    cb.save_trace(cb.generate_uniform_trace(n_tasks, 3.0, 7), path)
+    cfg = ref_config(policy="magm", estimator="learned", gpu_count=64, window=5.0)
+    t = time.perf_counter()
+    ref_run(ref, cfg, path=path, cap=n_tasks)
+    dt = time.perf_counter() - t
+    return n_tasks / dt, (f"first {n_tasks} rows of the c5 trace, one run_simulation on 1 core "
+                          f"(reference cost grows superlinearly with trace length, SURVEY F7)")
+
+
 def run_reference(args, d: Dist):
     if d.rank != 0:
         return
@@ -424,6 +441,36 @@ def run_carma(args, d: Dist):
                          "note": "latency/issue bound event loop; algorithmic bytes = 80 B per placed task"},
         }
 
+    # ---------------- stage 1 -> 2 fused (configs[4], c5)
+    fused = None
+    if not args.skip_fused:
+        t0 = time.time()
+        mf = cb.materialize_trace(cb.generate_uniform_trace(args.fused_tasks, 3.0, 7))
+        cfg5 = cb.make_config(cb.PolicyConfig(policy="magm", max_smact=0.8, monitor_window=5.0),
+                              cb.SimConstants(gpu_count=64))
+        fr = cb.FusedReplay(mf, cfg5, knn, dev)
+        log(f"[rank {d.rank}] fused inputs {args.fused_tasks} tasks in {time.time() - t0:.1f}s")
+        fr.run()  # warm-up (one: a step is ~13 s at 10^6 tasks)
+        torch.cuda.synchronize()
+        d.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fr.run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        f_ms = d.max(e0.elapsed_time(e1))
+        fres = fr.results().traces[0]
+        assert fres["status"] == 0
+        fr.close()
+        fused = {"metric": "fused estimator-in-the-loop placed tasks/sec", "unit": "placed tasks/s",
+                 "value": N * args.fused_tasks / (f_ms * 1e-3), "ms_per_step": f_ms, "steps": 1, "warmup": 1,
+                 "config": {"workload": f"c5: {args.fused_tasks} arrivals, uniform catalog, exp gaps mean 3 s, "
+                                        "seed 7; k-NN pre-pass over every arrival on device feeding the replay; "
+                                        "MAGM + learned, u=0.8, W=5 s, 64 simulated GPUs"},
+                 "events": int(fres["events"]), "oom_count": int(fres["oom_count"]),
+                 "note": "one trace: a single warp replays it (sequential event loop); replicas only across GPUs"}
+
     # ---------------- CPU baselines (rank 0, N = 1)
     cpu = None
     if d.rank == 0 and N == 1 and not args.skip_cpu:
@@ -436,6 +483,10 @@ def run_carma(args, d: Dist):
                 srate, ssample, _ = cpu_sweep_baseline(ref, threads)
                 replay["cpu_baseline"] = {"value": srate, "unit": "placed tasks/s", "cores": threads,
                                           "kind": "reference", "sample": ssample}
+            if fused is not None:
+                frate, fsample = cpu_fused_baseline(ref, args.fused_cpu_tasks)
+                fused["cpu_baseline"] = {"value": frate, "unit": "placed tasks/s", "cores": 1, "kind": "reference",
+                                         "sample": fsample}
 
     if d.rank != 0:
         return
@@ -463,6 +514,7 @@ def run_carma(args, d: Dist):
         "cpu_baseline": cpu,
         "clocks": clocks,
         "replay": replay,
+        "fused": fused,
     }
     print(json.dumps(line))
 
@@ -476,6 +528,9 @@ def main():
     ap.add_argument("--sweep-traces", type=int, default=SWEEP_TRACES)
     ap.add_argument("--skip-replay", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-fused", action="store_true")
+    ap.add_argument("--fused-tasks", type=int, default=1_000_000)
+    ap.add_argument("--fused-cpu-tasks", type=int, default=20_000)
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup raised to 3 (timing rule)")

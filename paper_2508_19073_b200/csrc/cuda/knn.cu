@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(128, 4)
 // g64 = 64 * 2^-53 (the reference's own fp64 rounding of d2), each folded
 // into a factor that dominates it.
 struct F32Bounds {
-    static constexpr float up_g = 1.0f + 0x1.0p-19f;     // >= (1 + g)
+    static constexpr float up_g = 1.0f + 0x1.0p-19f;     // >= (1 + g), g = 17u covers 2 x 8-term chains + fold
     static constexpr float dn_g = 1.0f - 0x1.0p-19f;     // <= (1 - g)
     static constexpr float up_g64 = 1.0f + 0x1.0p-22f;   // >= 1/(1 - g64), (1 + g64)
     static constexpr float dn_g64 = 1.0f - 0x1.0p-22f;   // <= 1/(1 + g64)
@@ -560,6 +560,29 @@ __device__ __forceinline__ float t_ub(float kth_ub, float eta) {
 __device__ __forceinline__ float ub_of(float sf, float eta) {
     const float r = __fadd_ru(__fsqrt_ru(__fmul_ru(sf, F32Bounds::up_g)), eta);
     return __fmul_ru(__fmul_ru(r, r), F32Bounds::up_g64);
+}
+
+// Packed fp32x2 arithmetic (sm_100: FADD2 / FFMA2, two lanes per instruction).
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 f2unpack(unsigned long long v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2sub(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
 }
 
 // Exact reference d2 (estimators.cpp:445-457) of point s against q in shared memory.
@@ -586,7 +609,10 @@ __global__ void __launch_bounds__(128, 4)
     __shared__ double qsh[128][kDims + 1];
     __shared__ uint32_t cbuf_i[128][kCandCap];
     __shared__ float cbuf_s[128][kCandCap];
+    // per warp: the next fp32 block on the left [0] and right [1] of the frontier
+    __shared__ float4 stage[4][2][kBlock * kF32Dims / 4];
     const unsigned lane = threadIdx.x & 31;
+    float4 (*stg)[kBlock * kF32Dims / 4] = stage[threadIdx.x >> 5];
     double* qs = qsh[threadIdx.x];
     uint32_t* ci = cbuf_i[threadIdx.x];
     float* cs = cbuf_s[threadIdx.x];
@@ -661,6 +687,9 @@ __global__ void __launch_bounds__(128, 4)
                 if (!(qmax <= 1e15)) eta = inf;  // huge or NaN query: exact on every point
             }
 
+            unsigned long long qf2[kF32Dims / 2];
+#pragma unroll
+            for (int j = 0; j < kF32Dims / 2; ++j) qf2[j] = f2pack(qf[2 * j], qf[2 * j + 1]);
             TopK<K> top;
             top.init(k);
             // k smallest UB values (float), same sentinel layout as TopK
@@ -684,6 +713,13 @@ __global__ void __launch_bounds__(128, 4)
             double tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q18) : t_in) : inf;
             double tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q18) : t_in) : inf;
             uint64_t visits = 0, exact = 0;
+            // Stage both neighbouring blocks (one coalesced 16-B load per lane
+            // each); every step then prefetches the next block on its side.
+            const float4* pf4 = reinterpret_cast<const float4*>(m.ptsf);
+            __syncwarp();
+            stg[0][lane] = __ldg(pf4 + (L - kBlock) * (kF32Dims / 4) + lane);
+            stg[1][lane] = __ldg(pf4 + R * (kF32Dims / 4) + lane);
+            __syncwarp();
 
             // Phase B: exact fp64 evaluation of the buffered candidates that
             // still pass the (possibly tightened) bound, then tighten kth.
@@ -728,28 +764,40 @@ __global__ void __launch_bounds__(128, 4)
                     valid = n - R >= kBlock ? 0xffu : (1u << (n - R)) - 1u;
                     R = n - R > kBlock ? R + kBlock : n;
                 }
-                // Phase A: fp32 sums for the block's 8 points.
+                // Phase A: fp32 sums for the block's 8 points, read from the
+                // staged copy; the side's next block loads meanwhile.
+                const int side = go_left ? 0 : 1;
+                const int64_t nxt = go_left ? L - kBlock : R;
+                const float4 pre = __ldg(pf4 + nxt * (kF32Dims / 4) + lane);
+                // Two packed partial sums per point (even / odd active dims),
+                // folded at the end: any order of the 16 non-negative terms
+                // stays within the 17u accumulation bound.
                 float sf[kBlock];
-                const float4* blk = reinterpret_cast<const float4*>(m.ptsf + s0 * kF32Dims);
+                const float4* blk = stg[side];
+                unsigned long long acc[kBlock];
 #pragma unroll
-                for (int c = 0; c < kBlock; ++c) sf[c] = 0.0f;
+                for (int c = 0; c < kBlock; ++c) acc[c] = 0ull;
 #pragma unroll
                 for (int h = 0; h < kF32Dims / 4; ++h) {
                     float4 v[kBlock];
 #pragma unroll
-                    for (int c = 0; c < kBlock; ++c) v[c] = __ldg(blk + c * (kF32Dims / 4) + h);
+                    for (int c = 0; c < kBlock; ++c) v[c] = blk[c * (kF32Dims / 4) + h];
 #pragma unroll
                     for (int c = 0; c < kBlock; ++c) {
-                        float d = v[c].x - qf[4 * h];
-                        sf[c] = fmaf(d, d, sf[c]);
-                        d = v[c].y - qf[4 * h + 1];
-                        sf[c] = fmaf(d, d, sf[c]);
-                        d = v[c].z - qf[4 * h + 2];
-                        sf[c] = fmaf(d, d, sf[c]);
-                        d = v[c].w - qf[4 * h + 3];
-                        sf[c] = fmaf(d, d, sf[c]);
+                        const unsigned long long d0 = f2sub(f2pack(v[c].x, v[c].y), qf2[2 * h]);
+                        acc[c] = f2fma(d0, d0, acc[c]);
+                        const unsigned long long d1 = f2sub(f2pack(v[c].z, v[c].w), qf2[2 * h + 1]);
+                        acc[c] = f2fma(d1, d1, acc[c]);
                     }
                 }
+#pragma unroll
+                for (int c = 0; c < kBlock; ++c) {
+                    const float2 a = f2unpack(acc[c]);
+                    sf[c] = a.x + a.y;
+                }
+                __syncwarp();
+                stg[side][lane] = pre;
+                __syncwarp();
                 unsigned cand = 0, upd = 0;
 #pragma unroll
                 for (int c = 0; c < kBlock; ++c) {

@@ -96,7 +96,7 @@ struct Layout {
     static constexpr size_t last_v = last_t + 8ull * G;
     static constexpr size_t ring_t = al8(last_v + 8ull * G);           // f64 [G][RG]
     static constexpr size_t ring_v = ring_t + 8ull * G * RG;
-    static constexpr size_t ht = ring_v + 8ull * G * RG;               // f64 [H]
+    static constexpr size_t ht = ring_v + 8ull * G * RG;               // u64 time keys [H]
     static constexpr size_t s_rem = ht + 8ull * H;                     // f64 [S] x 5
     static constexpr size_t s_rate = s_rem + 8ull * S;
     static constexpr size_t s_last = s_rate + 8ull * S;
@@ -146,28 +146,45 @@ struct Sc {
 };
 
 // ---------------------------------------------------------------- heap
+// 4-ary min-heap on (time, seq). Times are stored as order-preserving u64
+// keys (same order as the doubles; +0 and -0 collapse), so sifting uses
+// integer compares instead of long-latency fp64 compares.
+__device__ __forceinline__ uint64_t tkey(double t) {
+    if (t == 0.0) t = 0.0;
+    const uint64_t u = static_cast<uint64_t>(__double_as_longlong(t));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double tval(uint64_t k) {
+    const uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double(static_cast<long long>(u));
+}
+__device__ __forceinline__ bool klater(uint64_t ka, uint32_t sa, uint64_t kb, uint32_t sb) {
+    return ka != kb ? ka > kb : sa > sb;
+}
+
 template <class L>
 __device__ __forceinline__ uint32_t heap_push(char* b, Sc& c, double t, uint32_t info) {
     if (c.hsize >= static_cast<uint32_t>(L::H)) {
         c.status = kStatusRetry;
         return kNone;
     }
-    double* ht = RP_F64(ht);
+    uint64_t* hk = RP_U64(ht);
     uint32_t* hs = RP_U32(hs);
     uint32_t* hi = RP_U32(hinfo);
+    const uint64_t key = tkey(t);
     const uint32_t seq = c.seq_next++;
     uint32_t i = c.hsize++;
     while (i > 0) {
-        const uint32_t p = (i - 1) >> 1;
-        const double pt = ht[p];
+        const uint32_t p = (i - 1) >> 2;
+        const uint64_t pk = hk[p];
         const uint32_t ps = hs[p];
-        if (!later(pt, ps, t, seq)) break;
-        ht[i] = pt;
+        if (!klater(pk, ps, key, seq)) break;
+        hk[i] = pk;
         hs[i] = ps;
         hi[i] = hi[p];
         i = p;
     }
-    ht[i] = t;
+    hk[i] = key;
     hs[i] = seq;
     hi[i] = info;
     return seq;
@@ -175,26 +192,40 @@ __device__ __forceinline__ uint32_t heap_push(char* b, Sc& c, double t, uint32_t
 
 template <class L>
 __device__ __forceinline__ void heap_pop(char* b, Sc& c) {
-    double* ht = RP_F64(ht);
+    uint64_t* hk = RP_U64(ht);
     uint32_t* hs = RP_U32(hs);
     uint32_t* hi = RP_U32(hinfo);
     const uint32_t n = --c.hsize;
     if (n == 0) return;
-    const double t = ht[n];
+    const uint64_t k = hk[n];
     const uint32_t sq = hs[n], inf = hi[n];
     uint32_t i = 0;
     for (;;) {
-        uint32_t l = 2 * i + 1;
-        if (l >= n) break;
-        const uint32_t r = l + 1;
-        if (r < n && later(ht[l], hs[l], ht[r], hs[r])) l = r;
-        if (!later(t, sq, ht[l], hs[l])) break;
-        ht[i] = ht[l];
-        hs[i] = hs[l];
-        hi[i] = hi[l];
-        i = l;
+        const uint32_t c0 = 4 * i + 1;
+        if (c0 >= n) break;
+        uint32_t m = c0;
+        uint64_t mk = hk[c0];
+        uint32_t ms = hs[c0];
+#pragma unroll
+        for (uint32_t d = 1; d < 4; ++d) {
+            const uint32_t cc = c0 + d;
+            if (cc < n) {
+                const uint64_t ck = hk[cc];
+                const uint32_t cs = hs[cc];
+                if (klater(mk, ms, ck, cs)) {
+                    m = cc;
+                    mk = ck;
+                    ms = cs;
+                }
+            }
+        }
+        if (!klater(k, sq, mk, ms)) break;
+        hk[i] = mk;
+        hs[i] = ms;
+        hi[i] = hi[m];
+        i = m;
     }
-    ht[i] = t;
+    hk[i] = k;
     hs[i] = sq;
     hi[i] = inf;
 }
@@ -804,12 +835,12 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
         double t;
         uint32_t kind, payload, seq = 0;
         const double at = have_arr ? tasks[c.arrived].submit : 0.0;
-        if (have_arr && (!have_heap || !later(at, c.arrived, RP_F64(ht)[0], RP_U32(hs)[0]))) {
+        if (have_arr && (!have_heap || !klater(tkey(at), c.arrived, RP_U64(ht)[0], RP_U32(hs)[0]))) {
             t = at;
             kind = 0;
             payload = c.arrived;
         } else {
-            t = RP_F64(ht)[0];
+            t = tval(RP_U64(ht)[0]);
             seq = RP_U32(hs)[0];
             const uint32_t info = RP_U32(hinfo)[0];
             kind = info >> 30;
