@@ -38,6 +38,7 @@ SWEEP_POLICIES = ("exclusive", "rr", "magm", "lug")
 ALG_BYTES_PER_ESTIMATE = 164       # 19 f64 in + i32 bucket + u64 bytes
 ALG_BYTES_PER_TASK = 80            # 45 B in + 35 B out per placed task
 FLOPS_PER_EVAL = 58                # 19 x (sub, mul, add) + 1 weight mul, FMA-free
+FLOPS_PER_F32_EVAL = 48            # fp32 pre-filter: 16 dims x (sub + fma)
 
 
 def log(*a):
@@ -48,7 +49,7 @@ def log(*a):
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -58,13 +59,14 @@ class Clocks:
         self.proc = None
 
     def __enter__(self):
+        self.t_busy = time.time()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
-        time.sleep(0.3)
+        time.sleep(1.0)  # nvidia-smi needs ~0.5 s before its first sample
         return self
 
     def __exit__(self, *exc):
@@ -72,24 +74,39 @@ class Clocks:
             self.proc.terminate()
             self.proc.wait()
 
+    def mark(self, name: str) -> None:
+        setattr(self, name, time.time())
+
     def summary(self):
+        """Median SM clock over samples inside [t_begin, t_end] (the timed
+        region); if the region is shorter than the sampling period, the
+        samples of the surrounding busy window (warm-up + timed) are used."""
+        import datetime
         try:
             rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
         except OSError:
             rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons = [], 0.0, set()
+        parsed = []
         for r in rows:
             try:
-                sm.append(float(r[1]))
-                mx = max(mx, float(r[2]))
-                for name, v in zip(names, r[5:9]):
-                    if v.strip().lower() == "active":
-                        reasons.add(name)
+                ts = datetime.datetime.strptime(r[0].strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                parsed.append((ts, float(r[2]), float(r[3]), [n for n, v in zip(names, r[6:10])
+                                                              if v.strip().lower() == "active"]))
             except (ValueError, IndexError):
                 continue
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        t0, t1 = getattr(self, "t_begin", 0.0), getattr(self, "t_end", 1e30)
+        inside = [p for p in parsed if t0 - 0.05 <= p[0] <= t1 + 0.05]
+        window = "timed region"
+        if not inside:
+            w0 = getattr(self, "t_busy", t0)
+            inside = [p for p in parsed if w0 <= p[0] <= t1 + 0.2]
+            window = "warm-up + timed (timed region shorter than the 100 ms sampling period)"
+        sm = [p[1] for p in inside]
+        reasons = sorted({n for p in inside for n in p[3]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max((p[2] for p in parsed), default=None),
+                "reasons": reasons, "samples": len(sm), "window": window}
 
 
 # ------------------------------------------------------------------ dist
@@ -292,6 +309,8 @@ def run_carma(args, d: Dist):
     import ctypes
     fp64 = ctypes.c_double()
     abi.check(abi.lib.carma_probe_fp64(dev, ctypes.byref(fp64)))
+    fp32 = ctypes.c_double()
+    abi.check(abi.lib.carma_probe_fp32(dev, ctypes.byref(fp32)))
 
     # ---------------- stage 1 inputs
     t0 = time.time()
@@ -313,14 +332,16 @@ def run_carma(args, d: Dist):
         abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_PACKED, None, 1, Q,
                                                    d_b.data_ptr(), d_by.data_ptr(), None, None, stream.cuda_stream))
 
-    for _ in range(args.warmup):
-        knn_step()
-    torch.cuda.synchronize()
     search_ms, pipe_ms = [], []
     sm, pm = ctypes.c_double(), ctypes.c_double()
     with Clocks(dev) as clk:
+        clk.mark("t_busy")
+        for _ in range(args.warmup):
+            knn_step()
+        torch.cuda.synchronize()
         d.barrier()
         torch.cuda.synchronize()
+        clk.mark("t_begin")
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -331,11 +352,15 @@ def run_carma(args, d: Dist):
             pipe_ms.append(pm.value)
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark("t_end")
         d.barrier()
     knn_ms = d.max(e0.elapsed_time(e1) / args.steps)
     clocks = clk.summary()
     b_dev = d_b.cpu().numpy()
     launches, evals = knn.last_stats()
+    la_, e64_, e32_ = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    abi.check(abi.lib.carma_knn_last_work(knn.handle, ctypes.byref(la_), ctypes.byref(e64_), ctypes.byref(e32_)))
+    visits = e32_.value
     value = N * Q / (knn_ms * 1e-3)
 
     # e2e: pinned host packed rows -> carma_knn_predict_packed (chunked H2D /
@@ -360,17 +385,21 @@ def run_carma(args, d: Dist):
     # the 136-byte FeatureVector-row host API, once, for reference
     h_full = torch.from_numpy(rows.view(np.uint8).reshape(-1)).pin_memory().numpy().view(rows.dtype)
     h_fam = torch.from_numpy(fam).pin_memory().numpy()
-    t = time.perf_counter()
-    abi.check(abi.lib.carma_knn_predict(knn.handle, h_full.ctypes.data, h_fam.ctypes.data, 1, Q,
-                                        h_b.ctypes.data, h_by.ctypes.data))
-    e2e_full_s = time.perf_counter() - t
+    for _ in range(2):  # warm-up: scratch sized for 136-B rows
+        t = time.perf_counter()
+        abi.check(abi.lib.carma_knn_predict(knn.handle, h_full.ctypes.data, h_fam.ctypes.data, 1, Q,
+                                            h_b.ctypes.data, h_by.ctypes.data))
+        e2e_full_s = time.perf_counter() - t
     assert np.array_equal(h_b, b_dev)
     del d_rows, d_b, d_by, h_full, h_fam
 
     search_avg = statistics.mean(search_ms)
-    flops_per_launch = evals * FLOPS_PER_EVAL
-    achieved = flops_per_launch / (search_avg * 1e-3)
-    traffic = profile_traffic("knn_search")
+    # executed work of the exact pruned search: fp32 pre-filter evaluations
+    # (16 dims x (sub + fma) = 48 flops) dominate; exact fp64 evaluations are
+    # reported beside them
+    f32_flops = visits * FLOPS_PER_F32_EVAL
+    achieved = f32_flops / (search_avg * 1e-3)
+    traffic = profile_traffic("knn_search_f32")
 
     # ---------------- stage 2: policy sweep
     replay = None
@@ -503,14 +532,20 @@ def run_carma(args, d: Dist):
                 "api": "carma_knn_predict_packed (64 B packed rows, pinned host buffers)",
                 "feature_row_api_estimates_per_s": N * Q / e2e_full_s},
         "gpu_launches": int(launches) * args.steps,
-        "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": fp64.value / 1e12, "unit": "TFLOP/s",
-                     "frac": achieved / fp64.value, "traffic": traffic,
-                     "kernel": "knn_search", "kernel_ms": search_avg,
+        "roofline": {"bound": "fp32", "achieved": achieved / 1e12, "peak": fp32.value / 1e12, "unit": "TFLOP/s",
+                     "frac": achieved / fp32.value, "traffic": traffic,
+                     "kernel": "knn_search_f32", "kernel_ms": search_avg,
                      "kernel_share_of_step": search_avg / statistics.mean(pipe_ms),
-                     "peak_source": "measured: carma_probe_fp64 (separately rounded DADD/DMUL issue rate)",
-                     "work": f"{evals} (query, point) distance evaluations x {FLOPS_PER_EVAL} fp64 ops",
+                     "peak_source": "measured: carma_probe_fp32 (FFMA2 issue rate; the contract's MEASURED_PEAKS "
+                                    "file has no fp32/fp64 figures)",
+                     "work": f"{visits} fp32 pre-filter evaluations x {FLOPS_PER_F32_EVAL} flops + {evals} exact "
+                             f"fp64 evaluations x {FLOPS_PER_EVAL} flops",
+                     "fp64": {"achieved": evals * FLOPS_PER_EVAL / (search_avg * 1e-3) / 1e12,
+                              "peak": fp64.value / 1e12, "unit": "TFLOP/s"},
                      "brute_force_equivalent_tflops": Q * 162_400 / (search_avg * 1e-3) / 1e12,
-                     "hbm_gbs": ALG_BYTES_PER_ESTIMATE * Q / (search_avg * 1e-3) / 1e9, "hbm_peak_gbs": hbm},
+                     "hbm_gbs": ALG_BYTES_PER_ESTIMATE * Q / (search_avg * 1e-3) / 1e9, "hbm_peak_gbs": hbm,
+                     "note": "exact pruned search: the bound is instruction issue over the fp32 pass; the brute-force "
+                             "figure (162,400 flops/estimate) is what the pruning avoids"},
         "cpu_baseline": cpu,
         "clocks": clocks,
         "replay": replay,

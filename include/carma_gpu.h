@@ -309,6 +309,9 @@ carma_status carma_pick_batch(int device, const carma_replay_config* cfg,
  * ops per second, 1 op = 1 flop): the roofline denominator of the k-NN
  * distance kernel, which is FP64-pipe bound and FMA-free by contract. */
 carma_status carma_probe_fp64(int device, double* flops_per_s);
+/* Measured packed fp32 FMA throughput (FFMA2, 1 FMA = 2 flops): the roofline
+ * denominator of the k-NN fp32 pre-filter pass. */
+carma_status carma_probe_fp32(int device, double* flops_per_s);
 
 #ifdef __cplusplus
 }

@@ -118,6 +118,7 @@ SIGNATURES = {
     "carma_knn_last_timing": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "carma_replay_plan_timing": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "carma_probe_fp64": (c_int, [c_int, POINTER(c_double)]),
+    "carma_probe_fp32": (c_int, [c_int, POINTER(c_double)]),
     "carma_replay_plan_create": (c_int, [c_int, P, c_uint32, P, P, c_uint32, P, c_uint32, c_int32,
                                          POINTER(c_void_p)]),
     "carma_replay_plan_set_estimates_device": (c_int, [c_void_p, P]),

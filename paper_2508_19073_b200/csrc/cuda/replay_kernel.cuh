@@ -944,7 +944,7 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
 }
 
 template <class L, bool SMEM>
-__global__ void __launch_bounds__(128, SMEM ? 6 : 1) replay_kernel(Params p) {
+__global__ void __launch_bounds__(128, SMEM ? 8 : 1) replay_kernel(Params p) {
     extern __shared__ __align__(16) char smem[];
     const unsigned lane = threadIdx.x & 31;
     const unsigned wib = threadIdx.x >> 5;
