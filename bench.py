@@ -266,6 +266,101 @@ def cpu_fused_baseline(ref, n_tasks: int):
                           f"(reference cost grows superlinearly with trace length, SURVEY F7)")
 
 
+def small_configs(cb, abi, dev, ref):
+    """configs[0] (c1: 4096 MLP vectors, the reference's CPU batch) and
+    configs[2] (c3: one paper-style t90 trace on an 8-GPU server, MAGM u=0.8
+    with OOM recovery, estimator none and learned): latency-style lines."""
+    import ctypes
+
+    import torch
+    out = {}
+    # ---- c1
+    m = cb.fit_knn(0, 4000, 11, 5)
+    knn = cb.GpuKnn(dev)
+    knn.set_model(m)
+    ds = cb.generate_synthetic_dataset(0, 4096, 12345)
+    words, schema = cb.pack_features_bits(ds.rows, np.zeros(4096, np.int8))
+    abi.check(abi.lib.carma_knn_set_bit_schema(knn.handle, schema.ctypes.data))
+    d_rows = torch.from_numpy(words.view(np.uint8)).to("cuda")
+    d_b = torch.empty(4096, dtype=torch.int32, device="cuda")
+    d_by = torch.empty(4096, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+
+    def step():
+        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_BITPACKED, None, 0, 4096,
+                                                   d_b.data_ptr(), d_by.data_ptr(), None, None, s.cuda_stream))
+    for _ in range(5):
+        step()
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        step()
+    e1.record(s)
+    torch.cuda.synchronize()
+    dev_ms = e0.elapsed_time(e1) / reps
+    h_b = np.zeros(4096, np.int32)
+    h_by = np.zeros(4096, np.uint64)
+    for _ in range(3):
+        knn.predict_bitpacked(words, schema, 4096)
+    t = time.perf_counter()
+    for _ in range(reps):
+        h_b, h_by = knn.predict_bitpacked(words, schema, 4096)
+    e2e_ms = (time.perf_counter() - t) / reps * 1e3
+    assert np.array_equal(h_b, d_b.cpu().numpy())
+    c1 = {"workload": "c1: GPUMemNet MLP k-NN over 4096 MLP feature vectors (seed 12345), model seed 11",
+          "unit": "ms per 4096-row batch", "device_ms": dev_ms, "e2e_ms": e2e_ms,
+          "estimates_per_s": 4096 / (dev_ms * 1e-3), "e2e_estimates_per_s": 4096 / (e2e_ms * 1e-3)}
+    if ref is not None:
+        ck = ctypes.c_uint64()
+        ref.ref_bench_predict(0, 4000, 11, 5, 4096, 12345, 1, 1, ctypes.byref(ck))  # model cache
+        cpu_s = ref.ref_bench_predict(0, 4000, 11, 5, 4096, 12345, 1, 3, ctypes.byref(ck)) / 3
+        c1["cpu_baseline"] = {"value": cpu_s * 1e3, "unit": "ms per 4096-row batch", "cores": 1,
+                              "kind": "reference", "sample": "the same 4096 rows, estimate_learned, 1 thread"}
+    out["c1"] = c1
+    knn.close()
+    # ---- c3
+    c3 = {"workload": "c3: one t90 trace (seed 1) on an 8-GPU server, MAGM u=0.8, MPS, W=60 s; "
+                      "estimator none and learned", "unit": "ms per trace replay"}
+    for est in ("none", "learned"):
+        rc = cb.RunConfig(mix="t90", trace_seed=1,
+                          policy=cb.PolicyConfig(policy="magm", max_smact=0.8, estimator=est),
+                          constants=cb.SimConstants(gpu_count=8))
+        mt = cb.materialize_trace(cb.generate_trace("t90", 1))
+        cb.provision_estimates(rc, mt, dev)
+        cfg = cb.make_config(rc.policy, rc.constants)
+        plan = cb.ReplayPlan(cfg, mt.tasks, np.array([0, len(mt.tasks)], np.uint64), np.zeros(1, abi.job_dtype), dev)
+        for _ in range(3):
+            plan.run()
+        km, rm = ctypes.c_double(), ctypes.c_double()
+        runs = []
+        for _ in range(10):
+            plan.run()
+            abi.check(abi.lib.carma_replay_plan_timing(plan._h, ctypes.byref(km), ctypes.byref(rm)))
+            runs.append(rm.value)
+        r = plan.results().traces[0]
+        plan.close()
+        t = time.perf_counter()
+        for _ in range(10):
+            cb.replay(cfg, [mt.tasks])
+        e2e_ms = (time.perf_counter() - t) / 10 * 1e3
+        c3[est] = {"device_ms": statistics.median(runs), "e2e_ms": e2e_ms, "oom_count": int(r["oom_count"]),
+                   "events": int(r["events"])}
+        if ref is not None:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from oracle_bind import ref_config, ref_run
+            rcfg = ref_config(policy="magm", estimator=est, gpu_count=8)
+            ref_run(ref, rcfg, mix="t90", seed=1)
+            t = time.perf_counter()
+            for _ in range(5):
+                ref_run(ref, rcfg, mix="t90", seed=1)
+            c3[est]["cpu_baseline_ms"] = (time.perf_counter() - t) / 5 * 1e3
+    c3["note"] = ("a single 90-task trace is one warp of sequential events: GPU latency is launch-bound; the "
+                  "learned CPU run includes in-process estimator training, the GPU run is given estimates")
+    out["c3"] = c3
+    return out
+
+
 def run_reference(args, d: Dist):
     if d.rank != 0:
         return
@@ -320,16 +415,18 @@ def run_carma(args, d: Dist):
     for f in (1, 2):
         knn.set_model(cb.fit_knn(f, 4000, MODEL_SEEDS[f], 5))
     log(f"[rank {d.rank}] knn inputs {Q} rows in {time.time() - t0:.1f}s; fp64 probe {fp64.value / 1e12:.2f} TF/s")
-    # 64-byte packed rows (lossless, family inside; include/carma_gpu.h)
-    packed, table = cb.pack_features(rows, fam)
-    abi.check(abi.lib.carma_knn_set_act_table(knn.handle, table.ctypes.data))
+    # Bit-packed rows (lossless frame-of-reference packing, family inside;
+    # include/carma_gpu.h): 36 B/row on this batch instead of 136 B.
+    words, schema = cb.pack_features_bits(rows, fam)
+    abi.check(abi.lib.carma_knn_set_bit_schema(knn.handle, schema.ctypes.data))
+    wpr = int(schema["words_per_row"][0])
     stream = torch.cuda.current_stream()
-    d_rows = torch.from_numpy(packed.view(np.uint8).reshape(-1)).to("cuda")
+    d_rows = torch.from_numpy(words.view(np.uint8)).to("cuda")
     d_b = torch.empty(Q, dtype=torch.int32, device="cuda")
     d_by = torch.empty(Q, dtype=torch.int64, device="cuda")
 
     def knn_step():
-        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_PACKED, None, 1, Q,
+        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_BITPACKED, None, 1, Q,
                                                    d_b.data_ptr(), d_by.data_ptr(), None, None, stream.cuda_stream))
 
     search_ms, pipe_ms = [], []
@@ -363,15 +460,15 @@ def run_carma(args, d: Dist):
     visits = e32_.value
     value = N * Q / (knn_ms * 1e-3)
 
-    # e2e: pinned host packed rows -> carma_knn_predict_packed (chunked H2D /
-    # compute / D2H on two streams) -> pinned host buckets + bytes
-    h_rows = torch.from_numpy(packed.view(np.uint8).reshape(-1)).pin_memory().numpy().view(packed.dtype)
+    # e2e: pinned host bit-packed rows -> carma_knn_predict_bitpacked (chunked
+    # H2D / compute / D2H on two streams) -> pinned host buckets + bytes
+    h_rows = torch.from_numpy(words.view(np.uint8)).pin_memory().numpy().view(np.uint32)
     h_b = torch.empty(Q, dtype=torch.int32).pin_memory().numpy()
     h_by = torch.empty(Q, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
 
     def e2e_step():
-        abi.check(abi.lib.carma_knn_predict_packed(knn.handle, h_rows.ctypes.data, table.ctypes.data, Q,
-                                                   h_b.ctypes.data, h_by.ctypes.data))
+        abi.check(abi.lib.carma_knn_predict_bitpacked(knn.handle, h_rows.ctypes.data, schema.ctypes.data, Q,
+                                                      h_b.ctypes.data, h_by.ctypes.data))
 
     for _ in range(max(1, args.warmup - 1)):
         e2e_step()
@@ -382,7 +479,16 @@ def run_carma(args, d: Dist):
     e2e_s = d.max((time.perf_counter() - t) / args.steps)
     d.barrier()
     assert np.array_equal(h_b, b_dev), "host-API and device-resident predictions differ"
-    # the 136-byte FeatureVector-row host API, once, for reference
+    # the other host formats, warm, once each: 64-B packed rows and the
+    # 136-B FeatureVector rows
+    packed, table = cb.pack_features(rows, fam)
+    h_pk = torch.from_numpy(packed.view(np.uint8).reshape(-1)).pin_memory().numpy().view(packed.dtype)
+    for _ in range(2):
+        t = time.perf_counter()
+        abi.check(abi.lib.carma_knn_predict_packed(knn.handle, h_pk.ctypes.data, table.ctypes.data, Q,
+                                                   h_b.ctypes.data, h_by.ctypes.data))
+        e2e_pk_s = time.perf_counter() - t
+    assert np.array_equal(h_b, b_dev)
     h_full = torch.from_numpy(rows.view(np.uint8).reshape(-1)).pin_memory().numpy().view(rows.dtype)
     h_fam = torch.from_numpy(fam).pin_memory().numpy()
     for _ in range(2):  # warm-up: scratch sized for 136-B rows
@@ -391,7 +497,8 @@ def run_carma(args, d: Dist):
                                             h_b.ctypes.data, h_by.ctypes.data))
         e2e_full_s = time.perf_counter() - t
     assert np.array_equal(h_b, b_dev)
-    del d_rows, d_b, d_by, h_full, h_fam
+    del d_rows, d_b, d_by, h_full, h_fam, h_pk
+    abi.check(abi.lib.carma_knn_set_act_table(knn.handle, table.ctypes.data))
 
     search_avg = statistics.mean(search_ms)
     # executed work of the exact pruned search: fp32 pre-filter evaluations
@@ -517,6 +624,10 @@ def run_carma(args, d: Dist):
                 fused["cpu_baseline"] = {"value": frate, "unit": "placed tasks/s", "cores": 1, "kind": "reference",
                                          "sample": fsample}
 
+    small = None
+    if d.rank == 0 and N == 1 and not args.skip_small:
+        small = small_configs(cb, abi, dev, None if args.skip_cpu else ref_lib())
+
     if d.rank != 0:
         return
     hbm = peaks().get("hbm_gbs")
@@ -529,7 +640,8 @@ def run_carma(args, d: Dist):
         "e2e": {"value": N * Q / e2e_s, "unit": "estimates/s",
                 "h2d_bytes_per_step": int(h_rows.nbytes),
                 "d2h_bytes_per_step": int(h_b.nbytes + h_by.nbytes),
-                "api": "carma_knn_predict_packed (64 B packed rows, pinned host buffers)",
+                "api": f"carma_knn_predict_bitpacked ({4 * wpr} B bit-packed rows, pinned host buffers)",
+                "packed64_api_estimates_per_s": N * Q / e2e_pk_s,
                 "feature_row_api_estimates_per_s": N * Q / e2e_full_s},
         "gpu_launches": int(launches) * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved / 1e12, "peak": fp32.value / 1e12, "unit": "TFLOP/s",
@@ -550,6 +662,7 @@ def run_carma(args, d: Dist):
         "clocks": clocks,
         "replay": replay,
         "fused": fused,
+        "small_configs": small,
     }
     print(json.dumps(line))
 
@@ -564,6 +677,7 @@ def main():
     ap.add_argument("--skip-replay", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-fused", action="store_true")
+    ap.add_argument("--skip-small", action="store_true")
     ap.add_argument("--fused-tasks", type=int, default=1_000_000)
     ap.add_argument("--fused-cpu-tasks", type=int, default=20_000)
     args = ap.parse_args()

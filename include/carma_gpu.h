@@ -102,6 +102,31 @@ carma_status carma_pack_features(const carma_feature_row* rows, const int8_t* fa
                                  int32_t default_family, uint64_t n, double* act_table,
                                  carma_feature_packed* out);
 
+/* Frame-of-reference bit packing for bulk transfers: per batch, each field is
+ * stored as (value - base) in `width` bits at bit `offset` of a row of
+ * words_per_row little-endian u32 words; constant fields cost 0 bits. Field
+ * order: 0 n_linear, 1 n_batchnorm, 2 n_dropout, 3 n_conv, 4 batch_size,
+ * 5 total_params, 6 total_activations, 7 activation code, 8-10 kind[0..2],
+ * 11 has_layers, 12 tuple_acts[0], 13 tuple_params[0], 14 tuple_acts[1],
+ * 15 tuple_params[1], 16 tuple_acts[2], 17 tuple_params[2], 18 family.
+ * Every field must fit in 48 bits after the base is removed. */
+#define CARMA_ROWS_BITPACKED 3
+#define CARMA_BIT_FIELDS 19
+typedef struct carma_bit_schema {
+    uint32_t words_per_row;
+    uint32_t reserved;
+    uint8_t width[CARMA_BIT_FIELDS + 1];
+    uint16_t offset[CARMA_BIT_FIELDS + 1];
+    uint64_t base[CARMA_BIT_FIELDS + 1];
+    double act_table[16];
+} carma_bit_schema;
+
+/* Builds the schema for n rows (pass words == NULL to size: *n_words gets
+ * n * words_per_row + 2 padding words), then encodes the rows. */
+carma_status carma_pack_features_bits(const carma_feature_row* rows, const int8_t* family,
+                                      int32_t default_family, uint64_t n, carma_bit_schema* schema,
+                                      uint32_t* words, uint64_t* n_words);
+
 carma_status carma_knn_create(int device, carma_knn** out);
 carma_status carma_knn_destroy(carma_knn* h);
 /* Installs the model of one family: min/max bounds, the n normalised training
@@ -126,6 +151,12 @@ carma_status carma_knn_predict(carma_knn* h, const carma_feature_row* rows,
 carma_status carma_knn_predict_packed(carma_knn* h, const carma_feature_packed* rows,
                                       const double* act_table, uint64_t q,
                                       int32_t* bucket_out, uint64_t* bytes_out);
+/* Same over bit-packed rows (the family of each row is in the packing). */
+carma_status carma_knn_predict_bitpacked(carma_knn* h, const uint32_t* words,
+                                         const carma_bit_schema* schema, uint64_t q,
+                                         int32_t* bucket_out, uint64_t* bytes_out);
+/* Schema used by CARMA_ROWS_BITPACKED device calls. */
+carma_status carma_knn_set_bit_schema(carma_knn* h, const carma_bit_schema* schema);
 /* Same over raw 19-feature rows (predict_scalar). */
 carma_status carma_knn_predict_scalar(carma_knn* h, const double* raw, const int8_t* family,
                                       int32_t default_family, uint64_t q,

@@ -26,7 +26,7 @@ FAMILY = {"mlp": 0, "cnn": 1, "transformer": 2}
 ESTIMATOR = {"none": 0, "oracle": 1, "analytical": 2, "static_graph": 3, "learned": 4}
 MIX = {"t90": 0, "t60": 1}
 NO_ESTIMATE = np.uint64(0xFFFFFFFFFFFFFFFF)
-ROWS_FEATURES, ROWS_SCALAR, ROWS_PACKED = 0, 1, 2
+ROWS_FEATURES, ROWS_SCALAR, ROWS_PACKED, ROWS_BITPACKED = 0, 1, 2, 3
 GiB = 1 << 30
 MiB = 1 << 20
 
@@ -38,6 +38,11 @@ feature_row_dtype = np.dtype([
 ], align=True)
 
 feature_packed_dtype = np.dtype([("w", "<u8", (8,))])
+
+bit_schema_dtype = np.dtype([
+    ("words_per_row", "<u4"), ("reserved", "<u4"), ("width", "u1", (20,)), ("offset", "<u2", (20,)),
+    ("base", "<u8", (20,)), ("act_table", "<f8", (16,)),
+], align=True)
 
 task_outcome_dtype = np.dtype([
     ("final_dispatch", "<f8"), ("complete", "<f8"), ("ooms", "<u4"), ("attempts", "<u4"),
@@ -109,6 +114,9 @@ SIGNATURES = {
     "carma_knn_predict_packed": (c_int, [c_void_p, P, P, c_uint64, P, P]),
     "carma_knn_set_act_table": (c_int, [c_void_p, P]),
     "carma_pack_features": (c_int, [P, P, c_int32, c_uint64, P, P]),
+    "carma_pack_features_bits": (c_int, [P, P, c_int32, c_uint64, P, P, POINTER(c_uint64)]),
+    "carma_knn_predict_bitpacked": (c_int, [c_void_p, P, P, c_uint64, P, P]),
+    "carma_knn_set_bit_schema": (c_int, [c_void_p, P]),
     "carma_replay_plan_upload_tasks": (c_int, [c_void_p, P]),
     "carma_replay_plan_outcomes": (c_int, [c_void_p, P, P, P]),
     "carma_knn_predict_device": (c_int, [c_void_p, P, c_int32, P, c_int32, c_uint64, P, P, P, P, c_void_p]),

@@ -160,6 +160,20 @@ def pack_features(rows: np.ndarray, family=None, default_family: int = 0):
     return out, table
 
 
+def pack_features_bits(rows: np.ndarray, family=None, default_family: int = 0):
+    """Frame-of-reference bit-packed rows: (u32 words incl. 2 padding words, schema)."""
+    rows = np.ascontiguousarray(rows, abi.feature_row_dtype)
+    fam = None if family is None else np.ascontiguousarray(family, np.int8)
+    schema = np.zeros(1, abi.bit_schema_dtype)
+    nw = ctypes.c_uint64()
+    check(lib.carma_pack_features_bits(ptr(rows), ptr(fam), default_family, len(rows), ptr(schema), None,
+                                       ctypes.byref(nw)))
+    words = np.zeros(nw.value, np.uint32)
+    check(lib.carma_pack_features_bits(ptr(rows), ptr(fam), default_family, len(rows), ptr(schema), ptr(words),
+                                       ctypes.byref(nw)))
+    return words, schema
+
+
 def scalar_features(rows: np.ndarray) -> np.ndarray:
     out = np.zeros((len(rows), 19), np.float64)
     rows = np.ascontiguousarray(rows)
@@ -244,6 +258,13 @@ class GpuKnn:
         nbytes = np.zeros(q, np.uint64)
         check(lib.carma_knn_predict_packed(self._h, ptr(np.ascontiguousarray(packed)), ptr(table), q, ptr(bucket),
                                            ptr(nbytes)))
+        return bucket, nbytes
+
+    def predict_bitpacked(self, words: np.ndarray, schema: np.ndarray, q: int):
+        bucket = np.zeros(q, np.int32)
+        nbytes = np.zeros(q, np.uint64)
+        check(lib.carma_knn_predict_bitpacked(self._h, ptr(np.ascontiguousarray(words, np.uint32)), ptr(schema), q,
+                                              ptr(bucket), ptr(nbytes)))
         return bucket, nbytes
 
     def last_stats(self):

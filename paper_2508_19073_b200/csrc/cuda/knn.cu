@@ -74,6 +74,11 @@ struct ModelDev {
 struct KnnParams {
     ModelDev m[CARMA_FAMILIES];
     double act[16];  // packed rows: (cos, sin) per activation code
+    // bit-packed rows (CARMA_ROWS_BITPACKED)
+    uint64_t bbase[CARMA_BIT_FIELDS];
+    uint16_t boff[CARMA_BIT_FIELDS];
+    uint8_t bw[CARMA_BIT_FIELDS];
+    uint32_t bwpr;
     const void* rows;
     int32_t format;
     const int8_t* family;
@@ -129,7 +134,45 @@ __device__ __forceinline__ void featurize_packed(const KnnParams& p, const carma
     raw[18] = __dadd_rn(__dmul_rn(16.0, raw[5]), __dmul_rn(__dmul_rn(4.0, raw[4]), raw[6]));
 }
 
+// Field f of a bit-packed row: base + the width-bit value at its offset.
+__device__ __forceinline__ uint64_t bit_field(const KnnParams& p, const uint32_t* row, int f) {
+    const uint32_t w = p.bw[f];
+    if (w == 0) return p.bbase[f];
+    const uint32_t off = p.boff[f];
+    const uint32_t* q = row + (off >> 5);
+    const uint32_t sh = off & 31;
+    uint64_t v = (static_cast<uint64_t>(__ldg(q + 1)) << 32) | __ldg(q);
+    v >>= sh;
+    if (sh + w > 64) v |= static_cast<uint64_t>(__ldg(q + 2)) << (64 - sh);
+    return p.bbase[f] + (v & ((1ull << w) - 1ull));
+}
+
+__device__ __forceinline__ const uint32_t* bit_row(const KnnParams& p, uint64_t i) {
+    return static_cast<const uint32_t*>(p.rows) + i * p.bwpr;
+}
+
+__device__ __forceinline__ void featurize_bits(const KnnParams& p, const uint32_t* r, double* raw) {
+#pragma unroll
+    for (int f = 0; f < 7; ++f) raw[f] = u2d(bit_field(p, r, f));
+    const int code = static_cast<int>(bit_field(p, r, 7)) & 7;
+    raw[7] = p.act[2 * code];
+    raw[8] = p.act[2 * code + 1];
+    const bool h = bit_field(p, r, 11) != 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        raw[9 + 3 * k] = h ? static_cast<double>(static_cast<int32_t>(bit_field(p, r, 8 + k))) : 0.0;
+        raw[10 + 3 * k] = h ? u2d(bit_field(p, r, 12 + 2 * k)) : 0.0;
+        raw[11 + 3 * k] = h ? u2d(bit_field(p, r, 13 + 2 * k)) : 0.0;
+    }
+    raw[18] = __dadd_rn(__dmul_rn(16.0, raw[5]), __dmul_rn(__dmul_rn(4.0, raw[4]), raw[6]));
+}
+
 __device__ __forceinline__ double raw18_of(const KnnParams& p, uint64_t i) {
+    if (p.format == CARMA_ROWS_BITPACKED) {
+        const uint32_t* r = bit_row(p, i);
+        return __dadd_rn(__dmul_rn(16.0, u2d(bit_field(p, r, 5))),
+                         __dmul_rn(__dmul_rn(4.0, u2d(bit_field(p, r, 4))), u2d(bit_field(p, r, 6))));
+    }
     if (p.format == CARMA_ROWS_SCALAR) return static_cast<const double*>(p.rows)[i * kDims + 18];
     if (p.format == CARMA_ROWS_PACKED) {
         const carma_feature_packed* r = static_cast<const carma_feature_packed*>(p.rows) + i;
@@ -149,7 +192,9 @@ __device__ __forceinline__ double normalize(double raw, double lo, double hi) {
 __device__ __forceinline__ int family_of(const KnnParams& p, uint64_t i) {
     const int f = p.format == CARMA_ROWS_PACKED
                       ? static_cast<int>((static_cast<const carma_feature_packed*>(p.rows)[i].w[4] >> 48) & 0xff)
-                      : (p.family ? static_cast<int>(p.family[i]) : p.default_family);
+                      : p.format == CARMA_ROWS_BITPACKED
+                            ? static_cast<int>(bit_field(p, bit_row(p, i), 18))
+                            : (p.family ? static_cast<int>(p.family[i]) : p.default_family);
     return (f >= 0 && f < CARMA_FAMILIES && p.m[f].present) ? f : -1;
 }
 
@@ -364,6 +409,8 @@ __global__ void __launch_bounds__(128, 4)
                     for (int d = 0; d < kDims; ++d) raw[d] = r[d];
                 } else if (p.format == CARMA_ROWS_PACKED) {
                     featurize_packed(p, static_cast<const carma_feature_packed*>(p.rows)[row], raw);
+                } else if (p.format == CARMA_ROWS_BITPACKED) {
+                    featurize_bits(p, bit_row(p, row), raw);
                 } else {
                     featurize(static_cast<const carma_feature_row*>(p.rows)[row], raw);
                 }
@@ -656,6 +703,8 @@ __global__ void __launch_bounds__(128, 4)
                         for (int d = 0; d < kDims; ++d) raw[d] = r[d];
                     } else if (p.format == CARMA_ROWS_PACKED) {
                         featurize_packed(p, static_cast<const carma_feature_packed*>(p.rows)[row], raw);
+                    } else if (p.format == CARMA_ROWS_BITPACKED) {
+                        featurize_bits(p, bit_row(p, row), raw);
                     } else {
                         featurize(static_cast<const carma_feature_row*>(p.rows)[row], raw);
                     }
@@ -952,6 +1001,7 @@ struct KnnHandle {
     } scratch[2];
     DeviceBuffer evals;
     double act[16] = {0};
+    carma_bit_schema schema{};
     int path = 0;  // 0 auto (fp32 pre-filter when every model allows it), 1 exact fp64 blocks, 2 fp32 pre-filter
     uint64_t last_visits = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // pipeline start, search start, search end
@@ -965,6 +1015,12 @@ namespace {
 KnnParams make_params(const KnnHandle& h, uint32_t* n_bins) {
     KnnParams p{};
     std::memcpy(p.act, h.act, sizeof(p.act));
+    for (int f = 0; f < CARMA_BIT_FIELDS; ++f) {
+        p.bbase[f] = h.schema.base[f];
+        p.boff[f] = h.schema.offset[f];
+        p.bw[f] = h.schema.width[f];
+    }
+    p.bwpr = h.schema.words_per_row;
     uint32_t base = 0;
     for (int f = 0; f < CARMA_FAMILIES; ++f) {
         const HostModel& hm = h.model[f];
@@ -1081,7 +1137,7 @@ void check_ready(const KnnHandle* h) {
 
 carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int32_t format,
                           const int8_t* family, int32_t default_family, uint64_t q,
-                          int32_t* bucket_out, uint64_t* bytes_out) {
+                          int32_t* bucket_out, uint64_t* bytes_out, size_t tail_bytes = 0) {
     return guarded([&] {
         KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
         check_ready(h);
@@ -1104,7 +1160,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
             cudaStream_t s = h->pipe[c & 1];
             const uint64_t beg = c * chunk, cnt = std::min(chunk, q - beg);
             const char* src = static_cast<const char*>(rows) + beg * row_bytes;
-            sc.rows.ensure(chunk * row_bytes);
+            sc.rows.ensure(chunk * row_bytes + tail_bytes);
             sc.bucket.ensure(chunk * 4);
             sc.bytes.ensure(chunk * 8);
             if (family) sc.family.ensure(chunk);
@@ -1112,15 +1168,15 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
                 // Stage through pinned memory; wait until this buffer's previous
                 // chunk has been consumed.
                 CARMA_CUDA(cudaStreamSynchronize(s));
-                sc.stage_rows.ensure(chunk * row_bytes);
-                std::memcpy(sc.stage_rows.ptr, src, cnt * row_bytes);
+                sc.stage_rows.ensure(chunk * row_bytes + tail_bytes);
+                std::memcpy(sc.stage_rows.ptr, src, cnt * row_bytes + tail_bytes);
                 src = sc.stage_rows.as<char>();
                 if (family) {
                     sc.stage_family.ensure(chunk);
                     std::memcpy(sc.stage_family.ptr, family + beg, cnt);
                 }
             }
-            CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, src, cnt * row_bytes, cudaMemcpyHostToDevice, s));
+            CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, src, cnt * row_bytes + tail_bytes, cudaMemcpyHostToDevice, s));
             if (family)
                 CARMA_CUDA(cudaMemcpyAsync(sc.family.ptr,
                                            (!rows_pinned || !fam_pinned) ? sc.stage_family.as<int8_t>() : family + beg,
@@ -1322,6 +1378,26 @@ carma_status carma_knn_predict_packed(carma_knn* hh, const carma_feature_packed*
                         bytes_out);
 }
 
+carma_status carma_knn_set_bit_schema(carma_knn* hh, const carma_bit_schema* schema) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        if (!h || !schema) throw InvalidArg("null argument");
+        if (schema->words_per_row == 0) throw InvalidArg("schema has no words per row");
+        for (int f = 0; f < CARMA_BIT_FIELDS; ++f)
+            if (schema->width[f] > 48) throw InvalidArg("schema field wider than 48 bits");
+        h->schema = *schema;
+        std::memcpy(h->act, schema->act_table, sizeof(h->act));
+    });
+}
+
+carma_status carma_knn_predict_bitpacked(carma_knn* hh, const uint32_t* words, const carma_bit_schema* schema,
+                                         uint64_t q, int32_t* bucket_out, uint64_t* bytes_out) {
+    const carma_status st = carma_knn_set_bit_schema(hh, schema);
+    if (st != CARMA_OK) return st;
+    return predict_host(hh, words, 4ull * schema->words_per_row, CARMA_ROWS_BITPACKED, nullptr, 0, q, bucket_out,
+                        bytes_out, 8);
+}
+
 carma_status carma_knn_predict_scalar(carma_knn* h, const double* raw, const int8_t* family,
                                       int32_t default_family, uint64_t q, int32_t* bucket_out,
                                       uint64_t* bytes_out) {
@@ -1336,8 +1412,7 @@ carma_status carma_knn_predict_device(carma_knn* hh, const void* rows, int32_t f
     return guarded([&] {
         KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
         check_ready(h);
-        if (format != CARMA_ROWS_FEATURES && format != CARMA_ROWS_SCALAR && format != CARMA_ROWS_PACKED)
-            throw InvalidArg("unknown row format");
+        if (format < CARMA_ROWS_FEATURES || format > CARMA_ROWS_BITPACKED) throw InvalidArg("unknown row format");
         if (q == 0) return;
         if (!rows) throw InvalidArg("rows is null");
         std::lock_guard<std::mutex> lock(h->mu);

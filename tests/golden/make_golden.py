@@ -50,6 +50,16 @@ def main():
         knn[f"bucket_{fam}"] = b
         knn[f"bytes_{fam}"] = by
     knn["cases"] = np.array(KNN_CASES, np.int64)
+    # holdout report of train_learned_estimator (estimators.cpp:396-434):
+    # accuracy, macro_f1, underestimate_rate per case model
+    for fam, mseed, _, _ in KNN_CASES:
+        lo, hi = np.zeros(19), np.zeros(19)
+        pts, lab = np.zeros((4000, 19)), np.zeros(4000, np.int32)
+        n, br, h = ctypes.c_uint64(), ctypes.c_uint64(), np.zeros(3)
+        assert ref.ref_train(fam, 4000, mseed, 5, b"/tmp/carma_golden_model.json", lo.ctypes.data, hi.ctypes.data,
+                             pts.ctypes.data, lab.ctypes.data, 4000, ctypes.byref(n), ctypes.byref(br),
+                             h.ctypes.data) == 0
+        knn[f"holdout_{fam}"] = h
     np.savez_compressed(os.path.join(HERE, "knn.npz"), **knn)
 
     out = {}

@@ -221,3 +221,34 @@ def test_fp32_prefilter_cuts_fp64_work(gpu, models):
     abi.check(abi.lib.carma_knn_last_work(knn.handle, ctypes.byref(la), ctypes.byref(e64), ctypes.byref(e32)))
     assert np.array_equal(b1, b2)
     assert e32.value > 0 and e64.value * 4 < exact_only, (e64.value, e32.value, exact_only)
+
+
+def test_bitpacked_rows_match_oracle(gpu, olib, models):
+    rows, fams, want = [], [], []
+    for f, _, qs in FAMILIES:
+        ds = cb.generate_synthetic_dataset(f, 1200, qs + 9)
+        rows.append(ds.rows)
+        fams.append(np.full(1200, f, np.int8))
+        want.append(oracle_predict(olib, models[f], cb.scalar_features(ds.rows))[0])
+    rows, fams, want = np.concatenate(rows), np.concatenate(fams), np.concatenate(want)
+    knn = cb.GpuKnn(gpu)
+    for f in models:
+        knn.set_model(models[f])
+    words, schema = cb.pack_features_bits(rows, fams)
+    b, by = knn.predict_bitpacked(words, schema, len(rows))
+    assert np.array_equal(b, want)
+
+
+@pytest.mark.parametrize("family", [0, 1, 2])
+def test_train_learned_estimator_holdout_matches_reference(gpu, family):
+    """train_learned_estimator's 30% holdout report, scored with the GPU
+    predict: accuracy, macro-F1 and underestimate rate equal the reference's
+    doubles bit for bit (estimators.cpp:396-434)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "knn.npz"))
+    fam, mseed, _, _ = (int(x) for x in g["cases"][family])
+    est = cb.train_learned_estimator(fam, 4000, mseed, 5, device=gpu)
+    want = g[f"holdout_{family}"]
+    got = np.array([est.holdout.accuracy, est.holdout.macro_f1, est.holdout.underestimate_rate])
+    assert got.tobytes() == want.tobytes(), (got, want)
+    assert est.holdout.train_size == 2800 and est.holdout.holdout_size == 1200

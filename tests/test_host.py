@@ -129,3 +129,49 @@ def test_fit_shapes_and_holdout_split():
     assert np.all(m.points[:, active] >= 0.0) and np.all(m.points[:, active] <= 1.0)
     assert np.all(m.points[:, ~active] == 0.0)
     assert m.bucket_range == 1 << 30
+
+
+def unpack_bits(words, schema, n):
+    s = schema[0]
+    wpr = int(s["words_per_row"])
+    base_idx = np.arange(n, dtype=np.int64) * wpr
+    w = words.astype(np.uint64)
+    out = np.zeros((n, 19), np.uint64)
+    for f in range(19):
+        width, off, base = int(s["width"][f]), int(s["offset"][f]), np.uint64(s["base"][f])
+        if width == 0:
+            out[:, f] = base
+            continue
+        i = base_idx + (off >> 5)
+        sh = off & 31
+        v = (w[i] | (w[i + 1] << np.uint64(32))) >> np.uint64(sh)
+        if sh + width > 64:
+            v |= w[i + 2] << np.uint64(64 - sh)
+        out[:, f] = base + (v & np.uint64((1 << width) - 1))
+    return out
+
+
+@pytest.mark.parametrize("families", [(0,), (1, 2), (0, 1, 2)])
+def test_bitpacked_format_is_lossless(families):
+    rows, fams = [], []
+    for f in families:
+        ds = cb.generate_synthetic_dataset(f, 2000, 21 + f)
+        rows.append(ds.rows)
+        fams.append(np.full(2000, f, np.int8))
+    rows, fams = np.concatenate(rows), np.concatenate(fams)
+    words, schema = cb.pack_features_bits(rows, fams)
+    n = len(rows)
+    assert len(words) == n * int(schema["words_per_row"][0]) + 2
+    v = unpack_bits(words, schema, n)
+    assert np.array_equal(v[:, 0], rows["n_linear"]) and np.array_equal(v[:, 3], rows["n_conv"])
+    assert np.array_equal(v[:, 4], rows["batch_size"]) and np.array_equal(v[:, 5], rows["total_params"])
+    assert np.array_equal(v[:, 6], rows["total_activations"])
+    table = schema["act_table"][0]
+    assert np.array_equal(table[2 * v[:, 7].astype(np.int64)], rows["act_cos"])
+    assert np.array_equal(table[2 * v[:, 7].astype(np.int64) + 1], rows["act_sin"])
+    for k in range(3):
+        assert np.array_equal(v[:, 8 + k].astype(np.int32), rows["kind"][:, k])
+        assert np.array_equal(v[:, 12 + 2 * k], rows["tuple_acts"][:, k])
+        assert np.array_equal(v[:, 13 + 2 * k], rows["tuple_params"][:, k])
+    assert np.array_equal(v[:, 18].astype(np.int8), fams)
+    assert int(schema["words_per_row"][0]) * 4 < 64  # denser than the fixed 64-byte packing
