@@ -49,7 +49,7 @@ constexpr int kScatterCtas = 296;  // 2 per SM on a 148-SM B200
 constexpr int kMaxBins = 4096;
 constexpr int kBlock = 8;  // points per frontier step
 constexpr int kF32Dims = 16;  // fp32 pre-filter: active dims per point
-constexpr int kCandCap = 16;  // fp32 pre-filter: candidate buffer per lane
+constexpr int kCandCap = 24;  // fp32 pre-filter: candidate buffer per lane
 
 struct ModelDev {
     const double* pts;    // N x 20, sorted by (p18, original index)
@@ -570,10 +570,12 @@ __global__ void __launch_bounds__(128, 4)
 // where sf is the FFMA-accumulated sum (relative error g = 17u) and g64
 // bounds the reference's own fp64 rounding. A point can enter the exact
 // top-k only if LB <= kth, tested without a sqrt as sf <= T_lb(kth). kth is
-// an upper bound of the exact k-th best: the k-th smallest UB seen so far,
-// or the exact k-th best after a flush. Surviving candidates are buffered per
-// lane and evaluated exactly in fp64 (reference arithmetic) in phase B,
-// which also runs whenever a lane's buffer fills. Queries whose magnitudes
+// an upper bound of the exact k-th best: the k-th smallest UB seen so far
+// (UB is monotone in sf, so that is UB of the k-th smallest sf, kept in a
+// branch-free sorted register array), or the exact k-th best after a flush.
+// Surviving candidates are buffered per lane and evaluated exactly in fp64
+// (reference arithmetic) in phase B, which also runs before any lane's
+// buffer could overflow. Queries whose magnitudes
 // could overflow fp32 (|q| > 1e15 or NaN) never filter (eta = inf) and so
 // are evaluated exactly on every visited point.
 // ------------------------------------------------------------------------
@@ -593,14 +595,6 @@ struct F32Bounds {
 __device__ __forceinline__ float t_lb(float kth, float eta) {
     const float r = __fadd_ru(__fsqrt_ru(__fmul_ru(kth, F32Bounds::up_g64)), eta);
     return __fmul_ru(__fmul_ru(r, r), F32Bounds::up_g);  // inf stays inf
-}
-
-// sf below which a point's UB may improve the UB top-k:
-// sf < (1-g)(sqrt(kth_ub/(1+g64)) - eta)^2; -1 when impossible.
-__device__ __forceinline__ float t_ub(float kth_ub, float eta) {
-    const float r = __fsub_rd(__fsqrt_rd(__fmul_rd(kth_ub, F32Bounds::dn_g64)), eta);
-    if (!(r > 0.0f)) return -1.0f;
-    return __fmul_rd(__fmul_rd(r, r), F32Bounds::dn_g);
 }
 
 // UB = (sqrt(sf/(1-g)) + eta)^2 (1+g64), rounded up.
@@ -632,19 +626,14 @@ __device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsign
     return r;
 }
 
-// Exact reference d2 (estimators.cpp:445-457) of point s against q in shared memory.
-__device__ __forceinline__ double exact_d2(const double* pt, const double* qs) {
-    double d2 = 0.0;
+// Sorted insert into the ascending k-smallest array a, branch-free: slot j of
+// the result is min(a[j], max(a[j-1], v)); v = +inf leaves a unchanged and
+// the -1 sentinels (slots j < K-k) never move.
+template <int K>
+__device__ __forceinline__ void sorted_insert(float (&a)[K], float v) {
 #pragma unroll
-    for (int h = 0; h < 9; ++h) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(pt) + h);
-        const double a = __dsub_rn(v.x, qs[2 * h]);
-        d2 = __dadd_rn(d2, __dmul_rn(a, a));
-        const double b = __dsub_rn(v.y, qs[2 * h + 1]);
-        d2 = __dadd_rn(d2, __dmul_rn(b, b));
-    }
-    const double a = __dmul_rn(__dsub_rn(__ldg(pt + 18), qs[18]), 64.0);
-    return __dadd_rn(d2, __dmul_rn(a, a));
+    for (int j = K - 1; j > 0; --j) a[j] = fminf(a[j], fmaxf(a[j - 1], v));
+    a[0] = fminf(a[0], v);
 }
 
 template <int K>
@@ -653,16 +642,16 @@ __global__ void __launch_bounds__(128, 4)
                    int32_t* __restrict__ bucket_out, uint64_t* __restrict__ bytes_out,
                    double* __restrict__ topk_d2, int64_t* __restrict__ topk_idx,
                    unsigned long long* __restrict__ evals) {
-    __shared__ double qsh[128][kDims + 1];
-    __shared__ uint32_t cbuf_i[128][kCandCap];
-    __shared__ float cbuf_s[128][kCandCap];
+    // Per-thread rows are stored column-major ([item][thread]) so that lanes
+    // touching their own rows never share a bank.
+    __shared__ double qsh[kDims][128];
+    __shared__ uint32_t cbuf_i[kCandCap][128];
+    __shared__ float cbuf_s[kCandCap][128];
     // per warp: the next fp32 block on the left [0] and right [1] of the frontier
     __shared__ float4 stage[4][2][kBlock * kF32Dims / 4];
     const unsigned lane = threadIdx.x & 31;
+    const unsigned tid = threadIdx.x;
     float4 (*stg)[kBlock * kF32Dims / 4] = stage[threadIdx.x >> 5];
-    double* qs = qsh[threadIdx.x];
-    uint32_t* ci = cbuf_i[threadIdx.x];
-    float* cs = cbuf_s[threadIdx.x];
     const uint64_t total_w = (p.q + 31) / 32;
     const uint64_t per_cta = (total_w + gridDim.x - 1) / gridDim.x;
     const uint64_t w_beg = per_cta * blockIdx.x;
@@ -670,6 +659,7 @@ __global__ void __launch_bounds__(128, 4)
     const unsigned wpc = blockDim.x >> 5;
     unsigned long long my_visits = 0, my_exact = 0;
     const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    const float finf = __int_as_float(0x7f800000);
 
     for (uint64_t w = w_beg + (threadIdx.x >> 5); w < w_end; w += wpc) {
         const uint64_t slot = w * 32 + lane;
@@ -716,17 +706,17 @@ __global__ void __launch_bounds__(128, 4)
 #pragma unroll
                 for (int d = 0; d < kDims; ++d) {
                     const double v = mine ? normalize(raw[d], m.lo[d], m.hi[d]) : 0.0;
-                    qs[d] = v;
+                    if (d == 18) q18 = v;
+                    qsh[d][tid] = v;
                     const double av = fabs(v);
                     qmax = (av > qmax || av != av) ? av : qmax;
                 }
-                q18 = qs[18];
                 double e2 = 0.0;
 #pragma unroll
                 for (int j = 0; j < kF32Dims; ++j) {
                     const int a = m.adim[j];
+                    const double qa = a < kDims ? qsh[a][tid] : 0.0;
                     const double w = a == 18 ? 64.0 : 1.0;
-                    const double qa = a < kDims ? qs[a] : 0.0;
                     qf[j] = a < kDims ? __double2float_rn(w * qa) : 0.0f;
                     const double ej = a < kDims ? 2.0 * 0x1.0p-24 * (1.0 + 0x1.0p-24) * w * (m.pmax[j] + fabs(qa)) + 0x1.0p-140
                                                 : 0.0;
@@ -741,22 +731,24 @@ __global__ void __launch_bounds__(128, 4)
             for (int j = 0; j < kF32Dims / 2; ++j) qf2[j] = f2pack(qf[2 * j], qf[2 * j + 1]);
             TopK<K> top;
             top.init(k);
-            // k smallest UB values (float), same sentinel layout as TopK
-            float ubv[K];
+            // k smallest fp32 sums seen (same sentinel layout as TopK). UB is
+            // monotone in sf, so ub_of(sfk[K-1]) is the k-th smallest UB.
+            float sfk[K];
 #pragma unroll
-            for (int j = 0; j < K; ++j) ubv[j] = j < K - k ? -1.0f : __int_as_float(0x7f800000);
+            for (int j = 0; j < K; ++j) sfk[j] = j < K - k ? -1.0f : finf;
             double kth = inf;  // filter bound: >= the exact k-th best
             const float etaf = __double2float_ru(eta);
-            float T_lb = t_lb(__int_as_float(0x7f800000), etaf), T_ub = t_ub(__int_as_float(0x7f800000), etaf);
+            float T_lb = t_lb(finf, etaf);
             int cnt = 0;
 
             unsigned mm = members;
             for (int j = (__popc(members) - 1) / 2; j > 0; --j) mm &= mm - 1;
             const int mid_lane = __ffs(mm) - 1;
-            const int64_t n = static_cast<int64_t>(m.n);
-            const int64_t pos = live ? static_cast<int64_t>(qpos[row]) : 0;
-            const int64_t start = __shfl_sync(0xffffffffu, pos, mid_lane);
-            int64_t L = start, R = start;
+            // model indices fit int32 (carma_knn_set_model rejects n > 2^31 - 1)
+            const int32_t n = static_cast<int32_t>(m.n);
+            const int32_t pos = live ? static_cast<int32_t>(qpos[row]) : 0;
+            const int32_t start = __shfl_sync(0xffffffffu, pos, mid_lane);
+            int32_t L = start, R = start;
             const double t_in = fmin(pos > 0 ? t18_of(__ldg(m.key18 + pos - 1), q18) : inf,
                                      pos < n ? t18_of(__ldg(m.key18 + pos), q18) : inf);
             double tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q18) : t_in) : inf;
@@ -766,21 +758,33 @@ __global__ void __launch_bounds__(128, 4)
             // each); every step then prefetches the next block on its side.
             const float4* pf4 = reinterpret_cast<const float4*>(m.ptsf);
             __syncwarp();
-            stg[0][lane] = __ldg(pf4 + (L - kBlock) * (kF32Dims / 4) + lane);
-            stg[1][lane] = __ldg(pf4 + R * (kF32Dims / 4) + lane);
+            stg[0][lane] = __ldg(pf4 + static_cast<int64_t>(L - kBlock) * (kF32Dims / 4) + lane);
+            stg[1][lane] = __ldg(pf4 + static_cast<int64_t>(R) * (kF32Dims / 4) + lane);
             __syncwarp();
 
-            // Phase B: exact fp64 evaluation of the buffered candidates that
-            // still pass the (possibly tightened) bound, then tighten kth.
+            // Phase B: exact fp64 evaluation (reference arithmetic) of the
+            // buffered candidates that still pass the (possibly tightened)
+            // bound, then tighten kth.
             auto flush = [&]() {
                 for (;;) {
                     const bool have = cnt > 0;
                     if (!__any_sync(0xffffffffu, have)) break;
                     if (have) {
                         --cnt;
-                        if (cs[cnt] <= T_lb) {
-                            const uint32_t sidx = ci[cnt];
-                            const double d2 = exact_d2(m.pts + static_cast<int64_t>(sidx) * kStride, qs);
+                        if (!(cbuf_s[cnt][tid] > T_lb)) {
+                            const uint32_t sidx = cbuf_i[cnt][tid];
+                            const double* pt = m.pts + static_cast<int64_t>(sidx) * kStride;
+                            double d2 = 0.0;
+#pragma unroll
+                            for (int h = 0; h < 9; ++h) {
+                                const double2 v = __ldg(reinterpret_cast<const double2*>(pt) + h);
+                                const double a = __dsub_rn(v.x, qsh[2 * h][tid]);
+                                d2 = __dadd_rn(d2, __dmul_rn(a, a));
+                                const double b = __dsub_rn(v.y, qsh[2 * h + 1][tid]);
+                                d2 = __dadd_rn(d2, __dmul_rn(b, b));
+                            }
+                            const double a = __dmul_rn(__dsub_rn(__ldg(pt + 18), q18), 64.0);
+                            d2 = __dadd_rn(d2, __dmul_rn(a, a));
                             top.insert(d2, __ldg(m.orig + sidx));
                             ++exact;
                         }
@@ -802,7 +806,7 @@ __global__ void __launch_bounds__(128, 4)
                 const double rl = __shfl_sync(0xffffffffu, need_l ? tl : inf, mid_lane);
                 const double rr = __shfl_sync(0xffffffffu, need_r ? tr : inf, mid_lane);
                 const bool go_left = bl != 0 && (br == 0 || rl <= rr);
-                int64_t s0;
+                int32_t s0;
                 unsigned valid;
                 if (go_left) {
                     s0 = L - kBlock;
@@ -816,8 +820,8 @@ __global__ void __launch_bounds__(128, 4)
                 // Phase A: fp32 sums for the block's 8 points, read from the
                 // staged copy; the side's next block loads meanwhile.
                 const int side = go_left ? 0 : 1;
-                const int64_t nxt = go_left ? L - kBlock : R;
-                const float4 pre = __ldg(pf4 + nxt * (kF32Dims / 4) + lane);
+                const int32_t nxt = go_left ? L - kBlock : R;
+                const float4 pre = __ldg(pf4 + static_cast<int64_t>(nxt) * (kF32Dims / 4) + lane);
                 // Two packed partial sums per point (even / odd active dims),
                 // folded at the end: any order of the 16 non-negative terms
                 // stays within the 17u accumulation bound.
@@ -847,80 +851,52 @@ __global__ void __launch_bounds__(128, 4)
                 __syncwarp();
                 stg[side][lane] = pre;
                 __syncwarp();
-                unsigned cand = 0, upd = 0;
-#pragma unroll
-                for (int c = 0; c < kBlock; ++c) {
-                    cand |= (sf[c] <= T_lb) ? (1u << c) : 0u;
-                    upd |= (sf[c] < T_ub) ? (1u << c) : 0u;
-                }
-                cand &= valid;
-                upd &= valid;
-                if (!mine) cand = upd = 0;
                 visits += static_cast<uint64_t>(__popc(valid));
-                if (upd) {  // rare: a point whose UB may improve the UB top-k
-                    while (upd) {
-                        const int c = __ffs(upd) - 1;
-                        upd &= upd - 1;
-                        float v = sf[0];
+                // Fast path: after the first blocks almost no point improves
+                // the k smallest sums or passes the bound; one min decides.
+                float mn = sf[0];
 #pragma unroll
-                        for (int j = 1; j < kBlock; ++j)
-                            if (j == c) v = sf[j];
-                        const float ub = ub_of(v, etaf);
-                        if (ub < ubv[K - 1]) {
-                            bool placed = false;
+                for (int c = 1; c < kBlock; ++c) mn = fminf(mn, sf[c]);
+                unsigned cand = 0;
+                if (mine && (mn < sfk[K - 1] || !(mn > T_lb))) {
+                    unsigned upd = 0;
+                    const float sk = sfk[K - 1];
 #pragma unroll
-                            for (int j = K - 1; j >= 0; --j) {
-                                if (placed) continue;
-                                if (j > 0 && ubv[j - 1] > ub) {
-                                    ubv[j] = ubv[j - 1];
-                                } else {
-                                    ubv[j] = ub;
-                                    placed = true;
-                                }
-                            }
+                    for (int c = 0; c < kBlock; ++c) upd |= (sf[c] < sk) ? (1u << c) : 0u;
+                    upd &= valid;
+                    if (upd) {  // the k smallest sums moved: tighten the bound
+                        do {
+                            const int c = __ffs(upd) - 1;
+                            upd &= upd - 1;
+                            float v = sf[0];
+#pragma unroll
+                            for (int j = 1; j < kBlock; ++j)
+                                if (j == c) v = sf[j];
+                            sorted_insert<K>(sfk, v);
+                        } while (upd);
+                        const float kub = ub_of(sfk[K - 1], etaf);
+                        if (static_cast<double>(kub) < kth) {
+                            kth = static_cast<double>(kub);
+                            T_lb = t_lb(kub, etaf);
                         }
                     }
-                    const float kub = ubv[K - 1];
-                    T_ub = t_ub(kub, etaf);
-                    if (static_cast<double>(kub) < kth) {
-                        kth = static_cast<double>(kub);
-                        T_lb = t_lb(kub, etaf);
-                    }
-                    cand &= 0xffu;
+#pragma unroll
+                    for (int c = 0; c < kBlock; ++c) cand |= !(sf[c] > T_lb) ? (1u << c) : 0u;
+                    cand &= valid;
+                }
+                // Keep room for a whole block in every lane's buffer.
+                if (__any_sync(0xffffffffu, cnt > kCandCap - kBlock)) {
+                    flush();
 #pragma unroll
                     for (int c = 0; c < kBlock; ++c)
-                        if (!(sf[c] <= T_lb)) cand &= ~(1u << c);
+                        if (sf[c] > T_lb) cand &= ~(1u << c);
                 }
-                // Buffer the candidates; flush (warp-wide) when a lane is full.
-                bool full = false;
-                while (cand) {
-                    const int c = __ffs(cand) - 1;
-                    cand &= cand - 1;
-                    float v = sf[0];
+                if (cand) {
 #pragma unroll
-                    for (int j = 1; j < kBlock; ++j)
-                        if (j == c) v = sf[j];
-                    ci[cnt] = static_cast<uint32_t>(s0 + c);
-                    cs[cnt] = v;
-                    ++cnt;
-                    if (cnt == kCandCap) {
-                        full = true;
-                        break;
-                    }
-                }
-                // a full lane may still hold unbuffered candidates of this block
-                if (__any_sync(0xffffffffu, full)) {
-                    flush();
-                    while (cand) {
-                        const int c = __ffs(cand) - 1;
-                        cand &= cand - 1;
-                        float v = sf[0];
-#pragma unroll
-                        for (int j = 1; j < kBlock; ++j)
-                            if (j == c) v = sf[j];
-                        if (v <= T_lb) {
-                            ci[cnt] = static_cast<uint32_t>(s0 + c);
-                            cs[cnt] = v;
+                    for (int c = 0; c < kBlock; ++c) {
+                        if ((cand >> c) & 1u) {
+                            cbuf_i[cnt][tid] = static_cast<uint32_t>(s0 + c);
+                            cbuf_s[cnt][tid] = sf[c];
                             ++cnt;
                         }
                     }
