@@ -41,7 +41,7 @@ typedef enum carma_status {
     CARMA_ERR_CUDA = 2,        /* no device, launch or copy failure */
     CARMA_ERR_OVERFLOW = 3,    /* a trace exceeded every state capacity tier */
     CARMA_ERR_FAMILY = 4,      /* FamilyMismatch: no model for a requested family */
-    CARMA_ERR_UNSUPPORTED = 5, /* a config outside the kernel's domain (e.g. MIG) */
+    CARMA_ERR_UNSUPPORTED = 5, /* a config outside the kernel's domain (e.g. > 256 blocks) */
     CARMA_ERR_INCOMPLETE = 6   /* IncompleteRun: a trace could not finish */
 } carma_status;
 
@@ -194,9 +194,11 @@ carma_status carma_knn_last_timing(carma_knn* h, double* search_ms, double* pipe
 #define CARMA_POLICY_MUG 4
 #define CARMA_MODE_STREAMS 0 /* gpu.hpp:14 */
 #define CARMA_MODE_MPS 1
-#define CARMA_MODE_MIG 2 /* not supported by the replay kernel */
+#define CARMA_MODE_MIG 2 /* replay: yes; carma_pick_batch: UNSUPPORTED (views carry no instances) */
 #define CARMA_NO_ESTIMATE UINT64_MAX
 #define CARMA_MAX_GPUS 64
+
+#define CARMA_MAX_MIG 8
 
 /* PolicyConfig (manager.hpp:29-37) + SimConstants (memory_model.hpp:11-29). */
 typedef struct carma_replay_config {
@@ -211,7 +213,17 @@ typedef struct carma_replay_config {
     uint64_t alloc_block;
     double p_idle_w, p_max_w, p_boost_w, boost_threshold;
     double oom_startup_delay;
-} carma_replay_config;
+    /* CARMA_MODE_MIG only: every GPU's static instance table (GpuDevice ctor,
+     * gpu.cpp:26-54; RunConfig::mig_instances, runner.hpp:23), filled by
+     * carma_mig_layout (carma_host.h). Instance i owns allocation blocks
+     * [mig_base[i], mig_base[i] + mig_blocks[i]) and compute share
+     * mig_fraction[i]. */
+    int32_t mig_count; /* instances per GPU; 0 outside MIG mode */
+    int32_t mig_reserved;
+    double mig_fraction[CARMA_MAX_MIG];
+    uint16_t mig_base[CARMA_MAX_MIG];
+    uint16_t mig_blocks[CARMA_MAX_MIG];
+} carma_replay_config; /* 200 bytes */
 
 /* One materialised task (TaskSpec, task.hpp:63-80) as the replay sees it. */
 typedef struct carma_task {

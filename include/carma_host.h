@@ -70,6 +70,12 @@ carma_status carma_host_fit(int32_t family, uint64_t samples, uint64_t seed, uin
                             double* lo, double* hi, double* points, int32_t* labels,
                             uint64_t cap, uint64_t* n_out, uint64_t* bucket_range,
                             uint64_t* holdout_rows, uint64_t* n_holdout);
+/* The MIG instance table of GpuDevice's constructor (gpu.cpp:26-54) for
+ * cfg->gpu_capacity / cfg->alloc_block, written into cfg->mig_*. n = 0 uses
+ * the reference default {0.5, 0.5}. ConfigError cases return INVALID; more
+ * than CARMA_MAX_MIG instances or a table that is not block aligned return
+ * UNSUPPORTED. */
+carma_status carma_mig_layout(const double* fractions, uint32_t n, carma_replay_config* cfg);
 /* scalar_features for n feature rows -> n x 19 doubles. */
 carma_status carma_host_scalar_features(const carma_feature_row* rows, uint64_t n, double* out);
 

@@ -76,9 +76,15 @@ struct Seg {
     bool used;
 };
 
+struct Resident {
+    int id;
+    double demand;
+    int inst;  // MIG instance; 0 outside MIG mode (gpu.hpp:43-47)
+};
+
 struct Gpu {
     std::vector<Seg> segs;
-    std::vector<std::pair<int, double>> residents;  // (task, demand), insertion order
+    std::vector<Resident> residents;  // insertion order
     std::vector<std::pair<double, double>> steps;
     double energy = 0.0;
     uint64_t peak = 0;
@@ -87,6 +93,7 @@ struct Gpu {
 
 struct Run {
     std::vector<int> gpus;
+    std::vector<int> insts;  // MIG instance per entry of gpus
     std::vector<uint64_t> region_off, region_size;
     double remaining = 0.0, rate = 0.0, last_update = 0.0, executed = 0.0;
     uint64_t gen = 0;
@@ -147,19 +154,26 @@ struct Sim {
             if (!x.used) s += x.size;
         return s;
     }
-    // gpu.cpp:72-114 (whole-device range: range_begin = 0, range_end = capacity)
-    bool allocate(Gpu& g, uint64_t bytes, uint64_t* off, uint64_t* size) {
+    bool mig() const { return c.mode == CARMA_MODE_MIG; }
+    uint64_t inst_base(int i) const { return static_cast<uint64_t>(c.mig_base[i]) * c.alloc_block; }
+    uint64_t inst_cap(int i) const { return static_cast<uint64_t>(c.mig_blocks[i]) * c.alloc_block; }
+    // gpu.cpp:72-114
+    bool allocate_range(Gpu& g, uint64_t range_begin, uint64_t range_end, uint64_t bytes, uint64_t* off,
+                        uint64_t* size) {
         const uint64_t want = round_up(std::max<uint64_t>(bytes, 1));
         for (size_t i = 0; i < g.segs.size(); ++i) {
             Seg s = g.segs[i];
-            if (s.used || s.size < want) continue;
-            // In whole-device mode lo == seg.offset and hi == seg end, so the
-            // carve rule reduces to: tail iff the left neighbour is used and
-            // the right neighbour is not (absent), else head (gpu.cpp:91-97).
-            const bool left_used = i > 0 && g.segs[i - 1].used;
-            const bool right_used = i + 1 < g.segs.size() && g.segs[i + 1].used;
+            if (s.used) continue;
+            const uint64_t lo = std::max(s.off, range_begin);
+            const uint64_t hi = std::min(s.off + s.size, range_end);
+            if (lo >= hi) continue;
+            if (hi - lo < want) continue;
+            // first fit picks the segment; carve from the end facing away
+            // from a live neighbour (gpu.cpp:88-97)
+            const bool left_used = i > 0 && g.segs[i - 1].used && s.off == lo;
+            const bool right_used = i + 1 < g.segs.size() && g.segs[i + 1].used && s.off + s.size == hi;
             const bool tail = left_used && !right_used;
-            const uint64_t place = tail ? s.off + s.size - want : s.off;
+            const uint64_t place = tail ? hi - want : lo;
             std::vector<Seg> rep;
             if (place > s.off) rep.push_back({s.off, place - s.off, false});
             rep.push_back({place, want, true});
@@ -172,6 +186,31 @@ struct Sim {
             return true;
         }
         return false;
+    }
+    // gpu.cpp:151-167
+    uint64_t instance_free(const Gpu& g, int i) const {
+        uint64_t sum = 0;
+        for (const auto& x : g.segs) {
+            if (x.used) continue;
+            const uint64_t lo = std::max(x.off, inst_base(i));
+            const uint64_t hi = std::min(x.off + x.size, inst_base(i) + inst_cap(i));
+            if (lo < hi) sum += hi - lo;
+        }
+        return sum;
+    }
+    bool instance_idle(const Gpu& g, int i) const {
+        for (const auto& r : g.residents)
+            if (r.inst == i) return false;
+        return true;
+    }
+    // manager.cpp:125-134
+    int pick_instance(const Gpu& g, uint64_t need) const {
+        for (int i = 0; i < c.mig_count; ++i) {
+            if (!instance_idle(g, i)) continue;
+            if (instance_free(g, i) < std::max<uint64_t>(need, 1)) continue;
+            return i;
+        }
+        return -1;
     }
     // gpu.cpp:116-135
     void free_region(Gpu& g, uint64_t off, uint64_t size) {
@@ -189,22 +228,27 @@ struct Sim {
             return;
         }
     }
-    // gpu.cpp:183-216 (MPS / streams): per-resident rate, same for all residents.
-    double gpu_rate(const Gpu& g) const {
-        if (g.residents.empty()) return 0.0;
+    // gpu.cpp:183-216: effective rate of resident r (MIG: its instance's
+    // share; MPS: min(1, 1/sum demand); streams: 1/n).
+    double rate_of(const Gpu& g, const Resident& r) const {
+        if (mig()) return std::min(1.0, c.mig_fraction[r.inst] / r.demand);
         if (c.mode == CARMA_MODE_MPS) {
             double total = 0.0;
-            for (const auto& r : g.residents) total += r.second;
+            for (const auto& x : g.residents) total += x.demand;
             return std::min(1.0, 1.0 / total);
         }
         return 1.0 / static_cast<double>(g.residents.size());
     }
+    double task_rate(const Gpu& g, int id) const {
+        for (const auto& r : g.residents)
+            if (r.id == id) return rate_of(g, r);
+        return 0.0;
+    }
     // gpu.cpp:218-229
     double inst_smact(const Gpu& g) const {
         if (g.residents.empty()) return 0.0;
-        const double r = gpu_rate(g);
         double s = 0.0;
-        for (const auto& x : g.residents) s += x.second * r;
+        for (const auto& x : g.residents) s += x.demand * rate_of(g, x);
         return std::min(1.0, s);
     }
     // gpu.cpp:231-242
@@ -263,12 +307,12 @@ struct Sim {
         for (int g : touched) {
             record_smact(gpu[static_cast<size_t>(g)]);
             for (const auto& r : gpu[static_cast<size_t>(g)].residents)
-                affected.insert({tasks[r.first].rank, r.first});
+                affected.insert({tasks[r.id].rank, r.id});
         }
         for (const auto& [rank, id] : affected) {
             Run& r = run[static_cast<size_t>(id)];
             double rate = 1.0;
-            for (int g : r.gpus) rate = std::min(rate, gpu_rate(gpu[static_cast<size_t>(g)]));
+            for (int g : r.gpus) rate = std::min(rate, task_rate(gpu[static_cast<size_t>(g)], id));
             if (rate == r.rate && r.gen != 0) continue;
             const double dt = now - r.last_update;
             r.executed += r.rate * dt;
@@ -280,13 +324,15 @@ struct Sim {
         }
     }
     // world.cpp:73-130
-    bool place(int id, const std::vector<int>& ids) {
+    bool place(int id, const std::vector<int>& ids, const std::vector<int>& insts) {
         Run& r = run[static_cast<size_t>(id)];
         r.exists = true;
         std::vector<std::pair<uint64_t, uint64_t>> placed;
         for (size_t k = 0; k < ids.size(); ++k) {
             uint64_t off = 0, size = 0;
-            if (!allocate(gpu[static_cast<size_t>(ids[k])], tasks[id].true_mem, &off, &size)) {
+            const uint64_t lo = mig() ? inst_base(insts[k]) : 0;
+            const uint64_t hi = mig() ? lo + inst_cap(insts[k]) : c.gpu_capacity;
+            if (!allocate_range(gpu[static_cast<size_t>(ids[k])], lo, hi, tasks[id].true_mem, &off, &size)) {
                 for (size_t j = 0; j < placed.size(); ++j)
                     free_region(gpu[static_cast<size_t>(ids[j])], placed[j].first, placed[j].second);
                 return false;
@@ -294,6 +340,7 @@ struct Sim {
             placed.push_back({off, size});
         }
         r.gpus = ids;
+        r.insts = insts;
         r.region_off.clear();
         r.region_size.clear();
         for (auto& p : placed) {
@@ -303,7 +350,8 @@ struct Sim {
         r.remaining = tasks[id].work;
         r.last_update = now;
         r.resident = true;
-        for (int g : ids) gpu[static_cast<size_t>(g)].residents.push_back({id, tasks[id].demand});
+        for (size_t k = 0; k < ids.size(); ++k)
+            gpu[static_cast<size_t>(ids[k])].residents.push_back({id, tasks[id].demand, insts[k]});
         refresh_rates(ids);
         return true;
     }
@@ -320,7 +368,7 @@ struct Sim {
             Gpu& g = gpu[static_cast<size_t>(r.gpus[k])];
             free_region(g, r.region_off[k], r.region_size[k]);
             for (size_t j = 0; j < g.residents.size(); ++j)
-                if (g.residents[j].first == id) {
+                if (g.residents[j].id == id) {
                     g.residents.erase(g.residents.begin() + static_cast<std::ptrdiff_t>(j));
                     break;
                 }
@@ -343,18 +391,24 @@ struct Sim {
         }
         return e;
     }
-    // manager.cpp:136-245 (non-MIG)
-    std::vector<int> map_task(int id, bool from_recovery) {
+    // manager.cpp:136-245; inst receives the MIG instance of each chosen GPU.
+    std::vector<int> map_task(int id, bool from_recovery, std::vector<int>& inst) {
         std::vector<int> ids;
+        inst.clear();
         const size_t want = tasks[id].gpus;
         const int policy = from_recovery ? CARMA_POLICY_EXCLUSIVE : c.policy;
         if (policy == CARMA_POLICY_EXCLUSIVE) {
             for (int g = 0; g < c.gpu_count; ++g) {
                 if (!gpu[static_cast<size_t>(g)].residents.empty()) continue;
                 ids.push_back(g);
+                if (mig()) {
+                    const int i = pick_instance(gpu[static_cast<size_t>(g)], 1);
+                    inst.push_back(i < 0 ? 0 : i);
+                }
                 if (ids.size() == want) break;
             }
             if (ids.size() != want) ids.clear();
+            if (!mig()) inst.assign(ids.size(), 0);
             return ids;
         }
         const uint64_t est = tasks[id].estimate;
@@ -365,6 +419,21 @@ struct Sim {
         } else {
             el = eligible(need);
         }
+        std::map<int, int> inst_of;
+        if (mig()) {
+            std::vector<int> kept;
+            for (int g : el) {
+                const int i = pick_instance(gpu[static_cast<size_t>(g)], std::max<uint64_t>(need, 1));
+                if (i >= 0) {
+                    kept.push_back(g);
+                    inst_of[g] = i;
+                }
+            }
+            el.swap(kept);
+        }
+        auto fill_inst = [&]() {
+            for (int g : ids) inst.push_back(mig() ? inst_of[g] : 0);
+        };
         if (el.size() < want) return {};
         if (policy == CARMA_POLICY_RR) {
             for (int step = 0; step < c.gpu_count && ids.size() < want; ++step) {
@@ -373,6 +442,7 @@ struct Sim {
             }
             if (ids.size() == want) rr_cursor = (ids.back() + 1) % c.gpu_count;
             else ids.clear();
+            fill_inst();
             return ids;
         }
         std::vector<int> sorted = el;
@@ -389,6 +459,7 @@ struct Sim {
             return a < b;
         });
         ids.assign(sorted.begin(), sorted.begin() + static_cast<std::ptrdiff_t>(want));
+        fill_inst();
         return ids;
     }
     // manager.cpp:269-331
@@ -400,7 +471,8 @@ struct Sim {
         if (from_recovery) head = recovery_q.front();
         else if (!main_q.empty()) head = main_q.front();
         else return;
-        std::vector<int> ids = map_task(head, from_recovery);
+        std::vector<int> insts;
+        std::vector<int> ids = map_task(head, from_recovery, insts);
         if (ids.empty()) return;
         if (from_recovery) recovery_q.pop_front();
         else main_q.pop_front();
@@ -408,7 +480,7 @@ struct Sim {
         carma_task_result& o = out[head];
         if (o.attempts == 0) o.first_attempt = now;
         o.attempts++;
-        if (!place(head, ids)) {
+        if (!place(head, ids, insts)) {
             schedule(now + c.oom_startup_delay, CRASH, head, 0);
         } else {
             o.final_dispatch = now;

@@ -305,6 +305,9 @@ struct RefConfig {
     uint64_t estimator_seed;
     uint64_t estimator_k;
     uint64_t estimator_samples;
+    int32_t mig_count;         // RunConfig::mig_instances (runner.hpp:23)
+    int32_t mig_reserved;
+    double mig_fractions[8];
 };
 
 struct RefTaskOut {
@@ -350,6 +353,7 @@ RunConfig make_rc(const RefConfig& c) {
     rc.estimator_seed = c.estimator_seed;
     rc.estimator_k = c.estimator_k;
     rc.estimator_samples = c.estimator_samples;
+    for (int i = 0; i < c.mig_count && i < 8; ++i) rc.mig_instances.push_back(c.mig_fractions[i]);
     return rc;
 }
 

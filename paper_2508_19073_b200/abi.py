@@ -54,6 +54,8 @@ replay_config_dtype = np.dtype([
     ("gpu_capacity", "<u8"), ("alloc_block", "<u8"),
     ("p_idle_w", "<f8"), ("p_max_w", "<f8"), ("p_boost_w", "<f8"), ("boost_threshold", "<f8"),
     ("oom_startup_delay", "<f8"),
+    ("mig_count", "<i4"), ("mig_reserved", "<i4"), ("mig_fraction", "<f8", (8,)),
+    ("mig_base", "<u2", (8,)), ("mig_blocks", "<u2", (8,)),
 ], align=True)
 
 task_dtype = np.dtype([
@@ -90,7 +92,7 @@ pick_request_dtype = np.dtype([
 assert feature_row_dtype.itemsize == 136
 assert feature_packed_dtype.itemsize == 64
 assert task_outcome_dtype.itemsize == 24
-assert replay_config_dtype.itemsize == 96
+assert replay_config_dtype.itemsize == 200
 assert task_dtype.itemsize == 48
 assert task_result_dtype.itemsize == 64
 assert trace_result_dtype.itemsize == 80
@@ -149,6 +151,7 @@ SIGNATURES = {
     "carma_host_fit": (c_int, [c_int32, c_uint64, c_uint64, c_uint32, P, P, P, P, c_uint64,
                                POINTER(c_uint64), POINTER(c_uint64), P, POINTER(c_uint64)]),
     "carma_host_scalar_features": (c_int, [P, c_uint64, P]),
+    "carma_mig_layout": (c_int, [P, c_uint32, P]),
 }
 
 

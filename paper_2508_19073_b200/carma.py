@@ -362,7 +362,8 @@ class PolicyConfig:
     rr_apply_preconditions: bool = False
 
 
-def make_config(policy: PolicyConfig, consts: SimConstants) -> np.ndarray:
+def make_config(policy: PolicyConfig, consts: SimConstants, mig_instances: Optional[Sequence[float]] = None) -> np.ndarray:
+    """carma_replay_config of a PolicyConfig + SimConstants (+ RunConfig::mig_instances, runner.hpp:23)."""
     c = np.zeros(1, abi.replay_config_dtype)
     c["policy"] = abi.POLICY[policy.policy]
     c["mode"] = abi.MODE[policy.collocation_mode]
@@ -378,6 +379,9 @@ def make_config(policy: PolicyConfig, consts: SimConstants) -> np.ndarray:
     c["p_boost_w"] = consts.p_boost_w
     c["boost_threshold"] = consts.boost_threshold
     c["oom_startup_delay"] = consts.oom_startup_delay
+    if policy.collocation_mode == "mig":
+        fr = np.ascontiguousarray([] if mig_instances is None else mig_instances, np.float64)
+        check(lib.carma_mig_layout(ptr(fr) if len(fr) else None, len(fr), ptr(c)))
     return c
 
 
@@ -496,6 +500,7 @@ class RunConfig:
     estimator_seed: int = 11
     estimator_k: int = 5
     estimator_samples: int = 4000
+    mig_instances: List[float] = dataclasses.field(default_factory=list)  # fractions, mig mode only
 
 
 def provision_estimates(rc: RunConfig, m: Materialized, device: int = 0,
@@ -520,7 +525,7 @@ def run_simulation(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None)
     trace = load_trace(rc.trace_path) if rc.trace_path else generate_trace(rc.mix, rc.trace_seed)
     m = materialize_trace(trace)
     provision_estimates(rc, m, device, knn)
-    res = replay(make_config(rc.policy, rc.constants), [m.tasks], device=device)
+    res = replay(make_config(rc.policy, rc.constants, rc.mig_instances), [m.tasks], device=device)
     return res.traces[0], res.job_tasks(0), res.job_gpus(0)
 
 

@@ -1,5 +1,6 @@
 // Placement scoring shared by carma_pick_batch and the replay kernel:
-// Manager::eligible_gpus + map_task (proj/src/manager.cpp:109-245), non-MIG.
+// Manager::eligible_gpus + map_task (proj/src/manager.cpp:109-245); MIG
+// instance choice (pick_instance) is made by the caller and enters as inst_ok.
 //
 // A group of `width` lanes (a whole warp in the replay, 2..32 lanes per
 // decision in the batched kernel) scores one decision; lane l of the group
@@ -20,6 +21,7 @@ struct PickInput {
     double smact;         // windowed_smact(now, monitor_window)
     bool idle;            // no residents
     bool valid;           // g < gpu_count
+    bool inst_ok;         // MIG: pick_instance found an instance (manager.cpp:176-187); else true
 };
 
 // Lane-local helpers over a `width`-lane group inside a warp.
@@ -89,8 +91,8 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
         bool e;
         if (!in[j].valid) e = false;
         else if (policy == CARMA_POLICY_EXCLUSIVE) e = in[j].idle;
-        else if (rr_all) e = true;
-        else e = !(in[j].smact > c.max_smact) && !(in[j].free_bytes < need_floor);
+        else if (rr_all) e = in[j].inst_ok;
+        else e = in[j].inst_ok && !(in[j].smact > c.max_smact) && !(in[j].free_bytes < need_floor);
         el[j] = e;
         const unsigned b = group_bits(__ballot_sync(0xffffffffu, e), group_base, width);
         mask |= static_cast<uint64_t>(b) << (j * width);

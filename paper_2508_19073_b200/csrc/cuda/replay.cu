@@ -36,6 +36,7 @@ __global__ void pick_kernel(carma_replay_config cf, const carma_gpu_view* __rest
             carma_gpu_view v{};
             if (valid) v = views[d * n_gpus + g];
             in[j].valid = valid;
+            in[j].inst_ok = true;
             in[j].idle = v.idle != 0;
             in[j].free_bytes = v.total_free;
             in[j].smact = v.windowed_smact;
@@ -89,8 +90,8 @@ struct ReplayPlan {
     uint64_t n_tasks = 0, n_task_out = 0, n_gpu_out = 0;
     int max_g = 1;
     int max_blocks = 1;
-    uint32_t class_count[3] = {0, 0, 0};
-    int class_max_g[3] = {1, 1, 1};
+    uint32_t class_count[6] = {0, 0, 0, 0, 0, 0};
+    int class_max_g[6] = {1, 1, 1, 1, 1, 1};
     std::vector<uint32_t> class_list;  // jobs ordered: light, heavy, global-only
     DeviceBuffer d_cfgs, d_tasks, d_trace_off, d_jobs, d_task_off, d_gpu_off, d_list, d_task_out,
         d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate, d_outcomes;
@@ -108,12 +109,13 @@ using replay::Layout;
 // at <= 34 pending events and 8 residents; RR without preconditions stacks
 // up to 34 residents (11 per GPU) and ~200 pending events (stale completion
 // events stay queued: they are energy-integration breakpoints).
-template <int G> using LightL = Layout<G, 64, 32, 16, 16, 16, 2>;
-template <int G> using HeavyL = Layout<G, 320, 64, 32, 16, 16, 2>;
+// M = MIG collocation: those jobs run in their own kernels (classes 3..5).
+template <int G, bool M> using LightL = Layout<G, 64, 32, 16, 16, 16, 2, M>;
+template <int G, bool M> using HeavyL = Layout<G, 320, 64, 32, 16, 16, 2, M>;
 // Large shared-memory tier for long traces on many GPUs (c5: 10^6 tasks on
 // 64 GPUs peaks at 128 residents and ~215 pending events): one warp per CTA.
-using LargeL = Layout<64, 1024, 256, 32, 16, 128, 2>;
-using GlobalL = Layout<64, 8192, 2048, 256, 256, 4096, 4>;
+template <bool M> using LargeL = Layout<64, 1024, 256, 32, 16, 128, 2, M>;
+template <bool M> using GlobalL = Layout<64, 8192, 2048, 256, 256, 4096, 4, M>;
 
 // Configs whose policy can stack tasks without utilisation preconditions.
 bool heavy_config(const carma_replay_config& c) {
@@ -122,8 +124,8 @@ bool heavy_config(const carma_replay_config& c) {
 }
 
 void validate_config(const carma_replay_config& c) {
-    if (c.mode == CARMA_MODE_MIG) throw Unsupported("MIG collocation is not supported by the replay kernel");
-    if (c.mode != CARMA_MODE_MPS && c.mode != CARMA_MODE_STREAMS) throw InvalidArg("unknown collocation mode");
+    if (c.mode != CARMA_MODE_MPS && c.mode != CARMA_MODE_STREAMS && c.mode != CARMA_MODE_MIG)
+        throw InvalidArg("unknown collocation mode");
     if (c.policy < CARMA_POLICY_EXCLUSIVE || c.policy > CARMA_POLICY_MUG) throw InvalidArg("unknown policy");
     if (c.gpu_count < 1 || c.gpu_count > CARMA_MAX_GPUS) throw Unsupported("gpu_count must be in [1, 64]");
     if (!(c.monitor_window > 0.0)) throw InvalidArg("ConfigError: window must be > 0");
@@ -132,6 +134,19 @@ void validate_config(const carma_replay_config& c) {
         throw Unsupported("gpu_capacity must be a multiple of alloc_block");
     if (c.gpu_capacity / c.alloc_block > 64ull * replay::kMaxWords)
         throw Unsupported("more than 256 allocation blocks per GPU");
+    if (c.mode == CARMA_MODE_MIG) {
+        // the table carma_mig_layout builds (gpu.cpp:29-51)
+        if (c.mig_count < 1 || c.mig_count > CARMA_MAX_MIG)
+            throw InvalidArg("ConfigError: MIG mode needs 1..8 instances (carma_mig_layout)");
+        uint64_t end = 0;
+        for (int i = 0; i < c.mig_count; ++i) {
+            if (!(c.mig_fraction[i] > 0.0) || c.mig_fraction[i] > 1.0)
+                throw InvalidArg("ConfigError: mig instance fraction out of (0, 1]");
+            if (c.mig_base[i] != end) throw InvalidArg("ConfigError: MIG instances must tile the device in order");
+            end += c.mig_blocks[i];
+        }
+        if (end > c.gpu_capacity / c.alloc_block) throw InvalidArg("ConfigError: mig instances exceed capacity");
+    }
 }
 
 template <class L, bool SMEM>
@@ -157,17 +172,18 @@ void launch(ReplayPlan& pl, replay::Params p, int sms, int warps_per_cta = 4) {
     pl.launches++;
 }
 
-template <template <int> class LL>
+template <template <int, bool> class LL, bool M>
 void launch_shared(ReplayPlan& pl, const replay::Params& p, int max_g, int sms) {
-    if (max_g <= 4) launch<LL<4>, true>(pl, p, sms);
-    else if (max_g <= 8) launch<LL<8>, true>(pl, p, sms);
-    else if (max_g <= 16) launch<LL<16>, true>(pl, p, sms);
-    else if (max_g <= 32) launch<LL<32>, true>(pl, p, sms);
-    else launch<LL<64>, true>(pl, p, sms);
+    if (max_g <= 4) launch<LL<4, M>, true>(pl, p, sms);
+    else if (max_g <= 8) launch<LL<8, M>, true>(pl, p, sms);
+    else if (max_g <= 16) launch<LL<16, M>, true>(pl, p, sms);
+    else if (max_g <= 32) launch<LL<32, M>, true>(pl, p, sms);
+    else launch<LL<64, M>, true>(pl, p, sms);
 }
 
 // tier 0 = light shared-memory layout, 1 = heavy shared-memory, 2 = global
 // memory, 3 = large shared-memory (one warp per CTA)
+template <bool M>
 void launch_tier(ReplayPlan& pl, const replay::Params& base, const uint32_t* list_dev, uint32_t n_list, int tier,
                  int max_g, uint32_t* counters, uint32_t* retry_base) {
     replay::Params p = base;
@@ -179,10 +195,58 @@ void launch_tier(ReplayPlan& pl, const replay::Params& base, const uint32_t* lis
     CARMA_CUDA(cudaMemsetAsync(counters, 0, 8, pl.stream));
     int sms = 148;
     CARMA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl.device));
-    if (tier == 0) launch_shared<LightL>(pl, p, max_g, sms);
-    else if (tier == 1) launch_shared<HeavyL>(pl, p, max_g, sms);
-    else if (tier == 3) launch<LargeL, true>(pl, p, sms, 1);
-    else launch<GlobalL, false>(pl, p, sms);
+    if (tier == 0) launch_shared<LightL, M>(pl, p, max_g, sms);
+    else if (tier == 1) launch_shared<HeavyL, M>(pl, p, max_g, sms);
+    else if (tier == 3) launch<LargeL<M>, true>(pl, p, sms, 1);
+    else launch<GlobalL<M>, false>(pl, p, sms);
+}
+
+// One collocation group (classes cb..cb+2, jobs list[off0, ...)): the two
+// shared-memory classes, then overflowed and global-only jobs through the
+// large shared-memory tier and the global-memory tier.
+template <bool M>
+bool run_group(ReplayPlan& pl, const replay::Params& p, int cb, uint32_t off0) {
+    uint32_t* list = pl.d_list.as<uint32_t>() + off0;
+    uint32_t* retry = pl.d_list.as<uint32_t>() + pl.jobs.size() + off0;
+    uint32_t* counters = pl.d_counters.as<uint32_t>() + 2 * cb;  // class c: {next, retries}
+    uint32_t off = 0;
+    for (int cls = 0; cls < 2; ++cls) {
+        const uint32_t cnt = pl.class_count[cb + cls];
+        if (cnt) launch_tier<M>(pl, p, list + off, cnt, cls, pl.class_max_g[cb + cls], counters + 2 * cls, retry + off);
+        off += cnt;
+    }
+    if (!M) CARMA_CUDA(cudaEventRecord(pl.ev[1], pl.stream));
+    uint32_t n_retry[4] = {0, 0, 0, 0};
+    CARMA_CUDA(cudaMemcpyAsync(n_retry, counters, 16, cudaMemcpyDeviceToHost, pl.stream));
+    CARMA_CUDA(cudaStreamSynchronize(pl.stream));
+    const uint32_t c0 = pl.class_count[cb], c1 = pl.class_count[cb + 1];
+    uint32_t total = (c0 ? n_retry[1] : 0) + (c1 ? n_retry[3] : 0);
+    std::vector<uint32_t> ids(total);
+    const uint32_t r0 = c0 ? n_retry[1] : 0;
+    if (r0) CARMA_CUDA(cudaMemcpy(ids.data(), retry, r0 * 4, cudaMemcpyDeviceToHost));
+    if (total > r0) CARMA_CUDA(cudaMemcpy(ids.data() + r0, retry + c0, (total - r0) * 4, cudaMemcpyDeviceToHost));
+    // jobs that only fit the global tier
+    const auto gb = pl.class_list.begin() + off0 + c0 + c1;
+    ids.insert(ids.end(), gb, gb + pl.class_count[cb + 2]);
+    pl.retried += total;  // jobs that overflowed a shared-memory tier
+    total = static_cast<uint32_t>(ids.size());
+    const bool list_dirty = total > 0;
+    // Overflowed, global-only or begin-corrected jobs: the large shared-memory
+    // tier first, then the global-memory tier (a begin correction can follow
+    // an overflow, so up to three rounds).
+    for (int round = 0; round < 3 && total > 0; ++round) {
+        if (round > 0) pl.retried += total;
+        CARMA_CUDA(cudaMemcpy(list, ids.data(), total * 4, cudaMemcpyHostToDevice));
+        const bool large_ok = round == 0 && pl.max_blocks <= 128;
+        launch_tier<M>(pl, p, list, total, large_ok ? 3 : 2, pl.max_g, counters, retry);
+        uint32_t nr = 0;
+        CARMA_CUDA(cudaMemcpyAsync(&nr, counters + 1, 4, cudaMemcpyDeviceToHost, pl.stream));
+        CARMA_CUDA(cudaStreamSynchronize(pl.stream));
+        total = nr;
+        ids.resize(total);
+        if (total) CARMA_CUDA(cudaMemcpy(ids.data(), retry, total * 4, cudaMemcpyDeviceToHost));
+    }
+    return list_dirty;
 }
 
 void run_plan(ReplayPlan& pl) {
@@ -200,52 +264,18 @@ void run_plan(ReplayPlan& pl) {
     p.inv_scratch = pl.d_inv.as<uint32_t>();
     p.smact_begin = pl.d_begin.as<double>();
     const uint32_t n = static_cast<uint32_t>(pl.jobs.size());
-    uint32_t* list = pl.d_list.as<uint32_t>();          // [0, n): jobs grouped by class
-    uint32_t* retry = list + n;                         // [n, 2n): retry lists
-    uint32_t* counters = pl.d_counters.as<uint32_t>();  // class c: {next, retries} at [2c, 2c+1]
     pl.launches = 0;
     pl.retried = 0;
     CARMA_CUDA(cudaMemsetAsync(pl.d_begin.ptr, 0xff, n * sizeof(double), pl.stream));  // NaN: derive
+    CARMA_CUDA(cudaMemsetAsync(pl.d_counters.ptr, 0, 64, pl.stream));
     CARMA_CUDA(cudaEventRecord(pl.ev[0], pl.stream));
-    uint32_t off = 0;
-    for (int cls = 0; cls < 2; ++cls) {
-        const uint32_t cnt = pl.class_count[cls];
-        if (cnt) launch_tier(pl, p, list + off, cnt, cls, pl.class_max_g[cls], counters + 2 * cls, retry + off);
-        off += cnt;
-    }
-    CARMA_CUDA(cudaEventRecord(pl.ev[1], pl.stream));
-    uint32_t n_retry[4] = {0, 0, 0, 0};
-    CARMA_CUDA(cudaMemcpyAsync(n_retry, counters, 16, cudaMemcpyDeviceToHost, pl.stream));
-    CARMA_CUDA(cudaStreamSynchronize(pl.stream));
-    uint32_t total = (pl.class_count[0] ? n_retry[1] : 0) + (pl.class_count[1] ? n_retry[3] : 0);
-    std::vector<uint32_t> ids(total);
-    const uint32_t r0 = pl.class_count[0] ? n_retry[1] : 0;
-    if (r0) CARMA_CUDA(cudaMemcpy(ids.data(), retry, r0 * 4, cudaMemcpyDeviceToHost));
-    if (total > r0)
-        CARMA_CUDA(cudaMemcpy(ids.data() + r0, retry + pl.class_count[0], (total - r0) * 4, cudaMemcpyDeviceToHost));
-    // jobs that only fit the global tier
-    const uint32_t gbeg = pl.class_count[0] + pl.class_count[1];
-    ids.insert(ids.end(), pl.class_list.begin() + gbeg, pl.class_list.end());
-    pl.retried = total;  // jobs that overflowed a shared-memory tier
-    total = static_cast<uint32_t>(ids.size());
-    const bool list_dirty = total > 0;
-    // Overflowed, global-only or begin-corrected jobs: the large shared-memory
-    // tier first, then the global-memory tier (a begin correction can follow
-    // an overflow, so up to three rounds).
-    for (int round = 0; round < 3 && total > 0; ++round) {
-        if (round > 0) pl.retried += total;
-        CARMA_CUDA(cudaMemcpy(list, ids.data(), total * 4, cudaMemcpyHostToDevice));
-        const bool large_ok = round == 0 && pl.max_blocks <= 128;
-        launch_tier(pl, p, list, total, large_ok ? 3 : 2, pl.max_g, counters, retry);
-        uint32_t nr = 0;
-        CARMA_CUDA(cudaMemcpyAsync(&nr, counters + 1, 4, cudaMemcpyDeviceToHost, pl.stream));
-        CARMA_CUDA(cudaStreamSynchronize(pl.stream));
-        total = nr;
-        ids.resize(total);
-        if (total) CARMA_CUDA(cudaMemcpy(ids.data(), retry, total * 4, cudaMemcpyDeviceToHost));
-    }
+    const uint32_t n_std = pl.class_count[0] + pl.class_count[1] + pl.class_count[2];
+    bool dirty = false;
+    if (n_std) dirty |= run_group<false>(pl, p, 0, 0);
+    else CARMA_CUDA(cudaEventRecord(pl.ev[1], pl.stream));
+    if (n > n_std) dirty |= run_group<true>(pl, p, 3, n_std);
     CARMA_CUDA(cudaEventRecord(pl.ev[2], pl.stream));
-    if (list_dirty) CARMA_CUDA(cudaMemcpy(list, pl.class_list.data(), n * 4, cudaMemcpyHostToDevice));
+    if (dirty) CARMA_CUDA(cudaMemcpy(pl.d_list.ptr, pl.class_list.data(), n * 4, cudaMemcpyHostToDevice));
 }
 
 }  // namespace
@@ -314,11 +344,13 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
             up(pl->d_task_off, task_off.data(), n_jobs * sizeof(uint64_t));
             up(pl->d_gpu_off, gpu_off.data(), n_jobs * sizeof(uint64_t));
             std::vector<uint32_t> list(2 * static_cast<size_t>(n_jobs));
-            for (int cls = 0; cls < 3; ++cls)
+            for (int cls = 0; cls < 6; ++cls)
                 for (uint32_t i = 0; i < n_jobs; ++i) {
                     const carma_replay_config& c = configs[jobs[i].config];
-                    // > 128 allocation blocks: the shared-memory layouts hold 2 bitmap words
-                    const int jc = c.gpu_capacity / c.alloc_block > 128 ? 2 : static_cast<int>(heavy_config(c));
+                    // > 128 allocation blocks: the shared-memory layouts hold 2 bitmap words;
+                    // MIG jobs form classes 3..5 (their own kernels)
+                    const int jc = (c.gpu_capacity / c.alloc_block > 128 ? 2 : static_cast<int>(heavy_config(c))) +
+                                   (c.mode == CARMA_MODE_MIG ? 3 : 0);
                     if (jc != cls) continue;
                     pl->class_list.push_back(i);
                     pl->class_count[cls]++;
@@ -331,7 +363,7 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
             pl->d_gpu_out.ensure(go * sizeof(carma_gpu_result));
             pl->d_inv.ensure(to * 4);
             pl->d_begin.ensure(n_jobs * sizeof(double));
-            pl->d_counters.ensure(32);
+            pl->d_counters.ensure(64);
         } catch (...) {
             if (pl->stream) cudaStreamDestroy(pl->stream);
             delete pl;
@@ -488,6 +520,8 @@ carma_status carma_pick_batch(int device, const carma_replay_config* cfg, const 
     return guarded([&] {
         if (!cfg || !views || !reqs || !rr_cursor || !out_gpus) throw InvalidArg("null argument");
         if (n_gpus < 1 || n_gpus > CARMA_MAX_GPUS) throw Unsupported("n_gpus must be in [1, 64]");
+        if (cfg->mode == CARMA_MODE_MIG)
+            throw Unsupported("carma_pick_batch: MIG needs per-instance views; use the replay");
         if (n == 0) return;
         for (uint64_t i = 0; i < n; ++i)
             if (reqs[i].want < 1 || reqs[i].want > 2) throw Unsupported("want must be 1 or 2");

@@ -78,9 +78,11 @@ struct Params {
 
 // Compile-time state layout: G GPUs, H heap entries, S slots, RC residents
 // per GPU, RG SMACT ring entries per GPU, RQ recovery-queue entries.
-template <int G_, int H_, int S_, int RC_, int RG_, int RQ_, int W_>
+template <int G_, int H_, int S_, int RC_, int RG_, int RQ_, int W_, bool MIG_ = false>
 struct Layout {
     static constexpr int G = G_, H = H_, S = S_, RC = RC_, RG = RG_, RQ = RQ_, W = W_;
+    static constexpr bool MIG = MIG_;  // MIG collocation compiled in (separate kernels)
+    static constexpr size_t MI = MIG_ ? 1 : 0;
     static constexpr int GPL = (G + 31) / 32;
     static constexpr size_t al8(size_t x) { return (x + 15) / 16 * 16; }
     static constexpr size_t cfg = 0;                                   // carma_replay_config
@@ -104,21 +106,23 @@ struct Layout {
     static constexpr size_t s_dem = s_exec + 8ull * S;
     static constexpr size_t aff = s_dem + 8ull * S;                    // u64 [2 RC] x 2
     static constexpr size_t aff2 = aff + 16ull * RC;
-    static constexpr size_t nres = aff2 + 16ull * RC;                  // u32 [G] x 6
+    static constexpr size_t nres = aff2 + 16ull * RC;                  // u32 [G] x 7
     static constexpr size_t nsteps = nres + 4ull * G;
     static constexpr size_t rhead = nsteps + 4ull * G;
     static constexpr size_t rcnt = rhead + 4ull * G;
     static constexpr size_t peak = rcnt + 4ull * G;
     static constexpr size_t has_step = peak + 4ull * G;
-    static constexpr size_t hs = has_step + 4ull * G;                  // u32 [H] x 2
+    static constexpr size_t imask = has_step + 4ull * G;               // MIG: occupied instances
+    static constexpr size_t hs = imask + 4ull * G * MI;                // u32 [H] x 2
     static constexpr size_t hinfo = hs + 4ull * H;
-    static constexpr size_t s_task = hinfo + 4ull * H;                 // u32 [S] x 6
+    static constexpr size_t s_task = hinfo + 4ull * H;                 // u32 [S] x 7
     static constexpr size_t s_rank = s_task + 4ull * S;
     static constexpr size_t s_seq = s_rank + 4ull * S;
     static constexpr size_t s_gp = s_seq + 4ull * S;
     static constexpr size_t s_off = s_gp + 4ull * S;
     static constexpr size_t s_nb = s_off + 4ull * S;
-    static constexpr size_t free_stack = s_nb + 4ull * S;              // u32 [S]
+    static constexpr size_t s_inst = s_nb + 4ull * S;                  // MIG: inst0 | inst1 << 8
+    static constexpr size_t free_stack = s_inst + 4ull * S * MI;       // u32 [S]
     static constexpr size_t rq = free_stack + 4ull * S;                // u32 [RQ]
     static constexpr size_t res = rq + 4ull * RQ;                      // u16 [G][RC]
     static constexpr size_t bytes = al8(res + 2ull * G * RC);
@@ -266,19 +270,24 @@ __device__ __forceinline__ uint32_t free_blocks(const uint64_t* used, int g) {
     return f;
 }
 
-// GpuDevice::allocate_range in whole-device mode (gpu.cpp:72-114): first fit
-// over maximal free runs; carve from the tail iff the left neighbour is used
-// and the run reaches the end of the device (no right neighbour).
+// GpuDevice::allocate_range (gpu.cpp:72-114) over blocks [r0, r1): first
+// fit over the device's maximal free runs clipped to the range; carve from
+// the tail iff the run starts inside the range after a used block (left
+// neighbour used) and does not end at a used block inside the range (right
+// neighbour free or absent). The whole device is r0 = 0, r1 = nblk.
 template <class L>
-__device__ __forceinline__ int first_fit(char* b, int g, int nblk, int want) {
+__device__ __forceinline__ int first_fit(char* b, int g, int nblk, int want, int r0, int r1) {
     uint64_t* used = RP_U64(used);
     int pos = 0;
     while (pos < nblk) {
         const int start = next_bit<L>(used, g, pos, nblk, false);
-        if (start >= nblk) break;
+        if (start >= nblk || start >= r1) break;
         const int end = next_bit<L>(used, g, start, nblk, true);
-        if (end - start >= want) {
-            const int place = (start > 0 && end == nblk) ? end - want : start;
+        const int lo = start > r0 ? start : r0, hi = end < r1 ? end : r1;
+        if (lo < hi && hi - lo >= want) {
+            const bool left_used = start > 0 && start == lo;
+            const bool right_used = end < nblk && end == hi;
+            const int place = (left_used && !right_used) ? hi - want : lo;
             set_bits<L>(used, g, place, want, true);
             const uint32_t u = static_cast<uint32_t>(nblk) - free_blocks<L>(used, g);
             uint32_t* peak = RP_U32(peak);
@@ -288,6 +297,29 @@ __device__ __forceinline__ int first_fit(char* b, int g, int nblk, int want) {
         pos = end;
     }
     return -1;
+}
+
+// Free blocks in [r0, r1) (GpuDevice::instance_free, gpu.cpp:151-160).
+template <class L>
+__device__ __forceinline__ uint32_t free_in_range(const uint64_t* used, int g, int r0, int r1) {
+    uint32_t f = 0;
+#pragma unroll
+    for (int w = 0; w < L::W; ++w) {
+        const int lo = w * 64;
+        uint64_t m = ~0ull;
+        if (r0 > lo) m = r0 - lo >= 64 ? 0ull : (m & (~0ull << (r0 - lo)));
+        if (r1 < lo + 64) m = r1 <= lo ? 0ull : (m & (~0ull >> (lo + 64 - r1)));
+        f += __popcll(static_cast<long long>(~used[w * L::G + g] & m));
+    }
+    return f;
+}
+
+// MIG instance of slot on GPU g (the slot's first or second device).
+template <class L>
+__device__ __forceinline__ int inst_of(const char* b, uint32_t slot, int g) {
+    const uint32_t gp = reinterpret_cast<const uint32_t*>(b + L::s_gp)[slot];
+    const uint32_t in = reinterpret_cast<const uint32_t*>(b + L::s_inst)[slot];
+    return static_cast<int>(((gp & 0xff) == static_cast<uint32_t>(g) ? in : (in >> 8)) & 0xff);
 }
 
 // ----------------------------------------------------------------- SMACT
@@ -330,7 +362,17 @@ __device__ __forceinline__ bool refresh_gpu(char* b, int g, double now, double w
     const uint16_t* res = RP_U16(res) + g * L::RC;
     const double* dem = RP_F64(s_dem);
     double rate = 0.0, inst = 0.0;
-    if (n > 0) {
+    if (L::MIG && n > 0) {
+        // per resident min(1, f_instance / demand) (gpu.cpp:187-195); the
+        // per-GPU rate cache is unused in MIG mode
+        double sum = 0.0;
+        for (uint32_t r = 0; r < n; ++r) {
+            const uint32_t slot = res[r];
+            const double rr = dmin(1.0, __ddiv_rn(cf.mig_fraction[inst_of<L>(b, slot, g)], dem[slot]));
+            sum = __dadd_rn(sum, __dmul_rn(dem[slot], rr));
+        }
+        inst = dmin(1.0, sum);
+    } else if (n > 0) {
         if (cf.mode == CARMA_MODE_MPS) {
             double total = 0.0;
             for (uint32_t r = 0; r < n; ++r) total = __dadd_rn(total, dem[res[r]]);
@@ -464,8 +506,18 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
     for (uint32_t e = 0; e < na; ++e) {
         const uint32_t slot = static_cast<uint32_t>(aff2[e] & 0xffffffffu);
         const uint32_t g = gp[slot];
-        double rate = dmin(1.0, grate[g & 0xff]);
-        if ((g >> 16) > 1) rate = dmin(rate, grate[(g >> 8) & 0xff]);
+        double r0, r1 = 0.0;
+        if constexpr (L::MIG) {  // effective_rates (gpu.cpp:187-195)
+            const uint32_t in = RP_U32(s_inst)[slot];
+            const double d = RP_F64(s_dem)[slot];
+            r0 = dmin(1.0, __ddiv_rn(RP_CFG.mig_fraction[in & 0xff], d));
+            if ((g >> 16) > 1) r1 = dmin(1.0, __ddiv_rn(RP_CFG.mig_fraction[(in >> 8) & 0xff], d));
+        } else {
+            r0 = grate[g & 0xff];
+            if ((g >> 16) > 1) r1 = grate[(g >> 8) & 0xff];
+        }
+        double rate = dmin(1.0, r0);
+        if ((g >> 16) > 1) rate = dmin(rate, r1);
         const double old = s_rate[slot];
         if (rate == old && s_seq[slot] != kNone) continue;
         const double dt = __dsub_rn(c.now, s_last[slot]);
@@ -486,18 +538,23 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
 // slot and append the task to the resident lists.
 template <class L>
 __device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint32_t task, int g0, int g1,
-                                      int want, int nblk, unsigned lane) {
-    const uint64_t block = RP_CFG.alloc_block;
+                                      int i0, int i1, int want, int nblk, unsigned lane) {
+    const carma_replay_config& cf = RP_CFG;
+    const uint64_t block = cf.alloc_block;
     const uint64_t bytes = tk.true_mem > 0 ? tk.true_mem : 1;
     const uint64_t nb64 = (bytes + block - 1) / block;
     const int nb = nb64 > static_cast<uint64_t>(nblk) ? nblk + 1 : static_cast<int>(nb64);
+    // MIG: allocate_on_instance (gpu.cpp:67-70) inside the instance's blocks
+    constexpr bool mig = L::MIG;
+    const int a0 = mig ? cf.mig_base[i0] : 0, e0 = mig ? a0 + cf.mig_blocks[i0] : nblk;
     int off0 = -1, off1 = 0;
-    if ((g0 & 31) == static_cast<int>(lane) && nb <= nblk) off0 = first_fit<L>(b, g0, nblk, nb);
+    if ((g0 & 31) == static_cast<int>(lane) && nb <= nblk) off0 = first_fit<L>(b, g0, nblk, nb, a0, e0);
     off0 = __shfl_sync(0xffffffffu, off0, g0 & 31);
     if (off0 < 0) return false;
     if (want > 1) {
+        const int a1 = mig ? cf.mig_base[i1] : 0, e1 = mig ? a1 + cf.mig_blocks[i1] : nblk;
         int o = -1;
-        if ((g1 & 31) == static_cast<int>(lane)) o = first_fit<L>(b, g1, nblk, nb);
+        if ((g1 & 31) == static_cast<int>(lane)) o = first_fit<L>(b, g1, nblk, nb, a1, e1);
         o = __shfl_sync(0xffffffffu, o, g1 & 31);
         if (o < 0) {
             if ((g0 & 31) == static_cast<int>(lane)) set_bits<L>(RP_U64(used), g0, off0, nb, false);
@@ -523,6 +580,7 @@ __device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint
                          (static_cast<uint32_t>(want) << 16);
     RP_U32(s_off)[slot] = static_cast<uint32_t>(off0) | (static_cast<uint32_t>(off1) << 16);
     RP_U32(s_nb)[slot] = static_cast<uint32_t>(nb);
+    if (mig) RP_U32(s_inst)[slot] = static_cast<uint32_t>(i0) | (static_cast<uint32_t>(want > 1 ? i1 : 0) << 8);
     uint32_t* nres = RP_U32(nres);
     uint16_t* res = RP_U16(res);
     for (int k = 0; k < want; ++k) {
@@ -534,6 +592,7 @@ __device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint
         }
         res[g * L::RC + n] = static_cast<uint16_t>(slot);
         nres[g] = n + 1;
+        if (mig && (g & 31) == static_cast<int>(lane)) RP_U32(imask)[g] |= 1u << (k == 0 ? i0 : i1);
     }
     __syncwarp();
     return true;
@@ -568,6 +627,7 @@ __device__ __forceinline__ void finish(char* b, Sc& c, uint32_t slot, carma_task
             while (r < n && rl[r] != slot) ++r;
             for (; r + 1 < n; ++r) rl[r] = rl[r + 1];
             nres[g] = n - 1;
+            if constexpr (L::MIG) RP_U32(imask)[g] &= ~(1u << inst_of<L>(b, slot, g));
         }
     }
     const uint32_t task = RP_U32(s_task)[slot];
@@ -584,7 +644,8 @@ __device__ __forceinline__ void finish(char* b, Sc& c, uint32_t slot, carma_task
 // estimate, map_task. Returns the number of GPUs chosen (0 = no dispatch).
 template <class L>
 __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, const uint64_t* est,
-                                      uint32_t& head, bool& from_recovery, int& g0, int& g1, unsigned lane) {
+                                      uint32_t& head, bool& from_recovery, int& g0, int& g1, int& i0, int& i1,
+                                      unsigned lane) {
     const carma_replay_config& cf = RP_CFG;
     const int G = cf.gpu_count;
     const uint32_t* nres = RP_U32(nres);
@@ -601,18 +662,22 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
     else if (c.mq_head < c.arrived) head = c.mq_head;
     else return 0;
     const int policy = from_recovery ? CARMA_POLICY_EXCLUSIVE : cf.policy;
-    uint64_t floor = cf.min_free;
+    uint64_t floor = cf.min_free, need = 0;
     if (!from_recovery && cf.policy != CARMA_POLICY_EXCLUSIVE) {
         const uint64_t e = est ? est[head] : tasks[head].estimate;
         if (e != CARMA_NO_ESTIMATE) {
-            const uint64_t need = e < cf.gpu_capacity ? e : cf.gpu_capacity;
+            need = e < cf.gpu_capacity ? e : cf.gpu_capacity;
             if (need > floor) floor = need;
         }
     }
+    constexpr bool mig = L::MIG;
+    // pick_instance's bar (manager.cpp:125-134): max(need, 1) bytes; 1 for exclusive
+    const uint64_t inst_need = need > 1 ? need : 1;
     const bool need_smact = policy != CARMA_POLICY_EXCLUSIVE &&
                             !(policy == CARMA_POLICY_RR && !cf.rr_apply_preconditions);
     const uint64_t* used = RP_U64(used);
     PickInput in[L::GPL];
+    int inst[L::GPL];
 #pragma unroll
     for (int j = 0; j < L::GPL; ++j) {
         const int g = static_cast<int>(lane) + 32 * j;
@@ -621,11 +686,39 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
         in[j].idle = valid && nres[g] == 0;
         in[j].free_bytes = valid ? static_cast<uint64_t>(free_blocks<L>(used, g)) * cf.alloc_block : 0;
         in[j].smact = (valid && need_smact) ? windowed<L>(b, g, c.now, c.window) : 0.0;
+        in[j].inst_ok = true;
+        inst[j] = -1;
+        if (mig && valid) {
+            // first idle instance with enough free memory (pick_instance)
+            const uint32_t busy = RP_U32(imask)[g];
+            for (int i = 0; i < cf.mig_count; ++i) {
+                if ((busy >> i) & 1u) continue;
+                const int r0 = cf.mig_base[i];
+                const uint64_t fb = static_cast<uint64_t>(free_in_range<L>(used, g, r0, r0 + cf.mig_blocks[i])) *
+                                    cf.alloc_block;
+                if (fb < inst_need) continue;
+                inst[j] = i;
+                break;
+            }
+            in[j].inst_ok = inst[j] >= 0;
+        }
     }
     int gids[2];
     const int got = pick_gpus<L::GPL>(cf, policy, tasks[head].gpus, floor, in, lane, 0, 32, c.rr_cursor, gids);
     g0 = gids[0];
     g1 = gids[1];
+    i0 = i1 = 0;
+    if (mig && got > 0) {  // the chosen devices' instances (exclusive: value_or(0))
+        int mine0 = 0, mine1 = 0;
+#pragma unroll
+        for (int j = 0; j < L::GPL; ++j) {
+            const int g = static_cast<int>(lane) + 32 * j;
+            if (g == g0) mine0 = inst[j] < 0 ? 0 : inst[j];
+            if (g == g1) mine1 = inst[j] < 0 ? 0 : inst[j];
+        }
+        i0 = __shfl_sync(0xffffffffu, mine0, g0 & 31);
+        if (got > 1) i1 = __shfl_sync(0xffffffffu, mine1, g1 & 31);
+    }
     return got;
 }
 
@@ -685,6 +778,7 @@ __device__ __noinline__ void init_job(char* b, const Params& p, uint32_t j, unsi
         RP_U32(rcnt)[g] = 0;
         RP_U32(peak)[g] = 0;
         RP_U32(has_step)[g] = 0;
+        if constexpr (L::MIG) RP_U32(imask)[g] = 0;
     }
     for (int k = static_cast<int>(lane); k < L::S; k += 32) RP_U32(free_stack)[k] = L::S - 1 - k;
     c.now = 0.0;
@@ -900,8 +994,8 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             sched = false;
             uint32_t head = 0;
             bool from_recovery = false;
-            int g0 = -1, g1 = -1;
-            const int got = decide<L>(b, c, tasks, est, head, from_recovery, g0, g1, lane);
+            int g0 = -1, g1 = -1, i0 = 0, i1 = 0;
+            const int got = decide<L>(b, c, tasks, est, head, from_recovery, g0, g1, i0, i1, lane);
             if (got == 0) break;  // defer; retried on the next completion / expiry
             if (from_recovery) {
                 c.rq_head = c.rq_head + 1 == static_cast<uint32_t>(L::RQ) ? 0 : c.rq_head + 1;
@@ -911,7 +1005,7 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             }
             // dispatch (manager.cpp:247-260)
             if (lane == 0 && !from_recovery) out[head].first_attempt = c.now;
-            const bool ok = place<L>(b, c, tasks[head], head, g0, g1, got, nblk, lane);
+            const bool ok = place<L>(b, c, tasks[head], head, g0, g1, i0, i1, got, nblk, lane);
             if (c.status) break;
             if (ok) {
                 if (lane == 0) {

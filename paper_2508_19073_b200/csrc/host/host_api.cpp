@@ -5,6 +5,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../../include/carma_host.h"
 #include "model.hpp"
@@ -245,6 +246,46 @@ carma_status carma_host_fit(int32_t family, uint64_t samples, uint64_t seed, uin
         *bucket_range = m.bucket_range;
         if (holdout_rows) std::copy(m.holdout_rows.begin(), m.holdout_rows.end(), holdout_rows);
         if (n_holdout) *n_holdout = m.holdout_rows.size();
+    });
+}
+
+// GpuDevice::GpuDevice's MIG branch (gpu.cpp:29-51): instance capacities are
+// round_up(fraction * capacity) clipped to what is left, the last instance
+// absorbing the remainder when the fractions sum to 1.
+carma_status carma_mig_layout(const double* fractions, uint32_t n, carma_replay_config* cfg) {
+    return guarded([&] {
+        if (!cfg) throw InvalidArg("null config");
+        if (n && !fractions) throw InvalidArg("null fractions");
+        static const double kDefault[2] = {0.5, 0.5};  // gpu.cpp:31
+        const double* src = n ? fractions : kDefault;
+        const std::vector<double> f(src, src + (n ? n : 2));
+        if (f.size() > CARMA_MAX_MIG) throw Unsupported("more than 8 MIG instances per GPU");
+        double sum = 0.0;
+        for (double x : f) {
+            if (!(x > 0.0) || x > 1.0) throw InvalidArg("ConfigError: mig instance fraction out of (0, 1]");
+            sum += x;
+        }
+        if (sum > 1.0 + 1e-9) throw InvalidArg("ConfigError: mig instance fractions exceed the device");
+        const uint64_t capacity = cfg->gpu_capacity, block = cfg->alloc_block;
+        if (block == 0 || capacity % block != 0) throw Unsupported("MIG needs gpu_capacity to be a multiple of alloc_block");
+        auto round_up = [&](uint64_t b) { return (b + block - 1) / block * block; };
+        uint64_t base = 0;
+        carma_replay_config c = *cfg;
+        std::memset(c.mig_fraction, 0, sizeof(c.mig_fraction));
+        std::memset(c.mig_base, 0, sizeof(c.mig_base));
+        std::memset(c.mig_blocks, 0, sizeof(c.mig_blocks));
+        for (std::size_t i = 0; i < f.size(); ++i) {
+            uint64_t cap = round_up(static_cast<uint64_t>(f[i] * static_cast<double>(capacity)));
+            cap = std::min(cap, capacity - base);
+            if (i + 1 == f.size() && sum > 1.0 - 1e-9) cap = capacity - base;
+            c.mig_fraction[i] = f[i];
+            c.mig_base[i] = static_cast<uint16_t>(base / block);
+            c.mig_blocks[i] = static_cast<uint16_t>(cap / block);
+            base += cap;
+        }
+        if (base > capacity) throw InvalidArg("ConfigError: mig instances exceed capacity");
+        c.mig_count = static_cast<int32_t>(f.size());
+        *cfg = c;
     });
 }
 

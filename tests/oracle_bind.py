@@ -68,6 +68,7 @@ ref_config_dtype = np.dtype([
     ("max_smact", "<f8"), ("has_min_free", "<i4"), ("min_free", "<u8"), ("safety_margin", "<u8"),
     ("monitor_window", "<f8"), ("gpu_count", "<i4"), ("gpu_capacity", "<u8"), ("alloc_block", "<u8"),
     ("estimator_seed", "<u8"), ("estimator_k", "<u8"), ("estimator_samples", "<u8"),
+    ("mig_count", "<i4"), ("mig_reserved", "<i4"), ("mig_fractions", "<f8", (8,)),
 ], align=True)
 
 ref_task_out_dtype = np.dtype([
@@ -85,8 +86,10 @@ ref_trace_out_dtype = np.dtype([
 
 def ref_config(policy="magm", estimator="none", mode="mps", rr_pre=False, max_smact=0.8, min_free=None,
                margin=2 * abi.GiB, window=60.0, gpu_count=4, capacity=40 * abi.GiB, block=512 * abi.MiB,
-               est_seed=11, est_k=5, est_samples=4000):
+               est_seed=11, est_k=5, est_samples=4000, mig=()):
     c = np.zeros(1, ref_config_dtype)
+    c["mig_count"] = len(mig)
+    c["mig_fractions"][0, : len(mig)] = mig
     c["policy"] = abi.POLICY[policy]
     c["estimator"] = abi.ESTIMATOR[estimator]
     c["mode"] = abi.MODE[mode]
@@ -114,6 +117,10 @@ def replay_config_from(c):
     r["min_free"] = c["min_free"] if c["has_min_free"][0] else 0
     r["p_idle_w"], r["p_max_w"], r["p_boost_w"], r["boost_threshold"] = 55.0, 400.0, 30.0, 0.9
     r["oom_startup_delay"] = 5.0
+    if int(c["mode"][0]) == abi.MODE["mig"]:
+        n = int(c["mig_count"][0])
+        fr = np.ascontiguousarray(c["mig_fractions"][0, :n], np.float64)
+        abi.check(abi.lib.carma_mig_layout(fr.ctypes.data if n else None, n, r.ctypes.data))
     return r
 
 

@@ -229,3 +229,34 @@ def test_fused_c5_prefix_matches_oracle(gpu, olib, estimator):
     assert res.job_tasks(0).tobytes() == ot.tobytes()
     assert res.traces[0:1].tobytes() == np.array([otr]).tobytes()
     assert res.job_gpus(0).tobytes() == og.tobytes()
+
+
+# MIG (gpu.cpp:29-51, :151-195; manager.cpp:125-134, :176-187, :236-243).
+# Instance 0 holds the largest catalog task, so every run terminates (the
+# reference retries crashed tasks exclusively on instance 0).
+MIG_CASES = [("magm", (0.75, 0.25), "none", 4), ("rr", (0.7, 0.15, 0.15), "none", 4),
+             ("exclusive", (0.75, 0.125), "none", 4), ("lug", (0.8, 0.2), "oracle", 4),
+             ("mug", (1.0,), "none", 8), ("magm", (0.75, 0.125, 0.125), "analytical", 4),
+             ("magm", (0.9, 0.05, 0.05), "learned", 8), ("rr", (0.8, 0.2), "oracle", 2)]
+
+
+def test_replay_mig_matches_oracle(gpu, olib, models):
+    task_lists, cfgs, jobs = [], [], []
+    for c, (pol, fr, est, g) in enumerate(MIG_CASES):
+        cfgs.append(cb.make_config(cb.PolicyConfig(policy=pol, collocation_mode="mig",
+                                                   rr_apply_preconditions=pol == "rr" and est != "none"),
+                                   cb.SimConstants(gpu_count=g), fr))
+        for mix in ("t90", "t60"):
+            for seed in (11, 12, 13):
+                m = cb.materialize_trace(cb.generate_trace(mix, seed))
+                if est == "learned":
+                    m.tasks["estimate"] = learned_estimates(olib, m, models)
+                else:
+                    cb.set_persona_estimates(m, est)
+                task_lists.append(m.tasks)
+                jobs.append((len(task_lists) - 1, c))
+    cfgs = np.concatenate(cfgs)
+    res = cb.replay(cfgs, task_lists, jobs)
+    assert (res.traces["oom_count"] > 0).any()  # the instance limits bite
+    check_jobs(olib, res, cfgs, task_lists, jobs)
+

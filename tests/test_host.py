@@ -175,3 +175,19 @@ def test_bitpacked_format_is_lossless(families):
         assert np.array_equal(v[:, 13 + 2 * k], rows["tuple_params"][:, k])
     assert np.array_equal(v[:, 18].astype(np.int8), fams)
     assert int(schema["words_per_row"][0]) * 4 < 64  # denser than the fixed 64-byte packing
+
+
+def test_mig_layout_matches_gpudevice():
+    c = cb.make_config(cb.PolicyConfig(collocation_mode="mig"), cb.SimConstants(), None)
+    assert c["mig_count"][0] == 2 and list(c["mig_blocks"][0, :2]) == [40, 40]
+    c = cb.make_config(cb.PolicyConfig(collocation_mode="mig"), cb.SimConstants(), (0.3, 0.3, 0.4))
+    # round_up(trunc(0.3 * 40 GiB)) = 12 GiB = 24 blocks of 512 MiB; the last instance absorbs the rest
+    assert list(c["mig_base"][0, :3]) == [0, 24, 48] and list(c["mig_blocks"][0, :3]) == [24, 24, 32]
+    c = cb.make_config(cb.PolicyConfig(collocation_mode="mig"), cb.SimConstants(), (0.5, 0.2))
+    # sum < 1: nothing absorbs the tail (gpu.cpp:44-46)
+    assert list(c["mig_blocks"][0, :2]) == [40, 16] and c["mig_count"][0] == 2
+    for bad in ((0.6, 0.6), (0.0, 0.5), (1.5,)):
+        with pytest.raises(abi.CarmaError):
+            cb.make_config(cb.PolicyConfig(collocation_mode="mig"), cb.SimConstants(), bad)
+    with pytest.raises(abi.CarmaError):
+        cb.make_config(cb.PolicyConfig(collocation_mode="mig"), cb.SimConstants(), (0.1,) * 9)

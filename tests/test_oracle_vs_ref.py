@@ -79,6 +79,15 @@ GRID = [dict(policy=p) for p in ("exclusive", "rr", "magm", "lug", "mug")] + [
     dict(policy="magm", mode="streams", max_smact=1.0),
     dict(policy="lug", gpu_count=8, window=5.0),
     dict(policy="magm", gpu_count=2, window=5.0, min_free=3 << 30),
+    # MIG: instance 0 must hold the largest catalog task (27.9 GiB) or the
+    # reference never terminates (exclusive recovery retries instance 0).
+    dict(policy="magm", mode="mig", mig=(0.75, 0.25)),
+    dict(policy="rr", mode="mig", mig=(0.7, 0.15, 0.15)),
+    dict(policy="exclusive", mode="mig", mig=(0.75, 0.125)),
+    dict(policy="lug", mode="mig", mig=(0.8, 0.2), estimator="oracle"),
+    dict(policy="mug", mode="mig", mig=(1.0,), gpu_count=8),
+    dict(policy="magm", mode="mig", mig=(0.75, 0.125, 0.125), estimator="analytical"),
+    dict(policy="rr", mode="mig", mig=(0.8, 0.2), rr_pre=True, estimator="oracle", gpu_count=2),
 ]
 
 
