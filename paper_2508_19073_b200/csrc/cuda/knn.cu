@@ -33,6 +33,7 @@
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "../../../include/carma_gpu.h"
@@ -50,6 +51,12 @@ constexpr int kMaxBins = 4096;
 constexpr int kBlock = 8;  // points per frontier step
 constexpr int kF32Dims = 16;  // fp32 pre-filter: active dims per point
 constexpr int kCandCap = 24;  // fp32 pre-filter: candidate buffer per lane
+// Partial unrolling of the per-query setup loops: enough independent
+// divisions / field loads in flight without 19 copies of the code.
+#ifndef KNN_SETUP_UNROLL
+#define KNN_SETUP_UNROLL 1
+#endif
+constexpr int kSetupUnroll = KNN_SETUP_UNROLL;
 
 struct ModelDev {
     const double* pts;    // N x 20, sorted by (p18, original index)
@@ -196,6 +203,76 @@ __device__ __forceinline__ int family_of(const KnnParams& p, uint64_t i) {
                             ? static_cast<int>(bit_field(p, bit_row(p, i), 18))
                             : (p.family ? static_cast<int>(p.family[i]) : p.default_family);
     return (f >= 0 && f < CARMA_FAMILIES && p.m[f].present) ? f : -1;
+}
+
+// Compile-time row format versions for the search kernel: each instance
+// carries one featuriser only (smaller code, no per-row format branches).
+template <int FMT>
+__device__ __forceinline__ int family_of_t(const KnnParams& p, uint64_t i) {
+    int f;
+    if constexpr (FMT == CARMA_ROWS_PACKED)
+        f = static_cast<int>((static_cast<const carma_feature_packed*>(p.rows)[i].w[4] >> 48) & 0xff);
+    else if constexpr (FMT == CARMA_ROWS_BITPACKED)
+        f = static_cast<int>(bit_field(p, bit_row(p, i), 18));
+    else
+        f = p.family ? static_cast<int>(p.family[i]) : p.default_family;
+    return (f >= 0 && f < CARMA_FAMILIES && p.m[f].present) ? f : -1;
+}
+
+// Raw scalar features of `row` into column `tid` of a [19][128] shared
+// array. The bit-packed fields are extracted by a rolled loop (one copy of
+// the extraction code instead of 19: the setup code competes with the walk
+// for the instruction cache).
+template <int FMT>
+__device__ __forceinline__ void stage_raw(const KnnParams& p, uint32_t row, double (*qs)[128], unsigned tid);
+
+template <int FMT>
+__device__ __forceinline__ void load_raw(const KnnParams& p, uint32_t row, double* raw) {
+    if constexpr (FMT == CARMA_ROWS_SCALAR) {
+        const double* r = static_cast<const double*>(p.rows) + static_cast<uint64_t>(row) * kDims;
+#pragma unroll
+        for (int d = 0; d < kDims; ++d) raw[d] = r[d];
+    } else if constexpr (FMT == CARMA_ROWS_PACKED) {
+        featurize_packed(p, static_cast<const carma_feature_packed*>(p.rows)[row], raw);
+    } else if constexpr (FMT == CARMA_ROWS_BITPACKED) {
+        featurize_bits(p, bit_row(p, row), raw);
+    } else {
+        featurize(static_cast<const carma_feature_row*>(p.rows)[row], raw);
+    }
+}
+
+template <int FMT>
+__device__ __forceinline__ void stage_raw(const KnnParams& p, uint32_t row, double (*qs)[128], unsigned tid) {
+    if constexpr (FMT == CARMA_ROWS_BITPACKED) {
+        const uint32_t* r = bit_row(p, row);
+#pragma unroll (kSetupUnroll)
+        for (int f = 0; f < kDims; ++f) qs[f][tid] = __longlong_as_double(static_cast<long long>(bit_field(p, r, f)));
+        uint64_t v[kDims];
+#pragma unroll
+        for (int f = 0; f < kDims; ++f) v[f] = static_cast<uint64_t>(__double_as_longlong(qs[f][tid]));
+        // field -> feature mapping of featurize_bits
+        double raw[kDims];
+#pragma unroll
+        for (int f = 0; f < 7; ++f) raw[f] = u2d(v[f]);
+        const int code = static_cast<int>(v[7]) & 7;
+        raw[7] = p.act[2 * code];
+        raw[8] = p.act[2 * code + 1];
+        const bool h = v[11] != 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            raw[9 + 3 * k] = h ? static_cast<double>(static_cast<int32_t>(v[8 + k])) : 0.0;
+            raw[10 + 3 * k] = h ? u2d(v[12 + 2 * k]) : 0.0;
+            raw[11 + 3 * k] = h ? u2d(v[13 + 2 * k]) : 0.0;
+        }
+        raw[18] = __dadd_rn(__dmul_rn(16.0, raw[5]), __dmul_rn(__dmul_rn(4.0, raw[4]), raw[6]));
+#pragma unroll
+        for (int d = 0; d < kDims; ++d) qs[d][tid] = raw[d];
+    } else {
+        double raw[kDims];
+        load_raw<FMT>(p, row, raw);
+#pragma unroll
+        for (int d = 0; d < kDims; ++d) qs[d][tid] = raw[d];
+    }
 }
 
 // first index with key18[i] >= x
@@ -636,7 +713,7 @@ __device__ __forceinline__ void sorted_insert(float (&a)[K], float v) {
     a[0] = fminf(a[0], v);
 }
 
-template <int K>
+template <int K, int FMT>
 __global__ void __launch_bounds__(128, 4)
     knn_search_f32(KnnParams p, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ qpos,
                    int32_t* __restrict__ bucket_out, uint64_t* __restrict__ bytes_out,
@@ -665,7 +742,7 @@ __global__ void __launch_bounds__(128, 4)
         const uint64_t slot = w * 32 + lane;
         const bool live = slot < p.q;
         const uint32_t row = live ? perm[slot] : 0;
-        const int fam = live ? family_of(p, row) : -1;
+        const int fam = live ? family_of_t<FMT>(p, row) : -1;
         if (live && fam < 0) {  // FamilyMismatch -> no estimate
             if (bucket_out) bucket_out[row] = -1;
             if (bytes_out) bytes_out[row] = ~0ull;
@@ -685,42 +762,33 @@ __global__ void __launch_bounds__(128, 4)
             double eta = 0.0;
             double q18 = 0.0;
             {
-                double raw[kDims];
-                if (mine) {
-                    if (p.format == CARMA_ROWS_SCALAR) {
-                        const double* r = static_cast<const double*>(p.rows) + static_cast<uint64_t>(row) * kDims;
-#pragma unroll
-                        for (int d = 0; d < kDims; ++d) raw[d] = r[d];
-                    } else if (p.format == CARMA_ROWS_PACKED) {
-                        featurize_packed(p, static_cast<const carma_feature_packed*>(p.rows)[row], raw);
-                    } else if (p.format == CARMA_ROWS_BITPACKED) {
-                        featurize_bits(p, bit_row(p, row), raw);
-                    } else {
-                        featurize(static_cast<const carma_feature_row*>(p.rows)[row], raw);
-                    }
-                } else {
-#pragma unroll
-                    for (int d = 0; d < kDims; ++d) raw[d] = 0.0;
-                }
+                // Rolled loops: one division / bound sequence in the code
+                // instead of 19 / 16 (instruction-cache footprint).
+                if (mine) stage_raw<FMT>(p, row, qsh, tid);
                 double qmax = 0.0;
-#pragma unroll
+#pragma unroll (kSetupUnroll)
                 for (int d = 0; d < kDims; ++d) {
-                    const double v = mine ? normalize(raw[d], m.lo[d], m.hi[d]) : 0.0;
-                    if (d == 18) q18 = v;
+                    const double v = mine ? normalize(qsh[d][tid], m.lo[d], m.hi[d]) : 0.0;
                     qsh[d][tid] = v;
                     const double av = fabs(v);
                     qmax = (av > qmax || av != av) ? av : qmax;
                 }
+                q18 = qsh[18][tid];
                 double e2 = 0.0;
+#pragma unroll 1
+                for (int j = 0; j < kF32Dims; ++j) {
+                    const int a = m.adim[j];
+                    if (a < kDims) {
+                        const double qa = qsh[a][tid];
+                        const double w = a == 18 ? 64.0 : 1.0;
+                        const double ej = 2.0 * 0x1.0p-24 * (1.0 + 0x1.0p-24) * w * (m.pmax[j] + fabs(qa)) + 0x1.0p-140;
+                        e2 += ej * ej;
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j < kF32Dims; ++j) {
                     const int a = m.adim[j];
-                    const double qa = a < kDims ? qsh[a][tid] : 0.0;
-                    const double w = a == 18 ? 64.0 : 1.0;
-                    qf[j] = a < kDims ? __double2float_rn(w * qa) : 0.0f;
-                    const double ej = a < kDims ? 2.0 * 0x1.0p-24 * (1.0 + 0x1.0p-24) * w * (m.pmax[j] + fabs(qa)) + 0x1.0p-140
-                                                : 0.0;
-                    e2 += ej * ej;
+                    qf[j] = a < kDims ? __double2float_rn((a == 18 ? 64.0 : 1.0) * qsh[a][tid]) : 0.0f;
                 }
                 eta = sqrt(e2) * (1.0 + 0x1.0p-40);
                 if (!(qmax <= 1e15)) eta = inf;  // huge or NaN query: exact on every point
@@ -1043,12 +1111,27 @@ void launch_search(const KnnParams& p, int kmax, bool f32, const uint32_t* perm,
     // the tail short while each CTA stays in one region of the model.
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, 148u * 16u)));
     if (f32) {
-        if (kmax <= 5)
-            knn_search_f32<5><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
-        else if (kmax <= 8)
-            knn_search_f32<8><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
-        else
-            knn_search_f32<kMaxK><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+        auto go = [&](auto kc) {
+            constexpr int KK = decltype(kc)::value;
+            switch (p.format) {
+                case CARMA_ROWS_SCALAR:
+                    knn_search_f32<KK, CARMA_ROWS_SCALAR><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+                    break;
+                case CARMA_ROWS_PACKED:
+                    knn_search_f32<KK, CARMA_ROWS_PACKED><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+                    break;
+                case CARMA_ROWS_BITPACKED:
+                    knn_search_f32<KK, CARMA_ROWS_BITPACKED><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx,
+                                                                                     evals);
+                    break;
+                default:
+                    knn_search_f32<KK, CARMA_ROWS_FEATURES><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx,
+                                                                                   evals);
+            }
+        };
+        if (kmax <= 5) go(std::integral_constant<int, 5>{});
+        else if (kmax <= 8) go(std::integral_constant<int, 8>{});
+        else go(std::integral_constant<int, kMaxK>{});
     } else {
         if (kmax <= 5)
             knn_search<5><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);

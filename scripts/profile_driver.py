@@ -1,7 +1,7 @@
 """Small single-purpose drivers for ncu captures (one GPU).
 
   python scripts/profile_driver.py replay --traces 20000 --policies magm,rr
-  python scripts/profile_driver.py knn --rows 4194304
+  python scripts/profile_driver.py knn --rows 4194304 [--format rows|bitpacked]
 
 Each runs the workload `--reps` times (default 2) so `ncu -k regex:<kernel> -s <n> -c 1`
 can skip the first launch.
@@ -49,14 +49,22 @@ def knn(args):
     k = cb.GpuKnn(0)
     k.set_model(cb.fit_knn(1, 4000, 112, 5))
     k.set_model(cb.fit_knn(2, 4000, 213, 5))
-    d_rows = torch.from_numpy(rows.view(np.uint8)).cuda()
-    d_fam = torch.from_numpy(fam).cuda()
+    fmt, fam_ptr = 0, None
+    if args.format == "bitpacked":  # the bench's device path (36 B rows, family inside)
+        words, schema = cb.pack_features_bits(rows, fam)
+        abi.check(abi.lib.carma_knn_set_bit_schema(k.handle, schema.ctypes.data))
+        d_rows = torch.from_numpy(words.view(np.uint8)).cuda()
+        fmt = abi.ROWS_BITPACKED
+    else:
+        d_rows = torch.from_numpy(rows.view(np.uint8)).cuda()
+        d_fam = torch.from_numpy(fam).cuda()
+        fam_ptr = d_fam.data_ptr()
     b = torch.empty(len(rows), dtype=torch.int32, device="cuda")
     by = torch.empty(len(rows), dtype=torch.int64, device="cuda")
     import ctypes
     sm, pm = ctypes.c_double(), ctypes.c_double()
     for _ in range(args.reps):
-        abi.check(abi.lib.carma_knn_predict_device(k.handle, d_rows.data_ptr(), 0, d_fam.data_ptr(), 1, len(rows),
+        abi.check(abi.lib.carma_knn_predict_device(k.handle, d_rows.data_ptr(), fmt, fam_ptr, 1, len(rows),
                                                    b.data_ptr(), by.data_ptr(), None, None, None))
         abi.check(abi.lib.carma_knn_last_timing(k.handle, ctypes.byref(sm), ctypes.byref(pm)))
         print(f"knn {len(rows)} rows: search {sm.value:.2f} ms pipeline {pm.value:.2f} ms stats {k.last_stats()}",
@@ -93,6 +101,7 @@ if __name__ == "__main__":
     ap.add_argument("--traces", type=int, default=20000)
     ap.add_argument("--policies", default="exclusive,rr,magm,lug")
     ap.add_argument("--rows", type=int, default=1 << 22)
+    ap.add_argument("--format", choices=("rows", "bitpacked"), default="bitpacked")
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
     {"replay": replay, "knn": knn, "fused": fused}[a.what](a)

@@ -7,7 +7,7 @@ on boxes where /root/reference (and hence oracle/_ref) is absent:
   knn.npz     estimate_learned buckets/bytes for 2000 dataset rows per family,
               models trained like provision_estimators (runner.cpp:17-38)
   replay.npz  run_simulation outputs (per task / per GPU / report) for a grid
-              of policies, mixes, seeds, estimators and platforms
+              of policies, mixes, seeds, estimators, platforms and MIG tables
 Inputs are not stored: they are regenerated bit-identically by the product's
 host provisioning (checked by tests/test_oracle_vs_ref.py).
 """
@@ -36,6 +36,10 @@ for mix in ("t90", "t60"):
         REPLAY_CASES.append(dict(mix=mix, seed=seed, policy="rr", estimator="none", mode="streams"))
         REPLAY_CASES.append(dict(mix=mix, seed=seed, policy="magm", estimator="none", min_free=2 << 30))
         REPLAY_CASES.append(dict(mix=mix, seed=seed, policy="lug", estimator="learned", gpu_count=8, window=5.0))
+        # MIG (instance 0 holds the largest catalog task so every run terminates)
+        REPLAY_CASES.append(dict(mix=mix, seed=seed, policy="magm", estimator="none", mode="mig", mig=(0.75, 0.25)))
+        REPLAY_CASES.append(dict(mix=mix, seed=seed, policy="rr", estimator="oracle", mode="mig",
+                                 mig=(0.8, 0.1, 0.1), rr_pre=True))
 
 
 def main():

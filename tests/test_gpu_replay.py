@@ -159,7 +159,7 @@ def test_pick_batch_matches_oracle(gpu, olib):
 
 
 def test_gpu_replay_matches_reference_golden(gpu, olib):
-    """All 60 golden reference runs (tests/golden/replay.npz) in one batch; learned
+    """All 72 golden reference runs (12 of them MIG) (tests/golden/replay.npz) in one batch; learned
     estimates come from the GPU k-NN (GPUMemNet stage feeding stage 2)."""
     import os
 
