@@ -134,12 +134,13 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
     const int cur = rr_cursor;
     const uint64_t nmask = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
     uint64_t rot = cur == 0 ? mask : (((mask >> cur) | (mask << (n - cur))) & nmask);
+    // b, cur < n: the wrap-around is one conditional subtraction
     for (uint32_t k = 0; k < want; ++k) {
-        const int b = __ffsll(static_cast<long long>(rot)) - 1;
-        out[k] = (b + cur) % n;
+        const int b = __ffsll(static_cast<long long>(rot)) - 1 + cur;
+        out[k] = b >= n ? b - n : b;
         rot &= rot - 1;
     }
-    rr_cursor = (out[want - 1] + 1) % n;
+    rr_cursor = out[want - 1] + 1 == n ? 0 : out[want - 1] + 1;
     return static_cast<int>(want);
 }
 

@@ -252,6 +252,7 @@ __device__ __forceinline__ int next_bit(const uint64_t* used, int g, int from, i
 
 template <class L>
 __device__ __forceinline__ void set_bits(uint64_t* used, int g, int off, int nb, bool on) {
+#pragma unroll 1
     for (int x = off; x < off + nb;) {
         const int w = x >> 6, lo = x & 63;
         const int cnt = min(64 - lo, off + nb - x);
@@ -333,6 +334,7 @@ __device__ __forceinline__ double windowed(char* b, int g, double now, double wi
     const double* rv = RP_F64(ring_v) + g * L::RG;
     double integral = 0.0, level = 0.0, cursor = begin;
     const uint32_t h = RP_U32(rhead)[g], n = RP_U32(rcnt)[g];
+#pragma unroll 1
     for (uint32_t k = 0; k < n; ++k) {
         uint32_t idx = h + k;
         if (idx >= static_cast<uint32_t>(L::RG)) idx -= L::RG;
@@ -366,6 +368,7 @@ __device__ __forceinline__ bool refresh_gpu(char* b, int g, double now, double w
         // per resident min(1, f_instance / demand) (gpu.cpp:187-195); the
         // per-GPU rate cache is unused in MIG mode
         double sum = 0.0;
+#pragma unroll 1
         for (uint32_t r = 0; r < n; ++r) {
             const uint32_t slot = res[r];
             const double rr = dmin(1.0, __ddiv_rn(cf.mig_fraction[inst_of<L>(b, slot, g)], dem[slot]));
@@ -375,12 +378,14 @@ __device__ __forceinline__ bool refresh_gpu(char* b, int g, double now, double w
     } else if (n > 0) {
         if (cf.mode == CARMA_MODE_MPS) {
             double total = 0.0;
+#pragma unroll 1
             for (uint32_t r = 0; r < n; ++r) total = __dadd_rn(total, dem[res[r]]);
             rate = dmin(1.0, __ddiv_rn(1.0, total));
         } else {
             rate = __ddiv_rn(1.0, static_cast<double>(n));
         }
         double sum = 0.0;
+#pragma unroll 1
         for (uint32_t r = 0; r < n; ++r) sum = __dadd_rn(sum, __dmul_rn(dem[res[r]], rate));
         inst = dmin(1.0, sum);
     }
@@ -467,6 +472,7 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
     uint32_t na = 0;
     {
         const uint32_t n0 = nres[t0];
+#pragma unroll 1
         for (uint32_t r = lane; r < n0; r += 32) {
             const uint32_t slot = res[t0 * L::RC + r];
             aff[r] = (static_cast<uint64_t>(rank[slot]) << 32) | slot;
@@ -474,6 +480,7 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
         na = n0;
         if (nt > 1) {
             const uint32_t n1 = nres[t1];
+#pragma unroll 1
             for (uint32_t base = 0; base < n1; base += 32) {
                 const uint32_t r = base + lane;
                 bool keep = false;
@@ -490,9 +497,11 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
         }
     }
     __syncwarp();
+#pragma unroll 1
     for (uint32_t e = lane; e < na; e += 32) {
         const uint64_t key = aff[e];
         uint32_t pos = 0;
+#pragma unroll 1
         for (uint32_t k = 0; k < na; ++k) pos += aff[k] < key;
         aff2[pos] = key;
     }
@@ -503,6 +512,7 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
     double* s_exec = RP_F64(s_exec);
     double* s_rem = RP_F64(s_rem);
     uint32_t* s_seq = RP_U32(s_seq);
+#pragma unroll 1
     for (uint32_t e = 0; e < na; ++e) {
         const uint32_t slot = static_cast<uint32_t>(aff2[e] & 0xffffffffu);
         const uint32_t g = gp[slot];
@@ -625,6 +635,7 @@ __device__ __forceinline__ void finish(char* b, Sc& c, uint32_t slot, carma_task
             uint16_t* rl = res + g * L::RC;
             uint32_t r = 0;
             while (r < n && rl[r] != slot) ++r;
+#pragma unroll 1
             for (; r + 1 < n; ++r) rl[r] = rl[r + 1];
             nres[g] = n - 1;
             if constexpr (L::MIG) RP_U32(imask)[g] &= ~(1u << inst_of<L>(b, slot, g));
@@ -739,10 +750,13 @@ __device__ __noinline__ void init_job(char* b, const Params& p, uint32_t j, unsi
     nblk = static_cast<int>(cf.gpu_capacity / cf.alloc_block);
     // first_submit (runner.cpp:108-109) and the full-history window begin.
     double fs = tasks[0].submit;
+#pragma unroll 1
     for (uint32_t i = lane; i < T; i += 32) fs = dmin(fs, tasks[i].submit);
+#pragma unroll 1
     for (int o = 16; o > 0; o >>= 1) fs = dmin(fs, __shfl_xor_sync(0xffffffffu, fs, o));
     const double forced = p.smact_begin[j];
     c.begin0 = forced == forced ? forced : dmax0(fs);
+#pragma unroll 1
     for (uint32_t i = lane; i < T; i += 32) {
         carma_task_result r;
         r.first_attempt = r.final_dispatch = r.complete = r.first_crash = r.last_crash = -1.0;
@@ -816,6 +830,7 @@ __device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, un
     uint32_t* inv = p.inv_scratch + p.task_out_off[j];
     double lc = 0.0, fs = tasks[0].submit;
     bool complete = true;
+#pragma unroll 1
     for (uint32_t i = lane; i < T; i += 32) {
         carma_task_result& o = out[i];
         const double cpl = o.complete;
@@ -825,6 +840,7 @@ __device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, un
         o.attempts = o.ooms + (o.final_dispatch >= 0.0 ? 1u : 0u);
         inv[tasks[i].rank] = i;
     }
+#pragma unroll 1
     for (int o = 16; o > 0; o >>= 1) {
         const double x = __shfl_xor_sync(0xffffffffu, lc, o);
         lc = lc < x ? x : lc;
@@ -849,6 +865,7 @@ __device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, un
     carma_gpu_result* gout = p.gpu_out + p.gpu_out_off[j];
     const double overshoot = __dsub_rn(c.now, lc);
     double energy = 0.0;
+#pragma unroll 1
     for (int g = 0; g < G; ++g) {
         double e = RP_F64(energy)[g];
         if (overshoot > 0.0) e = __dsub_rn(e, __dmul_rn(RP_F64(power)[g], overshoot));
@@ -870,6 +887,7 @@ __device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, un
     // Sums in id (rank) order (metrics.cpp:25-45): each lane stages 32
     // values; lane order is rank order.
     double ws = 0.0, es = 0.0, js = 0.0;
+#pragma unroll 1
     for (uint32_t base = 0; base < T; base += 32) {
         const uint32_t r = base + lane;
         double w = 0.0, e = 0.0, jc = 0.0;
@@ -882,6 +900,7 @@ __device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, un
             jc = __dsub_rn(cp, sub);
         }
         const uint32_t cnt = min(32u, T - base);
+#pragma unroll 1
         for (uint32_t l = 0; l < cnt; ++l) {
             ws = __dadd_rn(ws, __shfl_sync(0xffffffffu, w, l));
             es = __dadd_rn(es, __shfl_sync(0xffffffffu, e, l));
