@@ -121,12 +121,13 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
         if (want > 1) out[1] = best[1];
         return static_cast<int>(want);
     }
+    // want <= 2: out[] is written with constant indices (a dynamic index
+    // would put the caller's array in local memory)
     if (policy == CARMA_POLICY_EXCLUSIVE) {
         uint64_t m = mask;
-        for (uint32_t k = 0; k < want; ++k) {
-            out[k] = __ffsll(static_cast<long long>(m)) - 1;
-            m &= m - 1;
-        }
+        out[0] = __ffsll(static_cast<long long>(m)) - 1;
+        m &= m - 1;
+        if (want > 1) out[1] = __ffsll(static_cast<long long>(m)) - 1;
         return static_cast<int>(want);
     }
     // RR: cyclic scan from the cursor (manager.cpp:196-209): rotate the mask
@@ -135,12 +136,16 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
     const uint64_t nmask = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
     uint64_t rot = cur == 0 ? mask : (((mask >> cur) | (mask << (n - cur))) & nmask);
     // b, cur < n: the wrap-around is one conditional subtraction
-    for (uint32_t k = 0; k < want; ++k) {
-        const int b = __ffsll(static_cast<long long>(rot)) - 1 + cur;
-        out[k] = b >= n ? b - n : b;
-        rot &= rot - 1;
+    const int b0 = __ffsll(static_cast<long long>(rot)) - 1 + cur;
+    out[0] = b0 >= n ? b0 - n : b0;
+    rot &= rot - 1;
+    int last = out[0];
+    if (want > 1) {
+        const int b1 = __ffsll(static_cast<long long>(rot)) - 1 + cur;
+        out[1] = b1 >= n ? b1 - n : b1;
+        last = out[1];
     }
-    rr_cursor = out[want - 1] + 1 == n ? 0 : out[want - 1] + 1;
+    rr_cursor = last + 1 == n ? 0 : last + 1;
     return static_cast<int>(want);
 }
 

@@ -49,6 +49,13 @@
 namespace carma_b200 {
 namespace replay {
 
+// Shared-memory tiers: 64 registers, 8 CTAs x 4 warps resident (throughput
+// of many jobs). The large tier (one long trace per warp, latency bound)
+// and the global tier take all the registers they want.
+#ifndef REPLAY_MIN_CTAS
+#define REPLAY_MIN_CTAS 8
+#endif
+
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kWindow = 1u, kCompletion = 2u, kCrash = 3u;
 constexpr int32_t kStatusRetry = -1;      // overflowed this tier
@@ -927,11 +934,18 @@ __device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, un
 
 template <class L>
 __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, unsigned lane) {
+    // init_job / finish_job are out of line and take their state by
+    // reference; the loop works on a copy whose address never escapes, so
+    // it stays in registers instead of local memory.
     Sc c;
     const carma_task* tasks;
     carma_task_result* out;
     int nblk;
-    init_job<L>(b, p, j, lane, c, tasks, out, nblk);
+    {
+        Sc c0;
+        init_job<L>(b, p, j, lane, c0, tasks, out, nblk);
+        c = c0;
+    }
     const uint64_t* est = p.est_override ? p.est_override + p.trace_off[p.jobs[j].trace] : nullptr;
     const uint64_t max_events = 1000ull * c.T + 1000000ull;
     uint64_t events = 0;
@@ -1053,11 +1067,12 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
     c.events_lo = static_cast<uint32_t>(events);
     c.events_hi = static_cast<uint32_t>(events >> 32);
     __syncwarp();
-    finish_job<L>(b, p, j, lane, c, tasks, out);
+    const Sc c1 = c;
+    finish_job<L>(b, p, j, lane, c1, tasks, out);
 }
 
 template <class L, bool SMEM>
-__global__ void __launch_bounds__(128, SMEM ? 8 : 1) replay_kernel(Params p) {
+__global__ void __launch_bounds__(128, (SMEM && L::H < 1024) ? REPLAY_MIN_CTAS : 1) replay_kernel(Params p) {
     extern __shared__ __align__(16) char smem[];
     const unsigned lane = threadIdx.x & 31;
     const unsigned wib = threadIdx.x >> 5;
