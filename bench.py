@@ -679,7 +679,7 @@ def main():
     ap.add_argument("--skip-fused", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
     ap.add_argument("--fused-tasks", type=int, default=1_000_000)
-    ap.add_argument("--fused-cpu-tasks", type=int, default=20_000)
+    ap.add_argument("--fused-cpu-tasks", type=int, default=100_000)
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup raised to 3 (timing rule)")

@@ -7,10 +7,10 @@ set -u
 OUT=${OUT:-gpurun_out}
 mkdir -p $OUT
 python bench.py > $OUT/bench.json 2> $OUT/bench.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/launches.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 1 --skip-cpu --skip-small --skip-fused > $OUT/launch_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:knn_search -s 1 -c 1 \
     -o $OUT/knn_search_full -f python scripts/profile_driver.py knn --rows 16777216 --reps 2 > $OUT/ncu_knn.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:replay_kernel -s 2 -c 1 \
-    -o $OUT/replay_kernel_full -f python scripts/profile_driver.py replay --traces 20000 --reps 2 > $OUT/ncu_replay.log 2>&1
+    -o $OUT/replay_kernel_full -f python scripts/profile_driver.py replay --traces 100000 --reps 2 > $OUT/ncu_replay.log 2>&1
 tail -2 $OUT/bench.err
