@@ -184,6 +184,18 @@ def profile_traffic(name: str):
         return None
 
 
+def recorded(name: str):
+    """A measurement too long for the bounded bench run (e.g. the reference on the
+    full 10^6-task c5 trace, scripts/c5_cpu_full.py, ~21 min), recorded once per
+    round under profiles/."""
+    try:
+        r = json.load(open(os.path.join(ROOT, "profiles", name)))
+        r["source"] = f"profiles/{name} (scripts/c5_cpu_full.py on the GPU box host, not re-run here)"
+        return r
+    except (OSError, ValueError):
+        return None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -264,6 +276,65 @@ def cpu_fused_baseline(ref, n_tasks: int):
     dt = time.perf_counter() - t
     return n_tasks / dt, (f"first {n_tasks} rows of the c5 trace, one run_simulation on 1 core "
                           f"(reference cost grows superlinearly with trace length, SURVEY F7)")
+
+
+SCORING_DECISIONS = 1 << 24  # per GPU
+SCORING_GPUS = 8
+
+
+def scoring_bench(abi, cb, dev, stream, warmup, steps, d):
+    """Batched eligible_gpus + map_task (manager.cpp:109-245): one decision per
+    (task, server view) over device-resident views (24 B per simulated GPU) and
+    requests (16 B), writing 2 GPU ids + the RR cursor. A pure HBM stream:
+    algorithmic bytes per decision = G*24 + 16 + 4 (cursor in) + 4 (out) + 8."""
+    import torch
+    n, g = SCORING_DECISIONS, SCORING_GPUS
+    rng = np.random.default_rng(5)
+    views = np.zeros((n, g), abi.gpu_view_dtype)
+    views["total_free"] = rng.integers(0, 81, (n, g), dtype=np.uint64) * np.uint64(512 << 20)
+    views["windowed_smact"] = rng.random((n, g))
+    views["idle"] = rng.random((n, g)) < 0.25
+    reqs = np.zeros(n, abi.pick_request_dtype)
+    reqs["estimate"] = rng.integers(0, 45, n, dtype=np.uint64) * np.uint64(1 << 30)
+    reqs["want"] = np.where(rng.random(n) < 0.15, 2, 1).astype(np.uint32)
+    cfg = cb.make_config(cb.PolicyConfig(policy="magm", max_smact=0.8), cb.SimConstants(gpu_count=g))
+    dv = torch.from_numpy(views.view(np.uint8).reshape(-1)).to("cuda")
+    dr = torch.from_numpy(reqs.view(np.uint8).reshape(-1)).to("cuda")
+    dc = torch.zeros(n, dtype=torch.int32, device="cuda")
+    do = torch.empty(2 * n, dtype=torch.int32, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > L2: every step starts cold
+
+    def step():
+        abi.check(abi.lib.carma_pick_batch_device(dev, cfg.ctypes.data, dv.data_ptr(), g, dr.data_ptr(), n,
+                                                  dc.data_ptr(), do.data_ptr(), stream.cuda_stream))
+
+    for _ in range(warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    d.barrier()
+    times = []
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = d.max(statistics.mean(times))
+    per = g * 24 + 16 + 4 + 4 + 8
+    gbs = per * n / (ms * 1e-3) / 1e9
+    hbm = peaks().get("hbm_gbs", 6650.0)
+    return {"metric": "placement decisions/sec (feasibility + MAGM score matrix)", "unit": "decisions/s",
+            "value": d.n * n / (ms * 1e-3), "ms_per_step": ms,
+            "config": {"workload": f"{n} decisions x {g} simulated GPUs per rank, MAGM u=0.8, random views "
+                                   f"(free in 512 MiB blocks, SMACT, idle), 15% two-GPU requests",
+                       "l2": "256 MiB buffer written between steps"},
+            "gpu_launches": 1,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                         "traffic": profile_traffic("pick_kernel"),
+                         "algorithmic_bytes_per_decision": per, "kernel": "pick_kernel"}}
 
 
 def small_configs(cb, abi, dev, ref):
@@ -577,6 +648,11 @@ def run_carma(args, d: Dist):
                          "note": "latency/issue bound event loop; algorithmic bytes = 80 B per placed task"},
         }
 
+    # ---------------- placement scoring (feasibility / score matrix, B9)
+    scoring = None
+    if not args.skip_scoring:
+        scoring = scoring_bench(abi, cb, dev, stream, args.warmup, args.steps, d)
+
     # ---------------- stage 1 -> 2 fused (configs[4], c5)
     fused = None
     if not args.skip_fused:
@@ -605,7 +681,8 @@ def run_carma(args, d: Dist):
                                         "seed 7; k-NN pre-pass over every arrival on device feeding the replay; "
                                         "MAGM + learned, u=0.8, W=5 s, 64 simulated GPUs"},
                  "events": int(fres["events"]), "oom_count": int(fres["oom_count"]),
-                 "note": "one trace: a single warp replays it (sequential event loop); replicas only across GPUs"}
+                 "note": "one trace: a single warp replays it (sequential event loop); replicas only across GPUs",
+                 "cpu_reference_full_trace": recorded("c5_cpu_full_r01.json")}
 
     # ---------------- CPU baselines (rank 0, N = 1)
     cpu = None
@@ -661,6 +738,7 @@ def run_carma(args, d: Dist):
         "cpu_baseline": cpu,
         "clocks": clocks,
         "replay": replay,
+        "scoring": scoring,
         "fused": fused,
         "small_configs": small,
     }
@@ -678,6 +756,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-fused", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
+    ap.add_argument("--skip-scoring", action="store_true")
     ap.add_argument("--fused-tasks", type=int, default=1_000_000)
     ap.add_argument("--fused-cpu-tasks", type=int, default=100_000)
     args = ap.parse_args()

@@ -346,6 +346,13 @@ carma_status carma_pick_batch(int device, const carma_replay_config* cfg,
                               const carma_gpu_view* views, uint32_t n_gpus,
                               const carma_pick_request* reqs, uint64_t n,
                               int32_t* rr_cursor, int32_t* out_gpus);
+/* Same on device-resident arrays (views, reqs, rr_cursor, out_gpus are device
+ * pointers; cfg is host memory), launched on `stream` (cudaStream_t or NULL).
+ * want must be 1 or 2 (not checked on the device path). */
+carma_status carma_pick_batch_device(int device, const carma_replay_config* cfg,
+                                     const carma_gpu_view* views, uint32_t n_gpus,
+                                     const carma_pick_request* reqs, uint64_t n,
+                                     int32_t* rr_cursor, int32_t* out_gpus, void* stream);
 
 /* ------------------------------------------------------------ probes */
 /* Measured fp64 add/mul issue throughput of `device` (separately rounded

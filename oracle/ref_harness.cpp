@@ -466,4 +466,25 @@ double ref_bench_sweep(const RefConfig* base, int mix, uint64_t seed0, uint64_t 
     }
 }
 
+// The reference's own run_sweep (runner.cpp:192-283): cells from RefConfig
+// rows (policy part), base constants/estimator provisioning from cells[0],
+// trace mix `mix`, the given seeds, one worker per hardware thread. Writes the
+// sweep CSV (per-seed rows + median rows) into csv[cap].
+int ref_run_sweep(const RefConfig* cells, int n_cells, int mix, const uint64_t* seeds, int n_seeds,
+                  char* csv, uint64_t cap) {
+    try {
+        SweepConfig sc;
+        sc.base = make_rc(cells[0]);
+        sc.base.mix = static_cast<TraceMix>(mix);
+        for (int c = 0; c < n_cells; ++c) sc.cells.push_back({make_rc(cells[c]).policy, std::string()});
+        sc.seeds.assign(seeds, seeds + n_seeds);
+        SweepResult r = run_sweep(sc);
+        if (r.csv.size() + 1 > cap) throw CarmaError("csv buffer too small");
+        std::memcpy(csv, r.csv.c_str(), r.csv.size() + 1);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 }  // extern "C"

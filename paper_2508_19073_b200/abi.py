@@ -16,6 +16,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcarma_b200.so")
 
 CARMA_OK = 0
+CARMA_ERR_INVALID, CARMA_ERR_CUDA, CARMA_ERR_OVERFLOW, CARMA_ERR_FAMILY = 1, 2, 3, 4
+CARMA_ERR_UNSUPPORTED, CARMA_ERR_INCOMPLETE = 5, 6
 STATUS_NAMES = {
     0: "OK", 1: "INVALID", 2: "CUDA", 3: "OVERFLOW", 4: "FAMILY", 5: "UNSUPPORTED", 6: "INCOMPLETE",
 }
@@ -138,6 +140,7 @@ SIGNATURES = {
     "carma_replay_plan_destroy": (c_int, [c_void_p]),
     "carma_replay_batch": (c_int, [c_int, P, c_uint32, P, P, c_uint32, P, c_uint32, P, P, P]),
     "carma_pick_batch": (c_int, [c_int, P, P, c_uint32, P, c_uint64, P, P]),
+    "carma_pick_batch_device": (c_int, [c_int, P, P, c_uint32, P, c_uint64, P, P, c_void_p]),
     # carma_host.h
     "carma_host_catalog_size": (c_int, []),
     "carma_host_catalog_entry": (c_int, [c_int, c_char_p, c_int, P, P, P, P]),

@@ -563,6 +563,139 @@ class FusedReplay:
         self.plan.close()
 
 
+# ------------------------------------------------------------------ sweep
+
+
+@dataclasses.dataclass
+class RunReport:
+    """RunReport scalars (metrics.hpp:44-57) of one replay."""
+
+    trace_name: str
+    config: PolicyConfig
+    trace_total_time: float
+    avg_wait: float
+    avg_exec: float
+    avg_jct: float
+    oom_count: int
+    energy_mj: float
+
+
+@dataclasses.dataclass
+class SweepCell:
+    """runner.hpp:54-57"""
+
+    policy: PolicyConfig
+    label: str = ""
+
+
+@dataclasses.dataclass
+class SweepConfig:
+    """runner.hpp:59-64 (max_threads is accepted for parity; the GPU runs every cell x seed at once)."""
+
+    base: RunConfig
+    cells: List[SweepCell]
+    seeds: List[int] = dataclasses.field(default_factory=lambda: [1])
+    max_threads: int = 0
+
+
+@dataclasses.dataclass
+class SweepResult:
+    """runner.hpp:66-69: reports[cell][seed] and the sweep CSV (per-seed rows + a median row per cell)."""
+
+    reports: List[List[RunReport]]
+    csv: str
+
+
+_CSV_HEADER = ("policy,estimator,mode,max_smact,min_free_gib,window_s,seed,trace,"
+               "total_time_s,avg_wait_s,avg_exec_s,avg_jct_s,oom_count,energy_mj")  # metrics.cpp:106-109
+
+
+def _csv_row(rep: RunReport, seed_field: str) -> str:
+    """runner.cpp:169-185 (printf formats reproduced with Python's % operator)."""
+    c = rep.config
+    min_free = "%.2f" % (c.min_free_mem / float(abi.GiB)) if c.min_free_mem is not None else "none"
+    return "%s,%s,%s,%.2f,%s,%.0f,%s,%s,%.3f,%.3f,%.3f,%.3f,%d,%.2f" % (
+        c.policy, c.estimator, c.collocation_mode, c.max_smact, min_free, c.monitor_window, seed_field,
+        rep.trace_name, rep.trace_total_time, rep.avg_wait, rep.avg_exec, rep.avg_jct, rep.oom_count,
+        rep.energy_mj)
+
+
+def run_sweep(config: SweepConfig, device: int = 0, knn: Optional[GpuKnn] = None) -> SweepResult:
+    """run_sweep (runner.cpp:192-283) on the GPU: every (cell, seed) run is one
+    replay job of a single plan; any failed run aborts the sweep with the
+    reference's message. Traces come from config.base (mix or trace file)."""
+    if not config.cells:
+        raise abi.CarmaError(abi.CARMA_ERR_INVALID, "ConfigError: sweep has no cells")
+    if not config.seeds:
+        raise abi.CarmaError(abi.CARMA_ERR_INVALID, "ConfigError: sweep has no seeds")
+    base = config.base
+    own_knn = knn is None and any(c.policy.estimator == "learned" for c in config.cells)
+    if own_knn:
+        knn = GpuKnn(device)
+    task_lists, trace_of, names = [], {}, {}
+    try:
+        for seed in config.seeds:
+            if base.trace_path:
+                trace, name = load_trace(base.trace_path), base.trace_path
+            else:
+                trace, name = generate_trace(base.mix, seed), f"{base.mix}-seed{seed}"
+            names[seed] = name
+            m = None
+            for cell in config.cells:
+                key = (seed, cell.policy.estimator, cell.policy.safety_margin)
+                if key in trace_of:
+                    continue
+                m = materialize_trace(trace) if m is None else m
+                mm = dataclasses.replace(m, tasks=m.tasks.copy())
+                rc = dataclasses.replace(base, policy=cell.policy, trace_seed=seed)
+                provision_estimates(rc, mm, device, knn)
+                trace_of[key] = len(task_lists)
+                task_lists.append(mm.tasks)
+        cfgs = np.concatenate([make_config(c.policy, base.constants, base.mig_instances) for c in config.cells])
+        jobs = [(trace_of[(seed, c.policy.estimator, c.policy.safety_margin)], ci)
+                for ci, c in enumerate(config.cells) for seed in config.seeds]
+        offs = np.concatenate([[0], np.cumsum([len(t) for t in task_lists])]).astype(np.uint64)
+        jarr = np.array(jobs, dtype=np.uint32).reshape(-1, 2)
+        j = np.zeros(len(jarr), abi.job_dtype)
+        j["trace"], j["config"] = jarr[:, 0], jarr[:, 1]
+        plan = ReplayPlan(cfgs, np.concatenate(task_lists), offs, j, device)
+        try:
+            plan.run()
+            res = plan.results(tasks=False)
+        finally:
+            plan.close()
+    finally:
+        if own_knn:
+            knn.close()
+    reports, k = [], 0
+    for ci, cell in enumerate(config.cells):
+        row = []
+        for seed in config.seeds:
+            t = res.traces[k]
+            if int(t["status"]) != 0:
+                label = cell.label or cell.policy.policy
+                raise abi.CarmaError(abi.CARMA_ERR_INCOMPLETE if int(t["status"]) == abi.CARMA_ERR_INCOMPLETE
+                                     else abi.CARMA_ERR_INVALID,
+                                     f"sweep cell '{label}' seed {seed} failed: status {int(t['status'])}")
+            row.append(RunReport(names[seed], cell.policy, float(t["trace_total_time"]), float(t["avg_wait"]),
+                                 float(t["avg_exec"]), float(t["avg_jct"]), int(t["oom_count"]),
+                                 float(t["energy_mj"])))
+            k += 1
+        reports.append(row)
+    lines = [_CSV_HEADER]
+    for row in reports:
+        lines += [_csv_row(r, str(seed)) for r, seed in zip(row, config.seeds)]
+        if len(config.seeds) > 1:  # metric-wise medians (runner.cpp:258-276)
+            med = dataclasses.replace(
+                row[0], trace_total_time=median([r.trace_total_time for r in row]),
+                avg_wait=median([r.avg_wait for r in row]), avg_exec=median([r.avg_exec for r in row]),
+                avg_jct=median([r.avg_jct for r in row]),
+                oom_count=int(math.floor(median([float(r.oom_count) for r in row]) + 0.5)),  # llround, >= 0
+                energy_mj=median([r.energy_mj for r in row]))
+            lines.append(_csv_row(med, "median"))
+    return SweepResult(reports, "\n".join(lines) + "\n")
+
+
 def median(values) -> float:
     """runner.cpp:149-155"""
     v = sorted(values)

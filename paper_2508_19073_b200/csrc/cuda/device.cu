@@ -1,5 +1,7 @@
 // Device discovery, error reporting and small runtime helpers.
 
+#include <atomic>
+#include <cstdint>
 #include <string>
 
 #include "../../../include/carma_gpu.h"
@@ -13,7 +15,11 @@ thread_local std::string g_last_error;
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
+// Checked once per device and cached: cudaGetDeviceProperties costs
+// milliseconds, and every compute entry point calls this.
 void require_device(int device) {
+    static std::atomic<uint64_t> ok_mask{0};
+    if (device >= 0 && device < 64 && ((ok_mask.load(std::memory_order_relaxed) >> device) & 1ull)) return;
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
     if (e != cudaSuccess || n == 0)
@@ -21,11 +27,13 @@ void require_device(int device) {
                           (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
                           "); the CARMA GPU path has no CPU fallback");
     if (device < 0 || device >= n) throw InvalidArg("device index out of range");
-    cudaDeviceProp prop;
-    CARMA_CUDA(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10)
-        throw CudaFailure("device " + std::to_string(device) + " is sm_" + std::to_string(prop.major) +
-                          std::to_string(prop.minor) + "; this build targets sm_100a only");
+    int major = 0, minor = 0;
+    CARMA_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CARMA_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10)
+        throw CudaFailure("device " + std::to_string(device) + " is sm_" + std::to_string(major) +
+                          std::to_string(minor) + "; this build targets sm_100a only");
+    if (device < 64) ok_mask.fetch_or(1ull << device, std::memory_order_relaxed);
 }
 
 bool is_pinned(const void* p) {
@@ -53,8 +61,9 @@ int carma_device_count(void) {
     }
     int usable = 0;
     for (int d = 0; d < n; ++d) {
-        cudaDeviceProp prop;
-        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10) ++usable;
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) == cudaSuccess && major == 10)
+            ++usable;
     }
     return usable;
 }

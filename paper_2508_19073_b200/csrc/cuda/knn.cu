@@ -870,7 +870,13 @@ __global__ void __launch_bounds__(128, 4)
                 const bool need_r = mine && R < n && tr <= kth;
                 const unsigned bl = __ballot_sync(0xffffffffu, need_l);
                 const unsigned br = __ballot_sync(0xffffffffu, need_r);
-                if ((bl | br) == 0) break;
+                const bool done = (bl | br) == 0;
+                // Phase B at one code site: at the end, and whenever a lane
+                // could not buffer a whole block.
+                if (done || __any_sync(0xffffffffu, cnt > kCandCap - kBlock)) {
+                    flush();
+                    if (done) break;
+                }
                 const double rl = __shfl_sync(0xffffffffu, need_l ? tl : inf, mid_lane);
                 const double rr = __shfl_sync(0xffffffffu, need_r ? tr : inf, mid_lane);
                 const bool go_left = bl != 0 && (br == 0 || rl <= rr);
@@ -952,13 +958,6 @@ __global__ void __launch_bounds__(128, 4)
                     for (int c = 0; c < kBlock; ++c) cand |= !(sf[c] > T_lb) ? (1u << c) : 0u;
                     cand &= valid;
                 }
-                // Keep room for a whole block in every lane's buffer.
-                if (__any_sync(0xffffffffu, cnt > kCandCap - kBlock)) {
-                    flush();
-#pragma unroll
-                    for (int c = 0; c < kBlock; ++c)
-                        if (sf[c] > T_lb) cand &= ~(1u << c);
-                }
                 if (cand) {
 #pragma unroll
                     for (int c = 0; c < kBlock; ++c) {
@@ -972,7 +971,6 @@ __global__ void __launch_bounds__(128, 4)
                 if (go_left) tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q18) : t_in) : inf;
                 else tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q18) : t_in) : inf;
             }
-            flush();
             my_visits += visits;
             my_exact += exact;
 

@@ -149,4 +149,69 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
     return static_cast<int>(want);
 }
 
+// One decision by one thread over its n (<= 16) GPU views (the batched
+// scoring kernel for small servers: no shuffles, the views are staged in
+// shared memory by the warp with coalesced loads). Same rules and tie
+// breaks as pick_gpus: exclusive = first `want` idle GPUs; RR = cyclic scan
+// from the cursor; MAGM/LUG/MUG = the `want` best keys, ties to the lower id.
+__device__ __forceinline__ int pick_serial(const carma_replay_config& c, int policy, uint32_t want,
+                                           uint64_t need_floor, const carma_gpu_view* v, int n, int& rr_cursor,
+                                           int* out) {
+    out[0] = out[1] = -1;
+    const bool rr_all = policy == CARMA_POLICY_RR && !c.rr_apply_preconditions;
+    uint32_t mask = 0;
+#pragma unroll 1
+    for (int g = 0; g < n; ++g) {
+        bool e;
+        if (policy == CARMA_POLICY_EXCLUSIVE) e = v[g].idle != 0;
+        else if (rr_all) e = true;
+        else e = !(v[g].windowed_smact > c.max_smact) && !(v[g].total_free < need_floor);
+        mask |= (e ? 1u : 0u) << g;
+    }
+    if (static_cast<uint32_t>(__popc(mask)) < want) return 0;
+    if (policy == CARMA_POLICY_EXCLUSIVE) {
+        out[0] = __ffs(mask) - 1;
+        if (want > 1) out[1] = __ffs(mask & (mask - 1)) - 1;
+        return static_cast<int>(want);
+    }
+    if (policy == CARMA_POLICY_RR) {
+        const int cur = rr_cursor;
+        const uint32_t rot = cur == 0 ? mask : ((mask >> cur) | (mask << (n - cur))) & ((n >= 32 ? 0u : (1u << n)) - 1u);
+        const int b0 = __ffs(rot) - 1 + cur;
+        out[0] = b0 >= n ? b0 - n : b0;
+        int last = out[0];
+        if (want > 1) {
+            const int b1 = __ffs(rot & (rot - 1)) - 1 + cur;
+            out[1] = b1 >= n ? b1 - n : b1;
+            last = out[1];
+        }
+        rr_cursor = last + 1 == n ? 0 : last + 1;
+        return static_cast<int>(want);
+    }
+    // MAGM / LUG / MUG: stable sort by key, ties to the lower id == arg-best
+    // (strictly better key wins; the scan is in id order).
+    int best0 = -1, best1 = -1;
+    uint64_t k0 = 0, k1 = 0;
+#pragma unroll 1
+    for (int g = 0; g < n; ++g) {
+        if (!((mask >> g) & 1u)) continue;
+        PickInput in;
+        in.free_bytes = v[g].total_free;
+        in.smact = v[g].windowed_smact;
+        const uint64_t k = policy_key(policy, in);
+        if (best0 < 0 || k > k0) {
+            best1 = best0;
+            k1 = k0;
+            best0 = g;
+            k0 = k;
+        } else if (best1 < 0 || k > k1) {
+            best1 = g;
+            k1 = k;
+        }
+    }
+    out[0] = best0;
+    if (want > 1) out[1] = best1;
+    return static_cast<int>(want);
+}
+
 }  // namespace carma_b200

@@ -64,6 +64,63 @@ __global__ void pick_kernel(carma_replay_config cf, const carma_gpu_view* __rest
     }
 }
 
+// Batched carma_pick_batch for n_gpus <= 16: one thread per decision. Each
+// warp streams its chunks of 32 decisions' views (32 * n_gpus * 24
+// contiguous bytes) into shared memory with asynchronous 16-byte copies
+// (LDGSTS), then every lane scores its own decision serially — no shuffles,
+// so the kernel streams at HBM speed (a double-buffered variant was slower:
+// the doubled shared memory cost more occupancy than the overlap gained).
+constexpr int kPickWarps = 4;
+constexpr int kPickMaxSerialGpus = 16;
+
+__device__ __forceinline__ void pick_stage(carma_gpu_view* sv, const carma_gpu_view* src_views, uint32_t bytes,
+                                           unsigned lane) {
+    const char* src = reinterpret_cast<const char*>(src_views);
+    if ((bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(sv));
+        for (uint32_t i = lane * 16; i < bytes; i += 32 * 16)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s0 + i), "l"(src + i) : "memory");
+    } else {  // unaligned tail chunk: plain 8-byte loads
+        const uint64_t* s8 = reinterpret_cast<const uint64_t*>(src);
+        uint64_t* dst = reinterpret_cast<uint64_t*>(sv);
+        for (uint32_t i = lane; i < bytes / 8; i += 32) dst[i] = __ldg(s8 + i);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(32 * kPickWarps) pick_kernel_thread(
+    carma_replay_config cf, const carma_gpu_view* __restrict__ views, uint32_t n_gpus,
+    const carma_pick_request* __restrict__ reqs, uint64_t n, int32_t* __restrict__ cursor,
+    int32_t* __restrict__ out) {
+    extern __shared__ __align__(16) char pick_smem[];
+    const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    carma_gpu_view* sv = reinterpret_cast<carma_gpu_view*>(pick_smem) + static_cast<size_t>(wib) * 32 * n_gpus;
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t base = warp * 32; base < n; base += n_warps * 32) {
+        const uint32_t cnt = static_cast<uint32_t>(n - base < 32 ? n - base : 32);
+        pick_stage(sv, views + base * n_gpus, cnt * n_gpus * static_cast<uint32_t>(sizeof(carma_gpu_view)), lane);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        if (lane < cnt) {
+            const uint64_t d = base + lane;
+            const carma_pick_request rq = reqs[d];
+            int cur = cursor[d];
+            const int policy = rq.from_recovery ? CARMA_POLICY_EXCLUSIVE : cf.policy;
+            uint64_t floor = cf.min_free;
+            if (!rq.from_recovery && cf.policy != CARMA_POLICY_EXCLUSIVE && rq.estimate != CARMA_NO_ESTIMATE) {
+                const uint64_t need = rq.estimate < cf.gpu_capacity ? rq.estimate : cf.gpu_capacity;
+                if (need > floor) floor = need;
+            }
+            int ids[2];
+            pick_serial(cf, policy, rq.want, floor, sv + lane * n_gpus, static_cast<int>(n_gpus), cur, ids);
+            reinterpret_cast<int2*>(out)[d] = make_int2(ids[0], ids[1]);
+            cursor[d] = cur;
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void compact_outcomes(const carma_task_result* __restrict__ in, uint64_t n,
                                  carma_task_outcome* __restrict__ out) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -514,21 +571,61 @@ carma_status carma_replay_batch(int device, const carma_replay_config* configs, 
     return st;
 }
 
+}  // extern "C"
+
+namespace carma_b200 {
+namespace {
+
+void validate_pick(const carma_replay_config* cfg, uint32_t n_gpus) {
+    if (!cfg) throw InvalidArg("null config");
+    if (n_gpus < 1 || n_gpus > CARMA_MAX_GPUS) throw Unsupported("n_gpus must be in [1, 64]");
+    if (cfg->mode == CARMA_MODE_MIG) throw Unsupported("carma_pick_batch: MIG needs per-instance views; use the replay");
+}
+
+// One launch over device-resident views / requests / cursors / outputs.
+void launch_pick(const carma_replay_config& cfg, const carma_gpu_view* views, uint32_t n_gpus,
+                 const carma_pick_request* reqs, uint64_t n, int32_t* cursor, int32_t* out, cudaStream_t s) {
+    carma_replay_config c = cfg;
+    c.gpu_count = static_cast<int32_t>(n_gpus);
+    if (n_gpus <= static_cast<uint32_t>(kPickMaxSerialGpus)) {
+        const size_t shmem = static_cast<size_t>(kPickWarps) * 32 * n_gpus * sizeof(carma_gpu_view);
+        if (shmem > 48 * 1024)
+            CARMA_CUDA(cudaFuncSetAttribute(pick_kernel_thread, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(shmem)));
+        const uint64_t warps = (n + 31) / 32;
+        const unsigned grid = grid_for(warps * 32, 32 * kPickWarps, 148u * 32u);
+        pick_kernel_thread<<<grid, 32 * kPickWarps, shmem, s>>>(c, views, n_gpus, reqs, n, cursor, out);
+        CARMA_CUDA(cudaGetLastError());
+        return;
+    }
+    unsigned width = 1;
+    while (width < n_gpus && width < 32) width <<= 1;
+    const unsigned groups_per_warp = 32 / width;
+    const uint64_t warps = (n + groups_per_warp - 1) / groups_per_warp;
+    const unsigned grid = grid_for(warps * 32, 256, 148u * 16u);
+    if (n_gpus > 32)
+        pick_kernel<2><<<grid, 256, 0, s>>>(c, views, n_gpus, reqs, n, cursor, out, width);
+    else
+        pick_kernel<1><<<grid, 256, 0, s>>>(c, views, n_gpus, reqs, n, cursor, out, width);
+    CARMA_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+}  // namespace carma_b200
+
+extern "C" {
+
 carma_status carma_pick_batch(int device, const carma_replay_config* cfg, const carma_gpu_view* views,
                               uint32_t n_gpus, const carma_pick_request* reqs, uint64_t n, int32_t* rr_cursor,
                               int32_t* out_gpus) {
     return guarded([&] {
-        if (!cfg || !views || !reqs || !rr_cursor || !out_gpus) throw InvalidArg("null argument");
-        if (n_gpus < 1 || n_gpus > CARMA_MAX_GPUS) throw Unsupported("n_gpus must be in [1, 64]");
-        if (cfg->mode == CARMA_MODE_MIG)
-            throw Unsupported("carma_pick_batch: MIG needs per-instance views; use the replay");
+        validate_pick(cfg, n_gpus);
+        if (!views || !reqs || !rr_cursor || !out_gpus) throw InvalidArg("null argument");
         if (n == 0) return;
         for (uint64_t i = 0; i < n; ++i)
             if (reqs[i].want < 1 || reqs[i].want > 2) throw Unsupported("want must be 1 or 2");
         require_device(device);
         DeviceGuard guard(device);
-        carma_replay_config c = *cfg;
-        c.gpu_count = static_cast<int32_t>(n_gpus);
         DeviceBuffer dv, dr, dc, dout;
         dv.ensure(n * n_gpus * sizeof(carma_gpu_view));
         dr.ensure(n * sizeof(carma_pick_request));
@@ -537,20 +634,23 @@ carma_status carma_pick_batch(int device, const carma_replay_config* cfg, const 
         CARMA_CUDA(cudaMemcpy(dv.ptr, views, n * n_gpus * sizeof(carma_gpu_view), cudaMemcpyHostToDevice));
         CARMA_CUDA(cudaMemcpy(dr.ptr, reqs, n * sizeof(carma_pick_request), cudaMemcpyHostToDevice));
         CARMA_CUDA(cudaMemcpy(dc.ptr, rr_cursor, n * 4, cudaMemcpyHostToDevice));
-        unsigned width = 1;
-        while (width < n_gpus && width < 32) width <<= 1;
-        const unsigned groups_per_warp = 32 / width;
-        const uint64_t warps = (n + groups_per_warp - 1) / groups_per_warp;
-        const unsigned grid = grid_for(warps * 32, 256, 148u * 16u);
-        if (n_gpus > 32)
-            pick_kernel<2><<<grid, 256>>>(c, dv.as<carma_gpu_view>(), n_gpus, dr.as<carma_pick_request>(), n,
-                                          dc.as<int32_t>(), dout.as<int32_t>(), width);
-        else
-            pick_kernel<1><<<grid, 256>>>(c, dv.as<carma_gpu_view>(), n_gpus, dr.as<carma_pick_request>(), n,
-                                          dc.as<int32_t>(), dout.as<int32_t>(), width);
-        CARMA_CUDA(cudaGetLastError());
+        launch_pick(*cfg, dv.as<carma_gpu_view>(), n_gpus, dr.as<carma_pick_request>(), n, dc.as<int32_t>(),
+                    dout.as<int32_t>(), nullptr);
         CARMA_CUDA(cudaMemcpy(out_gpus, dout.ptr, n * 8, cudaMemcpyDeviceToHost));
         CARMA_CUDA(cudaMemcpy(rr_cursor, dc.ptr, n * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+carma_status carma_pick_batch_device(int device, const carma_replay_config* cfg, const carma_gpu_view* views,
+                                     uint32_t n_gpus, const carma_pick_request* reqs, uint64_t n,
+                                     int32_t* rr_cursor, int32_t* out_gpus, void* stream) {
+    return guarded([&] {
+        validate_pick(cfg, n_gpus);
+        if (!views || !reqs || !rr_cursor || !out_gpus) throw InvalidArg("null argument");
+        if (n == 0) return;
+        require_device(device);
+        DeviceGuard guard(device);
+        launch_pick(*cfg, views, n_gpus, reqs, n, rr_cursor, out_gpus, static_cast<cudaStream_t>(stream));
     });
 }
 

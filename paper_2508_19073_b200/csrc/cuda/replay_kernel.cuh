@@ -360,6 +360,58 @@ __device__ __forceinline__ double windowed(char* b, int g, double now, double wi
     return __ddiv_rn(integral, span);
 }
 
+// windowed for a lane's two GPUs (G > 32) in lockstep: the same sums in the
+// same order per GPU, but two independent dependency chains per step.
+template <class L>
+__device__ __forceinline__ void windowed2(char* b, int g0, int g1, bool v1, double now, double window, double& o0,
+                                          double& o1) {
+    const double begin = dmax0(now - window);
+    const double span = now - begin;
+    if (span <= 0.0) {
+        o0 = RP_F64(inst)[g0];
+        o1 = v1 ? RP_F64(inst)[g1] : 0.0;
+        return;
+    }
+    const double* rt0 = RP_F64(ring_t) + g0 * L::RG;
+    const double* rv0 = RP_F64(ring_v) + g0 * L::RG;
+    const double* rt1 = RP_F64(ring_t) + g1 * L::RG;
+    const double* rv1 = RP_F64(ring_v) + g1 * L::RG;
+    double i0 = 0.0, l0 = 0.0, c0 = begin, i1 = 0.0, l1 = 0.0, c1 = begin;
+    uint32_t k0 = RP_U32(rhead)[g0], n0 = RP_U32(rcnt)[g0];
+    uint32_t k1 = RP_U32(rhead)[g1], n1 = v1 ? RP_U32(rcnt)[g1] : 0;
+#pragma unroll 1
+    while (n0 | n1) {
+        if (n0) {
+            const double t = rt0[k0], v = rv0[k0];
+            k0 = k0 + 1 == static_cast<uint32_t>(L::RG) ? 0 : k0 + 1;
+            --n0;
+            if (t >= now && !(t <= begin)) {
+                n0 = 0;
+            } else {
+                if (!(t <= begin)) i0 = __dadd_rn(i0, __dmul_rn(l0, __dsub_rn(t, c0)));
+                if (!(t <= begin)) c0 = t;
+                l0 = v;
+            }
+        }
+        if (n1) {
+            const double t = rt1[k1], v = rv1[k1];
+            k1 = k1 + 1 == static_cast<uint32_t>(L::RG) ? 0 : k1 + 1;
+            --n1;
+            if (t >= now && !(t <= begin)) {
+                n1 = 0;
+            } else {
+                if (!(t <= begin)) i1 = __dadd_rn(i1, __dmul_rn(l1, __dsub_rn(t, c1)));
+                if (!(t <= begin)) c1 = t;
+                l1 = v;
+            }
+        }
+    }
+    i0 = __dadd_rn(i0, __dmul_rn(l0, __dsub_rn(now, c0)));
+    i1 = __dadd_rn(i1, __dmul_rn(l1, __dsub_rn(now, c1)));
+    o0 = __ddiv_rn(i0, span);
+    o1 = v1 ? __ddiv_rn(i1, span) : 0.0;
+}
+
 // effective_rates / instantaneous_smact / power_draw (gpu.cpp:183-229,
 // 269-274) for GPU g after its resident list changed, then record_smact
 // (gpu.cpp:231-242) into the ring and the full-history integrator.
@@ -703,7 +755,7 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
         in[j].valid = valid;
         in[j].idle = valid && nres[g] == 0;
         in[j].free_bytes = valid ? static_cast<uint64_t>(free_blocks<L>(used, g)) * cf.alloc_block : 0;
-        in[j].smact = (valid && need_smact) ? windowed<L>(b, g, c.now, c.window) : 0.0;
+        if (L::GPL == 1) in[j].smact = (valid && need_smact) ? windowed<L>(b, g, c.now, c.window) : 0.0;
         in[j].inst_ok = true;
         inst[j] = -1;
         if (mig && valid) {
@@ -720,6 +772,12 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
             }
             in[j].inst_ok = inst[j] >= 0;
         }
+    }
+    if constexpr (L::GPL == 2) {
+        double s0 = 0.0, s1 = 0.0;
+        if (need_smact && in[0].valid) windowed2<L>(b, lane, lane + 32, in[1].valid, c.now, c.window, s0, s1);
+        in[0].smact = s0;
+        in[1].smact = s1;
     }
     int gids[2];
     const int got = pick_gpus<L::GPL>(cf, policy, tasks[head].gpus, floor, in, lane, 0, 32, c.rr_cursor, gids);

@@ -94,9 +94,28 @@ def fused(args):
     print("oom", r["oom_count"], "events", r["events"], "makespan", r["trace_total_time"], "status", r["status"])
 
 
+def scoring(args):
+    """The bench's scoring workload (bench.scoring_bench) once per rep."""
+    import torch
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class One:
+        n = 1
+
+        def barrier(self):
+            pass
+
+        def max(self, x):
+            return x
+
+    r = bench.scoring_bench(abi, cb, 0, torch.cuda.current_stream(), 1, args.reps, One())
+    print(f"scoring: {r['ms_per_step']:.3f} ms, {r['roofline']['achieved']:.0f} GB/s", flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=("replay", "knn", "fused"))
+    ap.add_argument("what", choices=("replay", "knn", "fused", "scoring"))
     ap.add_argument("--tasks", type=int, default=1_000_000)
     ap.add_argument("--traces", type=int, default=20000)
     ap.add_argument("--policies", default="exclusive,rr,magm,lug")
@@ -104,4 +123,4 @@ if __name__ == "__main__":
     ap.add_argument("--format", choices=("rows", "bitpacked"), default="bitpacked")
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
-    {"replay": replay, "knn": knn, "fused": fused}[a.what](a)
+    {"replay": replay, "knn": knn, "fused": fused, "scoring": scoring}[a.what](a)

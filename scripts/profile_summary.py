@@ -69,7 +69,8 @@ def launches(path):
         d = dict(zip(hdr, r))
         if d.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        name = d["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")
+        name = d["Kernel Name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+        name = name.replace("void ", "").split("(")[0].split("<")[0]
         v = float(d["Metric Value"].replace(",", ""))
         unit = d["Metric Unit"]
         v = v / 1e3 if unit == "nsecond" else v * 1e3 if unit == "msecond" else v  # -> usecond

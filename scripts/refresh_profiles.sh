@@ -14,3 +14,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:knn_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:replay_kernel -s 2 -c 1 \
     -o $OUT/replay_kernel_full -f python scripts/profile_driver.py replay --traces 100000 --reps 2 > $OUT/ncu_replay.log 2>&1
 tail -2 $OUT/bench.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:pick_kernel -s 1 -c 1 \
+    -o $OUT/pick_kernel_full -f python scripts/profile_driver.py scoring --reps 2 > $OUT/ncu_pick.log 2>&1

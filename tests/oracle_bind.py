@@ -60,6 +60,7 @@ def load_ref():
     lib.ref_bench_sweep.restype = c_double
     lib.ref_bench_sweep.argtypes = [P, c_int, c_uint64, c_uint64, P, c_int, c_int, POINTER(c_uint64),
                                     POINTER(c_double)]
+    lib.ref_run_sweep.argtypes = [P, c_int, c_int, P, c_int, c_char_p, c_uint64]
     return lib
 
 

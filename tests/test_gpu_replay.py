@@ -260,3 +260,32 @@ def test_replay_mig_matches_oracle(gpu, olib, models):
     assert (res.traces["oom_count"] > 0).any()  # the instance limits bite
     check_jobs(olib, res, cfgs, task_lists, jobs)
 
+
+
+def test_pick_batch_device_matches_host_path(gpu, olib):
+    """carma_pick_batch_device on device-resident arrays (the bench's scoring
+    workload shape) equals the host-buffer path decision for decision."""
+    import torch
+    rng = np.random.default_rng(7)
+    for g in (4, 8, 64):
+        n = 50000
+        views = np.zeros((n, g), abi.gpu_view_dtype)
+        views["total_free"] = rng.integers(0, 81, (n, g)).astype(np.uint64) * (512 * abi.MiB)
+        views["windowed_smact"] = rng.random((n, g))
+        views["idle"] = rng.random((n, g)) < 0.3
+        reqs = np.zeros(n, abi.pick_request_dtype)
+        reqs["estimate"] = rng.integers(0, 45, n).astype(np.uint64) * abi.GiB
+        reqs["want"] = np.where(rng.random(n) < 0.2, 2, 1).astype(np.uint32)
+        cursor = rng.integers(0, g, n).astype(np.int32)
+        for policy in ("rr", "magm", "lug"):
+            cfg = cfg_of(policy, gpu_count=g, rr_pre=True)
+            out, cur = cb.pick_batch(cfg, views, reqs, cursor)
+            dv = torch.from_numpy(views.view(np.uint8).reshape(-1)).cuda()
+            dr = torch.from_numpy(reqs.view(np.uint8).reshape(-1)).cuda()
+            dc = torch.from_numpy(cursor.copy()).cuda()
+            do = torch.empty(2 * n, dtype=torch.int32, device="cuda")
+            abi.check(abi.lib.carma_pick_batch_device(gpu, cfg.ctypes.data, dv.data_ptr(), g, dr.data_ptr(), n,
+                                                      dc.data_ptr(), do.data_ptr(), None))
+            torch.cuda.synchronize()
+            assert np.array_equal(do.cpu().numpy().reshape(n, 2), out), (g, policy)
+            assert np.array_equal(dc.cpu().numpy(), cur), (g, policy)
