@@ -223,7 +223,13 @@ typedef struct carma_replay_config {
     double mig_fraction[CARMA_MAX_MIG];
     uint16_t mig_base[CARMA_MAX_MIG];
     uint16_t mig_blocks[CARMA_MAX_MIG];
-} carma_replay_config; /* 200 bytes */
+    /* RunConfig::enable_timeline / sample_interval (runner.hpp:32-33): > 0
+     * schedules sample ticks from the first trace row's submit time every
+     * sample_interval seconds while any submitted task is unfinished
+     * (runner.cpp:80-93). Ticks are events (energy-integration breakpoints),
+     * so they change the run exactly as in the reference. 0 = off. */
+    double sample_interval;
+} carma_replay_config; /* 208 bytes */
 
 /* One materialised task (TaskSpec, task.hpp:63-80) as the replay sees it. */
 typedef struct carma_task {
@@ -295,6 +301,25 @@ carma_status carma_replay_plan_set_estimates_device(carma_replay_plan* p, const 
 carma_status carma_replay_plan_upload_tasks(carma_replay_plan* p, const carma_task* tasks);
 /* Runs all jobs on the device (inputs resident). stream: cudaStream_t or NULL. */
 carma_status carma_replay_plan_run(carma_replay_plan* p, void* stream);
+/* One timeline row per GPU per sample tick: World::emit_timeline_row
+ * (world.cpp:210-219) before formatting ("%.3f,%d,%.4f,%llu,%.2f"). */
+typedef struct carma_timeline_row {
+    double t;        /* World::now() */
+    double smact;    /* instantaneous_smact() */
+    double power_w;  /* power_draw() */
+    uint64_t used;   /* used_bytes() */
+    int32_t gpu;
+    int32_t reserved;
+} carma_timeline_row; /* 40 bytes */
+
+/* Device capacity for timeline rows of every job whose config has
+ * sample_interval > 0 (call before carma_replay_plan_run). A job that
+ * produces more rows keeps running; its extra rows are counted, not stored. */
+carma_status carma_replay_plan_set_timeline_capacity(carma_replay_plan* p, uint64_t rows_per_job);
+/* Rows of job j (host buffer of cap rows); *n_rows = rows produced (may
+ * exceed cap: then only cap were kept). */
+carma_status carma_replay_plan_timeline(carma_replay_plan* p, uint32_t job, carma_timeline_row* rows,
+                                        uint64_t cap, uint64_t* n_rows);
 carma_status carma_replay_plan_results(carma_replay_plan* p, carma_task_result* tasks,
                                        carma_trace_result* traces, carma_gpu_result* gpus);
 /* Kernel launches of the last run and the state tier each job finished in. */

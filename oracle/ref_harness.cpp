@@ -308,6 +308,7 @@ struct RefConfig {
     int32_t mig_count;         // RunConfig::mig_instances (runner.hpp:23)
     int32_t mig_reserved;
     double mig_fractions[8];
+    double sample_interval;    // > 0: RunConfig::enable_timeline with this interval
 };
 
 struct RefTaskOut {
@@ -354,6 +355,10 @@ RunConfig make_rc(const RefConfig& c) {
     rc.estimator_k = c.estimator_k;
     rc.estimator_samples = c.estimator_samples;
     for (int i = 0; i < c.mig_count && i < 8; ++i) rc.mig_instances.push_back(c.mig_fractions[i]);
+    if (c.sample_interval > 0.0) {
+        rc.enable_timeline = true;
+        rc.sample_interval = c.sample_interval;
+    }
     return rc;
 }
 
@@ -463,6 +468,24 @@ double ref_bench_sweep(const RefConfig* base, int mix, uint64_t seed0, uint64_t 
     } catch (const std::exception& e) {
         fail(e);
         return -1.0;
+    }
+}
+
+// The timeline of one run (RunArtifacts::timeline, header included),
+// newline-joined into buf[cap].
+int ref_timeline(const RefConfig* cfg, int mix, uint64_t seed, char* buf, uint64_t cap) {
+    try {
+        RunConfig rc = make_rc(*cfg);
+        rc.mix = static_cast<TraceMix>(mix);
+        rc.trace_seed = seed;
+        RunArtifacts art = run_simulation(rc);
+        std::string out;
+        for (const auto& l : art.timeline) out += l + "\n";
+        if (out.size() + 1 > cap) throw CarmaError("timeline buffer too small");
+        std::memcpy(buf, out.c_str(), out.size() + 1);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
     }
 }
 

@@ -362,8 +362,10 @@ class PolicyConfig:
     rr_apply_preconditions: bool = False
 
 
-def make_config(policy: PolicyConfig, consts: SimConstants, mig_instances: Optional[Sequence[float]] = None) -> np.ndarray:
-    """carma_replay_config of a PolicyConfig + SimConstants (+ RunConfig::mig_instances, runner.hpp:23)."""
+def make_config(policy: PolicyConfig, consts: SimConstants, mig_instances: Optional[Sequence[float]] = None,
+                sample_interval: float = 0.0) -> np.ndarray:
+    """carma_replay_config of a PolicyConfig + SimConstants (+ RunConfig::mig_instances and, when > 0,
+    the timeline's sample_interval, runner.hpp:23-33)."""
     c = np.zeros(1, abi.replay_config_dtype)
     c["policy"] = abi.POLICY[policy.policy]
     c["mode"] = abi.MODE[policy.collocation_mode]
@@ -379,6 +381,7 @@ def make_config(policy: PolicyConfig, consts: SimConstants, mig_instances: Optio
     c["p_boost_w"] = consts.p_boost_w
     c["boost_threshold"] = consts.boost_threshold
     c["oom_startup_delay"] = consts.oom_startup_delay
+    c["sample_interval"] = sample_interval
     if policy.collocation_mode == "mig":
         fr = np.ascontiguousarray([] if mig_instances is None else mig_instances, np.float64)
         check(lib.carma_mig_layout(ptr(fr) if len(fr) else None, len(fr), ptr(c)))
@@ -443,6 +446,19 @@ class ReplayPlan:
         check(lib.carma_replay_plan_results(self._h, ptr(tr) if tasks else None, ptr(jr), ptr(gr)))
         return ReplayResult(tr, jr, gr, self.task_offsets, self.gpu_offsets)
 
+    def set_timeline_capacity(self, rows_per_job: int) -> None:
+        check(lib.carma_replay_plan_set_timeline_capacity(self._h, rows_per_job))
+
+    def timeline(self, job: int) -> np.ndarray:
+        """Timeline rows of `job` (timeline_row_dtype); raises if rows were dropped."""
+        n = ctypes.c_uint64()
+        check(lib.carma_replay_plan_timeline(self._h, job, None, 0, ctypes.byref(n)))
+        rows = np.zeros(n.value, abi.timeline_row_dtype)
+        check(lib.carma_replay_plan_timeline(self._h, job, ptr(rows), n.value, ctypes.byref(n)))
+        if n.value > len(rows):
+            raise abi.CarmaError(abi.CARMA_ERR_OVERFLOW, f"timeline capacity too small ({n.value} rows)")
+        return rows
+
     def stats(self):
         la, rt = ctypes.c_uint64(), ctypes.c_uint64()
         check(lib.carma_replay_plan_stats(self._h, ctypes.byref(la), ctypes.byref(rt)))
@@ -501,6 +517,8 @@ class RunConfig:
     estimator_k: int = 5
     estimator_samples: int = 4000
     mig_instances: List[float] = dataclasses.field(default_factory=list)  # fractions, mig mode only
+    enable_timeline: bool = False
+    sample_interval: float = 10.0
 
 
 def provision_estimates(rc: RunConfig, m: Materialized, device: int = 0,
@@ -527,6 +545,51 @@ def run_simulation(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None)
     provision_estimates(rc, m, device, knn)
     res = replay(make_config(rc.policy, rc.constants, rc.mig_instances), [m.tasks], device=device)
     return res.traces[0], res.job_tasks(0), res.job_gpus(0)
+
+
+TIMELINE_HEADER = "t,gpu,smact,mem_used_bytes,power_w"  # runner.cpp:81
+
+
+def format_timeline(rows: np.ndarray) -> List[str]:
+    """World::emit_timeline_row's text (world.cpp:210-219), header first."""
+    return [TIMELINE_HEADER] + ["%.3f,%d,%.4f,%d,%.2f" % (r["t"], r["gpu"], r["smact"], r["used"], r["power_w"])
+                                for r in rows]
+
+
+@dataclasses.dataclass
+class RunArtifacts:
+    """run_simulation's artifacts (runner.hpp:38-47): report scalars, per-task and per-GPU results,
+    and the timeline text when RunConfig.enable_timeline is set."""
+
+    report: np.ndarray
+    tasks: np.ndarray
+    gpus: np.ndarray
+    timeline: List[str]
+
+
+def run_simulation_artifacts(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None,
+                             timeline_rows: int = 1 << 20) -> RunArtifacts:
+    """run_simulation with the reference's output switches: the sample ticks of
+    enable_timeline are events of the replay (they split the energy integration
+    exactly as in the reference), their rows come back formatted."""
+    trace = load_trace(rc.trace_path) if rc.trace_path else generate_trace(rc.mix, rc.trace_seed)
+    m = materialize_trace(trace)
+    provision_estimates(rc, m, device, knn)
+    cfg = make_config(rc.policy, rc.constants, rc.mig_instances, rc.sample_interval if rc.enable_timeline else 0.0)
+    jobs = np.zeros(1, abi.job_dtype)
+    plan = ReplayPlan(cfg, m.tasks, np.array([0, len(m.tasks)], np.uint64), jobs, device)
+    try:
+        if rc.enable_timeline:
+            plan.set_timeline_capacity(timeline_rows)
+        plan.run()
+        res = plan.results()
+        tl = format_timeline(plan.timeline(0)) if rc.enable_timeline else []
+    finally:
+        plan.close()
+    st = int(res.traces["status"][0])
+    if st != 0:
+        raise abi.CarmaError(3 if st < 0 else st, f"run failed (status {st})")
+    return RunArtifacts(res.traces[0], res.job_tasks(0), res.job_gpus(0), tl)
 
 
 class FusedReplay:

@@ -147,11 +147,13 @@ struct ReplayPlan {
     uint64_t n_tasks = 0, n_task_out = 0, n_gpu_out = 0;
     int max_g = 1;
     int max_blocks = 1;
-    uint32_t class_count[6] = {0, 0, 0, 0, 0, 0};
-    int class_max_g[6] = {1, 1, 1, 1, 1, 1};
-    std::vector<uint32_t> class_list;  // jobs ordered: light, heavy, global-only
+    // classes 3F + {light, heavy, global-only} for feature bits F (1 = MIG, 2 = timeline)
+    uint32_t class_count[12] = {};
+    int class_max_g[12] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+    std::vector<uint32_t> class_list;  // jobs ordered by class
     DeviceBuffer d_cfgs, d_tasks, d_trace_off, d_jobs, d_task_off, d_gpu_off, d_list, d_task_out,
-        d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate, d_outcomes;
+        d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate, d_outcomes, d_tl, d_tl_count;
+    uint64_t tl_cap = 0;
     const uint64_t* est_override = nullptr;
     uint64_t launches = 0, retried = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // run start, shared-memory tiers end, run end
@@ -166,13 +168,15 @@ using replay::Layout;
 // at <= 34 pending events and 8 residents; RR without preconditions stacks
 // up to 34 residents (11 per GPU) and ~200 pending events (stale completion
 // events stay queued: they are energy-integration breakpoints).
-// M = MIG collocation: those jobs run in their own kernels (classes 3..5).
-template <int G, bool M> using LightL = Layout<G, 64, 32, 16, 16, 16, 2, M>;
-template <int G, bool M> using HeavyL = Layout<G, 320, 64, 32, 16, 16, 2, M>;
+// F = feature bits (1 = MIG collocation, 2 = timeline ticks): those jobs run in
+// their own kernel instantiations (classes 3F..3F+2); timeline jobs use the
+// large and global tiers only.
+template <int G, int F> using LightL = Layout<G, 64, 32, 16, 16, 16, 2, F>;
+template <int G, int F> using HeavyL = Layout<G, 320, 64, 32, 16, 16, 2, F>;
 // Large shared-memory tier for long traces on many GPUs (c5: 10^6 tasks on
 // 64 GPUs peaks at 128 residents and ~215 pending events): one warp per CTA.
-template <bool M> using LargeL = Layout<64, 1024, 256, 32, 16, 128, 2, M>;
-template <bool M> using GlobalL = Layout<64, 8192, 2048, 256, 256, 4096, 4, M>;
+template <int F> using LargeL = Layout<64, 1024, 256, 32, 16, 128, 2, F>;
+template <int F> using GlobalL = Layout<64, 8192, 2048, 256, 256, 4096, 4, F>;
 
 // Configs whose policy can stack tasks without utilisation preconditions.
 bool heavy_config(const carma_replay_config& c) {
@@ -191,6 +195,7 @@ void validate_config(const carma_replay_config& c) {
         throw Unsupported("gpu_capacity must be a multiple of alloc_block");
     if (c.gpu_capacity / c.alloc_block > 64ull * replay::kMaxWords)
         throw Unsupported("more than 256 allocation blocks per GPU");
+    if (!(c.sample_interval >= 0.0)) throw InvalidArg("ConfigError: sample_interval must be >= 0");
     if (c.mode == CARMA_MODE_MIG) {
         // the table carma_mig_layout builds (gpu.cpp:29-51)
         if (c.mig_count < 1 || c.mig_count > CARMA_MAX_MIG)
@@ -229,18 +234,18 @@ void launch(ReplayPlan& pl, replay::Params p, int sms, int warps_per_cta = 4) {
     pl.launches++;
 }
 
-template <template <int, bool> class LL, bool M>
+template <template <int, int> class LL, int F>
 void launch_shared(ReplayPlan& pl, const replay::Params& p, int max_g, int sms) {
-    if (max_g <= 4) launch<LL<4, M>, true>(pl, p, sms);
-    else if (max_g <= 8) launch<LL<8, M>, true>(pl, p, sms);
-    else if (max_g <= 16) launch<LL<16, M>, true>(pl, p, sms);
-    else if (max_g <= 32) launch<LL<32, M>, true>(pl, p, sms);
-    else launch<LL<64, M>, true>(pl, p, sms);
+    if (max_g <= 4) launch<LL<4, F>, true>(pl, p, sms);
+    else if (max_g <= 8) launch<LL<8, F>, true>(pl, p, sms);
+    else if (max_g <= 16) launch<LL<16, F>, true>(pl, p, sms);
+    else if (max_g <= 32) launch<LL<32, F>, true>(pl, p, sms);
+    else launch<LL<64, F>, true>(pl, p, sms);
 }
 
 // tier 0 = light shared-memory layout, 1 = heavy shared-memory, 2 = global
 // memory, 3 = large shared-memory (one warp per CTA)
-template <bool M>
+template <int F>
 void launch_tier(ReplayPlan& pl, const replay::Params& base, const uint32_t* list_dev, uint32_t n_list, int tier,
                  int max_g, uint32_t* counters, uint32_t* retry_base) {
     replay::Params p = base;
@@ -252,27 +257,30 @@ void launch_tier(ReplayPlan& pl, const replay::Params& base, const uint32_t* lis
     CARMA_CUDA(cudaMemsetAsync(counters, 0, 8, pl.stream));
     int sms = 148;
     CARMA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl.device));
-    if (tier == 0) launch_shared<LightL, M>(pl, p, max_g, sms);
-    else if (tier == 1) launch_shared<HeavyL, M>(pl, p, max_g, sms);
-    else if (tier == 3) launch<LargeL<M>, true>(pl, p, sms, 1);
-    else launch<GlobalL<M>, false>(pl, p, sms);
+    if constexpr ((F & 2) == 0) {
+        if (tier == 0) return launch_shared<LightL, F>(pl, p, max_g, sms);
+        if (tier == 1) return launch_shared<HeavyL, F>(pl, p, max_g, sms);
+    }
+    if (tier == 3) launch<LargeL<F>, true>(pl, p, sms, 1);
+    else launch<GlobalL<F>, false>(pl, p, sms);
 }
 
 // One collocation group (classes cb..cb+2, jobs list[off0, ...)): the two
 // shared-memory classes, then overflowed and global-only jobs through the
 // large shared-memory tier and the global-memory tier.
-template <bool M>
-bool run_group(ReplayPlan& pl, const replay::Params& p, int cb, uint32_t off0) {
+template <int F>
+bool run_group(ReplayPlan& pl, const replay::Params& p, uint32_t off0) {
+    constexpr int cb = 3 * F;
     uint32_t* list = pl.d_list.as<uint32_t>() + off0;
     uint32_t* retry = pl.d_list.as<uint32_t>() + pl.jobs.size() + off0;
     uint32_t* counters = pl.d_counters.as<uint32_t>() + 2 * cb;  // class c: {next, retries}
     uint32_t off = 0;
     for (int cls = 0; cls < 2; ++cls) {
         const uint32_t cnt = pl.class_count[cb + cls];
-        if (cnt) launch_tier<M>(pl, p, list + off, cnt, cls, pl.class_max_g[cb + cls], counters + 2 * cls, retry + off);
+        if (cnt) launch_tier<F>(pl, p, list + off, cnt, cls, pl.class_max_g[cb + cls], counters + 2 * cls, retry + off);
         off += cnt;
     }
-    if (!M) CARMA_CUDA(cudaEventRecord(pl.ev[1], pl.stream));
+    if (F == 0) CARMA_CUDA(cudaEventRecord(pl.ev[1], pl.stream));
     uint32_t n_retry[4] = {0, 0, 0, 0};
     CARMA_CUDA(cudaMemcpyAsync(n_retry, counters, 16, cudaMemcpyDeviceToHost, pl.stream));
     CARMA_CUDA(cudaStreamSynchronize(pl.stream));
@@ -295,7 +303,7 @@ bool run_group(ReplayPlan& pl, const replay::Params& p, int cb, uint32_t off0) {
         if (round > 0) pl.retried += total;
         CARMA_CUDA(cudaMemcpy(list, ids.data(), total * 4, cudaMemcpyHostToDevice));
         const bool large_ok = round == 0 && pl.max_blocks <= 128;
-        launch_tier<M>(pl, p, list, total, large_ok ? 3 : 2, pl.max_g, counters, retry);
+        launch_tier<F>(pl, p, list, total, large_ok ? 3 : 2, pl.max_g, counters, retry);
         uint32_t nr = 0;
         CARMA_CUDA(cudaMemcpyAsync(&nr, counters + 1, 4, cudaMemcpyDeviceToHost, pl.stream));
         CARMA_CUDA(cudaStreamSynchronize(pl.stream));
@@ -320,17 +328,30 @@ void run_plan(ReplayPlan& pl) {
     p.gpu_out = pl.d_gpu_out.as<carma_gpu_result>();
     p.inv_scratch = pl.d_inv.as<uint32_t>();
     p.smact_begin = pl.d_begin.as<double>();
+    p.tl_out = pl.d_tl.as<carma_timeline_row>();
+    p.tl_cap = pl.tl_cap;
+    p.tl_count = pl.d_tl_count.as<uint64_t>();
     const uint32_t n = static_cast<uint32_t>(pl.jobs.size());
     pl.launches = 0;
     pl.retried = 0;
     CARMA_CUDA(cudaMemsetAsync(pl.d_begin.ptr, 0xff, n * sizeof(double), pl.stream));  // NaN: derive
-    CARMA_CUDA(cudaMemsetAsync(pl.d_counters.ptr, 0, 64, pl.stream));
+    CARMA_CUDA(cudaMemsetAsync(pl.d_counters.ptr, 0, 128, pl.stream));
     CARMA_CUDA(cudaEventRecord(pl.ev[0], pl.stream));
-    const uint32_t n_std = pl.class_count[0] + pl.class_count[1] + pl.class_count[2];
+    uint32_t off[4];
+    for (int f = 0, o = 0; f < 4; ++f) {
+        off[f] = static_cast<uint32_t>(o);
+        o += pl.class_count[3 * f] + pl.class_count[3 * f + 1] + pl.class_count[3 * f + 2];
+    }
+    auto count = [&](int f) { return pl.class_count[3 * f] + pl.class_count[3 * f + 1] + pl.class_count[3 * f + 2]; };
     bool dirty = false;
-    if (n_std) dirty |= run_group<false>(pl, p, 0, 0);
+    if (count(0)) dirty |= run_group<0>(pl, p, off[0]);
     else CARMA_CUDA(cudaEventRecord(pl.ev[1], pl.stream));
-    if (n > n_std) dirty |= run_group<true>(pl, p, 3, n_std);
+    if (count(1)) dirty |= run_group<1>(pl, p, off[1]);
+    if (count(2) || count(3)) {
+        if (pl.tl_cap == 0) throw InvalidArg("timeline jobs need carma_replay_plan_set_timeline_capacity first");
+        if (count(2)) dirty |= run_group<2>(pl, p, off[2]);
+        if (count(3)) dirty |= run_group<3>(pl, p, off[3]);
+    }
     CARMA_CUDA(cudaEventRecord(pl.ev[2], pl.stream));
     if (dirty) CARMA_CUDA(cudaMemcpy(pl.d_list.ptr, pl.class_list.data(), n * 4, cudaMemcpyHostToDevice));
 }
@@ -401,13 +422,16 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
             up(pl->d_task_off, task_off.data(), n_jobs * sizeof(uint64_t));
             up(pl->d_gpu_off, gpu_off.data(), n_jobs * sizeof(uint64_t));
             std::vector<uint32_t> list(2 * static_cast<size_t>(n_jobs));
-            for (int cls = 0; cls < 6; ++cls)
+            for (int cls = 0; cls < 12; ++cls)
                 for (uint32_t i = 0; i < n_jobs; ++i) {
                     const carma_replay_config& c = configs[jobs[i].config];
                     // > 128 allocation blocks: the shared-memory layouts hold 2 bitmap words;
-                    // MIG jobs form classes 3..5 (their own kernels)
-                    const int jc = (c.gpu_capacity / c.alloc_block > 128 ? 2 : static_cast<int>(heavy_config(c))) +
-                                   (c.mode == CARMA_MODE_MIG ? 3 : 0);
+                    // MIG / timeline jobs form classes 3F.. (their own kernels); timeline
+                    // jobs are global-only (large and global tiers)
+                    const int feat = (c.mode == CARMA_MODE_MIG ? 1 : 0) | (c.sample_interval > 0.0 ? 2 : 0);
+                    const int tier = (c.gpu_capacity / c.alloc_block > 128 || (feat & 2)) ? 2
+                                                                                           : static_cast<int>(heavy_config(c));
+                    const int jc = tier + 3 * feat;
                     if (jc != cls) continue;
                     pl->class_list.push_back(i);
                     pl->class_count[cls]++;
@@ -420,7 +444,8 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
             pl->d_gpu_out.ensure(go * sizeof(carma_gpu_result));
             pl->d_inv.ensure(to * 4);
             pl->d_begin.ensure(n_jobs * sizeof(double));
-            pl->d_counters.ensure(64);
+            pl->d_counters.ensure(128);
+            pl->d_tl_count.ensure(n_jobs * sizeof(uint64_t));
         } catch (...) {
             if (pl->stream) cudaStreamDestroy(pl->stream);
             delete pl;
@@ -536,6 +561,36 @@ carma_status carma_replay_plan_timing(carma_replay_plan* hp, double* kernel_ms, 
     });
 }
 
+carma_status carma_replay_plan_set_timeline_capacity(carma_replay_plan* hp, uint64_t rows_per_job) {
+    return guarded([&] {
+        auto* pl = reinterpret_cast<ReplayPlan*>(hp);
+        if (!pl) throw InvalidArg("null plan");
+        std::lock_guard<std::mutex> lock(pl->mu);
+        DeviceGuard guard(pl->device);
+        pl->d_tl.ensure(rows_per_job * pl->jobs.size() * sizeof(carma_timeline_row));
+        pl->tl_cap = rows_per_job;
+    });
+}
+
+carma_status carma_replay_plan_timeline(carma_replay_plan* hp, uint32_t job, carma_timeline_row* rows, uint64_t cap,
+                                        uint64_t* n_rows) {
+    return guarded([&] {
+        auto* pl = reinterpret_cast<ReplayPlan*>(hp);
+        if (!pl) throw InvalidArg("null plan");
+        if (job >= pl->jobs.size()) throw InvalidArg("job index out of range");
+        if (!(pl->cfgs[pl->jobs[job].config].sample_interval > 0.0)) throw InvalidArg("job has no timeline");
+        DeviceGuard guard(pl->device);
+        CARMA_CUDA(cudaStreamSynchronize(pl->stream));
+        uint64_t n = 0;
+        CARMA_CUDA(cudaMemcpy(&n, pl->d_tl_count.as<uint64_t>() + job, sizeof(n), cudaMemcpyDeviceToHost));
+        if (n_rows) *n_rows = n;
+        const uint64_t k = std::min(std::min(n, pl->tl_cap), cap);
+        if (rows && k)
+            CARMA_CUDA(cudaMemcpy(rows, pl->d_tl.as<carma_timeline_row>() + static_cast<uint64_t>(job) * pl->tl_cap,
+                                  k * sizeof(carma_timeline_row), cudaMemcpyDeviceToHost));
+    });
+}
+
 carma_status carma_replay_plan_destroy(carma_replay_plan* hp) {
     return guarded([&] {
         auto* pl = reinterpret_cast<ReplayPlan*>(hp);
@@ -545,7 +600,8 @@ carma_status carma_replay_plan_destroy(carma_replay_plan* hp) {
             cudaStreamSynchronize(pl->stream);
             DeviceBuffer* bufs[] = {&pl->d_cfgs, &pl->d_tasks, &pl->d_trace_off, &pl->d_jobs, &pl->d_task_off,
                                     &pl->d_gpu_off, &pl->d_list, &pl->d_task_out, &pl->d_trace_out, &pl->d_gpu_out,
-                                    &pl->d_inv, &pl->d_begin, &pl->d_counters, &pl->d_gstate, &pl->d_outcomes};
+                                    &pl->d_inv, &pl->d_begin, &pl->d_counters, &pl->d_gstate, &pl->d_outcomes,
+                                    &pl->d_tl, &pl->d_tl_count};
             for (auto* b : bufs) b->release();
             for (auto& e : pl->ev)
                 if (e) cudaEventDestroy(e);

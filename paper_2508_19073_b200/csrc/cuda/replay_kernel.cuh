@@ -57,7 +57,7 @@ namespace replay {
 #endif
 
 constexpr uint32_t kNone = 0xffffffffu;
-constexpr uint32_t kWindow = 1u, kCompletion = 2u, kCrash = 3u;
+constexpr uint32_t kWindow = 1u, kCompletion = 2u, kCrash = 3u, kTick = 4u;
 constexpr int32_t kStatusRetry = -1;      // overflowed this tier
 constexpr int32_t kStatusRedoSmact = -2;  // full-history SMACT needs the true window begin
 constexpr int kMaxWords = 4;              // bitmap words per GPU: <= 256 blocks
@@ -81,15 +81,21 @@ struct Params {
     uint32_t* retry_count;
     unsigned int* next_job;  // dynamic scheduler counter
     char* gstate;            // global-tier state, per warp
+    carma_timeline_row* tl_out;  // timeline rows, tl_cap per job (TL kernels only)
+    uint64_t tl_cap;
+    uint64_t* tl_count;          // rows produced, per job
 };
 
 // Compile-time state layout: G GPUs, H heap entries, S slots, RC residents
 // per GPU, RG SMACT ring entries per GPU, RQ recovery-queue entries.
-template <int G_, int H_, int S_, int RC_, int RG_, int RQ_, int W_, bool MIG_ = false>
+// F = feature bits compiled into the kernel: 1 = MIG collocation, 2 = timeline
+// sample ticks. Jobs that need them run in their own kernel instantiations.
+template <int G_, int H_, int S_, int RC_, int RG_, int RQ_, int W_, int F_ = 0>
 struct Layout {
     static constexpr int G = G_, H = H_, S = S_, RC = RC_, RG = RG_, RQ = RQ_, W = W_;
-    static constexpr bool MIG = MIG_;  // MIG collocation compiled in (separate kernels)
-    static constexpr size_t MI = MIG_ ? 1 : 0;
+    static constexpr bool MIG = (F_ & 1) != 0;
+    static constexpr bool TL = (F_ & 2) != 0;
+    static constexpr size_t MI = MIG ? 1 : 0;
     static constexpr int GPL = (G + 31) / 32;
     static constexpr size_t al8(size_t x) { return (x + 15) / 16 * 16; }
     static constexpr size_t cfg = 0;                                   // carma_replay_config
@@ -1007,12 +1013,25 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
     const uint64_t* est = p.est_override ? p.est_override + p.trace_off[p.jobs[j].trace] : nullptr;
     const uint64_t max_events = 1000ull * c.T + 1000000ull;
     uint64_t events = 0;
+    // timeline (L::TL only; dead code otherwise): the pending sample tick —
+    // the first at the first row's submit time, scheduled after every arrival
+    // (seq = T, runner.cpp:80-83) — completions so far and rows written
+    double tick_t = 0.0;
+    uint32_t tick_seq = 0, n_done = 0;
+    bool tick_live = false;
+    uint64_t tl_rows = 0;
+    if constexpr (L::TL) {
+        tick_live = RP_CFG.sample_interval > 0.0;
+        tick_t = tasks[0].submit;
+        tick_seq = c.T;
+        if (tick_live) c.seq_next = c.T + 1;
+    }
     const double delay = RP_CFG.oom_startup_delay;
     for (;;) {
         // ---- next event: arrival stream (seq = index) vs heap top
         const bool have_arr = c.arrived < c.T;
         const bool have_heap = c.hsize > 0;
-        if (!have_arr && !have_heap) break;
+        if (!have_arr && !have_heap && !(L::TL && tick_live)) break;
         if (events >= max_events) {
             c.status = CARMA_ERR_INCOMPLETE;
             break;
@@ -1020,7 +1039,19 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
         double t;
         uint32_t kind, payload, seq = 0;
         const double at = have_arr ? tasks[c.arrived].submit : 0.0;
-        if (have_arr && (!have_heap || !klater(tkey(at), c.arrived, RP_U64(ht)[0], RP_U32(hs)[0]))) {
+        bool tick = false;
+        if constexpr (L::TL) {  // the pending sample tick against both heads
+            if (tick_live) {
+                const uint64_t tk = tkey(tick_t);
+                tick = !(have_arr && klater(tk, tick_seq, tkey(at), c.arrived)) &&
+                       !(have_heap && klater(tk, tick_seq, RP_U64(ht)[0], RP_U32(hs)[0]));
+            }
+        }
+        if (tick) {
+            t = tick_t;
+            kind = kTick;
+            payload = 0;
+        } else if (have_arr && (!have_heap || !klater(tkey(at), c.arrived, RP_U64(ht)[0], RP_U32(hs)[0]))) {
             t = at;
             kind = 0;
             payload = c.arrived;
@@ -1046,6 +1077,41 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             }
         }
         c.now = t;
+        if constexpr (L::TL) {
+            if (kind == kTick) {
+                // emit_timeline_row (world.cpp:210-219), then reschedule while
+                // Manager::all_done() is false (runner.cpp:85-92)
+                const carma_replay_config& cf = RP_CFG;
+                const int G = cf.gpu_count;
+                const uint64_t* used = RP_U64(used);
+                const int nblk_g = static_cast<int>(cf.gpu_capacity / cf.alloc_block);
+#pragma unroll
+                for (int jj = 0; jj < L::GPL; ++jj) {
+                    const int g = static_cast<int>(lane) + 32 * jj;
+                    const uint64_t r = tl_rows + static_cast<uint64_t>(g);
+                    if (g < G && r < p.tl_cap) {
+                        carma_timeline_row row;
+                        row.t = t;
+                        row.smact = RP_F64(inst)[g];
+                        row.power_w = RP_F64(power)[g];
+                        row.used = static_cast<uint64_t>(nblk_g - static_cast<int>(free_blocks<L>(used, g))) *
+                                   cf.alloc_block;
+                        row.gpu = g;
+                        row.reserved = 0;
+                        p.tl_out[static_cast<uint64_t>(j) * p.tl_cap + r] = row;
+                    }
+                }
+                tl_rows += static_cast<uint64_t>(G);
+                if (!(c.arrived > 0 && n_done == c.arrived)) {
+                    tick_t = __dadd_rn(c.now, cf.sample_interval);
+                    tick_seq = c.seq_next++;
+                } else {
+                    tick_live = false;
+                }
+                __syncwarp();
+                continue;
+            }
+        }
         // ---- handle (World::step + Manager::on_event, manager.cpp:333-357)
         bool sched = true;
         int t0 = 0, t1 = 0, nt = 0;
@@ -1056,6 +1122,7 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
         } else if (kind == kCompletion) {
             if (RP_U32(s_seq)[payload] != seq) continue;  // superseded by a rate change
             finish<L>(b, c, payload, out, t0, t1, nt, lane);
+            if constexpr (L::TL) ++n_done;
         } else {  // oom_crash -> handle_oom (manager.cpp:262-267)
             c.oom++;
             if (lane == 0) {
@@ -1121,6 +1188,9 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
         }
         if (c.status) break;
         __syncwarp();
+    }
+    if constexpr (L::TL) {
+        if (lane == 0) p.tl_count[j] = tl_rows;
     }
     c.events_lo = static_cast<uint32_t>(events);
     c.events_hi = static_cast<uint32_t>(events >> 32);

@@ -61,6 +61,7 @@ def load_ref():
     lib.ref_bench_sweep.argtypes = [P, c_int, c_uint64, c_uint64, P, c_int, c_int, POINTER(c_uint64),
                                     POINTER(c_double)]
     lib.ref_run_sweep.argtypes = [P, c_int, c_int, P, c_int, c_char_p, c_uint64]
+    lib.ref_timeline.argtypes = [P, c_int, c_uint64, c_char_p, c_uint64]
     return lib
 
 
@@ -69,7 +70,7 @@ ref_config_dtype = np.dtype([
     ("max_smact", "<f8"), ("has_min_free", "<i4"), ("min_free", "<u8"), ("safety_margin", "<u8"),
     ("monitor_window", "<f8"), ("gpu_count", "<i4"), ("gpu_capacity", "<u8"), ("alloc_block", "<u8"),
     ("estimator_seed", "<u8"), ("estimator_k", "<u8"), ("estimator_samples", "<u8"),
-    ("mig_count", "<i4"), ("mig_reserved", "<i4"), ("mig_fractions", "<f8", (8,)),
+    ("mig_count", "<i4"), ("mig_reserved", "<i4"), ("mig_fractions", "<f8", (8,)), ("sample_interval", "<f8"),
 ], align=True)
 
 ref_task_out_dtype = np.dtype([
@@ -87,8 +88,9 @@ ref_trace_out_dtype = np.dtype([
 
 def ref_config(policy="magm", estimator="none", mode="mps", rr_pre=False, max_smact=0.8, min_free=None,
                margin=2 * abi.GiB, window=60.0, gpu_count=4, capacity=40 * abi.GiB, block=512 * abi.MiB,
-               est_seed=11, est_k=5, est_samples=4000, mig=()):
+               est_seed=11, est_k=5, est_samples=4000, mig=(), sample_interval=0.0):
     c = np.zeros(1, ref_config_dtype)
+    c["sample_interval"] = sample_interval
     c["mig_count"] = len(mig)
     c["mig_fractions"][0, : len(mig)] = mig
     c["policy"] = abi.POLICY[policy]
@@ -118,6 +120,7 @@ def replay_config_from(c):
     r["min_free"] = c["min_free"] if c["has_min_free"][0] else 0
     r["p_idle_w"], r["p_max_w"], r["p_boost_w"], r["boost_threshold"] = 55.0, 400.0, 30.0, 0.9
     r["oom_startup_delay"] = 5.0
+    r["sample_interval"] = c["sample_interval"]
     if int(c["mode"][0]) == abi.MODE["mig"]:
         n = int(c["mig_count"][0])
         fr = np.ascontiguousarray(c["mig_fractions"][0, :n], np.float64)

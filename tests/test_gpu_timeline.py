@@ -1,0 +1,49 @@
+"""RunConfig::enable_timeline on the GPU replay against the reference itself
+(oracle/_ref): the sample ticks are events, so every output (energy bits,
+completions, reports) must match the reference run WITH the timeline, and the
+timeline text (runner.cpp:80-93, world.cpp:210-219) must be identical."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2508_19073_b200 as cb
+from oracle_bind import ref_config, ref_run
+
+pytestmark = pytest.mark.gpu
+
+CASES = [dict(policy="magm", interval=10.0), dict(policy="rr", interval=7.3),
+         dict(policy="lug", interval=60.0, gpu_count=8, window=5.0),
+         dict(policy="exclusive", interval=10.0, estimator="oracle"),
+         dict(policy="magm", interval=10.0, mode="mig", mig=(0.75, 0.25))]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[str(i) for i in range(len(CASES))])
+@pytest.mark.parametrize("mix,seed", [("t90", 1), ("t60", 4)])
+def test_timeline_matches_reference(gpu, ref, case, mix, seed):
+    kw = dict(case)
+    interval = kw.pop("interval")
+    est = kw.get("estimator", "none")
+    rc = cb.RunConfig(mix=mix, trace_seed=seed, enable_timeline=True, sample_interval=interval,
+                      policy=cb.PolicyConfig(policy=kw["policy"], estimator=est,
+                                             collocation_mode=kw.get("mode", "mps"),
+                                             monitor_window=kw.get("window", 60.0)),
+                      constants=cb.SimConstants(gpu_count=kw.get("gpu_count", 4)),
+                      mig_instances=list(kw.get("mig", ())))
+    art = cb.run_simulation_artifacts(rc, device=gpu)
+    cfg = ref_config(**kw, sample_interval=interval)
+    tout, rout, ge, gs, gp = ref_run(ref, cfg, mix=mix, seed=seed)
+    buf = ctypes.create_string_buffer(1 << 22)
+    assert ref.ref_timeline(cfg.ctypes.data, cb.abi.MIX[mix], seed, buf, len(buf)) == 0
+    assert "\n".join(art.timeline) + "\n" == buf.value.decode()
+    assert np.array_equal(art.tasks["complete"], tout["complete"])
+    assert np.array_equal(art.tasks["executed"], tout["executed"])
+    assert art.report["energy_mj"] == rout["energy_mj"] and art.report["avg_jct"] == rout["avg_jct"]
+    assert np.array_equal(art.gpus["energy_j"], ge) and np.array_equal(art.gpus["mean_smact"], gs)
+
+
+def test_timeline_off_is_unchanged(gpu):
+    rc = cb.RunConfig(mix="t90", trace_seed=2)
+    a = cb.run_simulation_artifacts(rc, device=gpu)
+    r, t, g = cb.run_simulation(rc, device=gpu)
+    assert a.timeline == [] and a.report.tobytes() == r.tobytes() and a.tasks.tobytes() == t.tobytes()
