@@ -51,12 +51,6 @@ constexpr int kMaxBins = 4096;
 constexpr int kBlock = 8;  // points per frontier step
 constexpr int kF32Dims = 16;  // fp32 pre-filter: active dims per point
 constexpr int kCandCap = 24;  // fp32 pre-filter: candidate buffer per lane
-// Partial unrolling of the per-query setup loops: enough independent
-// divisions / field loads in flight without 19 copies of the code.
-#ifndef KNN_SETUP_UNROLL
-#define KNN_SETUP_UNROLL 1
-#endif
-constexpr int kSetupUnroll = KNN_SETUP_UNROLL;
 
 struct ModelDev {
     const double* pts;    // N x 20, sorted by (p18, original index)
@@ -91,7 +85,10 @@ struct KnnParams {
     const int8_t* family;
     int32_t default_family;
     uint64_t q;
+    double* qrec;  // fp32 path: per row the normalised query (19) + eta, written by knn_prep
 };
+
+constexpr int kQrec = 20;  // doubles per query record (160 B, 16-B aligned)
 
 __device__ __forceinline__ double u2d(uint64_t v) { return __ull2double_rn(v); }
 
@@ -219,13 +216,6 @@ __device__ __forceinline__ int family_of_t(const KnnParams& p, uint64_t i) {
     return (f >= 0 && f < CARMA_FAMILIES && p.m[f].present) ? f : -1;
 }
 
-// Raw scalar features of `row` into column `tid` of a [19][128] shared
-// array. The bit-packed fields are extracted by a rolled loop (one copy of
-// the extraction code instead of 19: the setup code competes with the walk
-// for the instruction cache).
-template <int FMT>
-__device__ __forceinline__ void stage_raw(const KnnParams& p, uint32_t row, double (*qs)[128], unsigned tid);
-
 template <int FMT>
 __device__ __forceinline__ void load_raw(const KnnParams& p, uint32_t row, double* raw) {
     if constexpr (FMT == CARMA_ROWS_SCALAR) {
@@ -241,39 +231,6 @@ __device__ __forceinline__ void load_raw(const KnnParams& p, uint32_t row, doubl
     }
 }
 
-template <int FMT>
-__device__ __forceinline__ void stage_raw(const KnnParams& p, uint32_t row, double (*qs)[128], unsigned tid) {
-    if constexpr (FMT == CARMA_ROWS_BITPACKED) {
-        const uint32_t* r = bit_row(p, row);
-#pragma unroll (kSetupUnroll)
-        for (int f = 0; f < kDims; ++f) qs[f][tid] = __longlong_as_double(static_cast<long long>(bit_field(p, r, f)));
-        uint64_t v[kDims];
-#pragma unroll
-        for (int f = 0; f < kDims; ++f) v[f] = static_cast<uint64_t>(__double_as_longlong(qs[f][tid]));
-        // field -> feature mapping of featurize_bits
-        double raw[kDims];
-#pragma unroll
-        for (int f = 0; f < 7; ++f) raw[f] = u2d(v[f]);
-        const int code = static_cast<int>(v[7]) & 7;
-        raw[7] = p.act[2 * code];
-        raw[8] = p.act[2 * code + 1];
-        const bool h = v[11] != 0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            raw[9 + 3 * k] = h ? static_cast<double>(static_cast<int32_t>(v[8 + k])) : 0.0;
-            raw[10 + 3 * k] = h ? u2d(v[12 + 2 * k]) : 0.0;
-            raw[11 + 3 * k] = h ? u2d(v[13 + 2 * k]) : 0.0;
-        }
-        raw[18] = __dadd_rn(__dmul_rn(16.0, raw[5]), __dmul_rn(__dmul_rn(4.0, raw[4]), raw[6]));
-#pragma unroll
-        for (int d = 0; d < kDims; ++d) qs[d][tid] = raw[d];
-    } else {
-        double raw[kDims];
-        load_raw<FMT>(p, row, raw);
-#pragma unroll
-        for (int d = 0; d < kDims; ++d) qs[d][tid] = raw[d];
-    }
-}
 
 // first index with key18[i] >= x
 __device__ __forceinline__ uint32_t lower_bound(const double* key, uint64_t n, double x) {
@@ -284,6 +241,17 @@ __device__ __forceinline__ uint32_t lower_bound(const double* key, uint64_t n, d
         else hi = mid;
     }
     return static_cast<uint32_t>(lo);
+}
+
+// Same over keys in shared or global memory (generic loads).
+__device__ __forceinline__ uint32_t lower_bound_any(const double* key, uint32_t n, double x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (key[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
 
 // Pass 1: bin and start position per row; per-CTA histogram -> hist[bin][cta].
@@ -302,6 +270,84 @@ __global__ void knn_keys(KnnParams p, uint32_t n_bins, uint32_t* __restrict__ qb
             const ModelDev& m = p.m[f];
             const double q18 = normalize(raw18_of(p, i), m.lo[18], m.hi[18]);
             pos = lower_bound(m.key18, m.n, q18);
+            bin = m.bin_base + (pos >> m.bin_shift);
+        }
+        const uint32_t b = bin == kInvalidBin ? n_bins - 1 : bin;
+        qbin[i] = b;
+        qpos[i] = pos;
+        atomicAdd(&sh[b], 1u);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < n_bins; b += blockDim.x)
+        hist[static_cast<uint64_t>(b) * gridDim.x + blockIdx.x] = sh[b];
+}
+
+// Pass 1 of the fp32 path: knn_keys plus the whole per-query setup of the
+// search (featurise, the 19 correctly rounded normalisations of
+// estimators.cpp:439-441, the fp32 error radius eta), written as a 160-B
+// record per row. This high-occupancy streaming kernel hides the division
+// latency that the search kernel (4 warps per scheduler) cannot.
+// When every model's keys fit (kPrepKeysMax doubles), the binary search runs
+// on a shared-memory copy of key18 (12 dependent probes per row).
+constexpr uint32_t kPrepKeysMax = 8192;
+
+template <int FMT>
+__global__ void __launch_bounds__(512, 2) knn_prep(KnnParams p, uint32_t n_bins, uint32_t* __restrict__ qbin, uint32_t* __restrict__ qpos,
+                         uint32_t* __restrict__ hist, int keys_in_smem) {
+    extern __shared__ __align__(16) uint32_t sh[];
+    double* skeys = reinterpret_cast<double*>(sh + ((n_bins + 3) & ~3u));
+    const double* keys[CARMA_FAMILIES];
+    {
+        uint32_t off = 0;
+        for (int f = 0; f < CARMA_FAMILIES; ++f) {
+            keys[f] = p.m[f].key18;
+            if (keys_in_smem && p.m[f].present) {
+                for (uint32_t i = threadIdx.x; i < p.m[f].n; i += blockDim.x) skeys[off + i] = p.m[f].key18[i];
+                keys[f] = skeys + off;
+                off += static_cast<uint32_t>(p.m[f].n);
+            }
+        }
+    }
+    for (uint32_t b = threadIdx.x; b < n_bins; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    const uint64_t per = (p.q + gridDim.x - 1) / gridDim.x;
+    const uint64_t beg = per * blockIdx.x;
+    const uint64_t end = min(p.q, beg + per);
+    for (uint64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+        const int f = family_of_t<FMT>(p, i);
+        uint32_t bin = kInvalidBin, pos = 0;
+        if (f >= 0) {
+            const ModelDev& m = p.m[f];
+            double raw[kDims];
+            load_raw<FMT>(p, static_cast<uint32_t>(i), raw);
+            double qn[kDims];
+            double qmax = 0.0;
+#pragma unroll
+            for (int d = 0; d < kDims; ++d) {
+                qn[d] = normalize(raw[d], m.lo[d], m.hi[d]);
+                const double av = fabs(qn[d]);
+                qmax = (av > qmax || av != av) ? av : qmax;
+            }
+            // active dims in ascending order are adim[0..]: walk d with a running j
+            double e2 = 0.0;
+            int j = 0;
+#pragma unroll
+            for (int d = 0; d < kDims; ++d) {
+                if ((m.active >> d) & 1u) {
+                    const double w = d == 18 ? 64.0 : 1.0;
+                    const double ej = 2.0 * 0x1.0p-24 * (1.0 + 0x1.0p-24) * w * (m.pmax[j] + fabs(qn[d])) + 0x1.0p-140;
+                    e2 += ej * ej;
+                    ++j;
+                }
+            }
+            double eta = sqrt(e2) * (1.0 + 0x1.0p-40);
+            if (!(qmax <= 1e15)) eta = inf;  // huge or NaN query: exact on every point
+            double2* rec = reinterpret_cast<double2*>(p.qrec + i * kQrec);
+#pragma unroll
+            for (int h = 0; h < 9; ++h) rec[h] = make_double2(qn[2 * h], qn[2 * h + 1]);
+            rec[9] = make_double2(qn[18], eta);
+            pos = lower_bound_any(keys[f], static_cast<uint32_t>(m.n), qn[18]);
             bin = m.bin_base + (pos >> m.bin_shift);
         }
         const uint32_t b = bin == kInvalidBin ? n_bins - 1 : bin;
@@ -758,40 +804,33 @@ __global__ void __launch_bounds__(128, 4)
 
             // Query: exact fp64 normalisation (estimators.cpp:439-441) into
             // shared memory, plus the fp32 copy of the active dims and eta.
+            // The query record written by knn_prep: normalised query into
+            // shared memory, eta, and the fp32 copy of the active dims.
             float qf[kF32Dims];
             double eta = 0.0;
             double q18 = 0.0;
             {
-                // Rolled loops: one division / bound sequence in the code
-                // instead of 19 / 16 (instruction-cache footprint).
-                if (mine) stage_raw<FMT>(p, row, qsh, tid);
-                double qmax = 0.0;
-#pragma unroll (kSetupUnroll)
-                for (int d = 0; d < kDims; ++d) {
-                    const double v = mine ? normalize(qsh[d][tid], m.lo[d], m.hi[d]) : 0.0;
-                    qsh[d][tid] = v;
-                    const double av = fabs(v);
-                    qmax = (av > qmax || av != av) ? av : qmax;
-                }
-                q18 = qsh[18][tid];
-                double e2 = 0.0;
-#pragma unroll 1
-                for (int j = 0; j < kF32Dims; ++j) {
-                    const int a = m.adim[j];
-                    if (a < kDims) {
-                        const double qa = qsh[a][tid];
-                        const double w = a == 18 ? 64.0 : 1.0;
-                        const double ej = 2.0 * 0x1.0p-24 * (1.0 + 0x1.0p-24) * w * (m.pmax[j] + fabs(qa)) + 0x1.0p-140;
-                        e2 += ej * ej;
+                if (mine) {
+                    const double2* rec = reinterpret_cast<const double2*>(p.qrec + static_cast<uint64_t>(row) * kQrec);
+#pragma unroll
+                    for (int h = 0; h < 9; ++h) {
+                        const double2 v = __ldg(rec + h);
+                        qsh[2 * h][tid] = v.x;
+                        qsh[2 * h + 1][tid] = v.y;
                     }
+                    const double2 v = __ldg(rec + 9);
+                    qsh[18][tid] = v.x;
+                    q18 = v.x;
+                    eta = v.y;
+                } else {
+#pragma unroll
+                    for (int d = 0; d < kDims; ++d) qsh[d][tid] = 0.0;
                 }
 #pragma unroll
                 for (int j = 0; j < kF32Dims; ++j) {
                     const int a = m.adim[j];
                     qf[j] = a < kDims ? __double2float_rn((a == 18 ? 64.0 : 1.0) * qsh[a][tid]) : 0.0f;
                 }
-                eta = sqrt(e2) * (1.0 + 0x1.0p-40);
-                if (!(qmax <= 1e15)) eta = inf;  // huge or NaN query: exact on every point
             }
 
             unsigned long long qf2[kF32Dims / 2];
@@ -1038,7 +1077,7 @@ struct KnnHandle {
     cudaStream_t pipe[2] = {nullptr, nullptr};
     HostModel model[CARMA_FAMILIES];
     struct Scratch {
-        DeviceBuffer rows, family, qbin, qpos, perm, hist, tot, bucket, bytes;
+        DeviceBuffer rows, family, qbin, qpos, perm, hist, tot, bucket, bytes, qrec;
         PinnedBuffer stage_rows, stage_family;
     } scratch[2];
     DeviceBuffer evals;
@@ -1168,9 +1207,48 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
     sc.hist.ensure(static_cast<size_t>(n_bins) * ctas * 4);
     const size_t shmem = n_bins * 4;
     const bool timed = h.timed && h.ev[0];
+    const bool f32 = use_f32(h);
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
-    knn_keys<<<ctas, 512, shmem, s>>>(p, n_bins, sc.qbin.as<uint32_t>(), sc.qpos.as<uint32_t>(),
-                                      sc.hist.as<uint32_t>());
+    if (f32) {
+        uint64_t nkeys = 0;
+        for (const auto& m : h.model)
+            if (m.present) nkeys += m.n;
+        const int keys_in_smem = nkeys <= kPrepKeysMax ? 1 : 0;
+        const size_t pshmem = ((n_bins + 3) & ~3u) * 4 + (keys_in_smem ? nkeys * 8 : 0);
+        if (pshmem > 48 * 1024) {
+            static const cudaError_t attr_ok = [] {
+                cudaError_t e = cudaSuccess;
+                const int lim = 100 * 1024;
+                e = cudaFuncSetAttribute(knn_prep<CARMA_ROWS_SCALAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+                if (e == cudaSuccess)
+                    e = cudaFuncSetAttribute(knn_prep<CARMA_ROWS_PACKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+                if (e == cudaSuccess)
+                    e = cudaFuncSetAttribute(knn_prep<CARMA_ROWS_BITPACKED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             lim);
+                if (e == cudaSuccess)
+                    e = cudaFuncSetAttribute(knn_prep<CARMA_ROWS_FEATURES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             lim);
+                return e;
+            }();
+            CARMA_CUDA(attr_ok);
+        }
+        sc.qrec.ensure(q * kQrec * sizeof(double));
+        p.qrec = sc.qrec.as<double>();
+        uint32_t* qb = sc.qbin.as<uint32_t>();
+        uint32_t* qp = sc.qpos.as<uint32_t>();
+        uint32_t* hs = sc.hist.as<uint32_t>();
+        switch (format) {
+            case CARMA_ROWS_SCALAR: knn_prep<CARMA_ROWS_SCALAR><<<ctas, 512, pshmem, s>>>(p, n_bins, qb, qp, hs, keys_in_smem); break;
+            case CARMA_ROWS_PACKED: knn_prep<CARMA_ROWS_PACKED><<<ctas, 512, pshmem, s>>>(p, n_bins, qb, qp, hs, keys_in_smem); break;
+            case CARMA_ROWS_BITPACKED:
+                knn_prep<CARMA_ROWS_BITPACKED><<<ctas, 512, pshmem, s>>>(p, n_bins, qb, qp, hs, keys_in_smem);
+                break;
+            default: knn_prep<CARMA_ROWS_FEATURES><<<ctas, 512, pshmem, s>>>(p, n_bins, qb, qp, hs, keys_in_smem);
+        }
+    } else {
+        knn_keys<<<ctas, 512, shmem, s>>>(p, n_bins, sc.qbin.as<uint32_t>(), sc.qpos.as<uint32_t>(),
+                                          sc.hist.as<uint32_t>());
+    }
     sc.tot.ensure(n_bins * 4);
     bin_totals<<<(n_bins + 7) / 8, 256, 0, s>>>(sc.hist.as<uint32_t>(), n_bins, ctas, sc.tot.as<uint32_t>());
     scan_bins<<<1, 1024, 0, s>>>(sc.tot.as<uint32_t>(), n_bins);
@@ -1178,7 +1256,7 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
     knn_scatter<<<ctas, 512, shmem, s>>>(q, n_bins, sc.qbin.as<uint32_t>(), sc.hist.as<uint32_t>(),
                                          sc.perm.as<uint32_t>());
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[1], s));
-    launch_search(p, max_k(h), use_f32(h), sc.perm.as<uint32_t>(), sc.qpos.as<uint32_t>(), bucket, bytes, d2,
+    launch_search(p, max_k(h), f32, sc.perm.as<uint32_t>(), sc.qpos.as<uint32_t>(), bucket, bytes, d2,
                   idx, evals, s);
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[2], s));
     CARMA_CUDA(cudaGetLastError());
