@@ -50,7 +50,10 @@ constexpr int kScatterCtas = 296;  // 2 per SM on a 148-SM B200
 constexpr int kMaxBins = 4096;
 constexpr int kBlock = 8;  // points per frontier step
 constexpr int kF32Dims = 16;  // fp32 pre-filter: active dims per point
-constexpr int kCandCap = 24;  // fp32 pre-filter: candidate buffer per lane
+#ifndef KNN_CAND_CAP
+#define KNN_CAND_CAP 24
+#endif
+constexpr int kCandCap = KNN_CAND_CAP;  // fp32 pre-filter: candidate buffer per lane
 
 struct ModelDev {
     const double* pts;    // N x 20, sorted by (p18, original index)
@@ -759,19 +762,26 @@ __device__ __forceinline__ void sorted_insert(float (&a)[K], float v) {
     a[0] = fminf(a[0], v);
 }
 
+#ifndef KNN_F32_CTAS
+#define KNN_F32_CTAS 4
+#endif
+constexpr size_t kF32Smem = kDims * 128 * 8 + kCandCap * 128 * 8 + 4 * 2 * kBlock * kF32Dims * 4;
 template <int K, int FMT>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(128, KNN_F32_CTAS)
     knn_search_f32(KnnParams p, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ qpos,
                    int32_t* __restrict__ bucket_out, uint64_t* __restrict__ bytes_out,
                    double* __restrict__ topk_d2, int64_t* __restrict__ topk_idx,
                    unsigned long long* __restrict__ evals) {
     // Per-thread rows are stored column-major ([item][thread]) so that lanes
-    // touching their own rows never share a bank.
-    __shared__ double qsh[kDims][128];
-    __shared__ uint32_t cbuf_i[kCandCap][128];
-    __shared__ float cbuf_s[kCandCap][128];
-    // per warp: the next fp32 block on the left [0] and right [1] of the frontier
-    __shared__ float4 stage[4][2][kBlock * kF32Dims / 4];
+    // touching their own rows never share a bank. Dynamic shared memory
+    // (kF32Smem bytes): qsh[19][128] f64, cbuf_i/cbuf_s[kCandCap][128],
+    // per warp the next fp32 block on the left [0] and right [1] of the frontier.
+    extern __shared__ __align__(16) char f32_smem[];
+    auto qsh = reinterpret_cast<double (*)[128]>(f32_smem);
+    auto cbuf_i = reinterpret_cast<uint32_t (*)[128]>(f32_smem + kDims * 128 * 8);
+    auto cbuf_s = reinterpret_cast<float (*)[128]>(f32_smem + kDims * 128 * 8 + kCandCap * 128 * 4);
+    auto stage = reinterpret_cast<float4 (*)[2][kBlock * kF32Dims / 4]>(f32_smem + kDims * 128 * 8 +
+                                                                          kCandCap * 128 * 8);
     const unsigned lane = threadIdx.x & 31;
     const unsigned tid = threadIdx.x;
     float4 (*stg)[kBlock * kF32Dims / 4] = stage[threadIdx.x >> 5];
@@ -803,7 +813,6 @@ __global__ void __launch_bounds__(128, 4)
             const int k = static_cast<int>(m.k < K ? m.k : K);
 
             // Query: exact fp64 normalisation (estimators.cpp:439-441) into
-            // shared memory, plus the fp32 copy of the active dims and eta.
             // The query record written by knn_prep: normalised query into
             // shared memory, eta, and the fp32 copy of the active dims.
             float qf[kF32Dims];
@@ -1150,19 +1159,30 @@ void launch_search(const KnnParams& p, int kmax, bool f32, const uint32_t* perm,
     if (f32) {
         auto go = [&](auto kc) {
             constexpr int KK = decltype(kc)::value;
+            if (kF32Smem > 48 * 1024) {
+                static const cudaError_t attr = [] {
+                    cudaError_t e = cudaSuccess;
+                    const int b = static_cast<int>(kF32Smem);
+                    for (auto fn : {knn_search_f32<KK, CARMA_ROWS_SCALAR>, knn_search_f32<KK, CARMA_ROWS_PACKED>,
+                                    knn_search_f32<KK, CARMA_ROWS_BITPACKED>, knn_search_f32<KK, CARMA_ROWS_FEATURES>})
+                        if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+                    return e;
+                }();
+                CARMA_CUDA(attr);
+            }
             switch (p.format) {
                 case CARMA_ROWS_SCALAR:
-                    knn_search_f32<KK, CARMA_ROWS_SCALAR><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+                    knn_search_f32<KK, CARMA_ROWS_SCALAR><<<grid, block, kF32Smem, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
                     break;
                 case CARMA_ROWS_PACKED:
-                    knn_search_f32<KK, CARMA_ROWS_PACKED><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
+                    knn_search_f32<KK, CARMA_ROWS_PACKED><<<grid, block, kF32Smem, s>>>(p, perm, qpos, bucket, bytes, d2, idx, evals);
                     break;
                 case CARMA_ROWS_BITPACKED:
-                    knn_search_f32<KK, CARMA_ROWS_BITPACKED><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx,
+                    knn_search_f32<KK, CARMA_ROWS_BITPACKED><<<grid, block, kF32Smem, s>>>(p, perm, qpos, bucket, bytes, d2, idx,
                                                                                      evals);
                     break;
                 default:
-                    knn_search_f32<KK, CARMA_ROWS_FEATURES><<<grid, block, 0, s>>>(p, perm, qpos, bucket, bytes, d2, idx,
+                    knn_search_f32<KK, CARMA_ROWS_FEATURES><<<grid, block, kF32Smem, s>>>(p, perm, qpos, bucket, bytes, d2, idx,
                                                                                    evals);
             }
         };
