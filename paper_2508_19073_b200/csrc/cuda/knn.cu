@@ -765,6 +765,11 @@ __device__ __forceinline__ void sorted_insert(float (&a)[K], float v) {
 #ifndef KNN_F32_CTAS
 #define KNN_F32_CTAS 4
 #endif
+// Host-buffer calls pipeline H2D / search / D2H over chunks of this many rows
+// on two streams.
+#ifndef KNN_E2E_CHUNK_LOG2
+#define KNN_E2E_CHUNK_LOG2 21
+#endif
 constexpr size_t kF32Smem = kDims * 128 * 8 + kCandCap * 128 * 8 + 4 * 2 * kBlock * kF32Dims * 4;
 template <int K, int FMT>
 __global__ void __launch_bounds__(128, KNN_F32_CTAS)
@@ -1300,7 +1305,16 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
         if (!rows) throw InvalidArg("rows is null");
         std::lock_guard<std::mutex> lock(h->mu);
         DeviceGuard g(h->device);
-        const uint64_t chunk = 1ull << 20;
+        // Chunks grow geometrically from 2^18 rows to the steady size and
+        // shrink again over the last rows (at most half of what remains), so
+        // the first H2D copy (pipeline fill) and the last search + D2H
+        // (drain) are short; scratch is sized for the steady chunk.
+        const uint64_t chunk = uint64_t{1} << KNN_E2E_CHUNK_LOG2;
+        const uint64_t small = uint64_t{1} << 18;
+        auto chunk_rows = [&](uint64_t c, uint64_t remaining) -> uint64_t {
+            const uint64_t grow = std::min<uint64_t>(chunk, small << std::min<uint64_t>(c, 20));
+            return std::min<uint64_t>(grow, std::max<uint64_t>(small, remaining / 2));
+        };
         const bool rows_pinned = is_pinned(rows);
         const bool fam_pinned = !family || is_pinned(family);
         const bool out_pinned = (!bucket_out || is_pinned(bucket_out)) && (!bytes_out || is_pinned(bytes_out));
@@ -1309,11 +1323,11 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
         CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 16, h->pipe[0]));
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
         uint64_t launches = 0;
-        const uint64_t n_chunks = (q + chunk - 1) / chunk;
-        for (uint64_t c = 0; c < n_chunks; ++c) {
+        uint64_t beg = 0, cnt = 0;
+        for (uint64_t c = 0; beg < q; ++c, beg += cnt) {
             KnnHandle::Scratch& sc = h->scratch[c & 1];
             cudaStream_t s = h->pipe[c & 1];
-            const uint64_t beg = c * chunk, cnt = std::min(chunk, q - beg);
+            cnt = std::min<uint64_t>(chunk_rows(c, q - beg), q - beg);
             const char* src = static_cast<const char*>(rows) + beg * row_bytes;
             sc.rows.ensure(chunk * row_bytes + tail_bytes);
             sc.bucket.ensure(chunk * 4);
