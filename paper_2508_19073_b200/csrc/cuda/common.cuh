@@ -22,19 +22,29 @@ namespace carma_b200 {
 // every compute entry point calls this first.
 void require_device(int device);
 
-// RAII device buffer (grow-only).
+// Caching device allocator: cudaFree returns memory to the driver and the
+// next cudaMalloc maps it again (~0.5 ms per pair on B200), which dominated
+// short calls (one replay plan: ~7 ms of create + destroy for a 0.9 ms run).
+// Blocks go back to a per-device free list instead; the cache is capped.
+// Contract: a block is released only when no queued work still uses it
+// (owners synchronise their streams first; DeviceBuffer::ensure synchronises
+// the device before recycling a block it outgrew).
+void* pool_alloc(size_t bytes, size_t* capacity);
+void pool_free(void* p, size_t capacity);
+
+// RAII device buffer (grow-only), backed by the caching allocator.
 struct DeviceBuffer {
     void* ptr = nullptr;
     size_t bytes = 0;
     void ensure(size_t want) {
         if (want <= bytes) return;
+        if (ptr) CARMA_CUDA(cudaDeviceSynchronize());  // queued work may still use the old block
         release();
         if (want == 0) return;
-        CARMA_CUDA(cudaMalloc(&ptr, want));
-        bytes = want;
+        ptr = pool_alloc(want, &bytes);
     }
     void release() {
-        if (ptr) cudaFree(ptr);
+        if (ptr) pool_free(ptr, bytes);
         ptr = nullptr;
         bytes = 0;
     }

@@ -1404,9 +1404,7 @@ carma_status carma_knn_destroy(carma_knn* hh) {
         if (!h) return;
         {
             DeviceGuard g(h->device);
-            cudaStreamSynchronize(h->stream);
-            cudaStreamSynchronize(h->pipe[0]);
-            cudaStreamSynchronize(h->pipe[1]);
+            cudaDeviceSynchronize();  // device calls may have queued work on caller streams
             for (auto& m : h->model) {
                 m.pts.release();
                 m.ptsf.release();

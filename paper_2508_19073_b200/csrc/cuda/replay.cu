@@ -12,6 +12,10 @@
 #include "pick.cuh"
 #include "replay_kernel.cuh"
 
+#ifndef REPLAY_SMALL_PLAN
+#define REPLAY_SMALL_PLAN 64  // plans with at most this many jobs in a class use the large tier
+#endif
+
 namespace carma_b200 {
 namespace {
 
@@ -277,7 +281,10 @@ bool run_group(ReplayPlan& pl, const replay::Params& p, uint32_t off0) {
     uint32_t off = 0;
     for (int cls = 0; cls < 2; ++cls) {
         const uint32_t cnt = pl.class_count[cb + cls];
-        if (cnt) launch_tier<F>(pl, p, list + off, cnt, cls, pl.class_max_g[cb + cls], counters + 2 * cls, retry + off);
+        // A handful of jobs cannot fill the GPU: the one-warp-per-CTA large
+        // tier (no register cap) finishes each of them sooner.
+        const int tier = (REPLAY_SMALL_PLAN > 0 && cnt <= REPLAY_SMALL_PLAN && pl.max_blocks <= 128) ? 3 : cls;
+        if (cnt) launch_tier<F>(pl, p, list + off, cnt, tier, pl.class_max_g[cb + cls], counters + 2 * cls, retry + off);
         off += cnt;
     }
     if (F == 0) CARMA_CUDA(cudaEventRecord(pl.ev[1], pl.stream));
