@@ -229,7 +229,13 @@ typedef struct carma_replay_config {
      * (runner.cpp:80-93). Ticks are events (energy-integration breakpoints),
      * so they change the run exactly as in the reference. 0 = off. */
     double sample_interval;
-} carma_replay_config; /* 208 bytes */
+    /* RunConfig::enable_event_log (bit 0, World::log_event, world.cpp:94-153)
+     * and verbose_decisions (bit 1, the decision log, manager.cpp:298-318):
+     * records are written per job (carma_replay_plan_log) and formatted by
+     * the host. They do not change the run. */
+    int32_t log_flags;
+    int32_t log_reserved;
+} carma_replay_config; /* 216 bytes */
 
 /* One materialised task (TaskSpec, task.hpp:63-80) as the replay sees it. */
 typedef struct carma_task {
@@ -311,6 +317,32 @@ typedef struct carma_timeline_row {
     int32_t gpu;
     int32_t reserved;
 } carma_timeline_row; /* 40 bytes */
+
+#define CARMA_LOG_EVENTS 1
+#define CARMA_LOG_DECISIONS 2
+#define CARMA_REC_PLACE 0     /* "t=%.3f ev=place task=%s gpus=%zu": gpu = #gpus */
+#define CARMA_REC_COMPLETE 1  /* "t=%.3f ev=complete task=%s" */
+#define CARMA_REC_OOM 2       /* "t=%.3f ev=alloc_oom gpu=%d task=%s req=%llu free=%llu largest=%llu" */
+#define CARMA_REC_DECIDE 3    /* "t=%.3f decide task=%s policy=%s gpu=%d|defer est_bytes=%llu" */
+
+/* One event-log or decision-log line before formatting. */
+typedef struct carma_log_record {
+    double t;
+    uint64_t a;     /* OOM: requested bytes; DECIDE: est_bytes */
+    uint64_t b;     /* OOM: free bytes in the allocation range */
+    uint64_t c;     /* OOM: largest free run in the range */
+    uint32_t task;  /* trace row */
+    int16_t gpu;    /* PLACE: GPUs used; OOM: device; DECIDE: first GPU or -1 (defer) */
+    uint8_t kind;   /* CARMA_REC_* */
+    uint8_t policy; /* DECIDE: policy printed */
+} carma_log_record; /* 40 bytes */
+
+/* Device capacity for log records of every job whose config has log_flags
+ * set (call before carma_replay_plan_run); extra records are counted. */
+carma_status carma_replay_plan_set_log_capacity(carma_replay_plan* p, uint64_t records_per_job);
+/* Records of job j in run order (host buffer of cap); *n = produced. */
+carma_status carma_replay_plan_log(carma_replay_plan* p, uint32_t job, carma_log_record* recs, uint64_t cap,
+                                   uint64_t* n);
 
 /* Device capacity for timeline rows of every job whose config has
  * sample_interval > 0 (call before carma_replay_plan_run). A job that

@@ -309,6 +309,8 @@ struct RefConfig {
     int32_t mig_reserved;
     double mig_fractions[8];
     double sample_interval;    // > 0: RunConfig::enable_timeline with this interval
+    int32_t log_flags;         // 1: enable_event_log, 2: verbose_decisions
+    int32_t log_reserved;
 };
 
 struct RefTaskOut {
@@ -359,6 +361,8 @@ RunConfig make_rc(const RefConfig& c) {
         rc.enable_timeline = true;
         rc.sample_interval = c.sample_interval;
     }
+    rc.enable_event_log = (c.log_flags & 1) != 0;
+    rc.verbose_decisions = (c.log_flags & 2) != 0;
     return rc;
 }
 
@@ -483,6 +487,26 @@ int ref_timeline(const RefConfig* cfg, int mix, uint64_t seed, char* buf, uint64
         for (const auto& l : art.timeline) out += l + "\n";
         if (out.size() + 1 > cap) throw CarmaError("timeline buffer too small");
         std::memcpy(buf, out.c_str(), out.size() + 1);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// The event log and decision log of one run, newline-joined.
+int ref_logs(const RefConfig* cfg, int mix, uint64_t seed, char* events, uint64_t ecap, char* decisions,
+             uint64_t dcap) {
+    try {
+        RunConfig rc = make_rc(*cfg);
+        rc.mix = static_cast<TraceMix>(mix);
+        rc.trace_seed = seed;
+        RunArtifacts art = run_simulation(rc);
+        std::string e, d;
+        for (const auto& l : art.event_log) e += l + "\n";
+        for (const auto& l : art.decision_log) d += l + "\n";
+        if (e.size() + 1 > ecap || d.size() + 1 > dcap) throw CarmaError("log buffer too small");
+        std::memcpy(events, e.c_str(), e.size() + 1);
+        std::memcpy(decisions, d.c_str(), d.size() + 1);
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

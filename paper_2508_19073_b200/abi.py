@@ -58,7 +58,15 @@ replay_config_dtype = np.dtype([
     ("oom_startup_delay", "<f8"),
     ("mig_count", "<i4"), ("mig_reserved", "<i4"), ("mig_fraction", "<f8", (8,)),
     ("mig_base", "<u2", (8,)), ("mig_blocks", "<u2", (8,)), ("sample_interval", "<f8"),
+    ("log_flags", "<i4"), ("log_reserved", "<i4"),
 ], align=True)
+
+log_record_dtype = np.dtype([
+    ("t", "<f8"), ("a", "<u8"), ("b", "<u8"), ("c", "<u8"), ("task", "<u4"), ("gpu", "<i2"), ("kind", "u1"),
+    ("policy", "u1"),
+], align=True)
+LOG_EVENTS, LOG_DECISIONS = 1, 2
+REC_PLACE, REC_COMPLETE, REC_OOM, REC_DECIDE = 0, 1, 2, 3
 
 timeline_row_dtype = np.dtype([
     ("t", "<f8"), ("smact", "<f8"), ("power_w", "<f8"), ("used", "<u8"), ("gpu", "<i4"), ("reserved", "<i4"),
@@ -98,7 +106,7 @@ pick_request_dtype = np.dtype([
 assert feature_row_dtype.itemsize == 136
 assert feature_packed_dtype.itemsize == 64
 assert task_outcome_dtype.itemsize == 24
-assert replay_config_dtype.itemsize == 208
+assert replay_config_dtype.itemsize == 216
 assert task_dtype.itemsize == 48
 assert task_result_dtype.itemsize == 64
 assert trace_result_dtype.itemsize == 80
@@ -147,6 +155,8 @@ SIGNATURES = {
     "carma_pick_batch_device": (c_int, [c_int, P, P, c_uint32, P, c_uint64, P, P, c_void_p]),
     "carma_replay_plan_set_timeline_capacity": (c_int, [c_void_p, c_uint64]),
     "carma_replay_plan_timeline": (c_int, [c_void_p, c_uint32, P, c_uint64, POINTER(c_uint64)]),
+    "carma_replay_plan_set_log_capacity": (c_int, [c_void_p, c_uint64]),
+    "carma_replay_plan_log": (c_int, [c_void_p, c_uint32, P, c_uint64, POINTER(c_uint64)]),
     # carma_host.h
     "carma_host_catalog_size": (c_int, []),
     "carma_host_catalog_entry": (c_int, [c_int, c_char_p, c_int, P, P, P, P]),

@@ -363,7 +363,7 @@ class PolicyConfig:
 
 
 def make_config(policy: PolicyConfig, consts: SimConstants, mig_instances: Optional[Sequence[float]] = None,
-                sample_interval: float = 0.0) -> np.ndarray:
+                sample_interval: float = 0.0, log_flags: int = 0) -> np.ndarray:
     """carma_replay_config of a PolicyConfig + SimConstants (+ RunConfig::mig_instances and, when > 0,
     the timeline's sample_interval, runner.hpp:23-33)."""
     c = np.zeros(1, abi.replay_config_dtype)
@@ -382,6 +382,7 @@ def make_config(policy: PolicyConfig, consts: SimConstants, mig_instances: Optio
     c["boost_threshold"] = consts.boost_threshold
     c["oom_startup_delay"] = consts.oom_startup_delay
     c["sample_interval"] = sample_interval
+    c["log_flags"] = log_flags
     if policy.collocation_mode == "mig":
         fr = np.ascontiguousarray([] if mig_instances is None else mig_instances, np.float64)
         check(lib.carma_mig_layout(ptr(fr) if len(fr) else None, len(fr), ptr(c)))
@@ -459,6 +460,19 @@ class ReplayPlan:
             raise abi.CarmaError(abi.CARMA_ERR_OVERFLOW, f"timeline capacity too small ({n.value} rows)")
         return rows
 
+    def set_log_capacity(self, records_per_job: int) -> None:
+        check(lib.carma_replay_plan_set_log_capacity(self._h, records_per_job))
+
+    def log(self, job: int) -> np.ndarray:
+        """Event / decision log records of `job` (log_record_dtype) in run order."""
+        n = ctypes.c_uint64()
+        check(lib.carma_replay_plan_log(self._h, job, None, 0, ctypes.byref(n)))
+        recs = np.zeros(n.value, abi.log_record_dtype)
+        check(lib.carma_replay_plan_log(self._h, job, ptr(recs), n.value, ctypes.byref(n)))
+        if n.value > len(recs):
+            raise abi.CarmaError(abi.CARMA_ERR_OVERFLOW, f"log capacity too small ({n.value} records)")
+        return recs
+
     def stats(self):
         la, rt = ctypes.c_uint64(), ctypes.c_uint64()
         check(lib.carma_replay_plan_stats(self._h, ctypes.byref(la), ctypes.byref(rt)))
@@ -519,6 +533,8 @@ class RunConfig:
     mig_instances: List[float] = dataclasses.field(default_factory=list)  # fractions, mig mode only
     enable_timeline: bool = False
     sample_interval: float = 10.0
+    enable_event_log: bool = False
+    verbose_decisions: bool = False
 
 
 def provision_estimates(rc: RunConfig, m: Materialized, device: int = 0,
@@ -556,40 +572,76 @@ def format_timeline(rows: np.ndarray) -> List[str]:
                                 for r in rows]
 
 
+_POLICY_NAMES = {v: k for k, v in abi.POLICY.items()}
+
+
+def task_ids(m: "Materialized") -> List[str]:
+    """TaskSpec ids of materialize_trace (traces.cpp:374): t%03zu-<catalog key>."""
+    keys = [e.key for e in builtin_catalog()]
+    return ["t%03d-%s" % (i, keys[e]) for i, e in enumerate(m.entry.tolist())]
+
+
+def format_logs(recs: np.ndarray, ids: Sequence[str]):
+    """(event_log, decision_log) lines exactly as World::log_event
+    (world.cpp:94-153) and the decision log (manager.cpp:298-318) print them."""
+    events, decisions = [], []
+    for r in recs:
+        t, task, kind = float(r["t"]), ids[int(r["task"])], int(r["kind"])
+        if kind == abi.REC_PLACE:
+            events.append("t=%.3f ev=place task=%s gpus=%d" % (t, task, int(r["gpu"])))
+        elif kind == abi.REC_COMPLETE:
+            events.append("t=%.3f ev=complete task=%s" % (t, task))
+        elif kind == abi.REC_OOM:
+            events.append("t=%.3f ev=alloc_oom gpu=%d task=%s req=%d free=%d largest=%d"
+                          % (t, int(r["gpu"]), task, int(r["a"]), int(r["b"]), int(r["c"])))
+        else:
+            gpu = "defer" if int(r["gpu"]) < 0 else "%d" % int(r["gpu"])
+            decisions.append("t=%.3f decide task=%s policy=%s gpu=%s est_bytes=%d"
+                             % (t, task, _POLICY_NAMES[int(r["policy"])], gpu, int(r["a"])))
+    return events, decisions
+
+
 @dataclasses.dataclass
 class RunArtifacts:
     """run_simulation's artifacts (runner.hpp:38-47): report scalars, per-task and per-GPU results,
-    and the timeline text when RunConfig.enable_timeline is set."""
+    and the timeline / event log / decision log text when the RunConfig switches are set."""
 
     report: np.ndarray
     tasks: np.ndarray
     gpus: np.ndarray
     timeline: List[str]
+    event_log: List[str] = dataclasses.field(default_factory=list)
+    decision_log: List[str] = dataclasses.field(default_factory=list)
 
 
 def run_simulation_artifacts(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None,
-                             timeline_rows: int = 1 << 20) -> RunArtifacts:
+                             timeline_rows: int = 1 << 20, log_records: int = 1 << 20) -> RunArtifacts:
     """run_simulation with the reference's output switches: the sample ticks of
     enable_timeline are events of the replay (they split the energy integration
     exactly as in the reference), their rows come back formatted."""
     trace = load_trace(rc.trace_path) if rc.trace_path else generate_trace(rc.mix, rc.trace_seed)
     m = materialize_trace(trace)
     provision_estimates(rc, m, device, knn)
-    cfg = make_config(rc.policy, rc.constants, rc.mig_instances, rc.sample_interval if rc.enable_timeline else 0.0)
+    flags = (abi.LOG_EVENTS if rc.enable_event_log else 0) | (abi.LOG_DECISIONS if rc.verbose_decisions else 0)
+    cfg = make_config(rc.policy, rc.constants, rc.mig_instances, rc.sample_interval if rc.enable_timeline else 0.0,
+                      flags)
     jobs = np.zeros(1, abi.job_dtype)
     plan = ReplayPlan(cfg, m.tasks, np.array([0, len(m.tasks)], np.uint64), jobs, device)
     try:
         if rc.enable_timeline:
             plan.set_timeline_capacity(timeline_rows)
+        if flags:
+            plan.set_log_capacity(log_records)
         plan.run()
         res = plan.results()
         tl = format_timeline(plan.timeline(0)) if rc.enable_timeline else []
+        ev, dec = format_logs(plan.log(0), task_ids(m)) if flags else ([], [])
     finally:
         plan.close()
     st = int(res.traces["status"][0])
     if st != 0:
         raise abi.CarmaError(3 if st < 0 else st, f"run failed (status {st})")
-    return RunArtifacts(res.traces[0], res.job_tasks(0), res.job_gpus(0), tl)
+    return RunArtifacts(res.traces[0], res.job_tasks(0), res.job_gpus(0), tl, ev, dec)
 
 
 class FusedReplay:

@@ -156,8 +156,9 @@ struct ReplayPlan {
     int class_max_g[12] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
     std::vector<uint32_t> class_list;  // jobs ordered by class
     DeviceBuffer d_cfgs, d_tasks, d_trace_off, d_jobs, d_task_off, d_gpu_off, d_list, d_task_out,
-        d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate, d_outcomes, d_tl, d_tl_count;
-    uint64_t tl_cap = 0;
+        d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate, d_outcomes, d_tl, d_tl_count, d_log,
+        d_log_count;
+    uint64_t tl_cap = 0, log_cap = 0;
     const uint64_t* est_override = nullptr;
     uint64_t launches = 0, retried = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // run start, shared-memory tiers end, run end
@@ -200,6 +201,7 @@ void validate_config(const carma_replay_config& c) {
     if (c.gpu_capacity / c.alloc_block > 64ull * replay::kMaxWords)
         throw Unsupported("more than 256 allocation blocks per GPU");
     if (!(c.sample_interval >= 0.0)) throw InvalidArg("ConfigError: sample_interval must be >= 0");
+    if (c.log_flags & ~(CARMA_LOG_EVENTS | CARMA_LOG_DECISIONS)) throw InvalidArg("unknown log_flags bits");
     if (c.mode == CARMA_MODE_MIG) {
         // the table carma_mig_layout builds (gpu.cpp:29-51)
         if (c.mig_count < 1 || c.mig_count > CARMA_MAX_MIG)
@@ -338,6 +340,9 @@ void run_plan(ReplayPlan& pl) {
     p.tl_out = pl.d_tl.as<carma_timeline_row>();
     p.tl_cap = pl.tl_cap;
     p.tl_count = pl.d_tl_count.as<uint64_t>();
+    p.log_out = pl.d_log.as<carma_log_record>();
+    p.log_cap = pl.log_cap;
+    p.log_count = pl.d_log_count.as<uint64_t>();
     const uint32_t n = static_cast<uint32_t>(pl.jobs.size());
     pl.launches = 0;
     pl.retried = 0;
@@ -355,7 +360,13 @@ void run_plan(ReplayPlan& pl) {
     else CARMA_CUDA(cudaEventRecord(pl.ev[1], pl.stream));
     if (count(1)) dirty |= run_group<1>(pl, p, off[1]);
     if (count(2) || count(3)) {
-        if (pl.tl_cap == 0) throw InvalidArg("timeline jobs need carma_replay_plan_set_timeline_capacity first");
+        for (const auto& jb : pl.jobs) {
+            const carma_replay_config& c = pl.cfgs[jb.config];
+            if (c.sample_interval > 0.0 && pl.tl_cap == 0)
+                throw InvalidArg("timeline jobs need carma_replay_plan_set_timeline_capacity first");
+            if (c.log_flags != 0 && pl.log_cap == 0)
+                throw InvalidArg("logging jobs need carma_replay_plan_set_log_capacity first");
+        }
         if (count(2)) dirty |= run_group<2>(pl, p, off[2]);
         if (count(3)) dirty |= run_group<3>(pl, p, off[3]);
     }
@@ -435,7 +446,8 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
                     // > 128 allocation blocks: the shared-memory layouts hold 2 bitmap words;
                     // MIG / timeline jobs form classes 3F.. (their own kernels); timeline
                     // jobs are global-only (large and global tiers)
-                    const int feat = (c.mode == CARMA_MODE_MIG ? 1 : 0) | (c.sample_interval > 0.0 ? 2 : 0);
+                    const int feat = (c.mode == CARMA_MODE_MIG ? 1 : 0) |
+                                     ((c.sample_interval > 0.0 || c.log_flags != 0) ? 2 : 0);
                     const int tier = (c.gpu_capacity / c.alloc_block > 128 || (feat & 2)) ? 2
                                                                                            : static_cast<int>(heavy_config(c));
                     const int jc = tier + 3 * feat;
@@ -453,6 +465,7 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
             pl->d_begin.ensure(n_jobs * sizeof(double));
             pl->d_counters.ensure(128);
             pl->d_tl_count.ensure(n_jobs * sizeof(uint64_t));
+            pl->d_log_count.ensure(n_jobs * sizeof(uint64_t));
         } catch (...) {
             if (pl->stream) cudaStreamDestroy(pl->stream);
             delete pl;
@@ -579,6 +592,36 @@ carma_status carma_replay_plan_set_timeline_capacity(carma_replay_plan* hp, uint
     });
 }
 
+carma_status carma_replay_plan_set_log_capacity(carma_replay_plan* hp, uint64_t records_per_job) {
+    return guarded([&] {
+        auto* pl = reinterpret_cast<ReplayPlan*>(hp);
+        if (!pl) throw InvalidArg("null plan");
+        std::lock_guard<std::mutex> lock(pl->mu);
+        DeviceGuard guard(pl->device);
+        pl->d_log.ensure(records_per_job * pl->jobs.size() * sizeof(carma_log_record));
+        pl->log_cap = records_per_job;
+    });
+}
+
+carma_status carma_replay_plan_log(carma_replay_plan* hp, uint32_t job, carma_log_record* recs, uint64_t cap,
+                                   uint64_t* n_out) {
+    return guarded([&] {
+        auto* pl = reinterpret_cast<ReplayPlan*>(hp);
+        if (!pl) throw InvalidArg("null plan");
+        if (job >= pl->jobs.size()) throw InvalidArg("job index out of range");
+        if (pl->cfgs[pl->jobs[job].config].log_flags == 0) throw InvalidArg("job has no log");
+        DeviceGuard guard(pl->device);
+        CARMA_CUDA(cudaStreamSynchronize(pl->stream));
+        uint64_t n = 0;
+        CARMA_CUDA(cudaMemcpy(&n, pl->d_log_count.as<uint64_t>() + job, sizeof(n), cudaMemcpyDeviceToHost));
+        if (n_out) *n_out = n;
+        const uint64_t k = std::min(std::min(n, pl->log_cap), cap);
+        if (recs && k)
+            CARMA_CUDA(cudaMemcpy(recs, pl->d_log.as<carma_log_record>() + static_cast<uint64_t>(job) * pl->log_cap,
+                                  k * sizeof(carma_log_record), cudaMemcpyDeviceToHost));
+    });
+}
+
 carma_status carma_replay_plan_timeline(carma_replay_plan* hp, uint32_t job, carma_timeline_row* rows, uint64_t cap,
                                         uint64_t* n_rows) {
     return guarded([&] {
@@ -608,7 +651,7 @@ carma_status carma_replay_plan_destroy(carma_replay_plan* hp) {
             DeviceBuffer* bufs[] = {&pl->d_cfgs, &pl->d_tasks, &pl->d_trace_off, &pl->d_jobs, &pl->d_task_off,
                                     &pl->d_gpu_off, &pl->d_list, &pl->d_task_out, &pl->d_trace_out, &pl->d_gpu_out,
                                     &pl->d_inv, &pl->d_begin, &pl->d_counters, &pl->d_gstate, &pl->d_outcomes,
-                                    &pl->d_tl, &pl->d_tl_count};
+                                    &pl->d_tl, &pl->d_tl_count, &pl->d_log, &pl->d_log_count};
             for (auto* b : bufs) b->release();
             for (auto& e : pl->ev)
                 if (e) cudaEventDestroy(e);

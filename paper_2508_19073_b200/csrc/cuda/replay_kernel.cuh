@@ -84,6 +84,15 @@ struct Params {
     carma_timeline_row* tl_out;  // timeline rows, tl_cap per job (TL kernels only)
     uint64_t tl_cap;
     uint64_t* tl_count;          // rows produced, per job
+    carma_log_record* log_out;   // event / decision log records, log_cap per job (TL kernels only)
+    uint64_t log_cap;
+    uint64_t* log_count;         // records produced, per job
+};
+
+// alloc_oom details of a failed placement (OomFailure, gpu.hpp:26-35), in blocks.
+struct OomInfo {
+    int gpu;
+    uint32_t free_blk, largest_blk;
 };
 
 // Compile-time state layout: G GPUs, H heap entries, S slots, RC residents
@@ -94,7 +103,7 @@ template <int G_, int H_, int S_, int RC_, int RG_, int RQ_, int W_, int F_ = 0>
 struct Layout {
     static constexpr int G = G_, H = H_, S = S_, RC = RC_, RG = RG_, RQ = RQ_, W = W_;
     static constexpr bool MIG = (F_ & 1) != 0;
-    static constexpr bool TL = (F_ & 2) != 0;
+    static constexpr bool TL = (F_ & 2) != 0;  // diagnostics: timeline ticks and/or event/decision logs
     static constexpr size_t MI = MIG ? 1 : 0;
     static constexpr int GPL = (G + 31) / 32;
     static constexpr size_t al8(size_t x) { return (x + 15) / 16 * 16; }
@@ -326,6 +335,29 @@ __device__ __forceinline__ uint32_t free_in_range(const uint64_t* used, int g, i
         f += __popcll(static_cast<long long>(~used[w * L::G + g] & m));
     }
     return f;
+}
+
+// Free blocks and the largest free run inside [r0, r1) (allocate_range's
+// total_free_in_range / largest_free_in_range, gpu.cpp:77-86).
+template <class L>
+__device__ __forceinline__ void range_stats(char* b, int g, int nblk, int r0, int r1, uint32_t& free_blk,
+                                            uint32_t& largest) {
+    const uint64_t* used = RP_U64(used);
+    free_blk = 0;
+    largest = 0;
+    int pos = 0;
+#pragma unroll 1
+    while (pos < nblk) {
+        const int start = next_bit<L>(used, g, pos, nblk, false);
+        if (start >= nblk || start >= r1) break;
+        const int end = next_bit<L>(used, g, start, nblk, true);
+        const int lo = start > r0 ? start : r0, hi = end < r1 ? end : r1;
+        if (lo < hi) {
+            free_blk += static_cast<uint32_t>(hi - lo);
+            if (static_cast<uint32_t>(hi - lo) > largest) largest = static_cast<uint32_t>(hi - lo);
+        }
+        pos = end;
+    }
 }
 
 // MIG instance of slot on GPU g (the slot's first or second device).
@@ -613,7 +645,7 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
 // slot and append the task to the resident lists.
 template <class L>
 __device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint32_t task, int g0, int g1,
-                                      int i0, int i1, int want, int nblk, unsigned lane) {
+                                      int i0, int i1, int want, int nblk, unsigned lane, OomInfo& oi) {
     const carma_replay_config& cf = RP_CFG;
     const uint64_t block = cf.alloc_block;
     const uint64_t bytes = tk.true_mem > 0 ? tk.true_mem : 1;
@@ -622,16 +654,30 @@ __device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint
     // MIG: allocate_on_instance (gpu.cpp:67-70) inside the instance's blocks
     constexpr bool mig = L::MIG;
     const int a0 = mig ? cf.mig_base[i0] : 0, e0 = mig ? a0 + cf.mig_blocks[i0] : nblk;
+    // failure details on the failing device (diagnostic kernels only)
+    auto oom = [&](int g, int r0, int r1) {
+        if constexpr (L::TL) {
+            uint32_t f = 0, lg = 0;
+            if ((g & 31) == static_cast<int>(lane)) range_stats<L>(b, g, nblk, r0, r1, f, lg);
+            oi.gpu = g;
+            oi.free_blk = __shfl_sync(0xffffffffu, f, g & 31);
+            oi.largest_blk = __shfl_sync(0xffffffffu, lg, g & 31);
+        }
+    };
     int off0 = -1, off1 = 0;
     if ((g0 & 31) == static_cast<int>(lane) && nb <= nblk) off0 = first_fit<L>(b, g0, nblk, nb, a0, e0);
     off0 = __shfl_sync(0xffffffffu, off0, g0 & 31);
-    if (off0 < 0) return false;
+    if (off0 < 0) {
+        oom(g0, a0, e0);
+        return false;
+    }
     if (want > 1) {
         const int a1 = mig ? cf.mig_base[i1] : 0, e1 = mig ? a1 + cf.mig_blocks[i1] : nblk;
         int o = -1;
-        if ((g1 & 31) == static_cast<int>(lane)) o = first_fit<L>(b, g1, nblk, nb, a1, e1);
+        if ((g1 & 31) == static_cast<int>(lane) && nb <= nblk) o = first_fit<L>(b, g1, nblk, nb, a1, e1);
         o = __shfl_sync(0xffffffffu, o, g1 & 31);
         if (o < 0) {
+            oom(g1, a1, e1);
             if ((g0 & 31) == static_cast<int>(lane)) set_bits<L>(RP_U64(used), g0, off0, nb, false);
             __syncwarp();
             return false;
@@ -721,7 +767,7 @@ __device__ __forceinline__ void finish(char* b, Sc& c, uint32_t slot, carma_task
 template <class L>
 __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, const uint64_t* est,
                                       uint32_t& head, bool& from_recovery, int& g0, int& g1, int& i0, int& i1,
-                                      unsigned lane) {
+                                      uint64_t& est_bytes, unsigned lane) {
     const carma_replay_config& cf = RP_CFG;
     const int G = cf.gpu_count;
     const uint32_t* nres = RP_U32(nres);
@@ -739,9 +785,11 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
     else return 0;
     const int policy = from_recovery ? CARMA_POLICY_EXCLUSIVE : cf.policy;
     uint64_t floor = cf.min_free, need = 0;
+    est_bytes = 0;  // the decision log's est_bytes (manager.cpp:292-294, 301-315)
     if (!from_recovery && cf.policy != CARMA_POLICY_EXCLUSIVE) {
         const uint64_t e = est ? est[head] : tasks[head].estimate;
         if (e != CARMA_NO_ESTIMATE) {
+            est_bytes = e;
             need = e < cf.gpu_capacity ? e : cf.gpu_capacity;
             if (need > floor) floor = need;
         }
@@ -1020,6 +1068,26 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
     uint32_t tick_seq = 0, n_done = 0;
     bool tick_live = false;
     uint64_t tl_rows = 0;
+    // event / decision log (L::TL kernels): records in run order, lane 0 writes
+    const int32_t log_flags = L::TL ? RP_CFG.log_flags : 0;
+    uint64_t n_log = 0;
+    auto log = [&](uint8_t kind, uint32_t task, int gpu, uint64_t a, uint64_t b2, uint64_t c2, uint8_t pol) {
+        if constexpr (L::TL) {
+            if (lane == 0 && n_log < p.log_cap) {
+                carma_log_record r;
+                r.t = c.now;
+                r.a = a;
+                r.b = b2;
+                r.c = c2;
+                r.task = task;
+                r.gpu = static_cast<int16_t>(gpu);
+                r.kind = kind;
+                r.policy = pol;
+                p.log_out[static_cast<uint64_t>(j) * p.log_cap + n_log] = r;
+            }
+            ++n_log;
+        }
+    };
     if constexpr (L::TL) {
         tick_live = RP_CFG.sample_interval > 0.0;
         tick_t = tasks[0].submit;
@@ -1122,7 +1190,11 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
         } else if (kind == kCompletion) {
             if (RP_U32(s_seq)[payload] != seq) continue;  // superseded by a rate change
             finish<L>(b, c, payload, out, t0, t1, nt, lane);
-            if constexpr (L::TL) ++n_done;
+            if constexpr (L::TL) {
+                ++n_done;
+                if (log_flags & CARMA_LOG_EVENTS)
+                    log(CARMA_REC_COMPLETE, RP_U32(s_task)[payload], 0, 0, 0, 0, 0);  // world.cpp:151-153
+            }
         } else {  // oom_crash -> handle_oom (manager.cpp:262-267)
             c.oom++;
             if (lane == 0) {
@@ -1150,10 +1222,19 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             }
             if (!sched) break;
             sched = false;
-            uint32_t head = 0;
+            uint32_t head = kNone;
             bool from_recovery = false;
             int g0 = -1, g1 = -1, i0 = 0, i1 = 0;
-            const int got = decide<L>(b, c, tasks, est, head, from_recovery, g0, g1, i0, i1, lane);
+            uint64_t est_bytes = 0;
+            const int got = decide<L>(b, c, tasks, est, head, from_recovery, g0, g1, i0, i1, est_bytes, lane);
+            if constexpr (L::TL) {
+                // the decision log of try_schedule (manager.cpp:298-318): logged whenever
+                // map_task ran; a deferral prints the configured policy
+                if ((log_flags & CARMA_LOG_DECISIONS) && head != kNone) {
+                    const int pol = got == 0 ? RP_CFG.policy : (from_recovery ? CARMA_POLICY_EXCLUSIVE : RP_CFG.policy);
+                    log(CARMA_REC_DECIDE, head, got == 0 ? -1 : g0, est_bytes, 0, 0, static_cast<uint8_t>(pol));
+                }
+            }
             if (got == 0) break;  // defer; retried on the next completion / expiry
             if (from_recovery) {
                 c.rq_head = c.rq_head + 1 == static_cast<uint32_t>(L::RQ) ? 0 : c.rq_head + 1;
@@ -1163,8 +1244,21 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             }
             // dispatch (manager.cpp:247-260)
             if (lane == 0 && !from_recovery) out[head].first_attempt = c.now;
-            const bool ok = place<L>(b, c, tasks[head], head, g0, g1, i0, i1, got, nblk, lane);
+            OomInfo oi{};
+            const bool ok = place<L>(b, c, tasks[head], head, g0, g1, i0, i1, got, nblk, lane, oi);
             if (c.status) break;
+            if constexpr (L::TL) {
+                if (log_flags & CARMA_LOG_EVENTS) {
+                    const uint64_t blk = RP_CFG.alloc_block;
+                    if (ok) {
+                        log(CARMA_REC_PLACE, head, got, 0, 0, 0, 0);  // world.cpp:126-128
+                    } else {  // world.cpp:94-104: want = round_up(max(bytes, 1))
+                        const uint64_t bytes = tasks[head].true_mem > 0 ? tasks[head].true_mem : 1;
+                        log(CARMA_REC_OOM, head, oi.gpu, (bytes + blk - 1) / blk * blk, oi.free_blk * blk,
+                            oi.largest_blk * blk, 0);
+                    }
+                }
+            }
             if (ok) {
                 if (lane == 0) {
                     carma_task_result& o = out[head];
@@ -1190,7 +1284,10 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
         __syncwarp();
     }
     if constexpr (L::TL) {
-        if (lane == 0) p.tl_count[j] = tl_rows;
+        if (lane == 0) {
+            p.tl_count[j] = tl_rows;
+            p.log_count[j] = n_log;
+        }
     }
     c.events_lo = static_cast<uint32_t>(events);
     c.events_hi = static_cast<uint32_t>(events >> 32);

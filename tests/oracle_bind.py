@@ -62,6 +62,7 @@ def load_ref():
                                     POINTER(c_double)]
     lib.ref_run_sweep.argtypes = [P, c_int, c_int, P, c_int, c_char_p, c_uint64]
     lib.ref_timeline.argtypes = [P, c_int, c_uint64, c_char_p, c_uint64]
+    lib.ref_logs.argtypes = [P, c_int, c_uint64, c_char_p, c_uint64, c_char_p, c_uint64]
     return lib
 
 
@@ -71,6 +72,7 @@ ref_config_dtype = np.dtype([
     ("monitor_window", "<f8"), ("gpu_count", "<i4"), ("gpu_capacity", "<u8"), ("alloc_block", "<u8"),
     ("estimator_seed", "<u8"), ("estimator_k", "<u8"), ("estimator_samples", "<u8"),
     ("mig_count", "<i4"), ("mig_reserved", "<i4"), ("mig_fractions", "<f8", (8,)), ("sample_interval", "<f8"),
+    ("log_flags", "<i4"), ("log_reserved", "<i4"),
 ], align=True)
 
 ref_task_out_dtype = np.dtype([
@@ -88,8 +90,9 @@ ref_trace_out_dtype = np.dtype([
 
 def ref_config(policy="magm", estimator="none", mode="mps", rr_pre=False, max_smact=0.8, min_free=None,
                margin=2 * abi.GiB, window=60.0, gpu_count=4, capacity=40 * abi.GiB, block=512 * abi.MiB,
-               est_seed=11, est_k=5, est_samples=4000, mig=(), sample_interval=0.0):
+               est_seed=11, est_k=5, est_samples=4000, mig=(), sample_interval=0.0, log_flags=0):
     c = np.zeros(1, ref_config_dtype)
+    c["log_flags"] = log_flags
     c["sample_interval"] = sample_interval
     c["mig_count"] = len(mig)
     c["mig_fractions"][0, : len(mig)] = mig
@@ -121,6 +124,7 @@ def replay_config_from(c):
     r["p_idle_w"], r["p_max_w"], r["p_boost_w"], r["boost_threshold"] = 55.0, 400.0, 30.0, 0.9
     r["oom_startup_delay"] = 5.0
     r["sample_interval"] = c["sample_interval"]
+    r["log_flags"] = c["log_flags"]
     if int(c["mode"][0]) == abi.MODE["mig"]:
         n = int(c["mig_count"][0])
         fr = np.ascontiguousarray(c["mig_fractions"][0, :n], np.float64)

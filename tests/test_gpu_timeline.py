@@ -3,6 +3,7 @@
 completions, reports) must match the reference run WITH the timeline, and the
 timeline text (runner.cpp:80-93, world.cpp:210-219) must be identical."""
 import ctypes
+import dataclasses
 
 import numpy as np
 import pytest
@@ -47,3 +48,33 @@ def test_timeline_off_is_unchanged(gpu):
     a = cb.run_simulation_artifacts(rc, device=gpu)
     r, t, g = cb.run_simulation(rc, device=gpu)
     assert a.timeline == [] and a.report.tobytes() == r.tobytes() and a.tasks.tobytes() == t.tobytes()
+
+
+LOG_CASES = [dict(policy="magm"), dict(policy="rr"), dict(policy="lug", estimator="oracle"),
+             dict(policy="magm", mode="mig", mig=(0.75, 0.25)), dict(policy="exclusive", gpu_count=8)]
+
+
+@pytest.mark.parametrize("case", LOG_CASES, ids=[str(i) for i in range(len(LOG_CASES))])
+@pytest.mark.parametrize("mix,seed", [("t90", 2), ("t60", 5)])
+def test_event_and_decision_logs_match_reference(gpu, ref, case, mix, seed):
+    """RunConfig::enable_event_log + verbose_decisions: place / complete /
+    alloc_oom lines (world.cpp:94-153) and decide lines (manager.cpp:298-318)
+    identical to the reference's, and the run itself unchanged."""
+    kw = dict(case)
+    est = kw.get("estimator", "none")
+    rc = cb.RunConfig(mix=mix, trace_seed=seed, enable_event_log=True, verbose_decisions=True,
+                      policy=cb.PolicyConfig(policy=kw["policy"], estimator=est,
+                                             collocation_mode=kw.get("mode", "mps")),
+                      constants=cb.SimConstants(gpu_count=kw.get("gpu_count", 4)),
+                      mig_instances=list(kw.get("mig", ())))
+    art = cb.run_simulation_artifacts(rc, device=gpu)
+    cfg = ref_config(**kw, log_flags=3)
+    ev = ctypes.create_string_buffer(1 << 22)
+    de = ctypes.create_string_buffer(1 << 22)
+    assert ref.ref_logs(cfg.ctypes.data, cb.abi.MIX[mix], seed, ev, len(ev), de, len(de)) == 0
+    assert "".join(l + "\n" for l in art.event_log) == ev.value.decode()
+    assert "".join(l + "\n" for l in art.decision_log) == de.value.decode()
+    if kw["policy"] == "rr":  # stacking without preconditions: OOM lines are exercised
+        assert any("alloc_oom" in l for l in art.event_log)
+    r, t, g = cb.run_simulation(dataclasses.replace(rc, enable_event_log=False, verbose_decisions=False), device=gpu)
+    assert r.tobytes() == art.report.tobytes() and t.tobytes() == art.tasks.tobytes()
