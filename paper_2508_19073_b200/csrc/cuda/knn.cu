@@ -91,7 +91,9 @@ struct KnnParams {
     double* qrec;  // fp32 path: per row the normalised query (19) + eta, written by knn_prep
 };
 
-constexpr int kQrec = 20;  // doubles per query record (160 B, 16-B aligned)
+// Query record (fp32 path): normalised query (19), eta, t_in (the smallest
+// t18 around the start position), the start position (bits). 176 B.
+constexpr int kQrec = 22;
 
 __device__ __forceinline__ double u2d(uint64_t v) { return __ull2double_rn(v); }
 
@@ -190,6 +192,13 @@ __device__ __forceinline__ double raw18_of(const KnnParams& p, uint64_t i) {
     const carma_feature_row& r = static_cast<const carma_feature_row*>(p.rows)[i];
     return __dadd_rn(__dmul_rn(16.0, u2d(r.total_params)),
                      __dmul_rn(__dmul_rn(4.0, u2d(r.batch_size)), u2d(r.total_activations)));
+}
+
+// t18 = fl(fl(64 * fl(key - q18))^2): the last term of a point's d2 and a lower
+// bound of the whole d2 (every term is >= 0, rounding is monotone).
+__device__ __forceinline__ double t18_of(double key, double q18) {
+    const double diff = __dmul_rn(__dsub_rn(key, q18), 64.0);
+    return __dmul_rn(diff, diff);
 }
 
 __device__ __forceinline__ double normalize(double raw, double lo, double hi) {
@@ -351,6 +360,9 @@ __global__ void __launch_bounds__(512, 2) knn_prep(KnnParams p, uint32_t n_bins,
             for (int h = 0; h < 9; ++h) rec[h] = make_double2(qn[2 * h], qn[2 * h + 1]);
             rec[9] = make_double2(qn[18], eta);
             pos = lower_bound_any(keys[f], static_cast<uint32_t>(m.n), qn[18]);
+            const double t_in = fmin(pos > 0 ? t18_of(keys[f][pos - 1], qn[18]) : inf,
+                                     pos < m.n ? t18_of(keys[f][pos], qn[18]) : inf);
+            rec[10] = make_double2(t_in, __longlong_as_double(static_cast<long long>(pos)));
             bin = m.bin_base + (pos >> m.bin_shift);
         }
         const uint32_t b = bin == kInvalidBin ? n_bins - 1 : bin;
@@ -485,10 +497,6 @@ __device__ __forceinline__ void insert_block(TopK<K>& top, const double (&d2)[kB
     }
 }
 
-__device__ __forceinline__ double t18_of(double key, double q18) {
-    const double diff = __dmul_rn(__dsub_rn(key, q18), 64.0);
-    return __dmul_rn(diff, diff);
-}
 
 template <int K>
 __global__ void __launch_bounds__(128, 4)
@@ -823,6 +831,8 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
             float qf[kF32Dims];
             double eta = 0.0;
             double q18 = 0.0;
+            double t_in = inf;  // precomputed by knn_prep
+            int32_t pos = 0;
             {
                 if (mine) {
                     const double2* rec = reinterpret_cast<const double2*>(p.qrec + static_cast<uint64_t>(row) * kQrec);
@@ -836,6 +846,9 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
                     qsh[18][tid] = v.x;
                     q18 = v.x;
                     eta = v.y;
+                    const double2 w = __ldg(rec + 10);
+                    t_in = w.x;
+                    pos = static_cast<int32_t>(__double_as_longlong(w.y));
                 } else {
 #pragma unroll
                     for (int d = 0; d < kDims; ++d) qsh[d][tid] = 0.0;
@@ -867,11 +880,8 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
             const int mid_lane = __ffs(mm) - 1;
             // model indices fit int32 (carma_knn_set_model rejects n > 2^31 - 1)
             const int32_t n = static_cast<int32_t>(m.n);
-            const int32_t pos = live ? static_cast<int32_t>(qpos[row]) : 0;
             const int32_t start = __shfl_sync(0xffffffffu, pos, mid_lane);
             int32_t L = start, R = start;
-            const double t_in = fmin(pos > 0 ? t18_of(__ldg(m.key18 + pos - 1), q18) : inf,
-                                     pos < n ? t18_of(__ldg(m.key18 + pos), q18) : inf);
             double tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q18) : t_in) : inf;
             double tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q18) : t_in) : inf;
             uint64_t visits = 0, exact = 0;
