@@ -137,6 +137,30 @@ carma_status carma_knn_set_model(carma_knn* h, int32_t family, const double* lo,
                                  const int32_t* labels, uint64_t n, uint32_t k,
                                  uint64_t bucket_range);
 
+/* HoldoutReport (estimators.hpp:96-103). */
+typedef struct carma_holdout_report {
+    double accuracy;
+    double macro_f1;
+    double underestimate_rate;
+    uint64_t train_size;
+    uint64_t holdout_size;
+} carma_holdout_report;
+
+/* train_learned_estimator (estimators.cpp:344-436) on the device, installing
+ * the model for `family`: the dataset (host rows, bucket labels, true bytes as
+ * generate_synthetic_dataset returns them) is uploaded once; the seeded split
+ * is the host's sequential shuffle (carma_host_split_order); the min/max
+ * bounds, the normalised training points, the holdout predictions and the
+ * confusion / underestimate counts are computed on the GPU; macro-F1 is summed
+ * on the host in the reference's label order. Bit-identical to the CPU fit. */
+carma_status carma_knn_train(carma_knn* h, int32_t family, const carma_feature_row* rows,
+                             const int32_t* bucket, const uint64_t* mem, uint64_t n, uint64_t seed,
+                             uint32_t k, uint64_t bucket_range, carma_holdout_report* report,
+                             double* lo_out, double* hi_out, double* points_out, int32_t* labels_out);
+/* The optional *_out buffers (nullable) receive the fitted LearnedEstimator
+ * state (estimators.hpp:108-133): lo[19], hi[19], points[train_size x 19] and
+ * labels[train_size] in training order (train_size = max(1, 7n/10)). */
+
 /* Host-buffer batch predict (the drop-in for estimate_learned over q rows).
  * family: per-row family (nullable: every row is default_family).
  * bucket_out[i] = LearnedEstimator::predict; bytes_out[i] = (bucket+1)*range.

@@ -76,6 +76,9 @@ carma_status carma_host_fit(int32_t family, uint64_t samples, uint64_t seed, uin
  * than CARMA_MAX_MIG instances or a table that is not block aligned return
  * UNSUPPORTED. */
 carma_status carma_mig_layout(const double* fractions, uint32_t n, carma_replay_config* cfg);
+/* The seeded 70/30 split of train_learned_estimator (estimators.cpp:355-361):
+ * order[n] = shuffled row indices, *train_n = max(1, 7n/10). */
+carma_status carma_host_split_order(uint64_t n, uint64_t seed, uint64_t* order, uint64_t* train_n);
 /* scalar_features for n feature rows -> n x 19 doubles. */
 carma_status carma_host_scalar_features(const carma_feature_row* rows, uint64_t n, double* out);
 

@@ -61,6 +61,11 @@ replay_config_dtype = np.dtype([
     ("log_flags", "<i4"), ("log_reserved", "<i4"),
 ], align=True)
 
+holdout_report_dtype = np.dtype([
+    ("accuracy", "<f8"), ("macro_f1", "<f8"), ("underestimate_rate", "<f8"), ("train_size", "<u8"),
+    ("holdout_size", "<u8"),
+], align=True)
+
 log_record_dtype = np.dtype([
     ("t", "<f8"), ("a", "<u8"), ("b", "<u8"), ("c", "<u8"), ("task", "<u4"), ("gpu", "<i2"), ("kind", "u1"),
     ("policy", "u1"),
@@ -156,6 +161,8 @@ SIGNATURES = {
     "carma_replay_plan_set_timeline_capacity": (c_int, [c_void_p, c_uint64]),
     "carma_replay_plan_timeline": (c_int, [c_void_p, c_uint32, P, c_uint64, POINTER(c_uint64)]),
     "carma_replay_plan_set_log_capacity": (c_int, [c_void_p, c_uint64]),
+    "carma_knn_train": (c_int, [c_void_p, c_int32, P, P, P, c_uint64, c_uint64, c_uint32, c_uint64, P, P, P, P, P]),
+    "carma_host_split_order": (c_int, [c_uint64, c_uint64, P, POINTER(c_uint64)]),
     "carma_replay_plan_log": (c_int, [c_void_p, c_uint32, P, c_uint64, POINTER(c_uint64)]),
     # carma_host.h
     "carma_host_catalog_size": (c_int, []),

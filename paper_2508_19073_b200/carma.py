@@ -306,33 +306,26 @@ class LearnedEstimator:
 
 def train_learned_estimator(family: int, samples: int, seed: int, k: int = 5, device: int = 0,
                             knn: Optional[GpuKnn] = None) -> LearnedEstimator:
-    """Fit on generate_synthetic_dataset(family, samples, seed) and score the
-    30% holdout with the GPU predict (estimators.cpp:344-436)."""
-    m = fit_knn(family, samples, seed, k)
-    knn = knn or GpuKnn(device)
-    knn.set_model(m)
+    """train_learned_estimator (estimators.cpp:344-436) on the GPU for
+    generate_synthetic_dataset(family, samples, seed): the bounds, normalised
+    points, holdout predictions and holdout counts on the device
+    (carma_knn_train); the model is installed in `knn`'s bank."""
     ds = generate_synthetic_dataset(family, samples, seed)
-    rep = HoldoutReport(train_size=len(m.labels), holdout_size=len(m.holdout_rows))
-    if len(m.holdout_rows):
-        rows = ds.rows[m.holdout_rows]
-        pred, nbytes = knn.predict(rows, default_family=family)
-        gold = ds.bucket[m.holdout_rows]
-        rep.accuracy = float(np.count_nonzero(pred == gold)) / len(gold)
-        rep.underestimate_rate = float(np.count_nonzero(nbytes < ds.mem[m.holdout_rows])) / len(gold)
-        f1 = 0.0
-        classes = 0
-        for label in sorted(set(pred.tolist()) | set(gold.tolist())):
-            tp = float(np.count_nonzero((pred == label) & (gold == label)))
-            fp = float(np.count_nonzero((pred == label) & (gold != label)))
-            fn = float(np.count_nonzero((pred != label) & (gold == label)))
-            if tp + fn == 0:
-                continue
-            prec = tp / (tp + fp) if tp + fp > 0 else 0.0
-            rec = tp / (tp + fn)
-            f1 += 2 * prec * rec / (prec + rec) if prec + rec > 0 else 0.0
-            classes += 1
-        rep.macro_f1 = f1 / classes if classes else 0.0
-    return LearnedEstimator(m, knn, rep)
+    knn = knn or GpuKnn(device)
+    order = np.zeros(samples, np.uint64)
+    tn = ctypes.c_uint64()
+    check(lib.carma_host_split_order(samples, seed, ptr(order), ctypes.byref(tn)))
+    n_train = tn.value
+    lo, hi = np.zeros(19), np.zeros(19)
+    pts, lab = np.zeros((n_train, 19)), np.zeros(n_train, np.int32)
+    rep = np.zeros(1, abi.holdout_report_dtype)
+    check(lib.carma_knn_train(knn.handle, family, ptr(ds.rows), ptr(ds.bucket), ptr(ds.mem), samples, seed, k,
+                              ds.bucket_range, ptr(rep), ptr(lo), ptr(hi), ptr(pts), ptr(lab)))
+    m = KnnModel(family, k, ds.bucket_range, lo, hi, pts, lab, order[n_train:].astype(np.int64), seed)
+    knn.models[family] = m
+    r = rep[0]
+    return LearnedEstimator(m, knn, HoldoutReport(float(r["accuracy"]), float(r["macro_f1"]), int(r["train_size"]),
+                                                  int(r["holdout_size"]), float(r["underestimate_rate"])))
 
 
 # ---------------------------------------------------------------- replay

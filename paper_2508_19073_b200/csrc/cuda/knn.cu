@@ -37,6 +37,7 @@
 #include <vector>
 
 #include "../../../include/carma_gpu.h"
+#include "../../../include/carma_host.h"
 #include "common.cuh"
 
 namespace carma_b200 {
@@ -1080,6 +1081,95 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
     }
 }
 
+// ------------------------------------------------------------------------
+// train_learned_estimator on the device (estimators.cpp:344-436).
+
+// Order-preserving 64-bit key of a double (+0 and -0 collapse) and back.
+__device__ __forceinline__ unsigned long long fkey(double x) {
+    if (x == 0.0) x = 0.0;
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+struct Bounds {
+    double lo[kDims], hi[kDims];
+};
+
+// lo/hi = min/max of scalar_features over the training rows (:363-374):
+// min and max are order-independent, so a reduction gives the sequential
+// result (up to the sign of a zero, which the features never carry).
+__global__ void fit_bounds(const carma_feature_row* __restrict__ rows, const uint64_t* __restrict__ order,
+                           uint64_t train_n, unsigned long long* __restrict__ keys /* [2][19] */) {
+    unsigned long long mn[kDims], mx[kDims];
+#pragma unroll
+    for (int d = 0; d < kDims; ++d) {
+        mn[d] = ~0ull;
+        mx[d] = 0ull;
+    }
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < train_n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double raw[kDims];
+        featurize(rows[order[i]], raw);
+#pragma unroll
+        for (int d = 0; d < kDims; ++d) {
+            const unsigned long long k = fkey(raw[d]);
+            mn[d] = k < mn[d] ? k : mn[d];
+            mx[d] = k > mx[d] ? k : mx[d];
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < kDims; ++d) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn[d], o);
+            const unsigned long long b = __shfl_xor_sync(0xffffffffu, mx[d], o);
+            mn[d] = a < mn[d] ? a : mn[d];
+            mx[d] = b > mx[d] ? b : mx[d];
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(keys + d, mn[d]);
+            atomicMax(keys + kDims + d, mx[d]);
+        }
+    }
+}
+
+// The normalised training points in training order (:380-393).
+__global__ void fit_points(const carma_feature_row* __restrict__ rows, const uint64_t* __restrict__ order,
+                           uint64_t train_n, Bounds b, double* __restrict__ points) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < train_n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double raw[kDims];
+        featurize(rows[order[i]], raw);
+#pragma unroll
+        for (int d = 0; d < kDims; ++d) points[i * kDims + d] = normalize(raw[d], b.lo[d], b.hi[d]);
+    }
+}
+
+__global__ void gather_rows(const carma_feature_row* __restrict__ rows, const uint64_t* __restrict__ idx, uint64_t n,
+                            carma_feature_row* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[i] = rows[idx[i]];
+}
+
+constexpr int kMaxLabel = 256;
+// Holdout counts (:396-419): per label tp / fp / fn, correct, underestimates.
+__global__ void holdout_counts(const int32_t* __restrict__ pred, const uint64_t* __restrict__ pred_bytes,
+                               const int32_t* __restrict__ bucket, const uint64_t* __restrict__ mem,
+                               const uint64_t* __restrict__ idx, uint64_t n, unsigned long long* __restrict__ cnt) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int p = pred[i], g = bucket[idx[i]];
+        if (p == g) {
+            atomicAdd(cnt + 3 * kMaxLabel, 1ull);
+            atomicAdd(cnt + 3 * p, 1ull);
+        } else {
+            atomicAdd(cnt + 3 * p + 1, 1ull);
+            atomicAdd(cnt + 3 * g + 2, 1ull);
+        }
+        if (pred_bytes[i] < mem[idx[i]]) atomicAdd(cnt + 3 * kMaxLabel + 1, 1ull);
+    }
+}
+
 struct HostModel {
     DeviceBuffer pts, ptsf, key18, orig, label_by_orig;
     bool f32_ok = false;
@@ -1105,6 +1195,7 @@ struct KnnHandle {
         PinnedBuffer stage_rows, stage_family;
     } scratch[2];
     DeviceBuffer evals;
+    DeviceBuffer train_rows;  // carma_knn_train: the uploaded dataset
     double act[16] = {0};
     carma_bit_schema schema{};
     int path = 0;  // 0 auto (fp32 pre-filter when every model allows it), 1 exact fp64 blocks, 2 fp32 pre-filter
@@ -1601,6 +1692,140 @@ carma_status carma_knn_predict_device(carma_knn* hh, const void* rows, int32_t f
         h->last_launches = run_pipeline(*h, h->scratch[0], rows, format, family, default_family, q,
                                         bucket_out, bytes_out, topk_d2, topk_idx,
                                         h->evals.as<unsigned long long>(), s);
+    });
+}
+
+carma_status carma_knn_train(carma_knn* hh, int32_t family, const carma_feature_row* rows, const int32_t* bucket,
+                             const uint64_t* mem, uint64_t n, uint64_t seed, uint32_t k, uint64_t bucket_range,
+                             carma_holdout_report* report, double* lo_out, double* hi_out, double* points_out,
+                             int32_t* labels_out) {
+    // The model install reuses carma_knn_set_model (it takes the handle's lock).
+    std::vector<double> lo(kDims), hi(kDims), points;
+    std::vector<int32_t> labels;
+    std::vector<uint64_t> order(n);
+    uint64_t train_n = 0;
+    carma_status st = guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        if (!h) throw InvalidArg("null handle");
+        if (family < 0 || family >= CARMA_FAMILIES) throw InvalidArg("unknown family");
+        if (n == 0) throw InvalidArg("EmptyDataset: dataset has no rows");
+        if (k < 1) throw InvalidArg("ConfigError: k must be >= 1");
+        if (!rows || !bucket || !mem) throw InvalidArg("null dataset array");
+        const carma_status so = carma_host_split_order(n, seed, order.data(), &train_n);
+        if (so != CARMA_OK) throw CarmaFailure(so, carma_last_error());
+        require_device(h->device);
+        DeviceGuard g(h->device);
+        DeviceBuffer d_rows, d_order, d_keys, d_points;
+        d_rows.ensure(n * sizeof(carma_feature_row));
+        d_order.ensure(n * 8);
+        d_keys.ensure(2 * kDims * 8);
+        d_points.ensure(train_n * kDims * 8);
+        CARMA_CUDA(cudaMemcpy(d_rows.ptr, rows, n * sizeof(carma_feature_row), cudaMemcpyHostToDevice));
+        CARMA_CUDA(cudaMemcpy(d_order.ptr, order.data(), n * 8, cudaMemcpyHostToDevice));
+        std::vector<unsigned long long> keys(2 * kDims);
+        for (int d = 0; d < kDims; ++d) {
+            keys[d] = ~0ull;
+            keys[kDims + d] = 0ull;
+        }
+        CARMA_CUDA(cudaMemcpy(d_keys.ptr, keys.data(), keys.size() * 8, cudaMemcpyHostToDevice));
+        const unsigned grid = grid_for(train_n, 256, 148u * 8u);
+        fit_bounds<<<grid, 256>>>(d_rows.as<carma_feature_row>(), d_order.as<uint64_t>(), train_n,
+                                  d_keys.as<unsigned long long>());
+        CARMA_CUDA(cudaGetLastError());
+        CARMA_CUDA(cudaMemcpy(keys.data(), d_keys.ptr, keys.size() * 8, cudaMemcpyDeviceToHost));
+        auto unkey = [](unsigned long long k2) {
+            const unsigned long long u = (k2 >> 63) ? (k2 & 0x7fffffffffffffffull) : ~k2;
+            double x;
+            std::memcpy(&x, &u, 8);
+            return x;
+        };
+        Bounds b;
+        bool varying = false;
+        for (int d = 0; d < kDims; ++d) {
+            b.lo[d] = lo[d] = unkey(keys[d]);
+            b.hi[d] = hi[d] = unkey(keys[kDims + d]);
+            varying |= hi[d] > lo[d];
+        }
+        if (!varying) throw InvalidArg("DegenerateFeature: all features have zero variance");
+        fit_points<<<grid, 256>>>(d_rows.as<carma_feature_row>(), d_order.as<uint64_t>(), train_n, b,
+                                  d_points.as<double>());
+        CARMA_CUDA(cudaGetLastError());
+        points.resize(train_n * kDims);
+        CARMA_CUDA(cudaMemcpy(points.data(), d_points.ptr, points.size() * 8, cudaMemcpyDeviceToHost));
+        labels.resize(train_n);
+        for (uint64_t i = 0; i < train_n; ++i) labels[i] = bucket[order[i]];
+        // keep the uploaded rows for the holdout below
+        h->train_rows.ensure(n * sizeof(carma_feature_row));
+        CARMA_CUDA(cudaMemcpy(h->train_rows.ptr, d_rows.ptr, n * sizeof(carma_feature_row),
+                              cudaMemcpyDeviceToDevice));
+    });
+    if (st != CARMA_OK) return st;
+    st = carma_knn_set_model(hh, family, lo.data(), hi.data(), points.data(), labels.data(), train_n, k,
+                             bucket_range);
+    if (st != CARMA_OK) return st;
+    if (lo_out) std::copy(lo.begin(), lo.end(), lo_out);
+    if (hi_out) std::copy(hi.begin(), hi.end(), hi_out);
+    if (points_out) std::copy(points.begin(), points.end(), points_out);
+    if (labels_out) std::copy(labels.begin(), labels.end(), labels_out);
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        const uint64_t nh = n - train_n;
+        carma_holdout_report rep{};
+        rep.train_size = train_n;
+        rep.holdout_size = nh;
+        if (nh > 0) {
+            std::lock_guard<std::mutex> lock(h->mu);
+            DeviceGuard g(h->device);
+            DeviceBuffer d_idx, d_hrows, d_pred, d_bytes, d_bucket, d_mem, d_cnt;
+            d_idx.ensure(nh * 8);
+            d_hrows.ensure(nh * sizeof(carma_feature_row));
+            d_pred.ensure(nh * 4);
+            d_bytes.ensure(nh * 8);
+            d_bucket.ensure(n * 4);
+            d_mem.ensure(n * 8);
+            d_cnt.ensure((3 * kMaxLabel + 2) * 8);
+            for (uint64_t i = 0; i < n; ++i)
+                if (bucket[i] < 0 || bucket[i] >= kMaxLabel) throw Unsupported("bucket labels must be in [0, 256)");
+            CARMA_CUDA(cudaMemcpy(d_idx.ptr, order.data() + train_n, nh * 8, cudaMemcpyHostToDevice));
+            CARMA_CUDA(cudaMemcpy(d_bucket.ptr, bucket, n * 4, cudaMemcpyHostToDevice));
+            CARMA_CUDA(cudaMemcpy(d_mem.ptr, mem, n * 8, cudaMemcpyHostToDevice));
+            CARMA_CUDA(cudaMemset(d_cnt.ptr, 0, (3 * kMaxLabel + 2) * 8));
+            const unsigned grid = grid_for(nh, 256, 148u * 8u);
+            gather_rows<<<grid, 256, 0, h->stream>>>(h->train_rows.as<carma_feature_row>(), d_idx.as<uint64_t>(), nh,
+                                                     d_hrows.as<carma_feature_row>());
+            // estimate_learned on the holdout rows (every row is of `family`)
+            h->timed = false;
+            h->evals.ensure(16);
+            CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 16, h->stream));
+            run_pipeline(*h, h->scratch[0], d_hrows.ptr, CARMA_ROWS_FEATURES, nullptr, family, nh,
+                         d_pred.as<int32_t>(), d_bytes.as<uint64_t>(), nullptr, nullptr,
+                         h->evals.as<unsigned long long>(), h->stream);
+            holdout_counts<<<grid, 256, 0, h->stream>>>(d_pred.as<int32_t>(), d_bytes.as<uint64_t>(),
+                                                        d_bucket.as<int32_t>(), d_mem.as<uint64_t>(),
+                                                        d_idx.as<uint64_t>(), nh, d_cnt.as<unsigned long long>());
+            CARMA_CUDA(cudaGetLastError());
+            std::vector<unsigned long long> c(3 * kMaxLabel + 2);
+            CARMA_CUDA(cudaStreamSynchronize(h->stream));
+            CARMA_CUDA(cudaMemcpy(c.data(), d_cnt.ptr, c.size() * 8, cudaMemcpyDeviceToHost));
+            const double hn = static_cast<double>(nh);
+            rep.accuracy = static_cast<double>(c[3 * kMaxLabel]) / hn;
+            rep.underestimate_rate = static_cast<double>(c[3 * kMaxLabel + 1]) / hn;
+            // macro F1 over the labels of the confusion map in ascending order (:420-433)
+            double f1_sum = 0.0;
+            uint64_t classes = 0;
+            for (int l = 0; l < kMaxLabel; ++l) {
+                const double tp = static_cast<double>(c[3 * l]), fp = static_cast<double>(c[3 * l + 1]),
+                             fn = static_cast<double>(c[3 * l + 2]);
+                if (tp + fp + fn == 0) continue;  // not in the map
+                if (tp + fn == 0) continue;       // class never appears in gold labels
+                const double prec = tp + fp > 0 ? tp / (tp + fp) : 0.0;
+                const double rec = tp / (tp + fn);
+                f1_sum += prec + rec > 0 ? 2 * prec * rec / (prec + rec) : 0.0;
+                ++classes;
+            }
+            rep.macro_f1 = classes ? f1_sum / static_cast<double>(classes) : 0.0;
+        }
+        if (report) *report = rep;
     });
 }
 

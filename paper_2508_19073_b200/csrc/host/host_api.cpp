@@ -249,6 +249,21 @@ carma_status carma_host_fit(int32_t family, uint64_t samples, uint64_t seed, uin
     });
 }
 
+// train_learned_estimator's seeded 70/30 split (estimators.cpp:355-361): the
+// shuffled row order (a sequential mt19937_64 stream, so it stays on the
+// host) and the training-set size.
+carma_status carma_host_split_order(uint64_t n, uint64_t seed, uint64_t* order, uint64_t* train_n) {
+    return guarded([&] {
+        if (n == 0) throw InvalidArg("EmptyDataset: dataset has no rows");
+        std::vector<std::size_t> o(n);
+        for (std::size_t i = 0; i < o.size(); ++i) o[i] = i;
+        Rng rng(seed ^ 0x9e3779b97f4a7c15ull);
+        rng.shuffle(o);
+        std::copy(o.begin(), o.end(), order);
+        *train_n = std::max<uint64_t>(1, n * 7 / 10);
+    });
+}
+
 // GpuDevice::GpuDevice's MIG branch (gpu.cpp:29-51): instance capacities are
 // round_up(fraction * capacity) clipped to what is left, the last instance
 // absorbing the remainder when the fractions sum to 1.

@@ -252,3 +252,22 @@ def test_train_learned_estimator_holdout_matches_reference(gpu, family):
     got = np.array([est.holdout.accuracy, est.holdout.macro_f1, est.holdout.underestimate_rate])
     assert got.tobytes() == want.tobytes(), (got, want)
     assert est.holdout.train_size == 2800 and est.holdout.holdout_size == 1200
+
+
+@pytest.mark.parametrize("family,samples,seed", [(0, 4000, 11), (1, 4000, 112), (2, 4000, 213), (1, 777, 5),
+                                                 (2, 5000, 3)])
+def test_train_on_device_equals_host_fit(gpu, family, samples, seed):
+    """carma_knn_train (bounds, normalised points and holdout on the GPU) fits
+    exactly the model of the host restatement of estimators.cpp:344-395."""
+    est = cb.train_learned_estimator(family, samples, seed, 5, device=gpu)
+    m = cb.fit_knn(family, samples, seed, 5)
+    assert np.array_equal(est.model.lo.view(np.uint64), m.lo.view(np.uint64))
+    assert np.array_equal(est.model.hi.view(np.uint64), m.hi.view(np.uint64))
+    assert np.array_equal(est.model.points.view(np.uint64), m.points.view(np.uint64))
+    assert np.array_equal(est.model.labels, m.labels)
+    assert np.array_equal(est.model.holdout_rows, m.holdout_rows)
+    assert est.holdout.train_size == len(m.labels) and est.holdout.holdout_size == len(m.holdout_rows)
+    ds = cb.generate_synthetic_dataset(family, 3000, seed + 1)
+    k2 = cb.GpuKnn(gpu)
+    k2.set_model(m)
+    assert np.array_equal(est.predict(ds.rows), k2.predict(ds.rows, default_family=family)[0])
