@@ -1430,19 +1430,22 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
             cudaStream_t s = h->pipe[c & 1];
             cnt = std::min<uint64_t>(chunk_rows(c, q - beg), q - beg);
             const char* src = static_cast<const char*>(rows) + beg * row_bytes;
-            sc.rows.ensure(chunk * row_bytes + tail_bytes);
-            sc.bucket.ensure(chunk * 4);
-            sc.bytes.ensure(chunk * 8);
-            if (family) sc.family.ensure(chunk);
+            // buffers for the largest chunk this call uses (not the steady
+            // size: pinned staging for 2^21 rows costs ~0.1 s to allocate)
+            const uint64_t cap_rows = std::min<uint64_t>(chunk, q);
+            sc.rows.ensure(cap_rows * row_bytes + tail_bytes);
+            sc.bucket.ensure(cap_rows * 4);
+            sc.bytes.ensure(cap_rows * 8);
+            if (family) sc.family.ensure(cap_rows);
             if (!rows_pinned || !fam_pinned) {
                 // Stage through pinned memory; wait until this buffer's previous
                 // chunk has been consumed.
                 CARMA_CUDA(cudaStreamSynchronize(s));
-                sc.stage_rows.ensure(chunk * row_bytes + tail_bytes);
+                sc.stage_rows.ensure(cap_rows * row_bytes + tail_bytes);
                 std::memcpy(sc.stage_rows.ptr, src, cnt * row_bytes + tail_bytes);
                 src = sc.stage_rows.as<char>();
                 if (family) {
-                    sc.stage_family.ensure(chunk);
+                    sc.stage_family.ensure(cap_rows);
                     std::memcpy(sc.stage_family.ptr, family + beg, cnt);
                 }
             }
