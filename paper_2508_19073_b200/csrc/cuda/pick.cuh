@@ -44,6 +44,21 @@ __device__ __forceinline__ uint64_t policy_key(int policy, const PickInput& in) 
     return policy == CARMA_POLICY_LUG ? ~k : k;
 }
 
+// (ka, ia) better than (kb, ib): key descending, id ascending — the borrow of
+// the 96-bit subtraction (kb : ~ib) - (ka : ~ia), one carry chain.
+__device__ __forceinline__ bool key_better(uint64_t ka, int ia, uint64_t kb, int ib) {
+    uint32_t r;
+    asm("{\n\t.reg .u32 t;\n\t"
+        "sub.cc.u32 t, %2, %1;\n\t"
+        "subc.cc.u32 t, %4, %3;\n\t"
+        "subc.cc.u32 t, %6, %5;\n\t"
+        "subc.u32 %0, 0, 0;\n\t}"
+        : "=r"(r)
+        : "r"(~static_cast<uint32_t>(ia)), "r"(~static_cast<uint32_t>(ib)), "r"(static_cast<uint32_t>(ka)),
+          "r"(static_cast<uint32_t>(kb)), "r"(static_cast<uint32_t>(ka >> 32)), "r"(static_cast<uint32_t>(kb >> 32)));
+    return r != 0;
+}
+
 // Arg-best of (key desc, id asc) over the lane's candidates, then across the
 // group (stable_sort by key with ties to the lowest id). -1 when none.
 template <int GPL>
@@ -55,7 +70,7 @@ __device__ __forceinline__ int arg_best(int policy, const PickInput (&in)[GPL], 
     for (int j = 0; j < GPL; ++j) {
         const uint64_t k = policy_key(policy, in[j]);
         const int id = static_cast<int>(lane_in_group + j * width);
-        if (cand[j] && (k > bk || (k == bk && id < bid))) {
+        if (cand[j] && key_better(k, id, bk, bid)) {
             bk = k;
             bid = id;
         }
@@ -64,7 +79,7 @@ __device__ __forceinline__ int arg_best(int policy, const PickInput (&in)[GPL], 
     for (unsigned off = 1; off < width; off <<= 1) {
         const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off, width);
         const int oid = __shfl_xor_sync(0xffffffffu, bid, off, width);
-        if (ok > bk || (ok == bk && oid < bid)) {
+        if (key_better(ok, oid, bk, bid)) {
             bk = ok;
             bid = oid;
         }

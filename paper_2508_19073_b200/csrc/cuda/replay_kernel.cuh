@@ -52,6 +52,9 @@ namespace replay {
 // Shared-memory tiers: 64 registers, 8 CTAs x 4 warps resident (throughput
 // of many jobs). The large tier (one long trace per warp, latency bound)
 // and the global tier take all the registers they want.
+#ifndef REPLAY_KLATER_CHAIN
+#define REPLAY_KLATER_CHAIN 1
+#endif
 #ifndef REPLAY_MIN_CTAS
 #define REPLAY_MIN_CTAS 8
 #endif
@@ -184,8 +187,23 @@ __device__ __forceinline__ double tval(uint64_t k) {
     const uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
     return __longlong_as_double(static_cast<long long>(u));
 }
+// (ka, sa) > (kb, sb) lexicographically, as the borrow of the 96-bit
+// subtraction (kb:sb) - (ka:sa): one carry chain instead of compare-and-select.
 __device__ __forceinline__ bool klater(uint64_t ka, uint32_t sa, uint64_t kb, uint32_t sb) {
+#if REPLAY_KLATER_CHAIN
+    uint32_t r;
+    asm("{\n\t.reg .u32 t;\n\t"
+        "sub.cc.u32 t, %2, %1;\n\t"
+        "subc.cc.u32 t, %4, %3;\n\t"
+        "subc.cc.u32 t, %6, %5;\n\t"
+        "subc.u32 %0, 0, 0;\n\t}"
+        : "=r"(r)
+        : "r"(sa), "r"(sb), "r"(static_cast<uint32_t>(ka)), "r"(static_cast<uint32_t>(kb)),
+          "r"(static_cast<uint32_t>(ka >> 32)), "r"(static_cast<uint32_t>(kb >> 32)));
+    return r != 0;
+#else
     return ka != kb ? ka > kb : sa > sb;
+#endif
 }
 
 template <class L>
