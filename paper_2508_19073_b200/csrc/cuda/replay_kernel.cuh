@@ -123,8 +123,8 @@ struct Layout {
     static constexpr size_t last_v = last_t + 8ull * G;
     static constexpr size_t ring_t = al8(last_v + 8ull * G);           // f64 [G][RG]
     static constexpr size_t ring_v = ring_t + 8ull * G * RG;
-    static constexpr size_t ht = ring_v + 8ull * G * RG;               // u64 time keys [H]
-    static constexpr size_t s_rem = ht + 8ull * H;                     // f64 [S] x 5
+    static constexpr size_t ht = al8(ring_v + 8ull * G * RG);          // HeapEnt [H] (16 B each)
+    static constexpr size_t s_rem = ht + 16ull * H;                    // f64 [S] x 5
     static constexpr size_t s_rate = s_rem + 8ull * S;
     static constexpr size_t s_last = s_rate + 8ull * S;
     static constexpr size_t s_exec = s_last + 8ull * S;
@@ -138,9 +138,7 @@ struct Layout {
     static constexpr size_t peak = rcnt + 4ull * G;
     static constexpr size_t has_step = peak + 4ull * G;
     static constexpr size_t imask = has_step + 4ull * G;               // MIG: occupied instances
-    static constexpr size_t hs = imask + 4ull * G * MI;                // u32 [H] x 2
-    static constexpr size_t hinfo = hs + 4ull * H;
-    static constexpr size_t s_task = hinfo + 4ull * H;                 // u32 [S] x 7
+    static constexpr size_t s_task = imask + 4ull * G * MI;            // u32 [S] x 7
     static constexpr size_t s_rank = s_task + 4ull * S;
     static constexpr size_t s_seq = s_rank + 4ull * S;
     static constexpr size_t s_gp = s_seq + 4ull * S;
@@ -206,72 +204,65 @@ __device__ __forceinline__ bool klater(uint64_t ka, uint32_t sa, uint64_t kb, ui
 #endif
 }
 
+// One heap entry: order key, seq and payload in 16 bytes, so a child or
+// parent moves with one 16-byte shared-memory load / store.
+struct __align__(16) HeapEnt {
+    uint64_t key;
+    uint32_t seq;
+    uint32_t info;
+};
+
 template <class L>
 __device__ __forceinline__ uint32_t heap_push(char* b, Sc& c, double t, uint32_t info) {
     if (c.hsize >= static_cast<uint32_t>(L::H)) {
         c.status = kStatusRetry;
         return kNone;
     }
-    uint64_t* hk = RP_U64(ht);
-    uint32_t* hs = RP_U32(hs);
-    uint32_t* hi = RP_U32(hinfo);
-    const uint64_t key = tkey(t);
-    const uint32_t seq = c.seq_next++;
+    HeapEnt* h = reinterpret_cast<HeapEnt*>(b + L::ht);
+    HeapEnt e;
+    e.key = tkey(t);
+    e.seq = c.seq_next++;
+    e.info = info;
     uint32_t i = c.hsize++;
     while (i > 0) {
         const uint32_t p = (i - 1) >> 2;
-        const uint64_t pk = hk[p];
-        const uint32_t ps = hs[p];
-        if (!klater(pk, ps, key, seq)) break;
-        hk[i] = pk;
-        hs[i] = ps;
-        hi[i] = hi[p];
+        const HeapEnt pe = h[p];
+        if (!klater(pe.key, pe.seq, e.key, e.seq)) break;
+        h[i] = pe;
         i = p;
     }
-    hk[i] = key;
-    hs[i] = seq;
-    hi[i] = info;
-    return seq;
+    h[i] = e;
+    return e.seq;
 }
 
 template <class L>
 __device__ __forceinline__ void heap_pop(char* b, Sc& c) {
-    uint64_t* hk = RP_U64(ht);
-    uint32_t* hs = RP_U32(hs);
-    uint32_t* hi = RP_U32(hinfo);
+    HeapEnt* h = reinterpret_cast<HeapEnt*>(b + L::ht);
     const uint32_t n = --c.hsize;
     if (n == 0) return;
-    const uint64_t k = hk[n];
-    const uint32_t sq = hs[n], inf = hi[n];
+    const HeapEnt last = h[n];
     uint32_t i = 0;
     for (;;) {
         const uint32_t c0 = 4 * i + 1;
         if (c0 >= n) break;
         uint32_t m = c0;
-        uint64_t mk = hk[c0];
-        uint32_t ms = hs[c0];
+        HeapEnt me = h[c0];
 #pragma unroll
         for (uint32_t d = 1; d < 4; ++d) {
             const uint32_t cc = c0 + d;
             if (cc < n) {
-                const uint64_t ck = hk[cc];
-                const uint32_t cs = hs[cc];
-                if (klater(mk, ms, ck, cs)) {
+                const HeapEnt ce = h[cc];
+                if (klater(me.key, me.seq, ce.key, ce.seq)) {
                     m = cc;
-                    mk = ck;
-                    ms = cs;
+                    me = ce;
                 }
             }
         }
-        if (!klater(k, sq, mk, ms)) break;
-        hk[i] = mk;
-        hs[i] = ms;
-        hi[i] = hi[m];
+        if (!klater(last.key, last.seq, me.key, me.seq)) break;
+        h[i] = me;
         i = m;
     }
-    hk[i] = k;
-    hs[i] = sq;
-    hi[i] = inf;
+    h[i] = last;
 }
 
 // ------------------------------------------------------------ allocator
@@ -1130,21 +1121,24 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             if (tick_live) {
                 const uint64_t tk = tkey(tick_t);
                 tick = !(have_arr && klater(tk, tick_seq, tkey(at), c.arrived)) &&
-                       !(have_heap && klater(tk, tick_seq, RP_U64(ht)[0], RP_U32(hs)[0]));
+                       !(have_heap && klater(tk, tick_seq, reinterpret_cast<const HeapEnt*>(b + L::ht)->key,
+                                             reinterpret_cast<const HeapEnt*>(b + L::ht)->seq));
             }
         }
         if (tick) {
             t = tick_t;
             kind = kTick;
             payload = 0;
-        } else if (have_arr && (!have_heap || !klater(tkey(at), c.arrived, RP_U64(ht)[0], RP_U32(hs)[0]))) {
+        } else if (have_arr && (!have_heap || !klater(tkey(at), c.arrived, reinterpret_cast<const HeapEnt*>(b + L::ht)->key,
+                                                      reinterpret_cast<const HeapEnt*>(b + L::ht)->seq))) {
             t = at;
             kind = 0;
             payload = c.arrived;
         } else {
-            t = tval(RP_U64(ht)[0]);
-            seq = RP_U32(hs)[0];
-            const uint32_t info = RP_U32(hinfo)[0];
+            const HeapEnt top = *reinterpret_cast<const HeapEnt*>(b + L::ht);
+            t = tval(top.key);
+            seq = top.seq;
+            const uint32_t info = top.info;
             kind = info >> 30;
             payload = info & 0x3fffffffu;
             heap_pop<L>(b, c);
