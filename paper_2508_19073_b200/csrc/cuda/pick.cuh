@@ -116,7 +116,7 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
     const bool ok = static_cast<uint32_t>(__popcll(static_cast<long long>(mask))) >= want;
     const bool sorted = policy == CARMA_POLICY_MAGM || policy == CARMA_POLICY_LUG || policy == CARMA_POLICY_MUG;
     // MAGM / LUG / MUG: stable sort by key then id == repeated arg-best.
-    int best[2] = {-1, -1};
+    int best0 = -1, best1 = -1;  // scalars: a dynamically indexed array would live in local memory
     const int rounds = __any_sync(0xffffffffu, ok && sorted && want > 1) ? 2
                        : (__any_sync(0xffffffffu, ok && sorted) ? 1 : 0);
     bool cand[GPL];
@@ -125,15 +125,16 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
 #pragma unroll 1
     for (int r = 0; r < rounds; ++r) {
         const int g = arg_best<GPL>(policy, in, cand, lane_in_group, width);
-        best[r] = g;
+        if (r == 0) best0 = g;
+        else best1 = g;
 #pragma unroll
         for (int j = 0; j < GPL; ++j)
             if (static_cast<int>(lane_in_group + j * width) == g) cand[j] = false;
     }
     if (!ok) return 0;
     if (sorted) {
-        out[0] = best[0];
-        if (want > 1) out[1] = best[1];
+        out[0] = best0;
+        if (want > 1) out[1] = best1;
         return static_cast<int>(want);
     }
     // want <= 2: out[] is written with constant indices (a dynamic index

@@ -148,7 +148,8 @@ struct Layout {
     static constexpr size_t free_stack = s_inst + 4ull * S * MI;       // u32 [S]
     static constexpr size_t rq = free_stack + 4ull * S;                // u32 [RQ]
     static constexpr size_t res = rq + 4ull * RQ;                      // u16 [G][RC]
-    static constexpr size_t bytes = al8(res + 2ull * G * RC);
+    static constexpr size_t ptrs = al8(res + 2ull * G * RC);          // tasks, out, est, nblk (warp-uniform)
+    static constexpr size_t bytes = ptrs + 32;
 };
 
 #define RP_F64(f) reinterpret_cast<double*>(b + L::f)
@@ -1059,15 +1060,29 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
     // reference; the loop works on a copy whose address never escapes, so
     // it stays in registers instead of local memory.
     Sc c;
-    const carma_task* tasks;
-    carma_task_result* out;
-    int nblk;
     {
         Sc c0;
-        init_job<L>(b, p, j, lane, c0, tasks, out, nblk);
+        const carma_task* tasks0;
+        carma_task_result* out0;
+        int nblk0;
+        init_job<L>(b, p, j, lane, c0, tasks0, out0, nblk0);
         c = c0;
+        // The warp-uniform base pointers live in shared memory, not in
+        // registers: under the 64-register cap they were spilled to local
+        // memory, which thrashed L1 (every reload a 256-B per-lane access).
+        if (lane == 0) {
+            uint64_t* q = RP_U64(ptrs);
+            q[0] = reinterpret_cast<uint64_t>(tasks0);
+            q[1] = reinterpret_cast<uint64_t>(out0);
+            q[2] = p.est_override ? reinterpret_cast<uint64_t>(p.est_override + p.trace_off[p.jobs[j].trace]) : 0ull;
+            q[3] = static_cast<uint64_t>(nblk0);
+        }
+        __syncwarp();
     }
-    const uint64_t* est = p.est_override ? p.est_override + p.trace_off[p.jobs[j].trace] : nullptr;
+#define tasks (reinterpret_cast<const carma_task* const*>(b + L::ptrs)[0])
+#define out (reinterpret_cast<carma_task_result* const*>(b + L::ptrs)[1])
+#define est (reinterpret_cast<const uint64_t* const*>(b + L::ptrs)[2])
+#define nblk (static_cast<int>(reinterpret_cast<const uint64_t*>(b + L::ptrs)[3]))
     const uint64_t max_events = 1000ull * c.T + 1000000ull;
     uint64_t events = 0;
     // timeline (L::TL only; dead code otherwise): the pending sample tick —
@@ -1306,6 +1321,10 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
     __syncwarp();
     const Sc c1 = c;
     finish_job<L>(b, p, j, lane, c1, tasks, out);
+#undef tasks
+#undef out
+#undef est
+#undef nblk
 }
 
 template <class L, bool SMEM>
