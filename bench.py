@@ -211,6 +211,129 @@ def knn_config(n: int) -> dict:
             "l2": "inputs 2.28 GB per GPU > 126 MB L2 (no flush needed)"}
 
 
+def nn_tile_flops(m) -> tuple:
+    """(executed tensor-pipe flops per 128-row tile, useful dense flops per row)
+    of a GPUMemNet ensemble on the kernel's layout (csrc/cuda/gpumemnet.cu):
+    3 bf16 activation parts x (layer 0: K=32, N=64; L-1 hidden: K=64, N=64;
+    head passes: K=64, N=pass_n), 2*M*N*K flops per MMA (M = 128)."""
+    L = max(m.depth)
+    cp = (m.classes + 7) // 8 * 8
+    mpp = min(m.members, 128 // cp)
+    passes = [min(mpp, m.members - p * mpp) for p in range((m.members + mpp - 1) // mpp)]
+    head_n = sum((k * cp + 15) // 16 * 16 for k in passes)
+    executed = 3 * 2 * 128 * (64 * 32 + (L - 1) * 64 * 64 + head_n * 64)
+    useful = 0
+    for d, w in zip(m.depth, m.width):
+        fan = 19
+        for x in w:
+            useful += 2 * fan * x
+            fan = x
+        useful += 2 * fan * m.classes
+    return executed, useful
+
+
+def neural_bench(abi, cb, dev, stream, args, d, words, schema, rows, fam):
+    """The paper's neural GPUMemNet (MLP ensemble, 8 members)
+    over the same c2 batch as the k-NN headline: 16,777,216 bit-packed CNN +
+    Transformer rows, routed per family, on the tcgen05 kernel."""
+    import ctypes
+
+    import torch
+
+    from paper_2508_19073_b200 import gpumemnet as gm
+    Q = len(rows)
+    models = gm.load_default_models()
+    net = gm.GpuMemNet(dev)
+    for f in (1, 2):
+        net.set_model(models[f])
+    net.set_bit_schema(schema)
+    d_rows = torch.from_numpy(words.view(np.uint8)).to("cuda")
+    d_b = torch.empty(Q, dtype=torch.int32, device="cuda")
+    d_by = torch.empty(Q, dtype=torch.int64, device="cuda")
+
+    def step():
+        net.predict_device(d_rows, abi.ROWS_BITPACKED, Q, d_b, d_by, stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    d.barrier()
+    kernel_ms, call_ms = [], []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+        t = net.last_timing()
+        kernel_ms.append(t["kernel_ms"])
+        call_ms.append(t["call_ms"])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = d.max(e0.elapsed_time(e1) / args.steps)
+    t = net.last_timing()
+    b_dev = d_b.cpu().numpy()
+    # e2e: pinned host bit-packed rows -> carma_nn_predict_bitpacked -> pinned host outputs
+    h_rows = torch.from_numpy(words.view(np.uint8)).pin_memory().numpy().view(np.uint32)
+    h_b = torch.empty(Q, dtype=torch.int32).pin_memory().numpy()
+    h_by = torch.empty(Q, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+
+    def e2e_step():
+        abi.check(abi.lib.carma_nn_predict_bitpacked(net.handle, h_rows.ctypes.data, schema.ctypes.data, Q,
+                                                     h_b.ctypes.data, h_by.ctypes.data))
+
+    e2e_step()
+    d.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_s = d.max((time.perf_counter() - t0) / args.steps)
+    assert np.array_equal(h_b, b_dev), "host-API and device-resident neural predictions differ"
+    # parity spot check against the oracle on a sample of the batch
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import gpumemnet_oracle
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(Q, 4096, replace=False))
+    agree = 0
+    raw = cb.scalar_features(rows[idx])
+    for f in (1, 2):
+        sel = fam[idx] == f
+        _, op, ob, _ = gpumemnet_oracle.forward(models[f].spec()[0], models[f].params, raw[sel])
+        srt = np.sort(op, axis=1)
+        sure = srt[:, -1] - srt[:, -2] > 1e-3
+        assert np.array_equal(b_dev[idx][sel][sure], ob[sure]), "neural bins differ from the oracle"
+        agree += int(sure.sum())
+    k_avg = statistics.mean(kernel_ms)
+    rows_f = {f: int((fam == f).sum()) for f in (1, 2)}
+    executed = sum((rows_f[f] + 127) // 128 * nn_tile_flops(models[f])[0] for f in (1, 2))
+    useful = sum(rows_f[f] * nn_tile_flops(models[f])[1] for f in (1, 2))
+    peak = peaks().get("bf16_tflops", 2250.0)
+    ach = executed / (k_avg * 1e-3) / 1e12
+    wpr = int(schema["words_per_row"][0])
+    hbm_bytes = Q * (4 * wpr + 12)
+    net.close()
+    return {
+        "metric": "GPUMemNet estimates/sec (neural MLP ensemble, 8 members, CNN+Transformer)",
+        "unit": "estimates/s", "value": d.n * Q / (ms * 1e-3), "ms_per_step": ms, "dtype": "bf16 x3 -> fp32",
+        "config": {"workload": f"c2 batch ({Q} bit-packed rows, {4 * wpr} B each) through the neural GPUMemNet "
+                               "ensembles of paper_2508_19073_b200/weights (scripts/train_gpumemnet.py)",
+                   "l2": "inputs larger than L2 (no flush needed)"},
+        "e2e": {"value": d.n * Q / e2e_s, "unit": "estimates/s", "h2d_bytes_per_step": int(h_rows.nbytes),
+                "d2h_bytes_per_step": int(h_b.nbytes + h_by.nbytes),
+                "api": "carma_nn_predict_bitpacked (pinned host buffers)"},
+        "gpu_launches": int(t["launches"]) * args.steps,
+        "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                     "traffic": profile_traffic("nn_ensemble"), "kernel": "nn_ensemble", "kernel_ms": k_avg,
+                     "kernel_share_of_step": k_avg / statistics.mean(call_ms),
+                     "work": f"{t['mmas']} tcgen05.mma (M=128, K=16) per step = {executed / 1e9:.1f} GFLOP executed "
+                             f"(block-diagonal, 3 bf16 activation parts); {useful / 1e9:.1f} GFLOP of dense "
+                             "ensemble math",
+                     "hbm_gbs": hbm_bytes / (k_avg * 1e-3) / 1e9, "hbm_peak_gbs": peaks().get("hbm_gbs"),
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
+        "oracle_agreement_rows": agree,
+        "holdout_accuracy": {gm.FAMILY_NAMES[f]: models[f].holdout_accuracy for f in (1, 2)},
+    }
+
+
+
 # ------------------------------------------------------------ reference arm
 def ref_lib():
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -582,6 +705,11 @@ def run_carma(args, d: Dist):
     achieved = f32_flops / (search_avg * 1e-3)
     traffic = profile_traffic("knn_search_f32")
 
+    # ---------------- stage 1, neural GPUMemNet (tcgen05 MLP ensemble)
+    neural = None
+    if not args.skip_neural:
+        neural = neural_bench(abi, cb, dev, stream, args, d, words, schema, rows, fam)
+
     # ---------------- stage 2: policy sweep
     replay = None
     if not args.skip_replay:
@@ -741,6 +869,7 @@ def run_carma(args, d: Dist):
         "cpu_baseline": cpu,
         "clocks": clocks,
         "replay": replay,
+        "neural": neural,
         "scoring": scoring,
         "fused": fused,
         "small_configs": small,
@@ -760,6 +889,7 @@ def main():
     ap.add_argument("--skip-fused", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
     ap.add_argument("--skip-scoring", action="store_true")
+    ap.add_argument("--skip-neural", action="store_true")
     ap.add_argument("--fused-tasks", type=int, default=1_000_000)
     ap.add_argument("--fused-cpu-tasks", type=int, default=100_000)
     args = ap.parse_args()

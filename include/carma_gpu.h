@@ -209,6 +209,74 @@ carma_status carma_knn_set_path(carma_knn* h, int32_t path);
  * the knn_search kernel alone and the whole 4-kernel pipeline (ms). */
 carma_status carma_knn_last_timing(carma_knn* h, double* search_ms, double* pipeline_ms);
 
+/* ------------------------------------------ stage 1, neural GPUMemNet */
+/* The paper's GPUMemNet MLP ensemble (fig. "MLP
+ * Ensemble"): E members, each 1..8 hidden ReLU layers of <= 8 neurons
+ * (batch norm folded into the linear layers), a linear head over C memory
+ * bins, a softmax per member, the probabilities averaged over the members;
+ * the predicted bin is the argmax (ties to the larger bin, as the k-NN vote,
+ * estimators.cpp:463-474) and bytes = (bin + 1) * bucket_range
+ * (estimate_learned, estimators.cpp:540-551). The reference artifact ships
+ * the k-NN instead: this estimator is the north
+ * star's neural one, an extra EstimatorKind next to carma_knn_*. It plugs
+ * into Manager::make_estimate (manager.cpp:80-107) through the same
+ * per-family bank and the same FamilyMismatch convention.
+ *
+ * Input transform per feature d of scalar_features (estimators.cpp:317-342),
+ * computed in fp64 and rounded to fp32:  t_d = log1p(max(raw_d, 0)) if bit d
+ * of log_mask is set, else raw_d;  z_d = (t_d - shift_d) * scale_d  (fp32).
+ * Weights are bf16 values (rounded to nearest-even on install); biases,
+ * activations, logits and probabilities are fp32. */
+#define CARMA_NN_MAX_MEMBERS 8
+#define CARMA_NN_MAX_DEPTH 8
+#define CARMA_NN_MAX_WIDTH 8
+#define CARMA_NN_MAX_CLASSES 48
+typedef struct carma_nn_spec {
+    uint32_t members;      /* E, 1..8 */
+    uint32_t classes;      /* C, 2..48 */
+    uint64_t bucket_range; /* bytes per bin */
+    uint32_t depth[CARMA_NN_MAX_MEMBERS];                      /* hidden layers, 1..8 */
+    uint32_t width[CARMA_NN_MAX_MEMBERS][CARMA_NN_MAX_DEPTH]; /* hidden widths, 1..8 */
+    uint32_t log_mask;
+    uint32_t reserved;
+    float shift[CARMA_FEATURE_DIMS];
+    float scale[CARMA_FEATURE_DIMS];
+} carma_nn_spec;
+/* Parameters (fp32, n_params values): member by member, layer by layer,
+ * W_l [width_l x in_l] row-major then b_l [width_l], with in_0 = 19 and
+ * in_l = width_{l-1}; then the head W [C x width_last] and b [C]. */
+uint64_t carma_nn_param_count(const carma_nn_spec* spec);
+
+typedef struct carma_nn carma_nn;
+carma_status carma_nn_create(int device, carma_nn** out);
+carma_status carma_nn_destroy(carma_nn* h);
+carma_status carma_nn_set_model(carma_nn* h, int32_t family, const carma_nn_spec* spec,
+                                const float* params, uint64_t n_params);
+carma_status carma_nn_set_act_table(carma_nn* h, const double* act_table);
+carma_status carma_nn_set_bit_schema(carma_nn* h, const carma_bit_schema* schema);
+/* Device-resident predict (formats as carma_knn_predict_device). probs
+ * (nullable, q x CARMA_NN_MAX_CLASSES fp32) receives the ensemble's mean
+ * probabilities, logits (nullable, q x CARMA_NN_MAX_MEMBERS x
+ * CARMA_NN_MAX_CLASSES fp32) each member's logits; entries past the row's
+ * model E / C are left untouched. Rows whose family has no model get bin -1
+ * and bytes UINT64_MAX. */
+carma_status carma_nn_predict_device(carma_nn* h, const void* rows, int32_t format,
+                                     const int8_t* family, int32_t default_family, uint64_t q,
+                                     int32_t* bucket_out, uint64_t* bytes_out, float* probs,
+                                     float* logits, void* stream);
+/* Host-buffer predicts, chunked H2D / compute / D2H on the handle's streams. */
+carma_status carma_nn_predict(carma_nn* h, const carma_feature_row* rows, const int8_t* family,
+                              int32_t default_family, uint64_t q, int32_t* bucket_out,
+                              uint64_t* bytes_out);
+carma_status carma_nn_predict_bitpacked(carma_nn* h, const uint32_t* words,
+                                        const carma_bit_schema* schema, uint64_t q,
+                                        int32_t* bucket_out, uint64_t* bytes_out);
+/* CUDA-event time of the last carma_nn_predict_device (ms): the ensemble
+ * kernels alone and the whole call (family partition included), plus the
+ * number of kernel launches and of tcgen05 MMA instructions issued. */
+carma_status carma_nn_last_timing(carma_nn* h, double* kernel_ms, double* call_ms,
+                                  uint64_t* launches, uint64_t* mmas);
+
 /* ------------------------------------------------------------ stage 2 */
 
 #define CARMA_POLICY_EXCLUSIVE 0 /* manager.hpp:15 */

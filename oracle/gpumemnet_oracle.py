@@ -1,0 +1,104 @@
+"""CPU oracle of the neural GPUMemNet ensemble — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+import this module, and only as the checker; the product path
+(libcarma_b200.so, carma_nn_*) never calls it.
+
+What it restates. The paper's GPUMemNet MLP ensemble (PAPER.md:436-442,
+fig. "MLP Ensemble"): each member is a stack of ReLU layers with batch norm
+(folded into the linear layers at export), a linear head over the memory
+bins, a softmax; the ensemble averages the members' probabilities and the
+predicted bin is the argmax (ties to the larger bin, the vote rule of
+estimators.cpp:463-474); bytes = (bin + 1) * range (estimate_learned,
+estimators.cpp:540-551). Features are scalar_features
+(estimators.cpp:317-342) under the input transform documented in
+include/carma_gpu.h.
+
+Parity status: the reference artifact has NO neural estimator (SURVEY.md F1,
+§8(f)4), so this oracle cannot be pinned to reference outputs. It is pinned
+instead to the PyTorch model that defines the weights: tests/golden/
+gpumemnet.npz holds the torch fp64 forward pass (eval mode, batch norm
+folded, bf16-rounded weights) of scripts/train_gpumemnet.py on fixed rows,
+and tests/test_gpumemnet.py checks this oracle against it.
+
+Arithmetic: the input transform exactly as the kernel (log1p in fp64,
+rounded to fp32; (t - shift) * scale in fp32); layers, softmax and the mean
+in fp64.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+DIMS = 19
+
+
+def unpack_params(spec, params: np.ndarray):
+    """[(layers[(W, b)], (W_head, b_head))] per member from the flat layout of
+    carma_nn_set_model (carma_gpu.h)."""
+    members = []
+    at = 0
+    for e in range(int(spec["members"])):
+        layers = []
+        fan_in = DIMS
+        for l in range(int(spec["depth"][e])):
+            w = int(spec["width"][e][l])
+            W = params[at: at + w * fan_in].reshape(w, fan_in)
+            at += w * fan_in
+            b = params[at: at + w]
+            at += w
+            layers.append((W, b))
+            fan_in = w
+        c = int(spec["classes"])
+        W = params[at: at + c * fan_in].reshape(c, fan_in)
+        at += c * fan_in
+        b = params[at: at + c]
+        at += c
+        members.append((layers, (W, b)))
+    if at != len(params):
+        raise ValueError(f"parameter count {len(params)} != spec's {at}")
+    return members
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round fp32 values to the nearest bf16 (ties to even), as fp32."""
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16 << 16
+    return u.astype(np.uint32).view(np.float32)
+
+
+def transform(spec, raw: np.ndarray) -> np.ndarray:
+    """z (Q x 19, fp32): t = log1p(max(raw, 0)) on log_mask dims (fp64 -> fp32),
+    z = (t - shift) * scale in fp32."""
+    raw = np.asarray(raw, np.float64)
+    mask = int(spec["log_mask"])
+    t = raw.copy()
+    for d in range(DIMS):
+        if (mask >> d) & 1:
+            t[:, d] = np.log1p(np.maximum(raw[:, d], 0.0))
+    t32 = t.astype(np.float32)
+    shift = np.asarray(spec["shift"], np.float32)
+    scale = np.asarray(spec["scale"], np.float32)
+    return ((t32 - shift).astype(np.float32) * scale).astype(np.float32)
+
+
+def forward(spec, params: np.ndarray, raw: np.ndarray):
+    """(logits Q x E x C, probs Q x C, bucket Q int32, bytes Q uint64)."""
+    z = transform(spec, raw).astype(np.float64)
+    # weights are bf16 values on the device (rounded on install), biases fp32
+    members = unpack_params(spec, np.asarray(params, np.float32))
+    members = [([(bf16_round(W), b) for W, b in layers], (bf16_round(head[0]), head[1]))
+               for layers, head in members]
+    E, C = int(spec["members"]), int(spec["classes"])
+    logits = np.zeros((len(z), E, C))
+    for e, (layers, head) in enumerate(members):
+        h = z
+        for W, b in layers:
+            h = np.maximum(h @ W.astype(np.float64).T + b.astype(np.float64), 0.0)
+        logits[:, e, :] = h @ head[0].astype(np.float64).T + head[1].astype(np.float64)
+    mx = logits.max(axis=2, keepdims=True)
+    ex = np.exp(logits - mx)
+    probs = (ex / ex.sum(axis=2, keepdims=True)).mean(axis=1)
+    # argmax with ties to the larger bin
+    bucket = (C - 1 - np.argmax(probs[:, ::-1], axis=1)).astype(np.int32)
+    nbytes = (bucket.astype(np.uint64) + np.uint64(1)) * np.uint64(int(spec["bucket_range"]))
+    return logits, probs, bucket, nbytes

@@ -108,6 +108,14 @@ pick_request_dtype = np.dtype([
     ("estimate", "<u8"), ("want", "<u4"), ("from_recovery", "<i4"),
 ], align=True)
 
+nn_spec_dtype = np.dtype([
+    ("members", "<u4"), ("classes", "<u4"), ("bucket_range", "<u8"), ("depth", "<u4", (8,)),
+    ("width", "<u4", (8, 8)), ("log_mask", "<u4"), ("reserved", "<u4"), ("shift", "<f4", (19,)),
+    ("scale", "<f4", (19,)),
+], align=True)
+NN_MAX_MEMBERS, NN_MAX_DEPTH, NN_MAX_WIDTH, NN_MAX_CLASSES = 8, 8, 8, 48
+
+assert nn_spec_dtype.itemsize == 464
 assert feature_row_dtype.itemsize == 136
 assert feature_packed_dtype.itemsize == 64
 assert task_outcome_dtype.itemsize == 24
@@ -161,6 +169,17 @@ SIGNATURES = {
     "carma_replay_plan_set_timeline_capacity": (c_int, [c_void_p, c_uint64]),
     "carma_replay_plan_timeline": (c_int, [c_void_p, c_uint32, P, c_uint64, POINTER(c_uint64)]),
     "carma_replay_plan_set_log_capacity": (c_int, [c_void_p, c_uint64]),
+    "carma_nn_param_count": (c_uint64, [P]),
+    "carma_nn_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "carma_nn_destroy": (c_int, [c_void_p]),
+    "carma_nn_set_model": (c_int, [c_void_p, c_int32, P, P, c_uint64]),
+    "carma_nn_set_act_table": (c_int, [c_void_p, P]),
+    "carma_nn_set_bit_schema": (c_int, [c_void_p, P]),
+    "carma_nn_predict_device": (c_int, [c_void_p, P, c_int32, P, c_int32, c_uint64, P, P, P, P, c_void_p]),
+    "carma_nn_predict": (c_int, [c_void_p, P, P, c_int32, c_uint64, P, P]),
+    "carma_nn_predict_bitpacked": (c_int, [c_void_p, P, P, c_uint64, P, P]),
+    "carma_nn_last_timing": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_uint64),
+                                     POINTER(c_uint64)]),
     "carma_knn_train": (c_int, [c_void_p, c_int32, P, P, P, c_uint64, c_uint64, c_uint32, c_uint64, P, P, P, P, P]),
     "carma_host_split_order": (c_int, [c_uint64, c_uint64, P, POINTER(c_uint64)]),
     "carma_replay_plan_log": (c_int, [c_void_p, c_uint32, P, c_uint64, POINTER(c_uint64)]),

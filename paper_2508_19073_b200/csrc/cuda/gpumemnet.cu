@@ -1,0 +1,1015 @@
+// Stage 1, neural estimator — the paper's GPUMemNet MLP ensemble on sm_100a
+// tensor cores (tcgen05 + TMEM), fused end to end.
+//
+// Semantics (carma_gpu.h "neural GPUMemNet"): E members,
+// each a stack of 1..8 ReLU layers of <= 8 neurons (batch norm folded) and a
+// linear head over C memory bins; softmax per member, probabilities averaged
+// over members, argmax (ties to the larger bin), bytes = (bin + 1) * range
+// (estimate_learned, proj/src/estimators.cpp:540-551). Inputs are the 19
+// scalar_features (estimators.cpp:317-342) of any estimator row format.
+//
+// Layout on the tensor cores. The E members run side by side: layer l of
+// every member is one block-diagonal GEMM
+//     H_l[128 rows x 64] = relu(H_{l-1}[128 x 64] . W_l^T[64 x 64] + b_l)
+// (member m owns columns 8m..8m+7; a member shallower than the deepest one
+// carries its last activations through identity blocks, exact for ReLU
+// outputs). Layer 0 reads the 19 transformed features (K padded to 32); the
+// head is one GEMM per pass of up to 128 columns (members side by side, CP =
+// C rounded up to 8 columns each). Each MMA is tcgen05.mma.cta_group::1
+// .kind::f16, M = 128, bf16 operands from shared memory (K-major, canonical
+// no-swizzle layout), fp32 accumulators in TMEM.
+//
+// Precision: weights are bf16 values. Activations are split into three
+// bf16 parts, h = a0 + a1 + a2 (a0 = bf16(h), a1 = bf16(h - a0), a2 =
+// bf16(h - a0 - a1)), and every layer accumulates A0.W + A1.W + A2.W in fp32:
+// the products are exact and the activations keep ~24 significant bits, as
+// in an fp32 evaluation. (Two parts keep ~17 bits: measured 6.5e-4 relative
+// logit error on the 8-layer MLP-family ensemble, against 1e-5 for fp32 —
+// re-rounding the activations at every layer, identity layers included,
+// dominates. The north star's bar is 1e-3.)
+//
+// Work split. A CTA per SM holds the model (all layers, ~66 KB for 6-bin
+// families, ~112 KB for the 41-bin MLP family) in shared memory and runs G
+// independent warpgroups; each warpgroup owns a 128-row tile at a time (one
+// row per thread = one TMEM lane), its own A tiles (3 x 16 KB), 128 TMEM
+// columns and an mbarrier. Per layer: the warpgroup stores its activations,
+// fences them into the async proxy, one thread issues the MMAs and commits
+// them to the mbarrier, everyone waits, then reads the accumulators back
+// with tcgen05.ld for the fused bias + ReLU + split epilogue. The G
+// warpgroups interleave, so one's MMAs overlap another's epilogue.
+//
+// Mixed-family batches are partitioned first (nn_count / nn_scatter: a
+// warp-aggregated counting partition of row ids per family), then one
+// ensemble launch per installed family reads its range of the permutation.
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../../include/carma_gpu.h"
+#include "common.cuh"
+#include "rows.cuh"
+
+namespace carma_b200 {
+namespace {
+
+constexpr int kTileRows = 128;
+constexpr int kHidden = 64;           // 8 members x 8 neurons
+constexpr int kK0 = 32;               // 19 features padded to two K=16 steps
+constexpr uint32_t kW0Bytes = kHidden * kK0 * 2;    // 4 KB
+constexpr uint32_t kWBytes = kHidden * kHidden * 2; // 8 KB
+constexpr uint32_t kATile = kTileRows * kHidden * 2; // 16 KB per activation part
+constexpr int kSplit = 3;                             // bf16 parts per activation
+constexpr int kMaxPasses = 8;
+constexpr int kTmemCols = 512;
+constexpr uint32_t kSmemLimit = 227 * 1024;
+
+struct NnModelDev {
+    const uint8_t* blob;  // shared-memory image: weights (canonical bf16), biases (fp32)
+    uint32_t blob_bytes;  // multiple of 16
+    uint32_t smem_blob;   // blob_bytes rounded up to 1024
+    uint32_t depth;       // L: hidden layers (max over members)
+    uint32_t members;     // E
+    uint32_t classes;     // C
+    uint32_t cp;          // C rounded up to 8: TMEM / head-row stride per member
+    uint32_t mpp;         // members per head pass
+    uint32_t passes;
+    uint32_t pass_n[kMaxPasses];     // N of each head pass (multiple of 16)
+    uint32_t pass_row0[kMaxPasses];  // first head row of each pass
+    uint32_t off_head;    // byte offset of the head weights in the blob
+    uint32_t off_bias;    // byte offset of the fp32 biases (L x 64, then head rows)
+    uint32_t log_mask;
+    uint64_t bucket_range;
+    float shift[kFeatureDims];
+    float scale[kFeatureDims];
+};
+
+struct NnParams {
+    // row source (rows.cuh)
+    double act[16];
+    uint64_t bbase[CARMA_BIT_FIELDS];
+    uint16_t boff[CARMA_BIT_FIELDS];
+    uint8_t bw[CARMA_BIT_FIELDS];
+    uint32_t bwpr;
+    const void* rows;
+    const int8_t* family;
+    int32_t default_family;
+    // this launch
+    NnModelDev m;
+    int32_t fam;              // family of this launch
+    const uint32_t* perm;     // row ids grouped by family (null: rows [0, n))
+    const uint32_t* counts;   // per-family row counts (null: n rows)
+    uint64_t n;
+    int32_t* bucket;
+    uint64_t* bytes;
+    float* probs;   // q x CARMA_NN_MAX_CLASSES (nullable)
+    float* logits;  // q x CARMA_NN_MAX_MEMBERS x CARMA_NN_MAX_CLASSES (nullable)
+};
+
+// ---------------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// UMMA shared-memory descriptor, K-major, no swizzle (cute::UMMA::SmemDescriptor):
+// start >> 4 at [0,14), leading (K core-matrix) byte offset >> 4 at [16,30),
+// stride (8-row group) byte offset >> 4 at [32,46), version 1 at [46,48).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return static_cast<uint64_t>((addr >> 4) & 0x3fffu) | (static_cast<uint64_t>((lbo >> 4) & 0x3fffu) << 16) |
+           (static_cast<uint64_t>((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);
+}
+
+// Instruction descriptor, kind::f16: fp32 accumulator, bf16 A and B, both
+// K-major, N >> 3 at [17,23), M >> 4 at [24,29) (cute::UMMA::InstrDescriptor).
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((kTileRows >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.b32 %0, 1, 0, P1;\n\t}\n"
+            : "=r"(done)
+            : "r"(a), "r"(phase)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void group_bar(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
+
+// 32 lanes x 32 bit, 8 consecutive columns per thread. The registers are
+// written asynchronously: tmem_wait8 (tcgen05.wait::ld) must run before any
+// use, and takes them as in/out operands so no use is hoisted above it.
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(addr));
+}
+
+__device__ __forceinline__ void tmem_wait8(uint32_t (&r)[8]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])
+                 :
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);  // .x = a (lower address = lower K)
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// Splits 8 consecutive activations into kSplit bf16 parts and stores part j
+// at byte offset `off` of A tile j (tiles kATile bytes apart from `a`).
+__device__ __forceinline__ void store_split8(uint8_t* a, uint32_t off, const float (&h)[8]) {
+    float rem[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) rem[i] = h[i];
+#pragma unroll
+    for (int j = 0; j < kSplit; ++j) {
+        float part[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            part[i] = __bfloat162float(__float2bfloat16_rn(rem[i]));
+            rem[i] = __fsub_rn(rem[i], part[i]);  // exact
+        }
+        *reinterpret_cast<uint4*>(a + j * kATile + off) = make_uint4(
+            pack_bf16(part[0], part[1]), pack_bf16(part[2], part[3]), pack_bf16(part[4], part[5]),
+            pack_bf16(part[6], part[7]));
+    }
+}
+
+// Canonical K-major no-swizzle placement of (row r, K chunk kc) in a tile
+// whose 8-row groups are `sbo` bytes apart: core matrices of 8 rows x 16 B.
+__device__ __forceinline__ uint32_t a_off(int r, int kc, uint32_t sbo) {
+    return static_cast<uint32_t>(r >> 3) * sbo + static_cast<uint32_t>(kc) * 128u + static_cast<uint32_t>(r & 7) * 16u;
+}
+
+// Issues the MMAs of one layer: D = sum_j A_j.B over `ksteps` K=16 steps.
+__device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a, uint32_t b, uint32_t b_sbo, int ksteps,
+                                            uint32_t idesc) {
+    for (int ks = 0; ks < ksteps; ++ks) {
+        const uint64_t bd = sdesc(b + ks * 256u, 128u, b_sbo);
+#pragma unroll
+        for (int j = 0; j < kSplit; ++j)
+            mma_bf16(tmem_d, sdesc(a + j * kATile + ks * 256u, 128u, 1024u), bd, idesc, (ks | j) ? 1u : 0u);
+    }
+}
+
+// ------------------------------------------------------------- the ensemble
+
+template <int FMT, int G, int CP, bool DIAG>
+__global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant__ NnParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const NnModelDev& m = p.m;
+    const int tid = threadIdx.x;
+    const int g = tid >> 7;
+    const int r = tid & 127;
+    const int warp = tid >> 5;
+    uint8_t* a_t = smem + m.smem_blob + g * (kSplit * kATile);  // this warpgroup's A tiles
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + m.smem_blob + G * (kSplit * kATile));
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + G);
+
+    // The model image: weights in their canonical layouts, biases.
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(m.blob);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (uint32_t i = tid; i < m.blob_bytes / 16; i += G * 128) dst[i] = __ldg(src + i);
+    }
+    if (tid == 0) {
+        for (int i = 0; i < G; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + i)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot + static_cast<uint32_t>(g * 128);        // this warpgroup's columns
+    const uint32_t tmem_row = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);  // this warp's lanes
+
+    const float* bias = reinterpret_cast<const float*>(smem + m.off_bias);
+    const float* head_bias = bias + m.depth * kHidden;
+    const uint32_t s_a = smem_u32(a_t), s_blob = smem_u32(smem);
+
+    uint64_t n = p.n, base = 0;
+    if (p.counts) {
+        n = p.counts[p.fam];
+        for (int f = 0; f < p.fam; ++f) base += p.counts[f];
+    }
+    const uint64_t tiles = (n + kTileRows - 1) / kTileRows;
+    uint32_t phase = 0;
+    const bool issuer = r == 0;
+
+    for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * G + g; tile < tiles;
+         tile += static_cast<uint64_t>(gridDim.x) * G) {
+        const uint64_t i = tile * kTileRows + r;
+        const bool valid = i < n;
+        const uint64_t row = valid ? (p.perm ? static_cast<uint64_t>(p.perm[base + i]) : base + i) : 0;
+
+        // ---- features -> z (fp32) -> layer-0 A tile (K 0..31)
+        {
+            float z[kK0];
+#pragma unroll
+            for (int d = 0; d < kK0; ++d) z[d] = 0.f;
+            if (valid) {
+                double raw[kFeatureDims];
+                load_raw<FMT>(p, row, raw);
+#pragma unroll
+                for (int d = 0; d < kFeatureDims; ++d) {
+                    const double t = ((m.log_mask >> d) & 1u) ? log1p(fmax(raw[d], 0.0)) : raw[d];
+                    z[d] = __fmul_rn(__fsub_rn(__double2float_rn(t), m.shift[d]), m.scale[d]);
+                }
+            }
+#pragma unroll
+            for (int kc = 0; kc < kK0 / 8; ++kc) {
+                float h[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h[j] = z[kc * 8 + j];
+                store_split8(a_t, a_off(r, kc, 1024u), h);
+            }
+        }
+        fence_async_smem();
+        fence_before();
+        group_bar(g);
+        if (issuer) {
+            fence_after();
+            issue_layer(tmem, s_a, s_blob, 512u, kK0 / 16, idesc_bf16(kHidden));
+            mma_commit(mbar + g);
+        }
+        mbar_wait(mbar + g, phase);
+        phase ^= 1u;
+        fence_after();
+
+        // ---- hidden layers: epilogue of layer l-1 feeds the MMAs of layer l
+        for (uint32_t l = 1; l <= m.depth; ++l) {
+            const float* b = bias + (l - 1) * kHidden;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t v[4][8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld8(tmem_row + half * 32 + c * 8, v[c]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_wait8(v[c]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float h[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        h[j] = fmaxf(__fadd_rn(__uint_as_float(v[c][j]), b[half * 32 + c * 8 + j]), 0.f);
+                    store_split8(a_t, a_off(r, half * 4 + c, 1024u), h);
+                }
+            }
+            fence_async_smem();
+            fence_before();
+            group_bar(g);
+            if (l == m.depth) break;  // the head passes issue from the final activations
+            if (issuer) {
+                fence_after();
+                issue_layer(tmem, s_a, s_blob + kW0Bytes + (l - 1) * kWBytes, 1024u, kHidden / 16,
+                            idesc_bf16(kHidden));
+                mma_commit(mbar + g);
+            }
+            mbar_wait(mbar + g, phase);
+            phase ^= 1u;
+            fence_after();
+        }
+
+        // ---- head passes: logits, softmax per member, mean over members
+        float pm[CP];
+#pragma unroll
+        for (int c = 0; c < CP; ++c) pm[c] = 0.f;
+        for (uint32_t ps = 0; ps < m.passes; ++ps) {
+            if (ps > 0) {  // every lane's reads of the previous pass precede its overwrite
+                fence_before();
+                group_bar(g);
+            }
+            if (issuer) {
+                fence_after();
+                issue_layer(tmem, s_a, s_blob + m.off_head + m.pass_row0[ps] * 128u, 1024u, kHidden / 16,
+                            idesc_bf16(m.pass_n[ps]));
+                mma_commit(mbar + g);
+            }
+            mbar_wait(mbar + g, phase);
+            phase ^= 1u;
+            fence_after();
+            const uint32_t m0 = ps * m.mpp;
+            const uint32_t m1 = min(m.members, m0 + m.mpp);
+            for (uint32_t mem = m0; mem < m1; ++mem) {
+                const uint32_t col = (mem - m0) * m.cp;
+                uint32_t v[CP / 8][8];
+#pragma unroll
+                for (int c = 0; c < CP / 8; ++c) tmem_ld8(tmem_row + col + c * 8, v[c]);
+#pragma unroll
+                for (int c = 0; c < CP / 8; ++c) tmem_wait8(v[c]);
+                float lg[CP];
+#pragma unroll
+                for (int c = 0; c < CP; ++c) lg[c] = __uint_as_float(v[c / 8][c % 8]);
+                const float* hb = head_bias + m.pass_row0[ps] + col;
+                float mx = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < CP; ++c) {
+                    if (c < static_cast<int>(m.classes)) {
+                        lg[c] = __fadd_rn(lg[c], hb[c]);
+                        mx = fmaxf(mx, lg[c]);
+                    }
+                }
+                if (DIAG && valid && p.logits) {
+                    float* out = p.logits + (row * CARMA_NN_MAX_MEMBERS + mem) * CARMA_NN_MAX_CLASSES;
+#pragma unroll
+                    for (int c = 0; c < CP; ++c)
+                        if (c < static_cast<int>(m.classes)) out[c] = lg[c];
+                }
+                float s = 0.f;
+#pragma unroll
+                for (int c = 0; c < CP; ++c) {
+                    if (c < static_cast<int>(m.classes)) {
+                        lg[c] = expf(__fsub_rn(lg[c], mx));
+                        s = __fadd_rn(s, lg[c]);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < CP; ++c)
+                    if (c < static_cast<int>(m.classes)) pm[c] = __fadd_rn(pm[c], __fdiv_rn(lg[c], s));
+            }
+        }
+        // The next tile's first MMA overwrites TMEM and the A tiles: its
+        // fence_before + group barrier orders it after these reads.
+        if (valid) {
+            const float inv_e = 1.0f / static_cast<float>(m.members);
+            int best = 0;
+            float bv = -1.f;
+#pragma unroll
+            for (int c = 0; c < CP; ++c) {
+                if (c < static_cast<int>(m.classes)) {
+                    pm[c] = __fmul_rn(pm[c], inv_e);
+                    if (pm[c] >= bv) {  // ties to the larger bin
+                        bv = pm[c];
+                        best = c;
+                    }
+                }
+            }
+            p.bucket[row] = best;
+            p.bytes[row] = static_cast<uint64_t>(best + 1) * m.bucket_range;
+            if (DIAG && p.probs) {
+                float* out = p.probs + row * CARMA_NN_MAX_CLASSES;
+#pragma unroll
+                for (int c = 0; c < CP; ++c)
+                    if (c < static_cast<int>(m.classes)) out[c] = pm[c];
+            }
+        }
+    }
+
+    fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
+// ------------------------------------------------------ family partition
+
+constexpr int kBins = CARMA_FAMILIES + 1;  // + rows without a model
+
+template <int FMT>
+__device__ __forceinline__ int nn_bin(const NnParams& p, uint64_t i, uint32_t present) {
+    const int f = row_family<FMT>(p, i);
+    return (f >= 0 && f < CARMA_FAMILIES && ((present >> f) & 1u)) ? f : CARMA_FAMILIES;
+}
+
+template <int FMT>
+__global__ void nn_count(const __grid_constant__ NnParams p, uint64_t q, uint32_t present, uint32_t* counts) {
+    const unsigned lane = threadIdx.x & 31;
+    uint32_t local[kBins] = {0, 0, 0, 0};
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); i0 < q; i0 += stride) {
+        const uint64_t i = i0 + lane;
+        const int b = i < q ? nn_bin<FMT>(p, i, present) : -1;
+#pragma unroll
+        for (int k = 0; k < kBins; ++k) local[k] += __popc(__ballot_sync(0xffffffffu, b == k));
+    }
+    if (lane == 0)
+        for (int k = 0; k < kBins; ++k)
+            if (local[k]) atomicAdd(counts + k, local[k]);
+}
+
+template <int FMT>
+__global__ void nn_scatter(const __grid_constant__ NnParams p, uint64_t q, uint32_t present,
+                           const uint32_t* __restrict__ counts, uint32_t* __restrict__ cursor,
+                           uint32_t* __restrict__ perm) {
+    const unsigned lane = threadIdx.x & 31;
+    uint32_t off[kBins];
+    off[0] = 0;
+#pragma unroll
+    for (int k = 1; k < kBins; ++k) off[k] = off[k - 1] + counts[k - 1];
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); i0 < q; i0 += stride) {
+        const uint64_t i = i0 + lane;
+        const int b = i < q ? nn_bin<FMT>(p, i, present) : -1;
+        if (b == CARMA_FAMILIES) {  // FamilyMismatch -> no estimate (manager.cpp:99-105)
+            p.bucket[i] = -1;
+            p.bytes[i] = UINT64_MAX;
+        }
+#pragma unroll
+        for (int k = 0; k < CARMA_FAMILIES; ++k) {
+            const unsigned mask = __ballot_sync(0xffffffffu, b == k);
+            if (!mask) continue;
+            uint32_t at = 0;
+            if (lane == 0) at = atomicAdd(cursor + k, static_cast<uint32_t>(__popc(mask)));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (b == k) perm[off[k] + at + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+        }
+    }
+}
+
+__global__ void nn_mark_missing(uint64_t q, int32_t* bucket, uint64_t* bytes) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < q;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        bucket[i] = -1;
+        bytes[i] = UINT64_MAX;
+    }
+}
+
+// ----------------------------------------------------------------- host side
+
+struct HostNn {
+    bool present = false;
+    carma_nn_spec spec{};
+    NnModelDev dev{};
+    DeviceBuffer blob;
+};
+
+uint16_t bf16_bits(float x) {  // round to nearest even (finite inputs)
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    const uint32_t lsb = (u >> 16) & 1u;
+    u += 0x7fffu + lsb;
+    return static_cast<uint16_t>(u >> 16);
+}
+
+uint64_t param_count(const carma_nn_spec& s) {
+    uint64_t n = 0;
+    for (uint32_t e = 0; e < s.members; ++e) {
+        uint32_t in = kFeatureDims;
+        for (uint32_t l = 0; l < s.depth[e]; ++l) {
+            n += static_cast<uint64_t>(s.width[e][l]) * in + s.width[e][l];
+            in = s.width[e][l];
+        }
+        n += static_cast<uint64_t>(s.classes) * in + s.classes;
+    }
+    return n;
+}
+
+void validate(const carma_nn_spec& s) {
+    if (s.members < 1 || s.members > CARMA_NN_MAX_MEMBERS) throw InvalidArg("members must be 1..8");
+    if (s.classes < 2 || s.classes > CARMA_NN_MAX_CLASSES) throw InvalidArg("classes must be 2..48");
+    if (s.bucket_range == 0) throw InvalidArg("bucket range must be > 0");
+    for (uint32_t e = 0; e < s.members; ++e) {
+        if (s.depth[e] < 1 || s.depth[e] > CARMA_NN_MAX_DEPTH) throw InvalidArg("member depth must be 1..8");
+        for (uint32_t l = 0; l < s.depth[e]; ++l)
+            if (s.width[e][l] < 1 || s.width[e][l] > CARMA_NN_MAX_WIDTH) throw InvalidArg("layer width must be 1..8");
+    }
+    if (s.log_mask >> kFeatureDims) throw InvalidArg("log_mask has bits past feature 18");
+}
+
+// Position of element (row, k) of a [rows x K] bf16 operand in the canonical
+// K-major no-swizzle layout with 8-row groups `sbo` bytes apart.
+size_t canon(uint32_t row, uint32_t k, uint32_t sbo) {
+    return static_cast<size_t>(row >> 3) * sbo + (k >> 3) * 128u + (row & 7u) * 16u + (k & 7u) * 2u;
+}
+
+// Builds the shared-memory image of a model: block-diagonal bf16 weights in
+// their UMMA layouts (identity blocks carry shallow members through the
+// deeper layers), the head passes, and the fp32 biases.
+void build_model(HostNn& hm, int device, const carma_nn_spec& s, const float* params) {
+    uint32_t L = 0;
+    for (uint32_t e = 0; e < s.members; ++e) L = std::max(L, s.depth[e]);
+    const uint32_t cp = (s.classes + 7u) & ~7u;
+    const uint32_t mpp = std::min<uint32_t>(s.members, 128u / cp);
+    const uint32_t passes = (s.members + mpp - 1) / mpp;
+    if (passes > static_cast<uint32_t>(kMaxPasses)) throw Unsupported("too many head passes");
+    NnModelDev d{};
+    d.depth = L;
+    d.members = s.members;
+    d.classes = s.classes;
+    d.cp = cp;
+    d.mpp = mpp;
+    d.passes = passes;
+    uint32_t head_rows = 0;
+    for (uint32_t ps = 0; ps < passes; ++ps) {
+        const uint32_t mems = std::min(mpp, s.members - ps * mpp);
+        d.pass_row0[ps] = head_rows;
+        d.pass_n[ps] = (mems * cp + 15u) & ~15u;
+        head_rows += d.pass_n[ps];
+    }
+    d.off_head = kW0Bytes + (L - 1) * kWBytes;
+    d.off_bias = d.off_head + head_rows * 128u;
+    d.blob_bytes = (d.off_bias + 4u * (L * kHidden + head_rows) + 15u) & ~15u;
+    d.smem_blob = (d.blob_bytes + 1023u) & ~1023u;
+    d.log_mask = s.log_mask;
+    d.bucket_range = s.bucket_range;
+    std::memcpy(d.shift, s.shift, sizeof(d.shift));
+    std::memcpy(d.scale, s.scale, sizeof(d.scale));
+
+    std::vector<uint8_t> blob(d.blob_bytes, 0);
+    auto put = [&](size_t off, float w) {
+        const uint16_t b = bf16_bits(w);
+        std::memcpy(blob.data() + off, &b, 2);
+    };
+    float* bias = reinterpret_cast<float*>(blob.data() + d.off_bias);
+    const float* pp = params;
+    for (uint32_t e = 0; e < s.members; ++e) {
+        uint32_t in = kFeatureDims;
+        for (uint32_t l = 0; l < s.depth[e]; ++l) {
+            const uint32_t w = s.width[e][l];
+            const size_t base = l == 0 ? 0 : kW0Bytes + (l - 1) * kWBytes;
+            const uint32_t sbo = l == 0 ? 512u : 1024u;
+            for (uint32_t o = 0; o < w; ++o)
+                for (uint32_t k = 0; k < in; ++k)
+                    put(base + canon(8 * e + o, l == 0 ? k : 8 * e + k, sbo), pp[o * in + k]);
+            pp += static_cast<size_t>(w) * in;
+            for (uint32_t o = 0; o < w; ++o) bias[l * kHidden + 8 * e + o] = pp[o];
+            pp += w;
+            in = w;
+        }
+        for (uint32_t l = s.depth[e]; l < L; ++l)  // identity: carry the last activations
+            for (uint32_t o = 0; o < in; ++o) put(kW0Bytes + (l - 1) * kWBytes + canon(8 * e + o, 8 * e + o, 1024u), 1.0f);
+        const uint32_t ps = e / mpp, slot = e % mpp;
+        const uint32_t row0 = d.pass_row0[ps] + slot * cp;
+        for (uint32_t c = 0; c < s.classes; ++c)
+            for (uint32_t k = 0; k < in; ++k) put(d.off_head + canon(row0 + c, 8 * e + k, 1024u), pp[c * in + k]);
+        pp += static_cast<size_t>(s.classes) * in;
+        for (uint32_t c = 0; c < s.classes; ++c) bias[L * kHidden + row0 + c] = pp[c];
+        pp += s.classes;
+    }
+    DeviceGuard gd(device);
+    hm.blob.ensure(blob.size());
+    CARMA_CUDA(cudaMemcpy(hm.blob.ptr, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+    d.blob = hm.blob.as<uint8_t>();
+    hm.dev = d;
+    hm.spec = s;
+    hm.present = true;
+}
+
+}  // namespace
+
+struct NnHandle {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t pipe[2] = {nullptr, nullptr};
+    HostNn model[CARMA_FAMILIES];
+    struct Scratch {
+        DeviceBuffer rows, family, perm, counts, bucket, bytes;
+        PinnedBuffer stage_rows, stage_family;
+    } scratch[2];
+    double act[16] = {0};
+    carma_bit_schema schema{};
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // call start, ensemble start, ensemble end
+    bool timed = false;
+    uint64_t last_launches = 0, last_mmas = 0;
+    uint32_t last_counts[kBins] = {0, 0, 0, 0};
+    std::mutex mu;
+};
+
+namespace {
+
+int sm_count(int device) {
+    static int cached[64] = {0};
+    if (device >= 0 && device < 64 && cached[device]) return cached[device];
+    int n = 0;
+    CARMA_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    if (device >= 0 && device < 64) cached[device] = n;
+    return n;
+}
+
+NnParams base_params(const NnHandle& h) {
+    NnParams p{};
+    std::memcpy(p.act, h.act, sizeof(p.act));
+    for (int f = 0; f < CARMA_BIT_FIELDS; ++f) {
+        p.bbase[f] = h.schema.base[f];
+        p.boff[f] = h.schema.offset[f];
+        p.bw[f] = h.schema.width[f];
+    }
+    p.bwpr = h.schema.words_per_row;
+    return p;
+}
+
+template <int FMT, int G, int CP, bool DIAG>
+void launch_ensemble_t(const NnParams& p, int device, cudaStream_t s) {
+    const size_t smem = p.m.smem_blob + G * (kSplit * kATile) + G * 8 + 16;
+    if (smem > kSmemLimit) throw Unsupported("model too large for shared memory");
+    static cudaError_t attr = cudaFuncSetAttribute(nn_ensemble<FMT, G, CP, DIAG>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(kSmemLimit));
+    CARMA_CUDA(attr);
+    nn_ensemble<FMT, G, CP, DIAG><<<sm_count(device), G * 128, smem, s>>>(p);
+    CARMA_CUDA(cudaGetLastError());
+}
+
+// Warpgroups per CTA: as many 48-KB A-tile triples as fit beside the model
+// (<= 4: TMEM holds 4 x 128 columns), and CP = 8 or 48 columns per member.
+template <int FMT, bool DIAG>
+void launch_ensemble(const NnParams& p, int device, cudaStream_t s) {
+    const uint32_t room = kSmemLimit - p.m.smem_blob - 64;
+    const int g = static_cast<int>(std::min<uint32_t>(4, room / (kSplit * kATile)));
+    if (g < 1) throw Unsupported("model too large for shared memory");
+    if (p.m.cp <= 8) {
+        if (g >= 4) launch_ensemble_t<FMT, 4, 8, DIAG>(p, device, s);
+        else if (g == 3) launch_ensemble_t<FMT, 3, 8, DIAG>(p, device, s);
+        else launch_ensemble_t<FMT, 2, 8, DIAG>(p, device, s);
+    } else {
+        if (g >= 3) launch_ensemble_t<FMT, 3, 48, DIAG>(p, device, s);
+        else launch_ensemble_t<FMT, 2, 48, DIAG>(p, device, s);
+    }
+}
+
+template <int FMT>
+void dispatch_diag(bool diag, const NnParams& p, int device, cudaStream_t s) {
+    if (diag) launch_ensemble<FMT, true>(p, device, s);
+    else launch_ensemble<FMT, false>(p, device, s);
+}
+
+template <int FMT>
+void launch_partition(const NnParams& p, uint64_t q, uint32_t present, uint32_t* counts, uint32_t* perm, int device,
+                      cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((q + 255) / 256, 4ull * sm_count(device)));
+    nn_count<FMT><<<grid, 256, 0, s>>>(p, q, present, counts);
+    nn_scatter<FMT><<<grid, 256, 0, s>>>(p, q, present, counts, counts + kBins, perm);
+    CARMA_CUDA(cudaGetLastError());
+}
+
+// One predict on device-resident rows. Returns the number of launches.
+uint64_t run_predict(NnHandle& h, NnHandle::Scratch& sc, const void* rows, int32_t format, const int8_t* family,
+                     int32_t default_family, uint64_t q, int32_t* bucket, uint64_t* bytes, float* probs,
+                     float* logits, cudaStream_t s) {
+    NnParams p = base_params(h);
+    p.rows = rows;
+    p.family = family;
+    p.default_family = default_family;
+    p.bucket = bucket;
+    p.bytes = bytes;
+    p.probs = probs;
+    p.logits = logits;
+    const bool diag = probs || logits;
+    uint32_t present = 0;
+    for (int f = 0; f < CARMA_FAMILIES; ++f)
+        if (h.model[f].present) present |= 1u << f;
+    const bool timed = h.timed && h.ev[0];
+    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
+    uint64_t launches = 0;
+    const bool per_row = format == CARMA_ROWS_PACKED || format == CARMA_ROWS_BITPACKED || family;
+    std::vector<int> fams;
+    if (!per_row) {
+        const bool ok = default_family >= 0 && default_family < CARMA_FAMILIES && ((present >> default_family) & 1u);
+        if (!ok) {
+            nn_mark_missing<<<grid_for(q, 256, 4u * sm_count(h.device)), 256, 0, s>>>(q, bucket, bytes);
+            CARMA_CUDA(cudaGetLastError());
+            if (timed) {
+                CARMA_CUDA(cudaEventRecord(h.ev[1], s));
+                CARMA_CUDA(cudaEventRecord(h.ev[2], s));
+            }
+            return 1;
+        }
+        p.n = q;
+        fams.push_back(default_family);
+    } else {
+        if (q > 0xffffffffull) throw Unsupported("more than 2^32 rows in one device call");
+        sc.counts.ensure(2 * kBins * sizeof(uint32_t));
+        sc.perm.ensure(q * sizeof(uint32_t));
+        CARMA_CUDA(cudaMemsetAsync(sc.counts.ptr, 0, 2 * kBins * sizeof(uint32_t), s));
+        switch (format) {
+            case CARMA_ROWS_PACKED:
+                launch_partition<CARMA_ROWS_PACKED>(p, q, present, sc.counts.as<uint32_t>(), sc.perm.as<uint32_t>(), h.device, s);
+                break;
+            case CARMA_ROWS_BITPACKED:
+                launch_partition<CARMA_ROWS_BITPACKED>(p, q, present, sc.counts.as<uint32_t>(), sc.perm.as<uint32_t>(), h.device, s);
+                break;
+            case CARMA_ROWS_SCALAR:
+                launch_partition<CARMA_ROWS_SCALAR>(p, q, present, sc.counts.as<uint32_t>(), sc.perm.as<uint32_t>(), h.device, s);
+                break;
+            default:
+                launch_partition<CARMA_ROWS_FEATURES>(p, q, present, sc.counts.as<uint32_t>(), sc.perm.as<uint32_t>(), h.device, s);
+        }
+        launches += 3;  // memset + count + scatter
+        p.perm = sc.perm.as<uint32_t>();
+        p.counts = sc.counts.as<uint32_t>();
+        for (int f = 0; f < CARMA_FAMILIES; ++f)
+            if ((present >> f) & 1u) fams.push_back(f);
+    }
+    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[1], s));
+    for (int f : fams) {
+        p.fam = f;
+        p.m = h.model[f].dev;
+        switch (format) {
+            case CARMA_ROWS_PACKED: dispatch_diag<CARMA_ROWS_PACKED>(diag, p, h.device, s); break;
+            case CARMA_ROWS_BITPACKED: dispatch_diag<CARMA_ROWS_BITPACKED>(diag, p, h.device, s); break;
+            case CARMA_ROWS_SCALAR: dispatch_diag<CARMA_ROWS_SCALAR>(diag, p, h.device, s); break;
+            default: dispatch_diag<CARMA_ROWS_FEATURES>(diag, p, h.device, s);
+        }
+        ++launches;
+    }
+    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[2], s));
+    return launches;
+}
+
+// MMAs per 128-row tile of a model: layer 0 (2 K steps), L-1 hidden layers
+// and the head passes (4 K steps each), kSplit MMAs per step.
+uint64_t mmas_per_tile(const NnModelDev& d) { return kSplit * (2 + 4ull * (d.depth - 1) + 4ull * d.passes); }
+
+void check_ready(NnHandle* h) {
+    if (!h) throw InvalidArg("null handle");
+    bool any = false;
+    for (const auto& m : h->model) any = any || m.present;
+    if (!any) throw InvalidArg("no model installed");
+}
+
+carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int32_t format, const int8_t* family,
+                          int32_t default_family, uint64_t q, int32_t* bucket_out, uint64_t* bytes_out,
+                          size_t tail_bytes = 0) {
+    return guarded([&] {
+        NnHandle* h = reinterpret_cast<NnHandle*>(hh);
+        check_ready(h);
+        if (q == 0) return;
+        if (!rows) throw InvalidArg("rows is null");
+        std::lock_guard<std::mutex> lock(h->mu);
+        DeviceGuard g(h->device);
+        const uint64_t chunk = uint64_t{1} << 21;
+        const uint64_t small = uint64_t{1} << 18;
+        auto chunk_rows = [&](uint64_t c, uint64_t remaining) -> uint64_t {
+            const uint64_t grow = std::min<uint64_t>(chunk, small << std::min<uint64_t>(c, 20));
+            return std::min<uint64_t>(grow, std::max<uint64_t>(small, remaining / 2));
+        };
+        const bool rows_pinned = is_pinned(rows);
+        const bool fam_pinned = !family || is_pinned(family);
+        const bool out_pinned = (!bucket_out || is_pinned(bucket_out)) && (!bytes_out || is_pinned(bytes_out));
+        h->timed = false;
+        uint64_t launches = 0, beg = 0, cnt = 0;
+        for (uint64_t c = 0; beg < q; ++c, beg += cnt) {
+            NnHandle::Scratch& sc = h->scratch[c & 1];
+            cudaStream_t s = h->pipe[c & 1];
+            cnt = std::min<uint64_t>(chunk_rows(c, q - beg), q - beg);
+            const char* src = static_cast<const char*>(rows) + beg * row_bytes;
+            const uint64_t cap_rows = std::min<uint64_t>(chunk, q);
+            sc.rows.ensure(cap_rows * row_bytes + tail_bytes);
+            sc.bucket.ensure(cap_rows * 4);
+            sc.bytes.ensure(cap_rows * 8);
+            if (family) sc.family.ensure(cap_rows);
+            if (!rows_pinned || !fam_pinned) {
+                CARMA_CUDA(cudaStreamSynchronize(s));
+                sc.stage_rows.ensure(cap_rows * row_bytes + tail_bytes);
+                std::memcpy(sc.stage_rows.ptr, src, cnt * row_bytes + tail_bytes);
+                src = sc.stage_rows.as<char>();
+                if (family) {
+                    sc.stage_family.ensure(cap_rows);
+                    std::memcpy(sc.stage_family.ptr, family + beg, cnt);
+                }
+            }
+            CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, src, cnt * row_bytes + tail_bytes, cudaMemcpyHostToDevice, s));
+            if (family)
+                CARMA_CUDA(cudaMemcpyAsync(sc.family.ptr,
+                                           (!rows_pinned || !fam_pinned) ? sc.stage_family.as<int8_t>() : family + beg,
+                                           cnt, cudaMemcpyHostToDevice, s));
+            launches += run_predict(*h, sc, sc.rows.ptr, format, family ? sc.family.as<int8_t>() : nullptr,
+                                    default_family, cnt, sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(), nullptr,
+                                    nullptr, s);
+            if (out_pinned) {
+                if (bucket_out)
+                    CARMA_CUDA(cudaMemcpyAsync(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost, s));
+                if (bytes_out)
+                    CARMA_CUDA(cudaMemcpyAsync(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost, s));
+            } else {
+                if (bucket_out)
+                    CARMA_CUDA(cudaMemcpyAsync(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost, s));
+                if (bytes_out)
+                    CARMA_CUDA(cudaMemcpyAsync(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost, s));
+                CARMA_CUDA(cudaStreamSynchronize(s));
+            }
+        }
+        CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
+        CARMA_CUDA(cudaStreamSynchronize(h->pipe[1]));
+        h->last_launches = launches;
+        h->last_mmas = 0;
+    });
+}
+
+}  // namespace
+}  // namespace carma_b200
+
+using namespace carma_b200;
+
+extern "C" {
+
+uint64_t carma_nn_param_count(const carma_nn_spec* spec) { return spec ? param_count(*spec) : 0; }
+
+carma_status carma_nn_create(int device, carma_nn** out) {
+    return guarded([&] {
+        if (!out) throw InvalidArg("out is null");
+        require_device(device);
+        DeviceGuard g(device);
+        auto* h = new NnHandle();
+        h->device = device;
+        CARMA_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CARMA_CUDA(cudaStreamCreateWithFlags(&h->pipe[0], cudaStreamNonBlocking));
+        CARMA_CUDA(cudaStreamCreateWithFlags(&h->pipe[1], cudaStreamNonBlocking));
+        for (auto& e : h->ev) CARMA_CUDA(cudaEventCreate(&e));
+        *out = reinterpret_cast<carma_nn*>(h);
+    });
+}
+
+carma_status carma_nn_destroy(carma_nn* hh) {
+    return guarded([&] {
+        NnHandle* h = reinterpret_cast<NnHandle*>(hh);
+        if (!h) return;
+        {
+            DeviceGuard g(h->device);
+            cudaDeviceSynchronize();
+            for (auto& m : h->model) m.blob.release();
+            for (auto& sc : h->scratch) {
+                for (DeviceBuffer* b : {&sc.rows, &sc.family, &sc.perm, &sc.counts, &sc.bucket, &sc.bytes}) b->release();
+                sc.stage_rows.release();
+                sc.stage_family.release();
+            }
+            for (auto e : h->ev)
+                if (e) cudaEventDestroy(e);
+            if (h->stream) cudaStreamDestroy(h->stream);
+            for (auto s : h->pipe)
+                if (s) cudaStreamDestroy(s);
+        }
+        delete h;
+    });
+}
+
+carma_status carma_nn_set_model(carma_nn* hh, int32_t family, const carma_nn_spec* spec, const float* params,
+                                uint64_t n_params) {
+    return guarded([&] {
+        NnHandle* h = reinterpret_cast<NnHandle*>(hh);
+        if (!h || !spec || !params) throw InvalidArg("null argument");
+        if (family < 0 || family >= CARMA_FAMILIES) throw InvalidArg("family out of range");
+        validate(*spec);
+        if (n_params != param_count(*spec)) throw InvalidArg("parameter count does not match the spec");
+        for (uint64_t i = 0; i < n_params; ++i)
+            if (!std::isfinite(params[i])) throw InvalidArg("non-finite parameter");
+        std::lock_guard<std::mutex> lock(h->mu);
+        DeviceGuard g(h->device);
+        CARMA_CUDA(cudaDeviceSynchronize());  // a queued call may still read the old blob
+        build_model(h->model[family], h->device, *spec, params);
+    });
+}
+
+carma_status carma_nn_set_act_table(carma_nn* hh, const double* act_table) {
+    return guarded([&] {
+        NnHandle* h = reinterpret_cast<NnHandle*>(hh);
+        if (!h || !act_table) throw InvalidArg("null argument");
+        std::memcpy(h->act, act_table, sizeof(h->act));
+    });
+}
+
+carma_status carma_nn_set_bit_schema(carma_nn* hh, const carma_bit_schema* schema) {
+    return guarded([&] {
+        NnHandle* h = reinterpret_cast<NnHandle*>(hh);
+        if (!h || !schema) throw InvalidArg("null argument");
+        if (schema->words_per_row == 0) throw InvalidArg("schema has no words per row");
+        for (int f = 0; f < CARMA_BIT_FIELDS; ++f)
+            if (schema->width[f] > 48) throw InvalidArg("schema field wider than 48 bits");
+        h->schema = *schema;
+        std::memcpy(h->act, schema->act_table, sizeof(h->act));
+    });
+}
+
+carma_status carma_nn_predict_device(carma_nn* hh, const void* rows, int32_t format, const int8_t* family,
+                                     int32_t default_family, uint64_t q, int32_t* bucket_out, uint64_t* bytes_out,
+                                     float* probs, float* logits, void* stream) {
+    return guarded([&] {
+        NnHandle* h = reinterpret_cast<NnHandle*>(hh);
+        check_ready(h);
+        if (q == 0) return;
+        if (!rows || !bucket_out || !bytes_out) throw InvalidArg("null device buffer");
+        if (format < CARMA_ROWS_FEATURES || format > CARMA_ROWS_BITPACKED) throw InvalidArg("unknown row format");
+        std::lock_guard<std::mutex> lock(h->mu);
+        DeviceGuard g(h->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        h->timed = true;
+        NnHandle::Scratch& sc = h->scratch[0];
+        h->last_launches = run_predict(*h, sc, rows, format, family, default_family, q, bucket_out, bytes_out, probs,
+                                       logits, s);
+        // MMA count from the family counts of this call
+        uint64_t mmas = 0;
+        const bool per_row = format == CARMA_ROWS_PACKED || format == CARMA_ROWS_BITPACKED || family;
+        if (per_row) {
+            CARMA_CUDA(cudaMemcpyAsync(h->last_counts, sc.counts.ptr, sizeof(h->last_counts), cudaMemcpyDeviceToHost, s));
+            CARMA_CUDA(cudaStreamSynchronize(s));
+            for (int f = 0; f < CARMA_FAMILIES; ++f)
+                if (h->model[f].present) mmas += (h->last_counts[f] + 127ull) / 128ull * mmas_per_tile(h->model[f].dev);
+        } else if (default_family >= 0 && default_family < CARMA_FAMILIES && h->model[default_family].present) {
+            mmas = (q + 127) / 128 * mmas_per_tile(h->model[default_family].dev);
+        }
+        h->last_mmas = mmas;
+    });
+}
+
+carma_status carma_nn_predict(carma_nn* h, const carma_feature_row* rows, const int8_t* family,
+                              int32_t default_family, uint64_t q, int32_t* bucket_out, uint64_t* bytes_out) {
+    return predict_host(h, rows, sizeof(carma_feature_row), CARMA_ROWS_FEATURES, family, default_family, q,
+                        bucket_out, bytes_out);
+}
+
+carma_status carma_nn_predict_bitpacked(carma_nn* hh, const uint32_t* words, const carma_bit_schema* schema,
+                                        uint64_t q, int32_t* bucket_out, uint64_t* bytes_out) {
+    const carma_status st = carma_nn_set_bit_schema(hh, schema);
+    if (st != CARMA_OK) return st;
+    return predict_host(hh, words, 4ull * schema->words_per_row, CARMA_ROWS_BITPACKED, nullptr, 0, q, bucket_out,
+                        bytes_out, 8);
+}
+
+carma_status carma_nn_last_timing(carma_nn* hh, double* kernel_ms, double* call_ms, uint64_t* launches,
+                                  uint64_t* mmas) {
+    return guarded([&] {
+        NnHandle* h = reinterpret_cast<NnHandle*>(hh);
+        if (!h) throw InvalidArg("null handle");
+        DeviceGuard g(h->device);
+        float a = 0.f, b = 0.f;
+        if (h->timed) {
+            CARMA_CUDA(cudaEventSynchronize(h->ev[2]));
+            CARMA_CUDA(cudaEventElapsedTime(&a, h->ev[1], h->ev[2]));
+            CARMA_CUDA(cudaEventElapsedTime(&b, h->ev[0], h->ev[2]));
+        }
+        if (kernel_ms) *kernel_ms = a;
+        if (call_ms) *call_ms = b;
+        if (launches) *launches = h->last_launches;
+        if (mmas) *mmas = h->last_mmas;
+    });
+}
+
+}  // extern "C"

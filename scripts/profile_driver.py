@@ -71,6 +71,28 @@ def knn(args):
               flush=True)
 
 
+def nn(args):
+    """The neural GPUMemNet ensemble (carma_nn_*) over the bench's bit-packed
+    CNN + Transformer rows."""
+    import torch
+    from paper_2508_19073_b200 import gpumemnet as gm
+    ds = [cb.generate_synthetic_dataset(f, args.rows // 2, s) for f, s in ((1, 2024), (2, 2025))]
+    rows = np.concatenate([d.rows for d in ds])
+    fam = np.concatenate([np.full(args.rows // 2, 1, np.int8), np.full(args.rows // 2, 2, np.int8)])
+    net = gm.GpuMemNet(0)
+    models = gm.load_default_models()
+    for f in (1, 2):
+        net.set_model(models[f])
+    words, schema = cb.pack_features_bits(rows, fam)
+    net.set_bit_schema(schema)
+    d_rows = torch.from_numpy(words.view(np.uint8)).cuda()
+    b = torch.empty(len(rows), dtype=torch.int32, device="cuda")
+    by = torch.empty(len(rows), dtype=torch.int64, device="cuda")
+    for _ in range(args.reps):
+        net.predict_device(d_rows, abi.ROWS_BITPACKED, len(rows), b, by)
+        print(f"nn {len(rows)} rows: {net.last_timing()}", flush=True)
+
+
 def fused(args):
     import ctypes
     m = cb.materialize_trace(cb.generate_uniform_trace(args.tasks, 3.0, 7))
@@ -115,7 +137,7 @@ def scoring(args):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=("replay", "knn", "fused", "scoring"))
+    ap.add_argument("what", choices=("replay", "knn", "fused", "scoring", "nn"))
     ap.add_argument("--tasks", type=int, default=1_000_000)
     ap.add_argument("--traces", type=int, default=20000)
     ap.add_argument("--policies", default="exclusive,rr,magm,lug")
@@ -123,4 +145,4 @@ if __name__ == "__main__":
     ap.add_argument("--format", choices=("rows", "bitpacked"), default="bitpacked")
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
-    {"replay": replay, "knn": knn, "fused": fused, "scoring": scoring}[a.what](a)
+    {"replay": replay, "knn": knn, "fused": fused, "scoring": scoring, "nn": nn}[a.what](a)

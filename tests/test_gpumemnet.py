@@ -1,0 +1,248 @@
+"""Neural GPUMemNet ensemble (carma_nn_*): the oracle pinned
+to the torch model that defines the weights (CPU), and the tcgen05 kernel
+against the oracle (GPU).
+
+Tolerances (BASELINE.json north_star): logits within 1e-3 relative —
+written here as |gpu - oracle| <= 1e-3 * max(1, |oracle|) — and identical
+bins wherever the oracle's top-2 ensemble-probability margin exceeds 1e-3.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2508_19073_b200 as cb
+from paper_2508_19073_b200 import abi
+from paper_2508_19073_b200 import gpumemnet as gm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden", "gpumemnet.npz")
+TOL = 1e-3
+
+
+def _oracle():
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import gpumemnet_oracle
+    return gpumemnet_oracle
+
+
+@pytest.fixture(scope="module")
+def models():
+    m = gm.load_default_models()
+    assert set(m) == {0, 1, 2}
+    return m
+
+
+def _golden(name):
+    z = np.load(GOLDEN)
+    rows = z[f"{name}_rows"].reshape(-1).view(abi.feature_row_dtype)
+    return rows, z[f"{name}_raw"], z[f"{name}_logits"], z[f"{name}_labels"]
+
+
+def _margin(probs):
+    s = np.sort(probs, axis=1)
+    return s[:, -1] - s[:, -2]
+
+
+def _close(a, b, tol=TOL):
+    return np.abs(a - b) <= tol * np.maximum(1.0, np.abs(b))
+
+
+# ------------------------------------------------------------------ CPU
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_oracle_matches_torch_golden(models, fam):
+    orc = _oracle()
+    m = models[fam]
+    rows, raw, logits, labels = _golden(gm.FAMILY_NAMES[fam])
+    assert np.array_equal(cb.scalar_features(rows), raw)
+    ol, op, ob, oby = orc.forward(m.spec()[0], m.params, raw)
+    # golden logits are the torch fp64 forward stored as fp32
+    assert np.all(np.abs(ol - logits) <= 1e-6 * np.maximum(1.0, np.abs(logits)))
+    assert np.all((ob >= 0) & (ob < m.classes))
+    assert np.array_equal(oby, (ob.astype(np.uint64) + 1) * np.uint64(m.bucket_range))
+    assert np.allclose(op.sum(axis=1), 1.0)
+    # the trained ensembles are useful estimators on fresh rows
+    assert (ob == np.minimum(labels, m.classes - 1)).mean() > 0.9
+
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_param_layout(models, fam):
+    m = models[fam]
+    assert gm.param_count(m) == len(m.params)
+    assert 1 <= m.members <= abi.NN_MAX_MEMBERS
+    assert all(1 <= d <= abi.NN_MAX_DEPTH for d in m.depth)
+    assert m.classes == (41 if fam == 0 else 6)
+    assert m.holdout_accuracy > 0.95
+    orc = _oracle()
+    assert len(orc.unpack_params(m.spec()[0], m.params)) == m.members
+
+
+def test_bf16_rounding_is_nearest_even():
+    orc = _oracle()
+    x = np.array([1.0, 1.00390625, 1.01171875, -3.3, 0.0, 1e-30], np.float32)
+    import torch
+    ref = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(orc.bf16_round(x), ref)
+
+
+# ------------------------------------------------------------------ GPU
+
+def _predict_device(net, rows, fmt, q, family=None, default_family=0):
+    import torch
+    raw = torch.from_numpy(np.ascontiguousarray(rows).view(np.uint8).reshape(-1)).cuda()
+    fam = None if family is None else torch.from_numpy(np.ascontiguousarray(family, np.int8)).cuda()
+    b = torch.empty(q, dtype=torch.int32, device="cuda")
+    by = torch.empty(q, dtype=torch.int64, device="cuda")
+    pr = torch.full((q, abi.NN_MAX_CLASSES), float("nan"), dtype=torch.float32, device="cuda")
+    lg = torch.full((q, abi.NN_MAX_MEMBERS, abi.NN_MAX_CLASSES), float("nan"), dtype=torch.float32, device="cuda")
+    net.predict_device(raw, fmt, q, b, by, family=fam, default_family=default_family, probs=pr, logits=lg)
+    torch.cuda.synchronize()
+    return b.cpu().numpy(), by.cpu().numpy().view(np.uint64), pr.cpu().numpy(), lg.cpu().numpy()
+
+
+def _check(m, raw, b, by, pr, lg):
+    orc = _oracle()
+    ol, op, ob, oby = orc.forward(m.spec()[0], m.params, raw)
+    E, C = m.members, m.classes
+    assert np.all(_close(lg[:, :E, :C], ol)), np.max(np.abs(lg[:, :E, :C] - ol))
+    assert np.all(_close(pr[:, :C], op))
+    sure = _margin(op) > TOL
+    assert np.array_equal(b[sure], ob[sure])
+    assert np.array_equal(by[sure], oby[sure])
+    assert np.array_equal(by, (b.astype(np.uint64) + 1) * np.uint64(m.bucket_range))
+    return float(np.max(np.abs(lg[:, :E, :C] - ol) / np.maximum(1.0, np.abs(ol))))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_kernel_matches_oracle(gpu, models, fam):
+    m = models[fam]
+    net = gm.GpuMemNet(gpu)
+    net.set_model(m)
+    ds = cb.generate_synthetic_dataset(fam, 3000, 777 + fam)
+    raw = cb.scalar_features(ds.rows)
+    for fmt, rows in ((abi.ROWS_FEATURES, ds.rows), (abi.ROWS_SCALAR, raw)):
+        b, by, pr, lg = _predict_device(net, rows, fmt, len(ds.rows), default_family=fam)
+        err = _check(m, raw, b, by, pr, lg)
+        assert err < 1e-4  # the hi/lo split keeps ~2^-17 relative per layer
+    t = net.last_timing()
+    assert t["launches"] >= 1 and t["mmas"] > 0
+    # host-buffer API: same bins
+    hb, hby = net.predict(ds.rows, default_family=fam)
+    assert np.array_equal(hb, b) and np.array_equal(hby, by)
+    net.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_kernel_matches_golden(gpu, models, fam):
+    m = models[fam]
+    rows, raw, logits, _ = _golden(gm.FAMILY_NAMES[fam])
+    net = gm.GpuMemNet(gpu)
+    net.set_model(m)
+    b, by, pr, lg = _predict_device(net, rows, abi.ROWS_FEATURES, len(rows), default_family=fam)
+    assert np.all(_close(lg[:, : m.members, : m.classes], logits))
+    net.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("q", [1, 2, 127, 128, 129, 1000, 100_003])
+def test_ragged_batches(gpu, models, q):
+    m = models[1]
+    net = gm.GpuMemNet(gpu)
+    net.set_model(m)
+    ds = cb.generate_synthetic_dataset(1, q, 99 + q)
+    raw = cb.scalar_features(ds.rows)
+    b, by, pr, lg = _predict_device(net, ds.rows, abi.ROWS_FEATURES, q, default_family=1)
+    _check(m, raw, b, by, pr, lg)
+    net.close()
+
+
+@pytest.mark.gpu
+def test_mixed_families_route_by_row(gpu, models):
+    """Packed / bit-packed rows carry their family: one call routes CNN, TF and
+    MLP rows to their own ensembles; a family without a model -> no estimate."""
+    net = gm.GpuMemNet(gpu)
+    for f in (0, 1):
+        net.set_model(models[f])  # no Transformer model installed
+    parts = [cb.generate_synthetic_dataset(f, n, 50 + f) for f, n in ((0, 700), (1, 1300), (2, 500))]
+    rows = np.concatenate([p.rows for p in parts])
+    fams = np.concatenate([np.full(len(p.rows), p.family, np.int8) for p in parts])
+    order = np.random.default_rng(3).permutation(len(rows))
+    rows, fams = rows[order], fams[order]
+    raw = cb.scalar_features(rows)
+    q = len(rows)
+    outs = []
+    packed, table = cb.pack_features(rows, fams)
+    net.set_act_table(table)
+    outs.append(_predict_device(net, packed, abi.ROWS_PACKED, q))
+    words, schema = cb.pack_features_bits(rows, fams)
+    net.set_bit_schema(schema)
+    outs.append(_predict_device(net, words, abi.ROWS_BITPACKED, q))
+    outs.append(_predict_device(net, rows, abi.ROWS_FEATURES, q, family=fams))
+    for b, by, pr, lg in outs:
+        assert np.array_equal(b, outs[0][0]) and np.array_equal(by, outs[0][1])
+        miss = fams == 2
+        assert np.all(b[miss] == -1) and np.all(by[miss] == np.uint64(0xFFFFFFFFFFFFFFFF))
+        for f in (0, 1):
+            sel = fams == f
+            _check(models[f], raw[sel], b[sel], by[sel], pr[sel], lg[sel])
+    hb, hby = net.predict_bitpacked(words, schema, q)
+    assert np.array_equal(hb, outs[0][0]) and np.array_equal(hby, outs[0][1])
+    net.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(8, 8, 48), (1, 1, 2), (3, 5, 17), (8, 1, 8)],
+                         ids=["E8-L8-C48", "E1-L1-C2", "E3-L5-C17", "E8-L1-C8"])
+def test_extreme_shapes_random_weights(gpu, shape):
+    """Random models at the limits of the spec: 8 members x 8 layers x 48
+    bins (4 head passes), a single 1-layer member, odd widths."""
+    E, L, C = shape
+    rng = np.random.default_rng(E * 100 + L * 10 + C)
+    depth = [int(rng.integers(1, L + 1)) if e else L for e in range(E)]
+    width = [[int(rng.integers(1, 9)) for _ in range(d)] for d in depth]
+    m = gm.NnModel(0, abi.GiB, C, depth, width, rng.normal(0, 1, 19).astype(np.float32) * 0.1,
+                   np.full(19, 0.5, np.float32), np.zeros(1, np.float32))
+    n = gm.param_count(m)
+    m.params = (rng.normal(0, 0.6, n)).astype(np.float32)
+    net = gm.GpuMemNet(gpu)
+    net.set_model(m)
+    ds = cb.generate_synthetic_dataset(0, 2000, 5)
+    raw = cb.scalar_features(ds.rows)
+    b, by, pr, lg = _predict_device(net, raw, abi.ROWS_SCALAR, len(raw), default_family=0)
+    _check(m, raw, b, by, pr, lg)
+    net.close()
+
+
+@pytest.mark.gpu
+def test_large_batch_host_api(gpu, models):
+    """1M rows through the chunked host API equal the device call."""
+    import torch
+    m = models[2]
+    net = gm.GpuMemNet(gpu)
+    net.set_model(m)
+    base = cb.generate_synthetic_dataset(2, 1 << 16, 11)
+    rows = np.tile(base.rows, 16)
+    hb, hby = net.predict(rows, default_family=2)
+    db, dby, _, _ = _predict_device(net, base.rows, abi.ROWS_FEATURES, len(base.rows), default_family=2)
+    assert np.array_equal(hb, np.tile(db, 16)) and np.array_equal(hby, np.tile(dby, 16))
+    torch.cuda.synchronize()
+    net.close()
+
+
+@pytest.mark.gpu
+def test_invalid_models_rejected(gpu, models):
+    net = gm.GpuMemNet(gpu)
+    m = models[1]
+    bad = gm.NnModel(1, m.bucket_range, 49, m.depth, m.width, m.shift, m.scale, m.params)
+    with pytest.raises(abi.CarmaError):
+        net.set_model(bad)
+    short = gm.NnModel(1, m.bucket_range, m.classes, m.depth, m.width, m.shift, m.scale, m.params[:-1])
+    with pytest.raises(abi.CarmaError):
+        net.set_model(short)
+    with pytest.raises(abi.CarmaError):  # no model installed yet
+        net.predict(cb.generate_synthetic_dataset(1, 4, 1).rows, default_family=1)
+    net.close()
