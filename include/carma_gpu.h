@@ -223,8 +223,8 @@ carma_status carma_knn_last_timing(carma_knn* h, double* search_ms, double* pipe
  * per-family bank and the same FamilyMismatch convention.
  *
  * Input transform per feature d of scalar_features (estimators.cpp:317-342),
- * computed in fp64 and rounded to fp32:  t_d = log1p(max(raw_d, 0)) if bit d
- * of log_mask is set, else raw_d;  z_d = (t_d - shift_d) * scale_d  (fp32).
+ * in fp32 on x_d = fp32(raw_d):  t_d = log1p(max(x_d, 0)) if bit d of
+ * log_mask is set, else x_d;  z_d = (t_d - shift_d) * scale_d.
  * Weights are bf16 values (rounded to nearest-even on install); biases,
  * activations, logits and probabilities are fp32. */
 #define CARMA_NN_MAX_MEMBERS 8

@@ -160,7 +160,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void group_bar(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
+__device__ __forceinline__ void group_bar(int g) { asm volatile("bar.sync %0, 256;" ::"r"(g + 1) : "memory"); }
 
 // 32 lanes x 32 bit, 8 consecutive columns per thread. The registers are
 // written asynchronously: tmem_wait8 (tcgen05.wait::ld) must run before any
@@ -178,28 +178,34 @@ __device__ __forceinline__ void tmem_wait8(uint32_t (&r)[8]) {
                  : "memory");
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);  // .x = a (lower address = lower K)
-    return *reinterpret_cast<const uint32_t*>(&v);
+// Two fp32 -> packed bf16 pair (round to nearest even): `lo` in the low half
+// (the lower K index), one F2FP instruction.
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
 }
 
 // Splits 8 consecutive activations into kSplit bf16 parts and stores part j
-// at byte offset `off` of A tile j (tiles kATile bytes apart from `a`).
+// at byte offset `off` of A tile j (tiles kATile bytes apart from `a`). The
+// parts are peeled pairwise: one F2FP, the two bf16 values back as fp32 by
+// bit moves, two exact subtractions.
 __device__ __forceinline__ void store_split8(uint8_t* a, uint32_t off, const float (&h)[8]) {
     float rem[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) rem[i] = h[i];
 #pragma unroll
     for (int j = 0; j < kSplit; ++j) {
-        float part[8];
+        uint32_t w[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            part[i] = __bfloat162float(__float2bfloat16_rn(rem[i]));
-            rem[i] = __fsub_rn(rem[i], part[i]);  // exact
+        for (int i = 0; i < 4; ++i) {
+            w[i] = cvt_bf16x2(rem[2 * i], rem[2 * i + 1]);
+            if (j + 1 < kSplit) {
+                rem[2 * i] = __fsub_rn(rem[2 * i], __uint_as_float(w[i] << 16));
+                rem[2 * i + 1] = __fsub_rn(rem[2 * i + 1], __uint_as_float(w[i] & 0xffff0000u));
+            }
         }
-        *reinterpret_cast<uint4*>(a + j * kATile + off) = make_uint4(
-            pack_bf16(part[0], part[1]), pack_bf16(part[2], part[3]), pack_bf16(part[4], part[5]),
-            pack_bf16(part[6], part[7]));
+        *reinterpret_cast<uint4*>(a + j * kATile + off) = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -222,15 +228,48 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a, uint32_
 
 // ------------------------------------------------------------- the ensemble
 
+// z for the 8 features of K chunk kc (zeros past feature 18).
+template <int KC, class P>
+__device__ __forceinline__ void transform_chunk(const P& p, const double (&raw)[kFeatureDims], float (&z)[8]) {
+    const NnModelDev& m = p.m;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        constexpr int d0 = KC * 8;
+        const int d = d0 + j;
+        if (d < kFeatureDims) {
+            const float x = __double2float_rn(raw[d]);
+            const float t = ((m.log_mask >> d) & 1u) ? log1pf(fmaxf(x, 0.f)) : x;
+            z[j] = __fmul_rn(__fsub_rn(t, m.shift[d]), m.scale[d]);
+        } else {
+            z[j] = 0.f;
+        }
+    }
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t addr, const float (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+                 : "memory");
+}
+
+// One warpgroup pair per 128-row tile: 256 threads, thread (half h, row r).
+// Both halves' warps w and w + 4 reach the same TMEM lanes (32 (w % 4) ..),
+// so they split the columns: half h owns hidden columns 32h..32h+31 (members
+// 4h..4h+3), every other member of the head, and K chunks {0, 3} / {1, 2} of
+// the input features. Twice the warps per tile of a one-thread-per-row split,
+// with the same shared memory and TMEM.
 template <int FMT, int G, int CP, bool DIAG>
-__global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant__ NnParams p) {
+__global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant__ NnParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const NnModelDev& m = p.m;
     const int tid = threadIdx.x;
-    const int g = tid >> 7;
+    const int g = tid >> 8;
+    const int h = (tid >> 7) & 1;
     const int r = tid & 127;
     const int warp = tid >> 5;
-    uint8_t* a_t = smem + m.smem_blob + g * (kSplit * kATile);  // this warpgroup's A tiles
+    uint8_t* a_t = smem + m.smem_blob + g * (kSplit * kATile);  // this group's A tiles
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + m.smem_blob + G * (kSplit * kATile));
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + G);
 
@@ -238,7 +277,7 @@ __global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant_
     {
         const uint4* src = reinterpret_cast<const uint4*>(m.blob);
         uint4* dst = reinterpret_cast<uint4*>(smem);
-        for (uint32_t i = tid; i < m.blob_bytes / 16; i += G * 128) dst[i] = __ldg(src + i);
+        for (uint32_t i = tid; i < m.blob_bytes / 16; i += G * 256) dst[i] = __ldg(src + i);
     }
     if (tid == 0) {
         for (int i = 0; i < G; ++i)
@@ -255,7 +294,7 @@ __global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant_
     fence_before();
     __syncthreads();
     fence_after();
-    const uint32_t tmem = *tmem_slot + static_cast<uint32_t>(g * 128);        // this warpgroup's columns
+    const uint32_t tmem = *tmem_slot + static_cast<uint32_t>(g * 128);                // this group's columns
     const uint32_t tmem_row = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);  // this warp's lanes
 
     const float* bias = reinterpret_cast<const float*>(smem + m.off_bias);
@@ -269,7 +308,7 @@ __global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant_
     }
     const uint64_t tiles = (n + kTileRows - 1) / kTileRows;
     uint32_t phase = 0;
-    const bool issuer = r == 0;
+    const bool issuer = tid == g * 256;
 
     for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * G + g; tile < tiles;
          tile += static_cast<uint64_t>(gridDim.x) * G) {
@@ -277,26 +316,35 @@ __global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant_
         const bool valid = i < n;
         const uint64_t row = valid ? (p.perm ? static_cast<uint64_t>(p.perm[base + i]) : base + i) : 0;
 
-        // ---- features -> z (fp32) -> layer-0 A tile (K 0..31)
+        // ---- features -> z (fp32) -> layer-0 A tile (K 0..31): half 0 writes
+        // chunks 0 and 3, half 1 chunks 1 and 2 (7 log1p features each)
         {
-            float z[kK0];
+            double raw[kFeatureDims];
+            if (valid) load_raw<FMT>(p, row, raw);
+            else
 #pragma unroll
-            for (int d = 0; d < kK0; ++d) z[d] = 0.f;
-            if (valid) {
-                double raw[kFeatureDims];
-                load_raw<FMT>(p, row, raw);
+                for (int d = 0; d < kFeatureDims; ++d) raw[d] = 0.0;
+            float z[8];
+            if (h == 0) {
+                transform_chunk<0>(p, raw, z);
+                if (!valid)
 #pragma unroll
-                for (int d = 0; d < kFeatureDims; ++d) {
-                    const double t = ((m.log_mask >> d) & 1u) ? log1p(fmax(raw[d], 0.0)) : raw[d];
-                    z[d] = __fmul_rn(__fsub_rn(__double2float_rn(t), m.shift[d]), m.scale[d]);
-                }
-            }
+                    for (int j = 0; j < 8; ++j) z[j] = 0.f;
+                store_split8(a_t, a_off(r, 0, 1024u), z);
 #pragma unroll
-            for (int kc = 0; kc < kK0 / 8; ++kc) {
-                float h[8];
+                for (int j = 0; j < 8; ++j) z[j] = 0.f;
+                store_split8(a_t, a_off(r, 3, 1024u), z);
+            } else {
+                transform_chunk<1>(p, raw, z);
+                if (!valid)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) h[j] = z[kc * 8 + j];
-                store_split8(a_t, a_off(r, kc, 1024u), h);
+                    for (int j = 0; j < 8; ++j) z[j] = 0.f;
+                store_split8(a_t, a_off(r, 1, 1024u), z);
+                transform_chunk<2>(p, raw, z);
+                if (!valid)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) z[j] = 0.f;
+                store_split8(a_t, a_off(r, 2, 1024u), z);
             }
         }
         fence_async_smem();
@@ -313,22 +361,21 @@ __global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant_
 
         // ---- hidden layers: epilogue of layer l-1 feeds the MMAs of layer l
         for (uint32_t l = 1; l <= m.depth; ++l) {
-            const float* b = bias + (l - 1) * kHidden;
+            const float* b = bias + (l - 1) * kHidden + h * 32;
+            uint32_t v[4][8];
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                uint32_t v[4][8];
+            for (int c = 0; c < 4; ++c) tmem_ld8(tmem_row + h * 32 + c * 8, v[c]);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld8(tmem_row + half * 32 + c * 8, v[c]);
+            for (int c = 0; c < 4; ++c) tmem_wait8(v[c]);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_wait8(v[c]);
+            for (int c = 0; c < 4; ++c) {
+                const float4 b0 = reinterpret_cast<const float4*>(b + c * 8)[0];
+                const float4 b1 = reinterpret_cast<const float4*>(b + c * 8)[1];
+                const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                float x[8];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    float h[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        h[j] = fmaxf(__fadd_rn(__uint_as_float(v[c][j]), b[half * 32 + c * 8 + j]), 0.f);
-                    store_split8(a_t, a_off(r, half * 4 + c, 1024u), h);
-                }
+                for (int j = 0; j < 8; ++j) x[j] = fmaxf(__fadd_rn(__uint_as_float(v[c][j]), bb[j]), 0.f);
+                store_split8(a_t, a_off(r, h * 4 + c, 1024u), x);
             }
             fence_async_smem();
             fence_before();
@@ -345,7 +392,7 @@ __global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant_
             fence_after();
         }
 
-        // ---- head passes: logits, softmax per member, mean over members
+        // ---- head passes: logits, softmax per member, partial means per half
         float pm[CP];
 #pragma unroll
         for (int c = 0; c < CP; ++c) pm[c] = 0.f;
@@ -365,7 +412,7 @@ __global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant_
             fence_after();
             const uint32_t m0 = ps * m.mpp;
             const uint32_t m1 = min(m.members, m0 + m.mpp);
-            for (uint32_t mem = m0; mem < m1; ++mem) {
+            for (uint32_t mem = m0 + h; mem < m1; mem += 2) {
                 const uint32_t col = (mem - m0) * m.cp;
                 uint32_t v[CP / 8][8];
 #pragma unroll
@@ -394,38 +441,64 @@ __global__ void __launch_bounds__(G * 128, 1) nn_ensemble(const __grid_constant_
 #pragma unroll
                 for (int c = 0; c < CP; ++c) {
                     if (c < static_cast<int>(m.classes)) {
-                        lg[c] = expf(__fsub_rn(lg[c], mx));
+                        lg[c] = __expf(__fsub_rn(lg[c], mx));
                         s = __fadd_rn(s, lg[c]);
                     }
                 }
+                const float inv_s = __frcp_rn(s);
 #pragma unroll
                 for (int c = 0; c < CP; ++c)
-                    if (c < static_cast<int>(m.classes)) pm[c] = __fadd_rn(pm[c], __fdiv_rn(lg[c], s));
+                    if (c < static_cast<int>(m.classes)) pm[c] = __fadd_rn(pm[c], __fmul_rn(lg[c], inv_s));
             }
         }
-        // The next tile's first MMA overwrites TMEM and the A tiles: its
-        // fence_before + group barrier orders it after these reads.
-        if (valid) {
-            const float inv_e = 1.0f / static_cast<float>(m.members);
-            int best = 0;
-            float bv = -1.f;
+        // ---- combine the halves through TMEM: half 1 parks its partial sums
+        // in the group's first columns once every read of the head is done;
+        // half 0 adds them (members in ascending order within each half).
+        fence_before();
+        group_bar(g);
+        if (h == 1) {
 #pragma unroll
-            for (int c = 0; c < CP; ++c) {
-                if (c < static_cast<int>(m.classes)) {
-                    pm[c] = __fmul_rn(pm[c], inv_e);
-                    if (pm[c] >= bv) {  // ties to the larger bin
-                        bv = pm[c];
-                        best = c;
+            for (int c = 0; c < CP / 8; ++c) {
+                float w[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) w[j] = pm[c * 8 + j];
+                tmem_st8(tmem_row + c * 8, w);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        fence_before();
+        group_bar(g);
+        fence_after();
+        if (h == 0) {
+            uint32_t v[CP / 8][8];
+#pragma unroll
+            for (int c = 0; c < CP / 8; ++c) tmem_ld8(tmem_row + c * 8, v[c]);
+#pragma unroll
+            for (int c = 0; c < CP / 8; ++c) tmem_wait8(v[c]);
+            // The next tile's first MMA overwrites TMEM and the A tiles: its
+            // fence_before + group barrier orders it after these reads.
+            if (valid) {
+                const float inv_e = 1.0f / static_cast<float>(m.members);
+                int best = 0;
+                float bv = -1.f;
+#pragma unroll
+                for (int c = 0; c < CP; ++c) {
+                    if (c < static_cast<int>(m.classes)) {
+                        pm[c] = __fmul_rn(__fadd_rn(pm[c], __uint_as_float(v[c / 8][c % 8])), inv_e);
+                        if (pm[c] >= bv) {  // ties to the larger bin
+                            bv = pm[c];
+                            best = c;
+                        }
                     }
                 }
-            }
-            p.bucket[row] = best;
-            p.bytes[row] = static_cast<uint64_t>(best + 1) * m.bucket_range;
-            if (DIAG && p.probs) {
-                float* out = p.probs + row * CARMA_NN_MAX_CLASSES;
+                p.bucket[row] = best;
+                p.bytes[row] = static_cast<uint64_t>(best + 1) * m.bucket_range;
+                if (DIAG && p.probs) {
+                    float* out = p.probs + row * CARMA_NN_MAX_CLASSES;
 #pragma unroll
-                for (int c = 0; c < CP; ++c)
-                    if (c < static_cast<int>(m.classes)) out[c] = pm[c];
+                    for (int c = 0; c < CP; ++c)
+                        if (c < static_cast<int>(m.classes)) out[c] = pm[c];
+                }
             }
         }
     }
@@ -674,7 +747,7 @@ void launch_ensemble_t(const NnParams& p, int device, cudaStream_t s) {
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(kSmemLimit));
     CARMA_CUDA(attr);
-    nn_ensemble<FMT, G, CP, DIAG><<<sm_count(device), G * 128, smem, s>>>(p);
+    nn_ensemble<FMT, G, CP, DIAG><<<sm_count(device), G * 256, smem, s>>>(p);
     CARMA_CUDA(cudaGetLastError());
 }
 
@@ -683,15 +756,16 @@ void launch_ensemble_t(const NnParams& p, int device, cudaStream_t s) {
 template <int FMT, bool DIAG>
 void launch_ensemble(const NnParams& p, int device, cudaStream_t s) {
     const uint32_t room = kSmemLimit - p.m.smem_blob - 64;
-    const int g = static_cast<int>(std::min<uint32_t>(4, room / (kSplit * kATile)));
+    const int g = static_cast<int>(std::min<uint32_t>(3, room / (kSplit * kATile)));
     if (g < 1) throw Unsupported("model too large for shared memory");
     if (p.m.cp <= 8) {
-        if (g >= 4) launch_ensemble_t<FMT, 4, 8, DIAG>(p, device, s);
-        else if (g == 3) launch_ensemble_t<FMT, 3, 8, DIAG>(p, device, s);
-        else launch_ensemble_t<FMT, 2, 8, DIAG>(p, device, s);
+        if (g >= 3) launch_ensemble_t<FMT, 3, 8, DIAG>(p, device, s);
+        else if (g == 2) launch_ensemble_t<FMT, 2, 8, DIAG>(p, device, s);
+        else launch_ensemble_t<FMT, 1, 8, DIAG>(p, device, s);
     } else {
         if (g >= 3) launch_ensemble_t<FMT, 3, 48, DIAG>(p, device, s);
-        else launch_ensemble_t<FMT, 2, 48, DIAG>(p, device, s);
+        else if (g == 2) launch_ensemble_t<FMT, 2, 48, DIAG>(p, device, s);
+        else launch_ensemble_t<FMT, 1, 48, DIAG>(p, device, s);
     }
 }
 

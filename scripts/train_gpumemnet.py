@@ -45,10 +45,9 @@ def member_widths(depth: int) -> list:
 
 def features(rows: np.ndarray, shift=None, scale=None):
     raw = cb.scalar_features(rows)
-    t = raw.copy()
+    t32 = raw.astype(np.float32)  # the transform of carma_gpu.h, in fp32
     for d in gm.LOG_DIMS:
-        t[:, d] = np.log1p(np.maximum(raw[:, d], 0.0))
-    t32 = t.astype(np.float32)
+        t32[:, d] = np.log1p(np.maximum(t32[:, d], np.float32(0)), dtype=np.float32)
     if shift is None:
         shift = t32.mean(axis=0).astype(np.float32)
         sd = t32.std(axis=0).astype(np.float32)
