@@ -60,8 +60,6 @@ namespace {
 constexpr int kTileRows = 128;
 constexpr int kHidden = 64;           // 8 members x 8 neurons
 constexpr int kK0 = 32;               // 19 features padded to two K=16 steps
-constexpr uint32_t kW0Bytes = kHidden * kK0 * 2;    // 4 KB
-constexpr uint32_t kWBytes = kHidden * kHidden * 2; // 8 KB
 constexpr uint32_t kATile = kTileRows * kHidden * 2; // 16 KB per activation part
 constexpr int kSplit = 3;                             // bf16 parts per activation
 constexpr int kMaxPasses = 8;
@@ -80,6 +78,11 @@ struct NnModelDev {
     uint32_t passes;
     uint32_t pass_n[kMaxPasses];     // N of each head pass (multiple of 16)
     uint32_t pass_row0[kMaxPasses];  // first head row of each pass
+    uint32_t alive[CARMA_NN_MAX_DEPTH];      // members with depth > l (members sorted by depth, descending)
+    uint32_t layer_n[CARMA_NN_MAX_DEPTH];    // MMA N of layer l (alive columns, padded to 16)
+    uint32_t layer_k[CARMA_NN_MAX_DEPTH];    // K steps (16) of layer l
+    uint32_t layer_off[CARMA_NN_MAX_DEPTH];  // byte offset of W_l in the blob (SBO = 16 * K_l)
+    uint8_t orig[CARMA_NN_MAX_MEMBERS];      // spec member index of sorted member m
     uint32_t off_head;    // byte offset of the head weights in the blob
     uint32_t off_bias;    // byte offset of the fp32 biases (L x 64, then head rows)
     uint32_t log_mask;
@@ -278,6 +281,10 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
         const uint4* src = reinterpret_cast<const uint4*>(m.blob);
         uint4* dst = reinterpret_cast<uint4*>(smem);
         for (uint32_t i = tid; i < m.blob_bytes / 16; i += G * 256) dst[i] = __ldg(src + i);
+        // A tiles start at zero: columns of absent members are read (times
+        // zero weights) by the head and by K padding, and must be finite.
+        uint4* at = reinterpret_cast<uint4*>(smem + m.smem_blob);
+        for (uint32_t i = tid; i < G * (kSplit * kATile) / 16; i += G * 256) at[i] = make_uint4(0, 0, 0, 0);
     }
     if (tid == 0) {
         for (int i = 0; i < G; ++i)
@@ -352,30 +359,35 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
         group_bar(g);
         if (issuer) {
             fence_after();
-            issue_layer(tmem, s_a, s_blob, 512u, kK0 / 16, idesc_bf16(kHidden));
+            issue_layer(tmem, s_a, s_blob + m.layer_off[0], 256u * m.layer_k[0], m.layer_k[0],
+                        idesc_bf16(m.layer_n[0]));
             mma_commit(mbar + g);
         }
         mbar_wait(mbar + g, phase);
         phase ^= 1u;
         fence_after();
 
-        // ---- hidden layers: epilogue of layer l-1 feeds the MMAs of layer l
+        // ---- hidden layers: epilogue of layer l-1 feeds the MMAs of layer l.
+        // Half h owns members h, h + 2, h + 4, h + 6; only the members still
+        // running (a prefix) are computed and stored — a finished member's
+        // columns keep its last activations for the head.
         for (uint32_t l = 1; l <= m.depth; ++l) {
-            const float* b = bias + (l - 1) * kHidden + h * 32;
-            uint32_t v[4][8];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld8(tmem_row + h * 32 + c * 8, v[c]);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_wait8(v[c]);
-#pragma unroll
+            const uint32_t alive = m.alive[l - 1];
+            const float* b = bias + (l - 1) * kHidden;
+#pragma unroll 1
             for (int c = 0; c < 4; ++c) {
-                const float4 b0 = reinterpret_cast<const float4*>(b + c * 8)[0];
-                const float4 b1 = reinterpret_cast<const float4*>(b + c * 8)[1];
+                const int mem = 2 * c + h;
+                if (mem >= static_cast<int>(alive)) break;
+                uint32_t v[1][8];
+                tmem_ld8(tmem_row + mem * 8, v[0]);
+                tmem_wait8(v[0]);
+                const float4 b0 = reinterpret_cast<const float4*>(b + mem * 8)[0];
+                const float4 b1 = reinterpret_cast<const float4*>(b + mem * 8)[1];
                 const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
                 float x[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) x[j] = fmaxf(__fadd_rn(__uint_as_float(v[c][j]), bb[j]), 0.f);
-                store_split8(a_t, a_off(r, h * 4 + c, 1024u), x);
+                for (int j = 0; j < 8; ++j) x[j] = fmaxf(__fadd_rn(__uint_as_float(v[0][j]), bb[j]), 0.f);
+                store_split8(a_t, a_off(r, mem, 1024u), x);
             }
             fence_async_smem();
             fence_before();
@@ -383,8 +395,8 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
             if (l == m.depth) break;  // the head passes issue from the final activations
             if (issuer) {
                 fence_after();
-                issue_layer(tmem, s_a, s_blob + kW0Bytes + (l - 1) * kWBytes, 1024u, kHidden / 16,
-                            idesc_bf16(kHidden));
+                issue_layer(tmem, s_a, s_blob + m.layer_off[l], 256u * m.layer_k[l], m.layer_k[l],
+                            idesc_bf16(m.layer_n[l]));
                 mma_commit(mbar + g);
             }
             mbar_wait(mbar + g, phase);
@@ -432,7 +444,7 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
                     }
                 }
                 if (DIAG && valid && p.logits) {
-                    float* out = p.logits + (row * CARMA_NN_MAX_MEMBERS + mem) * CARMA_NN_MAX_CLASSES;
+                    float* out = p.logits + (row * CARMA_NN_MAX_MEMBERS + m.orig[mem]) * CARMA_NN_MAX_CLASSES;
 #pragma unroll
                     for (int c = 0; c < CP; ++c)
                         if (c < static_cast<int>(m.classes)) out[c] = lg[c];
@@ -623,31 +635,67 @@ size_t canon(uint32_t row, uint32_t k, uint32_t sbo) {
     return static_cast<size_t>(row >> 3) * sbo + (k >> 3) * 128u + (row & 7u) * 16u + (k & 7u) * 2u;
 }
 
-// Builds the shared-memory image of a model: block-diagonal bf16 weights in
-// their UMMA layouts (identity blocks carry shallow members through the
-// deeper layers), the head passes, and the fp32 biases.
+// Builds the shared-memory image of a model. Members are sorted by depth
+// (descending, stable), so the members still running at layer l are a prefix
+// [0, alive_l): layer l is a block-diagonal GEMM over that prefix only
+// (N = 8 alive_l, K = 8 alive_{l-1}, both padded to 16 with zero weights),
+// and a member that has finished keeps its last activations in its A-tile
+// columns, untouched, until the head reads all of them. Then the head passes
+// and the fp32 biases.
 void build_model(HostNn& hm, int device, const carma_nn_spec& s, const float* params) {
+    const uint32_t E = s.members;
     uint32_t L = 0;
-    for (uint32_t e = 0; e < s.members; ++e) L = std::max(L, s.depth[e]);
+    for (uint32_t e = 0; e < E; ++e) L = std::max(L, s.depth[e]);
+    // spec offsets of each member's parameters
+    std::vector<const float*> mp(E);
+    {
+        const float* pp = params;
+        for (uint32_t e = 0; e < E; ++e) {
+            mp[e] = pp;
+            uint32_t in = kFeatureDims;
+            for (uint32_t l = 0; l < s.depth[e]; ++l) {
+                pp += static_cast<size_t>(s.width[e][l]) * in + s.width[e][l];
+                in = s.width[e][l];
+            }
+            pp += static_cast<size_t>(s.classes) * in + s.classes;
+        }
+    }
+    std::vector<uint32_t> ord(E);
+    for (uint32_t e = 0; e < E; ++e) ord[e] = e;
+    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return s.depth[a] > s.depth[b]; });
+
     const uint32_t cp = (s.classes + 7u) & ~7u;
-    const uint32_t mpp = std::min<uint32_t>(s.members, 128u / cp);
-    const uint32_t passes = (s.members + mpp - 1) / mpp;
+    const uint32_t mpp = std::min<uint32_t>(E, 128u / cp);
+    const uint32_t passes = (E + mpp - 1) / mpp;
     if (passes > static_cast<uint32_t>(kMaxPasses)) throw Unsupported("too many head passes");
+    auto pad16 = [](uint32_t x) { return (x + 15u) & ~15u; };
     NnModelDev d{};
     d.depth = L;
-    d.members = s.members;
+    d.members = E;
     d.classes = s.classes;
     d.cp = cp;
     d.mpp = mpp;
     d.passes = passes;
+    for (uint32_t i = 0; i < E; ++i) d.orig[i] = static_cast<uint8_t>(ord[i]);
+    uint32_t off = 0;
+    for (uint32_t l = 0; l < L; ++l) {
+        uint32_t a = 0;
+        for (uint32_t e = 0; e < E; ++e) a += s.depth[e] > l ? 1u : 0u;
+        d.alive[l] = a;
+        d.layer_n[l] = pad16(8 * a);
+        const uint32_t k = l == 0 ? kK0 : pad16(8 * d.alive[l - 1]);
+        d.layer_k[l] = k / 16;
+        d.layer_off[l] = off;
+        off += d.layer_n[l] * k * 2;
+    }
     uint32_t head_rows = 0;
     for (uint32_t ps = 0; ps < passes; ++ps) {
-        const uint32_t mems = std::min(mpp, s.members - ps * mpp);
+        const uint32_t mems = std::min(mpp, E - ps * mpp);
         d.pass_row0[ps] = head_rows;
-        d.pass_n[ps] = (mems * cp + 15u) & ~15u;
+        d.pass_n[ps] = pad16(mems * cp);
         head_rows += d.pass_n[ps];
     }
-    d.off_head = kW0Bytes + (L - 1) * kWBytes;
+    d.off_head = off;
     d.off_bias = d.off_head + head_rows * 128u;
     d.blob_bytes = (d.off_bias + 4u * (L * kHidden + head_rows) + 15u) & ~15u;
     d.smem_blob = (d.blob_bytes + 1023u) & ~1023u;
@@ -657,35 +705,32 @@ void build_model(HostNn& hm, int device, const carma_nn_spec& s, const float* pa
     std::memcpy(d.scale, s.scale, sizeof(d.scale));
 
     std::vector<uint8_t> blob(d.blob_bytes, 0);
-    auto put = [&](size_t off, float w) {
+    auto put = [&](size_t o, float w) {
         const uint16_t b = bf16_bits(w);
-        std::memcpy(blob.data() + off, &b, 2);
+        std::memcpy(blob.data() + o, &b, 2);
     };
     float* bias = reinterpret_cast<float*>(blob.data() + d.off_bias);
-    const float* pp = params;
-    for (uint32_t e = 0; e < s.members; ++e) {
+    for (uint32_t m = 0; m < E; ++m) {
+        const uint32_t e = ord[m];
+        const float* pp = mp[e];
         uint32_t in = kFeatureDims;
         for (uint32_t l = 0; l < s.depth[e]; ++l) {
             const uint32_t w = s.width[e][l];
-            const size_t base = l == 0 ? 0 : kW0Bytes + (l - 1) * kWBytes;
-            const uint32_t sbo = l == 0 ? 512u : 1024u;
+            const uint32_t sbo = 16u * 16u * d.layer_k[l];  // 8 rows x (K_l * 2 B)
             for (uint32_t o = 0; o < w; ++o)
                 for (uint32_t k = 0; k < in; ++k)
-                    put(base + canon(8 * e + o, l == 0 ? k : 8 * e + k, sbo), pp[o * in + k]);
+                    put(d.layer_off[l] + canon(8 * m + o, l == 0 ? k : 8 * m + k, sbo), pp[o * in + k]);
             pp += static_cast<size_t>(w) * in;
-            for (uint32_t o = 0; o < w; ++o) bias[l * kHidden + 8 * e + o] = pp[o];
+            for (uint32_t o = 0; o < w; ++o) bias[l * kHidden + 8 * m + o] = pp[o];
             pp += w;
             in = w;
         }
-        for (uint32_t l = s.depth[e]; l < L; ++l)  // identity: carry the last activations
-            for (uint32_t o = 0; o < in; ++o) put(kW0Bytes + (l - 1) * kWBytes + canon(8 * e + o, 8 * e + o, 1024u), 1.0f);
-        const uint32_t ps = e / mpp, slot = e % mpp;
+        const uint32_t ps = m / mpp, slot = m % mpp;
         const uint32_t row0 = d.pass_row0[ps] + slot * cp;
         for (uint32_t c = 0; c < s.classes; ++c)
-            for (uint32_t k = 0; k < in; ++k) put(d.off_head + canon(row0 + c, 8 * e + k, 1024u), pp[c * in + k]);
+            for (uint32_t k = 0; k < in; ++k) put(d.off_head + canon(row0 + c, 8 * m + k, 1024u), pp[c * in + k]);
         pp += static_cast<size_t>(s.classes) * in;
         for (uint32_t c = 0; c < s.classes; ++c) bias[L * kHidden + row0 + c] = pp[c];
-        pp += s.classes;
     }
     DeviceGuard gd(device);
     hm.blob.ensure(blob.size());
