@@ -214,14 +214,18 @@ def knn_config(n: int) -> dict:
 def nn_tile_flops(m) -> tuple:
     """(executed tensor-pipe flops per 128-row tile, useful dense flops per row)
     of a GPUMemNet ensemble on the kernel's layout (csrc/cuda/gpumemnet.cu):
-    3 bf16 activation parts x (layer 0: K=32, N=64; L-1 hidden: K=64, N=64;
-    head passes: K=64, N=pass_n), 2*M*N*K flops per MMA (M = 128)."""
+    members sorted by depth, layer l over the running prefix (N = 8 alive_l,
+    K = 8 alive_{l-1}, padded to 16; layer 0 K = 32), the head passes (K = 64),
+    3 bf16 activation parts, 2*M*N*K flops per MMA (M = 128)."""
     L = max(m.depth)
+    alive = [sum(1 for d in m.depth if d > l) for l in range(L)]
+    pad = lambda x: (x + 15) // 16 * 16  # noqa: E731
     cp = (m.classes + 7) // 8 * 8
     mpp = min(m.members, 128 // cp)
     passes = [min(mpp, m.members - p * mpp) for p in range((m.members + mpp - 1) // mpp)]
-    head_n = sum((k * cp + 15) // 16 * 16 for k in passes)
-    executed = 3 * 2 * 128 * (64 * 32 + (L - 1) * 64 * 64 + head_n * 64)
+    head_n = sum(pad(k * cp) for k in passes)
+    mnk = pad(8 * alive[0]) * 32 + sum(pad(8 * alive[l]) * pad(8 * alive[l - 1]) for l in range(1, L))
+    executed = 3 * 2 * 128 * (mnk + head_n * 64)
     useful = 0
     for d, w in zip(m.depth, m.width):
         fan = 19

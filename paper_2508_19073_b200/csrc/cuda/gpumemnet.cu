@@ -160,6 +160,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     }
 }
 
+__device__ __forceinline__ void group_bar(int g);
+__device__ __forceinline__ void fence_after();
+
+// Completion of a group's MMAs: one warp polls the mbarrier, the others sleep
+// in the group's hardware barrier (a polling warp per thread would take issue
+// slots from the other groups' epilogues).
+__device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t phase, bool waiter, int g) {
+    if (waiter) mbar_wait(bar, phase);
+    group_bar(g);
+    fence_after();
+}
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -316,6 +328,7 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
     const uint64_t tiles = (n + kTileRows - 1) / kTileRows;
     uint32_t phase = 0;
     const bool issuer = tid == g * 256;
+    const bool waiter = (tid >> 5) == g * 8;  // the issuer's warp
 
     for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * G + g; tile < tiles;
          tile += static_cast<uint64_t>(gridDim.x) * G) {
@@ -363,9 +376,8 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
                         idesc_bf16(m.layer_n[0]));
             mma_commit(mbar + g);
         }
-        mbar_wait(mbar + g, phase);
+        mma_wait(mbar + g, phase, waiter, g);
         phase ^= 1u;
-        fence_after();
 
         // ---- hidden layers: epilogue of layer l-1 feeds the MMAs of layer l.
         // Half h owns members h, h + 2, h + 4, h + 6; only the members still
@@ -399,9 +411,8 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
                             idesc_bf16(m.layer_n[l]));
                 mma_commit(mbar + g);
             }
-            mbar_wait(mbar + g, phase);
+            mma_wait(mbar + g, phase, waiter, g);
             phase ^= 1u;
-            fence_after();
         }
 
         // ---- head passes: logits, softmax per member, partial means per half
@@ -419,9 +430,8 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
                             idesc_bf16(m.pass_n[ps]));
                 mma_commit(mbar + g);
             }
-            mbar_wait(mbar + g, phase);
+            mma_wait(mbar + g, phase, waiter, g);
             phase ^= 1u;
-            fence_after();
             const uint32_t m0 = ps * m.mpp;
             const uint32_t m1 = min(m.members, m0 + m.mpp);
             for (uint32_t mem = m0 + h; mem < m1; mem += 2) {
@@ -903,9 +913,13 @@ uint64_t run_predict(NnHandle& h, NnHandle::Scratch& sc, const void* rows, int32
     return launches;
 }
 
-// MMAs per 128-row tile of a model: layer 0 (2 K steps), L-1 hidden layers
-// and the head passes (4 K steps each), kSplit MMAs per step.
-uint64_t mmas_per_tile(const NnModelDev& d) { return kSplit * (2 + 4ull * (d.depth - 1) + 4ull * d.passes); }
+// MMAs per 128-row tile of a model: the K steps of every layer and of the
+// head passes (K = 64: 4 steps each), kSplit MMAs per step.
+uint64_t mmas_per_tile(const NnModelDev& d) {
+    uint64_t steps = 4ull * d.passes;
+    for (uint32_t l = 0; l < d.depth; ++l) steps += d.layer_k[l];
+    return kSplit * steps;
+}
 
 void check_ready(NnHandle* h) {
     if (!h) throw InvalidArg("null handle");
