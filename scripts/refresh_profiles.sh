@@ -18,3 +18,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:pick
     -o $OUT/pick_kernel_full -f python scripts/profile_driver.py scoring --reps 2 > $OUT/ncu_pick.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:replay_kernel -c 1 \
     -o $OUT/replay_c5_full -f python scripts/profile_driver.py fused --tasks 100000 --reps 1 > $OUT/ncu_c5.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:nn_ensemble -s 1 -c 1 \
+    -o $OUT/nn_ensemble_full -f python scripts/profile_driver.py nn --rows 16777216 --reps 2 > $OUT/ncu_nn.log 2>&1
