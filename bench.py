@@ -305,6 +305,23 @@ def neural_bench(abi, cb, dev, stream, args, d, words, schema, rows, fam):
         sure = srt[:, -1] - srt[:, -2] > 1e-3
         assert np.array_equal(b_dev[idx][sel][sure], ob[sure]), "neural bins differ from the oracle"
         agree += int(sure.sum())
+    cpu = None
+    if d.rank == 0 and d.n == 1 and not args.skip_cpu:
+        # The reference has no neural estimator: the CPU baseline is the numpy
+        # oracle ("port", fp64 layers, BLAS threads) on a bounded sample.
+        from threadpoolctl import threadpool_info
+        threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
+        ns = 1 << 18
+        sidx = np.concatenate([np.arange(ns // 2), KNN_ROWS_PER_FAMILY + np.arange(ns // 2)])
+        sraw = cb.scalar_features(rows[sidx])
+        t0 = time.perf_counter()
+        for f in (1, 2):
+            sel = fam[sidx] == f
+            gpumemnet_oracle.forward(models[f].spec()[0], models[f].params, sraw[sel])
+        cpu_s = time.perf_counter() - t0
+        cpu = {"value": ns / cpu_s, "unit": "estimates/s", "cores": threads, "kind": "port",
+               "sample": f"first {ns // 2} CNN + first {ns // 2} Transformer rows of the batch through "
+                         "oracle/gpumemnet_oracle.py (numpy; no reference implementation exists)"}
     k_avg = statistics.mean(kernel_ms)
     rows_f = {f: int((fam == f).sum()) for f in (1, 2)}
     executed = sum((rows_f[f] + 127) // 128 * nn_tile_flops(models[f])[0] for f in (1, 2))
@@ -332,6 +349,7 @@ def neural_bench(abi, cb, dev, stream, args, d, words, schema, rows, fam):
                              "ensemble math",
                      "hbm_gbs": hbm_bytes / (k_avg * 1e-3) / 1e9, "hbm_peak_gbs": peaks().get("hbm_gbs"),
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
+        "cpu_baseline": cpu,
         "oracle_agreement_rows": agree,
         "holdout_accuracy": {gm.FAMILY_NAMES[f]: models[f].holdout_accuracy for f in (1, 2)},
     }
