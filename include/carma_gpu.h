@@ -397,6 +397,23 @@ carma_status carma_replay_plan_set_estimates_device(carma_replay_plan* p, const 
 /* Re-uploads the task array (same shape as at creation) from host memory,
  * e.g. the next sweep's traces; pinned host memory copies asynchronously. */
 carma_status carma_replay_plan_upload_tasks(carma_replay_plan* p, const carma_task* tasks);
+/* run_sweep's inputs generated on the device (runner.cpp:213-249 without the
+ * host loop): trace k * n_seeds + i = generate_trace(mix, seeds[i])
+ * (traces.cpp:266-306) materialised (task_from_catalog, traces.cpp:238-254;
+ * ids t000-.. so rank = row) with estimates from table k (n_tables tables of
+ * one u64 per catalog entry, host memory; NULL = no estimate, n_tables = 1):
+ * every estimator persona, learned included, is a function of the catalog
+ * entry. mix: CARMA_MIX_T90 (90 tasks) or CARMA_MIX_T60 (60). jobs index those
+ * traces as in carma_replay_plan_create. Bit-identical to the host generator. */
+carma_status carma_replay_plan_create_generated(int device, const carma_replay_config* configs,
+                                                uint32_t n_configs, int32_t mix, const uint64_t* seeds,
+                                                uint32_t n_seeds, const uint64_t* entry_estimates,
+                                                uint32_t n_tables, const carma_replay_job* jobs,
+                                                uint32_t n_jobs, carma_replay_plan** out);
+/* The catalog entry of every generated task (int32 per task, host buffer). */
+carma_status carma_replay_plan_entries(carma_replay_plan* p, int32_t* entries);
+/* The plan's task array as the replay sees it (host buffer, n_tasks). */
+carma_status carma_replay_plan_tasks(carma_replay_plan* p, carma_task* tasks);
 /* Runs all jobs on the device (inputs resident). stream: cudaStream_t or NULL. */
 carma_status carma_replay_plan_run(carma_replay_plan* p, void* stream);
 /* One timeline row per GPU per sample tick: World::emit_timeline_row

@@ -180,6 +180,10 @@ SIGNATURES = {
     "carma_nn_predict_bitpacked": (c_int, [c_void_p, P, P, c_uint64, P, P]),
     "carma_nn_last_timing": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_uint64),
                                      POINTER(c_uint64)]),
+    "carma_replay_plan_create_generated": (c_int, [c_int, P, c_uint32, c_int32, P, c_uint32, P, c_uint32, P, c_uint32,
+                                                   POINTER(c_void_p)]),
+    "carma_replay_plan_entries": (c_int, [c_void_p, P]),
+    "carma_replay_plan_tasks": (c_int, [c_void_p, P]),
     "carma_knn_train": (c_int, [c_void_p, c_int32, P, P, P, c_uint64, c_uint64, c_uint32, c_uint64, P, P, P, P, P]),
     "carma_host_split_order": (c_int, [c_uint64, c_uint64, P, POINTER(c_uint64)]),
     "carma_replay_plan_log": (c_int, [c_void_p, c_uint32, P, c_uint64, POINTER(c_uint64)]),

@@ -416,6 +416,42 @@ class ReplayPlan:
         self.task_offsets = np.concatenate([[0], np.cumsum(n_t)])
         self.gpu_offsets = np.concatenate([[0], np.cumsum(n_g)])
 
+    @classmethod
+    def generated(cls, configs: np.ndarray, mix: str, seeds, jobs: np.ndarray, tables: Optional[np.ndarray] = None,
+                  device: int = 0) -> "ReplayPlan":
+        """A plan whose traces are generated on the device
+        (carma_replay_plan_create_generated): trace k * len(seeds) + i is
+        generate_trace(mix, seeds[i]) materialised with estimate table k (one
+        u64 per catalog entry; None = no estimate)."""
+        self = cls.__new__(cls)
+        self.configs = np.ascontiguousarray(configs, abi.replay_config_dtype)
+        self.jobs = np.ascontiguousarray(jobs, abi.job_dtype)
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        n_tables = 1 if tables is None else len(tables)
+        tab = None if tables is None else np.ascontiguousarray(tables, np.uint64)
+        rows = 90 if mix == "t90" else 60
+        self.trace_offsets = (np.arange(n_tables * len(seeds) + 1, dtype=np.uint64) * np.uint64(rows))
+        self.tasks = None
+        h = ctypes.c_void_p()
+        check(lib.carma_replay_plan_create_generated(device, ptr(self.configs), len(self.configs), abi.MIX[mix],
+                                                     ptr(seeds), len(seeds), ptr(tab), n_tables, ptr(self.jobs),
+                                                     len(self.jobs), ctypes.byref(h)))
+        self._h = h
+        n_t = np.diff(self.trace_offsets.astype(np.int64))[self.jobs["trace"]]
+        n_g = self.configs["gpu_count"][self.jobs["config"]].astype(np.int64)
+        self.task_offsets = np.concatenate([[0], np.cumsum(n_t)])
+        self.gpu_offsets = np.concatenate([[0], np.cumsum(n_g)])
+        return self
+
+    def device_tasks(self):
+        """(tasks, catalog entries) of a generated plan, read back from the device."""
+        n = int(self.trace_offsets[-1])
+        t = np.zeros(n, abi.task_dtype)
+        e = np.zeros(n, np.int32)
+        check(lib.carma_replay_plan_tasks(self._h, ptr(t)))
+        check(lib.carma_replay_plan_entries(self._h, ptr(e)))
+        return t, e
+
     def set_estimates_device(self, dev_ptr: int) -> None:
         check(lib.carma_replay_plan_set_estimates_device(self._h, dev_ptr))
 
@@ -545,6 +581,17 @@ def provision_estimates(rc: RunConfig, m: Materialized, device: int = 0,
             knn.set_model(fit_knn(fam, rc.estimator_samples, seed, rc.estimator_k))
     _, nbytes = knn.predict(m.features, family=m.family)
     m.tasks["estimate"] = nbytes
+
+
+def entry_estimates(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None) -> np.ndarray:
+    """make_estimate of every catalog entry (one u64 each) under rc's estimator:
+    estimates are functions of the catalog entry, so a generated trace takes
+    its tasks' estimates from this table."""
+    n = lib.carma_host_catalog_size()
+    tr = Trace(np.zeros(n), np.arange(n, dtype=np.int32), np.ones(n, np.uint64))
+    m = materialize_trace(tr)
+    provision_estimates(rc, m, device, knn)
+    return m.tasks["estimate"].copy()
 
 
 def run_simulation(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None):
@@ -741,6 +788,35 @@ def run_sweep(config: SweepConfig, device: int = 0, knn: Optional[GpuKnn] = None
     if own_knn:
         knn = GpuKnn(device)
     task_lists, trace_of, names = [], {}, {}
+    if not base.trace_path and base.mix in ("t90", "t60"):
+        # Traces generated and materialised on the device, straight into the
+        # plan; estimates by catalog entry, one table per (estimator, margin).
+        try:
+            keys = []
+            for c in config.cells:
+                k = (c.policy.estimator, c.policy.safety_margin)
+                if k not in keys:
+                    keys.append(k)
+            tables = np.stack([entry_estimates(dataclasses.replace(base, policy=PolicyConfig(
+                estimator=e, safety_margin=mg)), device, knn) for e, mg in keys])
+            ns = len(config.seeds)
+            j = np.zeros(len(config.cells) * ns, abi.job_dtype)
+            for ci, c in enumerate(config.cells):
+                k = keys.index((c.policy.estimator, c.policy.safety_margin))
+                j["trace"][ci * ns:(ci + 1) * ns] = k * ns + np.arange(ns, dtype=np.uint32)
+                j["config"][ci * ns:(ci + 1) * ns] = ci
+            cfgs = np.concatenate([make_config(c.policy, base.constants, base.mig_instances) for c in config.cells])
+            plan = ReplayPlan.generated(cfgs, base.mix, config.seeds, j, tables, device)
+            try:
+                plan.run()
+                res = plan.results(tasks=False)
+            finally:
+                plan.close()
+        finally:
+            if own_knn:
+                knn.close()
+        names = {seed: f"{base.mix}-seed{seed}" for seed in config.seeds}
+        return _sweep_result(config, res, names)
     try:
         for seed in config.seeds:
             if base.trace_path:
@@ -775,6 +851,10 @@ def run_sweep(config: SweepConfig, device: int = 0, knn: Optional[GpuKnn] = None
     finally:
         if own_knn:
             knn.close()
+    return _sweep_result(config, res, names)
+
+
+def _sweep_result(config: SweepConfig, res: ReplayResult, names) -> SweepResult:
     reports, k = [], 0
     for ci, cell in enumerate(config.cells):
         row = []

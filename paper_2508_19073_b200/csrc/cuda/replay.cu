@@ -11,6 +11,7 @@
 #include "common.cuh"
 #include "pick.cuh"
 #include "replay_kernel.cuh"
+#include "tracegen.cuh"
 
 #ifndef REPLAY_SMALL_PLAN
 #define REPLAY_SMALL_PLAN 64  // plans with at most this many jobs in a class use the large tier
@@ -157,7 +158,7 @@ struct ReplayPlan {
     std::vector<uint32_t> class_list;  // jobs ordered by class
     DeviceBuffer d_cfgs, d_tasks, d_trace_off, d_jobs, d_task_off, d_gpu_off, d_list, d_task_out,
         d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate, d_outcomes, d_tl, d_tl_count, d_log,
-        d_log_count;
+        d_log_count, d_entries;
     uint64_t tl_cap = 0, log_cap = 0;
     const uint64_t* est_override = nullptr;
     uint64_t launches = 0, retried = 0;
@@ -377,17 +378,15 @@ void run_plan(ReplayPlan& pl) {
 }  // namespace
 }  // namespace carma_b200
 
-using namespace carma_b200;
-
-extern "C" {
-
-carma_status carma_replay_plan_create(int device, const carma_replay_config* configs, uint32_t n_configs,
-                                      const carma_task* tasks, const uint64_t* trace_offsets, uint32_t n_traces,
-                                      const carma_replay_job* jobs, uint32_t n_jobs, int32_t want_task_results,
-                                      carma_replay_plan** out) {
-    (void)want_task_results;
-    return guarded([&] {
-        if (!out || !configs || !tasks || !trace_offsets || !jobs) throw InvalidArg("null argument");
+namespace carma_b200 {
+// Plan construction shared by carma_replay_plan_create (host tasks, validated
+// and uploaded) and carma_replay_plan_create_generated (tasks == nullptr: the
+// caller fills d_tasks on the device).
+void build_plan(int device, const carma_replay_config* configs, uint32_t n_configs, const carma_task* tasks,
+                const uint64_t* trace_offsets, uint32_t n_traces, const carma_replay_job* jobs, uint32_t n_jobs,
+                carma_replay_plan** out) {
+    {
+        if (!out || !configs || !trace_offsets || !jobs) throw InvalidArg("null argument");
         if (n_configs == 0 || n_traces == 0 || n_jobs == 0) throw InvalidArg("empty plan");
         require_device(device);
         DeviceGuard guard(device);
@@ -407,7 +406,7 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
                 if (trace_offsets[t + 1] <= trace_offsets[t]) throw InvalidArg("ConfigError: trace contains no tasks");
                 if (trace_offsets[t + 1] - trace_offsets[t] > (1u << 30)) throw Unsupported("trace too long");
             }
-            for (uint64_t i = 0; i < pl->n_tasks; ++i) {
+            for (uint64_t i = 0; tasks && i < pl->n_tasks; ++i) {
                 if (tasks[i].gpus < 1 || tasks[i].gpus > 2) throw Unsupported("gpus_requested must be 1 or 2");
                 if (i > 0 && tasks[i].submit < tasks[i - 1].submit) {
                     // arrivals must be non-decreasing within a trace (load_trace_file)
@@ -434,7 +433,8 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
                 CARMA_CUDA(cudaMemcpy(b.ptr, src, bytes, cudaMemcpyHostToDevice));
             };
             up(pl->d_cfgs, configs, n_configs * sizeof(carma_replay_config));
-            up(pl->d_tasks, tasks, pl->n_tasks * sizeof(carma_task));
+            if (tasks) up(pl->d_tasks, tasks, pl->n_tasks * sizeof(carma_task));
+            else pl->d_tasks.ensure(pl->n_tasks * sizeof(carma_task));
             up(pl->d_trace_off, trace_offsets, (n_traces + 1) * sizeof(uint64_t));
             up(pl->d_jobs, jobs, n_jobs * sizeof(carma_replay_job));
             up(pl->d_task_off, task_off.data(), n_jobs * sizeof(uint64_t));
@@ -472,6 +472,89 @@ carma_status carma_replay_plan_create(int device, const carma_replay_config* con
             throw;
         }
         *out = reinterpret_cast<carma_replay_plan*>(pl);
+    }
+}
+
+}  // namespace carma_b200
+
+using namespace carma_b200;
+
+extern "C" {
+
+carma_status carma_replay_plan_create(int device, const carma_replay_config* configs, uint32_t n_configs,
+                                      const carma_task* tasks, const uint64_t* trace_offsets, uint32_t n_traces,
+                                      const carma_replay_job* jobs, uint32_t n_jobs, int32_t want_task_results,
+                                      carma_replay_plan** out) {
+    (void)want_task_results;
+    return guarded([&] {
+        if (!tasks) throw InvalidArg("null argument");
+        build_plan(device, configs, n_configs, tasks, trace_offsets, n_traces, jobs, n_jobs, out);
+    });
+}
+
+carma_status carma_replay_plan_create_generated(int device, const carma_replay_config* configs, uint32_t n_configs,
+                                                int32_t mix, const uint64_t* seeds, uint32_t n_seeds,
+                                                const uint64_t* entry_estimates, uint32_t n_tables,
+                                                const carma_replay_job* jobs, uint32_t n_jobs,
+                                                carma_replay_plan** out) {
+    return guarded([&] {
+        if (!seeds || n_seeds == 0) throw InvalidArg("ConfigError: sweep has no seeds");
+        if (n_tables == 0) n_tables = 1;
+        if (!entry_estimates && n_tables != 1) throw InvalidArg("estimate tables missing");
+        const uint32_t T = trace_rows(mix);
+        const uint64_t n_traces64 = static_cast<uint64_t>(n_seeds) * n_tables;
+        if (n_traces64 > 0xffffffffull) throw Unsupported("too many traces");
+        const uint32_t n_traces = static_cast<uint32_t>(n_traces64);
+        std::vector<uint64_t> offs(n_traces + 1);
+        for (uint32_t t = 0; t <= n_traces; ++t) offs[t] = static_cast<uint64_t>(t) * T;
+        build_plan(device, configs, n_configs, nullptr, offs.data(), n_traces, jobs, n_jobs, out);
+        auto* pl = reinterpret_cast<ReplayPlan*>(*out);
+        try {
+            DeviceGuard guard(device);
+            DeviceBuffer d_seeds, d_tables;
+            d_seeds.ensure(n_seeds * sizeof(uint64_t));
+            CARMA_CUDA(cudaMemcpyAsync(d_seeds.ptr, seeds, n_seeds * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                       pl->stream));
+            if (entry_estimates) {
+                const size_t tb = static_cast<size_t>(n_tables) * catalog_size() * sizeof(uint64_t);
+                d_tables.ensure(tb);
+                CARMA_CUDA(cudaMemcpyAsync(d_tables.ptr, entry_estimates, tb, cudaMemcpyHostToDevice, pl->stream));
+            }
+            pl->d_entries.ensure(pl->n_tasks * sizeof(int32_t));
+            launch_generate_traces(mix, d_seeds.as<uint64_t>(), n_seeds,
+                                   entry_estimates ? d_tables.as<uint64_t>() : nullptr, n_tables,
+                                   pl->d_tasks.as<carma_task>(), pl->d_entries.as<int32_t>(), pl->stream);
+            CARMA_CUDA(cudaStreamSynchronize(pl->stream));  // the staging buffers go out of scope
+        } catch (...) {
+            carma_replay_plan_destroy(*out);
+            *out = nullptr;
+            throw;
+        }
+    });
+}
+
+carma_status carma_replay_plan_entries(carma_replay_plan* hp, int32_t* entries) {
+    return guarded([&] {
+        auto* pl = reinterpret_cast<ReplayPlan*>(hp);
+        if (!pl || !entries) throw InvalidArg("null argument");
+        if (!pl->d_entries.ptr) throw InvalidArg("plan was not generated on the device");
+        std::lock_guard<std::mutex> lock(pl->mu);
+        DeviceGuard guard(pl->device);
+        CARMA_CUDA(cudaMemcpyAsync(entries, pl->d_entries.ptr, pl->n_tasks * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                   pl->stream));
+        CARMA_CUDA(cudaStreamSynchronize(pl->stream));
+    });
+}
+
+carma_status carma_replay_plan_tasks(carma_replay_plan* hp, carma_task* tasks) {
+    return guarded([&] {
+        auto* pl = reinterpret_cast<ReplayPlan*>(hp);
+        if (!pl || !tasks) throw InvalidArg("null argument");
+        std::lock_guard<std::mutex> lock(pl->mu);
+        DeviceGuard guard(pl->device);
+        CARMA_CUDA(cudaMemcpyAsync(tasks, pl->d_tasks.ptr, pl->n_tasks * sizeof(carma_task), cudaMemcpyDeviceToHost,
+                                   pl->stream));
+        CARMA_CUDA(cudaStreamSynchronize(pl->stream));
     });
 }
 
