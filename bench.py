@@ -742,6 +742,7 @@ def run_carma(args, d: Dist):
         t0 = time.time()
         n_tr = args.sweep_traces
         cfgs, tasks, offs, jobs = sweep_inputs(cb, n_tr)
+        sweep_gen_s = time.time() - t0
         n_placed = int(np.diff(offs.astype(np.int64))[jobs["trace"]].sum())
         plan = cb.ReplayPlan(cfgs, tasks, offs, jobs, device=dev)
         log(f"[rank {d.rank}] sweep inputs {n_tr} traces x {len(SWEEP_POLICIES)} in {time.time() - t0:.1f}s")
@@ -785,6 +786,24 @@ def run_carma(args, d: Dist):
         r_e2e = d.max((time.perf_counter() - t) / args.steps)
         plan.close()
         assert np.array_equal(o_j["energy_mj"], res.traces["energy_mj"])
+        # e2e from seeds: the sweep's traces generated and materialised on the
+        # device (carma_replay_plan_create_generated), replayed, outcomes read
+        # back — run_sweep's inputs without the host trace loop
+        seeds = np.arange(1, n_tr + 1, dtype=np.uint64)
+
+        def gen_step():
+            p = cb.ReplayPlan.generated(cfgs, "t90", seeds, jobs, device=dev)
+            abi.check(abi.lib.carma_replay_plan_run(p._h, None))
+            abi.check(abi.lib.carma_replay_plan_outcomes(p._h, o_t.ctypes.data, o_j.ctypes.data, o_g.ctypes.data))
+            p.close()
+
+        gen_step()
+        d.barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            gen_step()
+        r_gen = d.max((time.perf_counter() - t) / args.steps)
+        assert np.array_equal(o_j["energy_mj"], res.traces["energy_mj"]), "generated sweep differs"
         replay = {
             "metric": "trace-replay placed tasks/sec", "unit": "placed tasks/s",
             "value": N * n_placed / (run_avg * 1e-3), "ms_per_step": run_avg,
@@ -795,7 +814,13 @@ def run_carma(args, d: Dist):
             "e2e": {"value": N * n_placed / r_e2e, "unit": "placed tasks/s",
                     "h2d_bytes_per_step": int(h_tasks.nbytes),
                     "d2h_bytes_per_step": int(o_t.nbytes + o_j.nbytes + o_g.nbytes),
-                    "api": "carma_replay_plan_upload_tasks + run + outcomes (per-task outcomes, reports, per-GPU)"},
+                    "api": "carma_replay_plan_upload_tasks + run + outcomes (per-task outcomes, reports, per-GPU)",
+                    "from_seeds": {"value": N * n_placed / r_gen, "unit": "placed tasks/s",
+                                   "h2d_bytes_per_step": int(seeds.nbytes),
+                                   "d2h_bytes_per_step": int(o_t.nbytes + o_j.nbytes + o_g.nbytes),
+                                   "api": "carma_replay_plan_create_generated (traces generated on the device) "
+                                          "+ run + outcomes"},
+                    "host_trace_generation_s": sweep_gen_s},
             "gpu_launches": int(launches_r) * args.steps,
             "retried_jobs": int(retried),
             "roofline": {"bound": "hbm", "achieved": ALG_BYTES_PER_TASK * n_placed / (k_avg * 1e-3) / 1e9,
