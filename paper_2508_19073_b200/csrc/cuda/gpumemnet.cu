@@ -8,16 +8,18 @@
 // (estimate_learned, proj/src/estimators.cpp:540-551). Inputs are the 19
 // scalar_features (estimators.cpp:317-342) of any estimator row format.
 //
-// Layout on the tensor cores. The E members run side by side: layer l of
-// every member is one block-diagonal GEMM
-//     H_l[128 rows x 64] = relu(H_{l-1}[128 x 64] . W_l^T[64 x 64] + b_l)
-// (member m owns columns 8m..8m+7; a member shallower than the deepest one
-// carries its last activations through identity blocks, exact for ReLU
-// outputs). Layer 0 reads the 19 transformed features (K padded to 32); the
-// head is one GEMM per pass of up to 128 columns (members side by side, CP =
-// C rounded up to 8 columns each). Each MMA is tcgen05.mma.cta_group::1
-// .kind::f16, M = 128, bf16 operands from shared memory (K-major, canonical
-// no-swizzle layout), fp32 accumulators in TMEM.
+// Layout on the tensor cores. The E members run side by side, sorted by
+// depth (descending): layer l of the members still running (a prefix of
+// alive_l members) is one block-diagonal GEMM
+//     H_l[128 rows x 8 alive_l] = relu(H_{l-1} . W_l^T + b_l)
+// (member m owns columns 8m..8m+7; N and K padded to 16 with zero weights).
+// A member that has finished keeps its last activations in its A-tile
+// columns, untouched, until the head reads every member with one K = 64 GEMM
+// per pass of up to 128 columns (members side by side, CP = C rounded up to 8
+// columns each). Layer 0 reads the 19 transformed features (K padded to 32).
+// Each MMA is tcgen05.mma.cta_group::1.kind::f16, M = 128, bf16 operands from
+// shared memory (K-major, canonical no-swizzle layout), fp32 accumulators in
+// TMEM.
 //
 // Precision: weights are bf16 values. Activations are split into three
 // bf16 parts, h = a0 + a1 + a2 (a0 = bf16(h), a1 = bf16(h - a0), a2 =
@@ -25,18 +27,20 @@
 // the products are exact and the activations keep ~24 significant bits, as
 // in an fp32 evaluation. (Two parts keep ~17 bits: measured 6.5e-4 relative
 // logit error on the 8-layer MLP-family ensemble, against 1e-5 for fp32 —
-// re-rounding the activations at every layer, identity layers included,
-// dominates. The north star's bar is 1e-3.)
+// re-rounding the activations at every layer dominates. The north star's bar
+// is 1e-3.)
 //
-// Work split. A CTA per SM holds the model (all layers, ~66 KB for 6-bin
-// families, ~112 KB for the 41-bin MLP family) in shared memory and runs G
-// independent warpgroups; each warpgroup owns a 128-row tile at a time (one
-// row per thread = one TMEM lane), its own A tiles (3 x 16 KB), 128 TMEM
-// columns and an mbarrier. Per layer: the warpgroup stores its activations,
+// Work split. A CTA per SM holds the model (~42 KB for the 6-bin families,
+// ~90 KB for the 41-bin MLP family) in shared memory and runs G groups of
+// 256 threads (3, or 2 for the MLP family: 48 KB of A tiles per group). A
+// group owns a 128-row tile at a time, its A tiles (3 x 16 KB), 128 TMEM
+// columns and an mbarrier; its two warp halves share the TMEM lanes and split
+// the columns (see nn_ensemble). Per layer: the group stores its activations,
 // fences them into the async proxy, one thread issues the MMAs and commits
-// them to the mbarrier, everyone waits, then reads the accumulators back
-// with tcgen05.ld for the fused bias + ReLU + split epilogue. The G
-// warpgroups interleave, so one's MMAs overlap another's epilogue.
+// them to the mbarrier, one warp polls it while the others sleep in the group
+// barrier, then everyone reads the accumulators back with tcgen05.ld for the
+// fused bias + ReLU + split epilogue. The G groups interleave, so one's MMAs
+// overlap another's epilogue.
 //
 // Mixed-family batches are partitioned first (nn_count / nn_scatter: a
 // warp-aggregated counting partition of row ids per family), then one
