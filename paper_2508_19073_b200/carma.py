@@ -571,6 +571,19 @@ def provision_estimates(rc: RunConfig, m: Materialized, device: int = 0,
     """make_estimate for every task (manager.cpp:80-107); learned via the GPU k-NN bank
     trained like provision_estimators (runner.cpp:17-38)."""
     est = rc.policy.estimator
+    if est == "neural":
+        # The paper's neural GPUMemNet (gpumemnet.py), an estimator kind the
+        # reference does not ship; families without a model get no estimate.
+        from .gpumemnet import GpuMemNet, load_default_models
+        net = GpuMemNet(device)
+        try:
+            for mdl in load_default_models().values():
+                net.set_model(mdl)
+            _, nbytes = net.predict(m.features, family=m.family)
+        finally:
+            net.close()
+        m.tasks["estimate"] = nbytes
+        return
     if est != "learned":
         set_persona_estimates(m, est, rc.policy.safety_margin)
         return
@@ -691,11 +704,17 @@ class FusedReplay:
     estimate is a pure function of the task, so a pre-pass gives the bins
     make_estimate computes on every dispatch attempt (manager.cpp:292-294)."""
 
-    def __init__(self, m: "Materialized", cfg: np.ndarray, knn: GpuKnn, device: int = 0):
+    def __init__(self, m: "Materialized", cfg: np.ndarray, knn, device: int = 0):
+        """knn: a GpuKnn (the reference's learned estimator) or a
+        gpumemnet.GpuMemNet (the paper's neural one)."""
         import torch
         self.m, self.cfg, self.knn, self.device = m, cfg, knn, device
+        self.neural = not isinstance(knn, GpuKnn)
         self.packed, self.table = pack_features(m.features, m.family)
-        abi.check(lib.carma_knn_set_act_table(knn.handle, ptr(self.table)))
+        if self.neural:
+            knn.set_act_table(self.table)
+        else:
+            abi.check(lib.carma_knn_set_act_table(knn.handle, ptr(self.table)))
         self.d_rows = torch.from_numpy(self.packed.view(np.uint8).reshape(-1)).to(f"cuda:{device}")
         self.d_bucket = torch.empty(len(m.tasks), dtype=torch.int32, device=f"cuda:{device}")
         self.d_bytes = torch.empty(len(m.tasks), dtype=torch.int64, device=f"cuda:{device}")
@@ -706,9 +725,13 @@ class FusedReplay:
     def run(self) -> None:
         import torch
         s = torch.cuda.current_stream(self.device)
-        check(lib.carma_knn_predict_device(self.knn.handle, self.d_rows.data_ptr(), abi.ROWS_PACKED, None, 0,
-                                           len(self.m.tasks), self.d_bucket.data_ptr(), self.d_bytes.data_ptr(),
-                                           None, None, s.cuda_stream))
+        if self.neural:
+            self.knn.predict_device(self.d_rows, abi.ROWS_PACKED, len(self.m.tasks), self.d_bucket, self.d_bytes,
+                                    stream=s.cuda_stream)
+        else:
+            check(lib.carma_knn_predict_device(self.knn.handle, self.d_rows.data_ptr(), abi.ROWS_PACKED, None, 0,
+                                               len(self.m.tasks), self.d_bucket.data_ptr(), self.d_bytes.data_ptr(),
+                                               None, None, s.cuda_stream))
         self.plan.run(s.cuda_stream)
 
     def results(self) -> ReplayResult:
