@@ -22,10 +22,10 @@
 // TMEM.
 //
 // Precision: weights are bf16 values. Activations are split into three
-// bf16 parts, h = a0 + a1 + a2 (a0 = bf16(h), a1 = bf16(h - a0), a2 =
-// bf16(h - a0 - a1)), and every layer accumulates A0.W + A1.W + A2.W in fp32:
-// the products are exact and the activations keep ~24 significant bits, as
-// in an fp32 evaluation. (Two parts keep ~17 bits: measured 6.5e-4 relative
+// bf16 parts, h = a0 + a1 + a2 exactly (a0 = trunc_bf16(h), a1 =
+// trunc_bf16(h - a0), a2 = h - a0 - a1), and every layer accumulates
+// A0.W + A1.W + A2.W in fp32: the products are exact and the activations
+// keep all 24 bits of their fp32 value, as in an fp32 evaluation. (Two parts keep ~17 bits: measured 6.5e-4 relative
 // logit error on the 8-layer MLP-family ensemble, against 1e-5 for fp32 —
 // re-rounding the activations at every layer dominates. The north star's bar
 // is 1e-3.)
@@ -197,18 +197,20 @@ __device__ __forceinline__ void tmem_wait8(uint32_t (&r)[8]) {
                  : "memory");
 }
 
-// Two fp32 -> packed bf16 pair (round to nearest even): `lo` in the low half
-// (the lower K index), one F2FP instruction.
-__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+// Upper 16 bits of a (low half) and of b (high half): the bf16 truncations
+// of two fp32 values, packed, in one PRMT.
+__device__ __forceinline__ uint32_t pack_hi16(float a, float b) {
     uint32_t r;
-    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(a)), "r"(__float_as_uint(b)));
     return r;
 }
 
 // Splits 8 consecutive activations into kSplit bf16 parts and stores part j
-// at byte offset `off` of A tile j (tiles kATile bytes apart from `a`). The
-// parts are peeled pairwise: one F2FP, the two bf16 values back as fp32 by
-// bit moves, two exact subtractions.
+// at byte offset `off` of A tile j (tiles kATile bytes apart from `a`). Each
+// part is the truncation of what is left (top 8 significant bits); the
+// remainder x - trunc(x) is exact in fp32, so three parts hold all 24 bits of
+// the fp32 value exactly. Integer moves only (PRMT, LOP, FADD), no
+// conversion-pipe instructions.
 __device__ __forceinline__ void store_split8(uint8_t* a, uint32_t off, const float (&h)[8]) {
     float rem[8];
 #pragma unroll
@@ -218,10 +220,11 @@ __device__ __forceinline__ void store_split8(uint8_t* a, uint32_t off, const flo
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            w[i] = cvt_bf16x2(rem[2 * i], rem[2 * i + 1]);
+            w[i] = pack_hi16(rem[2 * i], rem[2 * i + 1]);
             if (j + 1 < kSplit) {
-                rem[2 * i] = __fsub_rn(rem[2 * i], __uint_as_float(w[i] << 16));
-                rem[2 * i + 1] = __fsub_rn(rem[2 * i + 1], __uint_as_float(w[i] & 0xffff0000u));
+                rem[2 * i] = __fsub_rn(rem[2 * i], __uint_as_float(__float_as_uint(rem[2 * i]) & 0xffff0000u));
+                rem[2 * i + 1] =
+                    __fsub_rn(rem[2 * i + 1], __uint_as_float(__float_as_uint(rem[2 * i + 1]) & 0xffff0000u));
             }
         }
         *reinterpret_cast<uint4*>(a + j * kATile + off) = make_uint4(w[0], w[1], w[2], w[3]);
