@@ -68,3 +68,44 @@ def test_sharded_sweep_equals_single_process(tmp_path, olib):
     want = np.concatenate([[oracle_replay(olib, cfg, cb.materialize_trace(cb.generate_trace("t90", s)).tasks)[2]]
                            for s in range(1, 13)])
     assert got.tobytes() == want.tobytes()
+
+
+def _nn_worker(rank, world, port, out_path):
+    """Estimator rows sharded over ranks (the neural GPUMemNet's shard runner
+    replaced by its numpy oracle: no GPU here)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.join(os.path.dirname(here), "oracle"))
+    import gpumemnet_oracle
+    import paper_2508_19073_b200 as cb
+    from paper_2508_19073_b200 import gpumemnet as gm
+
+    m = gm.load_default_models()[1]
+    raw = cb.scalar_features(cb.generate_synthetic_dataset(1, 1001, 9).rows)
+
+    def shard(b, e):
+        return gpumemnet_oracle.forward(m.spec()[0], m.params, raw[b:e])[3]
+
+    res = run_sharded(len(raw), np.ones(len(raw)), shard, rank, world, dist)
+    if rank == 0:
+        np.save(out_path, res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_neural_estimates_equal_single_process(tmp_path):
+    out = str(tmp_path / "nn.npy")
+    mp.spawn(_nn_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import gpumemnet_oracle
+    import paper_2508_19073_b200 as cb
+    from paper_2508_19073_b200 import gpumemnet as gm
+    m = gm.load_default_models()[1]
+    raw = cb.scalar_features(cb.generate_synthetic_dataset(1, 1001, 9).rows)
+    assert np.array_equal(got, gpumemnet_oracle.forward(m.spec()[0], m.params, raw)[3])
