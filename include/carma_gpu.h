@@ -238,13 +238,25 @@ typedef struct carma_nn_spec {
     uint32_t depth[CARMA_NN_MAX_MEMBERS];                      /* hidden layers, 1..8 */
     uint32_t width[CARMA_NN_MAX_MEMBERS][CARMA_NN_MAX_DEPTH]; /* hidden widths, 1..8 */
     uint32_t log_mask;
-    uint32_t reserved;
+    uint32_t arch; /* CARMA_NN_ARCH_MLP or CARMA_NN_ARCH_TRANSFORMER */
     float shift[CARMA_FEATURE_DIMS];
     float scale[CARMA_FEATURE_DIMS];
 } carma_nn_spec;
-/* Parameters (fp32, n_params values): member by member, layer by layer,
+#define CARMA_NN_ARCH_MLP 0
+#define CARMA_NN_ARCH_TRANSFORMER 1
+/* MLP parameters (fp32, n_params values): member by member, layer by layer,
  * W_l [width_l x in_l] row-major then b_l [width_l], with in_0 = 19 and
- * in_l = width_{l-1}; then the head W [C x width_last] and b [C]. */
+ * in_l = width_{l-1}; then the head W [C x width_last] and b [C].
+ *
+ * Transformer ensemble (arch = 1; depth[e] = encoder layers
+ * 1..4, width[e][0] = d in {4, 6, 8}): tokens are the three layer tuples
+ * z[9..11], z[12..14], z[15..17]; per member: embedding W [d x 3], b [d]
+ * (ReLU), positional encodings [3 x d]; per encoder layer (post-LN, one
+ * head, scores / sqrt(d), LayerNorm eps 1e-5): Wq [d x d], bq, Wk, bk, Wv,
+ * bv, Wo, bo, ln1 gain [d], bias [d], W1 [4 x d], b1 [4] (ReLU), W2 [d x 4],
+ * b2 [d], ln2 gain, bias; then mean pooling over the tokens, concatenated
+ * with the auxiliary features z[0..8], z[18]: H1 [8 x (d + 10)], b [8]
+ * (ReLU), H2 [C x 8], b [C]. Transformer weights stay fp32 (CUDA cores). */
 uint64_t carma_nn_param_count(const carma_nn_spec* spec);
 
 typedef struct carma_nn carma_nn;

@@ -110,7 +110,7 @@ pick_request_dtype = np.dtype([
 
 nn_spec_dtype = np.dtype([
     ("members", "<u4"), ("classes", "<u4"), ("bucket_range", "<u8"), ("depth", "<u4", (8,)),
-    ("width", "<u4", (8, 8)), ("log_mask", "<u4"), ("reserved", "<u4"), ("shift", "<f4", (19,)),
+    ("width", "<u4", (8, 8)), ("log_mask", "<u4"), ("arch", "<u4"), ("shift", "<f4", (19,)),
     ("scale", "<f4", (19,)),
 ], align=True)
 NN_MAX_MEMBERS, NN_MAX_DEPTH, NN_MAX_WIDTH, NN_MAX_CLASSES = 8, 8, 8, 48

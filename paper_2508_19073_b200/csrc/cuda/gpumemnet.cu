@@ -87,6 +87,10 @@ struct NnModelDev {
     uint32_t layer_k[CARMA_NN_MAX_DEPTH];    // K steps (16) of layer l
     uint32_t layer_off[CARMA_NN_MAX_DEPTH];  // byte offset of W_l in the blob (SBO = 16 * K_l)
     uint8_t orig[CARMA_NN_MAX_MEMBERS];      // spec member index of sorted member m
+    uint32_t arch;                           // CARMA_NN_ARCH_*
+    uint32_t tf_off[CARMA_NN_MAX_MEMBERS];   // transformer: float offset of member e's parameters
+    uint8_t tf_d[CARMA_NN_MAX_MEMBERS];      // transformer: model width d
+    uint8_t tf_layers[CARMA_NN_MAX_MEMBERS]; // transformer: encoder layers
     uint32_t off_head;    // byte offset of the head weights in the blob
     uint32_t off_bias;    // byte offset of the fp32 biases (L x 64, then head rows)
     uint32_t log_mask;
@@ -541,6 +545,241 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
     }
 }
 
+// ------------------------------------------------- the Transformer ensemble
+
+// LayerNorm over D values (biased variance, eps 1e-5), in place.
+template <int D>
+__device__ __forceinline__ void layer_norm(float (&x)[D], const float* g, const float* b) {
+    float mu = 0.f;
+#pragma unroll
+    for (int i = 0; i < D; ++i) mu += x[i];
+    mu *= 1.0f / D;
+    float var = 0.f;
+#pragma unroll
+    for (int i = 0; i < D; ++i) var = __fmaf_rn(x[i] - mu, x[i] - mu, var);
+    const float inv = rsqrtf(__fmaf_rn(var, 1.0f / D, 1e-5f));
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[i] = __fmaf_rn((x[i] - mu) * inv, g[i], b[i]);
+}
+
+// One member's logits for one row: the tokens are z[9..17], the auxiliary
+// features z[0..8], z[18]; w points at the member's parameters in shared
+// memory (layout in carma_gpu.h). The keys and values of all three tokens
+// are formed first; then each token's query, attention, residual, LayerNorm
+// and feed-forward update its own row of e in place. lg: this thread's
+// logits, strided by the block size in shared memory.
+template <int D>
+__device__ __noinline__ void tf_member(const float* w, int layers, int classes, const float (&z)[kFeatureDims],
+                                       float* lg, int lstride) {
+    float e[3][D];
+    const float* W = w;
+    const float* pos = w + 4 * D;
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            float a = W[3 * D + i];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) a = __fmaf_rn(W[i * 3 + j], z[9 + 3 * t + j], a);
+            e[t][i] = fmaxf(a, 0.f) + pos[t * D + i];
+        }
+    const float* p = w + 7 * D;
+    const float rs = rsqrtf(static_cast<float>(D));
+#pragma unroll 1
+    for (int l = 0; l < layers; ++l) {
+        const float *Wq = p, *bq = p + D * D, *Wk = bq + D, *bk = Wk + D * D, *Wv = bk + D, *bv = Wv + D * D;
+        const float *Wo = bv + D, *bo = Wo + D * D, *g1 = bo + D, *c1 = g1 + D, *W1 = c1 + D, *b1 = W1 + 4 * D;
+        const float *W2 = b1 + 4, *b2 = W2 + 4 * D, *g2 = b2 + D, *c2 = g2 + D;
+        p = c2 + D;
+        float k[3][D], v[3][D];
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                float ak = bk[i], av = bv[i];
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    ak = __fmaf_rn(Wk[i * D + j], e[t][j], ak);
+                    av = __fmaf_rn(Wv[i * D + j], e[t][j], av);
+                }
+                k[t][i] = ak;
+                v[t][i] = av;
+            }
+#pragma unroll 1
+        for (int t = 0; t < 3; ++t) {
+            float et[D];  // e[t] by selects: no dynamically indexed (local-memory) arrays
+#pragma unroll
+            for (int i = 0; i < D; ++i) et[i] = t == 0 ? e[0][i] : (t == 1 ? e[1][i] : e[2][i]);
+            float q[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                float a = bq[i];
+#pragma unroll
+                for (int j = 0; j < D; ++j) a = __fmaf_rn(Wq[i * D + j], et[j], a);
+                q[i] = a;
+            }
+            float sc[3];
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                float a = 0.f;
+#pragma unroll
+                for (int j = 0; j < D; ++j) a = __fmaf_rn(q[j], k[u][j], a);
+                sc[u] = a * rs;
+            }
+            const float mx = fmaxf(sc[0], fmaxf(sc[1], sc[2]));
+            float ssum = 0.f;
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                sc[u] = __expf(sc[u] - mx);
+                ssum += sc[u];
+            }
+            const float inv = __frcp_rn(ssum);
+            float o[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) o[j] = (sc[0] * v[0][j] + sc[1] * v[1][j] + sc[2] * v[2][j]) * inv;
+            float x[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                float a = bo[i];
+#pragma unroll
+                for (int j = 0; j < D; ++j) a = __fmaf_rn(Wo[i * D + j], o[j], a);
+                x[i] = et[i] + a;
+            }
+            layer_norm<D>(x, g1, c1);
+            float f[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                float a = b1[r];
+#pragma unroll
+                for (int j = 0; j < D; ++j) a = __fmaf_rn(W1[r * D + j], x[j], a);
+                f[r] = fmaxf(a, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                float a = b2[i];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) a = __fmaf_rn(W2[i * 4 + r], f[r], a);
+                x[i] += a;
+            }
+            layer_norm<D>(x, g2, c2);
+#pragma unroll
+            for (int i = 0; i < D; ++i) {  // other tokens need only k, v
+                if (t == 0) e[0][i] = x[i];
+                else if (t == 1) e[1][i] = x[i];
+                else e[2][i] = x[i];
+            }
+        }
+    }
+    // head: relu(H1 [mean(e); aux] + b) -> H2 . + b
+    float in[D + 10];
+#pragma unroll
+    for (int i = 0; i < D; ++i) in[i] = (e[0][i] + e[1][i] + e[2][i]) * (1.0f / 3.0f);
+#pragma unroll
+    for (int j = 0; j < 9; ++j) in[D + j] = z[j];
+    in[D + 9] = z[18];
+    const float *H1 = p, *h1 = H1 + 8 * (D + 10), *H2 = h1 + 8, *h2 = H2 + 8 * classes;
+    float hh[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        float a = h1[r];
+#pragma unroll
+        for (int j = 0; j < D + 10; ++j) a = __fmaf_rn(H1[r * (D + 10) + j], in[j], a);
+        hh[r] = fmaxf(a, 0.f);
+    }
+#pragma unroll 1
+    for (int c = 0; c < classes; ++c) {
+        float a = h2[c];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) a = __fmaf_rn(H2[c * 8 + r], hh[r], a);
+        lg[c * lstride] = a;
+    }
+}
+
+// Thread per row: the attention is over three tokens of width d <= 8 (a
+// 3 x 3 score matrix per row), far below any tensor-core tile, so the
+// Transformer ensemble runs on the FMA pipes from registers, its parameters
+// (~10 KB per family) broadcast from shared memory.
+template <int FMT, int CP, bool DIAG>
+__global__ void __launch_bounds__(128) tf_ensemble(const __grid_constant__ NnParams p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const NnModelDev& m = p.m;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(m.blob);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (uint32_t i = threadIdx.x; i < m.blob_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const float* wts = reinterpret_cast<const float*>(smem);
+    float* lg = reinterpret_cast<float*>(smem + m.blob_bytes) + threadIdx.x;  // [class][thread]
+    const int ls = blockDim.x;
+    uint64_t n = p.n, base = 0;
+    if (p.counts) {
+        n = p.counts[p.fam];
+        for (int f = 0; f < p.fam; ++f) base += p.counts[f];
+    }
+    const int C = static_cast<int>(m.classes);
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t row = p.perm ? static_cast<uint64_t>(p.perm[base + i]) : base + i;
+        double raw[kFeatureDims];
+        load_raw<FMT>(p, row, raw);
+        float z[kFeatureDims];
+#pragma unroll
+        for (int d = 0; d < kFeatureDims; ++d) {
+            const float x = __double2float_rn(raw[d]);
+            const float t = ((m.log_mask >> d) & 1u) ? log1pf(fmaxf(x, 0.f)) : x;
+            z[d] = __fmul_rn(__fsub_rn(t, m.shift[d]), m.scale[d]);
+        }
+        float pm[CP];
+#pragma unroll
+        for (int c = 0; c < CP; ++c) pm[c] = 0.f;
+#pragma unroll 1
+        for (uint32_t mem = 0; mem < m.members; ++mem) {
+            const float* w = wts + m.tf_off[mem];
+            const int d = m.tf_d[mem];
+            if (d == 4) tf_member<4>(w, m.tf_layers[mem], C, z, lg, ls);
+            else if (d == 6) tf_member<6>(w, m.tf_layers[mem], C, z, lg, ls);
+            else tf_member<8>(w, m.tf_layers[mem], C, z, lg, ls);
+            if (DIAG && p.logits) {
+                float* out = p.logits + (row * CARMA_NN_MAX_MEMBERS + mem) * CARMA_NN_MAX_CLASSES;
+                for (int c = 0; c < C; ++c) out[c] = lg[c * ls];
+            }
+            float mx = -INFINITY;
+            for (int c = 0; c < C; ++c) mx = fmaxf(mx, lg[c * ls]);
+            float s = 0.f;
+            for (int c = 0; c < C; ++c) {
+                const float ex = __expf(lg[c * ls] - mx);
+                lg[c * ls] = ex;
+                s += ex;
+            }
+            const float inv = __frcp_rn(s);
+#pragma unroll
+            for (int c = 0; c < CP; ++c)
+                if (c < C) pm[c] = __fmaf_rn(lg[c * ls], inv, pm[c]);
+        }
+        const float inv_e = 1.0f / static_cast<float>(m.members);
+        int best = 0;
+        float bv = -1.f;
+#pragma unroll
+        for (int c = 0; c < CP; ++c)
+            if (c < C) {
+                pm[c] *= inv_e;
+                if (pm[c] >= bv) {  // ties to the larger bin
+                    bv = pm[c];
+                    best = c;
+                }
+            }
+        p.bucket[row] = best;
+        p.bytes[row] = static_cast<uint64_t>(best + 1) * m.bucket_range;
+        if (DIAG && p.probs) {
+            float* out = p.probs + row * CARMA_NN_MAX_CLASSES;
+#pragma unroll
+            for (int c = 0; c < CP; ++c)
+                if (c < C) out[c] = pm[c];
+        }
+    }
+}
+
 // ------------------------------------------------------ family partition
 
 constexpr int kBins = CARMA_FAMILIES + 1;  // + rows without a model
@@ -621,7 +860,18 @@ uint16_t bf16_bits(float x) {  // round to nearest even (finite inputs)
     return static_cast<uint16_t>(u >> 16);
 }
 
+uint64_t tf_member_params(uint32_t d, uint32_t layers, uint32_t classes) {
+    return 3ull * d + d + 3ull * d + layers * (4ull * d * d + 17ull * d + 4) + 8ull * (d + 10) + 8 + 8ull * classes +
+           classes;
+}
+
 uint64_t param_count(const carma_nn_spec& s) {
+    if (s.arch == CARMA_NN_ARCH_TRANSFORMER) {
+        uint64_t n = 0;
+        for (uint32_t e = 0; e < s.members && e < CARMA_NN_MAX_MEMBERS; ++e)
+            n += tf_member_params(s.width[e][0], s.depth[e], s.classes);
+        return n;
+    }
     uint64_t n = 0;
     for (uint32_t e = 0; e < s.members; ++e) {
         uint32_t in = kFeatureDims;
@@ -638,6 +888,16 @@ void validate(const carma_nn_spec& s) {
     if (s.members < 1 || s.members > CARMA_NN_MAX_MEMBERS) throw InvalidArg("members must be 1..8");
     if (s.classes < 2 || s.classes > CARMA_NN_MAX_CLASSES) throw InvalidArg("classes must be 2..48");
     if (s.bucket_range == 0) throw InvalidArg("bucket range must be > 0");
+    if (s.arch > CARMA_NN_ARCH_TRANSFORMER) throw InvalidArg("unknown estimator architecture");
+    if (s.arch == CARMA_NN_ARCH_TRANSFORMER) {
+        for (uint32_t e = 0; e < s.members; ++e) {
+            if (s.depth[e] < 1 || s.depth[e] > 4) throw InvalidArg("encoder layers must be 1..4");
+            const uint32_t d = s.width[e][0];
+            if (d != 4 && d != 6 && d != 8) throw InvalidArg("transformer width must be 4, 6 or 8");
+        }
+        if (s.log_mask >> kFeatureDims) throw InvalidArg("log_mask has bits past feature 18");
+        return;
+    }
     for (uint32_t e = 0; e < s.members; ++e) {
         if (s.depth[e] < 1 || s.depth[e] > CARMA_NN_MAX_DEPTH) throw InvalidArg("member depth must be 1..8");
         for (uint32_t l = 0; l < s.depth[e]; ++l)
@@ -659,7 +919,39 @@ size_t canon(uint32_t row, uint32_t k, uint32_t sbo) {
 // and a member that has finished keeps its last activations in its A-tile
 // columns, untouched, until the head reads all of them. Then the head passes
 // and the fp32 biases.
+void build_model_tf(HostNn& hm, int device, const carma_nn_spec& s, const float* params) {
+    NnModelDev d{};
+    d.arch = CARMA_NN_ARCH_TRANSFORMER;
+    d.members = s.members;
+    d.classes = s.classes;
+    d.cp = (s.classes + 7u) & ~7u;
+    d.log_mask = s.log_mask;
+    d.bucket_range = s.bucket_range;
+    std::memcpy(d.shift, s.shift, sizeof(d.shift));
+    std::memcpy(d.scale, s.scale, sizeof(d.scale));
+    uint64_t off = 0;
+    for (uint32_t e = 0; e < s.members; ++e) {
+        d.orig[e] = static_cast<uint8_t>(e);
+        d.tf_off[e] = static_cast<uint32_t>(off);
+        d.tf_d[e] = static_cast<uint8_t>(s.width[e][0]);
+        d.tf_layers[e] = static_cast<uint8_t>(s.depth[e]);
+        off += tf_member_params(s.width[e][0], s.depth[e], s.classes);
+    }
+    d.blob_bytes = static_cast<uint32_t>((off * 4 + 15) & ~15ull);
+    d.smem_blob = d.blob_bytes;
+    std::vector<uint8_t> blob(d.blob_bytes, 0);
+    std::memcpy(blob.data(), params, off * 4);
+    DeviceGuard gd(device);
+    hm.blob.ensure(blob.size());
+    CARMA_CUDA(cudaMemcpy(hm.blob.ptr, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+    d.blob = hm.blob.as<uint8_t>();
+    hm.dev = d;
+    hm.spec = s;
+    hm.present = true;
+}
+
 void build_model(HostNn& hm, int device, const carma_nn_spec& s, const float* params) {
+    if (s.arch == CARMA_NN_ARCH_TRANSFORMER) return build_model_tf(hm, device, s, params);
     const uint32_t E = s.members;
     uint32_t L = 0;
     for (uint32_t e = 0; e < E; ++e) L = std::max(L, s.depth[e]);
@@ -815,8 +1107,28 @@ void launch_ensemble_t(const NnParams& p, int device, cudaStream_t s) {
 
 // Warpgroups per CTA: as many 48-KB A-tile triples as fit beside the model
 // (<= 4: TMEM holds 4 x 128 columns), and CP = 8 or 48 columns per member.
+template <int FMT, int CP, bool DIAG>
+void launch_tf_t(const NnParams& p, int device, cudaStream_t s) {
+    const size_t smem = p.m.blob_bytes + 128u * CARMA_NN_MAX_CLASSES * 4u;  // + per-thread logits
+    if (smem > kSmemLimit) throw Unsupported("model too large for shared memory");
+    static cudaError_t attr = cudaFuncSetAttribute(tf_ensemble<FMT, CP, DIAG>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(kSmemLimit));
+    CARMA_CUDA(attr);
+    const uint64_t want = (p.counts ? 0 : (p.n + 127) / 128);
+    const unsigned grid = static_cast<unsigned>(
+        want ? std::min<uint64_t>(want, 8ull * sm_count(device)) : 8ull * sm_count(device));
+    tf_ensemble<FMT, CP, DIAG><<<grid, 128, smem, s>>>(p);
+    CARMA_CUDA(cudaGetLastError());
+}
+
 template <int FMT, bool DIAG>
 void launch_ensemble(const NnParams& p, int device, cudaStream_t s) {
+    if (p.m.arch == CARMA_NN_ARCH_TRANSFORMER) {
+        if (p.m.cp <= 8) launch_tf_t<FMT, 8, DIAG>(p, device, s);
+        else launch_tf_t<FMT, 48, DIAG>(p, device, s);
+        return;
+    }
     const uint32_t room = kSmemLimit - p.m.smem_blob - 64;
     const int g = static_cast<int>(std::min<uint32_t>(3, room / (kSplit * kATile)));
     if (g < 1) throw Unsupported("model too large for shared memory");
@@ -923,6 +1235,7 @@ uint64_t run_predict(NnHandle& h, NnHandle::Scratch& sc, const void* rows, int32
 // MMAs per 128-row tile of a model: the K steps of every layer and of the
 // head passes (K = 64: 4 steps each), kSplit MMAs per step.
 uint64_t mmas_per_tile(const NnModelDev& d) {
+    if (d.arch == CARMA_NN_ARCH_TRANSFORMER) return 0;
     uint64_t steps = 4ull * d.passes;
     for (uint32_t l = 0; l < d.depth; ++l) steps += d.layer_k[l];
     return kSplit * steps;

@@ -31,6 +31,7 @@ FAMILY_NAMES = {0: "mlp", 1: "cnn", 2: "transformer"}
 # tuples' activations and params; 18 the 16P + 4BA footprint proxy.
 LOG_DIMS = (0, 1, 2, 3, 4, 5, 6, 10, 11, 13, 14, 16, 17, 18)
 LOG_MASK = sum(1 << d for d in LOG_DIMS)
+ARCH_MLP, ARCH_TRANSFORMER = 0, 1
 
 
 @dataclasses.dataclass
@@ -45,6 +46,7 @@ class NnModel:
     params: np.ndarray          # flat fp32, layout of carma_nn_set_model
     log_mask: int = LOG_MASK
     holdout_accuracy: float = float("nan")
+    arch: int = ARCH_MLP        # ARCH_TRANSFORMER: depth = encoder layers, width[e] = [d]
 
     @property
     def members(self) -> int:
@@ -59,6 +61,7 @@ class NnModel:
             s["depth"][0][e] = d
             s["width"][0][e][: len(w)] = w
         s["log_mask"] = self.log_mask
+        s["arch"] = self.arch
         s["shift"][0] = self.shift
         s["scale"][0] = self.scale
         return s
@@ -69,23 +72,28 @@ class NnModel:
             width[e, : len(w)] = w
         np.savez(path, family=self.family, bucket_range=self.bucket_range, classes=self.classes,
                  depth=np.asarray(self.depth, np.int32), width=width, shift=self.shift, scale=self.scale,
-                 params=self.params, log_mask=self.log_mask, holdout_accuracy=self.holdout_accuracy)
+                 params=self.params, log_mask=self.log_mask, holdout_accuracy=self.holdout_accuracy, arch=self.arch)
 
     @staticmethod
     def load(path: str) -> "NnModel":
         z = np.load(path)
         depth = [int(d) for d in z["depth"]]
-        width = [[int(v) for v in z["width"][e][:d]] for e, d in enumerate(depth)]
+        arch = int(z["arch"]) if "arch" in z else ARCH_MLP
+        if arch == ARCH_TRANSFORMER:
+            width = [[int(z["width"][e][0])] for e in range(len(depth))]
+        else:
+            width = [[int(v) for v in z["width"][e][:d]] for e, d in enumerate(depth)]
         return NnModel(int(z["family"]), int(z["bucket_range"]), int(z["classes"]), depth, width,
                        z["shift"].astype(np.float32), z["scale"].astype(np.float32), z["params"].astype(np.float32),
-                       int(z["log_mask"]), float(z["holdout_accuracy"]))
+                       int(z["log_mask"]), float(z["holdout_accuracy"]), arch)
 
 
-def load_default_models() -> Dict[int, NnModel]:
-    """The committed GPUMemNet ensembles, one per family."""
+def load_default_models(arch: int = ARCH_MLP) -> Dict[int, NnModel]:
+    """The committed GPUMemNet ensembles (MLP or Transformer), one per family."""
     out = {}
+    pre = "gpumemnet_tf_" if arch == ARCH_TRANSFORMER else "gpumemnet_"
     for f, name in FAMILY_NAMES.items():
-        path = os.path.join(WEIGHTS_DIR, f"gpumemnet_{name}.npz")
+        path = os.path.join(WEIGHTS_DIR, f"{pre}{name}.npz")
         if os.path.exists(path):
             out[f] = NnModel.load(path)
     return out

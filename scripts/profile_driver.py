@@ -80,7 +80,7 @@ def nn(args):
     rows = np.concatenate([d.rows for d in ds])
     fam = np.concatenate([np.full(args.rows // 2, 1, np.int8), np.full(args.rows // 2, 2, np.int8)])
     net = gm.GpuMemNet(0)
-    models = gm.load_default_models()
+    models = gm.load_default_models(gm.ARCH_TRANSFORMER if args.arch == "transformer" else gm.ARCH_MLP)
     for f in (1, 2):
         net.set_model(models[f])
     words, schema = cb.pack_features_bits(rows, fam)
@@ -144,5 +144,6 @@ if __name__ == "__main__":
     ap.add_argument("--rows", type=int, default=1 << 22)
     ap.add_argument("--format", choices=("rows", "bitpacked"), default="bitpacked")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--arch", choices=("mlp", "transformer"), default="mlp")
     a = ap.parse_args()
     {"replay": replay, "knn": knn, "fused": fused, "scoring": scoring, "nn": nn}[a.what](a)

@@ -71,6 +71,46 @@ class Member(torch.nn.Module):
         return self.head(self.body(x))
 
 
+class TfMember(torch.nn.Module):
+    """GPUMemNet Transformer classifier: an MLP input embedding
+    of the per-layer tuples (first / middle / last layer: kind, activations,
+    params = z[9..17]), learned positional encodings, post-LN encoder layers
+    (one head, feed-forward 4), mean pooling, concatenation with the
+    structured auxiliary features (z[0..8], z[18]) and an MLP head."""
+
+    def __init__(self, d, layers, classes):
+        super().__init__()
+        self.d = d
+        self.emb = torch.nn.Linear(3, d)
+        self.pos = torch.nn.Parameter(torch.randn(3, d) * 0.1)
+        self.enc = torch.nn.ModuleList([torch.nn.TransformerEncoderLayer(
+            d_model=d, nhead=1, dim_feedforward=4, dropout=0.0, batch_first=True) for _ in range(layers)])
+        self.h1 = torch.nn.Linear(d + 10, 8)
+        self.h2 = torch.nn.Linear(8, classes)
+
+    def forward(self, z):
+        tok = z[:, 9:18].reshape(-1, 3, 3)
+        e = torch.relu(self.emb(tok)) + self.pos
+        for layer in self.enc:
+            e = layer(e)
+        aux = torch.cat([z[:, 0:9], z[:, 18:19]], dim=1)
+        return self.h2(torch.relu(self.h1(torch.cat([e.mean(dim=1), aux], dim=1))))
+
+
+def tf_export(m: TfMember) -> list:
+    """Flat parameter blocks in the layout of carma_gpu.h (Transformer)."""
+    d = m.d
+    out = [m.emb.weight, m.emb.bias, m.pos]
+    for layer in m.enc:
+        w, b = layer.self_attn.in_proj_weight, layer.self_attn.in_proj_bias
+        out += [w[:d], b[:d], w[d:2 * d], b[d:2 * d], w[2 * d:], b[2 * d:],
+                layer.self_attn.out_proj.weight, layer.self_attn.out_proj.bias,
+                layer.norm1.weight, layer.norm1.bias, layer.linear1.weight, layer.linear1.bias,
+                layer.linear2.weight, layer.linear2.bias, layer.norm2.weight, layer.norm2.bias]
+    out += [m.h1.weight, m.h1.bias, m.h2.weight, m.h2.bias]
+    return [t.detach().float().numpy().ravel() for t in out]
+
+
 def fold(member: Member) -> list:
     """[(W, b)] per hidden layer with batch norm folded, then the head."""
     out = []
@@ -110,6 +150,59 @@ def torch_forward(folded_members, z: np.ndarray) -> np.ndarray:
                 h = torch.relu(h)
         outs.append(h)
     return torch.stack(outs, dim=1).numpy()
+
+
+def train_members(build, n_members, xt, yt, epochs):
+    members = []
+    n = len(xt)
+    for e in range(n_members):
+        m = build(e)
+        opt = torch.optim.Adam(m.parameters(), lr=1e-2)
+        sched = torch.optim.lr_scheduler.CosineAnnealingLR(opt, epochs)
+        m.train()
+        for _ in range(epochs):
+            order = torch.randperm(n)
+            for i in range(0, n, 256):
+                idx = order[i: i + 256]
+                if len(idx) < 2:
+                    continue
+                opt.zero_grad()
+                loss = torch.nn.functional.cross_entropy(m(xt[idx]), yt[idx])
+                loss.backward()
+                opt.step()
+            sched.step()
+        m.eval()
+        members.append(m)
+    return members
+
+
+def train_family_tf(family: int, samples: int, epochs: int, seed: int):
+    """The Transformer ensemble: 8 members, d in {4, 6}, 2-3 encoder layers
+    (PAPER.md:440), weights exported unrounded (fp32; the Transformer kernel
+    runs on the CUDA cores)."""
+    torch.manual_seed(seed)
+    rng = np.random.default_rng(seed)
+    ds = cb.generate_synthetic_dataset(family, samples, 1000 + family)
+    br = ds.bucket_range
+    classes = CAPACITY // br + 1
+    raw, z, shift, scale = features(ds.rows)
+    y = np.minimum(ds.bucket, classes - 1).astype(np.int64)
+    n_train = int(0.8 * samples)
+    perm = rng.permutation(samples)
+    tr, ho = perm[:n_train], perm[n_train:]
+    dims = [int(v) for v in rng.choice([4, 6], size=MEMBERS)]
+    layers = [int(v) for v in rng.integers(2, 4, size=MEMBERS)]
+    members = train_members(lambda e: TfMember(dims[e], layers[e], classes), MEMBERS,
+                            torch.from_numpy(z[tr]), torch.from_numpy(y[tr]), epochs)
+    with torch.no_grad():
+        logits = torch.stack([m(torch.from_numpy(z[ho])) for m in members], dim=1).double().numpy()
+    probs = torch.softmax(torch.from_numpy(logits), dim=2).mean(dim=1).numpy()
+    pred = classes - 1 - np.argmax(probs[:, ::-1], axis=1)
+    acc = float((pred == y[ho]).mean())
+    params = np.concatenate([np.concatenate(tf_export(m)) for m in members]).astype(np.float32)
+    model = gm.NnModel(family, br, classes, layers, [[d] for d in dims], shift, scale, params, gm.LOG_MASK, acc,
+                       arch=gm.ARCH_TRANSFORMER)
+    return model, members
 
 
 def train_family(family: int, samples: int, epochs: int, seed: int):
@@ -157,12 +250,36 @@ def train_family(family: int, samples: int, epochs: int, seed: int):
     return model, folded
 
 
+def main_tf(args) -> None:
+    golden = {}
+    for family, name in gm.FAMILY_NAMES.items():
+        t0 = time.time()
+        model, members = train_family_tf(family, args.samples, args.epochs, seed=17 + family)
+        model.save(os.path.join(gm.WEIGHTS_DIR, f"gpumemnet_tf_{name}.npz"))
+        ds = cb.generate_synthetic_dataset(family, 256, 4242 + family)
+        raw, z, _, _ = features(ds.rows, model.shift, model.scale)
+        with torch.no_grad():
+            zz = torch.from_numpy(z.astype(np.float64))
+            logits = torch.stack([m.double()(zz) for m in members], dim=1).numpy()
+        golden[f"{name}_rows"] = ds.rows.view(np.uint8).reshape(len(ds.rows), -1)
+        golden[f"{name}_raw"] = raw
+        golden[f"{name}_logits"] = logits.astype(np.float32)
+        golden[f"{name}_labels"] = ds.bucket
+        print(f"transformer {name}: classes {model.classes}, layers {model.depth}, d {[w[0] for w in model.width]}, "
+              f"holdout accuracy {model.holdout_accuracy:.4f}, {time.time() - t0:.1f} s")
+    np.savez_compressed(os.path.join(ROOT, "tests", "golden", "gpumemnet_tf.npz"), **golden)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--samples", type=int, default=20000)
     ap.add_argument("--epochs", type=int, default=30)
+    ap.add_argument("--arch", choices=("mlp", "transformer"), default="mlp")
     args = ap.parse_args()
     os.makedirs(gm.WEIGHTS_DIR, exist_ok=True)
+    if args.arch == "transformer":
+        main_tf(args)
+        return
     golden = {}
     for family, name in gm.FAMILY_NAMES.items():
         t0 = time.time()

@@ -272,3 +272,67 @@ def test_neural_estimates_drive_the_replay(gpu, models):
     tr, _, _ = cb.run_simulation(rc, device=gpu)
     assert tr.tobytes() == host.traces[0].tobytes()
     net.close()
+
+
+# ------------------------------------------------- the Transformer ensemble
+
+GOLDEN_TF = os.path.join(ROOT, "tests", "golden", "gpumemnet_tf.npz")
+
+
+@pytest.fixture(scope="module")
+def tf_models():
+    m = gm.load_default_models(gm.ARCH_TRANSFORMER)
+    assert set(m) == {0, 1, 2}
+    return m
+
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_tf_oracle_matches_torch_golden(tf_models, fam):
+    orc = _oracle()
+    m = tf_models[fam]
+    z = np.load(GOLDEN_TF)
+    name = gm.FAMILY_NAMES[fam]
+    raw, logits = z[f"{name}_raw"], z[f"{name}_logits"]
+    ol, op, ob, oby = orc.forward(m.spec()[0], m.params, raw)
+    assert np.all(np.abs(ol - logits) <= 1e-5 * np.maximum(1.0, np.abs(logits)))
+    assert gm.param_count(m) == len(m.params)
+    assert m.holdout_accuracy > 0.9
+    assert (ob == np.minimum(z[f"{name}_labels"], m.classes - 1)).mean() > 0.85
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_tf_kernel_matches_oracle(gpu, tf_models, fam):
+    m = tf_models[fam]
+    net = gm.GpuMemNet(gpu)
+    net.set_model(m)
+    ds = cb.generate_synthetic_dataset(fam, 3000, 555 + fam)
+    raw = cb.scalar_features(ds.rows)
+    for fmt, rows in ((abi.ROWS_FEATURES, ds.rows), (abi.ROWS_SCALAR, raw)):
+        b, by, pr, lg = _predict_device(net, rows, fmt, len(ds.rows), default_family=fam)
+        assert _check(m, raw, b, by, pr, lg) < 1e-4
+    hb, hby = net.predict(ds.rows, default_family=fam)
+    assert np.array_equal(hb, b) and np.array_equal(hby, by)
+    net.close()
+
+
+@pytest.mark.gpu
+def test_tf_and_mlp_banks_mix_by_family(gpu, models, tf_models):
+    """A bank may hold a Transformer ensemble for one family and an MLP
+    ensemble for another; bit-packed rows route per family."""
+    net = gm.GpuMemNet(gpu)
+    net.set_model(tf_models[1])
+    net.set_model(models[2])
+    parts = [cb.generate_synthetic_dataset(f, n, 70 + f) for f, n in ((1, 900), (2, 1100))]
+    rows = np.concatenate([p.rows for p in parts])
+    fams = np.concatenate([np.full(len(p.rows), p.family, np.int8) for p in parts])
+    order = np.random.default_rng(4).permutation(len(rows))
+    rows, fams = rows[order], fams[order]
+    raw = cb.scalar_features(rows)
+    words, schema = cb.pack_features_bits(rows, fams)
+    net.set_bit_schema(schema)
+    b, by, pr, lg = _predict_device(net, words, abi.ROWS_BITPACKED, len(rows))
+    for f, mdl in ((1, tf_models[1]), (2, models[2])):
+        sel = fams == f
+        _check(mdl, raw[sel], b[sel], by[sel], pr[sel], lg[sel])
+    net.close()
