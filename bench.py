@@ -322,6 +322,42 @@ def neural_bench(abi, cb, dev, stream, args, d, words, schema, rows, fam):
         cpu = {"value": ns / cpu_s, "unit": "estimates/s", "cores": threads, "kind": "port",
                "sample": f"first {ns // 2} CNN + first {ns // 2} Transformer rows of the batch through "
                          "oracle/gpumemnet_oracle.py (numpy; no reference implementation exists)"}
+    # the paper's Transformer ensemble on the same batch (CUDA cores)
+    tfm = gm.load_default_models(gm.ARCH_TRANSFORMER)
+    tnet = gm.GpuMemNet(dev)
+    for f in (1, 2):
+        tnet.set_model(tfm[f])
+    tnet.set_bit_schema(schema)
+
+    def tf_step():
+        tnet.predict_device(d_rows, abi.ROWS_BITPACKED, Q, d_b, d_by, stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        tf_step()
+    torch.cuda.synchronize()
+    d.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        tf_step()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    tf_ms = d.max(f0.elapsed_time(f1) / args.steps)
+    tb = d_b.cpu().numpy()
+    tf_agree = 0
+    for f in (1, 2):
+        sel = fam[idx] == f
+        _, op, ob, _ = gpumemnet_oracle.forward(tfm[f].spec()[0], tfm[f].params, raw[sel])
+        srt = np.sort(op, axis=1)
+        sure = srt[:, -1] - srt[:, -2] > 1e-3
+        assert np.array_equal(tb[idx][sel][sure], ob[sure]), "transformer bins differ from the oracle"
+        tf_agree += int(sure.sum())
+    tnet.close()
+    transformer = {"metric": "GPUMemNet estimates/sec (Transformer ensemble, 8 members)", "unit": "estimates/s",
+                   "value": d.n * Q / (tf_ms * 1e-3), "ms_per_step": tf_ms, "dtype": "f32",
+                   "kernel": "tf_ensemble (thread per row, three-token attention in registers, CUDA cores)",
+                   "oracle_agreement_rows": tf_agree,
+                   "holdout_accuracy": {gm.FAMILY_NAMES[f]: tfm[f].holdout_accuracy for f in (1, 2)}}
     k_avg = statistics.mean(kernel_ms)
     rows_f = {f: int((fam == f).sum()) for f in (1, 2)}
     executed = sum((rows_f[f] + 127) // 128 * nn_tile_flops(models[f])[0] for f in (1, 2))
@@ -354,6 +390,7 @@ def neural_bench(abi, cb, dev, stream, args, d, words, schema, rows, fam):
                      "hbm_gbs": hbm_bytes / (k_avg * 1e-3) / 1e9, "hbm_peak_gbs": peaks().get("hbm_gbs"),
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
         "cpu_baseline": cpu,
+        "transformer": transformer,
         "oracle_agreement_rows": agree,
         "holdout_accuracy": {gm.FAMILY_NAMES[f]: models[f].holdout_accuracy for f in (1, 2)},
     }

@@ -249,7 +249,7 @@ typedef struct carma_nn_spec {
  * in_l = width_{l-1}; then the head W [C x width_last] and b [C].
  *
  * Transformer ensemble (arch = 1; depth[e] = encoder layers
- * 1..4, width[e][0] = d in {4, 6, 8}): tokens are the three layer tuples
+ * 1..4, width[e][0] = d in {4, 6}): tokens are the three layer tuples
  * z[9..11], z[12..14], z[15..17]; per member: embedding W [d x 3], b [d]
  * (ReLU), positional encodings [3 x d]; per encoder layer (post-LN, one
  * head, scores / sqrt(d), LayerNorm eps 1e-5): Wq [d x d], bq, Wk, bk, Wv,

@@ -700,7 +700,7 @@ __device__ __noinline__ void tf_member(const float* w, int layers, int classes, 
 // Transformer ensemble runs on the FMA pipes from registers, its parameters
 // (~10 KB per family) broadcast from shared memory.
 template <int FMT, int CP, bool DIAG>
-__global__ void __launch_bounds__(128) tf_ensemble(const __grid_constant__ NnParams p) {
+__global__ void __launch_bounds__(128, 2) tf_ensemble(const __grid_constant__ NnParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const NnModelDev& m = p.m;
     {
@@ -738,8 +738,7 @@ __global__ void __launch_bounds__(128) tf_ensemble(const __grid_constant__ NnPar
             const float* w = wts + m.tf_off[mem];
             const int d = m.tf_d[mem];
             if (d == 4) tf_member<4>(w, m.tf_layers[mem], C, z, lg, ls);
-            else if (d == 6) tf_member<6>(w, m.tf_layers[mem], C, z, lg, ls);
-            else tf_member<8>(w, m.tf_layers[mem], C, z, lg, ls);
+            else tf_member<6>(w, m.tf_layers[mem], C, z, lg, ls);
             if (DIAG && p.logits) {
                 float* out = p.logits + (row * CARMA_NN_MAX_MEMBERS + mem) * CARMA_NN_MAX_CLASSES;
                 for (int c = 0; c < C; ++c) out[c] = lg[c * ls];
@@ -893,7 +892,7 @@ void validate(const carma_nn_spec& s) {
         for (uint32_t e = 0; e < s.members; ++e) {
             if (s.depth[e] < 1 || s.depth[e] > 4) throw InvalidArg("encoder layers must be 1..4");
             const uint32_t d = s.width[e][0];
-            if (d != 4 && d != 6 && d != 8) throw InvalidArg("transformer width must be 4, 6 or 8");
+            if (d != 4 && d != 6) throw InvalidArg("transformer width must be 4 or 6 (PAPER.md:440)");
         }
         if (s.log_mask >> kFeatureDims) throw InvalidArg("log_mask has bits past feature 18");
         return;
