@@ -1,4 +1,4 @@
-"""Neural GPUMemNet (the paper's MLP ensemble) on the B200 tensor cores.
+"""Neural GPUMemNet (the paper's MLP and Transformer ensembles) on the B200.
 
 Host mirror of the estimator interface for the neural EstimatorKind next to
 the k-NN (`GpuKnn`): a per-family model bank (Manager::set_learned_estimators,
