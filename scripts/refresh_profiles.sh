@@ -20,3 +20,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:repl
     -o $OUT/replay_c5_full -f python scripts/profile_driver.py fused --tasks 100000 --reps 1 > $OUT/ncu_c5.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:nn_ensemble -s 1 -c 1 \
     -o $OUT/nn_ensemble_full -f python scripts/profile_driver.py nn --rows 16777216 --reps 2 > $OUT/ncu_nn.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:tf_ensemble -s 1 -c 1 \
+    -o $OUT/tf_ensemble_full -f python scripts/profile_driver.py nn --arch transformer --rows 4194304 --reps 2 > $OUT/ncu_tf.log 2>&1
