@@ -680,6 +680,9 @@ __device__ __forceinline__ void sorted_insert(float (&a)[K], float v) {
 #endif
 // Host-buffer calls pipeline H2D / search / D2H over chunks of this many rows
 // on two streams.
+#ifndef KNN_E2E_SMALL_LOG2
+#define KNN_E2E_SMALL_LOG2 18
+#endif
 #ifndef KNN_E2E_CHUNK_LOG2
 #define KNN_E2E_CHUNK_LOG2 21
 #endif
@@ -1315,7 +1318,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
         // the first H2D copy (pipeline fill) and the last search + D2H
         // (drain) are short; scratch is sized for the steady chunk.
         const uint64_t chunk = uint64_t{1} << KNN_E2E_CHUNK_LOG2;
-        const uint64_t small = uint64_t{1} << 18;
+        const uint64_t small = uint64_t{1} << KNN_E2E_SMALL_LOG2;
         auto chunk_rows = [&](uint64_t c, uint64_t remaining) -> uint64_t {
             const uint64_t grow = std::min<uint64_t>(chunk, small << std::min<uint64_t>(c, 20));
             return std::min<uint64_t>(grow, std::max<uint64_t>(small, remaining / 2));
