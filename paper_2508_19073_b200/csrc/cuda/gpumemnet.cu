@@ -1065,7 +1065,9 @@ struct NnHandle {
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // call start, ensemble start, ensemble end
     bool timed = false;
     uint64_t last_launches = 0, last_mmas = 0;
-    uint32_t last_counts[kBins] = {0, 0, 0, 0};
+    PinnedBuffer counts_host;          // family counts of the last device call
+    cudaStream_t counts_stream = nullptr;
+    bool counts_pending = false;
     std::mutex mu;
 };
 
@@ -1313,6 +1315,7 @@ carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int3
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[1]));
         h->last_launches = launches;
         h->last_mmas = 0;
+        h->counts_pending = false;
     });
 }
 
@@ -1348,6 +1351,7 @@ carma_status carma_nn_destroy(carma_nn* hh) {
             DeviceGuard g(h->device);
             cudaDeviceSynchronize();
             for (auto& m : h->model) m.blob.release();
+            h->counts_host.release();
             for (auto& sc : h->scratch) {
                 for (DeviceBuffer* b : {&sc.rows, &sc.family, &sc.perm, &sc.counts, &sc.bucket, &sc.bytes}) b->release();
                 sc.stage_rows.release();
@@ -1416,18 +1420,20 @@ carma_status carma_nn_predict_device(carma_nn* hh, const void* rows, int32_t for
         NnHandle::Scratch& sc = h->scratch[0];
         h->last_launches = run_predict(*h, sc, rows, format, family, default_family, q, bucket_out, bytes_out, probs,
                                        logits, s);
-        // MMA count from the family counts of this call
-        uint64_t mmas = 0;
+        // MMA count of this call: from the family counts, read back (async,
+        // into pinned memory) and summed by carma_nn_last_timing
+        h->last_mmas = 0;
+        h->counts_pending = false;
         const bool per_row = format == CARMA_ROWS_PACKED || format == CARMA_ROWS_BITPACKED || family;
         if (per_row) {
-            CARMA_CUDA(cudaMemcpyAsync(h->last_counts, sc.counts.ptr, sizeof(h->last_counts), cudaMemcpyDeviceToHost, s));
-            CARMA_CUDA(cudaStreamSynchronize(s));
-            for (int f = 0; f < CARMA_FAMILIES; ++f)
-                if (h->model[f].present) mmas += (h->last_counts[f] + 127ull) / 128ull * mmas_per_tile(h->model[f].dev);
+            h->counts_host.ensure(sizeof(uint32_t) * kBins);
+            CARMA_CUDA(cudaMemcpyAsync(h->counts_host.ptr, sc.counts.ptr, sizeof(uint32_t) * kBins,
+                                       cudaMemcpyDeviceToHost, s));
+            h->counts_stream = s;
+            h->counts_pending = true;
         } else if (default_family >= 0 && default_family < CARMA_FAMILIES && h->model[default_family].present) {
-            mmas = (q + 127) / 128 * mmas_per_tile(h->model[default_family].dev);
+            h->last_mmas = (q + 127) / 128 * mmas_per_tile(h->model[default_family].dev);
         }
-        h->last_mmas = mmas;
     });
 }
 
@@ -1459,6 +1465,15 @@ carma_status carma_nn_last_timing(carma_nn* hh, double* kernel_ms, double* call_
         }
         if (kernel_ms) *kernel_ms = a;
         if (call_ms) *call_ms = b;
+        if (h->counts_pending) {
+            CARMA_CUDA(cudaStreamSynchronize(h->counts_stream));
+            const uint32_t* c = h->counts_host.as<uint32_t>();
+            uint64_t n = 0;
+            for (int f = 0; f < CARMA_FAMILIES; ++f)
+                if (h->model[f].present) n += (c[f] + 127ull) / 128ull * mmas_per_tile(h->model[f].dev);
+            h->last_mmas = n;
+            h->counts_pending = false;
+        }
         if (launches) *launches = h->last_launches;
         if (mmas) *mmas = h->last_mmas;
     });
