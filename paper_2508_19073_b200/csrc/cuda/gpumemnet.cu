@@ -805,32 +805,45 @@ __global__ void nn_count(const __grid_constant__ NnParams p, uint64_t q, uint32_
             if (local[k]) atomicAdd(counts + k, local[k]);
 }
 
+// Row ids grouped by family. Positions are claimed per block (shared-memory
+// counters, then one global atomic per family per block step): per-warp
+// global atomics on two counters serialised at ~1M operations per 16.7M rows.
 template <int FMT>
-__global__ void nn_scatter(const __grid_constant__ NnParams p, uint64_t q, uint32_t present,
-                           const uint32_t* __restrict__ counts, uint32_t* __restrict__ cursor,
-                           uint32_t* __restrict__ perm) {
+__global__ void __launch_bounds__(256) nn_scatter(const __grid_constant__ NnParams p, uint64_t q, uint32_t present,
+                                                  const uint32_t* __restrict__ counts, uint32_t* __restrict__ cursor,
+                                                  uint32_t* __restrict__ perm) {
+    __shared__ uint32_t s_cnt[CARMA_FAMILIES], s_base[CARMA_FAMILIES];
     const unsigned lane = threadIdx.x & 31;
     uint32_t off[kBins];
     off[0] = 0;
 #pragma unroll
     for (int k = 1; k < kBins; ++k) off[k] = off[k - 1] + counts[k - 1];
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); i0 < q; i0 += stride) {
-        const uint64_t i = i0 + lane;
+    for (uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x; b0 < q; b0 += stride) {
+        const uint64_t i = b0 + threadIdx.x;
         const int b = i < q ? nn_bin<FMT>(p, i, present) : -1;
         if (b == CARMA_FAMILIES) {  // FamilyMismatch -> no estimate (manager.cpp:99-105)
             p.bucket[i] = -1;
             p.bytes[i] = UINT64_MAX;
         }
+        if (threadIdx.x < CARMA_FAMILIES) s_cnt[threadIdx.x] = 0;
+        __syncthreads();
+        uint32_t local = 0;
 #pragma unroll
         for (int k = 0; k < CARMA_FAMILIES; ++k) {
             const unsigned mask = __ballot_sync(0xffffffffu, b == k);
             if (!mask) continue;
             uint32_t at = 0;
-            if (lane == 0) at = atomicAdd(cursor + k, static_cast<uint32_t>(__popc(mask)));
+            if (lane == 0) at = atomicAdd(s_cnt + k, static_cast<uint32_t>(__popc(mask)));
             at = __shfl_sync(0xffffffffu, at, 0);
-            if (b == k) perm[off[k] + at + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+            if (b == k) local = at + __popc(mask & ((1u << lane) - 1u));
         }
+        __syncthreads();
+        if (threadIdx.x < CARMA_FAMILIES && s_cnt[threadIdx.x])
+            s_base[threadIdx.x] = atomicAdd(cursor + threadIdx.x, s_cnt[threadIdx.x]);
+        __syncthreads();
+        if (b >= 0 && b < CARMA_FAMILIES) perm[off[b] + s_base[b] + local] = static_cast<uint32_t>(i);
+        __syncthreads();  // s_cnt / s_base are reused by the next step
     }
 }
 
