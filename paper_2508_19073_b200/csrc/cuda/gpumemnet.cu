@@ -185,20 +185,18 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void group_bar(int g) { asm volatile("bar.sync %0, 256;" ::"r"(g + 1) : "memory"); }
 
-// 32 lanes x 32 bit, 8 consecutive columns per thread. The registers are
-// written asynchronously: tmem_wait8 (tcgen05.wait::ld) must run before any
-// use, and takes them as in/out operands so no use is hoisted above it.
+// 32 lanes x 32 bit, 8 consecutive columns per thread, and the wait for
+// them in the same asm statement: tcgen05.ld writes its registers
+// asynchronously, so nothing (a register spill included) may read them
+// before tcgen05.wait::ld — with the wait in a separate statement the
+// compiler could spill a destination in between and reload a stale value.
 __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&r)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(addr));
-}
-
-__device__ __forceinline__ void tmem_wait8(uint32_t (&r)[8]) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])
-                 :
-                 : "memory");
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+        : "r"(addr)
+        : "memory");
 }
 
 // Upper 16 bits of a (low half) and of b (high half): the bf16 truncations
@@ -272,8 +270,11 @@ __device__ __forceinline__ void transform_chunk(const P& p, const double (&raw)[
     }
 }
 
+// tcgen05.st reads its source registers asynchronously: the wait::st sits in
+// the same asm statement so the registers cannot be reused before it.
 __device__ __forceinline__ void tmem_st8(uint32_t addr, const float (&v)[8]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n\t"
+                 "tcgen05.wait::st.sync.aligned;" ::"r"(addr),
                  "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
                  "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
                  "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
@@ -403,7 +404,6 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
                 if (mem >= static_cast<int>(alive)) break;
                 uint32_t v[1][8];
                 tmem_ld8(tmem_row + mem * 8, v[0]);
-                tmem_wait8(v[0]);
                 const float4 b0 = reinterpret_cast<const float4*>(b + mem * 8)[0];
                 const float4 b1 = reinterpret_cast<const float4*>(b + mem * 8)[1];
                 const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
@@ -450,8 +450,6 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
                 uint32_t v[CP / 8][8];
 #pragma unroll
                 for (int c = 0; c < CP / 8; ++c) tmem_ld8(tmem_row + col + c * 8, v[c]);
-#pragma unroll
-                for (int c = 0; c < CP / 8; ++c) tmem_wait8(v[c]);
                 float lg[CP];
 #pragma unroll
                 for (int c = 0; c < CP; ++c) lg[c] = __uint_as_float(v[c / 8][c % 8]);
@@ -497,7 +495,6 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
                 for (int j = 0; j < 8; ++j) w[j] = pm[c * 8 + j];
                 tmem_st8(tmem_row + c * 8, w);
             }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         fence_before();
         group_bar(g);
@@ -506,8 +503,6 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
             uint32_t v[CP / 8][8];
 #pragma unroll
             for (int c = 0; c < CP / 8; ++c) tmem_ld8(tmem_row + c * 8, v[c]);
-#pragma unroll
-            for (int c = 0; c < CP / 8; ++c) tmem_wait8(v[c]);
             // The next tile's first MMA overwrites TMEM and the A tiles: its
             // fence_before + group barrier orders it after these reads.
             if (valid) {

@@ -336,3 +336,25 @@ def test_tf_and_mlp_banks_mix_by_family(gpu, models, tf_models):
         sel = fams == f
         _check(mdl, raw[sel], b[sel], by[sel], pr[sel], lg[sel])
     net.close()
+
+
+@pytest.mark.gpu
+def test_grouped_rows_read_in_place(gpu, models):
+    """Rows already grouped by family (the c2 batch) skip the permutation;
+    the answers equal those of the same rows shuffled."""
+    net = gm.GpuMemNet(gpu)
+    for f in (0, 1):
+        net.set_model(models[f])  # family 2 rows (last) have no model
+    parts = [cb.generate_synthetic_dataset(f, n, 80 + f) for f, n in ((0, 1000), (1, 2100), (2, 300))]
+    rows = np.concatenate([p.rows for p in parts])
+    fams = np.concatenate([np.full(len(p.rows), p.family, np.int8) for p in parts])
+    words, schema = cb.pack_features_bits(rows, fams)
+    net.set_bit_schema(schema)
+    gb, gby, _, _ = _predict_device(net, words, abi.ROWS_BITPACKED, len(rows))
+    order = np.random.default_rng(5).permutation(len(rows))
+    words2, schema2 = cb.pack_features_bits(rows[order], fams[order])
+    net.set_bit_schema(schema2)
+    sb, sby, _, _ = _predict_device(net, words2, abi.ROWS_BITPACKED, len(rows))
+    assert np.array_equal(gb[order], sb) and np.array_equal(gby[order], sby)
+    assert np.all(gb[fams == 2] == -1)
+    net.close()
