@@ -1139,7 +1139,9 @@ void launch_ensemble(const NnParams& p, int device, cudaStream_t s) {
         return;
     }
     const uint32_t room = kSmemLimit - p.m.smem_blob - 64;
-    const int g = static_cast<int>(std::min<uint32_t>(3, room / (kSplit * kATile)));
+    // The diagnostic variants (probabilities / per-member logits out) run one
+    // group per CTA: 256 threads, a full register budget, no spills.
+    const int g = DIAG ? 1 : static_cast<int>(std::min<uint32_t>(3, room / (kSplit * kATile)));
     if (g < 1) throw Unsupported("model too large for shared memory");
     if (p.m.cp <= 8) {
         if (g >= 3) launch_ensemble_t<FMT, 3, 8, DIAG>(p, device, s);
