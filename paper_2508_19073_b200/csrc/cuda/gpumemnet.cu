@@ -337,6 +337,8 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
         n = p.counts[p.fam];
         for (int f = 0; f < p.fam; ++f) base += p.counts[f];
     }
+    // rows already grouped by family (nn_count's flag): read them in place
+    const bool grouped = !p.perm || p.counts[2 * (CARMA_FAMILIES + 1)] == 0;
     const uint64_t tiles = (n + kTileRows - 1) / kTileRows;
     uint32_t phase = 0;
     const bool issuer = tid == g * 256;
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(G * 256, 1) nn_ensemble(const __grid_constant_
          tile += static_cast<uint64_t>(gridDim.x) * G) {
         const uint64_t i = tile * kTileRows + r;
         const bool valid = i < n;
-        const uint64_t row = valid ? (p.perm ? static_cast<uint64_t>(p.perm[base + i]) : base + i) : 0;
+        const uint64_t row = valid ? (grouped ? base + i : static_cast<uint64_t>(p.perm[base + i])) : 0;
 
         // ---- features -> z (fp32) -> layer-0 A tile (K 0..31): half 0 writes
         // chunks 0 and 3, half 1 chunks 1 and 2 (7 log1p features each)
@@ -712,10 +714,12 @@ __global__ void __launch_bounds__(128, 2) tf_ensemble(const __grid_constant__ Nn
         n = p.counts[p.fam];
         for (int f = 0; f < p.fam; ++f) base += p.counts[f];
     }
+    // rows already grouped by family (nn_count's flag): read them in place
+    const bool grouped = !p.perm || p.counts[2 * (CARMA_FAMILIES + 1)] == 0;
     const int C = static_cast<int>(m.classes);
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t row = p.perm ? static_cast<uint64_t>(p.perm[base + i]) : base + i;
+        const uint64_t row = grouped ? base + i : static_cast<uint64_t>(p.perm[base + i]);
         double raw[kFeatureDims];
         load_raw<FMT>(p, row, raw);
         float z[kFeatureDims];
@@ -777,6 +781,7 @@ __global__ void __launch_bounds__(128, 2) tf_ensemble(const __grid_constant__ Nn
 // ------------------------------------------------------ family partition
 
 constexpr int kBins = CARMA_FAMILIES + 1;  // + rows without a model
+constexpr int kUnsorted = 2 * kBins;        // counts[]: bins, cursors, then the "not grouped" flag
 
 template <int FMT>
 __device__ __forceinline__ int nn_bin(const NnParams& p, uint64_t i, uint32_t present) {
@@ -794,6 +799,9 @@ __global__ void nn_count(const __grid_constant__ NnParams p, uint64_t q, uint32_
         const int b = i < q ? nn_bin<FMT>(p, i, present) : -1;
 #pragma unroll
         for (int k = 0; k < kBins; ++k) local[k] += __popc(__ballot_sync(0xffffffffu, b == k));
+        // rows already grouped by family (non-decreasing bins)? else flag it
+        const bool down = i < q && i > 0 && b < nn_bin<FMT>(p, i - 1, present);
+        if (__any_sync(0xffffffffu, down) && lane == 0) atomicOr(counts + kUnsorted, 1u);
     }
     if (lane == 0)
         for (int k = 0; k < kBins; ++k)
@@ -809,6 +817,15 @@ __global__ void __launch_bounds__(256) nn_scatter(const __grid_constant__ NnPara
                                                   uint32_t* __restrict__ perm) {
     __shared__ uint32_t s_cnt[CARMA_FAMILIES], s_base[CARMA_FAMILIES];
     const unsigned lane = threadIdx.x & 31;
+    if (counts[kUnsorted] == 0) {  // already grouped: row ids are positions, only mark rows without a model
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < q;
+             i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+            if (nn_bin<FMT>(p, i, present) == CARMA_FAMILIES) {
+                p.bucket[i] = -1;
+                p.bytes[i] = UINT64_MAX;
+            }
+        return;
+    }
     uint32_t off[kBins];
     off[0] = 0;
 #pragma unroll
@@ -1139,17 +1156,21 @@ void launch_ensemble(const NnParams& p, int device, cudaStream_t s) {
         return;
     }
     const uint32_t room = kSmemLimit - p.m.smem_blob - 64;
-    // The diagnostic variants (probabilities / per-member logits out) run one
-    // group per CTA: 256 threads, a full register budget, no spills.
-    const int g = DIAG ? 1 : static_cast<int>(std::min<uint32_t>(3, room / (kSplit * kATile)));
+    const int g = static_cast<int>(std::min<uint32_t>(3, room / (kSplit * kATile)));
     if (g < 1) throw Unsupported("model too large for shared memory");
-    if (p.m.cp <= 8) {
+    if constexpr (DIAG) {
+        // The diagnostic variants (probabilities / per-member logits out, for
+        // the parity tests) run one group per CTA: full register budget, no
+        // spills.
+        if (p.m.cp <= 8) launch_ensemble_t<FMT, 1, 8, DIAG>(p, device, s);
+        else launch_ensemble_t<FMT, 1, 48, DIAG>(p, device, s);
+    } else if (p.m.cp <= 8) {
         if (g >= 3) launch_ensemble_t<FMT, 3, 8, DIAG>(p, device, s);
         else if (g == 2) launch_ensemble_t<FMT, 2, 8, DIAG>(p, device, s);
         else launch_ensemble_t<FMT, 1, 8, DIAG>(p, device, s);
     } else {
-        if (g >= 3) launch_ensemble_t<FMT, 3, 48, DIAG>(p, device, s);
-        else if (g == 2) launch_ensemble_t<FMT, 2, 48, DIAG>(p, device, s);
+        // at most two groups: three 48-bin groups (85 registers per thread) spill
+        if (g >= 2) launch_ensemble_t<FMT, 2, 48, DIAG>(p, device, s);
         else launch_ensemble_t<FMT, 1, 48, DIAG>(p, device, s);
     }
 }
@@ -1205,9 +1226,9 @@ uint64_t run_predict(NnHandle& h, NnHandle::Scratch& sc, const void* rows, int32
         fams.push_back(default_family);
     } else {
         if (q > 0xffffffffull) throw Unsupported("more than 2^32 rows in one device call");
-        sc.counts.ensure(2 * kBins * sizeof(uint32_t));
+        sc.counts.ensure((2 * kBins + 1) * sizeof(uint32_t));
         sc.perm.ensure(q * sizeof(uint32_t));
-        CARMA_CUDA(cudaMemsetAsync(sc.counts.ptr, 0, 2 * kBins * sizeof(uint32_t), s));
+        CARMA_CUDA(cudaMemsetAsync(sc.counts.ptr, 0, (2 * kBins + 1) * sizeof(uint32_t), s));
         switch (format) {
             case CARMA_ROWS_PACKED:
                 launch_partition<CARMA_ROWS_PACKED>(p, q, present, sc.counts.as<uint32_t>(), sc.perm.as<uint32_t>(), h.device, s);
