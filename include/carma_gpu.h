@@ -532,6 +532,38 @@ carma_status carma_pick_batch_device(int device, const carma_replay_config* cfg,
                                      const carma_pick_request* reqs, uint64_t n,
                                      int32_t* rr_cursor, int32_t* out_gpus, void* stream);
 
+/* ------------------------------------------- one-process multi-device */
+/* The run_sweep worker pool (runner.cpp:209-249) over the GPUs of one box:
+ * units (rows, replay jobs) are split into contiguous shards balanced by
+ * weight, one host thread per device drives its own handle / plan and
+ * stream, and each writes its shard's results straight into the caller's
+ * output buffers at the shard's offsets (pin them for asynchronous DMA). No
+ * collective: nothing is reduced across GPUs. Results are identical to the
+ * single-device calls. The first failing shard's status is returned. */
+
+/* bounds[p] .. bounds[p+1] (p < parts): contiguous shards of n units whose
+ * weights (NULL: 1 each) are balanced; shard p starts at the first unit whose
+ * prefix weight reaches total * p / parts. */
+carma_status carma_shard_ranges(const uint64_t* weights, uint64_t n, uint32_t parts, uint64_t* bounds);
+/* carma_knn_predict over n_handles handles (one per device; models installed
+ * on each), rows sharded evenly. */
+carma_status carma_knn_predict_multi(carma_knn* const* handles, uint32_t n_handles,
+                                     const carma_feature_row* rows, const int8_t* family,
+                                     int32_t default_family, uint64_t q, int32_t* bucket_out,
+                                     uint64_t* bytes_out);
+/* carma_nn_predict likewise. */
+carma_status carma_nn_predict_multi(carma_nn* const* handles, uint32_t n_handles, const carma_feature_row* rows,
+                                    const int8_t* family, int32_t default_family, uint64_t q,
+                                    int32_t* bucket_out, uint64_t* bytes_out);
+/* carma_replay_batch over n_devices devices: jobs sharded by task count, each
+ * device replays its shard's traces; outputs laid out as carma_replay_batch's. */
+carma_status carma_replay_batch_multi(const int32_t* devices, uint32_t n_devices,
+                                      const carma_replay_config* configs, uint32_t n_configs,
+                                      const carma_task* tasks, const uint64_t* trace_offsets, uint32_t n_traces,
+                                      const carma_replay_job* jobs, uint32_t n_jobs,
+                                      carma_task_result* task_results, carma_trace_result* trace_results,
+                                      carma_gpu_result* gpu_results);
+
 /* ------------------------------------------------------------ probes */
 /* Measured fp64 add/mul issue throughput of `device` (separately rounded
  * ops per second, 1 op = 1 flop): the roofline denominator of the k-NN

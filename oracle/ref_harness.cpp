@@ -223,6 +223,71 @@ double ref_bench_predict(int family, uint64_t samples, uint64_t seed, uint64_t k
     }
 }
 
+// The FeatureVector summary the product's batch API consumes (the
+// carma_feature_row layout of include/carma_gpu.h, restated here so the
+// reference side needs no product header).
+struct FeatRow {
+    uint64_t n_linear, n_batchnorm, n_dropout, n_conv;
+    uint64_t batch_size, total_params, total_activations;
+    double act_cos, act_sin;
+    int32_t kind[3];
+    int32_t has_layers;
+    uint64_t tuple_acts[3];
+    uint64_t tuple_params[3];
+};
+static_assert(sizeof(FeatRow) == 136, "FeatRow must match carma_feature_row");
+
+// estimate_learned (estimators.cpp:540-551) over n feature rows on `threads`
+// host threads, each row routed to the model of its family trained exactly as
+// provision_estimators does (seed est_seed + 101 * family, runner.cpp:31-32).
+// The FeatureVector carries the first / middle / last layer tuples, which is
+// all scalar_features reads (estimators.cpp:317-342): with three tuples
+// [first, middle, last], L[size/2] is the middle one.
+int ref_estimate_rows(const FeatRow* rows, const int8_t* family, uint64_t n, uint64_t samples,
+                      uint64_t est_seed, uint64_t k, int threads, int32_t* out_bucket, uint64_t* out_bytes) {
+    try {
+        for (int f = 0; f < 3; ++f) model_for(f, samples, est_seed + 101ull * static_cast<uint64_t>(f), k);
+        std::vector<std::thread> pool;
+        std::atomic<int> bad{0};
+        std::string err;
+        std::mutex err_mu;
+        for (int t = 0; t < threads; ++t) {
+            pool.emplace_back([&, t]() {
+                try {
+                    const uint64_t b = n * static_cast<uint64_t>(t) / static_cast<uint64_t>(threads);
+                    const uint64_t e = n * static_cast<uint64_t>(t + 1) / static_cast<uint64_t>(threads);
+                    FeatureVector fv;
+                    fv.layer_tuples.resize(3);
+                    for (uint64_t i = b; i < e; ++i) {
+                        const FeatRow& r = rows[i];
+                        const int f = family[i];
+                        fv.n_linear = r.n_linear; fv.n_batchnorm = r.n_batchnorm; fv.n_dropout = r.n_dropout;
+                        fv.n_conv = r.n_conv; fv.batch_size = r.batch_size; fv.total_params = r.total_params;
+                        fv.total_activations = r.total_activations; fv.act_cos = r.act_cos; fv.act_sin = r.act_sin;
+                        fv.layer_tuples.resize(r.has_layers ? 3 : 0);
+                        for (int j = 0; r.has_layers && j < 3; ++j)
+                            fv.layer_tuples[static_cast<std::size_t>(j)] = {r.kind[j], r.tuple_acts[j], r.tuple_params[j]};
+                        const LearnedEstimator& est =
+                            model_for(f, samples, est_seed + 101ull * static_cast<uint64_t>(f), k);
+                        MemoryEstimate m = estimate_learned(est, fv, fam(f));
+                        out_bucket[i] = *m.bucket;
+                        out_bytes[i] = m.bytes;
+                    }
+                } catch (const std::exception& ex) {
+                    std::lock_guard<std::mutex> lock(err_mu);
+                    err = ex.what();
+                    bad = 1;
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        if (bad) throw CarmaError(err);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 // Trace generation (traces.cpp:266-306): rows as (submit, catalog index, epochs).
 int ref_gen_trace(int mix, uint64_t seed, double* submit, int32_t* cat_idx,
                   uint64_t* epochs, uint64_t cap, uint64_t* n_out) {
@@ -472,6 +537,56 @@ double ref_bench_sweep(const RefConfig* base, int mix, uint64_t seed0, uint64_t 
     } catch (const std::exception& e) {
         fail(e);
         return -1.0;
+    }
+}
+
+// run_simulation for every (config, seed) job of a generated-trace sweep on
+// `threads` host threads (run_sweep's pool, runner.cpp:209-249): job
+// j = c * n_seeds + s runs cfgs[c] on generate_trace(mix, seed0 + s). Outputs
+// per job (rout[j]; GPU results at j * G) and per task (tout at j *
+// tasks_per_trace, materialized order); every trace must have
+// tasks_per_trace tasks.
+int ref_run_jobs(const RefConfig* cfgs, int n_cfg, int mix, uint64_t seed0, uint64_t n_seeds, int threads,
+                 uint64_t tasks_per_trace, RefTaskOut* tout, RefTraceOut* rout, double* gpu_energy,
+                 double* gpu_smact, uint64_t* gpu_peak) {
+    try {
+        const uint64_t n_jobs = static_cast<uint64_t>(n_cfg) * n_seeds;
+        std::atomic<uint64_t> next{0};
+        std::atomic<int> bad{0};
+        std::string err;
+        std::mutex err_mu;
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t) {
+            pool.emplace_back([&]() {
+                for (;;) {
+                    const uint64_t j = next.fetch_add(1);
+                    if (j >= n_jobs || bad) return;
+                    try {
+                        const RefConfig& c = cfgs[j / n_seeds];
+                        const uint64_t g = static_cast<uint64_t>(c.gpu_count);
+                        RunConfig rc = make_rc(c);
+                        rc.mix = static_cast<TraceMix>(mix);
+                        rc.trace_seed = seed0 + j % n_seeds;
+                        std::vector<TaskSpec> tasks = materialize_trace(generate_trace(*rc.mix, rc.trace_seed));
+                        if (tasks.size() != tasks_per_trace) throw CarmaError("unexpected trace length");
+                        std::vector<std::string> order;
+                        for (const auto& tk : tasks) order.push_back(tk.id);
+                        RunArtifacts art = run_simulation(rc);
+                        export_run(art, order, tout + j * tasks_per_trace, rout + j, gpu_energy + j * g,
+                                   gpu_smact + j * g, gpu_peak + j * g);
+                    } catch (const std::exception& ex) {
+                        std::lock_guard<std::mutex> lock(err_mu);
+                        err = ex.what();
+                        bad = 1;
+                    }
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        if (bad) throw CarmaError(err);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
     }
 }
 

@@ -187,6 +187,10 @@ SIGNATURES = {
     "carma_knn_train": (c_int, [c_void_p, c_int32, P, P, P, c_uint64, c_uint64, c_uint32, c_uint64, P, P, P, P, P]),
     "carma_host_split_order": (c_int, [c_uint64, c_uint64, P, POINTER(c_uint64)]),
     "carma_replay_plan_log": (c_int, [c_void_p, c_uint32, P, c_uint64, POINTER(c_uint64)]),
+    "carma_shard_ranges": (c_int, [P, c_uint64, c_uint32, P]),
+    "carma_knn_predict_multi": (c_int, [P, c_uint32, P, P, c_int32, c_uint64, P, P]),
+    "carma_nn_predict_multi": (c_int, [P, c_uint32, P, P, c_int32, c_uint64, P, P]),
+    "carma_replay_batch_multi": (c_int, [P, c_uint32, P, c_uint32, P, P, c_uint32, P, c_uint32, P, P, P]),
     # carma_host.h
     "carma_host_catalog_size": (c_int, []),
     "carma_host_catalog_entry": (c_int, [c_int, c_char_p, c_int, P, P, P, P]),
@@ -244,3 +248,21 @@ def ptr(a) -> int | None:
     if isinstance(a, int):
         return a
     raise TypeError(f"cannot pass {type(a)} across the C ABI")
+
+
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
+
+
+def stream_arg(stream=None, device: int | None = None) -> int:
+    """The caller stream handed to a device-resident C ABI call.
+
+    ``stream``: a torch.cuda.Stream, a raw cudaStream_t (int), or None for
+    torch's current stream on ``device``. NULL would select the handle's own
+    stream, which the caller's later work is not ordered after; the legacy
+    default stream (handle 0) is therefore passed as cudaStreamLegacy."""
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream(device)
+    if hasattr(stream, "cuda_stream"):
+        stream = stream.cuda_stream
+    return int(stream) or CUDA_STREAM_LEGACY

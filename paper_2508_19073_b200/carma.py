@@ -455,8 +455,11 @@ class ReplayPlan:
     def set_estimates_device(self, dev_ptr: int) -> None:
         check(lib.carma_replay_plan_set_estimates_device(self._h, dev_ptr))
 
-    def run(self, stream: int = 0) -> None:
-        check(lib.carma_replay_plan_run(self._h, stream or None))
+    def run(self, stream=None) -> None:
+        """Runs every job. stream None: on the plan's own stream (results()
+        waits for it); a torch stream / cudaStream_t: ordered after the work
+        already queued there, and that stream's later work after the replay."""
+        check(lib.carma_replay_plan_run(self._h, None if stream is None else abi.stream_arg(stream)))
 
     def upload_tasks(self, tasks: np.ndarray) -> None:
         check(lib.carma_replay_plan_upload_tasks(self._h, ptr(np.ascontiguousarray(tasks, abi.task_dtype))))
@@ -542,6 +545,43 @@ def replay(configs: np.ndarray, task_lists: Sequence[np.ndarray], jobs: Iterable
         raise abi.CarmaError(abi.CARMA_OK + (3 if st < 0 else st),
                              f"{int(bad.sum())} job(s) failed (first status {st})")
     return res
+
+
+def predict_multi(knns: Sequence["GpuKnn"], rows: np.ndarray, family=None, default_family: int = 0):
+    """carma_knn_predict_multi: rows sharded over the handles (one per device,
+    models installed on each), one host thread per device, results gathered
+    into one host buffer at the shard offsets."""
+    q = len(rows)
+    rows = np.ascontiguousarray(rows, abi.feature_row_dtype)
+    fam = None if family is None else np.ascontiguousarray(family, np.int8)
+    hs = (ctypes.c_void_p * len(knns))(*[k.handle.value for k in knns])
+    bucket = np.zeros(q, np.int32)
+    nbytes = np.zeros(q, np.uint64)
+    check(lib.carma_knn_predict_multi(ctypes.cast(hs, ctypes.c_void_p), len(knns), ptr(rows), ptr(fam),
+                                      default_family, q, ptr(bucket), ptr(nbytes)))
+    return bucket, nbytes
+
+
+def replay_multi(devices: Sequence[int], configs: np.ndarray, tasks: np.ndarray, trace_offsets: np.ndarray,
+                 jobs: np.ndarray, task_results: bool = True) -> ReplayResult:
+    """carma_replay_batch_multi: jobs sharded by task count over `devices`,
+    one host thread + plan + stream per device, outputs in job order."""
+    configs = np.ascontiguousarray(configs, abi.replay_config_dtype)
+    tasks = np.ascontiguousarray(tasks, abi.task_dtype)
+    offs = np.ascontiguousarray(trace_offsets, np.uint64)
+    jobs = np.ascontiguousarray(jobs, abi.job_dtype)
+    n_t = np.diff(offs.astype(np.int64))[jobs["trace"]]
+    n_g = configs["gpu_count"][jobs["config"]].astype(np.int64)
+    t_off = np.concatenate([[0], np.cumsum(n_t)])
+    g_off = np.concatenate([[0], np.cumsum(n_g)])
+    tr = np.zeros(int(t_off[-1]) if task_results else 0, abi.task_result_dtype)
+    jr = np.zeros(len(jobs), abi.trace_result_dtype)
+    gr = np.zeros(int(g_off[-1]), abi.gpu_result_dtype)
+    dv = np.ascontiguousarray(devices, np.int32)
+    check(lib.carma_replay_batch_multi(ptr(dv), len(dv), ptr(configs), len(configs), ptr(tasks), ptr(offs),
+                                       len(offs) - 1, ptr(jobs), len(jobs), ptr(tr) if task_results else None,
+                                       ptr(jr), ptr(gr)))
+    return ReplayResult(tr, jr, gr, t_off, g_off)
 
 
 # ----------------------------------------------------------------- runner
@@ -718,21 +758,29 @@ class FusedReplay:
         self.d_rows = torch.from_numpy(self.packed.view(np.uint8).reshape(-1)).to(f"cuda:{device}")
         self.d_bucket = torch.empty(len(m.tasks), dtype=torch.int32, device=f"cuda:{device}")
         self.d_bytes = torch.empty(len(m.tasks), dtype=torch.int64, device=f"cuda:{device}")
+        # one stream orders the estimator pre-pass before the replay that reads its bytes
+        self.stream = torch.cuda.Stream(device)
         jobs = np.zeros(1, abi.job_dtype)
         self.plan = ReplayPlan(cfg, m.tasks, np.array([0, len(m.tasks)], np.uint64), jobs, device)
         self.plan.set_estimates_device(self.d_bytes.data_ptr())
 
-    def run(self) -> None:
+    def run(self, stream=None) -> None:
+        """Pre-pass then replay, both on the replay's own stream; `stream`
+        (default: torch's current stream) waits for both."""
         import torch
-        s = torch.cuda.current_stream(self.device)
+        caller = torch.cuda.current_stream(self.device) if stream is None else stream
+        s = self.stream
+        s.wait_stream(caller)  # inputs the caller wrote before this call
         if self.neural:
             self.knn.predict_device(self.d_rows, abi.ROWS_PACKED, len(self.m.tasks), self.d_bucket, self.d_bytes,
-                                    stream=s.cuda_stream)
+                                    stream=s)
         else:
             check(lib.carma_knn_predict_device(self.knn.handle, self.d_rows.data_ptr(), abi.ROWS_PACKED, None, 0,
                                                len(self.m.tasks), self.d_bucket.data_ptr(), self.d_bytes.data_ptr(),
-                                               None, None, s.cuda_stream))
-        self.plan.run(s.cuda_stream)
+                                               None, None, abi.stream_arg(s)))
+        self.plan.run(s)
+        if hasattr(caller, "wait_stream"):
+            caller.wait_stream(s)
 
     def results(self) -> ReplayResult:
         return self.plan.results()

@@ -78,6 +78,44 @@ struct PinnedBuffer {
     ~PinnedBuffer() { release(); }
 };
 
+// Orders the reuse of a handle's shared device buffers (scratch, counters)
+// across streams: a call that enqueues work touching them on stream s first
+// makes s wait for the last user's work (acquire), then marks its own work
+// as the last user (release). Host-side reuse (pinned staging, host-stream
+// pipelines) waits on the host instead (host_wait).
+struct StreamFence {
+    cudaEvent_t ev = nullptr;
+    bool live = false;
+    void acquire(cudaStream_t s) {
+        if (live) CARMA_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    }
+    void release(cudaStream_t s) {
+        if (!ev) CARMA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CARMA_CUDA(cudaEventRecord(ev, s));
+        live = true;
+    }
+    void host_wait() {
+        if (live) CARMA_CUDA(cudaEventSynchronize(ev));
+    }
+    void destroy() {
+        if (ev) cudaEventDestroy(ev);
+        ev = nullptr;
+        live = false;
+    }
+};
+
+// Makes `caller` (when given) wait for everything queued so far on `own`:
+// device calls that run on a handle's stream stay ordered before the
+// caller's later work (and inside its CUDA-event timings).
+inline void join_stream(cudaStream_t caller, cudaStream_t own) {
+    if (!caller || caller == own) return;
+    cudaEvent_t ev;
+    CARMA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CARMA_CUDA(cudaEventRecord(ev, own));
+    CARMA_CUDA(cudaStreamWaitEvent(caller, ev, 0));
+    CARMA_CUDA(cudaEventDestroy(ev));
+}
+
 // Scoped device switch.
 struct DeviceGuard {
     int prev = -1;

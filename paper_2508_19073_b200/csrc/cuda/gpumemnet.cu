@@ -1090,6 +1090,7 @@ struct NnHandle {
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // call start, ensemble start, ensemble end
     bool timed = false;
     uint64_t last_launches = 0, last_mmas = 0;
+    StreamFence fence;                 // last device-stream user of scratch[0]
     PinnedBuffer counts_host;          // family counts of the last device call
     cudaStream_t counts_stream = nullptr;
     bool counts_pending = false;
@@ -1300,6 +1301,7 @@ carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int3
         const bool fam_pinned = !family || is_pinned(family);
         const bool out_pinned = (!bucket_out || is_pinned(bucket_out)) && (!bytes_out || is_pinned(bytes_out));
         h->timed = false;
+        h->fence.host_wait();  // a device call may still use scratch[0]
         uint64_t launches = 0, beg = 0, cnt = 0;
         for (uint64_t c = 0; beg < q; ++c, beg += cnt) {
             NnHandle::Scratch& sc = h->scratch[c & 1];
@@ -1383,6 +1385,7 @@ carma_status carma_nn_destroy(carma_nn* hh) {
             cudaDeviceSynchronize();
             for (auto& m : h->model) m.blob.release();
             h->counts_host.release();
+            h->fence.destroy();
             for (auto& sc : h->scratch) {
                 for (DeviceBuffer* b : {&sc.rows, &sc.family, &sc.perm, &sc.counts, &sc.bucket, &sc.bytes}) b->release();
                 sc.stage_rows.release();
@@ -1449,8 +1452,10 @@ carma_status carma_nn_predict_device(carma_nn* hh, const void* rows, int32_t for
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
         h->timed = true;
         NnHandle::Scratch& sc = h->scratch[0];
+        h->fence.acquire(s);  // scratch[0] may be in use on another stream
         h->last_launches = run_predict(*h, sc, rows, format, family, default_family, q, bucket_out, bytes_out, probs,
                                        logits, s);
+        h->fence.release(s);
         // MMA count of this call: from the family counts, read back (async,
         // into pinned memory) and summed by carma_nn_last_timing
         h->last_mmas = 0;

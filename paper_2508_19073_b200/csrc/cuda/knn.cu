@@ -1102,6 +1102,7 @@ struct KnnHandle {
         PinnedBuffer stage_rows, stage_family;
     } scratch[2];
     DeviceBuffer evals;
+    StreamFence fence;        // last device-stream user of scratch[0] + evals
     DeviceBuffer train_rows;  // carma_knn_train: the uploaded dataset
     double act[16] = {0};
     carma_bit_schema schema{};
@@ -1327,6 +1328,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
         const bool fam_pinned = !family || is_pinned(family);
         const bool out_pinned = (!bucket_out || is_pinned(bucket_out)) && (!bytes_out || is_pinned(bytes_out));
         h->timed = false;
+        h->fence.host_wait();  // a device call may still use scratch[0] / evals
         h->evals.ensure(16);
         CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 16, h->pipe[0]));
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
@@ -1429,6 +1431,7 @@ carma_status carma_knn_destroy(carma_knn* hh) {
                 sc.stage_rows.release(); sc.stage_family.release();
             }
             h->evals.release();
+            h->fence.destroy();
             for (auto& e : h->ev)
                 if (e) cudaEventDestroy(e);
             cudaStreamDestroy(h->stream);
@@ -1597,11 +1600,13 @@ carma_status carma_knn_predict_device(carma_knn* hh, const void* rows, int32_t f
         DeviceGuard g(h->device);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
         h->evals.ensure(16);
+        h->fence.acquire(s);  // scratch[0] / evals may be in use on another stream
         CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 16, s));
         h->timed = true;
         h->last_launches = run_pipeline(*h, h->scratch[0], rows, format, family, default_family, q,
                                         bucket_out, bytes_out, topk_d2, topk_idx,
                                         h->evals.as<unsigned long long>(), s);
+        h->fence.release(s);
     });
 }
 

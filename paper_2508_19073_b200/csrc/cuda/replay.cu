@@ -581,6 +581,8 @@ carma_status carma_replay_plan_run(carma_replay_plan* hp, void* stream) {
             CARMA_CUDA(cudaEventDestroy(ev));
         }
         run_plan(*pl);
+        // ... and the caller's later work (and its event timings) after the replay
+        join_stream(static_cast<cudaStream_t>(stream), pl->stream);
     });
 }
 

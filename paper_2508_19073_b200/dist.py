@@ -14,21 +14,17 @@ from typing import Callable, List, Sequence, Tuple
 import numpy as np
 
 
-def balanced_shards(weights: Sequence[float], world: int) -> List[Tuple[int, int]]:
+def balanced_shards(weights: Sequence[int], world: int) -> List[Tuple[int, int]]:
     """Contiguous [begin, end) ranges, one per rank, balancing the summed weight
-    (rows: 1 each; replay jobs: their task counts)."""
-    w = np.asarray(weights, np.float64)
-    n = len(w)
-    if world <= 1 or n == 0:
-        return [(0, n)] + [(n, n)] * max(0, world - 1)
-    cum = np.concatenate([[0.0], np.cumsum(w)])
-    total = cum[-1]
-    cuts = [0]
-    for r in range(1, world):
-        cuts.append(int(np.searchsorted(cum, total * r / world, side="left")))
-    cuts.append(n)
-    cuts = np.maximum.accumulate(np.clip(cuts, 0, n))
-    return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+    (rows: 1 each; replay jobs: their task counts). The rule is the native
+    multi-device driver's (carma_shard_ranges), so a rank of a multi-process
+    run and a device of the one-process driver get the same units."""
+    from . import abi
+    w = np.ascontiguousarray(weights, np.uint64)
+    world = max(1, int(world))
+    bounds = np.zeros(world + 1, np.uint64)
+    abi.check(abi.lib.carma_shard_ranges(w.ctypes.data if len(w) else None, len(w), world, bounds.ctypes.data))
+    return [(int(bounds[r]), int(bounds[r + 1])) for r in range(world)]
 
 
 def gather_to_root(local: np.ndarray, rank: int, world: int, dist=None) -> np.ndarray | None:

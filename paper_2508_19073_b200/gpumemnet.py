@@ -141,10 +141,11 @@ class GpuMemNet:
         return bucket, nbytes
 
     def predict_device(self, rows, fmt: int, q: int, bucket, nbytes, family=None, default_family: int = 0,
-                       probs=None, logits=None, stream: int = 0) -> None:
-        """Device-resident predict (torch tensors or raw device pointers)."""
+                       probs=None, logits=None, stream=None) -> None:
+        """Device-resident predict (torch tensors or raw device pointers) on
+        `stream` (torch stream or cudaStream_t; None = torch's current stream)."""
         check(lib.carma_nn_predict_device(self._h, ptr(rows), fmt, ptr(family), default_family, q, ptr(bucket),
-                                          ptr(nbytes), ptr(probs), ptr(logits), stream or None))
+                                          ptr(nbytes), ptr(probs), ptr(logits), abi.stream_arg(stream, self.device)))
 
     def set_act_table(self, table: np.ndarray) -> None:
         check(lib.carma_nn_set_act_table(self._h, ptr(np.ascontiguousarray(table, np.float64))))

@@ -14,7 +14,16 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_uint32, c_uint
 
 import numpy as np
 
-from paper_2508_19073_b200 import abi
+# Enum values of the reference's public types (manager.hpp:15-19, gpu.hpp:14,
+# traces.hpp). Kept here, not imported from the product package, so a process
+# that only drives the reference (bench.py --impl reference) never maps
+# libcarma_b200.so.
+POLICY = {"exclusive": 0, "rr": 1, "magm": 2, "lug": 3, "mug": 4}
+MODE = {"streams": 0, "mps": 1, "mig": 2}
+ESTIMATOR = {"none": 0, "oracle": 1, "analytical": 2, "static_graph": 3, "learned": 4}
+MIX = {"t90": 0, "t60": 1}
+GiB = 1 << 30
+MiB = 1 << 20
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "build", "liboracle.so")
@@ -60,6 +69,8 @@ def load_ref():
     lib.ref_bench_sweep.restype = c_double
     lib.ref_bench_sweep.argtypes = [P, c_int, c_uint64, c_uint64, P, c_int, c_int, POINTER(c_uint64),
                                     POINTER(c_double)]
+    lib.ref_estimate_rows.argtypes = [P, P, c_uint64, c_uint64, c_uint64, c_uint64, c_int, P, P]
+    lib.ref_run_jobs.argtypes = [P, c_int, c_int, c_uint64, c_uint64, c_int, c_uint64, P, P, P, P, P]
     lib.ref_run_sweep.argtypes = [P, c_int, c_int, P, c_int, c_char_p, c_uint64]
     lib.ref_timeline.argtypes = [P, c_int, c_uint64, c_char_p, c_uint64]
     lib.ref_logs.argtypes = [P, c_int, c_uint64, c_char_p, c_uint64, c_char_p, c_uint64]
@@ -89,16 +100,16 @@ ref_trace_out_dtype = np.dtype([
 
 
 def ref_config(policy="magm", estimator="none", mode="mps", rr_pre=False, max_smact=0.8, min_free=None,
-               margin=2 * abi.GiB, window=60.0, gpu_count=4, capacity=40 * abi.GiB, block=512 * abi.MiB,
+               margin=2 * GiB, window=60.0, gpu_count=4, capacity=40 * GiB, block=512 * MiB,
                est_seed=11, est_k=5, est_samples=4000, mig=(), sample_interval=0.0, log_flags=0):
     c = np.zeros(1, ref_config_dtype)
     c["log_flags"] = log_flags
     c["sample_interval"] = sample_interval
     c["mig_count"] = len(mig)
     c["mig_fractions"][0, : len(mig)] = mig
-    c["policy"] = abi.POLICY[policy]
-    c["estimator"] = abi.ESTIMATOR[estimator]
-    c["mode"] = abi.MODE[mode]
+    c["policy"] = POLICY[policy]
+    c["estimator"] = ESTIMATOR[estimator]
+    c["mode"] = MODE[mode]
     c["rr_apply_preconditions"] = int(rr_pre)
     c["max_smact"] = max_smact
     c["has_min_free"] = int(min_free is not None)
@@ -116,6 +127,7 @@ def ref_config(policy="magm", estimator="none", mode="mps", rr_pre=False, max_sm
 
 def replay_config_from(c):
     """The carma_replay_config equivalent of a ref config row."""
+    from paper_2508_19073_b200 import abi
     r = np.zeros(1, abi.replay_config_dtype)
     for f in ("policy", "mode", "gpu_count", "rr_apply_preconditions", "max_smact", "monitor_window",
               "gpu_capacity", "alloc_block"):
@@ -139,7 +151,7 @@ def ref_run(ref, cfg, mix=None, seed=1, path=None, cap=1 << 20):
     ge = np.zeros(g)
     gs = np.zeros(g)
     gp = np.zeros(g, np.uint64)
-    rc = ref.ref_run(_ptr(cfg), abi.MIX[mix] if mix else -1, seed, path.encode() if path else None,
+    rc = ref.ref_run(_ptr(cfg), MIX[mix] if mix else -1, seed, path.encode() if path else None,
                      _ptr(tout), cap, _ptr(rout), _ptr(ge), _ptr(gs), _ptr(gp))
     if rc != 0:
         raise RuntimeError(ref.ref_last_error().decode())
@@ -148,6 +160,7 @@ def ref_run(ref, cfg, mix=None, seed=1, path=None, cap=1 << 20):
 
 
 def oracle_replay(olib, cfg, tasks):
+    from paper_2508_19073_b200 import abi
     n = len(tasks)
     tout = np.zeros(n, abi.task_result_dtype)
     tr = np.zeros(1, abi.trace_result_dtype)
@@ -170,3 +183,35 @@ def oracle_predict(olib, m, raw, k=None):
                                  m.bucket_range, _ptr(raw), q, _ptr(b), _ptr(by), _ptr(d2), _ptr(idx))
     assert rc == 0
     return b, by, d2, idx
+
+
+def ref_estimate_rows(ref, rows, family, samples=4000, est_seed=11, k=5, threads=None):
+    """The reference's estimate_learned over feature rows (abi.feature_row_dtype),
+    per-row family, models as provision_estimators trains them; host threads."""
+    rows = np.ascontiguousarray(rows)
+    family = np.ascontiguousarray(family, np.int8)
+    n = len(rows)
+    b = np.zeros(n, np.int32)
+    by = np.zeros(n, np.uint64)
+    rc = ref.ref_estimate_rows(_ptr(rows), _ptr(family), n, samples, est_seed, k, threads or os.cpu_count() or 1,
+                               _ptr(b), _ptr(by))
+    if rc != 0:
+        raise RuntimeError(ref.ref_last_error().decode())
+    return b, by
+
+
+def ref_run_jobs(ref, cfgs, mix, seed0, n_seeds, tasks_per_trace, threads=None):
+    """run_simulation of every (config, seed) job (job = c * n_seeds + s)."""
+    cfgs = np.ascontiguousarray(cfgs, ref_config_dtype)
+    nj = len(cfgs) * n_seeds
+    g = int(cfgs["gpu_count"].max())
+    assert (cfgs["gpu_count"] == g).all()
+    tout = np.zeros(nj * tasks_per_trace, ref_task_out_dtype)
+    rout = np.zeros(nj, ref_trace_out_dtype)
+    ge, gs = np.zeros(nj * g), np.zeros(nj * g)
+    gp = np.zeros(nj * g, np.uint64)
+    rc = ref.ref_run_jobs(_ptr(cfgs), len(cfgs), MIX[mix], seed0, n_seeds, threads or os.cpu_count() or 1,
+                          tasks_per_trace, _ptr(tout), _ptr(rout), _ptr(ge), _ptr(gs), _ptr(gp))
+    if rc != 0:
+        raise RuntimeError(ref.ref_last_error().decode())
+    return tout, rout, ge, gs, gp

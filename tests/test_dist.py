@@ -109,3 +109,16 @@ def test_sharded_neural_estimates_equal_single_process(tmp_path):
     m = gm.load_default_models()[1]
     raw = cb.scalar_features(cb.generate_synthetic_dataset(1, 1001, 9).rows)
     assert np.array_equal(got, gpumemnet_oracle.forward(m.spec()[0], m.params, raw)[3])
+
+
+def test_native_shard_rule_matches_restatement():
+    """carma_shard_ranges (the native multi-device driver's rule, also used by
+    dist.balanced_shards) against a numpy restatement of the rule."""
+    rng = np.random.default_rng(3)
+    for n, world in ((0, 3), (1, 4), (7, 8), (1000, 3), (400_000, 8), (33, 33)):
+        w = rng.integers(1, 200, n)
+        cum = np.concatenate([[0.0], np.cumsum(w.astype(np.float64))])
+        cuts = [0] + [min(int(np.searchsorted(cum, cum[-1] * r / world, side="left")), n)
+                      for r in range(1, world)] + [n]
+        cuts = np.maximum.accumulate(cuts)
+        assert balanced_shards(w, world) == [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]

@@ -231,6 +231,47 @@ def test_fused_c5_prefix_matches_oracle(gpu, olib, estimator):
     assert res.job_gpus(0).tobytes() == og.tobytes()
 
 
+def test_fused_orders_prepass_before_replay(gpu, olib):
+    """FusedReplay regression (round-1 race): the k-NN pre-pass and the replay
+    that reads its bytes run on one stream, after the caller's queued work.
+    The caller's stream is kept busy (a device sleep) and then overwrites the
+    estimates with a sentinel (0 bytes: every task fits anywhere); if the
+    replay read them before the pre-pass rewrote them, placements would
+    differ from the oracle's learned run."""
+    import torch
+    from cases import model
+    m = cb.materialize_trace(cb.generate_uniform_trace(4000, 3.0, 7))
+    cfg = cfg_of("magm", gpu_count=8, window=5.0)
+    knn = cb.GpuKnn(gpu)
+    for f in (1, 2):
+        knn.set_model(model(f))
+    want = m.tasks.copy()
+    raw = cb.scalar_features(m.features)
+    e = np.zeros(len(m.tasks), np.uint64)
+    for f in set(m.family.tolist()):
+        sel = m.family == f
+        e[sel] = oracle_predict(olib, model(f), raw[sel])[1]
+    want["estimate"] = e
+    rc, ot, otr, og = oracle_replay(olib, cfg, want)
+    assert rc == 0 and int(otr["oom_count"]) >= 0
+    fused = cb.FusedReplay(m, cfg, knn, gpu)
+    side = torch.cuda.Stream()
+    for caller in (torch.cuda.current_stream(), side):
+        for _ in range(3):
+            with torch.cuda.stream(caller):
+                torch.cuda._sleep(20_000_000)       # ~10 ms of queued caller work
+                fused.d_bytes.fill_(0)               # sentinel, ordered before the pre-pass
+                fused.run(stream=caller)
+                after = fused.d_bytes.clone()        # caller work after run() sees the pre-pass output
+            res = fused.results()
+            assert res.job_tasks(0).tobytes() == ot.tobytes()
+            assert res.traces[0:1].tobytes() == np.array([otr]).tobytes()
+            torch.cuda.synchronize()
+            assert np.array_equal(after.cpu().numpy().view(np.uint64), e)
+    fused.close()
+    knn.close()
+
+
 # MIG (gpu.cpp:29-51, :151-195; manager.cpp:125-134, :176-187, :236-243).
 # Instance 0 holds the largest catalog task, so every run terminates (the
 # reference retries crashed tasks exclusively on instance 0).

@@ -133,3 +133,27 @@ def test_oracle_large_trace_matches_reference(ref, olib, tmp_path):
     assert np.array_equal(ot["gpu"][:, 0], tout["gpu0"])
     assert otr["energy_mj"] == rout["energy_mj"] and otr["avg_jct"] == rout["avg_jct"]
     assert np.array_equal(og["mean_smact"], gs)
+
+
+def test_ref_batch_entries_match_single_calls(ref, olib):
+    """The full-size parity tests' reference entries (ref_estimate_rows over
+    feature rows, ref_run_jobs over a threaded job pool) agree with the
+    reference's per-dataset predict and single run_simulation, and the oracle."""
+    from oracle_bind import ref_estimate_rows, ref_run_jobs
+    rows = np.concatenate([cb.generate_synthetic_dataset(f, 1200, 40 + f).rows for f in (0, 1, 2)])
+    fam = np.repeat(np.array([0, 1, 2], np.int8), 1200)
+    b, by = ref_estimate_rows(ref, rows, fam, threads=3)
+    for f in (0, 1, 2):
+        sel = fam == f
+        ob, oby, _, _ = oracle_predict(olib, cb.fit_knn(f, 4000, 11 + 101 * f, 5), cb.scalar_features(rows[sel]))
+        assert np.array_equal(b[sel], ob) and np.array_equal(by[sel], oby)
+    cfgs = np.concatenate([ref_config(policy=p, max_smact=0.8) for p in ("exclusive", "rr", "magm", "lug")])
+    tout, rout, ge, gs, gp = ref_run_jobs(ref, cfgs, "t90", 3, 6, 90, threads=3)
+    for c, p in enumerate(("exclusive", "rr", "magm", "lug")):
+        for s in (0, 5):
+            j = c * 6 + s
+            one = ref_run(ref, ref_config(policy=p, max_smact=0.8), mix="t90", seed=3 + s)
+            assert tout[j * 90:(j + 1) * 90].tobytes() == one[0].tobytes()
+            assert rout[j].tobytes() == one[1].tobytes()
+            assert ge[j * 4:(j + 1) * 4].tobytes() == one[2].tobytes()
+            assert np.array_equal(gp[j * 4:(j + 1) * 4], one[4])
