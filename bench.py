@@ -5,11 +5,21 @@ Headline (BASELINE.json configs[1]): GPUMemNet estimates/s — the reference's
 k-NN memory-bin classifier over the 16,777,216-row CNN + Transformer batch
 (generate_synthetic_dataset(CNN, 8388608, 2024) + (Transformer, 8388608, 2025)),
 routed per family to the models provision_estimators trains (seeds 112, 213).
-Secondary (configs[3], same JSON line under "replay"): trace-replay placed
-tasks/s for the policy sweep t90 seeds 1..100000 x {exclusive, rr, magm, lug}.
+The paper's neural GPUMemNet ensembles (MLP on tcgen05, Transformer on CUDA
+cores) run over the same rows (line key "neural").
+Second half of the metric (configs[3], line key "replay", printed last so the
+driver's stdout tail keeps it): trace-replay placed tasks/s for the policy
+sweep t90 seeds 1..100000 x {exclusive, rr, magm, lug}.
 
-Scaling is weak: every rank runs the full per-GPU workload on its own GPU
-with no data-path collective; value = all ranks' units / max-over-ranks time.
+Scaling is STRONG: the 16.7M rows and the 400k replay jobs are the whole
+job; rank r of N takes the contiguous shard dist.balanced_shards gives it
+(rows by count, jobs by task count) with no data-path collective, and
+value = all units / max-over-ranks time. configs[4] (one 10^6-task trace),
+the scoring kernel and the small configs run at N = 1 only (a single trace
+does not shard; replicas would add nothing).
+
+The full measurement record goes to gpurun_out/bench_detail.json; stdout
+carries one compact JSON line.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl carma|reference]
 """
@@ -39,10 +49,16 @@ ALG_BYTES_PER_ESTIMATE = 164       # 19 f64 in + i32 bucket + u64
 ALG_BYTES_PER_TASK = 80            # 45 B in + 35 B out per placed task
 FLOPS_PER_EVAL = 58                # 19 x (sub, mul, add) + 1 weight mul, FMA-free
 FLOPS_PER_F32_EVAL = 48            # fp32 pre-filter: 16 dims x (sub + fma)
+FEATURE_ROW_BYTES = 136
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def host_cpus() -> dict:
+    import psutil
+    return {"logical_cpus": psutil.cpu_count(logical=True), "physical_cores": psutil.cpu_count(logical=False)}
 
 
 # ------------------------------------------------------------------ clocks
@@ -111,19 +127,26 @@ class Clocks:
 
 # ------------------------------------------------------------------ dist
 class Dist:
-    def __init__(self, gpus: int):
+    """One process per GPU (torchrun); NCCL only for the barrier and the
+    max-over-ranks of the timings (no data-path collective)."""
+
+    def __init__(self, gpus: int, backend: str = "nccl"):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.n = max(self.world, 1)
+        self.backend = backend
         if gpus and self.world > 1 and gpus != self.world:
             log(f"warning: --gpus {gpus} but WORLD_SIZE {self.world}")
         self.pg = None
         if self.world > 1:
-            import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if backend == "nccl":
+                import torch
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(backend)
             self.pg = dist
 
     def barrier(self):
@@ -134,8 +157,18 @@ class Dist:
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
         return float(t.item())
 
     def close(self):
@@ -162,7 +195,8 @@ def knn_inputs(cb):
 
 
 def sweep_inputs(cb, n_traces: int):
-    """t90 seeds 1..n_traces, materialised once; jobs = traces x 4 policies."""
+    """t90 seeds 1..n_traces, materialised once; jobs = traces x 4 policies
+    (job = policy * n_traces + trace)."""
     lists = [cb.materialize_trace(cb.generate_trace("t90", s)).tasks for s in range(1, n_traces + 1)]
     tasks = np.concatenate(lists)
     offs = np.concatenate([[0], np.cumsum([len(t) for t in lists])]).astype(np.uint64)
@@ -175,25 +209,31 @@ def sweep_inputs(cb, n_traces: int):
     return cfgs, tasks, offs, jobs
 
 
-def profile_traffic(name: str):
+def shard_jobs(tasks, offs, jobs, b: int, e: int):
+    """The replay inputs of jobs [b, e): only the traces they reference,
+    renumbered (what a rank uploads)."""
+    sub = jobs[b:e].copy()
+    used = np.unique(sub["trace"])
+    remap = np.zeros(len(offs) - 1, np.uint32)
+    remap[used] = np.arange(len(used), dtype=np.uint32)
+    sub["trace"] = remap[sub["trace"]]
+    o = offs.astype(np.int64)
+    lens = o[used + 1] - o[used]
+    idx = np.concatenate([np.arange(o[t], o[t + 1]) for t in used]) if len(used) else np.zeros(0, np.int64)
+    return tasks[idx], np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64), sub
+
+
+def profile_traffic(*names):
     """dram bytes per launch from the committed ncu --set full summary, if present."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(path)).get(name)
+        t = json.load(open(path))
     except (OSError, ValueError):
         return None
-
-
-def recorded(name: str):
-    """A measurement too long for the bounded bench run (e.g. the reference on the
-    full 10^6-task c5 trace, scripts/c5_cpu_full.py, ~21 min), recorded once per
-    round under profiles/."""
-    try:
-        r = json.load(open(os.path.join(ROOT, "profiles", name)))
-        r["source"] = f"profiles/{name} (scripts/c5_cpu_full.py on the GPU box host, not re-run here)"
-        return r
-    except (OSError, ValueError):
-        return None
+    for n in names:
+        if n in t:
+            return t[n]
+    return None
 
 
 def peaks():
@@ -203,12 +243,13 @@ def peaks():
         return {}
 
 
-def knn_config(n: int) -> dict:
-    return {"workload": "c2: GPUMemNet k-NN ensemble over 8,388,608 CNN (seed 2024) + 8,388,608 "
-                        "Transformer (seed 2025) feature vectors per GPU; models = provision_estimators "
-                        "(4000 samples, k=5, seeds 112/213)",
-            "rows_per_gpu": 2 * KNN_ROWS_PER_FAMILY, "parallelism": f"dp{n} (independent shards, no collective)",
-            "l2": "inputs 2.28 GB per GPU > 126 MB L2 (no flush needed)"}
+def knn_config(n: int, rows_shard: int) -> dict:
+    return {"workload": "c2: GPUMemNet k-NN ensemble over 8,388,608 CNN (seed 2024) + 8,388,608 Transformer "
+                        "(seed 2025) feature vectors in total; models = provision_estimators (4000 samples, k=5, "
+                        "seeds 112/213)",
+            "rows_total": 2 * KNN_ROWS_PER_FAMILY, "rows_per_gpu": rows_shard, "row_format": "carma_feature_row (136 B)",
+            "parallelism": f"dp{n}: contiguous row shards, no collective",
+            "l2": "inputs 2.28 GB > 126 MB L2 (no flush needed)"}
 
 
 def nn_tile_flops(m) -> tuple:
@@ -236,165 +277,41 @@ def nn_tile_flops(m) -> tuple:
     return executed, useful
 
 
-def neural_bench(abi, cb, dev, stream, args, d, words, schema, rows, fam):
-    """The paper's neural GPUMemNet (MLP ensemble, 8 members)
-    over the same c2 batch as the k-NN headline: 16,777,216 bit-packed CNN +
-    Transformer rows, routed per family, on the tcgen05 kernel."""
-    import ctypes
-
+def timed_device_steps(step, stream, warmup: int, steps: int, d, clk=None):
+    """W warm-up steps, barrier + sync, K steps bracketed by CUDA events on
+    `stream`, sync + barrier; returns max-over-ranks ms per step."""
     import torch
-
-    from paper_2508_19073_b200 import gpumemnet as gm
-    Q = len(rows)
-    models = gm.load_default_models()
-    net = gm.GpuMemNet(dev)
-    for f in (1, 2):
-        net.set_model(models[f])
-    net.set_bit_schema(schema)
-    d_rows = torch.from_numpy(words.view(np.uint8)).to("cuda")
-    d_b = torch.empty(Q, dtype=torch.int32, device="cuda")
-    d_by = torch.empty(Q, dtype=torch.int64, device="cuda")
-
-    def step():
-        net.predict_device(d_rows, abi.ROWS_BITPACKED, Q, d_b, d_by, stream=stream.cuda_stream)
-
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     d.barrier()
-    kernel_ms, call_ms = [], []
+    torch.cuda.synchronize()
+    if clk:
+        clk.mark("t_begin")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         step()
-        t = net.last_timing()
-        kernel_ms.append(t["kernel_ms"])
-        call_ms.append(t["call_ms"])
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = d.max(e0.elapsed_time(e1) / args.steps)
-    t = net.last_timing()
-    b_dev = d_b.cpu().numpy()
-    # e2e: pinned host bit-packed rows -> carma_nn_predict_bitpacked -> pinned host outputs
-    h_rows = torch.from_numpy(words.view(np.uint8)).pin_memory().numpy().view(np.uint32)
-    h_b = torch.empty(Q, dtype=torch.int32).pin_memory().numpy()
-    h_by = torch.empty(Q, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
-
-    def e2e_step():
-        abi.check(abi.lib.carma_nn_predict_bitpacked(net.handle, h_rows.ctypes.data, schema.ctypes.data, Q,
-                                                     h_b.ctypes.data, h_by.ctypes.data))
-
-    e2e_step()
+    if clk:
+        clk.mark("t_end")
     d.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
-    e2e_s = d.max((time.perf_counter() - t0) / args.steps)
-    assert np.array_equal(h_b, b_dev), "host-API and device-resident neural predictions differ"
-    # parity spot check against the oracle on a sample of the batch
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import gpumemnet_oracle
-    rng = np.random.default_rng(0)
-    idx = np.sort(rng.choice(Q, 4096, replace=False))
-    agree = 0
-    raw = cb.scalar_features(rows[idx])
-    for f in (1, 2):
-        sel = fam[idx] == f
-        _, op, ob, _ = gpumemnet_oracle.forward(models[f].spec()[0], models[f].params, raw[sel])
-        srt = np.sort(op, axis=1)
-        sure = srt[:, -1] - srt[:, -2] > 1e-3
-        assert np.array_equal(b_dev[idx][sel][sure], ob[sure]), "neural bins differ from the oracle"
-        agree += int(sure.sum())
-    cpu = None
-    if d.rank == 0 and d.n == 1 and not args.skip_cpu:
-        # The reference has no neural estimator: the CPU baseline is the numpy
-        # oracle ("port", fp64 layers, BLAS threads) on a bounded sample.
-        from threadpoolctl import threadpool_info
-        threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
-        ns = 1 << 18
-        sidx = np.concatenate([np.arange(ns // 2), KNN_ROWS_PER_FAMILY + np.arange(ns // 2)])
-        sraw = cb.scalar_features(rows[sidx])
-        t0 = time.perf_counter()
-        for f in (1, 2):
-            sel = fam[sidx] == f
-            gpumemnet_oracle.forward(models[f].spec()[0], models[f].params, sraw[sel])
-        cpu_s = time.perf_counter() - t0
-        cpu = {"value": ns / cpu_s, "unit": "estimates/s", "cores": threads, "kind": "port",
-               "sample": f"first {ns // 2} CNN + first {ns // 2} Transformer rows of the batch through "
-                         "oracle/gpumemnet_oracle.py (numpy; no reference implementation exists)"}
-    # the paper's Transformer ensemble on the same batch (CUDA cores; PAPER.md:440)
-    tfm = gm.load_default_models(gm.ARCH_TRANSFORMER)
-    tnet = gm.GpuMemNet(dev)
-    for f in (1, 2):
-        tnet.set_model(tfm[f])
-    tnet.set_bit_schema(schema)
+    return d.max(e0.elapsed_time(e1) / steps)
 
-    def tf_step():
-        tnet.predict_device(d_rows, abi.ROWS_BITPACKED, Q, d_b, d_by, stream=stream.cuda_stream)
 
-    for _ in range(args.warmup):
-        tf_step()
-    torch.cuda.synchronize()
+def timed_host_steps(step, warmup: int, steps: int, d):
+    """Host API calls (synchronous, host buffers in and out): wall clock per
+    step, max over ranks."""
+    for _ in range(warmup):
+        step()
     d.barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(args.steps):
-        tf_step()
-    f1.record(stream)
-    torch.cuda.synchronize()
-    tf_ms = d.max(f0.elapsed_time(f1) / args.steps)
-    tb = d_b.cpu().numpy()
-    tf_agree = 0
-    for f in (1, 2):
-        sel = fam[idx] == f
-        _, op, ob, _ = gpumemnet_oracle.forward(tfm[f].spec()[0], tfm[f].params, raw[sel])
-        srt = np.sort(op, axis=1)
-        sure = srt[:, -1] - srt[:, -2] > 1e-3
-        assert np.array_equal(tb[idx][sel][sure], ob[sure]), "transformer bins differ from the oracle"
-        tf_agree += int(sure.sum())
-    tnet.close()
-    transformer = {"metric": "GPUMemNet estimates/sec (Transformer ensemble, 8 members)", "unit": "estimates/s",
-                   "value": d.n * Q / (tf_ms * 1e-3), "ms_per_step": tf_ms, "dtype": "f32",
-                   "kernel": "tf_ensemble (thread per row, three-token attention in registers, CUDA cores)",
-                   "oracle_agreement_rows": tf_agree,
-                   "holdout_accuracy": {gm.FAMILY_NAMES[f]: tfm[f].holdout_accuracy for f in (1, 2)}}
-    k_avg = statistics.mean(kernel_ms)
-    rows_f = {f: int((fam == f).sum()) for f in (1, 2)}
-    executed = sum((rows_f[f] + 127) // 128 * nn_tile_flops(models[f])[0] for f in (1, 2))
-    useful = sum(rows_f[f] * nn_tile_flops(models[f])[1] for f in (1, 2))
-    peak = peaks().get("bf16_tflops", 2250.0)
-    ach = useful / (k_avg * 1e-3) / 1e12          # algorithmic (the ensemble's dense math)
-    ach_exec = executed / (k_avg * 1e-3) / 1e12   # what the tensor pipe executed
-    wpr = int(schema["words_per_row"][0])
-    hbm_bytes = Q * (4 * wpr + 12)
-    net.close()
-    return {
-        "metric": "GPUMemNet estimates/sec (neural MLP ensemble, 8 members, CNN+Transformer)",
-        "unit": "estimates/s", "value": d.n * Q / (ms * 1e-3), "ms_per_step": ms, "dtype": "bf16 x3 -> fp32",
-        "config": {"workload": f"c2 batch ({Q} bit-packed rows, {4 * wpr} B each) through the neural GPUMemNet "
-                               "ensembles of paper_2508_19073_b200/weights (scripts/train_gpumemnet.py)",
-                   "l2": "inputs larger than L2 (no flush needed)"},
-        "e2e": {"value": d.n * Q / e2e_s, "unit": "estimates/s", "h2d_bytes_per_step": int(h_rows.nbytes),
-                "d2h_bytes_per_step": int(h_b.nbytes + h_by.nbytes),
-                "api": "carma_nn_predict_bitpacked (pinned host buffers)"},
-        "gpu_launches": int(t["launches"]) * args.steps,
-        "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                     "traffic": profile_traffic("nn_ensemble"), "kernel": "nn_ensemble", "kernel_ms": k_avg,
-                     "kernel_share_of_step": k_avg / statistics.mean(call_ms),
-                     "work": f"algorithmic: {useful / 1e9:.1f} GFLOP of dense ensemble math per step (DESIGN §3); "
-                             f"executed: {t['mmas']} tcgen05.mma (M=128, K=16) = {executed / 1e9:.1f} GFLOP "
-                             "(block-diagonal padding, 3 bf16 activation parts)",
-                     "executed_tflops": ach_exec, "executed_frac": ach_exec / peak,
-                     "note": "latency-bound: a 9-stage dependent MMA -> epilogue chain per 128-row tile, "
-                             "3 tiles in flight per SM (shared memory); tiny layers (<= 8 neurons per member)",
-                     "hbm_gbs": hbm_bytes / (k_avg * 1e-3) / 1e9, "hbm_peak_gbs": peaks().get("hbm_gbs"),
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
-        "cpu_baseline": cpu,
-        "transformer": transformer,
-        "oracle_agreement_rows": agree,
-        "holdout_accuracy": {gm.FAMILY_NAMES[f]: models[f].holdout_accuracy for f in (1, 2)},
-    }
-
+    t = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t) / steps
+    d.barrier()
+    return d.max(dt)
 
 
 # ------------------------------------------------------------ reference arm
@@ -430,10 +347,9 @@ def cpu_sweep_baseline(ref, threads: int, target_s: float = 10.0):
     """The reference run_simulation pool (run_sweep shape) over t90 seeds x 4 policies."""
     import ctypes
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_bind import ref_config
-    from paper_2508_19073_b200 import abi
+    from oracle_bind import POLICY, ref_config
     cfg = ref_config(policy="magm", max_smact=0.8)
-    pols = np.array([abi.POLICY[p] for p in SWEEP_POLICIES], np.int32)
+    pols = np.array([POLICY[p] for p in SWEEP_POLICIES], np.int32)
     placed, esum = ctypes.c_uint64(), ctypes.c_double()
     n0 = max(8, threads)
     t = ref.ref_bench_sweep(cfg.ctypes.data, 0, 1, n0, pols.ctypes.data, len(pols), threads,
@@ -464,6 +380,311 @@ def cpu_fused_baseline(ref, n_tasks: int):
                           f"(reference cost grows superlinearly with trace length, SURVEY F7)")
 
 
+def c5_golden():
+    try:
+        return json.load(open(os.path.join(ROOT, "tests", "golden", "c5_ref.json")))
+    except (OSError, ValueError):
+        return None
+
+
+def run_reference(args, d: Dist):
+    """The reference's own CPU implementation of the path (oracle/_ref, the
+    unmodified library) on all host threads; rank 0 only."""
+    if d.rank != 0:
+        return
+    ref = ref_lib()
+    threads = os.cpu_count() or 1
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcarma_ref.so not built"}))
+        return
+    steps = []
+    for _ in range(args.warmup + args.steps):
+        rate, sample = cpu_knn_baseline(ref, threads, target_s=4.0)
+        steps.append(rate)
+    vals = steps[args.warmup:]
+    value = statistics.median(vals)
+    srate, ssample, _ = cpu_sweep_baseline(ref, threads, target_s=4.0)
+    cpus = host_cpus()
+    line = {
+        "impl": "reference", "metric": "GPUMemNet estimates/sec (k-NN, CNN+Transformer ensemble)",
+        "value": value, "unit": "estimates/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * 2 * KNN_ROWS_PER_FAMILY / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": knn_config(1, 2 * KNN_ROWS_PER_FAMILY),
+        "cpu_baseline": {"value": value, "unit": "estimates/s", "cores": threads, "kind": "reference",
+                         "sample": sample, **cpus},
+        "e2e": {"value": value, "unit": "estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "replay": {"value": srate, "unit": "placed tasks/s", "cores": threads, "sample": ssample},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ stage 1
+def knn_stage(abi, cb, dev, stream, args, d, rows, fam, b, e):
+    """The k-NN GPUMemNet over this rank's contiguous shard [b, e) of the c2
+    batch: device-resident 136-B feature rows (value) and the host API from
+    pinned 136-B rows (e2e)."""
+    import ctypes
+
+    import torch
+    Q = e - b
+    knn = cb.GpuKnn(dev)
+    for f in (1, 2):
+        knn.set_model(cb.fit_knn(f, 4000, MODEL_SEEDS[f], 5))
+    h_rows = torch.from_numpy(rows[b:e].view(np.uint8).reshape(-1)).pin_memory()
+    h_fam = torch.from_numpy(fam[b:e]).pin_memory()
+    d_rows = h_rows.to("cuda")
+    d_fam = h_fam.to("cuda")
+    d_b = torch.empty(Q, dtype=torch.int32, device="cuda")
+    d_by = torch.empty(Q, dtype=torch.int64, device="cuda")
+    search_ms, pipe_ms = [], []
+    sm, pm = ctypes.c_double(), ctypes.c_double()
+
+    def step():
+        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_FEATURES,
+                                                   d_fam.data_ptr(), 1, Q, d_b.data_ptr(), d_by.data_ptr(),
+                                                   None, None, abi.stream_arg(stream)))
+        abi.check(abi.lib.carma_knn_last_timing(knn.handle, ctypes.byref(sm), ctypes.byref(pm)))
+        search_ms.append(sm.value)
+        pipe_ms.append(pm.value)
+
+    with Clocks(dev) as clk:
+        ms = timed_device_steps(step, stream, args.warmup, args.steps, d, clk)
+    clocks = clk.summary()
+    search_ms, pipe_ms = search_ms[args.warmup:], pipe_ms[args.warmup:]
+    b_dev = d_b.cpu().numpy()
+    by_dev = d_by.cpu().numpy().view(np.uint64)
+    launches, evals = knn.last_stats()
+    la_, e64_, e32_ = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    abi.check(abi.lib.carma_knn_last_work(knn.handle, ctypes.byref(la_), ctypes.byref(e64_), ctypes.byref(e32_)))
+    visits = e32_.value
+    del d_rows, d_fam, d_b, d_by
+
+    # e2e: the drop-in call (carma_knn_predict: pinned 136-B rows + families in,
+    # buckets + bytes out; chunked H2D / compute / D2H inside)
+    h_rows_np = h_rows.numpy().view(abi.feature_row_dtype)
+    h_fam_np = h_fam.numpy()
+    h_b = torch.empty(Q, dtype=torch.int32).pin_memory().numpy()
+    h_by = torch.empty(Q, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+
+    def e2e_step():
+        abi.check(abi.lib.carma_knn_predict(knn.handle, h_rows_np.ctypes.data, h_fam_np.ctypes.data, 1, Q,
+                                            h_b.ctypes.data, h_by.ctypes.data))
+
+    e2e_s = timed_host_steps(e2e_step, max(1, args.warmup - 1), args.steps, d)
+    assert np.array_equal(h_b, b_dev) and np.array_equal(h_by, by_dev), "host-API and device predictions differ"
+    knn_handle = knn  # kept for the fused c5 run
+    search_avg = statistics.mean(search_ms)
+    f32_flops = visits * FLOPS_PER_F32_EVAL
+    achieved = f32_flops / (search_avg * 1e-3)
+    fp32, fp64 = ctypes.c_double(), ctypes.c_double()
+    abi.check(abi.lib.carma_probe_fp32(dev, ctypes.byref(fp32)))
+    abi.check(abi.lib.carma_probe_fp64(dev, ctypes.byref(fp64)))
+    N = d.n
+    QT = 2 * KNN_ROWS_PER_FAMILY
+    out = {
+        "value": QT / (ms * 1e-3), "ms_per_step": ms, "clocks": clocks,
+        "e2e": {"value": QT / e2e_s, "unit": "estimates/s",
+                "h2d_bytes_per_step": int(Q * (FEATURE_ROW_BYTES + 1)),
+                "d2h_bytes_per_step": int(Q * 12),
+                "api": "carma_knn_predict (pinned 136-B carma_feature_row + family in, bucket + bytes out)",
+                "ms_per_step": e2e_s * 1e3,
+                "pcie_gbs": Q * (FEATURE_ROW_BYTES + 1 + 12) / e2e_s / 1e9},
+        "gpu_launches": int(launches) * args.steps,
+        "roofline": {"bound": "fp32", "achieved": achieved / 1e12, "peak": fp32.value / 1e12, "unit": "TFLOP/s",
+                     "frac": achieved / fp32.value,
+                     "traffic": profile_traffic("knn_search_f32", "knn_search"),
+                     "kernel": "knn_search_f32", "kernel_ms": search_avg,
+                     "kernel_share_of_step": search_avg / statistics.mean(pipe_ms),
+                     "peak_source": "measured: carma_probe_fp32 (FFMA2 issue rate; MEASURED_PEAKS.json has no fp32 "
+                                    "figure)",
+                     "work": f"{visits} fp32 pre-filter evaluations x {FLOPS_PER_F32_EVAL} flops + {evals} exact "
+                             f"fp64 evaluations x {FLOPS_PER_EVAL} flops per launch on this rank",
+                     "fp64": {"achieved": evals * FLOPS_PER_EVAL / (search_avg * 1e-3) / 1e12,
+                              "peak": fp64.value / 1e12, "unit": "TFLOP/s"},
+                     "hbm_gbs": ALG_BYTES_PER_ESTIMATE * Q / (search_avg * 1e-3) / 1e9,
+                     "hbm_peak_gbs": peaks().get("hbm_gbs")},
+    }
+    return out, knn_handle, (h_rows_np, h_fam_np, b_dev)
+
+
+def neural_stage(abi, cb, dev, stream, args, d, h_rows, h_fam, rows_all, fam_all, b):
+    """The paper's neural GPUMemNet ensembles (MLP on tcgen05, Transformer on
+    CUDA cores) over the same shard of 136-B rows."""
+    import ctypes
+
+    import torch
+
+    from paper_2508_19073_b200 import gpumemnet as gm
+    Q = len(h_rows)
+    QT = 2 * KNN_ROWS_PER_FAMILY
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import gpumemnet_oracle
+    d_rows = torch.from_numpy(h_rows.view(np.uint8).reshape(-1)).to("cuda")
+    d_fam = torch.from_numpy(h_fam).to("cuda")
+    d_b = torch.empty(Q, dtype=torch.int32, device="cuda")
+    d_by = torch.empty(Q, dtype=torch.int64, device="cuda")
+    h_b = torch.empty(Q, dtype=torch.int32).pin_memory().numpy()
+    h_by = torch.empty(Q, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(Q, min(Q, 4096), replace=False))
+    raw = cb.scalar_features(h_rows[idx])
+    res = {}
+    for arch, key in ((gm.ARCH_MLP, "mlp"), (gm.ARCH_TRANSFORMER, "transformer")):
+        models = gm.load_default_models(arch)
+        net = gm.GpuMemNet(dev)
+        for f in (1, 2):
+            net.set_model(models[f])
+        kernel_ms, call_ms = [], []
+
+        def step():
+            net.predict_device(d_rows, abi.ROWS_FEATURES, Q, d_b, d_by, family=d_fam, default_family=1,
+                               stream=stream)
+            t = net.last_timing()
+            kernel_ms.append(t["kernel_ms"])
+            call_ms.append(t["call_ms"])
+
+        ms = timed_device_steps(step, stream, args.warmup, args.steps, d)
+        t = net.last_timing()
+        kernel_ms, call_ms = kernel_ms[args.warmup:], call_ms[args.warmup:]
+        b_dev = d_b.cpu().numpy()
+
+        def e2e_step():
+            abi.check(abi.lib.carma_nn_predict(net.handle, h_rows.ctypes.data, h_fam.ctypes.data, 1, Q,
+                                               h_b.ctypes.data, h_by.ctypes.data))
+
+        e2e_s = timed_host_steps(e2e_step, 1, args.steps, d)
+        assert np.array_equal(h_b, b_dev), f"{key}: host-API and device-resident neural predictions differ"
+        agree = 0
+        for f in (1, 2):
+            sel = h_fam[idx] == f
+            if not sel.any():
+                continue
+            _, op, ob, _ = gpumemnet_oracle.forward(models[f].spec()[0], models[f].params, raw[sel])
+            srt = np.sort(op, axis=1)
+            sure = srt[:, -1] - srt[:, -2] > 1e-3
+            assert np.array_equal(b_dev[idx][sel][sure], ob[sure]), f"{key}: bins differ from the oracle"
+            agree += int(sure.sum())
+        k_avg = statistics.mean(kernel_ms)
+        r = {"value": QT / (ms * 1e-3), "ms_per_step": ms,
+             "e2e": {"value": QT / e2e_s, "unit": "estimates/s", "h2d_bytes_per_step": int(Q * (FEATURE_ROW_BYTES + 1)),
+                     "d2h_bytes_per_step": int(Q * 12), "api": "carma_nn_predict (pinned 136-B rows)"},
+             "gpu_launches": int(t["launches"]) * args.steps, "kernel_ms": k_avg,
+             "kernel_share_of_step": k_avg / statistics.mean(call_ms), "oracle_agreement_rows": agree,
+             "holdout_accuracy": {gm.FAMILY_NAMES[f]: models[f].holdout_accuracy for f in (1, 2)}}
+        rows_f = {f: int((h_fam == f).sum()) for f in (1, 2)}
+        useful = sum(rows_f[f] * nn_tile_flops(models[f])[1] for f in (1, 2))
+        if key == "mlp":
+            executed = sum((rows_f[f] + 127) // 128 * nn_tile_flops(models[f])[0] for f in (1, 2))
+            peak = peaks().get("bf16_tflops", 2250.0)
+            ach = useful / (k_avg * 1e-3) / 1e12
+            r["dtype"] = "bf16 x3 -> fp32"
+            r["roofline"] = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                             "traffic": profile_traffic("nn_ensemble"), "kernel": "nn_ensemble",
+                             "executed_tflops": executed / (k_avg * 1e-3) / 1e12,
+                             "work": f"algorithmic {useful / 1e9:.1f} GFLOP (dense ensemble math) per launch; "
+                                     f"executed {executed / 1e9:.1f} GFLOP on the tensor pipe",
+                             "peak_source": "MEASURED_PEAKS.json bf16_tflops"}
+        else:
+            r["dtype"] = "f32"
+            r["kernel"] = "tf_ensemble (CUDA cores)"
+            r["useful_tflops"] = useful / (k_avg * 1e-3) / 1e12
+        res[key] = r
+        net.close()
+    cpu = None
+    if d.rank == 0 and d.n == 1 and not args.skip_cpu:
+        from threadpoolctl import threadpool_info
+        threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
+        ns = 1 << 18
+        sidx = np.concatenate([np.arange(ns // 2), KNN_ROWS_PER_FAMILY + np.arange(ns // 2)])
+        sraw = cb.scalar_features(rows_all[sidx])
+        models = gm.load_default_models()
+        t0 = time.perf_counter()
+        for f in (1, 2):
+            sel = fam_all[sidx] == f
+            gpumemnet_oracle.forward(models[f].spec()[0], models[f].params, sraw[sel])
+        cpu_s = time.perf_counter() - t0
+        cpu = {"value": ns / cpu_s, "unit": "estimates/s", "cores": threads, "kind": "port",
+               "sample": f"MLP ensemble, first {ns // 2} CNN + first {ns // 2} Transformer rows through "
+                         "oracle/gpumemnet_oracle.py (numpy; no reference implementation exists)"}
+    res["mlp"]["cpu_baseline"] = cpu
+    return res
+
+
+# ------------------------------------------------------------------ stage 2
+def replay_stage(abi, cb, dev, stream, args, d):
+    """The c4 policy sweep, jobs sharded by task count across ranks."""
+    import ctypes
+
+    import torch
+
+    from paper_2508_19073_b200 import dist as cdist
+    t0 = time.time()
+    n_tr = args.sweep_traces
+    cfgs, tasks_all, offs_all, jobs_all = sweep_inputs(cb, n_tr)
+    counts = np.diff(offs_all.astype(np.int64))[jobs_all["trace"]]
+    b, e = cdist.balanced_shards(counts, d.n)[d.rank]
+    tasks, offs, jobs = shard_jobs(tasks_all, offs_all, jobs_all, b, e)
+    n_placed = int(np.diff(offs.astype(np.int64))[jobs["trace"]].sum())
+    total_placed = int(counts.sum())
+    log(f"[rank {d.rank}] sweep inputs {n_tr} traces x {len(SWEEP_POLICIES)}, jobs [{b}, {e}) in "
+        f"{time.time() - t0:.1f}s")
+    plan = cb.ReplayPlan(cfgs, tasks, offs, jobs, device=dev)
+    km, rm = ctypes.c_double(), ctypes.c_double()
+    kernel_ms = []
+
+    def step():
+        plan.run(stream)
+        abi.check(abi.lib.carma_replay_plan_timing(plan._h, ctypes.byref(km), ctypes.byref(rm)))
+        kernel_ms.append(km.value)
+
+    ms = timed_device_steps(step, stream, args.warmup, args.steps, d)
+    kernel_ms = kernel_ms[args.warmup:]
+    res = plan.results(tasks=False)
+    assert (res.traces["status"] == 0).all()
+    launches_r, retried = plan.stats()
+    events = int(res.traces["events"].sum())
+    plan.close()
+    # e2e through the plan's host API: every step uploads the shard's tasks
+    # from pinned memory, replays, and reads back per-task outcomes, reports
+    # and per-GPU results into pinned memory
+    plan = cb.ReplayPlan(cfgs, tasks, offs, jobs, device=dev)
+    h_tasks = torch.from_numpy(tasks.view(np.uint8)).pin_memory().numpy().view(tasks.dtype)
+    o_t = torch.empty(n_placed * 24, dtype=torch.uint8).pin_memory().numpy().view(abi.task_outcome_dtype)
+    o_j = torch.empty(len(jobs) * 80, dtype=torch.uint8).pin_memory().numpy().view(abi.trace_result_dtype)
+    o_g = torch.empty(len(jobs) * 4 * 32, dtype=torch.uint8).pin_memory().numpy().view(abi.gpu_result_dtype)
+
+    def e2e_step():
+        abi.check(abi.lib.carma_replay_plan_upload_tasks(plan._h, h_tasks.ctypes.data))
+        abi.check(abi.lib.carma_replay_plan_run(plan._h, None))
+        abi.check(abi.lib.carma_replay_plan_outcomes(plan._h, o_t.ctypes.data, o_j.ctypes.data, o_g.ctypes.data))
+
+    r_e2e = timed_host_steps(e2e_step, 1, args.steps, d)
+    plan.close()
+    assert o_j.tobytes() == res.traces.tobytes(), "replay e2e reports differ from the device-timed run"
+    k_avg = statistics.mean(kernel_ms)
+    hbm = peaks().get("hbm_gbs", 6650.0)
+    ach = ALG_BYTES_PER_TASK * n_placed / (k_avg * 1e-3) / 1e9
+    return {
+        "metric": "trace-replay placed tasks/sec", "unit": "placed tasks/s",
+        "value": total_placed / (ms * 1e-3), "ms_per_step": ms,
+        "config": {"workload": f"c4 policy sweep: t90 seeds 1..{n_tr} x {{exclusive, rr, magm, lug}} "
+                               f"({len(jobs_all)} jobs, {total_placed} placed tasks in total), MPS, u=0.8, "
+                               "no estimator, 4 GPUs x 40 GiB, W=60 s",
+                   "parallelism": f"dp{d.n}: contiguous job shards balanced by task count",
+                   "jobs_this_rank": int(e - b), "placed_tasks_this_rank": n_placed},
+        "events_per_s": d.sum(events) / (ms * 1e-3),
+        "e2e": {"value": total_placed / r_e2e, "unit": "placed tasks/s", "ms_per_step": r_e2e * 1e3,
+                "h2d_bytes_per_step": int(h_tasks.nbytes),
+                "d2h_bytes_per_step": int(o_t.nbytes + o_j.nbytes + o_g.nbytes),
+                "api": "carma_replay_plan_upload_tasks + run + outcomes (pinned host buffers)"},
+        "gpu_launches": int(launches_r) * args.steps, "retried_jobs": int(retried),
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                     "traffic": profile_traffic("replay_kernel"), "kernel": "replay_kernel", "kernel_ms": k_avg,
+                     "note": "latency/issue-bound event loop; algorithmic bytes = 80 B per placed task"},
+    }
+
+
 SCORING_DECISIONS = 1 << 24  # per GPU
 SCORING_GPUS = 8
 
@@ -492,29 +713,29 @@ def scoring_bench(abi, cb, dev, stream, warmup, steps, d):
 
     def step():
         abi.check(abi.lib.carma_pick_batch_device(dev, cfg.ctypes.data, dv.data_ptr(), g, dr.data_ptr(), n,
-                                                  dc.data_ptr(), do.data_ptr(), stream.cuda_stream))
+                                                  dc.data_ptr(), do.data_ptr(), abi.stream_arg(stream)))
 
-    for _ in range(warmup):
-        flush.zero_()
-        step()
-    torch.cuda.synchronize()
-    d.barrier()
-    times = []
-    for _ in range(steps):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        step()
-        e1.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            flush.zero_()
+            step()
         torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
-    ms = d.max(statistics.mean(times))
+        times = []
+        for _ in range(steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    ms = statistics.mean(times)
     per = g * 24 + 16 + 4 + 4 + 8
     gbs = per * n / (ms * 1e-3) / 1e9
     hbm = peaks().get("hbm_gbs", 6650.0)
     return {"metric": "placement decisions/sec (feasibility + MAGM score matrix)", "unit": "decisions/s",
-            "value": d.n * n / (ms * 1e-3), "ms_per_step": ms,
-            "config": {"workload": f"{n} decisions x {g} simulated GPUs per rank, MAGM u=0.8, random views "
+            "value": n / (ms * 1e-3), "ms_per_step": ms,
+            "config": {"workload": f"{n} decisions x {g} simulated GPUs, MAGM u=0.8, random views "
                                    f"(free in 512 MiB blocks, SMACT, idle), 15% two-GPU requests",
                        "l2": "256 MiB buffer written between steps"},
             "gpu_launches": 1,
@@ -523,7 +744,58 @@ def scoring_bench(abi, cb, dev, stream, warmup, steps, d):
                          "algorithmic_bytes_per_decision": per, "kernel": "pick_kernel"}}
 
 
-def small_configs(cb, abi, dev, ref):
+def fused_stage(abi, cb, dev, stream, args, knn):
+    """configs[4] (c5): one 10^6-task trace, k-NN pre-pass over every arrival
+    feeding the replay on 64 simulated GPUs; checked against the committed
+    golden of the reference's full run (tests/golden/c5_ref.json)."""
+    import torch
+    t0 = time.time()
+    mf = cb.materialize_trace(cb.generate_uniform_trace(args.fused_tasks, 3.0, 7))
+    cfg5 = cb.make_config(cb.PolicyConfig(policy="magm", max_smact=0.8, monitor_window=5.0),
+                          cb.SimConstants(gpu_count=64))
+    for f in sorted(set(mf.family.tolist())):
+        if f not in knn.models:
+            knn.set_model(cb.fit_knn(f, 4000, 11 + 101 * f, 5))
+    fr = cb.FusedReplay(mf, cfg5, knn, dev)
+    log(f"fused inputs {args.fused_tasks} tasks in {time.time() - t0:.1f}s")
+    fr.run(stream)  # warm-up (one: a step is ~11 s at 10^6 tasks)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    fr.run(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    f_ms = e0.elapsed_time(e1)
+    res = fr.results()
+    fr.close()
+    t = res.traces[0]
+    assert t["status"] == 0
+    parity = "not checked (golden missing or different size)"
+    gold = c5_golden()
+    if gold and gold["n_tasks"] == args.fused_tasks:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import fullsize
+        want = gold["runs"]["learned"]
+        rec = fullsize.gpu_tasks_canonical(res.job_tasks(0))
+        ok = (int(t["oom_count"]) == want["oom_count"] and fullsize.digest_fields(rec) == want["task_digest"]
+              and all(np.float64(t[k]).view(np.uint64).item().to_bytes(8, "big").hex() == v
+                      for k, v in want["report"].items()))
+        assert ok, "c5 run differs from the reference golden"
+        parity = "bit-exact vs tests/golden/c5_ref.json (report, per-task digests of every field)"
+    full = gold["runs"]["learned"]["seconds"] if gold else None
+    return {"metric": "fused estimator-in-the-loop placed tasks/sec", "unit": "placed tasks/s",
+            "value": args.fused_tasks / (f_ms * 1e-3), "ms_per_step": f_ms, "steps": 1, "warmup": 1,
+            "config": {"workload": f"c5: {args.fused_tasks} arrivals, uniform catalog, exp gaps mean 3 s, seed 7; "
+                                   "k-NN pre-pass over every arrival feeding the replay; MAGM + learned, u=0.8, "
+                                   "W=5 s, 64 simulated GPUs"},
+            "events": int(t["events"]), "oom_count": int(t["oom_count"]), "parity": parity,
+            "cpu_reference_full_trace": None if full is None else
+            {"value": args.fused_tasks / full, "unit": "placed tasks/s", "cores": 1, "kind": "reference",
+             "seconds": full, "source": "tests/golden/c5_ref.json (make_c5_golden.py, the full reference run)"},
+            "note": "one trace: a single warp replays it (sequential event loop); not sharded"}
+
+
+def small_configs(cb, abi, dev, stream, ref):
     """configs[0] (c1: 4096 MLP vectors, the reference's CPU batch) and
     configs[2] (c3: one paper-style t90 trace on an 8-GPU server, MAGM u=0.8
     with OOM recovery, estimator none and learned): latency-style lines."""
@@ -531,38 +803,33 @@ def small_configs(cb, abi, dev, ref):
 
     import torch
     out = {}
-    # ---- c1
     m = cb.fit_knn(0, 4000, 11, 5)
     knn = cb.GpuKnn(dev)
     knn.set_model(m)
     ds = cb.generate_synthetic_dataset(0, 4096, 12345)
-    words, schema = cb.pack_features_bits(ds.rows, np.zeros(4096, np.int8))
-    abi.check(abi.lib.carma_knn_set_bit_schema(knn.handle, schema.ctypes.data))
-    d_rows = torch.from_numpy(words.view(np.uint8)).to("cuda")
+    d_rows = torch.from_numpy(ds.rows.view(np.uint8).reshape(-1)).to("cuda")
     d_b = torch.empty(4096, dtype=torch.int32, device="cuda")
     d_by = torch.empty(4096, dtype=torch.int64, device="cuda")
-    s = torch.cuda.current_stream()
 
     def step():
-        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_BITPACKED, None, 0, 4096,
-                                                   d_b.data_ptr(), d_by.data_ptr(), None, None, s.cuda_stream))
+        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_FEATURES, None, 0, 4096,
+                                                   d_b.data_ptr(), d_by.data_ptr(), None, None,
+                                                   abi.stream_arg(stream)))
     for _ in range(5):
         step()
     reps = 50
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
+    e0.record(stream)
     for _ in range(reps):
         step()
-    e1.record(s)
+    e1.record(stream)
     torch.cuda.synchronize()
     dev_ms = e0.elapsed_time(e1) / reps
-    h_b = np.zeros(4096, np.int32)
-    h_by = np.zeros(4096, np.uint64)
     for _ in range(3):
-        knn.predict_bitpacked(words, schema, 4096)
+        knn.predict(ds.rows, default_family=0)
     t = time.perf_counter()
     for _ in range(reps):
-        h_b, h_by = knn.predict_bitpacked(words, schema, 4096)
+        h_b, _ = knn.predict(ds.rows, default_family=0)
     e2e_ms = (time.perf_counter() - t) / reps * 1e3
     assert np.array_equal(h_b, d_b.cpu().numpy())
     c1 = {"workload": "c1: GPUMemNet MLP k-NN over 4096 MLP feature vectors (seed 12345), model seed 11",
@@ -576,7 +843,6 @@ def small_configs(cb, abi, dev, ref):
                               "kind": "reference", "sample": "the same 4096 rows, estimate_learned, 1 thread"}
     out["c1"] = c1
     knn.close()
-    # ---- c3
     c3 = {"workload": "c3: one t90 trace (seed 1) on an 8-GPU server, MAGM u=0.8, MPS, W=60 s; "
                       "estimator none and learned", "unit": "ms per trace replay"}
     for est in ("none", "learned"):
@@ -597,9 +863,6 @@ def small_configs(cb, abi, dev, ref):
             runs.append(rm.value)
         r = plan.results().traces[0]
         plan.close()
-        # e2e: the user's call, run_simulation (trace generation, estimator
-        # provisioning incl. training for "learned", the replay, read-back),
-        # like the reference's run_simulation the CPU line times
         t = time.perf_counter()
         for _ in range(10):
             cb.run_simulation(rc, device=dev)
@@ -621,348 +884,104 @@ def small_configs(cb, abi, dev, ref):
     return out
 
 
-def run_reference(args, d: Dist):
-    if d.rank != 0:
-        return
-    ref = ref_lib()
-    threads = os.cpu_count() or 1
-    if ref is None:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcarma_ref.so not built"}))
-        return
-    steps = []
-    for _ in range(args.warmup + args.steps):
-        rate, sample = cpu_knn_baseline(ref, threads, target_s=4.0)
-        steps.append(rate)
-    vals = steps[args.warmup:]
-    value = statistics.median(vals)
-    srate, ssample, _ = cpu_sweep_baseline(ref, threads, target_s=4.0)
-    line = {
-        "impl": "reference", "metric": "GPUMemNet estimates/sec (k-NN, CNN+Transformer ensemble)",
-        "value": value, "unit": "estimates/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": knn_config(1),
-        "cpu_baseline": {"value": value, "unit": "estimates/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
-        "e2e": {"value": value, "unit": "estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "replay": {"value": srate, "unit": "placed tasks/s", "cores": threads, "sample": ssample},
-    }
-    print(json.dumps(line))
-
-
 # ------------------------------------------------------------------ ours
+def compact(x, keep):
+    return None if x is None else {k: x[k] for k in keep if k in x}
+
+
 def run_carma(args, d: Dist):
     import torch
 
     import paper_2508_19073_b200 as cb
     from paper_2508_19073_b200 import abi
+    from paper_2508_19073_b200 import dist as cdist
 
     dev = d.local
     torch.cuda.set_device(dev)
     if abi.lib.carma_device_count() < 1:
         raise SystemExit("no sm_100 device visible")
     N = d.n
-    import ctypes
-    fp64 = ctypes.c_double()
-    abi.check(abi.lib.carma_probe_fp64(dev, ctypes.byref(fp64)))
-    fp32 = ctypes.c_double()
-    abi.check(abi.lib.carma_probe_fp32(dev, ctypes.byref(fp32)))
-
-    # ---------------- stage 1 inputs
+    stream = torch.cuda.Stream(dev)  # every timed call runs on this explicit stream
     t0 = time.time()
     rows, fam = knn_inputs(cb)
-    Q = len(rows)
-    knn = cb.GpuKnn(dev)
-    for f in (1, 2):
-        knn.set_model(cb.fit_knn(f, 4000, MODEL_SEEDS[f], 5))
-    log(f"[rank {d.rank}] knn inputs {Q} rows in {time.time() - t0:.1f}s; fp64 probe {fp64.value / 1e12:.2f} TF/s")
-    # Bit-packed rows (lossless frame-of-reference packing, family inside;
-    # include/carma_gpu.h): 36 B/row on this batch instead of 136 B.
-    words, schema = cb.pack_features_bits(rows, fam)
-    abi.check(abi.lib.carma_knn_set_bit_schema(knn.handle, schema.ctypes.data))
-    wpr = int(schema["words_per_row"][0])
-    stream = torch.cuda.current_stream()
-    d_rows = torch.from_numpy(words.view(np.uint8)).to("cuda")
-    d_b = torch.empty(Q, dtype=torch.int32, device="cuda")
-    d_by = torch.empty(Q, dtype=torch.int64, device="cuda")
-
-    def knn_step():
-        abi.check(abi.lib.carma_knn_predict_device(knn.handle, d_rows.data_ptr(), abi.ROWS_BITPACKED, None, 1, Q,
-                                                   d_b.data_ptr(), d_by.data_ptr(), None, None, stream.cuda_stream))
-
-    search_ms, pipe_ms = [], []
-    sm, pm = ctypes.c_double(), ctypes.c_double()
-    with Clocks(dev) as clk:
-        clk.mark("t_busy")
-        for _ in range(args.warmup):
-            knn_step()
-        torch.cuda.synchronize()
-        d.barrier()
-        torch.cuda.synchronize()
-        clk.mark("t_begin")
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            knn_step()
-            abi.check(abi.lib.carma_knn_last_timing(knn.handle, ctypes.byref(sm), ctypes.byref(pm)))
-            search_ms.append(sm.value)
-            pipe_ms.append(pm.value)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        clk.mark("t_end")
-        d.barrier()
-    knn_ms = d.max(e0.elapsed_time(e1) / args.steps)
-    clocks = clk.summary()
-    b_dev = d_b.cpu().numpy()
-    launches, evals = knn.last_stats()
-    la_, e64_, e32_ = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
-    abi.check(abi.lib.carma_knn_last_work(knn.handle, ctypes.byref(la_), ctypes.byref(e64_), ctypes.byref(e32_)))
-    visits = e32_.value
-    value = N * Q / (knn_ms * 1e-3)
-
-    # e2e: pinned host bit-packed rows -> carma_knn_predict_bitpacked (chunked
-    # H2D / compute / D2H on two streams) -> pinned host buckets + bytes
-    h_rows = torch.from_numpy(words.view(np.uint8)).pin_memory().numpy().view(np.uint32)
-    h_b = torch.empty(Q, dtype=torch.int32).pin_memory().numpy()
-    h_by = torch.empty(Q, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
-
-    def e2e_step():
-        abi.check(abi.lib.carma_knn_predict_bitpacked(knn.handle, h_rows.ctypes.data, schema.ctypes.data, Q,
-                                                      h_b.ctypes.data, h_by.ctypes.data))
-
-    for _ in range(max(1, args.warmup - 1)):
-        e2e_step()
-    d.barrier()
-    t = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
-    e2e_s = d.max((time.perf_counter() - t) / args.steps)
-    d.barrier()
-    assert np.array_equal(h_b, b_dev), "host-API and device-resident predictions differ"
-    # the other host formats, warm, once each: 64-B packed rows and the
-    # 136-B FeatureVector rows
-    packed, table = cb.pack_features(rows, fam)
-    h_pk = torch.from_numpy(packed.view(np.uint8).reshape(-1)).pin_memory().numpy().view(packed.dtype)
-    for _ in range(2):
-        t = time.perf_counter()
-        abi.check(abi.lib.carma_knn_predict_packed(knn.handle, h_pk.ctypes.data, table.ctypes.data, Q,
-                                                   h_b.ctypes.data, h_by.ctypes.data))
-        e2e_pk_s = time.perf_counter() - t
-    assert np.array_equal(h_b, b_dev)
-    h_full = torch.from_numpy(rows.view(np.uint8).reshape(-1)).pin_memory().numpy().view(rows.dtype)
-    h_fam = torch.from_numpy(fam).pin_memory().numpy()
-    for _ in range(2):  # warm-up: scratch sized for 136-B rows
-        t = time.perf_counter()
-        abi.check(abi.lib.carma_knn_predict(knn.handle, h_full.ctypes.data, h_fam.ctypes.data, 1, Q,
-                                            h_b.ctypes.data, h_by.ctypes.data))
-        e2e_full_s = time.perf_counter() - t
-    assert np.array_equal(h_b, b_dev)
-    del d_rows, d_b, d_by, h_full, h_fam, h_pk
-    abi.check(abi.lib.carma_knn_set_act_table(knn.handle, table.ctypes.data))
-
-    search_avg = statistics.mean(search_ms)
-    # executed work of the exact pruned search: fp32 pre-filter evaluations
-    # (16 dims x (sub + fma) = 48 flops) dominate; exact fp64 evaluations are
-    # reported beside them
-    f32_flops = visits * FLOPS_PER_F32_EVAL
-    achieved = f32_flops / (search_avg * 1e-3)
-    traffic = profile_traffic("knn_search_f32")
-
-    # ---------------- stage 1, neural GPUMemNet (tcgen05 MLP ensemble)
+    QT = len(rows)
+    b, e = cdist.balanced_shards_count(QT, N)[d.rank]
+    log(f"[rank {d.rank}] knn inputs {QT} rows in {time.time() - t0:.1f}s; shard [{b}, {e})")
+    knn_res, knn, (h_rows, h_fam, _) = knn_stage(abi, cb, dev, stream, args, d, rows, fam, b, e)
     neural = None
     if not args.skip_neural:
-        neural = neural_bench(abi, cb, dev, stream, args, d, words, schema, rows, fam)
+        neural = neural_stage(abi, cb, dev, stream, args, d, h_rows, h_fam, rows, fam, b)
+    replay = None if args.skip_replay else replay_stage(abi, cb, dev, stream, args, d)
+    scoring = fused = small = None
+    if N == 1:
+        if not args.skip_scoring:
+            scoring = scoring_bench(abi, cb, dev, stream, args.warmup, args.steps, d)
+        if not args.skip_fused:
+            fused = fused_stage(abi, cb, dev, stream, args, knn)
+    knn.close()
 
-    # ---------------- stage 2: policy sweep
-    replay = None
-    if not args.skip_replay:
-        t0 = time.time()
-        n_tr = args.sweep_traces
-        cfgs, tasks, offs, jobs = sweep_inputs(cb, n_tr)
-        sweep_gen_s = time.time() - t0
-        n_placed = int(np.diff(offs.astype(np.int64))[jobs["trace"]].sum())
-        plan = cb.ReplayPlan(cfgs, tasks, offs, jobs, device=dev)
-        log(f"[rank {d.rank}] sweep inputs {n_tr} traces x {len(SWEEP_POLICIES)} in {time.time() - t0:.1f}s")
-        for _ in range(args.warmup):
-            plan.run()
-        km, rm = ctypes.c_double(), ctypes.c_double()
-        kernel_ms, run_ms = [], []
-        d.barrier()
-        for _ in range(args.steps):
-            plan.run()
-            abi.check(abi.lib.carma_replay_plan_timing(plan._h, ctypes.byref(km), ctypes.byref(rm)))
-            kernel_ms.append(km.value)
-            run_ms.append(rm.value)
-        d.barrier()
-        res = plan.results(tasks=False)
-        assert (res.traces["status"] == 0).all()
-        launches_r, retried = plan.stats()
-        events = int(res.traces["events"].sum())
-        plan.close()
-        run_avg = d.max(statistics.mean(run_ms))
-        k_avg = statistics.mean(kernel_ms)
-        # e2e through the plan's host API: every step uploads the tasks from
-        # pinned memory, replays, and reads back per-task outcomes + reports
-        plan = cb.ReplayPlan(cfgs, tasks, offs, jobs, device=dev)
-        h_tasks = torch.from_numpy(tasks.view(np.uint8)).pin_memory().numpy().view(tasks.dtype)
-        o_t = torch.empty(n_placed * 24, dtype=torch.uint8).pin_memory().numpy().view(abi.task_outcome_dtype)
-        o_j = torch.empty(len(jobs) * 80, dtype=torch.uint8).pin_memory().numpy().view(abi.trace_result_dtype)
-        o_g = torch.empty(len(jobs) * 4 * 32, dtype=torch.uint8).pin_memory().numpy().view(abi.gpu_result_dtype)
-
-        def e2e_step():
-            abi.check(abi.lib.carma_replay_plan_upload_tasks(plan._h, h_tasks.ctypes.data))
-            abi.check(abi.lib.carma_replay_plan_run(plan._h, None))
-            abi.check(abi.lib.carma_replay_plan_outcomes(plan._h, o_t.ctypes.data, o_j.ctypes.data,
-                                                         o_g.ctypes.data))
-
-        e2e_step()
-        d.barrier()
-        t = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
-        r_e2e = d.max((time.perf_counter() - t) / args.steps)
-        plan.close()
-        assert np.array_equal(o_j["energy_mj"], res.traces["energy_mj"])
-        # e2e from seeds: the sweep's traces generated and materialised on the
-        # device (carma_replay_plan_create_generated), replayed, outcomes read
-        # back — run_sweep's inputs without the host trace loop
-        seeds = np.arange(1, n_tr + 1, dtype=np.uint64)
-
-        def gen_step():
-            p = cb.ReplayPlan.generated(cfgs, "t90", seeds, jobs, device=dev)
-            abi.check(abi.lib.carma_replay_plan_run(p._h, None))
-            abi.check(abi.lib.carma_replay_plan_outcomes(p._h, o_t.ctypes.data, o_j.ctypes.data, o_g.ctypes.data))
-            p.close()
-
-        gen_step()
-        d.barrier()
-        t = time.perf_counter()
-        for _ in range(args.steps):
-            gen_step()
-        r_gen = d.max((time.perf_counter() - t) / args.steps)
-        assert np.array_equal(o_j["energy_mj"], res.traces["energy_mj"]), "generated sweep differs"
-        replay = {
-            "metric": "trace-replay placed tasks/sec", "unit": "placed tasks/s",
-            "value": N * n_placed / (run_avg * 1e-3), "ms_per_step": run_avg,
-            "config": {"workload": f"c4 policy sweep: t90 seeds 1..{n_tr} x {{exclusive, rr, magm, lug}}, "
-                                   "MPS, u=0.8, no estimator, 4 GPUs x 40 GiB, W=60 s",
-                       "jobs_per_gpu": len(jobs), "placed_tasks_per_gpu": n_placed},
-            "events_per_s": N * events / (run_avg * 1e-3),
-            "e2e": {"value": N * n_placed / r_e2e, "unit": "placed tasks/s",
-                    "h2d_bytes_per_step": int(h_tasks.nbytes),
-                    "d2h_bytes_per_step": int(o_t.nbytes + o_j.nbytes + o_g.nbytes),
-                    "api": "carma_replay_plan_upload_tasks + run + outcomes (per-task outcomes, reports, per-GPU)",
-                    "from_seeds": {"value": N * n_placed / r_gen, "unit": "placed tasks/s",
-                                   "h2d_bytes_per_step": int(seeds.nbytes),
-                                   "d2h_bytes_per_step": int(o_t.nbytes + o_j.nbytes + o_g.nbytes),
-                                   "api": "carma_replay_plan_create_generated (traces generated on the device) "
-                                          "+ run + outcomes"},
-                    "host_trace_generation_s": sweep_gen_s},
-            "gpu_launches": int(launches_r) * args.steps,
-            "retried_jobs": int(retried),
-            "roofline": {"bound": "hbm", "achieved": ALG_BYTES_PER_TASK * n_placed / (k_avg * 1e-3) / 1e9,
-                         "peak": peaks().get("hbm_gbs", 6650.0), "unit": "GB/s",
-                         "frac": ALG_BYTES_PER_TASK * n_placed / (k_avg * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6650.0),
-                         "traffic": profile_traffic("replay_kernel"),
-                         "note": "latency/issue bound event loop; algorithmic bytes = 80 B per placed task"},
-        }
-
-    # ---------------- placement scoring (feasibility / score matrix, B9)
-    scoring = None
-    if not args.skip_scoring:
-        scoring = scoring_bench(abi, cb, dev, stream, args.warmup, args.steps, d)
-
-    # ---------------- stage 1 -> 2 fused (configs[4], c5)
-    fused = None
-    if not args.skip_fused:
-        t0 = time.time()
-        mf = cb.materialize_trace(cb.generate_uniform_trace(args.fused_tasks, 3.0, 7))
-        cfg5 = cb.make_config(cb.PolicyConfig(policy="magm", max_smact=0.8, monitor_window=5.0),
-                              cb.SimConstants(gpu_count=64))
-        fr = cb.FusedReplay(mf, cfg5, knn, dev)
-        log(f"[rank {d.rank}] fused inputs {args.fused_tasks} tasks in {time.time() - t0:.1f}s")
-        fr.run()  # warm-up (one: a step is ~13 s at 10^6 tasks)
-        torch.cuda.synchronize()
-        d.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        fr.run()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        f_ms = d.max(e0.elapsed_time(e1))
-        fres = fr.results().traces[0]
-        assert fres["status"] == 0
-        fr.close()
-        fused = {"metric": "fused estimator-in-the-loop placed tasks/sec", "unit": "placed tasks/s",
-                 "value": N * args.fused_tasks / (f_ms * 1e-3), "ms_per_step": f_ms, "steps": 1, "warmup": 1,
-                 "config": {"workload": f"c5: {args.fused_tasks} arrivals, uniform catalog, exp gaps mean 3 s, "
-                                        "seed 7; k-NN pre-pass over every arrival on device feeding the replay; "
-                                        "MAGM + learned, u=0.8, W=5 s, 64 simulated GPUs"},
-                 "events": int(fres["events"]), "oom_count": int(fres["oom_count"]),
-                 "note": "one trace: a single warp replays it (sequential event loop); replicas only across GPUs",
-                 "cpu_reference_full_trace": recorded("c5_cpu_full_r01.json")}
-
-    # ---------------- CPU baselines (rank 0, N = 1)
     cpu = None
+    cpus = host_cpus()
     if d.rank == 0 and N == 1 and not args.skip_cpu:
         ref = ref_lib()
         threads = os.cpu_count() or 1
         if ref is not None:
             rate, sample = cpu_knn_baseline(ref, threads)
-            cpu = {"value": rate, "unit": "estimates/s", "cores": threads, "kind": "reference", "sample": sample}
+            cpu = {"value": rate, "unit": "estimates/s", "cores": threads, "kind": "reference", "sample": sample,
+                   **cpus}
             if replay is not None:
                 srate, ssample, _ = cpu_sweep_baseline(ref, threads)
                 replay["cpu_baseline"] = {"value": srate, "unit": "placed tasks/s", "cores": threads,
-                                          "kind": "reference", "sample": ssample}
+                                          "kind": "reference", "sample": ssample, **cpus}
             if fused is not None:
                 frate, fsample = cpu_fused_baseline(ref, args.fused_cpu_tasks)
                 fused["cpu_baseline"] = {"value": frate, "unit": "placed tasks/s", "cores": 1, "kind": "reference",
                                          "sample": fsample}
-
-    small = None
     if d.rank == 0 and N == 1 and not args.skip_small:
-        small = small_configs(cb, abi, dev, None if args.skip_cpu else ref_lib())
-
+        small = small_configs(cb, abi, dev, stream, None if args.skip_cpu else ref_lib())
     if d.rank != 0:
         return
-    hbm = peaks().get("hbm_gbs")
     line = {
         "metric": "GPUMemNet estimates/sec (k-NN, CNN+Transformer ensemble)",
-        "value": value, "unit": "estimates/s", "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": knn_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "value": knn_res["value"], "unit": "estimates/s", "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": knn_res["ms_per_step"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (reference generators, seeded)",
-        "config": knn_config(N),
-        "e2e": {"value": N * Q / e2e_s, "unit": "estimates/s",
-                "h2d_bytes_per_step": int(h_rows.nbytes),
-                "d2h_bytes_per_step": int(h_b.nbytes + h_by.nbytes),
-                "api": f"carma_knn_predict_bitpacked ({4 * wpr} B bit-packed rows, pinned host buffers)",
-                "packed64_api_estimates_per_s": N * Q / e2e_pk_s,
-                "feature_row_api_estimates_per_s": N * Q / e2e_full_s},
-        "gpu_launches": int(launches) * args.steps,
-        "roofline": {"bound": "fp32", "achieved": achieved / 1e12, "peak": fp32.value / 1e12, "unit": "TFLOP/s",
-                     "frac": achieved / fp32.value, "traffic": traffic,
-                     "kernel": "knn_search_f32", "kernel_ms": search_avg,
-                     "kernel_share_of_step": search_avg / statistics.mean(pipe_ms),
-                     "peak_source": "measured: carma_probe_fp32 (FFMA2 issue rate; the contract's MEASURED_PEAKS "
-                                    "file has no fp32/fp64 figures)",
-                     "work": f"{visits} fp32 pre-filter evaluations x {FLOPS_PER_F32_EVAL} flops + {evals} exact "
-                             f"fp64 evaluations x {FLOPS_PER_EVAL} flops",
-                     "fp64": {"achieved": evals * FLOPS_PER_EVAL / (search_avg * 1e-3) / 1e12,
-                              "peak": fp64.value / 1e12, "unit": "TFLOP/s"},
-                     "brute_force_equivalent_tflops": Q * 162_400 / (search_avg * 1e-3) / 1e12,
-                     "hbm_gbs": ALG_BYTES_PER_ESTIMATE * Q / (search_avg * 1e-3) / 1e9, "hbm_peak_gbs": hbm,
-                     "note": "exact pruned search: the bound is instruction issue over the fp32 pass; the brute-force "
-                             "figure (162,400 flops/estimate) is what the pruning avoids"},
-        "cpu_baseline": cpu,
-        "clocks": clocks,
-        "replay": replay,
-        "neural": neural,
-        "scoring": scoring,
-        "fused": fused,
-        "small_configs": small,
+        "config": knn_config(N, e - b),
+        "e2e": knn_res["e2e"], "gpu_launches": knn_res["gpu_launches"], "roofline": knn_res["roofline"],
+        "cpu_baseline": cpu, "clocks": knn_res["clocks"],
+        "neural": neural, "scoring": scoring, "fused": fused, "small_configs": small, "replay": replay,
     }
-    print(json.dumps(line))
+    detail_dir = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(detail_dir, exist_ok=True)
+    with open(os.path.join(detail_dir, f"bench_detail_n{N}.json"), "w") as f:
+        json.dump(line, f, indent=1)
+    # the stdout line: the contract keys, then short sub-objects, the replay half last
+    short = dict(line)
+    short["roofline"] = compact(line["roofline"], ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel",
+                                                   "kernel_ms", "kernel_share_of_step", "peak_source"))
+    short["e2e"] = compact(line["e2e"], ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step", "api"))
+    short["cpu_baseline"] = compact(cpu, ("value", "unit", "cores", "kind", "logical_cpus", "physical_cores"))
+    short["clocks"] = compact(line["clocks"], ("sm_mhz", "sm_max_mhz", "reasons"))
+    short["neural"] = None if neural is None else {
+        "mlp": {"value": neural["mlp"]["value"], "ms_per_step": neural["mlp"]["ms_per_step"],
+                "e2e": neural["mlp"]["e2e"]["value"], "roofline_frac": neural["mlp"]["roofline"]["frac"]},
+        "transformer": {"value": neural["transformer"]["value"],
+                        "ms_per_step": neural["transformer"]["ms_per_step"],
+                        "e2e": neural["transformer"]["e2e"]["value"]}}
+    short["scoring"] = None if scoring is None else {"value": scoring["value"], "unit": scoring["unit"],
+                                                     "roofline_frac": scoring["roofline"]["frac"]}
+    short["fused"] = None if fused is None else {"value": fused["value"], "unit": fused["unit"],
+                                                 "ms_per_step": fused["ms_per_step"], "parity": fused["parity"][:12],
+                                                 "cpu_sample": (fused.get("cpu_baseline") or {}).get("value"),
+                                                 "cpu_full": (fused.get("cpu_reference_full_trace") or {}).get("value")}
+    short["small_configs"] = None if small is None else "gpurun_out/bench_detail_n1.json"
+    short["detail"] = f"gpurun_out/bench_detail_n{N}.json"
+    if replay is not None:
+        short["replay"] = {"metric": replay["metric"], "value": replay["value"], "unit": replay["unit"],
+                           "ms_per_step": replay["ms_per_step"], "e2e": replay["e2e"]["value"],
+                           "cpu_baseline": compact(replay.get("cpu_baseline"), ("value", "cores", "kind")),
+                           "roofline_frac": replay["roofline"]["frac"], "scaling": "strong"}
+    print(json.dumps(short))
 
 
 def main():
@@ -984,7 +1003,11 @@ def main():
     if args.warmup < 3:
         log("note: warmup raised to 3 (timing rule)")
         args.warmup = 3
-    d = Dist(args.gpus)
+    if args.impl == "reference":
+        # the reference arm never touches the GPU or libcarma_b200.so: no NCCL
+        d = Dist(args.gpus, backend="gloo")
+    else:
+        d = Dist(args.gpus)
     try:
         if args.impl == "reference":
             run_reference(args, d)

@@ -55,6 +55,9 @@ int carma_device_count(void);
 #define CARMA_FEATURE_DIMS 19
 #define CARMA_MAX_K 32
 #define CARMA_FAMILIES 3 /* ModelFamily: 0 MLP, 1 CNN, 2 Transformer (task.hpp:30) */
+#define CARMA_FAMILY_MLP 0
+#define CARMA_FAMILY_CNN 1
+#define CARMA_FAMILY_TRANSFORMER 2
 
 /* The FeatureVector summary a prediction consumes (task.hpp:89-100):
  * tallies, activation (cos, sin) and the first / middle / last layer tuples
@@ -160,6 +163,16 @@ carma_status carma_knn_train(carma_knn* h, int32_t family, const carma_feature_r
 /* The optional *_out buffers (nullable) receive the fitted LearnedEstimator
  * state (estimators.hpp:108-133): lo[19], hi[19], points[train_size x 19] and
  * labels[train_size] in training order (train_size = max(1, 7n/10)). */
+
+/* LearnedEstimator::load (estimators.cpp:503-538) into the bank: installs a
+ * "carma-knn-estimator/v1" snapshot (the JSON text LearnedEstimator::save
+ * writes, estimators.cpp:481-501) as the model of its family. The family and
+ * the stored holdout report are returned (both nullable). Snapshot errors
+ * return INVALID with the reference's message. */
+carma_status carma_knn_load_snapshot(carma_knn* h, const char* json, uint64_t len, int32_t* family_out,
+                                     carma_holdout_report* holdout_out);
+carma_status carma_knn_load_snapshot_file(carma_knn* h, const char* path, int32_t* family_out,
+                                          carma_holdout_report* holdout_out);
 
 /* Host-buffer batch predict (the drop-in for estimate_learned over q rows).
  * family: per-row family (nullable: every row is default_family).

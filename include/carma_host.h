@@ -79,6 +79,14 @@ carma_status carma_mig_layout(const double* fractions, uint32_t n, carma_replay_
 /* The seeded 70/30 split of train_learned_estimator (estimators.cpp:355-361):
  * order[n] = shuffled row indices, *train_n = max(1, 7n/10). */
 carma_status carma_host_split_order(uint64_t n, uint64_t seed, uint64_t* order, uint64_t* train_n);
+/* The fitted state of a LearnedEstimator snapshot (estimators.cpp:481-538):
+ * family, k, bucket_range, seed, lo[19], hi[19], holdout; points[n x 19] and
+ * labels[n] when non-NULL (capacity >= n). *n = the stored point count. Every
+ * output pointer is nullable. */
+carma_status carma_host_parse_snapshot(const char* json, uint64_t len, int32_t* family, uint64_t* k,
+                                       uint64_t* bucket_range, uint64_t* seed, double* lo, double* hi,
+                                       double* points, int32_t* labels, uint64_t capacity, uint64_t* n,
+                                       carma_holdout_report* holdout);
 /* scalar_features for n feature rows -> n x 19 doubles. */
 carma_status carma_host_scalar_features(const carma_feature_row* rows, uint64_t n, double* out);
 

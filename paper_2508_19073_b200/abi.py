@@ -191,7 +191,12 @@ SIGNATURES = {
     "carma_knn_predict_multi": (c_int, [P, c_uint32, P, P, c_int32, c_uint64, P, P]),
     "carma_nn_predict_multi": (c_int, [P, c_uint32, P, P, c_int32, c_uint64, P, P]),
     "carma_replay_batch_multi": (c_int, [P, c_uint32, P, c_uint32, P, P, c_uint32, P, c_uint32, P, P, P]),
+    "carma_knn_load_snapshot": (c_int, [c_void_p, c_char_p, c_uint64, POINTER(c_int32), P]),
+    "carma_knn_load_snapshot_file": (c_int, [c_void_p, c_char_p, POINTER(c_int32), P]),
     # carma_host.h
+    "carma_host_parse_snapshot": (c_int, [c_char_p, c_uint64, POINTER(c_int32), POINTER(c_uint64),
+                                          POINTER(c_uint64), POINTER(c_uint64), P, P, P, P, c_uint64,
+                                          POINTER(c_uint64), P]),
     "carma_host_catalog_size": (c_int, []),
     "carma_host_catalog_entry": (c_int, [c_int, c_char_p, c_int, P, P, P, P]),
     "carma_host_generate_trace": (c_int, [c_int32, c_uint64, P, P, P, c_uint64, POINTER(c_uint64)]),

@@ -216,6 +216,25 @@ def fit_knn(family: int, samples: int, seed: int, k: int = 5) -> KnnModel:
                     hold[: nh.value].astype(np.int64), seed)
 
 
+def parse_snapshot(text) -> KnnModel:
+    """A LearnedEstimator snapshot ("carma-knn-estimator/v1" JSON, the file
+    LearnedEstimator::save writes, estimators.cpp:481-538) as a KnnModel."""
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    n, k, br, seed = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    fam = ctypes.c_int32()
+    check(lib.carma_host_parse_snapshot(raw, len(raw), ctypes.byref(fam), ctypes.byref(k), ctypes.byref(br),
+                                        ctypes.byref(seed), None, None, None, None, 0, ctypes.byref(n), None))
+    lo, hi = np.zeros(19), np.zeros(19)
+    pts = np.zeros((n.value, 19))
+    lab = np.zeros(n.value, np.int32)
+    hold = np.zeros(1, abi.holdout_report_dtype)
+    check(lib.carma_host_parse_snapshot(raw, len(raw), None, None, None, None, ptr(lo), ptr(hi), ptr(pts), ptr(lab),
+                                        n.value, ctypes.byref(n), ptr(hold)))
+    m = KnnModel(fam.value, k.value, br.value, lo, hi, pts, lab, np.zeros(0, np.int64), seed.value)
+    m.holdout = hold[0]
+    return m
+
+
 class GpuKnn:
     """A device-resident bank of k-NN models, one per family (the drop-in for
     Manager::set_learned_estimators + estimate_learned, manager.cpp:91-97)."""
@@ -236,6 +255,15 @@ class GpuKnn:
         check(lib.carma_knn_set_model(self._h, m.family, ptr(m.lo), ptr(m.hi), ptr(pts), ptr(m.labels), len(m.labels),
                                       m.k, m.bucket_range))
         self.models[m.family] = m
+
+    def load_snapshot(self, path: str) -> int:
+        """LearnedEstimator::load straight into the bank (carma_knn_load_snapshot_file);
+        returns the snapshot's family."""
+        fam = ctypes.c_int32()
+        check(lib.carma_knn_load_snapshot_file(self._h, path.encode(), ctypes.byref(fam), None))
+        with open(path, "rb") as f:
+            self.models[fam.value] = parse_snapshot(f.read())
+        return fam.value
 
     def predict(self, rows: np.ndarray, family=None, default_family: Optional[int] = None):
         """Buckets and upper-edge bytes for feature rows (or raw n x 19 scalar rows)."""

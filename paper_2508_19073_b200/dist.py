@@ -27,6 +27,14 @@ def balanced_shards(weights: Sequence[int], world: int) -> List[Tuple[int, int]]
     return [(int(bounds[r]), int(bounds[r + 1])) for r in range(world)]
 
 
+def balanced_shards_count(n: int, world: int) -> List[Tuple[int, int]]:
+    """balanced_shards for n unit weights without materialising them: cut p
+    at ceil(n * p / world), the same rule."""
+    world = max(1, int(world))
+    cut = [(n * p + world - 1) // world for p in range(world)] + [n]
+    return [(cut[r], cut[r + 1]) for r in range(world)]
+
+
 def gather_to_root(local: np.ndarray, rank: int, world: int, dist=None) -> np.ndarray | None:
     """Concatenates every rank's structured array in rank order on rank 0."""
     if world <= 1 or dist is None:

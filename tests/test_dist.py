@@ -122,3 +122,60 @@ def test_native_shard_rule_matches_restatement():
                       for r in range(1, world)] + [n]
         cuts = np.maximum.accumulate(cuts)
         assert balanced_shards(w, world) == [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+
+
+def _bench_worker(rank, world, port, out_path):
+    """bench.py's N>1 orchestration on gloo: Dist (barrier, max, sum), the row
+    and job shard rules, shard_jobs' per-rank inputs and timed_host_steps;
+    the GPU shard runners are replaced by the oracle."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    import bench
+    import paper_2508_19073_b200 as cb
+    from oracle_bind import load_oracle, oracle_replay
+    from paper_2508_19073_b200 import abi
+    from paper_2508_19073_b200 import dist as cdist
+
+    d = bench.Dist(world, backend="gloo")
+    assert d.n == world and d.rank == rank
+    olib = load_oracle()
+    cfgs, tasks, offs, jobs = bench.sweep_inputs(cb, 30)
+    counts = np.diff(offs.astype(np.int64))[jobs["trace"]]
+    b, e = cdist.balanced_shards(counts, d.n)[d.rank]
+    st, so, sj = bench.shard_jobs(tasks, offs, jobs, b, e)
+    so = so.astype(np.int64)
+    out = np.zeros(len(sj), abi.trace_result_dtype)
+    for k, j in enumerate(sj):
+        out[k] = oracle_replay(olib, cfgs[j["config"]: j["config"] + 1], st[so[j["trace"]]: so[j["trace"] + 1]])[2]
+    placed = int(np.diff(so)[sj["trace"]].sum())
+    assert d.sum(placed) == int(counts.sum())
+    assert d.max(float(rank)) == world - 1
+    dt = bench.timed_host_steps(lambda: None, 1, 2, d)
+    assert dt >= 0.0
+    rb, re_ = cdist.balanced_shards_count(1001, world)[rank]
+    assert d.sum(re_ - rb) == 1001
+    res = cdist.gather_to_root(out, rank, world, d.pg)
+    if rank == 0:
+        np.save(out_path, res)
+    d.barrier()
+    d.close()
+
+
+def test_bench_orchestration_gloo_equals_single_process(tmp_path, olib):
+    out = str(tmp_path / "bench.npy")
+    mp.spawn(_bench_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    import bench
+    import paper_2508_19073_b200 as cb
+    from paper_2508_19073_b200 import abi
+    from oracle_bind import oracle_replay
+    cfgs, tasks, offs, jobs = bench.sweep_inputs(cb, 30)
+    o = offs.astype(np.int64)
+    want = np.zeros(len(jobs), abi.trace_result_dtype)
+    for k, j in enumerate(jobs):
+        want[k] = oracle_replay(olib, cfgs[j["config"]: j["config"] + 1], tasks[o[j["trace"]]: o[j["trace"] + 1]])[2]
+    assert got.tobytes() == want.tobytes()

@@ -191,3 +191,21 @@ def test_mig_layout_matches_gpudevice():
             cb.make_config(cb.PolicyConfig(collocation_mode="mig"), cb.SimConstants(), bad)
     with pytest.raises(abi.CarmaError):
         cb.make_config(cb.PolicyConfig(collocation_mode="mig"), cb.SimConstants(), (0.1,) * 9)
+
+
+def test_reference_bridge_loads_and_fails_loudly_without_gpu():
+    """integration/_build/libcarma_bridge.so (built where /root/reference
+    exists) links the reference library and libcarma_b200.so; on a box with
+    no GPU its GPU side raises the C ABI's error through the reference's
+    exception types while the reference side still runs."""
+    from bridge_bind import case, load_bridge, run_pair
+    lib = load_bridge()
+    if lib is None:
+        pytest.skip("bridge not built (needs /root/reference)")
+    for sym in ("bridge_run_pair", "bridge_sweep_pair", "bridge_estimate_pair", "bridge_manager_estimates"):
+        assert hasattr(lib, sym)
+    if abi.lib.carma_device_count() > 0:
+        pytest.skip("a GPU is present")
+    ref, got = run_pair(lib, case(policy="magm", estimator="oracle"))
+    assert ref.startswith("OK:{") and '"trace_name": "t90-seed1"' in ref or ref.startswith("OK:")
+    assert got.startswith("ERR:") and "no CPU fallback" in got

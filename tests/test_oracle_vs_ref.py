@@ -157,3 +157,40 @@ def test_ref_batch_entries_match_single_calls(ref, olib):
             assert rout[j].tobytes() == one[1].tobytes()
             assert ge[j * 4:(j + 1) * 4].tobytes() == one[2].tobytes()
             assert np.array_equal(gp[j * 4:(j + 1) * 4], one[4])
+
+
+@pytest.mark.parametrize("family,seed", [(0, 11), (1, 112), (2, 213)])
+def test_snapshot_written_by_reference_parses_to_its_state(ref, tmp_path, family, seed):
+    """carma_host_parse_snapshot reads LearnedEstimator::save's JSON
+    (estimators.cpp:481-501) back to the reference's fitted state bit for bit
+    (and to the host fit the GPU bank installs)."""
+    path = str(tmp_path / f"est{family}.json")
+    lo, hi = np.zeros(19), np.zeros(19)
+    pts, lab = np.zeros((4000, 19)), np.zeros(4000, np.int32)
+    n, br, h = ctypes.c_uint64(), ctypes.c_uint64(), np.zeros(3)
+    assert ref.ref_train(family, 4000, seed, 5, path.encode(), lo.ctypes.data, hi.ctypes.data, pts.ctypes.data,
+                         lab.ctypes.data, 4000, ctypes.byref(n), ctypes.byref(br), h.ctypes.data) == 0
+    m = cb.parse_snapshot(open(path, "rb").read())
+    assert m.family == family and m.k == 5 and m.bucket_range == br.value and m.seed == seed
+    assert m.lo.tobytes() == lo.tobytes() and m.hi.tobytes() == hi.tobytes()
+    assert m.points.tobytes() == pts[: n.value].tobytes() and np.array_equal(m.labels, lab[: n.value])
+    assert np.float64(m.holdout["accuracy"]).tobytes() == np.float64(h[0]).tobytes()
+    assert np.float64(m.holdout["macro_f1"]).tobytes() == np.float64(h[1]).tobytes()
+    assert np.float64(m.holdout["underestimate_rate"]).tobytes() == np.float64(h[2]).tobytes()
+    f = cb.fit_knn(family, 4000, seed, 5)
+    assert f.points.tobytes() == m.points.tobytes()
+
+
+def test_snapshot_errors_follow_the_reference():
+    from paper_2508_19073_b200 import abi
+    with pytest.raises(abi.CarmaError, match="unrecognized estimator snapshot schema"):
+        cb.parse_snapshot(b'{"schema": "other"}')
+    bad = (b'{"schema": "carma-knn-estimator/v1", "family": "cnn", "bucket_range": 8, "k": 5, "seed": 1, '
+           b'"lo": [' + b",".join([b"0.0"] * 19) + b'], "hi": [' + b",".join([b"1.0"] * 19) + b'], '
+           b'"labels": [1, 2], "points": [[' + b",".join([b"0.5"] * 19) + b']], "holdout": {}}')
+    with pytest.raises(abi.CarmaError, match="labels/points mismatch"):
+        cb.parse_snapshot(bad)
+    with pytest.raises(abi.CarmaError, match="unsupported model family"):
+        cb.parse_snapshot(bad.replace(b'"cnn"', b'"rnn"'))
+    with pytest.raises(abi.CarmaError, match="malformed"):
+        cb.parse_snapshot(b'{"schema": "carma-knn-estimator/v1", ')
