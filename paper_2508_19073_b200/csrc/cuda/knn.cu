@@ -563,15 +563,22 @@ __global__ void __launch_bounds__(128, 4)
                 // Vote over the kk = min(k, n) neighbours (estimators.cpp:463-474):
                 // real entries are slots [K-k, K) whose id is a training index.
                 int best = 0, best_votes = 0;
+                // labels of the k nearest, loaded once (vm: filled slots)
+                int lab[K];
+                unsigned vm = 0;
 #pragma unroll
                 for (int a = 0; a < K; ++a) {
-                    if (a < K - k || top.id[a] == 0x7fffffff) continue;
-                    const int la = __ldg(m.label_by_orig + top.id[a]);
+                    const bool ok = a >= K - k && top.id[a] != 0x7fffffff;
+                    lab[a] = ok ? __ldg(m.label_by_orig + top.id[a]) : 0;
+                    vm |= ok ? (1u << a) : 0u;
+                }
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    if (!((vm >> a) & 1u)) continue;
+                    const int la = lab[a];
                     int votes = 0;
 #pragma unroll
-                    for (int b = 0; b < K; ++b)
-                        if (b >= K - k && top.id[b] != 0x7fffffff && __ldg(m.label_by_orig + top.id[b]) == la)
-                            ++votes;
+                    for (int b = 0; b < K; ++b) votes += (((vm >> b) & 1u) && lab[b] == la) ? 1 : 0;
                     if (votes > best_votes || (votes == best_votes && la > best)) {
                         best = la;
                         best_votes = votes;
@@ -805,26 +812,50 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
             // buffered candidates that still pass the (possibly tightened)
             // bound, then tighten kth.
             auto flush = [&]() {
+                // Two candidates per lane per round: their fp64 chains (19
+                // dependent adds each, reference order) interleave, which
+                // halves this latency-bound phase. The top-k is independent
+                // of insertion order.
                 for (;;) {
-                    const bool have = cnt > 0;
-                    if (!__any_sync(0xffffffffu, have)) break;
-                    if (have) {
+                    if (!__any_sync(0xffffffffu, cnt > 0)) break;
+                    uint32_t ia = 0xffffffffu, ib = 0xffffffffu;
+                    if (cnt > 0) {
                         --cnt;
-                        if (!(cbuf_s[cnt][tid] > T_lb)) {
-                            const uint32_t sidx = cbuf_i[cnt][tid];
-                            const double* pt = m.pts + static_cast<int64_t>(sidx) * kStride;
-                            double d2 = 0.0;
+                        if (!(cbuf_s[cnt][tid] > T_lb)) ia = cbuf_i[cnt][tid];
+                    }
+                    if (cnt > 0) {
+                        --cnt;
+                        if (!(cbuf_s[cnt][tid] > T_lb)) ib = cbuf_i[cnt][tid];
+                    }
+                    if (ia == 0xffffffffu) {
+                        ia = ib;
+                        ib = 0xffffffffu;
+                    }
+                    if (ia != 0xffffffffu) {
+                        const bool two = ib != 0xffffffffu;
+                        const double* pa = m.pts + static_cast<int64_t>(ia) * kStride;
+                        const double* pb = m.pts + static_cast<int64_t>(two ? ib : ia) * kStride;
+                        double da = 0.0, db = 0.0;
 #pragma unroll
-                            for (int h = 0; h < 9; ++h) {
-                                const double2 v = __ldg(reinterpret_cast<const double2*>(pt) + h);
-                                const double a = __dsub_rn(v.x, qsh[2 * h][tid]);
-                                d2 = __dadd_rn(d2, __dmul_rn(a, a));
-                                const double b = __dsub_rn(v.y, qsh[2 * h + 1][tid]);
-                                d2 = __dadd_rn(d2, __dmul_rn(b, b));
-                            }
-                            const double a = __dmul_rn(__dsub_rn(__ldg(pt + 18), q18), 64.0);
-                            d2 = __dadd_rn(d2, __dmul_rn(a, a));
-                            top.insert(d2, __ldg(m.orig + sidx));
+                        for (int h = 0; h < 9; ++h) {
+                            const double2 va = __ldg(reinterpret_cast<const double2*>(pa) + h);
+                            const double2 vb = __ldg(reinterpret_cast<const double2*>(pb) + h);
+                            const double q0 = qsh[2 * h][tid], q1 = qsh[2 * h + 1][tid];
+                            const double a0 = __dsub_rn(va.x, q0), b0 = __dsub_rn(vb.x, q0);
+                            da = __dadd_rn(da, __dmul_rn(a0, a0));
+                            db = __dadd_rn(db, __dmul_rn(b0, b0));
+                            const double a1 = __dsub_rn(va.y, q1), b1 = __dsub_rn(vb.y, q1);
+                            da = __dadd_rn(da, __dmul_rn(a1, a1));
+                            db = __dadd_rn(db, __dmul_rn(b1, b1));
+                        }
+                        const double a = __dmul_rn(__dsub_rn(__ldg(pa + 18), q18), 64.0);
+                        const double b = __dmul_rn(__dsub_rn(__ldg(pb + 18), q18), 64.0);
+                        da = __dadd_rn(da, __dmul_rn(a, a));
+                        db = __dadd_rn(db, __dmul_rn(b, b));
+                        top.insert(da, __ldg(m.orig + ia));
+                        ++exact;
+                        if (two) {
+                            top.insert(db, __ldg(m.orig + ib));
                             ++exact;
                         }
                     }
@@ -867,6 +898,10 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
                 const int side = go_left ? 0 : 1;
                 const int32_t nxt = go_left ? L - kBlock : R;
                 const float4 pre = __ldg(pf4 + static_cast<int64_t>(nxt) * (kF32Dims / 4) + lane);
+                // The side's next bound key, loaded before the block's math so
+                // its latency hides behind it (consumed by the next ballot).
+                const int32_t kidx = go_left ? (L > 0 ? L - 1 : 0) : (R < n ? R : n - 1);
+                const double knext = __ldg(m.key18 + kidx);
                 // Two packed partial sums per point (even / odd active dims),
                 // folded at the end: any order of the 16 non-negative terms
                 // stays within the 17u accumulation bound.
@@ -939,23 +974,30 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
                         }
                     }
                 }
-                if (go_left) tl = L > 0 ? (L <= pos ? t18_of(__ldg(m.key18 + L - 1), q18) : t_in) : inf;
-                else tr = R < n ? (R >= pos ? t18_of(__ldg(m.key18 + R), q18) : t_in) : inf;
+                if (go_left) tl = L > 0 ? (L <= pos ? t18_of(knext, q18) : t_in) : inf;
+                else tr = R < n ? (R >= pos ? t18_of(knext, q18) : t_in) : inf;
             }
             my_visits += visits;
             my_exact += exact;
 
             if (mine) {
                 int best = 0, best_votes = 0;
+                // labels of the k nearest, loaded once (vm: filled slots)
+                int lab[K];
+                unsigned vm = 0;
 #pragma unroll
                 for (int a = 0; a < K; ++a) {
-                    if (a < K - k || top.id[a] == 0x7fffffff) continue;
-                    const int la = __ldg(m.label_by_orig + top.id[a]);
+                    const bool ok = a >= K - k && top.id[a] != 0x7fffffff;
+                    lab[a] = ok ? __ldg(m.label_by_orig + top.id[a]) : 0;
+                    vm |= ok ? (1u << a) : 0u;
+                }
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    if (!((vm >> a) & 1u)) continue;
+                    const int la = lab[a];
                     int votes = 0;
 #pragma unroll
-                    for (int b = 0; b < K; ++b)
-                        if (b >= K - k && top.id[b] != 0x7fffffff && __ldg(m.label_by_orig + top.id[b]) == la)
-                            ++votes;
+                    for (int b = 0; b < K; ++b) votes += (((vm >> b) & 1u) && lab[b] == la) ? 1 : 0;
                     if (votes > best_votes || (votes == best_votes && la > best)) {
                         best = la;
                         best_votes = votes;

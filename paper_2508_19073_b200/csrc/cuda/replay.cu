@@ -183,6 +183,11 @@ template <int G, int F> using HeavyL = Layout<G, 320, 64, 32, 16, 16, 2, F>;
 // 64 GPUs peaks at 128 residents and ~215 pending events): one warp per CTA.
 template <int F> using LargeL = Layout<64, 1024, 256, 32, 16, 128, 2, F>;
 template <int F> using GlobalL = Layout<64, 8192, 2048, 256, 256, 4096, 4, F>;
+// The same with 64 bitmap words per GPU (<= 4096 allocation blocks: e.g. a
+// 192 GiB device at 512 MiB blocks, or 40 GiB at 16 MiB) for plans that
+// hold such a config.
+template <int F> using GlobalWideL = Layout<64, 8192, 2048, 256, 256, 4096, replay::kMaxWords, F>;
+constexpr int kGlobalBlocks = 64 * 4;
 
 // Configs whose policy can stack tasks without utilisation preconditions.
 bool heavy_config(const carma_replay_config& c) {
@@ -200,7 +205,7 @@ void validate_config(const carma_replay_config& c) {
     if (c.gpu_capacity % c.alloc_block != 0)
         throw Unsupported("gpu_capacity must be a multiple of alloc_block");
     if (c.gpu_capacity / c.alloc_block > 64ull * replay::kMaxWords)
-        throw Unsupported("more than 256 allocation blocks per GPU");
+        throw Unsupported("more than 4096 allocation blocks per GPU");
     if (!(c.sample_interval >= 0.0)) throw InvalidArg("ConfigError: sample_interval must be >= 0");
     if (c.log_flags & ~(CARMA_LOG_EVENTS | CARMA_LOG_DECISIONS)) throw InvalidArg("unknown log_flags bits");
     if (c.mode == CARMA_MODE_MIG) {
@@ -269,6 +274,7 @@ void launch_tier(ReplayPlan& pl, const replay::Params& base, const uint32_t* lis
         if (tier == 1) return launch_shared<HeavyL, F>(pl, p, max_g, sms);
     }
     if (tier == 3) launch<LargeL<F>, true>(pl, p, sms, 1);
+    else if (pl.max_blocks > kGlobalBlocks) launch<GlobalWideL<F>, false>(pl, p, sms);
     else launch<GlobalL<F>, false>(pl, p, sms);
 }
 

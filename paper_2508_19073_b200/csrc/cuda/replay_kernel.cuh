@@ -63,7 +63,7 @@ constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kWindow = 1u, kCompletion = 2u, kCrash = 3u, kTick = 4u;
 constexpr int32_t kStatusRetry = -1;      // overflowed this tier
 constexpr int32_t kStatusRedoSmact = -2;  // full-history SMACT needs the true window begin
-constexpr int kMaxWords = 4;              // bitmap words per GPU: <= 256 blocks
+constexpr int kMaxWords = 64;             // bitmap words per GPU: <= 4096 blocks (wide global tier)
 
 struct Params {
     const carma_replay_config* cfgs;
