@@ -87,6 +87,10 @@ carma_status carma_host_parse_snapshot(const char* json, uint64_t len, int32_t* 
                                        uint64_t* bucket_range, uint64_t* seed, double* lo, double* hi,
                                        double* points, int32_t* labels, uint64_t capacity, uint64_t* n,
                                        carma_holdout_report* holdout);
+/* Test hook: compares the device trace generator's log1p (glibc's own
+ * algorithm, csrc/cuda/glibc_log1p.cuh, built for the host) with the C
+ * library's log1p on n pseudo-random inputs; *mismatches = differing results. */
+carma_status carma_host_check_log1p(uint64_t n, uint64_t seed, uint64_t* mismatches);
 /* scalar_features for n feature rows -> n x 19 doubles. */
 carma_status carma_host_scalar_features(const carma_feature_row* rows, uint64_t n, double* out);
 

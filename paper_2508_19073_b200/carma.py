@@ -212,8 +212,10 @@ def fit_knn(family: int, samples: int, seed: int, k: int = 5) -> KnnModel:
     n, br, nh = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
     check(lib.carma_host_fit(family, samples, seed, k, ptr(lo), ptr(hi), ptr(pts), ptr(lab), samples,
                              ctypes.byref(n), ctypes.byref(br), ptr(hold), ctypes.byref(nh)))
-    return KnnModel(family, k, br.value, lo, hi, pts[: n.value].copy(), lab[: n.value].copy(),
-                    hold[: nh.value].astype(np.int64), seed)
+    m = KnnModel(family, k, br.value, lo, hi, pts[: n.value].copy(), lab[: n.value].copy(),
+                 hold[: nh.value].astype(np.int64), seed)
+    m.samples = samples
+    return m
 
 
 def parse_snapshot(text) -> KnnModel:
@@ -619,7 +621,7 @@ def replay_multi(devices: Sequence[int], configs: np.ndarray, tasks: np.ndarray,
 class RunConfig:
     """runner.hpp:18-40 (trace source, policy, constants, estimator provisioning)."""
 
-    mix: Optional[str] = "t90"
+    mix: Optional[str] = None  # runner.hpp:20: unset by default; trace_path is used when mix is not set
     trace_seed: int = 1
     trace_path: Optional[str] = None
     policy: PolicyConfig = dataclasses.field(default_factory=PolicyConfig)
@@ -657,8 +659,12 @@ def provision_estimates(rc: RunConfig, m: Materialized, device: int = 0,
         return
     knn = knn or GpuKnn(device)
     for fam in sorted(set(m.family.tolist())):
-        if fam not in knn.models:
-            seed = rc.estimator_seed + fam * 101
+        seed = rc.estimator_seed + fam * 101
+        have = knn.models.get(fam)
+        # provision_estimators (runner.cpp:17-38) trains per config: a bank
+        # model trained with other settings is replaced, not reused
+        if have is None or (have.seed, have.k, getattr(have, "samples", None)) != \
+                (seed, rc.estimator_k, rc.estimator_samples):
             knn.set_model(fit_knn(fam, rc.estimator_samples, seed, rc.estimator_k))
     _, nbytes = knn.predict(m.features, family=m.family)
     m.tasks["estimate"] = nbytes
@@ -675,9 +681,19 @@ def entry_estimates(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None
     return m.tasks["estimate"].copy()
 
 
+def _run_trace(rc: "RunConfig"):
+    """run_simulation's trace source (runner.cpp:42-55): the mix when set,
+    else the trace file, else ConfigError."""
+    if rc.mix:
+        return generate_trace(rc.mix, rc.trace_seed)
+    if not rc.trace_path:
+        raise abi.CarmaError(abi.CARMA_ERR_INVALID, "ConfigError: run needs either a trace path or a mix+seed")
+    return load_trace(rc.trace_path)
+
+
 def run_simulation(rc: RunConfig, device: int = 0, knn: Optional[GpuKnn] = None):
     """Replays one trace on the GPU; returns (trace result, task results, gpu results)."""
-    trace = load_trace(rc.trace_path) if rc.trace_path else generate_trace(rc.mix, rc.trace_seed)
+    trace = _run_trace(rc)
     m = materialize_trace(trace)
     provision_estimates(rc, m, device, knn)
     res = replay(make_config(rc.policy, rc.constants, rc.mig_instances), [m.tasks], device=device)
@@ -740,7 +756,7 @@ def run_simulation_artifacts(rc: RunConfig, device: int = 0, knn: Optional[GpuKn
     """run_simulation with the reference's output switches: the sample ticks of
     enable_timeline are events of the replay (they split the energy integration
     exactly as in the reference), their rows come back formatted."""
-    trace = load_trace(rc.trace_path) if rc.trace_path else generate_trace(rc.mix, rc.trace_seed)
+    trace = _run_trace(rc)
     m = materialize_trace(trace)
     provision_estimates(rc, m, device, knn)
     flags = (abi.LOG_EVENTS if rc.enable_event_log else 0) | (abi.LOG_DECISIONS if rc.verbose_decisions else 0)
@@ -887,7 +903,9 @@ def run_sweep(config: SweepConfig, device: int = 0, knn: Optional[GpuKnn] = None
     if own_knn:
         knn = GpuKnn(device)
     task_lists, trace_of, names = [], {}, {}
-    if not base.trace_path and base.mix in ("t90", "t60"):
+    if not base.mix and not base.trace_path:
+        raise abi.CarmaError(abi.CARMA_ERR_INVALID, "ConfigError: run needs either a trace path or a mix+seed")
+    if base.mix in ("t90", "t60"):
         # Traces generated and materialised on the device, straight into the
         # plan; estimates by catalog entry, one table per (estimator, margin).
         try:
@@ -918,10 +936,10 @@ def run_sweep(config: SweepConfig, device: int = 0, knn: Optional[GpuKnn] = None
         return _sweep_result(config, res, names)
     try:
         for seed in config.seeds:
-            if base.trace_path:
-                trace, name = load_trace(base.trace_path), base.trace_path
-            else:
+            if base.mix:
                 trace, name = generate_trace(base.mix, seed), f"{base.mix}-seed{seed}"
+            else:
+                trace, name = load_trace(base.trace_path), base.trace_path
             names[seed] = name
             m = None
             for cell in config.cells:

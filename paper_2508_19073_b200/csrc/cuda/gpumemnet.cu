@@ -1422,6 +1422,7 @@ carma_status carma_nn_set_act_table(carma_nn* hh, const double* act_table) {
     return guarded([&] {
         NnHandle* h = reinterpret_cast<NnHandle*>(hh);
         if (!h || !act_table) throw InvalidArg("null argument");
+        std::lock_guard<std::mutex> lock(h->mu);
         std::memcpy(h->act, act_table, sizeof(h->act));
     });
 }
@@ -1433,6 +1434,7 @@ carma_status carma_nn_set_bit_schema(carma_nn* hh, const carma_bit_schema* schem
         if (schema->words_per_row == 0) throw InvalidArg("schema has no words per row");
         for (int f = 0; f < CARMA_BIT_FIELDS; ++f)
             if (schema->width[f] > 48) throw InvalidArg("schema field wider than 48 bits");
+        std::lock_guard<std::mutex> lock(h->mu);
         h->schema = *schema;
         std::memcpy(h->act, schema->act_table, sizeof(h->act));
     });

@@ -1031,6 +1031,86 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
 }
 
 // ------------------------------------------------------------------------
+// k > kMaxK: exact brute force, one thread per query. The reference's whole
+// predict_scalar (estimators.cpp:438-475) without pruning: every point's d2 in
+// the reference's dim order, the k smallest (d2, training index) pairs kept
+// sorted in a per-thread list in global scratch ([slot][thread], coalesced),
+// the vote over their labels. Used only for models with k > 16 (no register
+// top-k); correctness over speed.
+template <int FMT>
+__global__ void __launch_bounds__(128) knn_brute(KnnParams p, uint64_t q0, uint64_t nq, double* __restrict__ sd2,
+                                                 int32_t* __restrict__ sid, int32_t* __restrict__ bucket_out,
+                                                 uint64_t* __restrict__ bytes_out, double* __restrict__ topk_d2,
+                                                 int64_t* __restrict__ topk_idx) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (t >= nq) return;
+    const uint64_t row = q0 + t;
+    const int f = family_of_t<FMT>(p, row);
+    if (f < 0) {
+        if (bucket_out) bucket_out[row] = -1;
+        if (bytes_out) bytes_out[row] = ~0ull;
+        return;
+    }
+    const ModelDev& m = p.m[f];
+    double raw[kDims], q[kDims];
+    load_raw<FMT>(p, row, raw);
+#pragma unroll
+    for (int d = 0; d < kDims; ++d) q[d] = normalize(raw[d], m.lo[d], m.hi[d]);
+    const uint32_t k = static_cast<uint32_t>(m.k < m.n ? m.k : m.n);
+    uint32_t cnt = 0;
+    for (uint64_t s = 0; s < m.n; ++s) {
+        const double* pt = m.pts + s * kStride;
+        double d2 = 0.0;
+#pragma unroll
+        for (int d = 0; d < kDims; ++d) {
+            double diff = __dsub_rn(__ldg(pt + d), q[d]);
+            if (d == kDims - 1) diff = __dmul_rn(diff, 64.0);
+            d2 = __dadd_rn(d2, __dmul_rn(diff, diff));
+        }
+        const int32_t oi = __ldg(m.orig + s);
+        if (cnt == k) {
+            const double ld = sd2[(k - 1) * nq + t];
+            const int32_t li = sid[(k - 1) * nq + t];
+            if (!(d2 < ld || (d2 == ld && oi < li))) continue;
+        } else {
+            ++cnt;
+        }
+        uint32_t j = cnt - 1;  // shift larger entries up by one
+        while (j > 0) {
+            const double pd = sd2[(j - 1) * nq + t];
+            const int32_t pi = sid[(j - 1) * nq + t];
+            if (!(pd > d2 || (pd == d2 && pi > oi))) break;
+            sd2[j * nq + t] = pd;
+            sid[j * nq + t] = pi;
+            --j;
+        }
+        sd2[j * nq + t] = d2;
+        sid[j * nq + t] = oi;
+    }
+    // votes; ties go to the larger label (estimators.cpp:463-474)
+    int best = 0, best_votes = 0;
+    for (uint32_t a = 0; a < cnt; ++a) {
+        const int la = __ldg(m.label_by_orig + sid[a * nq + t]);
+        int votes = 0;
+        for (uint32_t b = 0; b < cnt; ++b) votes += __ldg(m.label_by_orig + sid[b * nq + t]) == la ? 1 : 0;
+        if (votes > best_votes || (votes == best_votes && la > best)) {
+            best = la;
+            best_votes = votes;
+        }
+    }
+    if (bucket_out) bucket_out[row] = best;
+    if (bytes_out) bytes_out[row] = (static_cast<uint64_t>(best) + 1ull) * m.bucket_range;
+    if (topk_d2 || topk_idx) {
+        const double inf = __longlong_as_double(0x7ff0000000000000ll);
+        for (uint32_t a = 0; a < m.k; ++a) {
+            const uint64_t o = row * m.k + a;
+            if (topk_d2) topk_d2[o] = a < cnt ? sd2[a * nq + t] : inf;
+            if (topk_idx) topk_idx[o] = a < cnt ? sid[a * nq + t] : -1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
 // train_learned_estimator on the device (estimators.cpp:344-436).
 
 // Order-preserving 64-bit key of a double (+0 and -0 collapse) and back.
@@ -1140,7 +1220,7 @@ struct KnnHandle {
     cudaStream_t pipe[2] = {nullptr, nullptr};
     HostModel model[CARMA_FAMILIES];
     struct Scratch {
-        DeviceBuffer rows, family, qbin, qpos, perm, hist, tot, bucket, bytes, qrec;
+        DeviceBuffer rows, family, qbin, qpos, perm, hist, tot, bucket, bytes, qrec, brute_d2, brute_id;
         PinnedBuffer stage_rows, stage_family;
     } scratch[2];
     DeviceBuffer evals;
@@ -1283,6 +1363,38 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
     sc.hist.ensure(static_cast<size_t>(n_bins) * ctas * 4);
     const size_t shmem = n_bins * 4;
     const bool timed = h.timed && h.ev[0];
+    if (max_k(h) > kMaxK) {  // exact brute force, query chunks bounded by the scratch
+        if (timed) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
+        if (timed) CARMA_CUDA(cudaEventRecord(h.ev[1], s));
+        const uint64_t kc = static_cast<uint64_t>(max_k(h));
+        const uint64_t chunk = std::max<uint64_t>(1024, (256ull << 20) / (kc * 12));
+        uint64_t launches = 0;
+        for (uint64_t q0 = 0; q0 < q; q0 += chunk) {
+            const uint64_t nq = std::min(chunk, q - q0);
+            sc.brute_d2.ensure(nq * kc * 8);
+            sc.brute_id.ensure(nq * kc * 4);
+            const unsigned grid = static_cast<unsigned>((nq + 127) / 128);
+            double* bd = sc.brute_d2.as<double>();
+            int32_t* bi = sc.brute_id.as<int32_t>();
+            switch (format) {
+                case CARMA_ROWS_SCALAR:
+                    knn_brute<CARMA_ROWS_SCALAR><<<grid, 128, 0, s>>>(p, q0, nq, bd, bi, bucket, bytes, d2, idx);
+                    break;
+                case CARMA_ROWS_PACKED:
+                    knn_brute<CARMA_ROWS_PACKED><<<grid, 128, 0, s>>>(p, q0, nq, bd, bi, bucket, bytes, d2, idx);
+                    break;
+                case CARMA_ROWS_BITPACKED:
+                    knn_brute<CARMA_ROWS_BITPACKED><<<grid, 128, 0, s>>>(p, q0, nq, bd, bi, bucket, bytes, d2, idx);
+                    break;
+                default:
+                    knn_brute<CARMA_ROWS_FEATURES><<<grid, 128, 0, s>>>(p, q0, nq, bd, bi, bucket, bytes, d2, idx);
+            }
+            CARMA_CUDA(cudaGetLastError());
+            ++launches;
+        }
+        if (timed) CARMA_CUDA(cudaEventRecord(h.ev[2], s));
+        return launches;
+    }
     const bool f32 = use_f32(h);
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
     if (f32) {
@@ -1348,13 +1460,15 @@ void check_ready(const KnnHandle* h) {
 
 carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int32_t format,
                           const int8_t* family, int32_t default_family, uint64_t q,
-                          int32_t* bucket_out, uint64_t* bytes_out, size_t tail_bytes = 0) {
+                          int32_t* bucket_out, uint64_t* bytes_out, size_t tail_bytes = 0,
+                          const double* act_table = nullptr) {
     return guarded([&] {
         KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
         check_ready(h);
         if (q == 0) return;
         if (!rows) throw InvalidArg("rows is null");
         std::lock_guard<std::mutex> lock(h->mu);
+        if (act_table) std::memcpy(h->act, act_table, sizeof(h->act));  // under the lock
         DeviceGuard g(h->device);
         // Chunks grow geometrically from 2^18 rows to the steady size and
         // shrink again over the last rows (at most half of what remains), so
@@ -1470,6 +1584,7 @@ carma_status carma_knn_destroy(carma_knn* hh) {
             for (auto& sc : h->scratch) {
                 sc.rows.release(); sc.family.release(); sc.qbin.release(); sc.qpos.release();
                 sc.perm.release(); sc.hist.release(); sc.tot.release(); sc.bucket.release(); sc.bytes.release();
+                sc.brute_d2.release(); sc.brute_id.release();
                 sc.stage_rows.release(); sc.stage_family.release();
             }
             h->evals.release();
@@ -1494,7 +1609,7 @@ carma_status carma_knn_set_model(carma_knn* hh, int32_t family, const double* lo
         if (n == 0) throw InvalidArg("EmptyDataset: model has no points");
         if (n > 0x7fffffffull) throw InvalidArg("model too large");
         if (k < 1) throw InvalidArg("k must be >= 1");
-        if (k > kMaxK) throw Unsupported("k > 16 is not supported by the GPU kernel");
+        if (k > 65536) throw Unsupported("k > 65536 is not supported by the GPU kernel");
         if (bucket_range == 0) throw InvalidArg("NonPositiveRange: bucket range must be > 0");
         if (!lo || !hi || !points || !labels) throw InvalidArg("null model array");
         std::lock_guard<std::mutex> lock(h->mu);
@@ -1589,16 +1704,15 @@ carma_status carma_knn_set_act_table(carma_knn* hh, const double* act_table) {
     return guarded([&] {
         KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
         if (!h || !act_table) throw InvalidArg("null argument");
+        std::lock_guard<std::mutex> lock(h->mu);
         std::memcpy(h->act, act_table, sizeof(h->act));
     });
 }
 
 carma_status carma_knn_predict_packed(carma_knn* hh, const carma_feature_packed* rows, const double* act_table,
                                       uint64_t q, int32_t* bucket_out, uint64_t* bytes_out) {
-    KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
-    if (h && act_table) std::memcpy(h->act, act_table, sizeof(h->act));
     return predict_host(hh, rows, sizeof(carma_feature_packed), CARMA_ROWS_PACKED, nullptr, 0, q, bucket_out,
-                        bytes_out);
+                        bytes_out, 0, act_table);
 }
 
 carma_status carma_knn_set_bit_schema(carma_knn* hh, const carma_bit_schema* schema) {
@@ -1608,6 +1722,7 @@ carma_status carma_knn_set_bit_schema(carma_knn* hh, const carma_bit_schema* sch
         if (schema->words_per_row == 0) throw InvalidArg("schema has no words per row");
         for (int f = 0; f < CARMA_BIT_FIELDS; ++f)
             if (schema->width[f] > 48) throw InvalidArg("schema field wider than 48 bits");
+        std::lock_guard<std::mutex> lock(h->mu);
         h->schema = *schema;
         std::memcpy(h->act, schema->act_table, sizeof(h->act));
     });

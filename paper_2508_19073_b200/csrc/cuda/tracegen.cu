@@ -9,10 +9,9 @@
 // reference's Rng, rng.hpp:13-53: seeding, twist and tempering of the
 // standard), uniform(n) is the 128-bit multiply-shift, next_double the top
 // 53 bits, the exponential gap -mean * log1p(-u), the millisecond grid
-// round(t * 1000) / 1000 (no FMA contraction: --fmad=false). log1p is CUDA's
-// (<= 1 ulp, like glibc's); a 1-ulp difference in a gap moves a submit time
-// only if it straddles a half-millisecond, which the GPU tests rule out on
-// every row of seeds 1..100,000 (t90) and 1..20,000 (t60).
+// round(t * 1000) / 1000 (no FMA contraction: --fmad=false). log1p is
+// glibc's own algorithm and operation order (glibc_log1p.cuh), so every seed
+// gives the host generator's bits by construction, not by sampling.
 
 #include <cmath>
 #include <cstring>
@@ -23,6 +22,7 @@
 #include "../../../include/carma_host.h"
 #include "../host/model.hpp"
 #include "common.cuh"
+#include "glibc_log1p.cuh"
 #include "tracegen.cuh"
 
 namespace carma_b200 {
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(128) gen_traces(int32_t mix, const uint64_t* _
     double clock = 0.0;
     for (int k = 0; k < T; ++k) {
         const GenEntry& e = c_cat.e[picks[k]];
-        if (k > 0) clock = __dadd_rn(clock, __dmul_rn(-120.0, log1p(-rng.next_double())));
+        if (k > 0) clock = __dadd_rn(clock, __dmul_rn(-120.0, glibc_log1p(-rng.next_double())));
         carma_task t;
         t.submit = __ddiv_rn(round(__dmul_rn(clock, 1000.0)), 1000.0);
         const uint64_t epochs = e.n_opts == 1 ? e.opts[0] : e.opts[rng.uniform(e.n_opts)];
@@ -181,3 +181,35 @@ void launch_generate_traces(int32_t mix, const uint64_t* d_seeds, uint32_t n_see
 }
 
 }  // namespace carma_b200
+
+// Pins glibc_log1p (the code the device runs, built for the host) to the C
+// library's log1p: n inputs from a xorshift stream over the ranges the trace
+// generator and the branch boundaries exercise. Returns the mismatch count.
+extern "C" carma_status carma_host_check_log1p(uint64_t n, uint64_t seed, uint64_t* mismatches) {
+    return carma_b200::guarded([&] {
+        if (!mismatches) throw carma_b200::InvalidArg("null argument");
+        uint64_t s = seed ? seed : 88172645463325252ull, bad = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            s ^= s << 13;
+            s ^= s >> 7;
+            s ^= s << 17;
+            const double u = static_cast<double>(s >> 11) * 0x1.0p-53;
+            double x = -u;  // the generator's domain: log1p(-u), u in [0, 1)
+            switch (i % 6) {
+                case 1: x = -static_cast<double>(s >> 40) * 0x1.0p-24; break;
+                case 2: x = -u * 1e-6; break;
+                case 3: x = u * 0.5 - 0.25; break;
+                case 4: {  // hi words around the k = 0 boundary 0xbfd2bec3
+                    const uint64_t b = (static_cast<uint64_t>(0xbfd2bec2u + (s & 3)) << 32) | (s >> 32);
+                    std::memcpy(&x, &b, 8);
+                    break;
+                }
+                case 5: x = (u - 0.5) * 0x1.0p-27; break;  // the |x| < 2^-29 branch
+                default: break;
+            }
+            const double a = std::log1p(x), b = carma_b200::glibc_log1p(x);
+            if (std::memcmp(&a, &b, 8) != 0) ++bad;
+        }
+        *mismatches = bad;
+    });
+}

@@ -30,7 +30,8 @@ RUNS = [
     dict(policy="lug", max_smact=0.5, window=30.0, gpu_count=8, seed=5),
     dict(policy="magm", mode="mig", mig=(0.75, 0.125, 0.125), seed=6),
     dict(policy="mug", mode="mig", mig=(0.8, 0.2), seed=7, estimator="oracle"),
-    dict(policy="magm", capacity=40 * GiB, block=256 * MiB, gpu_count=2, seed=8, estimator="learned"),
+    dict(policy="magm", capacity=80 * GiB, block=256 * MiB, gpu_count=2, seed=8, estimator="learned"),
+    dict(policy="lug", capacity=192 * GiB, gpu_count=8, seed=9, estimator="oracle"),
 ]
 
 
@@ -61,15 +62,16 @@ def test_gpu_run_sweep_t60_mig_equals_reference(bridge):
     assert ref.startswith("OK:") and got == ref
 
 
+@pytest.mark.parametrize("k", [5, 31])
 @pytest.mark.parametrize("how", [0, 1, 2], ids=["add", "train", "load"])
 @pytest.mark.parametrize("family", [0, 1, 2])
-def test_estimator_bank_equals_estimate_learned(bridge, family, how):
+def test_estimator_bank_equals_estimate_learned(bridge, family, how, k):
     import ctypes
     n = 3000
     rb, gb = np.zeros(n, np.int32), np.full(n, -9, np.int32)
     rby, gby = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
     err = ctypes.create_string_buffer(512)
-    rc = bridge.bridge_estimate_pair(family, n, 777 + family, 4000, 11 + 101 * family, 5, how, 0, rb.ctypes.data,
+    rc = bridge.bridge_estimate_pair(family, n, 777 + family, 4000, 11 + 101 * family, k, how, 0, rb.ctypes.data,
                                      rby.ctypes.data, gb.ctypes.data, gby.ctypes.data, err, 512)
     assert rc == 0, err.value.decode()
     assert np.array_equal(rb, gb) and np.array_equal(rby, gby)

@@ -83,8 +83,10 @@ def test_bank_routes_by_family_and_flags_mismatch(gpu, olib, models):
 
 
 @pytest.mark.parametrize("path", [1, 2], ids=["exact-fp64", "fp32-prefilter"])
-@pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 16, 17, 40, 101])
 def test_knn_k_variants_and_vote_ties(gpu, olib, k, path):
+    """k <= 16: the register top-k search kernels; k > 16: the exact brute-force
+    kernel (any k, estimators.cpp:460 kk = min(k, n))."""
     m = cb.fit_knn(1, 1500, 77, k)
     knn = cb.GpuKnn(gpu)
     knn.set_model(m)
@@ -108,7 +110,7 @@ def test_knn_degenerate_models_ties_and_outliers(gpu, olib):
     hi = np.ones(19)
     hi[5] = 0.0  # a constant feature (hi == lo -> normalised to 0)
     labels = np.array([4, 4, 1, 2, 2, 3, 0], np.int32)
-    for k in (3, 5, 9, 16):
+    for k in (3, 5, 9, 16, 25):
         m = cb.KnnModel(1, k, 8 * abi.GiB, lo, hi, pts.copy(), labels, np.zeros(0, np.int64))
         knn = cb.GpuKnn(gpu)
         knn.set_model(m)

@@ -14,11 +14,11 @@ pytestmark = pytest.mark.gpu
 
 
 def cfg_of(policy="magm", mode="mps", gpu_count=4, max_smact=0.8, min_free=None, window=60.0, rr_pre=False,
-           capacity=40 * abi.GiB):
+           capacity=40 * abi.GiB, block=512 * abi.MiB, mig=None):
     return cb.make_config(cb.PolicyConfig(policy=policy, collocation_mode=mode, max_smact=max_smact,
                                           min_free_mem=min_free, monitor_window=window,
                                           rr_apply_preconditions=rr_pre),
-                          cb.SimConstants(gpu_count=gpu_count, gpu_capacity=capacity))
+                          cb.SimConstants(gpu_count=gpu_count, gpu_capacity=capacity, alloc_block=block), mig)
 
 
 def learned_estimates(olib, m, models):
@@ -330,3 +330,24 @@ def test_pick_batch_device_matches_host_path(gpu, olib):
             torch.cuda.synchronize()
             assert np.array_equal(do.cpu().numpy().reshape(n, 2), out), (g, policy)
             assert np.array_equal(dc.cpu().numpy(), cur), (g, policy)
+
+
+@pytest.mark.parametrize("capacity,block", [(192 * abi.GiB, 512 * abi.MiB), (40 * abi.GiB, 16 * abi.MiB),
+                                            (192 * abi.GiB, 48 * abi.MiB)])
+def test_replay_more_than_256_blocks(gpu, olib, models, capacity, block):
+    """Devices with 384 / 2560 / 4096 allocation blocks (a 192 GiB B200-class
+    GPU at 512 MiB blocks, fine 16 MiB blocks): the wide global tier's 64-word
+    bitmaps, every policy, MPS / streams / MIG, against the oracle."""
+    task_lists = []
+    for mix, seed in (("t90", 1), ("t90", 2), ("t60", 3)):
+        m = cb.materialize_trace(cb.generate_trace(mix, seed))
+        m.tasks["estimate"] = learned_estimates(olib, m, models)
+        task_lists.append(m.tasks)
+    cfgs = np.concatenate([cfg_of(p, gpu_count=g, capacity=capacity, block=block)
+                           for p in ("exclusive", "rr", "magm", "lug", "mug") for g in (4, 8)] +
+                          [cfg_of("magm", mode="streams", max_smact=1.0, capacity=capacity, block=block)] +
+                          ([cfg_of("lug", mode="mig", mig=[0.75, 0.25], capacity=capacity, block=block)]
+                           if capacity > 64 * abi.GiB else []))
+    jobs = [(t, c) for c in range(len(cfgs)) for t in range(len(task_lists))]
+    res = cb.replay(cfgs, task_lists, jobs)
+    check_jobs(olib, res, cfgs, task_lists, jobs)

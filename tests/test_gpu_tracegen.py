@@ -25,9 +25,13 @@ def one_config():
     return cb.make_config(cb.PolicyConfig(policy="magm", max_smact=0.8), cb.SimConstants())
 
 
-@pytest.mark.parametrize("mix,n", [("t90", 100_000), ("t60", 20_000)])
-def test_generated_tasks_equal_host_generator(gpu, mix, n):
-    seeds = np.arange(1, n + 1, dtype=np.uint64)
+@pytest.mark.parametrize("mix,n,first", [("t90", 100_000, 1), ("t60", 20_000, 1),
+                                         ("t90", 50_000, 0), ("t60", 50_000, 0)])
+def test_generated_tasks_equal_host_generator(gpu, mix, n, first):
+    """first = 0: random 64-bit seeds (the device log1p is glibc's algorithm,
+    so no seed range is special)."""
+    seeds = np.arange(first, first + n, dtype=np.uint64) if first else \
+        np.random.default_rng(2026).integers(1, 2**63, n, dtype=np.uint64)
     jobs = np.zeros(n, abi.job_dtype)
     jobs["trace"] = np.arange(n, dtype=np.uint32)
     plan = cb.ReplayPlan.generated(one_config(), mix, seeds, jobs, device=gpu)

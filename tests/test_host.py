@@ -209,3 +209,13 @@ def test_reference_bridge_loads_and_fails_loudly_without_gpu():
     ref, got = run_pair(lib, case(policy="magm", estimator="oracle"))
     assert ref.startswith("OK:{") and '"trace_name": "t90-seed1"' in ref or ref.startswith("OK:")
     assert got.startswith("ERR:") and "no CPU fallback" in got
+
+
+def test_device_log1p_is_glibc_bit_for_bit():
+    """The trace generator's log1p (glibc_log1p.cuh, the code the device runs)
+    equals the C library's on 6M inputs: the generator's domain (-u, u in
+    [0, 1)), tiny arguments, both sides of every branch boundary."""
+    import ctypes
+    bad = ctypes.c_uint64()
+    abi.check(abi.lib.carma_host_check_log1p(6_000_000, 12345, ctypes.byref(bad)))
+    assert bad.value == 0

@@ -9,7 +9,7 @@ import pytest
 import paper_2508_19073_b200 as cb
 from paper_2508_19073_b200 import abi
 from cases import model
-from oracle_bind import oracle_predict, oracle_replay, ref_config, ref_run, replay_config_from
+from oracle_bind import GiB, MiB, oracle_predict, oracle_replay, ref_config, ref_run, replay_config_from
 
 
 @pytest.mark.parametrize("family,seed", [(0, 11), (1, 112), (2, 213), (1, 7)])
@@ -88,6 +88,10 @@ GRID = [dict(policy=p) for p in ("exclusive", "rr", "magm", "lug", "mug")] + [
     dict(policy="mug", mode="mig", mig=(1.0,), gpu_count=8),
     dict(policy="magm", mode="mig", mig=(0.75, 0.125, 0.125), estimator="analytical"),
     dict(policy="rr", mode="mig", mig=(0.8, 0.2), rr_pre=True, estimator="oracle", gpu_count=2),
+    # more than 256 allocation blocks per GPU (the wide global tier)
+    dict(policy="magm", capacity=192 * GiB, block=512 * MiB, gpu_count=8),
+    dict(policy="rr", capacity=40 * GiB, block=16 * MiB),
+    dict(policy="lug", capacity=192 * GiB, block=64 * MiB, mode="mig", mig=(0.75, 0.25), estimator="oracle"),
 ]
 
 
