@@ -278,6 +278,11 @@ carma_status carma_nn_destroy(carma_nn* h);
 carma_status carma_nn_set_model(carma_nn* h, int32_t family, const carma_nn_spec* spec,
                                 const float* params, uint64_t n_params);
 carma_status carma_nn_set_act_table(carma_nn* h, const double* act_table);
+/* MLP ensembles: 0 = auto (the CUDA-core kernel, mlp_ffma: fp32 FFMA, thread
+ * per row), 1 = the tcgen05 kernel (nn_ensemble: block-diagonal bf16 GEMMs),
+ * 2 = CUDA cores. Results agree within the 1e-3 logit bar; both are tested.
+ * Transformer ensembles always run on the CUDA cores. */
+carma_status carma_nn_set_path(carma_nn* h, int32_t path);
 carma_status carma_nn_set_bit_schema(carma_nn* h, const carma_bit_schema* schema);
 /* Device-resident predict (formats as carma_knn_predict_device). probs
  * (nullable, q x CARMA_NN_MAX_CLASSES fp32) receives the ensemble's mean

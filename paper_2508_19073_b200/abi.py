@@ -174,6 +174,7 @@ SIGNATURES = {
     "carma_nn_destroy": (c_int, [c_void_p]),
     "carma_nn_set_model": (c_int, [c_void_p, c_int32, P, P, c_uint64]),
     "carma_nn_set_act_table": (c_int, [c_void_p, P]),
+    "carma_nn_set_path": (c_int, [c_void_p, c_int32]),
     "carma_nn_set_bit_schema": (c_int, [c_void_p, P]),
     "carma_nn_predict_device": (c_int, [c_void_p, P, c_int32, P, c_int32, c_uint64, P, P, P, P, c_void_p]),
     "carma_nn_predict": (c_int, [c_void_p, P, P, c_int32, c_uint64, P, P]),

@@ -91,6 +91,10 @@ struct NnModelDev {
     uint32_t tf_off[CARMA_NN_MAX_MEMBERS];   // transformer: float offset of member e's parameters
     uint8_t tf_d[CARMA_NN_MAX_MEMBERS];      // transformer: model width d
     uint8_t tf_layers[CARMA_NN_MAX_MEMBERS]; // transformer: encoder layers
+    const float* fblob;   // MLP, CUDA-core path: fp32 padded image (see mlp_ffma)
+    uint32_t fblob_bytes;
+    uint32_t ff_off[CARMA_NN_MAX_MEMBERS];   // float offset of member e (spec order) in fblob
+    uint8_t ff_depth[CARMA_NN_MAX_MEMBERS];  // hidden layers of member e
     uint32_t off_head;    // byte offset of the head weights in the blob
     uint32_t off_bias;    // byte offset of the fp32 biases (L x 64, then head rows)
     uint32_t log_mask;
@@ -778,6 +782,212 @@ __global__ void __launch_bounds__(128, 2) tf_ensemble(const __grid_constant__ Nn
     }
 }
 
+// ------------------------------------------------ MLP ensemble, CUDA cores
+//
+// The same ensemble as nn_ensemble on the FMA pipes, thread per row (R rows
+// per thread share every weight load). Each member's layers are tiny (<= 8
+// neurons, K <= 19): as GEMMs they fill an M = 128 tensor-core tile only
+// through block-diagonal padding and three bf16 activation parts (26.7x
+// the useful flops, bench "neural" roofline), while here every useful FMA
+// is one FFMA and the weights are warp-uniform broadcasts from shared memory
+// (LDS.128: 4 weights per load, reused by the R rows). Arithmetic is fp32
+// throughout (the bf16-valued weights of the model, fp32 activations), so
+// logits are at least as close to the oracle as the tensor path's.
+//
+// fblob, per member (spec order), floats: W0 [8][20] (19 features + pad,
+// rows past the layer width zero) and b0 [8]; layers l = 1..depth-1: W [8][8],
+// b [8]; head W [C][8], b [C]. Zero rows give relu(0) = 0 activations,
+// which zero columns of the next layer ignore.
+constexpr int kFfIn = 20;
+#ifndef NN_FFMA_ROWS
+#define NN_FFMA_ROWS 2
+#endif
+
+template <int FMT, int R, int CP, bool DIAG>
+__global__ void __launch_bounds__(128) mlp_ffma(const __grid_constant__ NnParams p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const NnModelDev& m = p.m;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(m.fblob);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (uint32_t i = threadIdx.x; i < m.fblob_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const float* wts = reinterpret_cast<const float*>(smem);
+    // CP > 8: logits spill to shared memory, [class][thread][r]
+    float* lgs = reinterpret_cast<float*>(smem + m.fblob_bytes) + threadIdx.x * R;
+    const int ls = blockDim.x * R;
+    uint64_t n = p.n, base = 0;
+    if (p.counts) {
+        n = p.counts[p.fam];
+        for (int f = 0; f < p.fam; ++f) base += p.counts[f];
+    }
+    const bool grouped = !p.perm || p.counts[2 * (CARMA_FAMILIES + 1)] == 0;
+    const int C = static_cast<int>(m.classes);
+    const uint64_t n_items = (n + R - 1) / R;
+    for (uint64_t it = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; it < n_items;
+         it += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint64_t row[R];
+        bool live[R];
+        float z[R][kFeatureDims];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint64_t i = it * R + r;
+            live[r] = i < n;
+            const uint64_t ii = live[r] ? i : it * R;
+            row[r] = grouped ? base + ii : static_cast<uint64_t>(p.perm[base + ii]);
+            double raw[kFeatureDims];
+            load_raw<FMT>(p, row[r], raw);
+#pragma unroll
+            for (int d = 0; d < kFeatureDims; ++d) {
+                const float x = __double2float_rn(raw[d]);
+                const float t = ((m.log_mask >> d) & 1u) ? log1pf(fmaxf(x, 0.f)) : x;
+                z[r][d] = __fmul_rn(__fsub_rn(t, m.shift[d]), m.scale[d]);
+            }
+        }
+        float pm[R][CP];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < CP; ++c) pm[r][c] = 0.f;
+#pragma unroll 1
+        for (uint32_t mem = 0; mem < m.members; ++mem) {
+            const float* w = wts + m.ff_off[mem];
+            float h[R][8];
+#pragma unroll
+            for (int o = 0; o < 8; ++o) {
+                const float* wr = w + o * kFfIn;
+                float a[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) a[r] = w[8 * kFfIn + o];
+#pragma unroll
+                for (int k4 = 0; k4 < kFfIn / 4; ++k4) {
+                    const float4 v = *reinterpret_cast<const float4*>(wr + 4 * k4);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        a[r] = __fmaf_rn(v.x, z[r][4 * k4], a[r]);
+                        a[r] = __fmaf_rn(v.y, z[r][4 * k4 + 1], a[r]);
+                        a[r] = __fmaf_rn(v.z, z[r][4 * k4 + 2], a[r]);
+                        if (4 * k4 + 3 < kFeatureDims) a[r] = __fmaf_rn(v.w, z[r][4 * k4 + 3], a[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) h[r][o] = fmaxf(a[r], 0.f);
+            }
+            w += 8 * kFfIn + 8;
+            const int depth = m.ff_depth[mem];
+#pragma unroll 1
+            for (int l = 1; l < depth; ++l) {
+                float g[R][8];
+#pragma unroll
+                for (int o = 0; o < 8; ++o) {
+                    const float4 v0 = *reinterpret_cast<const float4*>(w + o * 8);
+                    const float4 v1 = *reinterpret_cast<const float4*>(w + o * 8 + 4);
+                    const float bo = w[64 + o];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        float a = __fmaf_rn(v0.x, h[r][0], bo);
+                        a = __fmaf_rn(v0.y, h[r][1], a);
+                        a = __fmaf_rn(v0.z, h[r][2], a);
+                        a = __fmaf_rn(v0.w, h[r][3], a);
+                        a = __fmaf_rn(v1.x, h[r][4], a);
+                        a = __fmaf_rn(v1.y, h[r][5], a);
+                        a = __fmaf_rn(v1.z, h[r][6], a);
+                        a = __fmaf_rn(v1.w, h[r][7], a);
+                        g[r][o] = fmaxf(a, 0.f);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int o = 0; o < 8; ++o) h[r][o] = g[r][o];
+                w += 72;
+            }
+            // head logits, softmax, running mean of the probabilities
+            float lg[R][CP <= 8 ? CP : 1];
+            float mx[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) mx[r] = -INFINITY;
+            const float* hb = w + 8 * C;
+#pragma unroll(CP <= 8 ? CP : 1)
+            for (int c = 0; c < (CP <= 8 ? CP : C); ++c) {
+                if (CP <= 8 && c >= C) break;
+                const float4 v0 = *reinterpret_cast<const float4*>(w + c * 8);
+                const float4 v1 = *reinterpret_cast<const float4*>(w + c * 8 + 4);
+                const float bc = hb[c];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float a = __fmaf_rn(v0.x, h[r][0], bc);
+                    a = __fmaf_rn(v0.y, h[r][1], a);
+                    a = __fmaf_rn(v0.z, h[r][2], a);
+                    a = __fmaf_rn(v0.w, h[r][3], a);
+                    a = __fmaf_rn(v1.x, h[r][4], a);
+                    a = __fmaf_rn(v1.y, h[r][5], a);
+                    a = __fmaf_rn(v1.z, h[r][6], a);
+                    a = __fmaf_rn(v1.w, h[r][7], a);
+                    if constexpr (CP <= 8) lg[r][CP <= 8 ? c : 0] = a;
+                    else lgs[c * ls + r] = a;
+                    mx[r] = fmaxf(mx[r], a);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (DIAG && p.logits && live[r]) {
+                    float* out = p.logits + (row[r] * CARMA_NN_MAX_MEMBERS + mem) * CARMA_NN_MAX_CLASSES;
+                    for (int c = 0; c < C; ++c) out[c] = CP <= 8 ? lg[r][CP <= 8 ? (c < CP ? c : 0) : 0] : lgs[c * ls + r];
+                }
+                float sum = 0.f;
+                if constexpr (CP <= 8) {
+#pragma unroll
+                    for (int c = 0; c < CP; ++c)
+                        if (c < C) {
+                            lg[r][c] = __expf(lg[r][c] - mx[r]);
+                            sum += lg[r][c];
+                        }
+                    const float inv = __frcp_rn(sum);
+#pragma unroll
+                    for (int c = 0; c < CP; ++c)
+                        if (c < C) pm[r][c] = __fmaf_rn(lg[r][c], inv, pm[r][c]);
+                } else {
+                    for (int c = 0; c < C; ++c) {
+                        const float ex = __expf(lgs[c * ls + r] - mx[r]);
+                        lgs[c * ls + r] = ex;
+                        sum += ex;
+                    }
+                    const float inv = __frcp_rn(sum);
+#pragma unroll
+                    for (int c = 0; c < CP; ++c)
+                        if (c < C) pm[r][c] = __fmaf_rn(lgs[c * ls + r], inv, pm[r][c]);
+                }
+            }
+        }
+        const float inv_e = 1.0f / static_cast<float>(m.members);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (!live[r]) continue;
+            int best = 0;
+            float bv = -1.f;
+#pragma unroll
+            for (int c = 0; c < CP; ++c)
+                if (c < C) {
+                    pm[r][c] *= inv_e;
+                    if (pm[r][c] >= bv) {  // ties to the larger bin
+                        bv = pm[r][c];
+                        best = c;
+                    }
+                }
+            p.bucket[row[r]] = best;
+            p.bytes[row[r]] = static_cast<uint64_t>(best + 1) * m.bucket_range;
+            if (DIAG && p.probs) {
+                float* out = p.probs + row[r] * CARMA_NN_MAX_CLASSES;
+#pragma unroll
+                for (int c = 0; c < CP; ++c)
+                    if (c < C) out[c] = pm[r][c];
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------ family partition
 
 constexpr int kBins = CARMA_FAMILIES + 1;  // + rows without a model
@@ -874,6 +1084,7 @@ struct HostNn {
     carma_nn_spec spec{};
     NnModelDev dev{};
     DeviceBuffer blob;
+    DeviceBuffer fblob;  // MLP: fp32 image of the CUDA-core path (mlp_ffma)
 };
 
 uint16_t bf16_bits(float x) {  // round to nearest even (finite inputs)
@@ -1065,10 +1276,47 @@ void build_model(HostNn& hm, int device, const carma_nn_spec& s, const float* pa
         pp += static_cast<size_t>(s.classes) * in;
         for (uint32_t c = 0; c < s.classes; ++c) bias[L * kHidden + row0 + c] = pp[c];
     }
+    // the CUDA-core path's image (mlp_ffma): per member in spec order, the
+    // same bf16-valued weights as fp32, padded to 8 neurons
+    std::vector<float> fb;
+    for (uint32_t e = 0; e < E; ++e) {
+        d.ff_off[e] = static_cast<uint32_t>(fb.size());
+        d.ff_depth[e] = static_cast<uint8_t>(s.depth[e]);
+        const float* pp = mp[e];
+        uint32_t in = kFeatureDims;
+        auto bfv = [](float x) {
+            const uint32_t u = static_cast<uint32_t>(bf16_bits(x)) << 16;
+            float f;
+            std::memcpy(&f, &u, 4);
+            return f;
+        };
+        for (uint32_t l = 0; l < s.depth[e]; ++l) {
+            const uint32_t w = s.width[e][l], cols = l == 0 ? kFfIn : 8;
+            const size_t o0 = fb.size();
+            fb.resize(o0 + 8 * cols + 8, 0.f);
+            for (uint32_t o = 0; o < w; ++o)
+                for (uint32_t k = 0; k < in; ++k) fb[o0 + o * cols + k] = bfv(pp[o * in + k]);
+            pp += static_cast<size_t>(w) * in;
+            for (uint32_t o = 0; o < w; ++o) fb[o0 + 8 * cols + o] = pp[o];
+            pp += w;
+            in = w;
+        }
+        const size_t h0 = fb.size();
+        fb.resize(h0 + 9ull * s.classes, 0.f);
+        for (uint32_t c = 0; c < s.classes; ++c)
+            for (uint32_t k = 0; k < in; ++k) fb[h0 + c * 8 + k] = bfv(pp[c * in + k]);
+        pp += static_cast<size_t>(s.classes) * in;
+        for (uint32_t c = 0; c < s.classes; ++c) fb[h0 + 8ull * s.classes + c] = pp[c];
+        fb.resize((fb.size() + 3) & ~size_t{3}, 0.f);  // members 16-B aligned
+    }
+    d.fblob_bytes = static_cast<uint32_t>(fb.size() * 4);
     DeviceGuard gd(device);
     hm.blob.ensure(blob.size());
     CARMA_CUDA(cudaMemcpy(hm.blob.ptr, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+    hm.fblob.ensure(fb.size() * 4);
+    CARMA_CUDA(cudaMemcpy(hm.fblob.ptr, fb.data(), fb.size() * 4, cudaMemcpyHostToDevice));
     d.blob = hm.blob.as<uint8_t>();
+    d.fblob = hm.fblob.as<float>();
     hm.dev = d;
     hm.spec = s;
     hm.present = true;
@@ -1094,6 +1342,7 @@ struct NnHandle {
     PinnedBuffer counts_host;          // family counts of the last device call
     cudaStream_t counts_stream = nullptr;
     bool counts_pending = false;
+    int32_t path = 0;  // MLP ensembles: 0 auto (CUDA cores), 1 tcgen05, 2 CUDA cores
     std::mutex mu;
 };
 
@@ -1149,8 +1398,30 @@ void launch_tf_t(const NnParams& p, int device, cudaStream_t s) {
     CARMA_CUDA(cudaGetLastError());
 }
 
+template <int FMT, int R, int CP, bool DIAG>
+void launch_ffma_t(const NnParams& p, int device, cudaStream_t s) {
+    const size_t smem = p.m.fblob_bytes + (CP > 8 ? 128u * R * CP * 4u : 0u);
+    if (smem > kSmemLimit) throw Unsupported("model too large for shared memory");
+    static cudaError_t attr = cudaFuncSetAttribute(mlp_ffma<FMT, R, CP, DIAG>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(kSmemLimit));
+    CARMA_CUDA(attr);
+    int per_sm = 1;
+    CARMA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mlp_ffma<FMT, R, CP, DIAG>, 128, smem));
+    const uint64_t cap = static_cast<uint64_t>(std::max(per_sm, 1)) * sm_count(device);
+    const uint64_t want = p.counts ? cap : (p.n + 128ull * R - 1) / (128ull * R);
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min(want, cap)));
+    mlp_ffma<FMT, R, CP, DIAG><<<grid, 128, smem, s>>>(p);
+    CARMA_CUDA(cudaGetLastError());
+}
+
 template <int FMT, bool DIAG>
-void launch_ensemble(const NnParams& p, int device, cudaStream_t s) {
+void launch_ensemble(const NnParams& p, int device, cudaStream_t s, int32_t path) {
+    if (p.m.arch == CARMA_NN_ARCH_MLP && path != 1) {
+        if (p.m.cp <= 8) launch_ffma_t<FMT, NN_FFMA_ROWS, 8, DIAG>(p, device, s);
+        else launch_ffma_t<FMT, 1, 48, DIAG>(p, device, s);
+        return;
+    }
     if (p.m.arch == CARMA_NN_ARCH_TRANSFORMER) {
         if (p.m.cp <= 8) launch_tf_t<FMT, 8, DIAG>(p, device, s);
         else launch_tf_t<FMT, 48, DIAG>(p, device, s);
@@ -1177,9 +1448,9 @@ void launch_ensemble(const NnParams& p, int device, cudaStream_t s) {
 }
 
 template <int FMT>
-void dispatch_diag(bool diag, const NnParams& p, int device, cudaStream_t s) {
-    if (diag) launch_ensemble<FMT, true>(p, device, s);
-    else launch_ensemble<FMT, false>(p, device, s);
+void dispatch_diag(bool diag, const NnParams& p, int device, cudaStream_t s, int32_t path) {
+    if (diag) launch_ensemble<FMT, true>(p, device, s, path);
+    else launch_ensemble<FMT, false>(p, device, s, path);
 }
 
 template <int FMT>
@@ -1254,10 +1525,10 @@ uint64_t run_predict(NnHandle& h, NnHandle::Scratch& sc, const void* rows, int32
         p.fam = f;
         p.m = h.model[f].dev;
         switch (format) {
-            case CARMA_ROWS_PACKED: dispatch_diag<CARMA_ROWS_PACKED>(diag, p, h.device, s); break;
-            case CARMA_ROWS_BITPACKED: dispatch_diag<CARMA_ROWS_BITPACKED>(diag, p, h.device, s); break;
-            case CARMA_ROWS_SCALAR: dispatch_diag<CARMA_ROWS_SCALAR>(diag, p, h.device, s); break;
-            default: dispatch_diag<CARMA_ROWS_FEATURES>(diag, p, h.device, s);
+            case CARMA_ROWS_PACKED: dispatch_diag<CARMA_ROWS_PACKED>(diag, p, h.device, s, h.path); break;
+            case CARMA_ROWS_BITPACKED: dispatch_diag<CARMA_ROWS_BITPACKED>(diag, p, h.device, s, h.path); break;
+            case CARMA_ROWS_SCALAR: dispatch_diag<CARMA_ROWS_SCALAR>(diag, p, h.device, s, h.path); break;
+            default: dispatch_diag<CARMA_ROWS_FEATURES>(diag, p, h.device, s, h.path);
         }
         ++launches;
     }
@@ -1267,7 +1538,8 @@ uint64_t run_predict(NnHandle& h, NnHandle::Scratch& sc, const void* rows, int32
 
 // MMAs per 128-row tile of a model: the K steps of every layer and of the
 // head passes (K = 64: 4 steps each), kSplit MMAs per step.
-uint64_t mmas_per_tile(const NnModelDev& d) {
+uint64_t mmas_per_tile(const NnModelDev& d, int32_t path) {
+    if (d.arch == CARMA_NN_ARCH_MLP && path != 1) return 0;  // CUDA-core path
     if (d.arch == CARMA_NN_ARCH_TRANSFORMER) return 0;
     uint64_t steps = 4ull * d.passes;
     for (uint32_t l = 0; l < d.depth; ++l) steps += d.layer_k[l];
@@ -1383,7 +1655,10 @@ carma_status carma_nn_destroy(carma_nn* hh) {
         {
             DeviceGuard g(h->device);
             cudaDeviceSynchronize();
-            for (auto& m : h->model) m.blob.release();
+            for (auto& m : h->model) {
+                m.blob.release();
+                m.fblob.release();
+            }
             h->counts_host.release();
             h->fence.destroy();
             for (auto& sc : h->scratch) {
@@ -1424,6 +1699,16 @@ carma_status carma_nn_set_act_table(carma_nn* hh, const double* act_table) {
         if (!h || !act_table) throw InvalidArg("null argument");
         std::lock_guard<std::mutex> lock(h->mu);
         std::memcpy(h->act, act_table, sizeof(h->act));
+    });
+}
+
+carma_status carma_nn_set_path(carma_nn* hh, int32_t path) {
+    return guarded([&] {
+        NnHandle* h = reinterpret_cast<NnHandle*>(hh);
+        if (!h) throw InvalidArg("null handle");
+        if (path < 0 || path > 2) throw InvalidArg("path must be 0 (auto), 1 (tcgen05) or 2 (CUDA cores)");
+        std::lock_guard<std::mutex> lock(h->mu);
+        h->path = path;
     });
 }
 
@@ -1470,7 +1755,7 @@ carma_status carma_nn_predict_device(carma_nn* hh, const void* rows, int32_t for
             h->counts_stream = s;
             h->counts_pending = true;
         } else if (default_family >= 0 && default_family < CARMA_FAMILIES && h->model[default_family].present) {
-            h->last_mmas = (q + 127) / 128 * mmas_per_tile(h->model[default_family].dev);
+            h->last_mmas = (q + 127) / 128 * mmas_per_tile(h->model[default_family].dev, h->path);
         }
     });
 }
@@ -1508,7 +1793,7 @@ carma_status carma_nn_last_timing(carma_nn* hh, double* kernel_ms, double* call_
             const uint32_t* c = h->counts_host.as<uint32_t>();
             uint64_t n = 0;
             for (int f = 0; f < CARMA_FAMILIES; ++f)
-                if (h->model[f].present) n += (c[f] + 127ull) / 128ull * mmas_per_tile(h->model[f].dev);
+                if (h->model[f].present) n += (c[f] + 127ull) / 128ull * mmas_per_tile(h->model[f].dev, h->path);
             h->last_mmas = n;
             h->counts_pending = false;
         }

@@ -147,6 +147,10 @@ class GpuMemNet:
         check(lib.carma_nn_predict_device(self._h, ptr(rows), fmt, ptr(family), default_family, q, ptr(bucket),
                                           ptr(nbytes), ptr(probs), ptr(logits), abi.stream_arg(stream, self.device)))
 
+    def set_path(self, path: int) -> None:
+        """MLP ensembles: 0 auto (CUDA cores), 1 tcgen05 tensor cores, 2 CUDA cores."""
+        check(lib.carma_nn_set_path(self._h, path))
+
     def set_act_table(self, table: np.ndarray) -> None:
         check(lib.carma_nn_set_act_table(self._h, ptr(np.ascontiguousarray(table, np.float64))))
 

@@ -83,6 +83,7 @@ def nn(args):
     models = gm.load_default_models(gm.ARCH_TRANSFORMER if args.arch == "transformer" else gm.ARCH_MLP)
     for f in (1, 2):
         net.set_model(models[f])
+    net.set_path(args.path)
     words, schema = cb.pack_features_bits(rows, fam)
     net.set_bit_schema(schema)
     d_rows = torch.from_numpy(words.view(np.uint8)).cuda()
@@ -145,5 +146,6 @@ if __name__ == "__main__":
     ap.add_argument("--format", choices=("rows", "bitpacked"), default="bitpacked")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--arch", choices=("mlp", "transformer"), default="mlp")
+    ap.add_argument("--path", type=int, default=0, help="neural MLP: 0 auto, 1 tcgen05, 2 CUDA cores")
     a = ap.parse_args()
     {"replay": replay, "knn": knn, "fused": fused, "scoring": scoring, "nn": nn}[a.what](a)

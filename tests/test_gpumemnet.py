@@ -117,18 +117,20 @@ def _check(m, raw, b, by, pr, lg):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("fam", [0, 1, 2])
-def test_kernel_matches_oracle(gpu, models, fam):
+@pytest.mark.parametrize("path", [1, 2], ids=["tcgen05", "cuda-cores"])
+def test_kernel_matches_oracle(gpu, models, fam, path):
     m = models[fam]
     net = gm.GpuMemNet(gpu)
+    net.set_path(path)
     net.set_model(m)
     ds = cb.generate_synthetic_dataset(fam, 3000, 777 + fam)
     raw = cb.scalar_features(ds.rows)
     for fmt, rows in ((abi.ROWS_FEATURES, ds.rows), (abi.ROWS_SCALAR, raw)):
         b, by, pr, lg = _predict_device(net, rows, fmt, len(ds.rows), default_family=fam)
         err = _check(m, raw, b, by, pr, lg)
-        assert err < 1e-4  # three bf16 activation parts keep ~24 bits per layer
+        assert err < 1e-4  # fp32 FMAs / three bf16 activation parts keep ~24 bits per layer
     t = net.last_timing()
-    assert t["launches"] >= 1 and t["mmas"] > 0
+    assert t["launches"] >= 1 and (t["mmas"] > 0) == (path == 1)
     # host-buffer API: same bins
     hb, hby = net.predict(ds.rows, default_family=fam)
     assert np.array_equal(hb, b) and np.array_equal(hby, by)
@@ -137,10 +139,12 @@ def test_kernel_matches_oracle(gpu, models, fam):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("fam", [0, 1, 2])
-def test_kernel_matches_golden(gpu, models, fam):
+@pytest.mark.parametrize("path", [1, 2], ids=["tcgen05", "cuda-cores"])
+def test_kernel_matches_golden(gpu, models, fam, path):
     m = models[fam]
     rows, raw, logits, _ = _golden(gm.FAMILY_NAMES[fam])
     net = gm.GpuMemNet(gpu)
+    net.set_path(path)
     net.set_model(m)
     b, by, pr, lg = _predict_device(net, rows, abi.ROWS_FEATURES, len(rows), default_family=fam)
     assert np.all(_close(lg[:, : m.members, : m.classes], logits))
@@ -149,9 +153,11 @@ def test_kernel_matches_golden(gpu, models, fam):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("q", [1, 2, 127, 128, 129, 1000, 100_003])
-def test_ragged_batches(gpu, models, q):
+@pytest.mark.parametrize("path", [1, 2], ids=["tcgen05", "cuda-cores"])
+def test_ragged_batches(gpu, models, q, path):
     m = models[1]
     net = gm.GpuMemNet(gpu)
+    net.set_path(path)
     net.set_model(m)
     ds = cb.generate_synthetic_dataset(1, q, 99 + q)
     raw = cb.scalar_features(ds.rows)
@@ -161,10 +167,12 @@ def test_ragged_batches(gpu, models, q):
 
 
 @pytest.mark.gpu
-def test_mixed_families_route_by_row(gpu, models):
+@pytest.mark.parametrize("path", [1, 2], ids=["tcgen05", "cuda-cores"])
+def test_mixed_families_route_by_row(gpu, models, path):
     """Packed / bit-packed rows carry their family: one call routes CNN, TF and
     MLP rows to their own ensembles; a family without a model -> no estimate."""
     net = gm.GpuMemNet(gpu)
+    net.set_path(path)
     for f in (0, 1):
         net.set_model(models[f])  # no Transformer model installed
     parts = [cb.generate_synthetic_dataset(f, n, 50 + f) for f, n in ((0, 700), (1, 1300), (2, 500))]
@@ -197,7 +205,8 @@ def test_mixed_families_route_by_row(gpu, models):
 @pytest.mark.gpu
 @pytest.mark.parametrize("shape", [(8, 8, 48), (1, 1, 2), (3, 5, 17), (8, 1, 8)],
                          ids=["E8-L8-C48", "E1-L1-C2", "E3-L5-C17", "E8-L1-C8"])
-def test_extreme_shapes_random_weights(gpu, shape):
+@pytest.mark.parametrize("path", [1, 2], ids=["tcgen05", "cuda-cores"])
+def test_extreme_shapes_random_weights(gpu, shape, path):
     """Random models at the limits of the spec: 8 members x 8 layers x 48
     bins (4 head passes), a single 1-layer member, odd widths."""
     E, L, C = shape
@@ -209,6 +218,7 @@ def test_extreme_shapes_random_weights(gpu, shape):
     n = gm.param_count(m)
     m.params = (rng.normal(0, 0.6, n)).astype(np.float32)
     net = gm.GpuMemNet(gpu)
+    net.set_path(path)
     net.set_model(m)
     ds = cb.generate_synthetic_dataset(0, 2000, 5)
     raw = cb.scalar_features(ds.rows)
