@@ -177,19 +177,21 @@ class Dist:
 
 
 # ------------------------------------------------------------------ data
-def knn_inputs(cb):
-    """The c2 batch: 8,388,608 CNN rows (seed 2024) + 8,388,608 Transformer rows (seed 2025)."""
-    out = {}
-
-    def gen(f):
-        out[f] = cb.generate_synthetic_dataset(f, KNN_ROWS_PER_FAMILY, KNN_SEEDS[f])
-
-    th = [threading.Thread(target=gen, args=(f,)) for f in KNN_SEEDS]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    rows = np.concatenate([out[1].rows, out[2].rows])
+def knn_inputs(cb, dev: int = 0):
+    """The c2 batch: 8,388,608 CNN rows (seed 2024) + 8,388,608 Transformer rows
+    (seed 2025), from the device generator (carma_dataset_generate_device,
+    bit-identical to the host / reference generator: tests/test_gpu_dataset.py)
+    and copied to host memory once (the e2e arms start from host rows)."""
+    import torch
+    from paper_2508_19073_b200 import abi
+    n = KNN_ROWS_PER_FAMILY
+    rb = abi.feature_row_dtype.itemsize
+    d_rows = torch.empty(2 * n * rb, dtype=torch.uint8, device=f"cuda:{dev}")
+    for k, f in enumerate(KNN_SEEDS):
+        cb.generate_synthetic_dataset_device(f, n, KNN_SEEDS[f], d_rows[k * n * rb:(k + 1) * n * rb], device=dev)
+    torch.cuda.synchronize(dev)
+    rows = d_rows.cpu().numpy().view(abi.feature_row_dtype)
+    del d_rows
     fam = np.concatenate([np.full(KNN_ROWS_PER_FAMILY, 1, np.int8), np.full(KNN_ROWS_PER_FAMILY, 2, np.int8)])
     return rows, fam
 
@@ -903,10 +905,11 @@ def run_carma(args, d: Dist):
     N = d.n
     stream = torch.cuda.Stream(dev)  # every timed call runs on this explicit stream
     t0 = time.time()
-    rows, fam = knn_inputs(cb)
+    rows, fam = knn_inputs(cb, dev)
     QT = len(rows)
     b, e = cdist.balanced_shards_count(QT, N)[d.rank]
-    log(f"[rank {d.rank}] knn inputs {QT} rows in {time.time() - t0:.1f}s; shard [{b}, {e})")
+    gen_s = time.time() - t0
+    log(f"[rank {d.rank}] knn inputs {QT} rows generated on the device in {gen_s:.2f}s; shard [{b}, {e})")
     knn_res, knn, (h_rows, h_fam, _) = knn_stage(abi, cb, dev, stream, args, d, rows, fam, b, e)
     neural = None
     if not args.skip_neural:
@@ -946,7 +949,7 @@ def run_carma(args, d: Dist):
         "value": knn_res["value"], "unit": "estimates/s", "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": knn_res["ms_per_step"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (reference generators, seeded)",
-        "config": knn_config(N, e - b),
+        "config": {**knn_config(N, e - b), "input_generation_s": gen_s},
         "e2e": knn_res["e2e"], "gpu_launches": knn_res["gpu_launches"], "roofline": knn_res["roofline"],
         "cpu_baseline": cpu, "clocks": knn_res["clocks"],
         "neural": neural, "scoring": scoring, "fused": fused, "small_configs": small, "replay": replay,

@@ -140,6 +140,29 @@ carma_status carma_knn_set_model(carma_knn* h, int32_t family, const double* lo,
                                  const int32_t* labels, uint64_t n, uint32_t k,
                                  uint64_t bucket_range);
 
+/* generate_synthetic_dataset(family, n, seed) (estimators.cpp:221-264, with
+ * the family's default GenerationBounds, bucket range and SimConstants) on the
+ * device, bit-identical to the reference's sequential mt19937_64 generator:
+ * rows[i] = extract_features of the i-th feasible sampled architecture,
+ * bucket[i] = bucketize(mem), mem[i] = ground_truth_memory (outputs nullable).
+ * The _device form takes device buffers and a stream (synchronised once per
+ * generation round); the plain form takes host buffers. stats (nullable):
+ * the engine words drawn, rows parsed / feasible (rounds may parse past the
+ * n-th feasible row), rounds. n = 0 returns INVALID (InvalidBounds). */
+typedef struct carma_dataset_stats {
+    uint64_t words_generated;
+    uint64_t rows_parsed;
+    uint64_t rows_accepted;
+    uint32_t rounds;
+    uint32_t reserved;
+} carma_dataset_stats;
+carma_status carma_dataset_generate_device(int32_t device, int32_t family, uint64_t n, uint64_t seed,
+                                           carma_feature_row* rows, int32_t* bucket, uint64_t* mem, void* stream,
+                                           carma_dataset_stats* stats);
+carma_status carma_dataset_generate(int32_t device, int32_t family, uint64_t n, uint64_t seed,
+                                    carma_feature_row* rows, int32_t* bucket, uint64_t* mem,
+                                    carma_dataset_stats* stats);
+
 /* HoldoutReport (estimators.hpp:96-103). */
 typedef struct carma_holdout_report {
     double accuracy;

@@ -61,6 +61,11 @@ replay_config_dtype = np.dtype([
     ("log_flags", "<i4"), ("log_reserved", "<i4"),
 ], align=True)
 
+dataset_stats_dtype = np.dtype([
+    ("words_generated", "<u8"), ("rows_parsed", "<u8"), ("rows_accepted", "<u8"), ("rounds", "<u4"),
+    ("reserved", "<u4"),
+], align=True)
+
 holdout_report_dtype = np.dtype([
     ("accuracy", "<f8"), ("macro_f1", "<f8"), ("underestimate_rate", "<f8"), ("train_size", "<u8"),
     ("holdout_size", "<u8"),
@@ -185,6 +190,8 @@ SIGNATURES = {
                                                    POINTER(c_void_p)]),
     "carma_replay_plan_entries": (c_int, [c_void_p, P]),
     "carma_replay_plan_tasks": (c_int, [c_void_p, P]),
+    "carma_dataset_generate_device": (c_int, [c_int32, c_int32, c_uint64, c_uint64, P, P, P, c_void_p, P]),
+    "carma_dataset_generate": (c_int, [c_int32, c_int32, c_uint64, c_uint64, P, P, P, P]),
     "carma_knn_train": (c_int, [c_void_p, c_int32, P, P, P, c_uint64, c_uint64, c_uint32, c_uint64, P, P, P, P, P]),
     "carma_host_split_order": (c_int, [c_uint64, c_uint64, P, POINTER(c_uint64)]),
     "carma_replay_plan_log": (c_int, [c_void_p, c_uint32, P, c_uint64, POINTER(c_uint64)]),

@@ -142,12 +142,29 @@ class EstimatorDataset:
         return abi.GiB if self.family == 0 else 8 * abi.GiB
 
 
-def generate_synthetic_dataset(family: int, n: int, seed: int) -> EstimatorDataset:
+def generate_synthetic_dataset(family: int, n: int, seed: int, device: Optional[int] = None) -> EstimatorDataset:
+    """generate_synthetic_dataset (estimators.cpp:221-264). device=None: the
+    host generator (csrc/host/model.cpp); device=d: the GPU generator
+    (csrc/cuda/dataset.cu, carma_dataset_generate), bit-identical."""
     rows = np.zeros(n, abi.feature_row_dtype)
     b = np.zeros(n, np.int32)
     m = np.zeros(n, np.uint64)
-    check(lib.carma_host_dataset(family, n, seed, ptr(rows), ptr(b), ptr(m)))
+    if device is None:
+        check(lib.carma_host_dataset(family, n, seed, ptr(rows), ptr(b), ptr(m)))
+    else:
+        check(lib.carma_dataset_generate(device, family, n, seed, ptr(rows), ptr(b), ptr(m), None))
     return EstimatorDataset(rows, b, m, family, seed)
+
+
+def generate_synthetic_dataset_device(family: int, n: int, seed: int, rows=None, bucket=None, mem=None,
+                                      device: int = 0, stream=None) -> np.ndarray:
+    """The GPU generator into device tensors (torch, any nullable): rows as
+    n x 136 bytes (carma_feature_row), bucket int32[n], mem int64[n] (u64
+    bits). Returns the carma_dataset_stats record."""
+    st = np.zeros(1, abi.dataset_stats_dtype)
+    check(lib.carma_dataset_generate_device(device, family, n, seed, ptr(rows), ptr(bucket), ptr(mem),
+                                            abi.stream_arg(stream, device), ptr(st)))
+    return st[0]
 
 
 def pack_features(rows: np.ndarray, family=None, default_family: int = 0):
