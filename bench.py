@@ -50,6 +50,12 @@ ALG_BYTES_PER_TASK = 80            # 45 B in + 35 B out per place
 FLOPS_PER_EVAL = 58                # 19 x (sub, mul, add) + 1 weight mul, FMA-free
 FLOPS_PER_F32_EVAL = 48            # fp32 pre-filter: 16 dims x (sub + fma)
 FEATURE_ROW_BYTES = 136
+# host-buffer calls re-encode the 136-B rows (+ 1-B family) into 64-B packed
+# rows on host threads, chunk by chunk, overlapped with the H2D copies
+# (csrc/host/stage.cpp); CARMA_E2E_RAW=1 ships the raw rows
+E2E_WIRE_BYTES = FEATURE_ROW_BYTES + 1 if os.environ.get("CARMA_E2E_RAW", "0") not in ("", "0") else 64
+E2E_API = ("{fn} (pinned 136-B carma_feature_row + family in, bucket + bytes out; rows re-encoded to 64-B packed "
+           "rows by the host thread pool inside the call, overlapped with H2D)")
 
 
 def log(*a):
@@ -487,11 +493,12 @@ def knn_stage(abi, cb, dev, stream, args, d, rows, fam, b, e):
     out = {
         "value": QT / (ms * 1e-3), "ms_per_step": ms, "clocks": clocks,
         "e2e": {"value": QT / e2e_s, "unit": "estimates/s",
-                "h2d_bytes_per_step": int(Q * (FEATURE_ROW_BYTES + 1)),
+                "h2d_bytes_per_step": int(Q * E2E_WIRE_BYTES),
                 "d2h_bytes_per_step": int(Q * 12),
-                "api": "carma_knn_predict (pinned 136-B carma_feature_row + family in, bucket + bytes out)",
+                "api": E2E_API.format(fn="carma_knn_predict"),
+                "host_row_bytes_read": int(Q * (FEATURE_ROW_BYTES + 1)),
                 "ms_per_step": e2e_s * 1e3,
-                "pcie_gbs": Q * (FEATURE_ROW_BYTES + 1 + 12) / e2e_s / 1e9},
+                "pcie_gbs": Q * (E2E_WIRE_BYTES + 12) / e2e_s / 1e9},
         "gpu_launches": int(launches) * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved / 1e12, "peak": fp32.value / 1e12, "unit": "TFLOP/s",
                      "frac": achieved / fp32.value,
@@ -569,24 +576,46 @@ def neural_stage(abi, cb, dev, stream, args, d, h_rows, h_fam, rows_all, fam_all
             agree += int(sure.sum())
         k_avg = statistics.mean(kernel_ms)
         r = {"value": QT / (ms * 1e-3), "ms_per_step": ms,
-             "e2e": {"value": QT / e2e_s, "unit": "estimates/s", "h2d_bytes_per_step": int(Q * (FEATURE_ROW_BYTES + 1)),
-                     "d2h_bytes_per_step": int(Q * 12), "api": "carma_nn_predict (pinned 136-B rows)"},
+             "e2e": {"value": QT / e2e_s, "unit": "estimates/s", "h2d_bytes_per_step": int(Q * E2E_WIRE_BYTES),
+                     "d2h_bytes_per_step": int(Q * 12), "api": E2E_API.format(fn="carma_nn_predict")},
              "gpu_launches": int(t["launches"]) * args.steps, "kernel_ms": k_avg,
              "kernel_share_of_step": k_avg / statistics.mean(call_ms), "oracle_agreement_rows": agree,
              "holdout_accuracy": {gm.FAMILY_NAMES[f]: models[f].holdout_accuracy for f in (1, 2)}}
         rows_f = {f: int((h_fam == f).sum()) for f in (1, 2)}
         useful = sum(rows_f[f] * nn_tile_flops(models[f])[1] for f in (1, 2))
         if key == "mlp":
-            executed = sum((rows_f[f] + 127) // 128 * nn_tile_flops(models[f])[0] for f in (1, 2))
-            peak = peaks().get("bf16_tflops", 2250.0)
+            # default path: mlp_ffma (fp32 FFMA on the CUDA cores); the tcgen05
+            # path (nn_ensemble) is timed beside it for the record
+            import ctypes as _ct
+            fp32 = _ct.c_double()
+            abi.check(abi.lib.carma_probe_fp32(dev, _ct.byref(fp32)))
             ach = useful / (k_avg * 1e-3) / 1e12
-            r["dtype"] = "bf16 x3 -> fp32"
-            r["roofline"] = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                             "traffic": profile_traffic("nn_ensemble"), "kernel": "nn_ensemble",
-                             "executed_tflops": executed / (k_avg * 1e-3) / 1e12,
-                             "work": f"algorithmic {useful / 1e9:.1f} GFLOP (dense ensemble math) per launch; "
-                                     f"executed {executed / 1e9:.1f} GFLOP on the tensor pipe",
-                             "peak_source": "MEASURED_PEAKS.json bf16_tflops"}
+            r["dtype"] = "f32"
+            r["roofline"] = {"bound": "fp32", "achieved": ach, "peak": fp32.value / 1e12, "unit": "TFLOP/s",
+                             "frac": ach / (fp32.value / 1e12), "traffic": profile_traffic("mlp_ffma"),
+                             "kernel": "mlp_ffma",
+                             "work": f"algorithmic {useful / 1e9:.1f} GFLOP (dense ensemble math, 2 flops per "
+                                     "multiply-add) per launch",
+                             "peak_source": "measured: carma_probe_fp32 (FFMA2 issue rate)"}
+            net.set_path(1)
+            tc_ms = []
+
+            def tc_step():
+                net.predict_device(d_rows, abi.ROWS_FEATURES, Q, d_b, d_by, family=d_fam, default_family=1,
+                                   stream=stream)
+                tc_ms.append(net.last_timing()["kernel_ms"])
+
+            timed_device_steps(tc_step, stream, args.warmup, args.steps, d)
+            executed = sum((rows_f[f] + 127) // 128 * nn_tile_flops(models[f])[0] for f in (1, 2))
+            tc_k = statistics.mean(tc_ms[args.warmup:])
+            peak = peaks().get("bf16_tflops", 2250.0)
+            r["tcgen05_path"] = {"kernel": "nn_ensemble", "kernel_ms": tc_k, "value": QT / (tc_k * 1e-3),
+                                 "useful_tflops": useful / (tc_k * 1e-3) / 1e12,
+                                 "executed_tflops": executed / (tc_k * 1e-3) / 1e12,
+                                 "executed_frac_of_bf16_peak": executed / (tc_k * 1e-3) / 1e12 / peak,
+                                 "traffic": profile_traffic("nn_ensemble"),
+                                 "note": "block-diagonal bf16 x3 on tcgen05 (M=128, K=16); slower than the "
+                                         "CUDA-core path, kept selectable (carma_nn_set_path)"}
         else:
             r["dtype"] = "f32"
             r["kernel"] = "tf_ensemble (CUDA cores)"

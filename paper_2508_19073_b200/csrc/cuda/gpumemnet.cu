@@ -50,12 +50,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
 
 #include "../../../include/carma_gpu.h"
 #include "common.cuh"
+#include "../host/stage.hpp"
 #include "rows.cuh"
 
 namespace carma_b200 {
@@ -1331,7 +1333,8 @@ struct NnHandle {
     HostNn model[CARMA_FAMILIES];
     struct Scratch {
         DeviceBuffer rows, family, perm, counts, bucket, bytes;
-        PinnedBuffer stage_rows, stage_family;
+        PinnedBuffer stage_rows, stage_family, stage_packed;
+        cudaEvent_t staged = nullptr;  // the H2D copy out of stage_packed is done
     } scratch[2];
     double act[16] = {0};
     carma_bit_schema schema{};
@@ -1574,13 +1577,44 @@ carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int3
         const bool out_pinned = (!bucket_out || is_pinned(bucket_out)) && (!bytes_out || is_pinned(bytes_out));
         h->timed = false;
         h->fence.host_wait();  // a device call may still use scratch[0]
+        auto copy_out = [&](NnHandle::Scratch& sc, cudaStream_t s, uint64_t beg, uint64_t cnt) {
+            if (bucket_out)
+                CARMA_CUDA(cudaMemcpyAsync(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost, s));
+            if (bytes_out)
+                CARMA_CUDA(cudaMemcpyAsync(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost, s));
+            if (!out_pinned) CARMA_CUDA(cudaStreamSynchronize(s));
+        };
+        // Feature rows travel re-encoded as 64-byte packed rows (stage.hpp);
+        // CARMA_E2E_RAW=1 sends the 136-byte rows as they are.
+        static const bool raw_env = std::getenv("CARMA_E2E_RAW") && std::atoi(std::getenv("CARMA_E2E_RAW")) != 0;
+        const bool pack = format == CARMA_ROWS_FEATURES && !raw_env;
+        if (pack) std::memcpy(h->act, canonical_act_table(), sizeof(h->act));
         uint64_t launches = 0, beg = 0, cnt = 0;
         for (uint64_t c = 0; beg < q; ++c, beg += cnt) {
             NnHandle::Scratch& sc = h->scratch[c & 1];
             cudaStream_t s = h->pipe[c & 1];
             cnt = std::min<uint64_t>(chunk_rows(c, q - beg), q - beg);
-            const char* src = static_cast<const char*>(rows) + beg * row_bytes;
             const uint64_t cap_rows = std::min<uint64_t>(chunk, q);
+            if (pack) {
+                sc.stage_packed.ensure(cap_rows * sizeof(carma_feature_packed));
+                sc.rows.ensure(cap_rows * row_bytes);
+                sc.bucket.ensure(cap_rows * 4);
+                sc.bytes.ensure(cap_rows * 8);
+                if (!sc.staged) CARMA_CUDA(cudaEventCreateWithFlags(&sc.staged, cudaEventDisableTiming));
+                CARMA_CUDA(cudaEventSynchronize(sc.staged));
+                auto* pk = sc.stage_packed.as<carma_feature_packed>();
+                if (pack_rows_canonical(static_cast<const carma_feature_row*>(rows) + beg, family ? family + beg : nullptr,
+                                        default_family, cnt, pk)) {
+                    CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, pk, cnt * sizeof(carma_feature_packed),
+                                               cudaMemcpyHostToDevice, s));
+                    CARMA_CUDA(cudaEventRecord(sc.staged, s));
+                    launches += run_predict(*h, sc, sc.rows.ptr, CARMA_ROWS_PACKED, nullptr, default_family, cnt,
+                                            sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(), nullptr, nullptr, s);
+                    copy_out(sc, s, beg, cnt);
+                    continue;
+                }
+            }
+            const char* src = static_cast<const char*>(rows) + beg * row_bytes;
             sc.rows.ensure(cap_rows * row_bytes + tail_bytes);
             sc.bucket.ensure(cap_rows * 4);
             sc.bytes.ensure(cap_rows * 8);
@@ -1603,18 +1637,7 @@ carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int3
             launches += run_predict(*h, sc, sc.rows.ptr, format, family ? sc.family.as<int8_t>() : nullptr,
                                     default_family, cnt, sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(), nullptr,
                                     nullptr, s);
-            if (out_pinned) {
-                if (bucket_out)
-                    CARMA_CUDA(cudaMemcpyAsync(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost, s));
-                if (bytes_out)
-                    CARMA_CUDA(cudaMemcpyAsync(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost, s));
-            } else {
-                if (bucket_out)
-                    CARMA_CUDA(cudaMemcpyAsync(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost, s));
-                if (bytes_out)
-                    CARMA_CUDA(cudaMemcpyAsync(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost, s));
-                CARMA_CUDA(cudaStreamSynchronize(s));
-            }
+            copy_out(sc, s, beg, cnt);
         }
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[1]));
@@ -1665,6 +1688,8 @@ carma_status carma_nn_destroy(carma_nn* hh) {
                 for (DeviceBuffer* b : {&sc.rows, &sc.family, &sc.perm, &sc.counts, &sc.bucket, &sc.bytes}) b->release();
                 sc.stage_rows.release();
                 sc.stage_family.release();
+                sc.stage_packed.release();
+                if (sc.staged) cudaEventDestroy(sc.staged);
             }
             for (auto e : h->ev)
                 if (e) cudaEventDestroy(e);

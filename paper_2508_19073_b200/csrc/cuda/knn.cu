@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -39,6 +40,8 @@
 #include "../../../include/carma_gpu.h"
 #include "../../../include/carma_host.h"
 #include "common.cuh"
+#include "../host/stage.hpp"
+#include "../host/stage.hpp"
 #include "rows.cuh"
 
 namespace carma_b200 {
@@ -1221,7 +1224,8 @@ struct KnnHandle {
     HostModel model[CARMA_FAMILIES];
     struct Scratch {
         DeviceBuffer rows, family, qbin, qpos, perm, hist, tot, bucket, bytes, qrec, brute_d2, brute_id;
-        PinnedBuffer stage_rows, stage_family;
+        PinnedBuffer stage_rows, stage_family, stage_packed;
+        cudaEvent_t staged = nullptr;  // the H2D copy out of stage_packed is done
     } scratch[2];
     DeviceBuffer evals;
     StreamFence fence;        // last device-stream user of scratch[0] + evals
@@ -1488,16 +1492,56 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
         h->evals.ensure(16);
         CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 16, h->pipe[0]));
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
+        auto copy_out = [&](KnnHandle::Scratch& sc, cudaStream_t s, uint64_t beg, uint64_t cnt) {
+            if (out_pinned) {
+                if (bucket_out)
+                    CARMA_CUDA(cudaMemcpyAsync(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost, s));
+                if (bytes_out)
+                    CARMA_CUDA(cudaMemcpyAsync(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost, s));
+            } else {
+                CARMA_CUDA(cudaStreamSynchronize(s));
+                if (bucket_out)
+                    CARMA_CUDA(cudaMemcpy(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost));
+                if (bytes_out)
+                    CARMA_CUDA(cudaMemcpy(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost));
+            }
+        };
         uint64_t launches = 0;
         uint64_t beg = 0, cnt = 0;
+        // Feature rows travel re-encoded as 64-byte packed rows (family inside;
+        // stage.hpp), packed by the host pool while the previous chunk copies
+        // and searches. CARMA_E2E_RAW=1 sends the 136-byte rows as they are.
+        static const bool raw_env = std::getenv("CARMA_E2E_RAW") && std::atoi(std::getenv("CARMA_E2E_RAW")) != 0;
+        const bool pack = format == CARMA_ROWS_FEATURES && !raw_env;
+        if (pack) std::memcpy(h->act, canonical_act_table(), sizeof(h->act));
         for (uint64_t c = 0; beg < q; ++c, beg += cnt) {
             KnnHandle::Scratch& sc = h->scratch[c & 1];
             cudaStream_t s = h->pipe[c & 1];
             cnt = std::min<uint64_t>(chunk_rows(c, q - beg), q - beg);
+            const uint64_t cap_rows = std::min<uint64_t>(chunk, q);
+            if (pack) {
+                sc.stage_packed.ensure(cap_rows * sizeof(carma_feature_packed));
+                sc.rows.ensure(cap_rows * row_bytes);
+                sc.bucket.ensure(cap_rows * 4);
+                sc.bytes.ensure(cap_rows * 8);
+                if (!sc.staged) CARMA_CUDA(cudaEventCreateWithFlags(&sc.staged, cudaEventDisableTiming));
+                CARMA_CUDA(cudaEventSynchronize(sc.staged));  // the previous copy out of this stage buffer
+                auto* pk = sc.stage_packed.as<carma_feature_packed>();
+                if (pack_rows_canonical(static_cast<const carma_feature_row*>(rows) + beg, family ? family + beg : nullptr,
+                                        default_family, cnt, pk)) {
+                    CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, pk, cnt * sizeof(carma_feature_packed),
+                                               cudaMemcpyHostToDevice, s));
+                    CARMA_CUDA(cudaEventRecord(sc.staged, s));
+                    launches += run_pipeline(*h, sc, sc.rows.ptr, CARMA_ROWS_PACKED, nullptr, default_family, cnt,
+                                             sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(), nullptr, nullptr,
+                                             h->evals.as<unsigned long long>(), s);
+                    copy_out(sc, s, beg, cnt);
+                    continue;
+                }
+            }
             const char* src = static_cast<const char*>(rows) + beg * row_bytes;
             // buffers for the largest chunk this call uses (not the steady
             // size: pinned staging for 2^21 rows costs ~0.1 s to allocate)
-            const uint64_t cap_rows = std::min<uint64_t>(chunk, q);
             sc.rows.ensure(cap_rows * row_bytes + tail_bytes);
             sc.bucket.ensure(cap_rows * 4);
             sc.bytes.ensure(cap_rows * 8);
@@ -1522,18 +1566,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
             launches += run_pipeline(*h, sc, sc.rows.ptr, format, family ? sc.family.as<int8_t>() : nullptr,
                                      default_family, cnt, sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(),
                                      nullptr, nullptr, h->evals.as<unsigned long long>(), s);
-            if (out_pinned) {
-                if (bucket_out)
-                    CARMA_CUDA(cudaMemcpyAsync(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost, s));
-                if (bytes_out)
-                    CARMA_CUDA(cudaMemcpyAsync(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost, s));
-            } else {
-                CARMA_CUDA(cudaStreamSynchronize(s));
-                if (bucket_out)
-                    CARMA_CUDA(cudaMemcpy(bucket_out + beg, sc.bucket.ptr, cnt * 4, cudaMemcpyDeviceToHost));
-                if (bytes_out)
-                    CARMA_CUDA(cudaMemcpy(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost));
-            }
+            copy_out(sc, s, beg, cnt);
         }
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[1]));
@@ -1585,7 +1618,8 @@ carma_status carma_knn_destroy(carma_knn* hh) {
                 sc.rows.release(); sc.family.release(); sc.qbin.release(); sc.qpos.release();
                 sc.perm.release(); sc.hist.release(); sc.tot.release(); sc.bucket.release(); sc.bytes.release();
                 sc.brute_d2.release(); sc.brute_id.release();
-                sc.stage_rows.release(); sc.stage_family.release();
+                sc.stage_rows.release(); sc.stage_family.release(); sc.stage_packed.release();
+                if (sc.staged) cudaEventDestroy(sc.staged);
             }
             h->evals.release();
             h->fence.destroy();

@@ -1,0 +1,163 @@
+// Host staging for the host-buffer predict calls (see stage.hpp).
+
+#include "stage.hpp"
+
+#include <immintrin.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <numbers>
+#include <thread>
+#include <vector>
+
+namespace carma_b200 {
+
+const double* canonical_act_table() {
+    static const struct T {
+        double v[16];
+        T() {
+            for (int i = 0; i < 8; ++i) {
+                const double a = 2.0 * std::numbers::pi * static_cast<double>(i) / 8.0;  // task.cpp:181-189
+                v[2 * i] = std::cos(a);
+                v[2 * i + 1] = std::sin(a);
+            }
+        }
+    } t;
+    return t.v;
+}
+
+namespace {
+
+// A fixed pool of workers; one bulk job at a time (callers serialise on mu_).
+class Pool {
+  public:
+    Pool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        n_ = std::min(hw, 32u);
+        for (uint32_t i = 1; i < n_; ++i) threads_.emplace_back([this, i] { loop(i); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> l(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+    uint32_t size() const { return n_; }
+    void run(uint32_t parts, const std::function<void(uint32_t, uint32_t)>& fn) {
+        std::lock_guard<std::mutex> job(mu_);
+        parts = std::max(1u, std::min(parts, n_));
+        {
+            std::lock_guard<std::mutex> l(m_);
+            fn_ = &fn;
+            parts_ = parts;
+            pending_ = parts - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn(0, parts);
+        std::unique_lock<std::mutex> l(m_);
+        done_.wait(l, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+  private:
+    void loop(uint32_t id) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(uint32_t, uint32_t)>* fn;
+            uint32_t parts;
+            {
+                std::unique_lock<std::mutex> l(m_);
+                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                fn = fn_;
+                parts = parts_;
+            }
+            if (id < parts) {
+                (*fn)(id, parts);
+                std::lock_guard<std::mutex> l(m_);
+                if (--pending_ == 0) done_.notify_one();
+            }
+        }
+    }
+    uint32_t n_ = 1;
+    std::vector<std::thread> threads_;
+    std::mutex mu_, m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(uint32_t, uint32_t)>* fn_ = nullptr;
+    uint32_t parts_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+Pool& pool() {
+    static Pool p;
+    return p;
+}
+
+inline bool pack_one(const carma_feature_row& r, uint64_t f, const uint64_t* canon, long long* o) {
+    constexpr uint64_t k48 = 1ull << 48;
+    const uint64_t big = r.total_params | r.total_activations | r.tuple_acts[0] | r.tuple_params[0] |
+                         r.tuple_acts[1] | r.tuple_params[1] | r.tuple_acts[2] | r.tuple_params[2];
+    const uint64_t tally = r.n_linear | r.n_batchnorm | r.n_dropout | r.n_conv;
+    const uint32_t kinds = static_cast<uint32_t>(r.kind[0]) | static_cast<uint32_t>(r.kind[1]) |
+                           static_cast<uint32_t>(r.kind[2]);
+    uint64_t cb, sb;
+    std::memcpy(&cb, &r.act_cos, 8);
+    std::memcpy(&sb, &r.act_sin, 8);
+    uint64_t code = 8;
+    for (uint64_t k = 0; k < 8; ++k)
+        if (cb == canon[2 * k] && sb == canon[2 * k + 1]) code = k;
+    if (big >= k48 || tally > 255 || r.batch_size >= (1ull << 32) || kinds > 15 || code == 8) return false;
+    const uint64_t w[8] = {
+        r.total_params | (r.n_linear << 48) | (r.n_batchnorm << 56),
+        r.total_activations | (r.n_dropout << 48) | (r.n_conv << 56),
+        r.tuple_acts[0] | ((r.batch_size & 0xffffull) << 48),
+        r.tuple_params[0] | (static_cast<uint64_t>(r.kind[0]) << 48) | (static_cast<uint64_t>(r.kind[1]) << 52) |
+            (static_cast<uint64_t>(r.kind[2]) << 56) | (static_cast<uint64_t>(r.has_layers ? 1 : 0) << 60) |
+            (code << 61),
+        r.tuple_acts[1] | (f << 48),
+        r.tuple_params[1] | ((r.batch_size >> 16) << 48),
+        r.tuple_acts[2],
+        r.tuple_params[2]};
+    for (int k = 0; k < 8; ++k) _mm_stream_si64(o + k, static_cast<long long>(w[k]));
+    return true;
+}
+
+}  // namespace
+
+void host_parallel(uint32_t parts, const std::function<void(uint32_t, uint32_t)>& fn) { pool().run(parts, fn); }
+
+uint32_t host_workers() { return pool().size(); }
+
+bool pack_rows_canonical(const carma_feature_row* rows, const int8_t* family, int32_t default_family, uint64_t n,
+                         carma_feature_packed* out) {
+    uint64_t canon[16];
+    std::memcpy(canon, canonical_act_table(), sizeof(canon));
+    std::atomic<bool> ok{true};
+    const uint32_t parts = static_cast<uint32_t>(std::min<uint64_t>(host_workers(), (n + 16383) / 16384));
+    const int8_t dflt = default_family >= 0 && default_family < CARMA_FAMILIES ? static_cast<int8_t>(default_family)
+                                                                                 : static_cast<int8_t>(-1);
+    host_parallel(parts, [&](uint32_t p, uint32_t np) {
+        const uint64_t b = n * p / np, e = n * (p + 1) / np;
+        bool good = true;
+        for (uint64_t i = b; i < e && good; ++i) {
+            // the family byte as the packed format stores it (w4 >> 48 & 0xff):
+            // a negative or absent family decodes to "no model", as for raw rows
+            const uint64_t f = static_cast<uint8_t>(family ? family[i] : dflt);
+            good = pack_one(rows[i], f, canon, reinterpret_cast<long long*>(out + i));
+        }
+        _mm_sfence();
+        if (!good) ok.store(false, std::memory_order_relaxed);
+    });
+    return ok.load();
+}
+
+}  // namespace carma_b200

@@ -1,0 +1,33 @@
+// Host-side staging for the host-buffer predict calls (carma_knn_predict,
+// carma_nn_predict): the 136-byte carma_feature_row batch is re-encoded, by a
+// pool of host threads and chunk by chunk, into the 64-byte lossless packed
+// format (include/carma_gpu.h) in pinned staging memory, overlapped with the
+// previous chunk's H2D copy and search — the PCIe bytes per row fall from 137
+// (row + family) to 64. The activation code indexes the canonical table of
+// the 8 registry activations (extract_features' glibc cos / sin of
+// 2*pi*i/8, task.cpp:181-189, 301-323); a chunk holding any row the packed
+// format cannot carry is sent as raw rows instead.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+
+#include "../../../include/carma_gpu.h"
+
+namespace carma_b200 {
+
+// The 16-double (cos, sin) table of the 8 registry activations.
+const double* canonical_act_table();
+
+// Runs fn(part, parts) on `parts` persistent worker threads (the caller's
+// thread takes part 0) and returns when all parts are done.
+void host_parallel(uint32_t parts, const std::function<void(uint32_t, uint32_t)>& fn);
+uint32_t host_workers();  // parts host_parallel uses for a bulk pass
+
+// Packs rows[0, n) (+ family, nullable -> default_family) into out with
+// non-temporal stores; false if some row does not fit the packed format
+// (out is then unspecified).
+bool pack_rows_canonical(const carma_feature_row* rows, const int8_t* family, int32_t default_family, uint64_t n,
+                         carma_feature_packed* out);
+
+}  // namespace carma_b200

@@ -273,3 +273,43 @@ def test_train_on_device_equals_host_fit(gpu, family, samples, seed):
     k2 = cb.GpuKnn(gpu)
     k2.set_model(m)
     assert np.array_equal(est.predict(ds.rows), k2.predict(ds.rows, default_family=family)[0])
+
+
+def _mixed_rows():
+    """~700k rows over 3+ host-pipeline chunks: the three families, rows whose
+    family is negative or has no model, and in one chunk a row whose
+    activation is not a registry activation (that chunk cannot travel packed
+    and goes as raw 136-byte rows)."""
+    parts, fams = [], []
+    for f, s in ((0, 3), (1, 4), (2, 5)):
+        ds = cb.generate_synthetic_dataset(f, 230_000, s)
+        parts.append(ds.rows)
+        fams.append(np.full(230_000, f, np.int8))
+    rows, fam = np.concatenate(parts), np.concatenate(fams)
+    perm = np.random.default_rng(1).permutation(len(rows))
+    rows, fam = rows[perm].copy(), fam[perm].copy()
+    fam[::997] = -1
+    fam[5::1009] = 7
+    rows["act_cos"][400_123] = 0.3
+    rows["act_sin"][400_123] = 0.25
+    return rows, fam
+
+
+def test_host_api_packed_staging_and_raw_fallback(gpu, models):
+    """carma_knn_predict re-encodes host feature rows as 64-byte packed rows per
+    chunk (csrc/host/stage.cpp) and falls back to raw rows for a chunk that
+    does not fit; results equal the device-resident raw-row path bit for bit."""
+    rows, fam = _mixed_rows()
+    knn = cb.GpuKnn(gpu)
+    for f in models:
+        knn.set_model(models[f])
+    hb, hby = knn.predict(rows, family=fam, default_family=0)
+    db, dby, _, _ = _device_predict(knn, rows, family=fam, default_family=0)
+    assert np.array_equal(hb, db) and np.array_equal(hby, dby)
+    assert (hb[fam == -1] == -1).all() and (hby[fam == 7] == np.uint64(2**64 - 1)).all()
+    # no family array: default_family for every row, also out of range
+    hb2, _ = knn.predict(rows[:300_000], default_family=2)
+    db2, _, _, _ = _device_predict(knn, rows[:300_000], default_family=2)
+    assert np.array_equal(hb2, db2)
+    hb3, _ = knn.predict(rows[:1000], default_family=9)
+    assert (hb3 == -1).all()

@@ -368,3 +368,27 @@ def test_grouped_rows_read_in_place(gpu, models):
     assert np.array_equal(gb[order], sb) and np.array_equal(gby[order], sby)
     assert np.all(gb[fams == 2] == -1)
     net.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", [1, 2], ids=["tcgen05", "cuda-cores"])
+def test_host_api_packed_staging_and_raw_fallback(gpu, models, path):
+    """carma_nn_predict re-encodes host feature rows as 64-byte packed rows per
+    chunk and falls back to raw rows for a chunk holding a non-registry
+    activation; identical to the device-resident raw-row path."""
+    parts = [cb.generate_synthetic_dataset(f, 200_000, 60 + f) for f in (0, 1, 2)]
+    rows = np.concatenate([p.rows for p in parts])
+    fams = np.concatenate([np.full(len(p.rows), p.family, np.int8) for p in parts])
+    order = np.random.default_rng(4).permutation(len(rows))
+    rows, fams = rows[order].copy(), fams[order].copy()
+    fams[::991] = -1
+    rows["act_cos"][350_001] = 0.3
+    net = gm.GpuMemNet(gpu)
+    net.set_path(path)
+    for f in (0, 1, 2):
+        net.set_model(models[f])
+    hb, hby = net.predict(rows, family=fams, default_family=0)
+    db, dby, _, _ = _predict_device(net, rows, abi.ROWS_FEATURES, len(rows), family=fams)
+    assert np.array_equal(hb, db) and np.array_equal(hby, dby)
+    assert (hb[fams == -1] == -1).all()
+    net.close()
