@@ -13,7 +13,7 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_uint32, c_uint
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcarma_b200.so")
+LIB_PATH = os.environ.get("CARMA_B200_LIB") or os.path.join(_HERE, "libcarma_b200.so")  # override: A/B builds
 
 CARMA_OK = 0
 CARMA_ERR_INVALID, CARMA_ERR_CUDA, CARMA_ERR_OVERFLOW, CARMA_ERR_FAMILY = 1, 2, 3, 4

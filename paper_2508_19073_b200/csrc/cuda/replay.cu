@@ -852,3 +852,13 @@ carma_status carma_pick_batch_device(int device, const carma_replay_config* cfg,
 }
 
 }  // extern "C"
+
+#if REPLAY_PROF
+// Diagnostic builds only: reads and clears the per-region cycle counters.
+extern "C" int carma_debug_replay_prof(unsigned long long* out) {
+    if (cudaMemcpyFromSymbol(out, carma_b200::replay::g_replay_prof, 16 * sizeof(unsigned long long)) != cudaSuccess)
+        return 1;
+    const unsigned long long z[16] = {};
+    return cudaMemcpyToSymbol(carma_b200::replay::g_replay_prof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -59,6 +59,21 @@ namespace replay {
 #define REPLAY_MIN_CTAS 8
 #endif
 
+#ifndef REPLAY_PROF
+#define REPLAY_PROF 0
+#endif
+#if REPLAY_PROF
+// Diagnostic builds only (-DREPLAY_PROF=1): clock64 cycles per event-loop
+// region, summed over jobs: 0 next event, 1 integrate, 2 handle, 3 refresh,
+// 4 decide, 5 place, 6 push, 7 events.
+__device__ unsigned long long g_replay_prof[16];
+#define RPROF_T(v) const long long v = clock64()
+#define RPROF_ADD(r, t0) prof[r] += static_cast<unsigned long long>(clock64() - (t0))
+#else
+#define RPROF_T(v)
+#define RPROF_ADD(r, t0)
+#endif
+
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kWindow = 1u, kCompletion = 2u, kCrash = 3u, kTick = 4u;
 constexpr int32_t kStatusRetry = -1;      // overflowed this tier
@@ -107,6 +122,9 @@ struct Layout {
     static constexpr int G = G_, H = H_, S = S_, RC = RC_, RG = RG_, RQ = RQ_, W = W_;
     static constexpr bool MIG = (F_ & 1) != 0;
     static constexpr bool TL = (F_ & 2) != 0;  // diagnostics: timeline ticks and/or event/decision logs
+    // Event queue: a sorted ring (O(1) pop, warp-parallel insert) for the
+    // long-trace tiers, a 4-ary heap for the short-trace tiers.
+    static constexpr bool SQ = H_ >= 1024;
     static constexpr size_t MI = MIG ? 1 : 0;
     static constexpr int GPL = (G + 31) / 32;
     static constexpr size_t al8(size_t x) { return (x + 15) / 16 * 16; }
@@ -167,7 +185,7 @@ __device__ __forceinline__ bool later(double ta, uint32_t sa, double tb, uint32_
 // Warp-uniform scalar state (replicated in every lane).
 struct Sc {
     double now, deadline, window, begin0;
-    uint32_t seq_next, arrived, mq_head, rq_head, rq_cnt, hsize, nfree, T;
+    uint32_t seq_next, arrived, mq_head, rq_head, rq_cnt, hsize, hhead, nfree, T;
     int rr_cursor;
     int32_t oom, status;
     uint32_t events_lo, events_hi;
@@ -213,6 +231,12 @@ struct __align__(16) HeapEnt {
     uint32_t info;
 };
 
+// The earliest pending event (the queue is non-empty).
+template <class L>
+__device__ __forceinline__ const HeapEnt& heap_top(const char* b, const Sc& c) {
+    return reinterpret_cast<const HeapEnt*>(b + L::ht)[L::SQ ? c.hhead : 0];
+}
+
 template <class L>
 __device__ __forceinline__ uint32_t heap_push(char* b, Sc& c, double t, uint32_t info) {
     if (c.hsize >= static_cast<uint32_t>(L::H)) {
@@ -224,6 +248,72 @@ __device__ __forceinline__ uint32_t heap_push(char* b, Sc& c, double t, uint32_t
     e.key = tkey(t);
     e.seq = c.seq_next++;
     e.info = info;
+    if constexpr (L::SQ) {
+        // Sorted ring [hhead, hhead + hsize): the new event has the largest
+        // seq so far, so it goes after every entry whose key is <= its key.
+        // The lanes find that position in parallel, then shift the shorter
+        // side by one slot, 32 entries at a time.
+        const unsigned lane = threadIdx.x & 31;
+        const uint32_t n = c.hsize, hd = c.hhead;
+        auto at = [&](uint32_t i) {
+            const uint32_t x = hd + i;
+            return x >= static_cast<uint32_t>(L::H) ? x - static_cast<uint32_t>(L::H) : x;
+        };
+        // two parallel probes: 32 evenly spaced samples pick the segment,
+        // then the segment's entries (<= 32 at a time) give the position
+        const uint32_t stride = (n + 31) >> 5;
+        const uint32_t si = lane * stride;
+        const unsigned below = __ballot_sync(0xffffffffu, si < n && h[at(si)].key <= e.key);
+        uint32_t pos = 0;
+        if (below) {
+            const uint32_t m = static_cast<uint32_t>(__popc(below));
+            const uint32_t seg_end = min(m * stride, n);
+#pragma unroll 1
+            for (uint32_t base = (m - 1) * stride; base < seg_end; base += 32) {
+                const uint32_t i = base + lane;
+                const unsigned le = __ballot_sync(0xffffffffu, i < seg_end && h[at(i)].key <= e.key);
+                pos = base + static_cast<uint32_t>(__popc(le));
+                if (le != 0xffffffffu) break;
+            }
+        }
+        constexpr uint32_t H = static_cast<uint32_t>(L::H);
+        if (pos < n - pos) {
+            // nearer the head: move [0, pos) down one slot (the head moves
+            // back), bottom chunk first
+#pragma unroll 1
+            for (uint32_t lo = 0; lo < pos; lo += 32) {
+                const uint32_t i = lo + lane;
+                HeapEnt v;
+                if (i < pos) v = h[at(i)];
+                __syncwarp();
+                if (i < pos) {
+                    const uint32_t x = at(i);
+                    h[x == 0 ? H - 1 : x - 1] = v;
+                }
+                __syncwarp();
+            }
+            const uint32_t x = at(pos);
+            if (lane == 0) h[x == 0 ? H - 1 : x - 1] = e;
+            c.hhead = hd == 0 ? H - 1 : hd - 1;
+        } else {
+            // nearer the tail: move [pos, n) up one slot, top chunk first
+#pragma unroll 1
+            for (uint32_t hi = n; hi > pos;) {
+                const uint32_t lo = hi - pos > 32 ? hi - 32 : pos;
+                const uint32_t i = lo + lane;
+                HeapEnt v;
+                if (i < hi) v = h[at(i)];
+                __syncwarp();
+                if (i < hi) h[at(i + 1)] = v;
+                __syncwarp();
+                hi = lo;
+            }
+            if (lane == 0) h[at(pos)] = e;
+        }
+        __syncwarp();
+        c.hsize = n + 1;
+        return e.seq;
+    }
     uint32_t i = c.hsize++;
     while (i > 0) {
         const uint32_t p = (i - 1) >> 2;
@@ -238,6 +328,11 @@ __device__ __forceinline__ uint32_t heap_push(char* b, Sc& c, double t, uint32_t
 
 template <class L>
 __device__ __forceinline__ void heap_pop(char* b, Sc& c) {
+    if constexpr (L::SQ) {
+        c.hhead = c.hhead + 1 == static_cast<uint32_t>(L::H) ? 0 : c.hhead + 1;
+        --c.hsize;
+        return;
+    }
     HeapEnt* h = reinterpret_cast<HeapEnt*>(b + L::ht);
     const uint32_t n = --c.hsize;
     if (n == 0) return;
@@ -933,6 +1028,7 @@ __device__ __noinline__ void init_job(char* b, const Params& p, uint32_t j, unsi
     c.rq_head = 0;
     c.rq_cnt = 0;
     c.hsize = 0;
+    c.hhead = 0;
     c.nfree = L::S;
     c.T = T;
     c.rr_cursor = 0;
@@ -1119,7 +1215,11 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
         if (tick_live) c.seq_next = c.T + 1;
     }
     const double delay = RP_CFG.oom_startup_delay;
+#if REPLAY_PROF
+    unsigned long long prof[16] = {};
+#endif
     for (;;) {
+        RPROF_T(tp0);
         // ---- next event: arrival stream (seq = index) vs heap top
         const bool have_arr = c.arrived < c.T;
         const bool have_heap = c.hsize > 0;
@@ -1136,29 +1236,34 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             if (tick_live) {
                 const uint64_t tk = tkey(tick_t);
                 tick = !(have_arr && klater(tk, tick_seq, tkey(at), c.arrived)) &&
-                       !(have_heap && klater(tk, tick_seq, reinterpret_cast<const HeapEnt*>(b + L::ht)->key,
-                                             reinterpret_cast<const HeapEnt*>(b + L::ht)->seq));
+                       !(have_heap && klater(tk, tick_seq, heap_top<L>(b, c).key, heap_top<L>(b, c).seq));
             }
         }
         if (tick) {
             t = tick_t;
             kind = kTick;
             payload = 0;
-        } else if (have_arr && (!have_heap || !klater(tkey(at), c.arrived, reinterpret_cast<const HeapEnt*>(b + L::ht)->key,
-                                                      reinterpret_cast<const HeapEnt*>(b + L::ht)->seq))) {
+        } else if (have_arr && (!have_heap || !klater(tkey(at), c.arrived, heap_top<L>(b, c).key,
+                                                      heap_top<L>(b, c).seq))) {
             t = at;
             kind = 0;
             payload = c.arrived;
         } else {
-            const HeapEnt top = *reinterpret_cast<const HeapEnt*>(b + L::ht);
+            const HeapEnt top = heap_top<L>(b, c);
             t = tval(top.key);
             seq = top.seq;
             const uint32_t info = top.info;
             kind = info >> 30;
             payload = info & 0x3fffffffu;
+#if REPLAY_PROF
+            prof[8] += c.hsize;
+            prof[9] += 1;
+#endif
             heap_pop<L>(b, c);
         }
         ++events;
+        RPROF_ADD(0, tp0);
+        RPROF_T(tp1);
         // ---- integrate_to (world.cpp:37-44)
         const double dt = __dsub_rn(t, c.now);
         if (dt > 0.0) {
@@ -1172,6 +1277,8 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             }
         }
         c.now = t;
+        RPROF_ADD(1, tp1);
+        RPROF_T(tp2);
         if constexpr (L::TL) {
             if (kind == kTick) {
                 // emit_timeline_row (world.cpp:210-219), then reschedule while
@@ -1240,10 +1347,18 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             c.rq_cnt++;
             __syncwarp();
         }
+        RPROF_ADD(2, tp2);
         // ---- refresh_rates after finish / place, then try_schedule
         for (;;) {
             if (nt) {
+                RPROF_T(tp3);
                 refresh_rates<L>(b, c, t0, t1, nt, lane);
+                RPROF_ADD(3, tp3);
+#if REPLAY_PROF
+                prof[12] += RP_U32(nres)[t0] + (nt > 1 ? RP_U32(nres)[t1] : 0);
+                prof[13] += 1;
+                prof[14] += RP_U32(rcnt)[t0];
+#endif
                 nt = 0;
                 if (c.status) break;
             }
@@ -1253,7 +1368,13 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             bool from_recovery = false;
             int g0 = -1, g1 = -1, i0 = 0, i1 = 0;
             uint64_t est_bytes = 0;
+            RPROF_T(tp4);
             const int got = decide<L>(b, c, tasks, est, head, from_recovery, g0, g1, i0, i1, est_bytes, lane);
+            RPROF_ADD(4, tp4);
+#if REPLAY_PROF
+            prof[10] += head != kNone;
+            prof[11] += 1;
+#endif
             if constexpr (L::TL) {
                 // the decision log of try_schedule (manager.cpp:298-318): logged whenever
                 // map_task ran; a deferral prints the configured policy
@@ -1272,7 +1393,9 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             // dispatch (manager.cpp:247-260)
             if (lane == 0 && !from_recovery) out[head].first_attempt = c.now;
             OomInfo oi{};
+            RPROF_T(tp5);
             const bool ok = place<L>(b, c, tasks[head], head, g0, g1, i0, i1, got, nblk, lane, oi);
+            RPROF_ADD(5, tp5);
             if (c.status) break;
             if constexpr (L::TL) {
                 if (log_flags & CARMA_LOG_EVENTS) {
@@ -1300,11 +1423,13 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             // crash (on failure, manager.cpp:251-256) then arm_window
             // (manager.cpp:275-278): one push site for both.
             c.deadline = __dadd_rn(c.now, c.window);
+            RPROF_T(tp6);
 #pragma unroll 1
             for (int e = ok ? 1 : 0; e < 2; ++e) {
                 if (e == 0) heap_push<L>(b, c, __dadd_rn(c.now, delay), (kCrash << 30) | head);
                 else heap_push<L>(b, c, c.deadline, kWindow << 30);
             }
+            RPROF_ADD(6, tp6);
             if (c.status) break;
         }
         if (c.status) break;
@@ -1316,6 +1441,12 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             p.log_count[j] = n_log;
         }
     }
+#if REPLAY_PROF
+    prof[7] = events;
+    prof[15] = c.seq_next;
+    if (lane == 0)
+        for (int r = 0; r < 16; ++r) atomicAdd(&g_replay_prof[r], prof[r]);
+#endif
     c.events_lo = static_cast<uint32_t>(events);
     c.events_hi = static_cast<uint32_t>(events >> 32);
     __syncwarp();

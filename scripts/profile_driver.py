@@ -115,6 +115,16 @@ def fused(args):
               f"(tier0 {km.value:.1f}), stats {fr.plan.stats()}", flush=True)
     r = fr.results().traces[0]
     print("oom", r["oom_count"], "events", r["events"], "makespan", r["trace_total_time"], "status", r["status"])
+    if hasattr(abi.lib, "carma_debug_replay_prof"):  # REPLAY_PROF builds: cycles per event-loop region
+        v = (ctypes.c_ulonglong * 16)()
+        abi.lib.carma_debug_replay_prof(v)
+        names = ["next_event", "integrate", "handle", "refresh", "decide", "place", "push", "events"]
+        tot = sum(v[:7])
+        for n, x in zip(names, v):
+            print(f"  {n:10s} {x:16d}" + (f"  {100 * x / tot:5.1f}%  {x / max(v[7], 1):8.1f} cyc/event" if n != "events" else ""))
+        print(f"  heap pops {v[9]}, mean heap size {v[8] / max(v[9], 1):.1f}; decides {v[11]}, with a head {v[10]}; "
+              f"refreshes {v[13]}, mean residents on touched GPUs {v[12] / max(v[13], 1):.2f}, "
+              f"mean ring entries {v[14] / max(v[13], 1):.2f}; pushes {v[15]}")
 
 
 def scoring(args):
