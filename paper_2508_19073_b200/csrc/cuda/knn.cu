@@ -94,6 +94,10 @@ struct KnnParams {
     int32_t default_family;
     uint64_t q;
     double* qrec;  // fp32 path: per row the normalised query (19) + eta, written by knn_prep
+    // sorted layout: qrec indexed by the bucketed slot (written by
+    // knn_prep_sorted), and bucket / bytes written by slot, un-permuted after
+    int32_t qrec_by_slot;
+    int32_t out_by_slot;
 };
 
 // Query record (fp32 path): normalised query (19), eta, t_in (the smallest
@@ -202,6 +206,71 @@ __global__ void knn_keys(KnnParams p, uint32_t n_bins, uint32_t* __restrict__ qb
         hist[static_cast<uint64_t>(b) * gridDim.x + blockIdx.x] = sh[b];
 }
 
+// The fp32 path's query record of row i (family f >= 0, start position pos
+// over the keys): featurise, the 19 correctly rounded normalisations
+// (estimators.cpp:439-441), the fp32 error radius eta, t_in.
+template <int FMT>
+__device__ __forceinline__ void write_qrec(const KnnParams& p, uint64_t i, int f, uint32_t pos,
+                                           const double* __restrict__ keys, double2* rec) {
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    const ModelDev& m = p.m[f];
+    double raw[kDims];
+    load_raw<FMT>(p, static_cast<uint32_t>(i), raw);
+    double qn[kDims];
+    double qmax = 0.0;
+#pragma unroll
+    for (int d = 0; d < kDims; ++d) {
+        qn[d] = normalize(raw[d], m.lo[d], m.hi[d]);
+        const double av = fabs(qn[d]);
+        qmax = (av > qmax || av != av) ? av : qmax;
+    }
+    // active dims in ascending order are adim[0..]: walk d with a running j
+    double e2 = 0.0;
+    int j = 0;
+#pragma unroll
+    for (int d = 0; d < kDims; ++d) {
+        if ((m.active >> d) & 1u) {
+            const double w = d == 18 ? 64.0 : 1.0;
+            const double ej = 2.0 * 0x1.0p-24 * (1.0 + 0x1.0p-24) * w * (m.pmax[j] + fabs(qn[d])) + 0x1.0p-140;
+            e2 += ej * ej;
+            ++j;
+        }
+    }
+    double eta = sqrt(e2) * (1.0 + 0x1.0p-40);
+    if (!(qmax <= 1e15)) eta = inf;  // huge or NaN query: exact on every point
+#pragma unroll
+    for (int h = 0; h < 9; ++h) rec[h] = make_double2(qn[2 * h], qn[2 * h + 1]);
+    rec[9] = make_double2(qn[18], eta);
+    const double t_in = fmin(pos > 0 ? t18_of(keys[pos - 1], qn[18]) : inf,
+                             pos < m.n ? t18_of(keys[pos], qn[18]) : inf);
+    rec[10] = make_double2(t_in, __longlong_as_double(static_cast<long long>(pos)));
+}
+
+// Sorted layout, pass 2 (after the bucketing): the record of the row in each
+// bucketed slot, written at the slot, so the search reads its warp's 32
+// records as one contiguous 5.6 KB span instead of 32 random ones.
+template <int FMT>
+__global__ void __launch_bounds__(256) knn_prep_sorted(KnnParams p, const uint32_t* __restrict__ perm,
+                                                       const uint32_t* __restrict__ qpos) {
+    const uint64_t slot = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (slot >= p.q) return;
+    const uint32_t row = perm[slot];
+    const int f = family_of_t<FMT>(p, row);
+    if (f < 0) return;
+    write_qrec<FMT>(p, row, f, qpos[row], p.m[f].key18, reinterpret_cast<double2*>(p.qrec + slot * kQrec));
+}
+
+// bucket / bytes from slot order back to row order.
+__global__ void __launch_bounds__(256) knn_unpermute(uint64_t q, const uint32_t* __restrict__ perm,
+                                                     const int32_t* __restrict__ sb, const uint64_t* __restrict__ sby,
+                                                     int32_t* __restrict__ bucket, uint64_t* __restrict__ bytes) {
+    const uint64_t slot = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (slot >= q) return;
+    const uint32_t row = perm[slot];
+    if (bucket) bucket[row] = sb[slot];
+    if (bytes) bytes[row] = sby[slot];
+}
+
 // Pass 1 of the fp32 path: knn_keys plus the whole per-query setup of the
 // search (featurise, the 19 correctly rounded normalisations of
 // estimators.cpp:439-441, the fp32 error radius eta), written as a 160-B
@@ -239,38 +308,8 @@ __global__ void __launch_bounds__(512, 2) knn_prep(KnnParams p, uint32_t n_bins,
         uint32_t bin = kInvalidBin, pos = 0;
         if (f >= 0) {
             const ModelDev& m = p.m[f];
-            double raw[kDims];
-            load_raw<FMT>(p, static_cast<uint32_t>(i), raw);
-            double qn[kDims];
-            double qmax = 0.0;
-#pragma unroll
-            for (int d = 0; d < kDims; ++d) {
-                qn[d] = normalize(raw[d], m.lo[d], m.hi[d]);
-                const double av = fabs(qn[d]);
-                qmax = (av > qmax || av != av) ? av : qmax;
-            }
-            // active dims in ascending order are adim[0..]: walk d with a running j
-            double e2 = 0.0;
-            int j = 0;
-#pragma unroll
-            for (int d = 0; d < kDims; ++d) {
-                if ((m.active >> d) & 1u) {
-                    const double w = d == 18 ? 64.0 : 1.0;
-                    const double ej = 2.0 * 0x1.0p-24 * (1.0 + 0x1.0p-24) * w * (m.pmax[j] + fabs(qn[d])) + 0x1.0p-140;
-                    e2 += ej * ej;
-                    ++j;
-                }
-            }
-            double eta = sqrt(e2) * (1.0 + 0x1.0p-40);
-            if (!(qmax <= 1e15)) eta = inf;  // huge or NaN query: exact on every point
-            double2* rec = reinterpret_cast<double2*>(p.qrec + i * kQrec);
-#pragma unroll
-            for (int h = 0; h < 9; ++h) rec[h] = make_double2(qn[2 * h], qn[2 * h + 1]);
-            rec[9] = make_double2(qn[18], eta);
-            pos = lower_bound_any(keys[f], static_cast<uint32_t>(m.n), qn[18]);
-            const double t_in = fmin(pos > 0 ? t18_of(keys[f][pos - 1], qn[18]) : inf,
-                                     pos < m.n ? t18_of(keys[f][pos], qn[18]) : inf);
-            rec[10] = make_double2(t_in, __longlong_as_double(static_cast<long long>(pos)));
+            pos = lower_bound_any(keys[f], static_cast<uint32_t>(m.n), normalize(raw18_of(p, i), m.lo[18], m.hi[18]));
+            write_qrec<FMT>(p, i, f, pos, keys[f], reinterpret_cast<double2*>(p.qrec + i * kQrec));
             bin = m.bin_base + (pos >> m.bin_shift);
         }
         const uint32_t b = bin == kInvalidBin ? n_bins - 1 : bin;
@@ -685,6 +724,9 @@ __device__ __forceinline__ void sorted_insert(float (&a)[K], float v) {
     a[0] = fminf(a[0], v);
 }
 
+#ifndef KNN_LAYOUT
+#define KNN_LAYOUT 0
+#endif
 #ifndef KNN_F32_CTAS
 #define KNN_F32_CTAS 4
 #endif
@@ -730,9 +772,10 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
         const bool live = slot < p.q;
         const uint32_t row = live ? perm[slot] : 0;
         const int fam = live ? family_of_t<FMT>(p, row) : -1;
+        const uint64_t orow = p.out_by_slot ? slot : row;  // output index
         if (live && fam < 0) {  // FamilyMismatch -> no estimate
-            if (bucket_out) bucket_out[row] = -1;
-            if (bytes_out) bytes_out[row] = ~0ull;
+            if (bucket_out) bucket_out[orow] = -1;
+            if (bytes_out) bytes_out[orow] = ~0ull;
         }
         unsigned pending = __ballot_sync(0xffffffffu, fam >= 0);
         while (pending) {
@@ -753,7 +796,8 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
             int32_t pos = 0;
             {
                 if (mine) {
-                    const double2* rec = reinterpret_cast<const double2*>(p.qrec + static_cast<uint64_t>(row) * kQrec);
+                    const double2* rec =
+                        reinterpret_cast<const double2*>(p.qrec + (p.qrec_by_slot ? slot : static_cast<uint64_t>(row)) * kQrec);
 #pragma unroll
                     for (int h = 0; h < 9; ++h) {
                         const double2 v = __ldg(rec + h);
@@ -1006,8 +1050,8 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
                         best_votes = votes;
                     }
                 }
-                if (bucket_out) bucket_out[row] = best;
-                if (bytes_out) bytes_out[row] = (static_cast<uint64_t>(best) + 1ull) * m.bucket_range;
+                if (bucket_out) bucket_out[orow] = best;
+                if (bytes_out) bytes_out[orow] = (static_cast<uint64_t>(best) + 1ull) * m.bucket_range;
                 if (topk_d2 || topk_idx) {
 #pragma unroll
                     for (int a = 0; a < K; ++a) {
@@ -1223,7 +1267,7 @@ struct KnnHandle {
     cudaStream_t pipe[2] = {nullptr, nullptr};
     HostModel model[CARMA_FAMILIES];
     struct Scratch {
-        DeviceBuffer rows, family, qbin, qpos, perm, hist, tot, bucket, bytes, qrec, brute_d2, brute_id;
+        DeviceBuffer rows, family, qbin, qpos, perm, hist, tot, bucket, bytes, qrec, brute_d2, brute_id, sbucket, sbytes;
         PinnedBuffer stage_rows, stage_family, stage_packed;
         cudaEvent_t staged = nullptr;  // the H2D copy out of stage_packed is done
     } scratch[2];
@@ -1234,7 +1278,7 @@ struct KnnHandle {
     carma_bit_schema schema{};
     int path = 0;  // 0 auto (fp32 pre-filter when every model allows it), 1 exact fp64 blocks, 2 fp32 pre-filter
     uint64_t last_visits = 0;
-    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // pipeline start, search start, search end
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // pipeline start, search start / end, pipeline end
     bool timed = false;
     uint64_t last_launches = 0, last_evals = 0;
     std::mutex mu;
@@ -1397,11 +1441,28 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
             ++launches;
         }
         if (timed) CARMA_CUDA(cudaEventRecord(h.ev[2], s));
+        if (timed) CARMA_CUDA(cudaEventRecord(h.ev[3], s));
         return launches;
     }
     const bool f32 = use_f32(h);
+    // Layout of the fp32 path (KNN_LAYOUT; CARMA_KNN_LAYOUT overrides for
+    // A/B runs): 0 query records by row, written by knn_prep; 1 records by
+    // bucketed slot (knn_keys, bucketing, knn_prep_sorted), so each warp
+    // reads one contiguous span; 2 = 1 + bucket / bytes written by slot and
+    // un-permuted by knn_unpermute (the search's scattered 4-B / 8-B stores
+    // move to a streaming kernel). Measured on c2 (136-B rows): the search
+    // 11.87 / 11.73 / 11.67 ms, its DRAM 7.1 / ~5 / 3.3 GB, the whole
+    // pipeline 14.02 / 14.33 / 14.83 ms (knn_prep_sorted reads its rows at
+    // random), so 0 is the default. Writing the records at random slots from
+    // an in-order pass instead (fused into the scatter) took 4.7 ms.
+    static const int layout = [] {
+        const char* e = std::getenv("CARMA_KNN_LAYOUT");
+        return e ? std::atoi(e) : KNN_LAYOUT;
+    }();
+    const bool sorted = f32 && layout >= 1;
+    const bool sorted_out = sorted && layout == 2 && (bucket || bytes);
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
-    if (f32) {
+    if (f32 && !sorted) {
         uint64_t nkeys = 0;
         for (const auto& m : h.model)
             if (m.present) nkeys += m.n;
@@ -1441,18 +1502,49 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
         knn_keys<<<ctas, 512, shmem, s>>>(p, n_bins, sc.qbin.as<uint32_t>(), sc.qpos.as<uint32_t>(),
                                           sc.hist.as<uint32_t>());
     }
+    uint64_t extra = 0;
     sc.tot.ensure(n_bins * 4);
     bin_totals<<<(n_bins + 7) / 8, 256, 0, s>>>(sc.hist.as<uint32_t>(), n_bins, ctas, sc.tot.as<uint32_t>());
     scan_bins<<<1, 1024, 0, s>>>(sc.tot.as<uint32_t>(), n_bins);
     bin_offsets<<<(n_bins + 7) / 8, 256, 0, s>>>(sc.hist.as<uint32_t>(), n_bins, ctas, sc.tot.as<uint32_t>());
+    int32_t* sb = bucket;
+    uint64_t* sby = bytes;
     knn_scatter<<<ctas, 512, shmem, s>>>(q, n_bins, sc.qbin.as<uint32_t>(), sc.hist.as<uint32_t>(),
                                          sc.perm.as<uint32_t>());
+    if (sorted) {
+        sc.qrec.ensure(q * kQrec * sizeof(double));
+        p.qrec = sc.qrec.as<double>();
+        p.qrec_by_slot = 1;
+        const unsigned g = static_cast<unsigned>((q + 255) / 256);
+        const uint32_t* pm = sc.perm.as<uint32_t>();
+        const uint32_t* qp = sc.qpos.as<uint32_t>();
+        switch (format) {
+            case CARMA_ROWS_SCALAR: knn_prep_sorted<CARMA_ROWS_SCALAR><<<g, 256, 0, s>>>(p, pm, qp); break;
+            case CARMA_ROWS_PACKED: knn_prep_sorted<CARMA_ROWS_PACKED><<<g, 256, 0, s>>>(p, pm, qp); break;
+            case CARMA_ROWS_BITPACKED: knn_prep_sorted<CARMA_ROWS_BITPACKED><<<g, 256, 0, s>>>(p, pm, qp); break;
+            default: knn_prep_sorted<CARMA_ROWS_FEATURES><<<g, 256, 0, s>>>(p, pm, qp);
+        }
+        ++extra;
+        if (sorted_out) {
+            p.out_by_slot = 1;
+            sc.sbucket.ensure(q * 4);
+            sc.sbytes.ensure(q * 8);
+            sb = sc.sbucket.as<int32_t>();
+            sby = sc.sbytes.as<uint64_t>();
+        }
+    }
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[1], s));
-    launch_search(p, max_k(h), f32, sc.perm.as<uint32_t>(), sc.qpos.as<uint32_t>(), bucket, bytes, d2,
+    launch_search(p, max_k(h), f32, sc.perm.as<uint32_t>(), sc.qpos.as<uint32_t>(), sb, sby, d2,
                   idx, evals, s);
     if (timed) CARMA_CUDA(cudaEventRecord(h.ev[2], s));
+    if (sorted_out) {
+        knn_unpermute<<<static_cast<unsigned>((q + 255) / 256), 256, 0, s>>>(q, sc.perm.as<uint32_t>(), sb, sby,
+                                                                          bucket, bytes);
+        ++extra;
+    }
+    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[3], s));
     CARMA_CUDA(cudaGetLastError());
-    return 6;
+    return 6 + extra;
 }
 
 void check_ready(const KnnHandle* h) {
@@ -1617,7 +1709,7 @@ carma_status carma_knn_destroy(carma_knn* hh) {
             for (auto& sc : h->scratch) {
                 sc.rows.release(); sc.family.release(); sc.qbin.release(); sc.qpos.release();
                 sc.perm.release(); sc.hist.release(); sc.tot.release(); sc.bucket.release(); sc.bytes.release();
-                sc.brute_d2.release(); sc.brute_id.release();
+                sc.brute_d2.release(); sc.brute_id.release(); sc.sbucket.release(); sc.sbytes.release();
                 sc.stage_rows.release(); sc.stage_family.release(); sc.stage_packed.release();
                 if (sc.staged) cudaEventDestroy(sc.staged);
             }
@@ -1940,10 +2032,10 @@ carma_status carma_knn_last_timing(carma_knn* hh, double* search_ms, double* pip
         KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
         if (!h) throw InvalidArg("null handle");
         DeviceGuard g(h->device);
-        CARMA_CUDA(cudaEventSynchronize(h->ev[2]));
+        CARMA_CUDA(cudaEventSynchronize(h->ev[3]));
         float a = 0.f, b = 0.f;
         CARMA_CUDA(cudaEventElapsedTime(&a, h->ev[1], h->ev[2]));
-        CARMA_CUDA(cudaEventElapsedTime(&b, h->ev[0], h->ev[2]));
+        CARMA_CUDA(cudaEventElapsedTime(&b, h->ev[0], h->ev[3]));
         if (search_ms) *search_ms = a;
         if (pipeline_ms) *pipeline_ms = b;
     });
