@@ -341,7 +341,10 @@ carma_status carma_nn_last_timing(carma_nn* h, double* kernel_ms, double* call_m
 #define CARMA_MODE_MPS 1
 #define CARMA_MODE_MIG 2 /* replay: yes; carma_pick_batch: UNSUPPORTED (views carry no instances) */
 #define CARMA_NO_ESTIMATE UINT64_MAX
-#define CARMA_MAX_GPUS 64
+#define CARMA_MAX_GPUS 64 /* carma_pick_batch views per decision */
+/* Simulated GPUs per replay config: <= 64 run in the shared-memory tiers,
+ * 65..256 in a global-memory tier (GPU ids fit the packed 8-bit fields). */
+#define CARMA_MAX_REPLAY_GPUS 256
 
 #define CARMA_MAX_MIG 8
 

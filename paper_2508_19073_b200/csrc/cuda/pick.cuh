@@ -99,6 +99,73 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
                                          int& rr_cursor, int* out) {
     const int n = c.gpu_count;
     const bool rr_all = policy == CARMA_POLICY_RR && !c.rr_apply_preconditions;
+    if constexpr (GPL > 2) {
+        // > 64 GPUs (the replay's many-GPU tier: one decision per warp, GPU
+        // g = lane + 32 j): the eligibility set as one ballot word per j.
+        bool el[GPL];
+        unsigned mw[GPL];
+        uint32_t total = 0;
+#pragma unroll
+        for (int j = 0; j < GPL; ++j) {
+            bool e;
+            if (!in[j].valid) e = false;
+            else if (policy == CARMA_POLICY_EXCLUSIVE) e = in[j].idle;
+            else if (rr_all) e = in[j].inst_ok;
+            else e = in[j].inst_ok && !(in[j].smact > c.max_smact) && !(in[j].free_bytes < need_floor);
+            el[j] = e;
+            mw[j] = __ballot_sync(0xffffffffu, e);
+            total += static_cast<uint32_t>(__popc(mw[j]));
+        }
+        // first eligible id >= from (-1 when none)
+        auto next_from = [&](int from) {
+            int res = -1;
+#pragma unroll
+            for (int j = GPL - 1; j >= 0; --j) {
+                unsigned m = mw[j];
+                if (j < (from >> 5)) m = 0u;
+                else if (j == (from >> 5)) m &= ~0u << (from & 31);
+                if (m) res = j * 32 + __ffs(m) - 1;
+            }
+            return res;
+        };
+        out[0] = out[1] = -1;
+        const bool ok = total >= want;
+        const bool sorted = policy == CARMA_POLICY_MAGM || policy == CARMA_POLICY_LUG || policy == CARMA_POLICY_MUG;
+        if (sorted) {
+            if (!ok) return 0;
+            bool cand[GPL];
+#pragma unroll
+            for (int j = 0; j < GPL; ++j) cand[j] = el[j];
+            const int g0 = arg_best<GPL>(policy, in, cand, lane_in_group, width);
+            out[0] = g0;
+            if (want > 1) {
+#pragma unroll
+                for (int j = 0; j < GPL; ++j)
+                    if (static_cast<int>(lane_in_group + j * width) == g0) cand[j] = false;
+                out[1] = arg_best<GPL>(policy, in, cand, lane_in_group, width);
+            }
+            return static_cast<int>(want);
+        }
+        if (!ok) return 0;
+        if (policy == CARMA_POLICY_EXCLUSIVE) {
+            out[0] = next_from(0);
+            if (want > 1) out[1] = next_from(out[0] + 1);
+            return static_cast<int>(want);
+        }
+        // RR: cyclic scan from the cursor (manager.cpp:196-209)
+        int b0 = next_from(rr_cursor);
+        if (b0 < 0) b0 = next_from(0);
+        out[0] = b0;
+        int last = b0;
+        if (want > 1) {
+            int b1 = next_from(b0 + 1);
+            if (b1 < 0) b1 = next_from(0);
+            out[1] = b1;
+            last = b1;
+        }
+        rr_cursor = last + 1 == n ? 0 : last + 1;
+        return static_cast<int>(want);
+    }
     bool el[GPL];
     uint64_t mask = 0;
 #pragma unroll

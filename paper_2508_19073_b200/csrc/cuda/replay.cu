@@ -187,6 +187,9 @@ template <int F> using GlobalL = Layout<64, 8192, 2048, 256, 256, 4096, 4, F>;
 // 192 GiB device at 512 MiB blocks, or 40 GiB at 16 MiB) for plans that
 // hold such a config.
 template <int F> using GlobalWideL = Layout<64, 8192, 2048, 256, 256, 4096, replay::kMaxWords, F>;
+// Plans with more than 64 simulated GPUs: up to 256 GPUs (8 per lane) and
+// up to 4096 blocks per GPU, global memory.
+template <int F> using GlobalManyL = Layout<CARMA_MAX_REPLAY_GPUS, 8192, 2048, 256, 256, 4096, replay::kMaxWords, F>;
 constexpr int kGlobalBlocks = 64 * 4;
 
 // Configs whose policy can stack tasks without utilisation preconditions.
@@ -199,7 +202,7 @@ void validate_config(const carma_replay_config& c) {
     if (c.mode != CARMA_MODE_MPS && c.mode != CARMA_MODE_STREAMS && c.mode != CARMA_MODE_MIG)
         throw InvalidArg("unknown collocation mode");
     if (c.policy < CARMA_POLICY_EXCLUSIVE || c.policy > CARMA_POLICY_MUG) throw InvalidArg("unknown policy");
-    if (c.gpu_count < 1 || c.gpu_count > CARMA_MAX_GPUS) throw Unsupported("gpu_count must be in [1, 64]");
+    if (c.gpu_count < 1 || c.gpu_count > CARMA_MAX_REPLAY_GPUS) throw Unsupported("gpu_count must be in [1, 256]");
     if (!(c.monitor_window > 0.0)) throw InvalidArg("ConfigError: window must be > 0");
     if (c.alloc_block == 0) throw Unsupported("alloc_block = 0 is not supported");
     if (c.gpu_capacity % c.alloc_block != 0)
@@ -274,6 +277,7 @@ void launch_tier(ReplayPlan& pl, const replay::Params& base, const uint32_t* lis
         if (tier == 1) return launch_shared<HeavyL, F>(pl, p, max_g, sms);
     }
     if (tier == 3) launch<LargeL<F>, true>(pl, p, sms, 1);
+    else if (pl.max_g > 64) launch<GlobalManyL<F>, false>(pl, p, sms);
     else if (pl.max_blocks > kGlobalBlocks) launch<GlobalWideL<F>, false>(pl, p, sms);
     else launch<GlobalL<F>, false>(pl, p, sms);
 }
@@ -318,7 +322,7 @@ bool run_group(ReplayPlan& pl, const replay::Params& p, uint32_t off0) {
     for (int round = 0; round < 3 && total > 0; ++round) {
         if (round > 0) pl.retried += total;
         CARMA_CUDA(cudaMemcpy(list, ids.data(), total * 4, cudaMemcpyHostToDevice));
-        const bool large_ok = round == 0 && pl.max_blocks <= 128;
+        const bool large_ok = round == 0 && pl.max_blocks <= 128 && pl.max_g <= 64;
         launch_tier<F>(pl, p, list, total, large_ok ? 3 : 2, pl.max_g, counters, retry);
         uint32_t nr = 0;
         CARMA_CUDA(cudaMemcpyAsync(&nr, counters + 1, 4, cudaMemcpyDeviceToHost, pl.stream));
@@ -454,7 +458,7 @@ void build_plan(int device, const carma_replay_config* configs, uint32_t n_confi
                     // jobs are global-only (large and global tiers)
                     const int feat = (c.mode == CARMA_MODE_MIG ? 1 : 0) |
                                      ((c.sample_interval > 0.0 || c.log_flags != 0) ? 2 : 0);
-                    const int tier = (c.gpu_capacity / c.alloc_block > 128 || (feat & 2)) ? 2
+                    const int tier = (c.gpu_capacity / c.alloc_block > 128 || (feat & 2) || c.gpu_count > 64) ? 2
                                                                                            : static_cast<int>(heavy_config(c));
                     const int jc = tier + 3 * feat;
                     if (jc != cls) continue;

@@ -932,11 +932,17 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
             in[j].inst_ok = inst[j] >= 0;
         }
     }
-    if constexpr (L::GPL == 2) {
-        double s0 = 0.0, s1 = 0.0;
-        if (need_smact && in[0].valid) windowed2<L>(b, lane, lane + 32, in[1].valid, c.now, c.window, s0, s1);
-        in[0].smact = s0;
-        in[1].smact = s1;
+    if constexpr (L::GPL >= 2) {  // the lane's GPUs in pairs: two independent chains per step
+#pragma unroll
+        for (int j = 0; j < L::GPL; j += 2) {
+            double s0 = 0.0, s1 = 0.0;
+            const bool v1 = j + 1 < L::GPL && in[j + 1 < L::GPL ? j + 1 : j].valid;
+            if (need_smact && in[j].valid)
+                windowed2<L>(b, static_cast<int>(lane) + 32 * j, static_cast<int>(lane) + 32 * (j + 1), v1, c.now,
+                             c.window, s0, s1);
+            in[j].smact = s0;
+            if (j + 1 < L::GPL) in[j + 1].smact = s1;
+        }
     }
     int gids[2];
     const int got = pick_gpus<L::GPL>(cf, policy, tasks[head].gpus, floor, in, lane, 0, 32, c.rr_cursor, gids);

@@ -92,6 +92,26 @@ def test_replay_large_trace_many_gpus(gpu, olib):
     assert not np.array_equal(m.tasks["rank"], np.arange(4000))
 
 
+@pytest.mark.parametrize("gpus", [65, 100, 128, 256])
+def test_replay_more_than_64_gpus(gpu, olib, gpus):
+    """65..256 simulated GPUs run in the many-GPU global tier (8 GPUs per
+    lane, multi-word eligibility sets): every policy, 1- and 2-GPU tasks,
+    bit-exact against the oracle (pinned to the reference beyond 64 GPUs in
+    test_oracle_vs_ref.py)."""
+    tr = cb.generate_uniform_trace(3000, 0.2, 13)
+    m = cb.materialize_trace(tr)
+    cb.set_persona_estimates(m, "oracle")
+    assert (m.tasks["gpus"] == 2).any()
+    cfgs = np.concatenate([cfg_of(p, gpu_count=gpus, window=5.0, rr_pre=pre)
+                           for p, pre in (("magm", False), ("lug", False), ("mug", False), ("rr", False),
+                                          ("rr", True), ("exclusive", False))])
+    jobs = [(0, c) for c in range(len(cfgs))]
+    res = cb.replay(cfgs, [m.tasks], jobs)
+    check_jobs(olib, res, cfgs, [m.tasks], jobs)
+    used = set(res.job_tasks(0)["gpu"][:, 0].tolist())
+    assert max(used) >= 64, "the trace must reach GPUs past 63"
+
+
 def test_replay_overflow_tier_escalation(gpu, olib):
     """RR without preconditions on 80 GiB GPUs stacks > 24 residents per GPU:
     the shared-memory tier overflows and the job re-runs in the global tier."""

@@ -198,3 +198,22 @@ def test_snapshot_errors_follow_the_reference():
         cb.parse_snapshot(bad.replace(b'"cnn"', b'"rnn"'))
     with pytest.raises(abi.CarmaError, match="malformed"):
         cb.parse_snapshot(b'{"schema": "carma-knn-estimator/v1", ')
+
+
+@pytest.mark.parametrize("gpus,policy", [(128, "magm"), (256, "lug"), (100, "rr")])
+def test_oracle_many_gpus_matches_reference(ref, olib, tmp_path, gpus, policy):
+    """Pins the oracle beyond 64 simulated GPUs (the GPU's many-GPU tier is
+    checked against it in tests/test_gpu_replay.py)."""
+    tr = cb.generate_uniform_trace(1500, 0.3, 9)
+    path = str(tmp_path / "many.trace")
+    cb.save_trace(tr, path)
+    cfg = ref_config(policy=policy, estimator="oracle", gpu_count=gpus, window=5.0)
+    tout, rout, ge, gs, gp = ref_run(ref, cfg, path=path)
+    m = cb.materialize_trace(cb.load_trace(path))
+    cb.set_persona_estimates(m, "oracle")
+    rc, ot, otr, og = oracle_replay(olib, replay_config_from(cfg), m.tasks)
+    assert rc == 0
+    assert np.array_equal(ot["complete"], tout["complete"]) and np.array_equal(ot["ooms"], tout["ooms"])
+    assert np.array_equal(ot["gpu"][:, 0], tout["gpu0"])
+    assert otr["energy_mj"] == rout["energy_mj"] and otr["avg_jct"] == rout["avg_jct"]
+    assert np.array_equal(og["mean_smact"], gs)
