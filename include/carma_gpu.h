@@ -345,6 +345,8 @@ carma_status carma_nn_last_timing(carma_nn* h, double* kernel_ms, double* call_m
 /* Simulated GPUs per replay config: <= 64 run in the shared-memory tiers,
  * 65..256 in a global-memory tier (GPU ids fit the packed 8-bit fields). */
 #define CARMA_MAX_REPLAY_GPUS 256
+/* GPUs one task may request (TaskSpec::gpus_requested) in the replay. */
+#define CARMA_MAX_TASK_GPUS 8
 
 #define CARMA_MAX_MIG 8
 

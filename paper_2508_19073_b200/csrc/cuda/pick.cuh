@@ -131,38 +131,38 @@ __device__ __forceinline__ int pick_gpus(const carma_replay_config& c, int polic
         out[0] = out[1] = -1;
         const bool ok = total >= want;
         const bool sorted = policy == CARMA_POLICY_MAGM || policy == CARMA_POLICY_LUG || policy == CARMA_POLICY_MUG;
-        if (sorted) {
-            if (!ok) return 0;
+        if (!ok) return 0;
+        // want <= CARMA_MAX_TASK_GPUS devices (the many-GPU tier's multi-GPU tasks)
+        if (sorted) {  // stable sort by key then id == repeated arg-best
             bool cand[GPL];
 #pragma unroll
             for (int j = 0; j < GPL; ++j) cand[j] = el[j];
-            const int g0 = arg_best<GPL>(policy, in, cand, lane_in_group, width);
-            out[0] = g0;
-            if (want > 1) {
+            for (uint32_t r = 0; r < want; ++r) {
+                const int g = arg_best<GPL>(policy, in, cand, lane_in_group, width);
+                out[r] = g;
 #pragma unroll
                 for (int j = 0; j < GPL; ++j)
-                    if (static_cast<int>(lane_in_group + j * width) == g0) cand[j] = false;
-                out[1] = arg_best<GPL>(policy, in, cand, lane_in_group, width);
+                    if (static_cast<int>(lane_in_group + j * width) == g) cand[j] = false;
             }
             return static_cast<int>(want);
         }
-        if (!ok) return 0;
-        if (policy == CARMA_POLICY_EXCLUSIVE) {
-            out[0] = next_from(0);
-            if (want > 1) out[1] = next_from(out[0] + 1);
+        if (policy == CARMA_POLICY_EXCLUSIVE) {  // the first idle devices in id order
+            int bgn = 0;
+            for (uint32_t r = 0; r < want; ++r) {
+                out[r] = next_from(bgn);
+                bgn = out[r] + 1;
+            }
             return static_cast<int>(want);
         }
         // RR: cyclic scan from the cursor (manager.cpp:196-209)
-        int b0 = next_from(rr_cursor);
-        if (b0 < 0) b0 = next_from(0);
-        out[0] = b0;
-        int last = b0;
-        if (want > 1) {
-            int b1 = next_from(b0 + 1);
-            if (b1 < 0) b1 = next_from(0);
-            out[1] = b1;
-            last = b1;
+        int from = rr_cursor;
+        for (uint32_t r = 0; r < want; ++r) {
+            int g = next_from(from);
+            if (g < 0) g = next_from(0);
+            out[r] = g;
+            from = g + 1;
         }
+        const int last = out[want - 1];
         rr_cursor = last + 1 == n ? 0 : last + 1;
         return static_cast<int>(want);
     }

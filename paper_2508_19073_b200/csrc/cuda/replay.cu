@@ -152,9 +152,12 @@ struct ReplayPlan {
     uint64_t n_tasks = 0, n_task_out = 0, n_gpu_out = 0;
     int max_g = 1;
     int max_blocks = 1;
-    // classes 3F + {light, heavy, global-only} for feature bits F (1 = MIG, 2 = timeline)
-    uint32_t class_count[12] = {};
-    int class_max_g[12] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+    // classes 3F + {light, heavy, global-only} for feature bits F (1 = MIG, 2 = timeline,
+    // 4 = tasks requesting more than 2 GPUs)
+    static constexpr int kClasses = 24;
+    uint32_t class_count[kClasses] = {};
+    int class_max_g[kClasses] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+    std::vector<uint32_t> trace_max_gpus;  // max gpus_requested per trace (host-built plans)
     std::vector<uint32_t> class_list;  // jobs ordered by class
     DeviceBuffer d_cfgs, d_tasks, d_trace_off, d_jobs, d_task_off, d_gpu_off, d_list, d_task_out,
         d_trace_out, d_gpu_out, d_inv, d_begin, d_counters, d_gstate, d_outcomes, d_tl, d_tl_count, d_log,
@@ -192,6 +195,12 @@ template <int F> using GlobalWideL = Layout<64, 8192, 2048, 256, 256, 4096, repl
 template <int F> using GlobalManyL = Layout<CARMA_MAX_REPLAY_GPUS, 8192, 2048, 256, 256, 4096, replay::kMaxWords, F>;
 constexpr int kGlobalBlocks = 64 * 4;
 
+// Configs the block bitmap cannot represent (GpuDevice is byte-granular).
+bool needs_segments(const carma_replay_config& c) {
+    return c.alloc_block == 0 || c.gpu_capacity % c.alloc_block != 0 ||
+           c.gpu_capacity / c.alloc_block > 64ull * replay::kMaxWords;
+}
+
 // Configs whose policy can stack tasks without utilisation preconditions.
 bool heavy_config(const carma_replay_config& c) {
     return (c.policy == CARMA_POLICY_RR && !c.rr_apply_preconditions) || c.max_smact >= 1.0 ||
@@ -204,11 +213,11 @@ void validate_config(const carma_replay_config& c) {
     if (c.policy < CARMA_POLICY_EXCLUSIVE || c.policy > CARMA_POLICY_MUG) throw InvalidArg("unknown policy");
     if (c.gpu_count < 1 || c.gpu_count > CARMA_MAX_REPLAY_GPUS) throw Unsupported("gpu_count must be in [1, 256]");
     if (!(c.monitor_window > 0.0)) throw InvalidArg("ConfigError: window must be > 0");
-    if (c.alloc_block == 0) throw Unsupported("alloc_block = 0 is not supported");
-    if (c.gpu_capacity % c.alloc_block != 0)
-        throw Unsupported("gpu_capacity must be a multiple of alloc_block");
-    if (c.gpu_capacity / c.alloc_block > 64ull * replay::kMaxWords)
-        throw Unsupported("more than 4096 allocation blocks per GPU");
+    // alloc_block = 0, capacities that are not a block multiple and more than
+    // 4096 blocks run on the byte-granular segment allocator of the generic
+    // instantiations (needs_segments); MIG instance tables stay block-based.
+    if (c.mode == CARMA_MODE_MIG && needs_segments(c))
+        throw Unsupported("MIG needs alloc_block > 0, a block-multiple capacity and <= 4096 blocks");
     if (!(c.sample_interval >= 0.0)) throw InvalidArg("ConfigError: sample_interval must be >= 0");
     if (c.log_flags & ~(CARMA_LOG_EVENTS | CARMA_LOG_DECISIONS)) throw InvalidArg("unknown log_flags bits");
     if (c.mode == CARMA_MODE_MIG) {
@@ -272,14 +281,21 @@ void launch_tier(ReplayPlan& pl, const replay::Params& base, const uint32_t* lis
     CARMA_CUDA(cudaMemsetAsync(counters, 0, 8, pl.stream));
     int sms = 148;
     CARMA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl.device));
-    if constexpr ((F & 2) == 0) {
-        if (tier == 0) return launch_shared<LightL, F>(pl, p, max_g, sms);
-        if (tier == 1) return launch_shared<HeavyL, F>(pl, p, max_g, sms);
+    if constexpr ((F & 4) != 0) {
+        // multi-GPU tasks: the many-GPU global tier only (up to 8 GPUs per task)
+        (void)tier;
+        (void)max_g;
+        launch<GlobalManyL<F>, false>(pl, p, sms);
+    } else {
+        if constexpr ((F & 2) == 0) {
+            if (tier == 0) return launch_shared<LightL, F>(pl, p, max_g, sms);
+            if (tier == 1) return launch_shared<HeavyL, F>(pl, p, max_g, sms);
+        }
+        if (tier == 3) launch<LargeL<F>, true>(pl, p, sms, 1);
+        else if (pl.max_g > 64) launch<GlobalManyL<F>, false>(pl, p, sms);
+        else if (pl.max_blocks > kGlobalBlocks) launch<GlobalWideL<F>, false>(pl, p, sms);
+        else launch<GlobalL<F>, false>(pl, p, sms);
     }
-    if (tier == 3) launch<LargeL<F>, true>(pl, p, sms, 1);
-    else if (pl.max_g > 64) launch<GlobalManyL<F>, false>(pl, p, sms);
-    else if (pl.max_blocks > kGlobalBlocks) launch<GlobalWideL<F>, false>(pl, p, sms);
-    else launch<GlobalL<F>, false>(pl, p, sms);
 }
 
 // One collocation group (classes cb..cb+2, jobs list[off0, ...)): the two
@@ -322,7 +338,7 @@ bool run_group(ReplayPlan& pl, const replay::Params& p, uint32_t off0) {
     for (int round = 0; round < 3 && total > 0; ++round) {
         if (round > 0) pl.retried += total;
         CARMA_CUDA(cudaMemcpy(list, ids.data(), total * 4, cudaMemcpyHostToDevice));
-        const bool large_ok = round == 0 && pl.max_blocks <= 128 && pl.max_g <= 64;
+        const bool large_ok = round == 0 && pl.max_blocks <= 128 && pl.max_g <= 64 && (F & 4) == 0;
         launch_tier<F>(pl, p, list, total, large_ok ? 3 : 2, pl.max_g, counters, retry);
         uint32_t nr = 0;
         CARMA_CUDA(cudaMemcpyAsync(&nr, counters + 1, 4, cudaMemcpyDeviceToHost, pl.stream));
@@ -358,10 +374,10 @@ void run_plan(ReplayPlan& pl) {
     pl.launches = 0;
     pl.retried = 0;
     CARMA_CUDA(cudaMemsetAsync(pl.d_begin.ptr, 0xff, n * sizeof(double), pl.stream));  // NaN: derive
-    CARMA_CUDA(cudaMemsetAsync(pl.d_counters.ptr, 0, 128, pl.stream));
+    CARMA_CUDA(cudaMemsetAsync(pl.d_counters.ptr, 0, 512, pl.stream));
     CARMA_CUDA(cudaEventRecord(pl.ev[0], pl.stream));
-    uint32_t off[4];
-    for (int f = 0, o = 0; f < 4; ++f) {
+    uint32_t off[8];
+    for (int f = 0, o = 0; f < 8; ++f) {
         off[f] = static_cast<uint32_t>(o);
         o += pl.class_count[3 * f] + pl.class_count[3 * f + 1] + pl.class_count[3 * f + 2];
     }
@@ -370,7 +386,7 @@ void run_plan(ReplayPlan& pl) {
     if (count(0)) dirty |= run_group<0>(pl, p, off[0]);
     else CARMA_CUDA(cudaEventRecord(pl.ev[1], pl.stream));
     if (count(1)) dirty |= run_group<1>(pl, p, off[1]);
-    if (count(2) || count(3)) {
+    if (count(2) || count(3) || count(6) || count(7)) {
         for (const auto& jb : pl.jobs) {
             const carma_replay_config& c = pl.cfgs[jb.config];
             if (c.sample_interval > 0.0 && pl.tl_cap == 0)
@@ -380,7 +396,11 @@ void run_plan(ReplayPlan& pl) {
         }
         if (count(2)) dirty |= run_group<2>(pl, p, off[2]);
         if (count(3)) dirty |= run_group<3>(pl, p, off[3]);
+        if (count(6)) dirty |= run_group<6>(pl, p, off[6]);
+        if (count(7)) dirty |= run_group<7>(pl, p, off[7]);
     }
+    if (count(4)) dirty |= run_group<4>(pl, p, off[4]);
+    if (count(5)) dirty |= run_group<5>(pl, p, off[5]);
     CARMA_CUDA(cudaEventRecord(pl.ev[2], pl.stream));
     if (dirty) CARMA_CUDA(cudaMemcpy(pl.d_list.ptr, pl.class_list.data(), n * 4, cudaMemcpyHostToDevice));
 }
@@ -410,14 +430,20 @@ void build_plan(int device, const carma_replay_config* configs, uint32_t n_confi
             for (const auto& c : pl->cfgs) {
                 validate_config(c);
                 pl->max_g = std::max(pl->max_g, c.gpu_count);
-                pl->max_blocks = std::max(pl->max_blocks, static_cast<int>(c.gpu_capacity / c.alloc_block));
+                if (!needs_segments(c))
+                    pl->max_blocks = std::max(pl->max_blocks, static_cast<int>(c.gpu_capacity / c.alloc_block));
             }
             for (uint32_t t = 0; t < n_traces; ++t) {
                 if (trace_offsets[t + 1] <= trace_offsets[t]) throw InvalidArg("ConfigError: trace contains no tasks");
                 if (trace_offsets[t + 1] - trace_offsets[t] > (1u << 30)) throw Unsupported("trace too long");
             }
+            pl->trace_max_gpus.assign(n_traces, 1);
+            for (uint32_t t = 0; tasks && t < n_traces; ++t)
+                for (uint64_t i = trace_offsets[t]; i < trace_offsets[t + 1]; ++i)
+                    pl->trace_max_gpus[t] = std::max(pl->trace_max_gpus[t], tasks[i].gpus);
             for (uint64_t i = 0; tasks && i < pl->n_tasks; ++i) {
-                if (tasks[i].gpus < 1 || tasks[i].gpus > 2) throw Unsupported("gpus_requested must be 1 or 2");
+                if (tasks[i].gpus < 1 || tasks[i].gpus > CARMA_MAX_TASK_GPUS)
+                    throw Unsupported("gpus_requested must be in [1, 8]");
                 if (i > 0 && tasks[i].submit < tasks[i - 1].submit) {
                     // arrivals must be non-decreasing within a trace (load_trace_file)
                     bool boundary = false;
@@ -450,15 +476,16 @@ void build_plan(int device, const carma_replay_config* configs, uint32_t n_confi
             up(pl->d_task_off, task_off.data(), n_jobs * sizeof(uint64_t));
             up(pl->d_gpu_off, gpu_off.data(), n_jobs * sizeof(uint64_t));
             std::vector<uint32_t> list(2 * static_cast<size_t>(n_jobs));
-            for (int cls = 0; cls < 12; ++cls)
+            for (int cls = 0; cls < ReplayPlan::kClasses; ++cls)
                 for (uint32_t i = 0; i < n_jobs; ++i) {
                     const carma_replay_config& c = configs[jobs[i].config];
                     // > 128 allocation blocks: the shared-memory layouts hold 2 bitmap words;
                     // MIG / timeline jobs form classes 3F.. (their own kernels); timeline
                     // jobs are global-only (large and global tiers)
                     const int feat = (c.mode == CARMA_MODE_MIG ? 1 : 0) |
-                                     ((c.sample_interval > 0.0 || c.log_flags != 0) ? 2 : 0);
-                    const int tier = (c.gpu_capacity / c.alloc_block > 128 || (feat & 2) || c.gpu_count > 64) ? 2
+                                     ((c.sample_interval > 0.0 || c.log_flags != 0) ? 2 : 0) |
+                                     ((pl->trace_max_gpus[jobs[i].trace] > 2 || needs_segments(c)) ? 4 : 0);
+                    const int tier = ((feat & 6) || c.gpu_count > 64 || c.gpu_capacity / c.alloc_block > 128) ? 2
                                                                                            : static_cast<int>(heavy_config(c));
                     const int jc = tier + 3 * feat;
                     if (jc != cls) continue;
@@ -473,7 +500,7 @@ void build_plan(int device, const carma_replay_config* configs, uint32_t n_confi
             pl->d_gpu_out.ensure(go * sizeof(carma_gpu_result));
             pl->d_inv.ensure(to * 4);
             pl->d_begin.ensure(n_jobs * sizeof(double));
-            pl->d_counters.ensure(128);
+            pl->d_counters.ensure(512);
             pl->d_tl_count.ensure(n_jobs * sizeof(uint64_t));
             pl->d_log_count.ensure(n_jobs * sizeof(uint64_t));
         } catch (...) {

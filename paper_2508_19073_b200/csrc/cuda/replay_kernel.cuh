@@ -107,10 +107,12 @@ struct Params {
     uint64_t* log_count;         // records produced, per job
 };
 
-// alloc_oom details of a failed placement (OomFailure, gpu.hpp:26-35), in blocks.
+// alloc_oom details of a failed placement (OomFailure, gpu.hpp:26-35), in
+// blocks (bitmap allocator) or bytes (segment allocator: *_b).
 struct OomInfo {
     int gpu;
     uint32_t free_blk, largest_blk;
+    uint64_t free_b, largest_b;
 };
 
 // Compile-time state layout: G GPUs, H heap entries, S slots, RC residents
@@ -125,6 +127,16 @@ struct Layout {
     // Event queue: a sorted ring (O(1) pop, warp-parallel insert) for the
     // long-trace tiers, a 4-ary heap for the short-trace tiers.
     static constexpr bool SQ = H_ >= 1024;
+    // F bit 4: tasks may request up to 8 GPUs (multi-GPU jobs run in their
+    // own global-tier instantiations); the slot keeps its full GPU list.
+    // The generic instantiations (F bit 4) also carry the reference's
+    // byte-granular segment allocator (gpu.cpp:58-130), chosen per config at
+    // run time for alloc_block = 0, capacities that are not a block multiple
+    // and more than 4096 blocks.
+    static constexpr bool MG = (F_ & 4) != 0;
+    static constexpr int WM = MG ? CARMA_MAX_TASK_GPUS : 2;
+    static constexpr size_t MGI = MG ? 1 : 0;
+    static constexpr int NSEG = 2 * RC_ + 2;  // segments per GPU: <= 2 x live allocations + 1
     static constexpr size_t MI = MIG ? 1 : 0;
     static constexpr int GPL = (G + 31) / 32;
     static constexpr size_t al8(size_t x) { return (x + 15) / 16 * 16; }
@@ -147,9 +159,9 @@ struct Layout {
     static constexpr size_t s_last = s_rate + 8ull * S;
     static constexpr size_t s_exec = s_last + 8ull * S;
     static constexpr size_t s_dem = s_exec + 8ull * S;
-    static constexpr size_t aff = s_dem + 8ull * S;                    // u64 [2 RC] x 2
-    static constexpr size_t aff2 = aff + 16ull * RC;
-    static constexpr size_t nres = aff2 + 16ull * RC;                  // u32 [G] x 7
+    static constexpr size_t aff = s_dem + 8ull * S;                    // u64 [WM RC] x 2
+    static constexpr size_t aff2 = aff + 8ull * WM * RC;
+    static constexpr size_t nres = aff2 + 8ull * WM * RC;              // u32 [G] x 7
     static constexpr size_t nsteps = nres + 4ull * G;
     static constexpr size_t rhead = nsteps + 4ull * G;
     static constexpr size_t rcnt = rhead + 4ull * G;
@@ -163,7 +175,17 @@ struct Layout {
     static constexpr size_t s_off = s_gp + 4ull * S;
     static constexpr size_t s_nb = s_off + 4ull * S;
     static constexpr size_t s_inst = s_nb + 4ull * S;                  // MIG: inst0 | inst1 << 8
-    static constexpr size_t free_stack = s_inst + 4ull * S * MI;       // u32 [S]
+    static constexpr size_t s_gl = s_inst + 4ull * S * MI;             // MG: u8 [S][WM] GPU ids
+    static constexpr size_t s_il = s_gl + 1ull * S * WM * MGI;         // MG + MIG: u8 [S][WM] instances
+    static constexpr size_t s_ol = al8(s_il + 1ull * S * WM * MGI * MI);  // MG: u16 [S][WM] block offsets
+    static constexpr size_t s_ob = al8(s_ol + 2ull * S * WM * MGI);   // MG: u64 [S][WM] byte offsets (segments)
+    static constexpr size_t s_wb = s_ob + 8ull * S * WM * MGI;        // MG: u64 [S] bytes per device (segments)
+    static constexpr size_t seg_off = s_wb + 8ull * S * MGI;          // MG: u64 [G][NSEG] segment offsets
+    static constexpr size_t seg_len = seg_off + 8ull * G * NSEG * MGI;  // u64 [G][NSEG] size | used << 63
+    static constexpr size_t seg_n = seg_len + 8ull * G * NSEG * MGI;    // u32 [G]
+    static constexpr size_t seg_free = al8(seg_n + 4ull * G * MGI);   // u64 [G] total free bytes
+    static constexpr size_t seg_peak = seg_free + 8ull * G * MGI;     // u64 [G] peak used bytes
+    static constexpr size_t free_stack = al8(seg_peak + 8ull * G * MGI);  // u32 [S]
     static constexpr size_t rq = free_stack + 4ull * S;                // u32 [RQ]
     static constexpr size_t res = rq + 4ull * RQ;                      // u16 [G][RC]
     static constexpr size_t ptrs = al8(res + 2ull * G * RC);          // tasks, out, est, nblk (warp-uniform)
@@ -427,6 +449,112 @@ __device__ __forceinline__ int first_fit(char* b, int g, int nblk, int want, int
     return -1;
 }
 
+// ------------------------------------------------ segment allocator (bytes)
+// GpuDevice's segment list (gpu.cpp:58-130) for the generic instantiations:
+// segments in address order, size | used << 63. Owner lane only.
+constexpr uint64_t kSegUsed = 1ull << 63;
+
+template <class L>
+__device__ __forceinline__ void seg_init(char* b, int g, uint64_t capacity) {
+    RP_U64(seg_off)[g * L::NSEG] = 0;
+    RP_U64(seg_len)[g * L::NSEG] = capacity;
+    RP_U32(seg_n)[g] = 1;
+    RP_U64(seg_free)[g] = capacity;
+    RP_U64(seg_peak)[g] = 0;
+}
+
+// allocate_range(r0, r1, want) with want already rounded (gpu.cpp:72-114):
+// first fit over the free segments clipped to the range, carved from the end
+// facing away from a live neighbour. Returns false (with the range's free
+// and largest free bytes) on failure, or when the list would overflow (*ovf).
+template <class L>
+__device__ __forceinline__ bool seg_alloc(char* b, int g, uint64_t capacity, uint64_t r0, uint64_t r1, uint64_t want,
+                                          uint64_t& off, uint64_t& tot_free, uint64_t& largest, bool& ovf) {
+    uint64_t* so = RP_U64(seg_off) + g * L::NSEG;
+    uint64_t* sl = RP_U64(seg_len) + g * L::NSEG;
+    const uint32_t n = RP_U32(seg_n)[g];
+    tot_free = largest = 0;
+    ovf = false;
+#pragma unroll 1
+    for (uint32_t i = 0; i < n; ++i) {
+        const uint64_t len = sl[i];
+        if (len & kSegUsed) continue;
+        const uint64_t lo = so[i] > r0 ? so[i] : r0;
+        const uint64_t end = so[i] + len;
+        const uint64_t hi = end < r1 ? end : r1;
+        if (lo >= hi) continue;
+        const uint64_t avail = hi - lo;
+        tot_free += avail;
+        if (avail > largest) largest = avail;
+        if (avail < want) continue;
+        const bool left_used = i > 0 && (sl[i - 1] & kSegUsed) && so[i] == lo;
+        const bool right_used = i + 1 < n && (sl[i + 1] & kSegUsed) && end == hi;
+        const uint64_t place = (left_used && !right_used) ? hi - want : lo;
+        const uint32_t k = (place > so[i] ? 1u : 0u) + 1u + (place + want < end ? 1u : 0u);
+        if (n + k - 1 > static_cast<uint32_t>(L::NSEG)) {
+            ovf = true;
+            return false;
+        }
+        // shift [i + 1, n) up by k - 1, then write the replacement at i
+#pragma unroll 1
+        for (uint32_t x = n; x-- > i + 1;) {
+            so[x + k - 1] = so[x];
+            sl[x + k - 1] = sl[x];
+        }
+        const uint64_t base = so[i];
+        uint32_t w = i;
+        if (place > base) {
+            so[w] = base;
+            sl[w++] = place - base;
+        }
+        so[w] = place;
+        sl[w++] = want | kSegUsed;
+        if (place + want < end) {
+            so[w] = place + want;
+            sl[w] = end - place - want;
+        }
+        RP_U32(seg_n)[g] = n + k - 1;
+        const uint64_t fr = RP_U64(seg_free)[g] - want;
+        RP_U64(seg_free)[g] = fr;
+        if (capacity - fr > RP_U64(seg_peak)[g]) RP_U64(seg_peak)[g] = capacity - fr;
+        off = place;
+        return true;
+    }
+    return false;
+}
+
+// free_region (gpu.cpp:116-130): mark free, coalesce right then left.
+template <class L>
+__device__ __forceinline__ void seg_release(char* b, int g, uint64_t off, uint64_t size) {
+    uint64_t* so = RP_U64(seg_off) + g * L::NSEG;
+    uint64_t* sl = RP_U64(seg_len) + g * L::NSEG;
+    uint32_t n = RP_U32(seg_n)[g];
+    uint32_t i = 0;
+    while (i < n && !(so[i] == off && sl[i] == (size | kSegUsed))) ++i;
+    if (i == n) return;
+    sl[i] = size;
+    RP_U64(seg_free)[g] += size;
+    if (i + 1 < n && !(sl[i + 1] & kSegUsed)) {
+        sl[i] += sl[i + 1];
+#pragma unroll 1
+        for (uint32_t x = i + 1; x + 1 < n; ++x) {
+            so[x] = so[x + 1];
+            sl[x] = sl[x + 1];
+        }
+        --n;
+    }
+    if (i > 0 && !(sl[i - 1] & kSegUsed)) {
+        sl[i - 1] += sl[i];
+#pragma unroll 1
+        for (uint32_t x = i; x + 1 < n; ++x) {
+            so[x] = so[x + 1];
+            sl[x] = sl[x + 1];
+        }
+        --n;
+    }
+    RP_U32(seg_n)[g] = n;
+}
+
 // Free blocks in [r0, r1) (GpuDevice::instance_free, gpu.cpp:151-160).
 template <class L>
 __device__ __forceinline__ uint32_t free_in_range(const uint64_t* used, int g, int r0, int r1) {
@@ -468,6 +596,15 @@ __device__ __forceinline__ void range_stats(char* b, int g, int nblk, int r0, in
 // MIG instance of slot on GPU g (the slot's first or second device).
 template <class L>
 __device__ __forceinline__ int inst_of(const char* b, uint32_t slot, int g) {
+    if constexpr (L::MG) {
+        const uint8_t* gl = reinterpret_cast<const uint8_t*>(b + L::s_gl) + slot * L::WM;
+        const uint8_t* il = reinterpret_cast<const uint8_t*>(b + L::s_il) + slot * L::WM;
+        const int want = static_cast<int>(reinterpret_cast<const uint32_t*>(b + L::s_gp)[slot] >> 16);
+        int r = 0;
+        for (int k = 0; k < want; ++k)
+            if (gl[k] == g) r = il[k];
+        return r;
+    }
     const uint32_t gp = reinterpret_cast<const uint32_t*>(b + L::s_gp)[slot];
     const uint32_t in = reinterpret_cast<const uint32_t*>(b + L::s_inst)[slot];
     return static_cast<int>(((gp & 0xff) == static_cast<uint32_t>(g) ? in : (in >> 8)) & 0xff);
@@ -650,14 +787,24 @@ __device__ __forceinline__ bool refresh_gpu(char* b, int g, double now, double w
     return true;
 }
 
-// World::refresh_rates (world.cpp:157-186) for touched GPUs t0 (, t1).
+// World::refresh_rates (world.cpp:157-186) for the touched GPUs tg[0, nt).
 template <class L>
-__device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, int nt, unsigned lane) {
+__device__ __forceinline__ void refresh_rates(char* b, Sc& c, const int (&tg)[L::WM], int nt, unsigned lane) {
+    const int t0 = tg[0], t1 = tg[1];
     bool ok = true;
+    if constexpr (L::MG) {
+#pragma unroll
+        for (int k = 0; k < L::WM; ++k) {
+            if (k >= nt) break;
+            const int g = tg[k];
+            if ((g & 31) == static_cast<int>(lane)) ok = refresh_gpu<L>(b, g, c.now, c.window, c.begin0) && ok;
+        }
+    } else {
 #pragma unroll 1
-    for (int k = 0; k < nt; ++k) {
-        const int g = k == 0 ? t0 : t1;
-        if ((g & 31) == static_cast<int>(lane)) ok = refresh_gpu<L>(b, g, c.now, c.window, c.begin0) && ok;
+        for (int k = 0; k < nt; ++k) {
+            const int g = k == 0 ? t0 : t1;
+            if ((g & 31) == static_cast<int>(lane)) ok = refresh_gpu<L>(b, g, c.now, c.window, c.begin0) && ok;
+        }
     }
     if (!__all_sync(0xffffffffu, ok)) {
         c.status = kStatusRetry;
@@ -672,7 +819,32 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
     uint64_t* aff = RP_U64(aff);
     uint64_t* aff2 = RP_U64(aff2);
     uint32_t na = 0;
-    {
+    if constexpr (L::MG) {
+        // residents of tg[k] not already collected from tg[0..k)
+        const uint8_t* gls = reinterpret_cast<const uint8_t*>(b + L::s_gl);
+#pragma unroll
+        for (int k = 0; k < L::WM; ++k) {
+            if (k >= nt) break;
+            const uint32_t nk = nres[tg[k]];
+#pragma unroll 1
+            for (uint32_t base = 0; base < nk; base += 32) {
+                const uint32_t r = base + lane;
+                bool keep = false;
+                uint32_t slot = 0;
+                if (r < nk) {
+                    slot = res[tg[k] * L::RC + r];
+                    keep = true;
+                    const uint32_t w = gp[slot] >> 16;
+                    for (uint32_t m = 0; m < w; ++m)
+                        for (int j = 0; j < k; ++j)
+                            if (gls[slot * L::WM + m] == tg[j]) keep = false;
+                }
+                const unsigned bm = __ballot_sync(0xffffffffu, keep);
+                if (keep) aff[na + __popc(bm & ((1u << lane) - 1u))] = (static_cast<uint64_t>(rank[slot]) << 32) | slot;
+                na += __popc(bm);
+            }
+        }
+    } else {
         const uint32_t n0 = nres[t0];
 #pragma unroll 1
         for (uint32_t r = lane; r < n0; r += 32) {
@@ -719,7 +891,19 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
         const uint32_t slot = static_cast<uint32_t>(aff2[e] & 0xffffffffu);
         const uint32_t g = gp[slot];
         double r0, r1 = 0.0;
-        if constexpr (L::MIG) {  // effective_rates (gpu.cpp:187-195)
+        if constexpr (L::MG) {  // min over every device of the task (world.cpp:165-175)
+            const uint8_t* gls = reinterpret_cast<const uint8_t*>(b + L::s_gl) + slot * L::WM;
+            const uint8_t* ils = reinterpret_cast<const uint8_t*>(b + L::s_il) + slot * L::WM;
+            const double d = RP_F64(s_dem)[slot];
+            double rate = 1.0;
+            for (uint32_t m = 0; m < (g >> 16); ++m) {
+                double rm;
+                if constexpr (L::MIG) rm = dmin(1.0, __ddiv_rn(RP_CFG.mig_fraction[ils[m]], d));
+                else rm = grate[gls[m]];
+                rate = dmin(rate, rm);
+            }
+            r0 = rate;
+        } else if constexpr (L::MIG) {  // effective_rates (gpu.cpp:187-195)
             const uint32_t in = RP_U32(s_inst)[slot];
             const double d = RP_F64(s_dem)[slot];
             r0 = dmin(1.0, __ddiv_rn(RP_CFG.mig_fraction[in & 0xff], d));
@@ -729,7 +913,7 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
             if ((g >> 16) > 1) r1 = grate[(g >> 8) & 0xff];
         }
         double rate = dmin(1.0, r0);
-        if ((g >> 16) > 1) rate = dmin(rate, r1);
+        if (!L::MG && (g >> 16) > 1) rate = dmin(rate, r1);
         const double old = s_rate[slot];
         if (rate == old && s_seq[slot] != kNone) continue;
         const double dt = __dsub_rn(c.now, s_last[slot]);
@@ -749,13 +933,15 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, int t0, int t1, in
 // allocate on every GPU in order (rolling back on failure), then take a
 // slot and append the task to the resident lists.
 template <class L>
-__device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint32_t task, int g0, int g1,
-                                      int i0, int i1, int want, int nblk, unsigned lane, OomInfo& oi) {
+__device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint32_t task, const int (&gl)[L::WM],
+                                      const int (&il)[L::WM], int want, int nblk, unsigned lane, OomInfo& oi) {
+    const int g0 = gl[0], g1 = gl[1], i0 = il[0], i1 = il[1];
     const carma_replay_config& cf = RP_CFG;
     const uint64_t block = cf.alloc_block;
     const uint64_t bytes = tk.true_mem > 0 ? tk.true_mem : 1;
-    const uint64_t nb64 = (bytes + block - 1) / block;
-    const int nb = nb64 > static_cast<uint64_t>(nblk) ? nblk + 1 : static_cast<int>(nb64);
+    const bool seg = L::MG && nblk < 0;  // byte-granular segment allocator (nblk = -1)
+    const uint64_t nb64 = seg ? 0 : (bytes + block - 1) / block;
+    const int nb = seg ? 0 : (nb64 > static_cast<uint64_t>(nblk) ? nblk + 1 : static_cast<int>(nb64));
     // MIG: allocate_on_instance (gpu.cpp:67-70) inside the instance's blocks
     constexpr bool mig = L::MIG;
     const int a0 = mig ? cf.mig_base[i0] : 0, e0 = mig ? a0 + cf.mig_blocks[i0] : nblk;
@@ -769,6 +955,105 @@ __device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint
             oi.largest_blk = __shfl_sync(0xffffffffu, lg, g & 31);
         }
     };
+    if constexpr (L::MG) {
+        // allocate on every device in order, rolling back on the first failure (world.cpp:84-110)
+        int offs[L::WM];
+        uint64_t offs_b[L::WM];
+        // round_up(max(bytes, 1)) (gpu.cpp:58-61, 74)
+        const uint64_t want_b = seg ? (block == 0 ? bytes : (bytes + block - 1) / block * block) : 0;
+#pragma unroll
+        for (int k = 0; k < L::WM; ++k) {
+            if (k >= want) break;
+            const int g = gl[k];
+            if (seg) {
+                uint64_t o = 0, f = 0, lg = 0;
+                bool okk = false, ovf = false;
+                if ((g & 31) == static_cast<int>(lane))
+                    okk = seg_alloc<L>(b, g, cf.gpu_capacity, 0, cf.gpu_capacity, want_b, o, f, lg, ovf);
+                okk = __shfl_sync(0xffffffffu, okk, g & 31);
+                ovf = __shfl_sync(0xffffffffu, ovf, g & 31);
+                o = __shfl_sync(0xffffffffu, o, g & 31);
+                if (ovf) {
+                    c.status = kStatusRetry;
+                    return false;
+                }
+                if (!okk) {
+                    oi.gpu = g;
+                    oi.free_b = __shfl_sync(0xffffffffu, f, g & 31);
+                    oi.largest_b = __shfl_sync(0xffffffffu, lg, g & 31);
+#pragma unroll
+                    for (int j = 0; j < L::WM; ++j) {
+                        if (j >= k) break;
+                        if ((gl[j] & 31) == static_cast<int>(lane)) seg_release<L>(b, gl[j], offs_b[j], want_b);
+                    }
+                    __syncwarp();
+                    return false;
+                }
+                offs_b[k] = o;
+                offs[k] = 0;
+                continue;
+            }
+            const int a = mig ? cf.mig_base[il[k]] : 0, e = mig ? a + cf.mig_blocks[il[k]] : nblk;
+            int o = -1;
+            if ((g & 31) == static_cast<int>(lane) && nb <= nblk) o = first_fit<L>(b, g, nblk, nb, a, e);
+            o = __shfl_sync(0xffffffffu, o, g & 31);
+            if (o < 0) {
+                oom(g, a, e);
+#pragma unroll
+                for (int j = 0; j < L::WM; ++j) {
+                    if (j >= k) break;
+                    if ((gl[j] & 31) == static_cast<int>(lane)) set_bits<L>(RP_U64(used), gl[j], offs[j], nb, false);
+                }
+                __syncwarp();
+                return false;
+            }
+            offs[k] = o;
+        }
+        if (c.nfree == 0) {
+            c.status = kStatusRetry;
+            return false;
+        }
+        const uint32_t slot = RP_U32(free_stack)[--c.nfree];
+        RP_U32(s_task)[slot] = task;
+        RP_U32(s_rank)[slot] = tk.rank;
+        RP_F64(s_rem)[slot] = tk.work;
+        RP_F64(s_rate)[slot] = 0.0;
+        RP_F64(s_last)[slot] = c.now;
+        RP_F64(s_exec)[slot] = 0.0;
+        RP_F64(s_dem)[slot] = tk.demand;
+        RP_U32(s_seq)[slot] = kNone;
+        RP_U32(s_gp)[slot] = static_cast<uint32_t>(g0) | (static_cast<uint32_t>(want > 1 ? g1 : 0) << 8) |
+                             (static_cast<uint32_t>(want) << 16);
+        RP_U32(s_nb)[slot] = static_cast<uint32_t>(nb);
+        if (seg && lane == 0) RP_U64(s_wb)[slot] = want_b;
+        uint8_t* gls = reinterpret_cast<uint8_t*>(b + L::s_gl) + slot * L::WM;
+        uint8_t* ils = reinterpret_cast<uint8_t*>(b + L::s_il) + slot * L::WM;
+        uint16_t* ols = reinterpret_cast<uint16_t*>(b + L::s_ol) + slot * L::WM;
+        uint32_t* nres = RP_U32(nres);
+        uint16_t* res = RP_U16(res);
+#pragma unroll
+        for (int k = 0; k < L::WM; ++k) {
+            if (k >= want) break;
+            const int g = gl[k];
+            if (lane == 0) {
+                gls[k] = static_cast<uint8_t>(g);
+                ols[k] = static_cast<uint16_t>(offs[k]);
+                if (seg) RP_U64(s_ob)[slot * L::WM + k] = offs_b[k];
+                if (mig) ils[k] = static_cast<uint8_t>(il[k]);
+            }
+            const uint32_t n = nres[g];
+            if (n >= static_cast<uint32_t>(L::RC)) {
+                c.status = kStatusRetry;
+                return false;
+            }
+            res[g * L::RC + n] = static_cast<uint16_t>(slot);
+            nres[g] = n + 1;
+            if (mig && (g & 31) == static_cast<int>(lane)) RP_U32(imask)[g] |= 1u << il[k];
+            __syncwarp();
+        }
+        __syncwarp();
+        return true;
+    }
     int off0 = -1, off1 = 0;
     if ((g0 & 31) == static_cast<int>(lane) && nb <= nblk) off0 = first_fit<L>(b, g0, nblk, nb, a0, e0);
     off0 = __shfl_sync(0xffffffffu, off0, g0 & 31);
@@ -826,8 +1111,8 @@ __device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint
 
 // World::finish (world.cpp:132-155) without the trailing refresh_rates.
 template <class L>
-__device__ __forceinline__ void finish(char* b, Sc& c, uint32_t slot, carma_task_result* out, int& g0, int& g1,
-                                       int& want, unsigned lane) {
+__device__ __forceinline__ void finish(char* b, Sc& c, uint32_t slot, carma_task_result* out, int (&tg)[L::WM],
+                                       int& want, unsigned lane, bool nblk_seg = false) {
     double* s_last = RP_F64(s_last);
     double* s_rem = RP_F64(s_rem);
     const double dt = __dsub_rn(c.now, s_last[slot]);
@@ -837,15 +1122,28 @@ __device__ __forceinline__ void finish(char* b, Sc& c, uint32_t slot, carma_task
     s_last[slot] = c.now;
     const uint32_t gp = RP_U32(s_gp)[slot], of = RP_U32(s_off)[slot];
     want = static_cast<int>(gp >> 16);
-    g0 = static_cast<int>(gp & 0xff);
-    g1 = static_cast<int>((gp >> 8) & 0xff);
+    const int g0 = static_cast<int>(gp & 0xff), g1 = static_cast<int>((gp >> 8) & 0xff);
+    tg[0] = g0;
+    tg[1] = g1;
+    const uint8_t* gls = reinterpret_cast<const uint8_t*>(b + L::s_gl) + slot * L::WM;
+    const uint16_t* ols = reinterpret_cast<const uint16_t*>(b + L::s_ol) + slot * L::WM;
+    if constexpr (L::MG) {
+#pragma unroll
+        for (int k = 0; k < L::WM; ++k)
+            if (k < want) tg[k] = gls[k];
+    }
     const int nb = static_cast<int>(RP_U32(s_nb)[slot]);
     uint32_t* nres = RP_U32(nres);
     uint16_t* res = RP_U16(res);
     for (int k = 0; k < want; ++k) {
-        const int g = k == 0 ? g0 : g1;
+        const int g = L::MG ? tg[k < L::WM ? k : 0] : (k == 0 ? g0 : g1);
         if ((g & 31) == static_cast<int>(lane)) {
-            set_bits<L>(RP_U64(used), g, k == 0 ? static_cast<int>(of & 0xffff) : static_cast<int>(of >> 16), nb, false);
+            if (L::MG && nblk_seg) seg_release<L>(b, g, RP_U64(s_ob)[slot * L::WM + k], RP_U64(s_wb)[slot]);
+            else
+                set_bits<L>(RP_U64(used), g,
+                            L::MG ? static_cast<int>(ols[k])
+                                  : (k == 0 ? static_cast<int>(of & 0xffff) : static_cast<int>(of >> 16)),
+                            nb, false);
             // remove_resident preserving insertion order (gpu.cpp:175-181)
             const uint32_t n = nres[g];
             uint16_t* rl = res + g * L::RC;
@@ -871,8 +1169,8 @@ __device__ __forceinline__ void finish(char* b, Sc& c, uint32_t slot, carma_task
 // estimate, map_task. Returns the number of GPUs chosen (0 = no dispatch).
 template <class L>
 __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, const uint64_t* est,
-                                      uint32_t& head, bool& from_recovery, int& g0, int& g1, int& i0, int& i1,
-                                      uint64_t& est_bytes, unsigned lane) {
+                                      uint32_t& head, bool& from_recovery, int (&gl)[L::WM], int (&il)[L::WM],
+                                      uint64_t& est_bytes, unsigned lane, bool seg_mode = false) {
     const carma_replay_config& cf = RP_CFG;
     const int G = cf.gpu_count;
     const uint32_t* nres = RP_U32(nres);
@@ -913,7 +1211,8 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
         const bool valid = g < G;
         in[j].valid = valid;
         in[j].idle = valid && nres[g] == 0;
-        in[j].free_bytes = valid ? static_cast<uint64_t>(free_blocks<L>(used, g)) * cf.alloc_block : 0;
+        if (L::MG && seg_mode) in[j].free_bytes = valid ? RP_U64(seg_free)[g] : 0;
+        else in[j].free_bytes = valid ? static_cast<uint64_t>(free_blocks<L>(used, g)) * cf.alloc_block : 0;
         if (L::GPL == 1) in[j].smact = (valid && need_smact) ? windowed<L>(b, g, c.now, c.window) : 0.0;
         in[j].inst_ok = true;
         inst[j] = -1;
@@ -944,11 +1243,24 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
             if (j + 1 < L::GPL) in[j + 1].smact = s1;
         }
     }
-    int gids[2];
-    const int got = pick_gpus<L::GPL>(cf, policy, tasks[head].gpus, floor, in, lane, 0, 32, c.rr_cursor, gids);
-    g0 = gids[0];
-    g1 = gids[1];
-    i0 = i1 = 0;
+    const int got = pick_gpus<L::GPL>(cf, policy, tasks[head].gpus, floor, in, lane, 0, 32, c.rr_cursor, gl);
+    const int g0 = gl[0], g1 = gl[1];
+#pragma unroll
+    for (int k = 0; k < L::WM; ++k) il[k] = 0;
+    if constexpr (L::MG) {
+        if (mig && got > 0) {
+#pragma unroll
+            for (int k = 0; k < L::WM; ++k) {
+                if (k >= got) break;
+                int mine = 0;
+#pragma unroll
+                for (int j = 0; j < L::GPL; ++j)
+                    if (static_cast<int>(lane) + 32 * j == gl[k]) mine = inst[j] < 0 ? 0 : inst[j];
+                il[k] = __shfl_sync(0xffffffffu, mine, gl[k] & 31);
+            }
+        }
+        return got;
+    }
     if (mig && got > 0) {  // the chosen devices' instances (exclusive: value_or(0))
         int mine0 = 0, mine1 = 0;
 #pragma unroll
@@ -957,8 +1269,8 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
             if (g == g0) mine0 = inst[j] < 0 ? 0 : inst[j];
             if (g == g1) mine1 = inst[j] < 0 ? 0 : inst[j];
         }
-        i0 = __shfl_sync(0xffffffffu, mine0, g0 & 31);
-        if (got > 1) i1 = __shfl_sync(0xffffffffu, mine1, g1 & 31);
+        il[0] = __shfl_sync(0xffffffffu, mine0, g0 & 31);
+        if (got > 1) il[1] = __shfl_sync(0xffffffffu, mine1, g1 & 31);
     }
     return got;
 }
@@ -977,11 +1289,19 @@ __device__ __noinline__ void init_job(char* b, const Params& p, uint32_t j, unsi
     const uint32_t T = static_cast<uint32_t>(p.trace_off[job.trace + 1] - tb);
     tasks = p.tasks + tb;
     out = p.task_out + p.task_out_off[j];
-    nblk = static_cast<int>(cf.gpu_capacity / cf.alloc_block);
+    // byte-granular segments (generic instantiations): nblk = -1
+    const bool seg = L::MG && (cf.alloc_block == 0 || cf.gpu_capacity % cf.alloc_block != 0 ||
+                               cf.gpu_capacity / cf.alloc_block > 64ull * L::W);
+    nblk = seg ? -1 : static_cast<int>(cf.gpu_capacity / cf.alloc_block);
     // first_submit (runner.cpp:108-109) and the full-history window begin.
     double fs = tasks[0].submit;
+    bool bad = false;  // gpus_requested outside what this instantiation places (1..WM)
 #pragma unroll 1
-    for (uint32_t i = lane; i < T; i += 32) fs = dmin(fs, tasks[i].submit);
+    for (uint32_t i = lane; i < T; i += 32) {
+        fs = dmin(fs, tasks[i].submit);
+        bad |= tasks[i].gpus < 1 || tasks[i].gpus > static_cast<uint32_t>(L::WM);
+    }
+    bad = __any_sync(0xffffffffu, bad);
 #pragma unroll 1
     for (int o = 16; o > 0; o >>= 1) fs = dmin(fs, __shfl_xor_sync(0xffffffffu, fs, o));
     const double forced = p.smact_begin[j];
@@ -1021,6 +1341,9 @@ __device__ __noinline__ void init_job(char* b, const Params& p, uint32_t j, unsi
         RP_U32(rhead)[g] = 0;
         RP_U32(rcnt)[g] = 0;
         RP_U32(peak)[g] = 0;
+        if constexpr (L::MG) {
+            if (seg) seg_init<L>(b, g, cf.gpu_capacity);
+        }
         RP_U32(has_step)[g] = 0;
         if constexpr (L::MIG) RP_U32(imask)[g] = 0;
     }
@@ -1041,6 +1364,10 @@ __device__ __noinline__ void init_job(char* b, const Params& p, uint32_t j, unsi
     c.oom = 0;
     c.status = 0;
     c.events_lo = c.events_hi = 0;
+    if (bad) {  // tasks re-uploaded after the plan was classified: no event runs
+        c.status = CARMA_ERR_UNSUPPORTED;
+        c.arrived = T;
+    }
     __syncwarp();
 }
 
@@ -1049,6 +1376,7 @@ template <class L>
 __device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, unsigned lane, const Sc& c,
                                         const carma_task* tasks, carma_task_result* out) {
     const carma_replay_config& cf = RP_CFG;
+    const bool seg_job = L::MG && static_cast<int>(reinterpret_cast<const uint64_t*>(b + L::ptrs)[3]) < 0;
     carma_trace_result& tr = p.trace_out[j];
     if (c.status == kStatusRetry) {
         if (lane == 0) {
@@ -1109,7 +1437,8 @@ __device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, un
                 mean = __ddiv_rn(__dadd_rn(RP_F64(integ)[g], __dmul_rn(RP_F64(lvl)[g], __dsub_rn(lc, RP_F64(cur)[g]))),
                                  span);
             r.mean_smact = mean;
-            r.peak_used = static_cast<uint64_t>(RP_U32(peak)[g]) * cf.alloc_block;
+            if (L::MG && seg_job) r.peak_used = RP_U64(seg_peak)[g];
+            else r.peak_used = static_cast<uint64_t>(RP_U32(peak)[g]) * cf.alloc_block;
             r.smact_steps = RP_U32(nsteps)[g];
             gout[g] = r;
         }
@@ -1292,7 +1621,8 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
                 const carma_replay_config& cf = RP_CFG;
                 const int G = cf.gpu_count;
                 const uint64_t* used = RP_U64(used);
-                const int nblk_g = static_cast<int>(cf.gpu_capacity / cf.alloc_block);
+                const bool seg_tl = L::MG && nblk < 0;
+                const int nblk_g = seg_tl ? 0 : static_cast<int>(cf.gpu_capacity / cf.alloc_block);
 #pragma unroll
                 for (int jj = 0; jj < L::GPL; ++jj) {
                     const int g = static_cast<int>(lane) + 32 * jj;
@@ -1302,8 +1632,9 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
                         row.t = t;
                         row.smact = RP_F64(inst)[g];
                         row.power_w = RP_F64(power)[g];
-                        row.used = static_cast<uint64_t>(nblk_g - static_cast<int>(free_blocks<L>(used, g))) *
-                                   cf.alloc_block;
+                        if (seg_tl) row.used = cf.gpu_capacity - RP_U64(seg_free)[g];
+                        else row.used = static_cast<uint64_t>(nblk_g - static_cast<int>(free_blocks<L>(used, g))) *
+                                        cf.alloc_block;
                         row.gpu = g;
                         row.reserved = 0;
                         p.tl_out[static_cast<uint64_t>(j) * p.tl_cap + r] = row;
@@ -1322,14 +1653,17 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
         }
         // ---- handle (World::step + Manager::on_event, manager.cpp:333-357)
         bool sched = true;
-        int t0 = 0, t1 = 0, nt = 0;
+        int tg[L::WM];
+#pragma unroll
+        for (int k = 0; k < L::WM; ++k) tg[k] = 0;
+        int nt = 0;
         if (kind == 0) {
             c.arrived++;  // Manager::submit: joins the main queue
         } else if (kind == kWindow) {
             sched = t == c.deadline;
         } else if (kind == kCompletion) {
             if (RP_U32(s_seq)[payload] != seq) continue;  // superseded by a rate change
-            finish<L>(b, c, payload, out, t0, t1, nt, lane);
+            finish<L>(b, c, payload, out, tg, nt, lane, nblk < 0);
             if constexpr (L::TL) {
                 ++n_done;
                 if (log_flags & CARMA_LOG_EVENTS)
@@ -1358,12 +1692,12 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
         for (;;) {
             if (nt) {
                 RPROF_T(tp3);
-                refresh_rates<L>(b, c, t0, t1, nt, lane);
+                refresh_rates<L>(b, c, tg, nt, lane);
                 RPROF_ADD(3, tp3);
 #if REPLAY_PROF
-                prof[12] += RP_U32(nres)[t0] + (nt > 1 ? RP_U32(nres)[t1] : 0);
+                prof[12] += RP_U32(nres)[tg[0]] + (nt > 1 ? RP_U32(nres)[tg[1]] : 0);
                 prof[13] += 1;
-                prof[14] += RP_U32(rcnt)[t0];
+                prof[14] += RP_U32(rcnt)[tg[0]];
 #endif
                 nt = 0;
                 if (c.status) break;
@@ -1372,10 +1706,13 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             sched = false;
             uint32_t head = kNone;
             bool from_recovery = false;
-            int g0 = -1, g1 = -1, i0 = 0, i1 = 0;
+            int gl[L::WM], il[L::WM];
+#pragma unroll
+            for (int k = 0; k < L::WM; ++k) gl[k] = il[k] = 0;
             uint64_t est_bytes = 0;
             RPROF_T(tp4);
-            const int got = decide<L>(b, c, tasks, est, head, from_recovery, g0, g1, i0, i1, est_bytes, lane);
+            const int got = decide<L>(b, c, tasks, est, head, from_recovery, gl, il, est_bytes, lane, nblk < 0);
+            const int g0 = gl[0], g1 = gl[1];
             RPROF_ADD(4, tp4);
 #if REPLAY_PROF
             prof[10] += head != kNone;
@@ -1400,7 +1737,7 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
             if (lane == 0 && !from_recovery) out[head].first_attempt = c.now;
             OomInfo oi{};
             RPROF_T(tp5);
-            const bool ok = place<L>(b, c, tasks[head], head, g0, g1, i0, i1, got, nblk, lane, oi);
+            const bool ok = place<L>(b, c, tasks[head], head, gl, il, got, nblk, lane, oi);
             RPROF_ADD(5, tp5);
             if (c.status) break;
             if constexpr (L::TL) {
@@ -1410,8 +1747,12 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
                         log(CARMA_REC_PLACE, head, got, 0, 0, 0, 0);  // world.cpp:126-128
                     } else {  // world.cpp:94-104: want = round_up(max(bytes, 1))
                         const uint64_t bytes = tasks[head].true_mem > 0 ? tasks[head].true_mem : 1;
-                        log(CARMA_REC_OOM, head, oi.gpu, (bytes + blk - 1) / blk * blk, oi.free_blk * blk,
-                            oi.largest_blk * blk, 0);
+                        if (L::MG && nblk < 0)
+                            log(CARMA_REC_OOM, head, oi.gpu, blk == 0 ? bytes : (bytes + blk - 1) / blk * blk,
+                                oi.free_b, oi.largest_b, 0);
+                        else
+                            log(CARMA_REC_OOM, head, oi.gpu, (bytes + blk - 1) / blk * blk, oi.free_blk * blk,
+                                oi.largest_blk * blk, 0);
                     }
                 }
             }
@@ -1422,8 +1763,8 @@ __device__ __forceinline__ void run_job(char* b, const Params& p, uint32_t j, un
                     o.gpu[0] = static_cast<int16_t>(g0);
                     o.gpu[1] = static_cast<int16_t>(got > 1 ? g1 : -1);
                 }
-                t0 = g0;
-                t1 = g1;
+#pragma unroll
+                for (int k = 0; k < L::WM; ++k) tg[k] = gl[k];
                 nt = got;
             }
             // crash (on failure, manager.cpp:251-256) then arm_window

@@ -371,3 +371,60 @@ def test_replay_more_than_256_blocks(gpu, olib, models, capacity, block):
     jobs = [(t, c) for c in range(len(cfgs)) for t in range(len(task_lists))]
     res = cb.replay(cfgs, task_lists, jobs)
     check_jobs(olib, res, cfgs, task_lists, jobs)
+
+
+@pytest.mark.parametrize("gpus,mode", [(8, "mps"), (64, "mps"), (130, "mps"), (16, "mig"), (12, "streams")])
+def test_replay_tasks_requesting_up_to_8_gpus(gpu, olib, gpus, mode):
+    """Tasks asking for 1..8 GPUs (TaskSpec::gpus_requested; the catalog only
+    has 1 and 2) run in the multi-GPU instantiations (F bit 4): allocation on
+    every device with roll-back, the task rate as the min over its devices,
+    affected-task de-duplication over all touched devices; bit-exact against
+    the oracle for every policy."""
+    m = cb.materialize_trace(cb.generate_uniform_trace(1500, 0.5, 21))
+    cb.set_persona_estimates(m, "oracle")
+    rng = np.random.default_rng(gpus)
+    m.tasks["gpus"] = rng.integers(1, 9, len(m.tasks)).astype(np.uint32)
+    mig = [0.75, 0.25] if mode == "mig" else None
+    cfgs = np.concatenate([cfg_of(p, mode=mode, gpu_count=gpus, window=5.0, rr_pre=pre, mig=mig)
+                           for p, pre in (("magm", False), ("lug", False), ("mug", False), ("rr", False),
+                                          ("rr", True), ("exclusive", False))])
+    jobs = [(0, c) for c in range(len(cfgs))]
+    res = cb.replay(cfgs, [m.tasks], jobs)
+    check_jobs(olib, res, cfgs, [m.tasks], jobs)
+    placed = res.job_tasks(0)
+    assert (placed["final_dispatch"][m.tasks["gpus"] > 2] >= 0).any(), "some wide tasks must be placed"
+
+
+def test_replay_rejects_wide_tasks_uploaded_into_a_narrow_plan(gpu):
+    """A plan classified with 1-2 GPU tasks reports UNSUPPORTED per job when
+    re-uploaded tasks ask for more (device-side check; no silent misplacement)."""
+    m = cb.materialize_trace(cb.generate_uniform_trace(200, 1.0, 3))
+    cfg = cfg_of("magm", gpu_count=8, window=5.0)
+    offs = np.array([0, len(m.tasks)], np.uint64)
+    jobs = np.zeros(1, abi.job_dtype)
+    plan = cb.ReplayPlan(cfg, m.tasks, offs, jobs)
+    t2 = m.tasks.copy()
+    t2["gpus"][5] = 4
+    abi.check(abi.lib.carma_replay_plan_upload_tasks(plan._h, t2.ctypes.data))
+    plan.run()
+    assert plan.results().traces["status"][0] == abi.CARMA_ERR_UNSUPPORTED
+    plan.close()
+
+
+@pytest.mark.parametrize("capacity,block", [(40 * abi.GiB, 0), (40 * abi.GiB + 100 * abi.MiB, 512 * abi.MiB),
+                                            (192 * abi.GiB, 8 * abi.MiB), (32 * abi.GiB + 7, 0)])
+def test_replay_byte_granular_allocator(gpu, olib, capacity, block):
+    """alloc_block = 0 (round_up is the identity), capacities that are not a
+    block multiple (tail carving leaves unaligned offsets) and > 4096 blocks
+    run on the segment allocator (gpu.cpp:58-130) of the generic
+    instantiations; bit-exact against the oracle, whose allocator is the same
+    segment list and is pinned to the reference (test_oracle_vs_ref.py)."""
+    m = cb.materialize_trace(cb.generate_uniform_trace(1200, 0.5, 17))
+    cb.set_persona_estimates(m, "oracle")
+    cfgs = np.concatenate([cfg_of(p, gpu_count=g, window=5.0, rr_pre=pre, capacity=capacity, block=block)
+                           for p, pre, g in (("magm", False, 8), ("lug", False, 8), ("rr", False, 4),
+                                             ("exclusive", False, 8), ("magm", False, 100))])
+    jobs = [(0, c) for c in range(len(cfgs))]
+    res = cb.replay(cfgs, [m.tasks], jobs)
+    check_jobs(olib, res, cfgs, [m.tasks], jobs)
+    assert res.traces["oom_count"][2] > 0  # RR stacking: OOM crashes and their free / largest reports

@@ -16,7 +16,10 @@ pytestmark = pytest.mark.gpu
 CASES = [dict(policy="magm", interval=10.0), dict(policy="rr", interval=7.3),
          dict(policy="lug", interval=60.0, gpu_count=8, window=5.0),
          dict(policy="exclusive", interval=10.0, estimator="oracle"),
-         dict(policy="magm", interval=10.0, mode="mig", mig=(0.75, 0.25))]
+         dict(policy="magm", interval=10.0, mode="mig", mig=(0.75, 0.25)),
+         # byte-granular allocator (generic instantiations): alloc_block 0, non-multiple capacity
+         dict(policy="rr", interval=7.3, block=0),
+         dict(policy="magm", interval=10.0, capacity=40 * 2**30 + 100 * 2**20)]
 
 
 @pytest.mark.parametrize("case", CASES, ids=[str(i) for i in range(len(CASES))])
@@ -29,7 +32,9 @@ def test_timeline_matches_reference(gpu, ref, case, mix, seed):
                       policy=cb.PolicyConfig(policy=kw["policy"], estimator=est,
                                              collocation_mode=kw.get("mode", "mps"),
                                              monitor_window=kw.get("window", 60.0)),
-                      constants=cb.SimConstants(gpu_count=kw.get("gpu_count", 4)),
+                      constants=cb.SimConstants(gpu_count=kw.get("gpu_count", 4),
+                                                **({"gpu_capacity": kw["capacity"]} if "capacity" in kw else {}),
+                                                **({"alloc_block": kw["block"]} if "block" in kw else {})),
                       mig_instances=list(kw.get("mig", ())))
     art = cb.run_simulation_artifacts(rc, device=gpu)
     cfg = ref_config(**kw, sample_interval=interval)
@@ -51,7 +56,8 @@ def test_timeline_off_is_unchanged(gpu):
 
 
 LOG_CASES = [dict(policy="magm"), dict(policy="rr"), dict(policy="lug", estimator="oracle"),
-             dict(policy="magm", mode="mig", mig=(0.75, 0.25)), dict(policy="exclusive", gpu_count=8)]
+             dict(policy="magm", mode="mig", mig=(0.75, 0.25)), dict(policy="exclusive", gpu_count=8),
+             dict(policy="rr", block=0), dict(policy="rr", capacity=40 * 2**30 + 100 * 2**20)]
 
 
 @pytest.mark.parametrize("case", LOG_CASES, ids=[str(i) for i in range(len(LOG_CASES))])
@@ -65,7 +71,9 @@ def test_event_and_decision_logs_match_reference(gpu, ref, case, mix, seed):
     rc = cb.RunConfig(mix=mix, trace_seed=seed, enable_event_log=True, verbose_decisions=True,
                       policy=cb.PolicyConfig(policy=kw["policy"], estimator=est,
                                              collocation_mode=kw.get("mode", "mps")),
-                      constants=cb.SimConstants(gpu_count=kw.get("gpu_count", 4)),
+                      constants=cb.SimConstants(gpu_count=kw.get("gpu_count", 4),
+                                                **({"gpu_capacity": kw["capacity"]} if "capacity" in kw else {}),
+                                                **({"alloc_block": kw["block"]} if "block" in kw else {})),
                       mig_instances=list(kw.get("mig", ())))
     art = cb.run_simulation_artifacts(rc, device=gpu)
     cfg = ref_config(**kw, log_flags=3)

@@ -217,3 +217,20 @@ def test_oracle_many_gpus_matches_reference(ref, olib, tmp_path, gpus, policy):
     assert np.array_equal(ot["gpu"][:, 0], tout["gpu0"])
     assert otr["energy_mj"] == rout["energy_mj"] and otr["avg_jct"] == rout["avg_jct"]
     assert np.array_equal(og["mean_smact"], gs)
+
+
+@pytest.mark.parametrize("capacity,block", [(40 * GiB, 0), (40 * GiB + 100 * MiB, 512 * MiB)])
+def test_oracle_byte_granular_allocator_matches_reference(ref, olib, capacity, block):
+    """The oracle's segment allocator against the reference's GpuDevice with
+    alloc_block = 0 and a capacity that is not a block multiple (RR without
+    preconditions stacks tasks, so OOM crashes and free/largest reports occur)."""
+    for policy, pre in (("rr", False), ("magm", False)):
+        cfg = ref_config(policy=policy, rr_pre=pre, gpu_count=4, capacity=capacity, block=block, max_smact=1.0)
+        for seed in (1, 2, 3):
+            tout, rout, ge, gs, gp = ref_run(ref, cfg, mix="t90", seed=seed)
+            m = cb.materialize_trace(cb.generate_trace("t90", seed))
+            rc, ot, otr, og = oracle_replay(olib, replay_config_from(cfg), m.tasks)
+            assert rc == 0
+            assert np.array_equal(ot["complete"], tout["complete"]) and np.array_equal(ot["ooms"], tout["ooms"])
+            assert otr["energy_mj"] == rout["energy_mj"] and otr["avg_jct"] == rout["avg_jct"]
+            assert np.array_equal(og["peak_used"], gp)
