@@ -50,12 +50,12 @@ ALG_BYTES_PER_TASK = 80            # 45 B in + 35 B out per place
 FLOPS_PER_EVAL = 58                # 19 x (sub, mul, add) + 1 weight mul, FMA-free
 FLOPS_PER_F32_EVAL = 48            # fp32 pre-filter: 16 dims x (sub + fma)
 FEATURE_ROW_BYTES = 136
-# host-buffer calls re-encode the 136-B rows (+ 1-B family) into 64-B packed
-# rows on host threads, chunk by chunk, overlapped with the H2D copies
-# (csrc/host/stage.cpp); CARMA_E2E_RAW=1 ships the raw rows
-E2E_WIRE_BYTES = FEATURE_ROW_BYTES + 1 if os.environ.get("CARMA_E2E_RAW", "0") not in ("", "0") else 64
-E2E_API = ("{fn} (pinned 136-B carma_feature_row + family in, bucket + bytes out; rows re-encoded to 64-B packed "
-           "rows by the host thread pool inside the call, overlapped with H2D)")
+# host-buffer calls re-encode every other chunk of 136-B rows (+ 1-B family)
+# into 64-B packed rows on host threads while the copy engine ships the
+# other chunks raw, so PCIe and host memory bandwidth overlap
+# (csrc/host/stage.cpp); h2d_bytes_per_step is the call's own count
+E2E_API = ("{fn} (pinned 136-B carma_feature_row + family in, bucket + bytes out; half the chunks re-encoded to "
+           "64-B packed rows by the host thread pool inside the call, overlapped with the raw chunks' H2D)")
 
 
 def log(*a):
@@ -480,6 +480,8 @@ def knn_stage(abi, cb, dev, stream, args, d, rows, fam, b, e):
                                             h_b.ctypes.data, h_by.ctypes.data))
 
     e2e_s = timed_host_steps(e2e_step, max(1, args.warmup - 1), args.steps, d)
+    h2d = ctypes.c_uint64()
+    abi.check(abi.lib.carma_knn_last_h2d_bytes(knn.handle, ctypes.byref(h2d)))
     assert np.array_equal(h_b, b_dev) and np.array_equal(h_by, by_dev), "host-API and device predictions differ"
     knn_handle = knn  # kept for the fused c5 run
     search_avg = statistics.mean(search_ms)
@@ -493,12 +495,12 @@ def knn_stage(abi, cb, dev, stream, args, d, rows, fam, b, e):
     out = {
         "value": QT / (ms * 1e-3), "ms_per_step": ms, "clocks": clocks,
         "e2e": {"value": QT / e2e_s, "unit": "estimates/s",
-                "h2d_bytes_per_step": int(Q * E2E_WIRE_BYTES),
+                "h2d_bytes_per_step": int(h2d.value),
                 "d2h_bytes_per_step": int(Q * 12),
                 "api": E2E_API.format(fn="carma_knn_predict"),
                 "host_row_bytes_read": int(Q * (FEATURE_ROW_BYTES + 1)),
                 "ms_per_step": e2e_s * 1e3,
-                "pcie_gbs": Q * (E2E_WIRE_BYTES + 12) / e2e_s / 1e9},
+                "pcie_gbs": (h2d.value + Q * 12) / e2e_s / 1e9},
         "gpu_launches": int(launches) * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved / 1e12, "peak": fp32.value / 1e12, "unit": "TFLOP/s",
                      "frac": achieved / fp32.value,
@@ -563,6 +565,8 @@ def neural_stage(abi, cb, dev, stream, args, d, h_rows, h_fam, rows_all, fam_all
                                                h_b.ctypes.data, h_by.ctypes.data))
 
         e2e_s = timed_host_steps(e2e_step, 1, args.steps, d)
+        h2d = ctypes.c_uint64()
+        abi.check(abi.lib.carma_nn_last_h2d_bytes(net.handle, ctypes.byref(h2d)))
         assert np.array_equal(h_b, b_dev), f"{key}: host-API and device-resident neural predictions differ"
         agree = 0
         for f in (1, 2):
@@ -576,7 +580,7 @@ def neural_stage(abi, cb, dev, stream, args, d, h_rows, h_fam, rows_all, fam_all
             agree += int(sure.sum())
         k_avg = statistics.mean(kernel_ms)
         r = {"value": QT / (ms * 1e-3), "ms_per_step": ms,
-             "e2e": {"value": QT / e2e_s, "unit": "estimates/s", "h2d_bytes_per_step": int(Q * E2E_WIRE_BYTES),
+             "e2e": {"value": QT / e2e_s, "unit": "estimates/s", "h2d_bytes_per_step": int(h2d.value),
                      "d2h_bytes_per_step": int(Q * 12), "api": E2E_API.format(fn="carma_nn_predict")},
              "gpu_launches": int(t["launches"]) * args.steps, "kernel_ms": k_avg,
              "kernel_share_of_step": k_avg / statistics.mean(call_ms), "oracle_agreement_rows": agree,

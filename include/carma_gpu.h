@@ -235,6 +235,9 @@ carma_status carma_knn_set_act_table(carma_knn* h, const double* act_table);
  * fp64 (query, point) distance evaluations performed. */
 carma_status carma_knn_last_stats(carma_knn* h, uint64_t* launches, uint64_t* evaluations);
 /* Same, plus the fp32 pre-filter evaluations (0 on the exact-only path). */
+/* Bytes the last host-buffer predict copied host -> device (rows travel as
+ * 64-byte packed rows or as they are, chunk by chunk; see stage.hpp). */
+carma_status carma_knn_last_h2d_bytes(carma_knn* h, uint64_t* bytes);
 carma_status carma_knn_last_work(carma_knn* h, uint64_t* launches, uint64_t* fp64_evals,
                                  uint64_t* fp32_evals);
 /* Search path: 0 auto (fp32 pre-filter whenever every installed model has
@@ -296,6 +299,8 @@ typedef struct carma_nn_spec {
 uint64_t carma_nn_param_count(const carma_nn_spec* spec);
 
 typedef struct carma_nn carma_nn;
+/* Bytes the last host-buffer carma_nn_predict copied host -> device. */
+carma_status carma_nn_last_h2d_bytes(carma_nn* h, uint64_t* bytes);
 carma_status carma_nn_create(int device, carma_nn** out);
 carma_status carma_nn_destroy(carma_nn* h);
 carma_status carma_nn_set_model(carma_nn* h, int32_t family, const carma_nn_spec* spec,

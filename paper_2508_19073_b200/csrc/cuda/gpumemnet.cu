@@ -1341,6 +1341,7 @@ struct NnHandle {
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // call start, ensemble start, ensemble end
     bool timed = false;
     uint64_t last_launches = 0, last_mmas = 0;
+    uint64_t last_h2d = 0;  // bytes copied host -> device by the last host-buffer call
     StreamFence fence;                 // last device-stream user of scratch[0]
     PinnedBuffer counts_host;          // family counts of the last device call
     cudaStream_t counts_stream = nullptr;
@@ -1589,13 +1590,13 @@ carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int3
         static const bool raw_env = std::getenv("CARMA_E2E_RAW") && std::atoi(std::getenv("CARMA_E2E_RAW")) != 0;
         const bool pack = format == CARMA_ROWS_FEATURES && !raw_env;
         if (pack) std::memcpy(h->act, canonical_act_table(), sizeof(h->act));
-        uint64_t launches = 0, beg = 0, cnt = 0;
+        uint64_t launches = 0, beg = 0, cnt = 0, h2d = 0;
         for (uint64_t c = 0; beg < q; ++c, beg += cnt) {
             NnHandle::Scratch& sc = h->scratch[c & 1];
             cudaStream_t s = h->pipe[c & 1];
             cnt = std::min<uint64_t>(chunk_rows(c, q - beg), q - beg);
             const uint64_t cap_rows = std::min<uint64_t>(chunk, q);
-            if (pack) {
+            if (pack && !raw_chunk(c, rows_pinned && fam_pinned)) {
                 sc.stage_packed.ensure(cap_rows * sizeof(carma_feature_packed));
                 sc.rows.ensure(cap_rows * row_bytes);
                 sc.bucket.ensure(cap_rows * 4);
@@ -1607,6 +1608,7 @@ carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int3
                                         default_family, cnt, pk)) {
                     CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, pk, cnt * sizeof(carma_feature_packed),
                                                cudaMemcpyHostToDevice, s));
+                    h2d += cnt * sizeof(carma_feature_packed);
                     CARMA_CUDA(cudaEventRecord(sc.staged, s));
                     launches += run_predict(*h, sc, sc.rows.ptr, CARMA_ROWS_PACKED, nullptr, default_family, cnt,
                                             sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(), nullptr, nullptr, s);
@@ -1630,6 +1632,7 @@ carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int3
                 }
             }
             CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, src, cnt * row_bytes + tail_bytes, cudaMemcpyHostToDevice, s));
+            h2d += cnt * row_bytes + tail_bytes + (family ? cnt : 0);
             if (family)
                 CARMA_CUDA(cudaMemcpyAsync(sc.family.ptr,
                                            (!rows_pinned || !fam_pinned) ? sc.stage_family.as<int8_t>() : family + beg,
@@ -1642,6 +1645,7 @@ carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int3
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[0]));
         CARMA_CUDA(cudaStreamSynchronize(h->pipe[1]));
         h->last_launches = launches;
+        h->last_h2d = h2d;
         h->last_mmas = 0;
         h->counts_pending = false;
     });
@@ -1828,3 +1832,11 @@ carma_status carma_nn_last_timing(carma_nn* hh, double* kernel_ms, double* call_
 }
 
 }  // extern "C"
+
+extern "C" carma_status carma_nn_last_h2d_bytes(carma_nn* hh, uint64_t* bytes) {
+    return guarded([&] {
+        const NnHandle* h = reinterpret_cast<const NnHandle*>(hh);
+        if (!h || !bytes) throw InvalidArg("null argument");
+        *bytes = h->last_h2d;
+    });
+}

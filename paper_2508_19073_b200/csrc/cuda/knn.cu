@@ -1281,6 +1281,7 @@ struct KnnHandle {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // pipeline start, search start / end, pipeline end
     bool timed = false;
     uint64_t last_launches = 0, last_evals = 0;
+    uint64_t last_h2d = 0;  // bytes copied host -> device by the last host-buffer call
     std::mutex mu;
 };
 
@@ -1598,7 +1599,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
                     CARMA_CUDA(cudaMemcpy(bytes_out + beg, sc.bytes.ptr, cnt * 8, cudaMemcpyDeviceToHost));
             }
         };
-        uint64_t launches = 0;
+        uint64_t launches = 0, h2d = 0;
         uint64_t beg = 0, cnt = 0;
         // Feature rows travel re-encoded as 64-byte packed rows (family inside;
         // stage.hpp), packed by the host pool while the previous chunk copies
@@ -1611,7 +1612,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
             cudaStream_t s = h->pipe[c & 1];
             cnt = std::min<uint64_t>(chunk_rows(c, q - beg), q - beg);
             const uint64_t cap_rows = std::min<uint64_t>(chunk, q);
-            if (pack) {
+            if (pack && !raw_chunk(c, rows_pinned && fam_pinned)) {
                 sc.stage_packed.ensure(cap_rows * sizeof(carma_feature_packed));
                 sc.rows.ensure(cap_rows * row_bytes);
                 sc.bucket.ensure(cap_rows * 4);
@@ -1623,6 +1624,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
                                         default_family, cnt, pk)) {
                     CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, pk, cnt * sizeof(carma_feature_packed),
                                                cudaMemcpyHostToDevice, s));
+                    h2d += cnt * sizeof(carma_feature_packed);
                     CARMA_CUDA(cudaEventRecord(sc.staged, s));
                     launches += run_pipeline(*h, sc, sc.rows.ptr, CARMA_ROWS_PACKED, nullptr, default_family, cnt,
                                              sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(), nullptr, nullptr,
@@ -1651,6 +1653,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
                 }
             }
             CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, src, cnt * row_bytes + tail_bytes, cudaMemcpyHostToDevice, s));
+            h2d += cnt * row_bytes + tail_bytes + (family ? cnt : 0);
             if (family)
                 CARMA_CUDA(cudaMemcpyAsync(sc.family.ptr,
                                            (!rows_pinned || !fam_pinned) ? sc.stage_family.as<int8_t>() : family + beg,
@@ -1665,6 +1668,7 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
         unsigned long long ev[2] = {0, 0};
         CARMA_CUDA(cudaMemcpy(ev, h->evals.ptr, 16, cudaMemcpyDeviceToHost));
         h->last_launches = launches;
+        h->last_h2d = h2d;
         h->last_evals = ev[0];
         h->last_visits = ev[1];
     });
@@ -2074,3 +2078,11 @@ carma_status carma_knn_set_path(carma_knn* hh, int32_t path) {
 }
 
 }  // extern "C"
+
+extern "C" carma_status carma_knn_last_h2d_bytes(carma_knn* hh, uint64_t* bytes) {
+    return guarded([&] {
+        const KnnHandle* h = reinterpret_cast<const KnnHandle*>(hh);
+        if (!h || !bytes) throw InvalidArg("null argument");
+        *bytes = h->last_h2d;
+    });
+}

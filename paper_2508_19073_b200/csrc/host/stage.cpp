@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numbers>
@@ -136,6 +137,14 @@ inline bool pack_one(const carma_feature_row& r, uint64_t f, const uint64_t* can
 void host_parallel(uint32_t parts, const std::function<void(uint32_t, uint32_t)>& fn) { pool().run(parts, fn); }
 
 uint32_t host_workers() { return pool().size(); }
+
+bool raw_chunk(uint64_t c, bool inputs_pinned) {
+    static const uint64_t every = [] {
+        const char* e = std::getenv("CARMA_E2E_RAW_EVERY");
+        return e ? std::strtoull(e, nullptr, 10) : 2ull;
+    }();
+    return inputs_pinned && every > 0 && c % every == every - 1;
+}
 
 bool pack_rows_canonical(const carma_feature_row* rows, const int8_t* family, int32_t default_family, uint64_t n,
                          carma_feature_packed* out) {

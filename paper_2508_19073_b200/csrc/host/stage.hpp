@@ -30,4 +30,11 @@ uint32_t host_workers();  // parts host_parallel uses for a bulk pass
 bool pack_rows_canonical(const carma_feature_row* rows, const int8_t* family, int32_t default_family, uint64_t n,
                          carma_feature_packed* out);
 
+// Whether chunk c of a host-buffer call ships raw rows although it could be
+// packed: with pinned inputs the copy engine reads raw rows straight from
+// host memory while the pool packs the other chunks, so PCIe and host memory
+// bandwidth are both busy (CARMA_E2E_RAW_EVERY = k: every k-th chunk raw;
+// 0 = pack every chunk).
+bool raw_chunk(uint64_t c, bool inputs_pinned);
+
 }  // namespace carma_b200

@@ -313,3 +313,22 @@ def test_host_api_packed_staging_and_raw_fallback(gpu, models):
     assert np.array_equal(hb2, db2)
     hb3, _ = knn.predict(rows[:1000], default_family=9)
     assert (hb3 == -1).all()
+
+
+def test_host_api_pinned_rows_mix_raw_and_packed_chunks(gpu, models):
+    """Pinned inputs: every other chunk ships raw (the copy engine reads the
+    rows while the host pool packs the next chunk); results are identical."""
+    import torch
+    rows, fam = _mixed_rows()
+    h_rows = torch.from_numpy(rows.view(np.uint8).reshape(-1)).pin_memory().numpy().view(abi.feature_row_dtype)
+    h_fam = torch.from_numpy(fam).pin_memory().numpy()
+    knn = cb.GpuKnn(gpu)
+    for f in models:
+        knn.set_model(models[f])
+    hb, hby = knn.predict(h_rows, family=h_fam, default_family=0)
+    import ctypes
+    n = ctypes.c_uint64()
+    abi.check(abi.lib.carma_knn_last_h2d_bytes(knn.handle, ctypes.byref(n)))
+    assert 64 * len(rows) < n.value < 137 * len(rows)  # a mix of packed and raw chunks
+    db, dby, _, _ = _device_predict(knn, rows, family=fam, default_family=0)
+    assert np.array_equal(hb, db) and np.array_equal(hby, dby)
