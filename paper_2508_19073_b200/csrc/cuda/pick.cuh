@@ -75,6 +75,22 @@ __device__ __forceinline__ int arg_best(int policy, const PickInput (&in)[GPL], 
             bid = id;
         }
     }
+    if (GPL >= 2 && width == 32) {
+        // whole-warp group over > 32 GPUs (the replay's large tiers; on the
+        // throughput-bound small tiers the shuffles measured faster): three
+        // 32-bit max reductions — key
+        // high word, key low word among the leaders, then the smallest id
+        // (as its complement) among those
+        const bool has = bid != 0x7fffffff;
+        if (!__any_sync(0xffffffffu, has)) return -1;
+        const unsigned hi = static_cast<unsigned>(bk >> 32), lo = static_cast<unsigned>(bk);
+        const unsigned m1 = __reduce_max_sync(0xffffffffu, has ? hi : 0u);
+        const bool h1 = has && hi == m1;
+        const unsigned m2 = __reduce_max_sync(0xffffffffu, h1 ? lo : 0u);
+        const bool h2 = h1 && lo == m2;
+        const unsigned m3 = __reduce_max_sync(0xffffffffu, h2 ? ~static_cast<unsigned>(bid) : 0u);
+        return static_cast<int>(~m3);
+    }
 #pragma unroll 1
     for (unsigned off = 1; off < width; off <<= 1) {
         const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off, width);
