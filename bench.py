@@ -689,10 +689,14 @@ def replay_stage(abi, cb, dev, stream, args, d):
     o_j = torch.empty(len(jobs) * 80, dtype=torch.uint8).pin_memory().numpy().view(abi.trace_result_dtype)
     o_g = torch.empty(len(jobs) * 4 * 32, dtype=torch.uint8).pin_memory().numpy().view(abi.gpu_result_dtype)
 
+    # per-task outcomes stream into the pinned buffer as each job finishes
+    # (carma_replay_plan_set_outcome_sink); reports and per-GPU results follow
+    abi.check(abi.lib.carma_replay_plan_set_outcome_sink(plan._h, o_t.ctypes.data))
+
     def e2e_step():
         abi.check(abi.lib.carma_replay_plan_upload_tasks(plan._h, h_tasks.ctypes.data))
         abi.check(abi.lib.carma_replay_plan_run(plan._h, None))
-        abi.check(abi.lib.carma_replay_plan_outcomes(plan._h, o_t.ctypes.data, o_j.ctypes.data, o_g.ctypes.data))
+        abi.check(abi.lib.carma_replay_plan_outcomes(plan._h, None, o_j.ctypes.data, o_g.ctypes.data))
 
     r_e2e = timed_host_steps(e2e_step, 1, args.steps, d)
     plan.close()
@@ -712,7 +716,8 @@ def replay_stage(abi, cb, dev, stream, args, d):
         "e2e": {"value": total_placed / r_e2e, "unit": "placed tasks/s", "ms_per_step": r_e2e * 1e3,
                 "h2d_bytes_per_step": int(h_tasks.nbytes),
                 "d2h_bytes_per_step": int(o_t.nbytes + o_j.nbytes + o_g.nbytes),
-                "api": "carma_replay_plan_upload_tasks + run + outcomes (pinned host buffers)"},
+                "api": "carma_replay_plan_upload_tasks + run (per-task outcomes streamed into a pinned sink as jobs "
+                       "finish) + outcomes (reports, per-GPU results)"},
         "gpu_launches": int(launches_r) * args.steps, "retried_jobs": int(retried),
         "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                      "traffic": profile_traffic("replay_kernel"), "kernel": "replay_kernel", "kernel_ms": k_avg,

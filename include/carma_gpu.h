@@ -542,6 +542,12 @@ typedef struct carma_task_outcome {
     uint32_t attempts;
 } carma_task_outcome; /* 24 bytes */
 
+/* Outcome sink: every later run writes each job's per-task outcomes (the
+ * layout of carma_replay_plan_outcomes) straight into this pinned host
+ * buffer as the job finishes, so the D2H overlaps the jobs still running;
+ * NULL detaches it. The buffer must stay valid and pinned while attached. */
+carma_status carma_replay_plan_set_outcome_sink(carma_replay_plan* p, carma_task_outcome* host_outcomes);
+
 /* Compact results: per-task outcomes (nullable) + traces + GPUs. */
 carma_status carma_replay_plan_outcomes(carma_replay_plan* p, carma_task_outcome* tasks,
                                         carma_trace_result* traces, carma_gpu_result* gpus);

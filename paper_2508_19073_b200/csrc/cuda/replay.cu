@@ -164,6 +164,7 @@ struct ReplayPlan {
         d_log_count, d_entries;
     uint64_t tl_cap = 0, log_cap = 0;
     const uint64_t* est_override = nullptr;
+    carma_task_outcome* outcome_sink = nullptr;  // device view of a pinned host buffer
     uint64_t launches = 0, retried = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // run start, shared-memory tiers end, run end
     std::mutex mu;
@@ -370,6 +371,7 @@ void run_plan(ReplayPlan& pl) {
     p.log_out = pl.d_log.as<carma_log_record>();
     p.log_cap = pl.log_cap;
     p.log_count = pl.d_log_count.as<uint64_t>();
+    p.outcome_sink = pl.outcome_sink;
     const uint32_t n = static_cast<uint32_t>(pl.jobs.size());
     pl.launches = 0;
     pl.retried = 0;
@@ -632,6 +634,23 @@ carma_status carma_replay_plan_upload_tasks(carma_replay_plan* hp, const carma_t
         CARMA_CUDA(cudaMemcpyAsync(pl->d_tasks.ptr, tasks, pl->n_tasks * sizeof(carma_task), cudaMemcpyHostToDevice,
                                    pl->stream));
         if (!is_pinned(tasks)) CARMA_CUDA(cudaStreamSynchronize(pl->stream));
+    });
+}
+
+carma_status carma_replay_plan_set_outcome_sink(carma_replay_plan* hp, carma_task_outcome* host_outcomes) {
+    return guarded([&] {
+        auto* pl = reinterpret_cast<ReplayPlan*>(hp);
+        if (!pl) throw InvalidArg("null plan");
+        std::lock_guard<std::mutex> lock(pl->mu);
+        if (!host_outcomes) {
+            pl->outcome_sink = nullptr;
+            return;
+        }
+        if (!is_pinned(host_outcomes)) throw InvalidArg("the outcome sink must be pinned (page-locked) host memory");
+        DeviceGuard guard(pl->device);
+        void* dp = nullptr;
+        CARMA_CUDA(cudaHostGetDevicePointer(&dp, host_outcomes, 0));
+        pl->outcome_sink = static_cast<carma_task_outcome*>(dp);
     });
 }
 

@@ -105,6 +105,7 @@ struct Params {
     carma_log_record* log_out;   // event / decision log records, log_cap per job (TL kernels only)
     uint64_t log_cap;
     uint64_t* log_count;         // records produced, per job
+    carma_task_outcome* outcome_sink;  // nullable: per-task outcomes written straight to pinned host memory
 };
 
 // alloc_oom details of a failed placement (OomFailure, gpu.hpp:26-35), in
@@ -1398,6 +1399,14 @@ __device__ __noinline__ void finish_job(char* b, const Params& p, uint32_t j, un
         complete = complete && cpl >= 0.0;
         o.attempts = o.ooms + (o.final_dispatch >= 0.0 ? 1u : 0u);
         inv[tasks[i].rank] = i;
+        if (p.outcome_sink) {  // the D2H of the outcomes streams out while later jobs still run
+            carma_task_outcome oc;
+            oc.final_dispatch = o.final_dispatch;
+            oc.complete = cpl;
+            oc.ooms = o.ooms;
+            oc.attempts = o.attempts;
+            p.outcome_sink[p.task_out_off[j] + i] = oc;
+        }
     }
 #pragma unroll 1
     for (int o = 16; o > 0; o >>= 1) {

@@ -428,3 +428,31 @@ def test_replay_byte_granular_allocator(gpu, olib, capacity, block):
     res = cb.replay(cfgs, [m.tasks], jobs)
     check_jobs(olib, res, cfgs, [m.tasks], jobs)
     assert res.traces["oom_count"][2] > 0  # RR stacking: OOM crashes and their free / largest reports
+
+
+def test_outcome_sink_streams_the_same_outcomes(gpu):
+    """carma_replay_plan_set_outcome_sink: the per-task outcomes written to
+    pinned host memory by the kernel as jobs finish equal the compacted
+    read-back (incl. jobs that overflow a tier and re-run)."""
+    import torch
+    lists = [cb.materialize_trace(cb.generate_trace("t90", s)).tasks for s in range(1, 201)]
+    tasks = np.concatenate(lists)
+    offs = np.concatenate([[0], np.cumsum([len(t) for t in lists])]).astype(np.uint64)
+    cfgs = np.concatenate([cfg_of(p, gpu_count=4) for p in ("exclusive", "rr", "magm", "lug")] +
+                          [cfg_of("rr", gpu_count=2, capacity=80 * abi.GiB, window=1.0)])
+    jobs = np.zeros(len(lists) * len(cfgs), abi.job_dtype)
+    jobs["trace"] = np.tile(np.arange(len(lists), dtype=np.uint32), len(cfgs))
+    jobs["config"] = np.repeat(np.arange(len(cfgs), dtype=np.uint32), len(lists))
+    plan = cb.ReplayPlan(cfgs, tasks, offs, jobs)
+    n_out = int(np.diff(offs.astype(np.int64))[jobs["trace"]].sum())
+    sink = torch.empty(n_out * 24, dtype=torch.uint8).pin_memory().numpy().view(abi.task_outcome_dtype)
+    sink[:] = np.frombuffer(b"\xff" * sink.nbytes, dtype=abi.task_outcome_dtype)
+    abi.check(abi.lib.carma_replay_plan_set_outcome_sink(plan._h, sink.ctypes.data))
+    plan.run()
+    ref_o = np.zeros(n_out, abi.task_outcome_dtype)
+    abi.check(abi.lib.carma_replay_plan_outcomes(plan._h, ref_o.ctypes.data, None, None))
+    assert sink.tobytes() == ref_o.tobytes()
+    pageable = np.zeros(4, abi.task_outcome_dtype)
+    assert abi.lib.carma_replay_plan_set_outcome_sink(plan._h, pageable.ctypes.data) == abi.CARMA_ERR_INVALID
+    abi.check(abi.lib.carma_replay_plan_set_outcome_sink(plan._h, None))
+    plan.close()
