@@ -581,6 +581,13 @@ carma_status carma_pick_batch(int device, const carma_replay_config* cfg,
                               const carma_gpu_view* views, uint32_t n_gpus,
                               const carma_pick_request* reqs, uint64_t n,
                               int32_t* rr_cursor, int32_t* out_gpus);
+/* carma_pick_batch beyond its fast paths: up to 256 GPUs per snapshot and
+ * up to 8 GPUs per decision (want in [1, 8]); out_gpus is n x 8 (-1 padded;
+ * all -1 = defer). One decision per warp. Host buffers. */
+carma_status carma_pick_batch_wide(int device, const carma_replay_config* cfg,
+                                   const carma_gpu_view* views, uint32_t n_gpus,
+                                   const carma_pick_request* reqs, uint64_t n,
+                                   int32_t* rr_cursor, int32_t* out_gpus);
 /* Same on device-resident arrays (views, reqs, rr_cursor, out_gpus are device
  * pointers; cfg is host memory), launched on `stream` (cudaStream_t or NULL).
  * want must be 1 or 2 (not checked on the device path). */

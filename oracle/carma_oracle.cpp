@@ -618,10 +618,10 @@ extern "C" int oracle_replay(const carma_replay_config* cfg, const carma_task* t
     return tr.status;
 }
 
-extern "C" int oracle_pick(const carma_replay_config* cfg, const carma_gpu_view* gpus,
-                           uint32_t n_gpus, const carma_pick_request* req, int32_t* rr_cursor,
-                           int32_t* out) {
-    out[0] = out[1] = -1;
+// map_task over one snapshot; out[0, out_n) gets the chosen ids, -1 padded.
+static int oracle_pick_n(const carma_replay_config* cfg, const carma_gpu_view* gpus, uint32_t n_gpus,
+                         const carma_pick_request* req, int32_t* rr_cursor, int32_t* out, uint32_t out_n) {
+    for (uint32_t i = 0; i < out_n; ++i) out[i] = -1;
     const uint32_t want = req->want;
     const int policy = req->from_recovery ? CARMA_POLICY_EXCLUSIVE : cfg->policy;
     std::vector<int> ids;
@@ -664,8 +664,21 @@ extern "C" int oracle_pick(const carma_replay_config* cfg, const carma_gpu_view*
             }
         }
     }
-    for (size_t i = 0; i < ids.size() && i < 2; ++i) out[i] = ids[i];
+    for (size_t i = 0; i < ids.size() && i < out_n; ++i) out[i] = ids[i];
     return 0;
+}
+
+extern "C" int oracle_pick(const carma_replay_config* cfg, const carma_gpu_view* gpus,
+                           uint32_t n_gpus, const carma_pick_request* req, int32_t* rr_cursor,
+                           int32_t* out) {
+    return oracle_pick_n(cfg, gpus, n_gpus, req, rr_cursor, out, 2);
+}
+
+// The same for up to 8 GPUs per decision (out: 8 ids).
+extern "C" int oracle_pick_wide(const carma_replay_config* cfg, const carma_gpu_view* gpus,
+                                uint32_t n_gpus, const carma_pick_request* req, int32_t* rr_cursor,
+                                int32_t* out) {
+    return oracle_pick_n(cfg, gpus, n_gpus, req, rr_cursor, out, 8);
 }
 
 // Test-only: peak sizes of the replay state over one run (heap of pending

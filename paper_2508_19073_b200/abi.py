@@ -190,6 +190,7 @@ SIGNATURES = {
                                                    POINTER(c_void_p)]),
     "carma_replay_plan_entries": (c_int, [c_void_p, P]),
     "carma_replay_plan_tasks": (c_int, [c_void_p, P]),
+    "carma_pick_batch_wide": (c_int, [c_int, P, P, c_uint32, P, c_uint64, P, P]),
     "carma_replay_plan_set_outcome_sink": (c_int, [c_void_p, P]),
     "carma_knn_last_h2d_bytes": (c_int, [c_void_p, POINTER(c_uint64)]),
     "carma_nn_last_h2d_bytes": (c_int, [c_void_p, POINTER(c_uint64)]),

@@ -69,6 +69,53 @@ __global__ void pick_kernel(carma_replay_config cf, const carma_gpu_view* __rest
     }
 }
 
+// carma_pick_batch_wide: one decision per warp over up to 256 GPUs (8 per
+// lane) and up to 8 GPUs per decision; out is n x 8.
+__global__ void __launch_bounds__(128) pick_kernel_wide(carma_replay_config cf, const carma_gpu_view* __restrict__ views,
+                                                        uint32_t n_gpus, const carma_pick_request* __restrict__ reqs,
+                                                        uint64_t n, int32_t* __restrict__ cursor,
+                                                        int32_t* __restrict__ out) {
+    constexpr int GPL = CARMA_MAX_REPLAY_GPUS / 32;
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t d = warp; d < n; d += n_warps) {
+        PickInput in[GPL];
+#pragma unroll
+        for (int j = 0; j < GPL; ++j) {
+            const uint32_t g = lane + 32 * j;
+            const bool valid = g < n_gpus;
+            carma_gpu_view v{};
+            if (valid) v = views[d * n_gpus + g];
+            in[j].valid = valid;
+            in[j].inst_ok = true;
+            in[j].idle = v.idle != 0;
+            in[j].free_bytes = v.total_free;
+            in[j].smact = v.windowed_smact;
+        }
+        const carma_pick_request rq = reqs[d];
+        int cur = cursor[d];
+        const int policy = rq.from_recovery ? CARMA_POLICY_EXCLUSIVE : cf.policy;
+        uint64_t floor = cf.min_free;
+        if (!rq.from_recovery && cf.policy != CARMA_POLICY_EXCLUSIVE && rq.estimate != CARMA_NO_ESTIMATE) {
+            const uint64_t need = rq.estimate < cf.gpu_capacity ? rq.estimate : cf.gpu_capacity;
+            if (need > floor) floor = need;
+        }
+        int ids[CARMA_MAX_TASK_GPUS];
+#pragma unroll
+        for (int k = 0; k < CARMA_MAX_TASK_GPUS; ++k) ids[k] = -1;
+        const int got = pick_gpus<GPL>(cf, policy, rq.want, floor, in, lane, 0, 32, cur, ids);
+        if (lane < CARMA_MAX_TASK_GPUS) {
+            int v = -1;
+#pragma unroll
+            for (int k = 0; k < CARMA_MAX_TASK_GPUS; ++k)
+                if (static_cast<int>(lane) == k && k < got) v = ids[k];
+            out[d * CARMA_MAX_TASK_GPUS + lane] = v;
+        }
+        if (lane == 0) cursor[d] = cur;
+    }
+}
+
 // Batched carma_pick_batch for n_gpus <= 16: one thread per decision. Each
 // warp streams its chunks of 32 decisions' views (32 * n_gpus * 24
 // contiguous bytes) into shared memory with asynchronous 16-byte copies
@@ -884,6 +931,38 @@ carma_status carma_pick_batch(int device, const carma_replay_config* cfg, const 
         launch_pick(*cfg, dv.as<carma_gpu_view>(), n_gpus, dr.as<carma_pick_request>(), n, dc.as<int32_t>(),
                     dout.as<int32_t>(), nullptr);
         CARMA_CUDA(cudaMemcpy(out_gpus, dout.ptr, n * 8, cudaMemcpyDeviceToHost));
+        CARMA_CUDA(cudaMemcpy(rr_cursor, dc.ptr, n * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+carma_status carma_pick_batch_wide(int device, const carma_replay_config* cfg, const carma_gpu_view* views,
+                                   uint32_t n_gpus, const carma_pick_request* reqs, uint64_t n, int32_t* rr_cursor,
+                                   int32_t* out_gpus) {
+    return guarded([&] {
+        if (!cfg) throw InvalidArg("null config");
+        if (n_gpus < 1 || n_gpus > CARMA_MAX_REPLAY_GPUS) throw Unsupported("n_gpus must be in [1, 256]");
+        if (cfg->mode == CARMA_MODE_MIG) throw Unsupported("carma_pick_batch: MIG needs per-instance views; use the replay");
+        if (!views || !reqs || !rr_cursor || !out_gpus) throw InvalidArg("null argument");
+        if (n == 0) return;
+        for (uint64_t i = 0; i < n; ++i)
+            if (reqs[i].want < 1 || reqs[i].want > CARMA_MAX_TASK_GPUS) throw Unsupported("want must be in [1, 8]");
+        require_device(device);
+        DeviceGuard guard(device);
+        DeviceBuffer dv, dr, dc, dout;
+        dv.ensure(n * n_gpus * sizeof(carma_gpu_view));
+        dr.ensure(n * sizeof(carma_pick_request));
+        dc.ensure(n * 4);
+        dout.ensure(n * 4 * CARMA_MAX_TASK_GPUS);
+        CARMA_CUDA(cudaMemcpy(dv.ptr, views, n * n_gpus * sizeof(carma_gpu_view), cudaMemcpyHostToDevice));
+        CARMA_CUDA(cudaMemcpy(dr.ptr, reqs, n * sizeof(carma_pick_request), cudaMemcpyHostToDevice));
+        CARMA_CUDA(cudaMemcpy(dc.ptr, rr_cursor, n * 4, cudaMemcpyHostToDevice));
+        carma_replay_config c = *cfg;
+        c.gpu_count = static_cast<int32_t>(n_gpus);
+        const unsigned grid = grid_for(n * 32, 128, 148u * 16u);
+        pick_kernel_wide<<<grid, 128>>>(c, dv.as<carma_gpu_view>(), n_gpus, dr.as<carma_pick_request>(), n,
+                                        dc.as<int32_t>(), dout.as<int32_t>());
+        CARMA_CUDA(cudaGetLastError());
+        CARMA_CUDA(cudaMemcpy(out_gpus, dout.ptr, n * 4 * CARMA_MAX_TASK_GPUS, cudaMemcpyDeviceToHost));
         CARMA_CUDA(cudaMemcpy(rr_cursor, dc.ptr, n * 4, cudaMemcpyDeviceToHost));
     });
 }

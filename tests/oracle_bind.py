@@ -46,6 +46,8 @@ def load_oracle() -> ctypes.CDLL:
     lib.oracle_replay.argtypes = [P, P, c_uint32, P, P, P]
     lib.oracle_pick.restype = c_int
     lib.oracle_pick.argtypes = [P, P, c_uint32, P, P, P]
+    lib.oracle_pick_wide.restype = c_int
+    lib.oracle_pick_wide.argtypes = [P, P, c_uint32, P, P, P]
     return lib
 
 

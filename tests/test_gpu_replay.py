@@ -456,3 +456,36 @@ def test_outcome_sink_streams_the_same_outcomes(gpu):
     assert abi.lib.carma_replay_plan_set_outcome_sink(plan._h, pageable.ctypes.data) == abi.CARMA_ERR_INVALID
     abi.check(abi.lib.carma_replay_plan_set_outcome_sink(plan._h, None))
     plan.close()
+
+
+def test_pick_batch_wide_matches_oracle(gpu, olib):
+    """carma_pick_batch_wide: up to 256 GPUs per snapshot, up to 8 GPUs per
+    decision, every policy, against the oracle's map_task (oracle_pick_wide)."""
+    rng = np.random.default_rng(2)
+    for g in (1, 5, 40, 64, 100, 256):
+        n = 800
+        views = np.zeros((n, g), abi.gpu_view_dtype)
+        views["total_free"] = rng.integers(0, 81, (n, g)).astype(np.uint64) * (512 * abi.MiB)
+        views["total_free"][:, ::3] = 20 * abi.GiB  # ties
+        views["windowed_smact"] = np.round(rng.random((n, g)), 1)
+        views["idle"] = rng.random((n, g)) < 0.4
+        reqs = np.zeros(n, abi.pick_request_dtype)
+        reqs["estimate"] = np.where(rng.random(n) < 0.3, abi.NO_ESTIMATE,
+                                    rng.integers(0, 45, n).astype(np.uint64) * abi.GiB)
+        reqs["want"] = rng.integers(1, min(8, g) + 1, n).astype(np.uint32)
+        reqs["from_recovery"] = rng.random(n) < 0.1
+        cursor0 = rng.integers(0, g, n).astype(np.int32)
+        for policy in ("exclusive", "rr", "magm", "lug", "mug"):
+            for rr_pre in (False, True):
+                cfg = cfg_of(policy, gpu_count=g, min_free=abi.GiB, rr_pre=rr_pre)
+                cur = cursor0.copy()
+                out = np.zeros((n, 8), np.int32)
+                abi.check(abi.lib.carma_pick_batch_wide(gpu, cfg.ctypes.data, views.ctypes.data, g,
+                                                        reqs.ctypes.data, n, cur.ctypes.data, out.ctypes.data))
+                for i in range(0, n, 3):
+                    oc = np.array([cursor0[i]], np.int32)
+                    oo = np.zeros(8, np.int32)
+                    olib.oracle_pick_wide(cfg.ctypes.data, views[i].ctypes.data, g, reqs[i: i + 1].ctypes.data,
+                                          oc.ctypes.data, oo.ctypes.data)
+                    assert out[i].tolist() == oo.tolist(), (g, policy, rr_pre, i)
+                    assert cur[i] == oc[0]
