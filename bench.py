@@ -936,7 +936,9 @@ def run_carma(args, d: Dist):
     from paper_2508_19073_b200 import abi
     from paper_2508_19073_b200 import dist as cdist
 
-    dev = d.local
+    dev = int(os.environ.get("BENCH_DEVICE", d.local))
+    if dev != d.local:
+        log(f"[rank {d.rank}] dry run: device {dev} (BENCH_DEVICE), backend {d.backend}")
     torch.cuda.set_device(dev)
     if abi.lib.carma_device_count() < 1:
         raise SystemExit("no sm_100 device visible")
@@ -1048,7 +1050,9 @@ def main():
         # the reference arm never touches the GPU or libcarma_b200.so: no NCCL
         d = Dist(args.gpus, backend="gloo")
     else:
-        d = Dist(args.gpus)
+        # BENCH_DIST_BACKEND=gloo + BENCH_DEVICE=0: a dry run of the N > 1
+        # orchestration (sharding, barrier, max-over-ranks) on one GPU
+        d = Dist(args.gpus, backend=os.environ.get("BENCH_DIST_BACKEND", "nccl"))
     try:
         if args.impl == "reference":
             run_reference(args, d)
