@@ -154,6 +154,23 @@ int bridge_estimate_pair(int family, uint64_t n, uint64_t qseed, uint64_t sample
     }
 }
 
+// LearnedEstimator::load of a snapshot written by this repository (the
+// Python LearnedEstimator.save), then estimate_learned over
+// generate_synthetic_dataset(family, n, qseed): the reference's own buckets.
+int bridge_snapshot_predict(const char* path, int family, uint64_t n, uint64_t qseed, int32_t* bucket,
+                            char* err, uint64_t err_cap) {
+    try {
+        const auto fam = static_cast<ModelFamily>(family);
+        const LearnedEstimator est = LearnedEstimator::load(path);
+        const EstimatorDataset q = generate_synthetic_dataset(fam, n, qseed);
+        for (std::size_t i = 0; i < q.rows.size(); ++i) bucket[i] = *estimate_learned(est, q.rows[i].features, fam).bucket;
+        return 0;
+    } catch (const std::exception& e) {
+        put(e.what(), err, err_cap);
+        return 1;
+    }
+}
+
 // Manager::make_estimate (bank of provision_estimators) vs the GPU bank over
 // the materialised tasks of generate_trace(mix, seed): -1 / UINT64_MAX for
 // "no estimate".

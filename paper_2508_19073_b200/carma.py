@@ -350,6 +350,23 @@ class LearnedEstimator:
     def predict(self, rows: np.ndarray) -> np.ndarray:
         return self.knn.predict(rows, default_family=self.model.family)[0]
 
+    def save(self, path: str) -> None:
+        """LearnedEstimator::save (estimators.cpp:481-501): the
+        "carma-knn-estimator/v1" JSON snapshot, same keys and order; doubles
+        in shortest round-trip form, so LearnedEstimator::load (and
+        carma_knn_load_snapshot) read back the identical state."""
+        m, h = self.model, self.holdout
+        names = {0: "mlp", 1: "cnn", 2: "transformer"}
+        doc = {"schema": "carma-knn-estimator/v1", "family": names[m.family], "bucket_range": int(m.bucket_range),
+               "k": int(m.k), "seed": int(m.seed), "lo": [float(x) for x in m.lo], "hi": [float(x) for x in m.hi],
+               "labels": [int(x) for x in m.labels], "points": [[float(x) for x in p] for p in m.points],
+               "holdout": {"accuracy": float(h.accuracy), "macro_f1": float(h.macro_f1),
+                           "train_size": int(h.train_size), "holdout_size": int(h.holdout_size),
+                           "underestimate_rate": float(h.underestimate_rate)}}
+        import json
+        with open(path, "w") as f:
+            f.write(json.dumps(doc, indent=2) + "\n")
+
 
 def train_learned_estimator(family: int, samples: int, seed: int, k: int = 5, device: int = 0,
                             knn: Optional[GpuKnn] = None) -> LearnedEstimator:

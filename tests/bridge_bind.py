@@ -37,6 +37,7 @@ def load_bridge():
                                          P, P, P, P, c_char_p, c_uint64]
     lib.bridge_manager_estimates.argtypes = [c_int, c_uint64, c_int, P, P, c_uint64, POINTER(c_uint64), c_char_p,
                                              c_uint64]
+    lib.bridge_snapshot_predict.argtypes = [c_char_p, c_int, c_uint64, c_uint64, P, c_char_p, c_uint64]
     return lib
 
 

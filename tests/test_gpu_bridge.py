@@ -4,9 +4,12 @@ gpu_run_simulation / gpu_run_sweep / GpuEstimatorBank must give the
 reference's own run_simulation / run_sweep / make_estimate results byte for
 byte (emit_report JSON of every report, the sweep CSV, every estimate), and
 fail with the same messages where the reference fails."""
+import ctypes
+
 import numpy as np
 import pytest
 
+import paper_2508_19073_b200 as cb
 from bridge_bind import GiB, MiB, case, load_bridge, run_pair, sweep_pair
 
 pytestmark = pytest.mark.gpu
@@ -32,6 +35,10 @@ RUNS = [
     dict(policy="mug", mode="mig", mig=(0.8, 0.2), seed=7, estimator="oracle"),
     dict(policy="magm", capacity=80 * GiB, block=256 * MiB, gpu_count=2, seed=8, estimator="learned"),
     dict(policy="lug", capacity=192 * GiB, gpu_count=8, seed=9, estimator="oracle"),
+    # byte-granular segment allocator (generic replay instantiations)
+    dict(policy="rr", block=0, seed=10),
+    dict(policy="magm", capacity=40 * GiB + 100 * MiB, seed=11, estimator="learned"),
+    dict(policy="magm", gpu_count=100, seed=12, estimator="oracle"),
 ]
 
 
@@ -88,3 +95,23 @@ def test_estimator_bank_equals_manager_make_estimate(bridge, mix, seed):
                                            512) == 0, err.value.decode()
     assert n.value in (60, 90)
     assert np.array_equal(r[: n.value], g[: n.value])
+
+
+@pytest.mark.parametrize("family", [0, 1, 2])
+def test_snapshot_saved_here_loads_in_the_reference(bridge, gpu, tmp_path, family):
+    """train_learned_estimator on the GPU, LearnedEstimator.save here, then the
+    reference's own LearnedEstimator::load + estimate_learned: its buckets equal
+    the GPU bank's for the same queries (the snapshot round-trips exactly)."""
+    est = cb.train_learned_estimator(family, 4000, 11 + 101 * family, 5, device=gpu)
+    path = str(tmp_path / "est.json")
+    est.save(path)
+    n, qseed = 3000, 4242
+    rb = np.zeros(n, np.int32)
+    err = ctypes.create_string_buffer(512)
+    assert bridge.bridge_snapshot_predict(path.encode(), family, n, qseed, rb.ctypes.data, err, 512) == 0, err.value
+    rows = cb.generate_synthetic_dataset(family, n, qseed).rows
+    assert np.array_equal(est.predict(rows), rb)
+    knn = cb.GpuKnn(gpu)  # and carma_knn_load_snapshot reads it back to the same predictions
+    knn.load_snapshot(path)
+    assert np.array_equal(knn.predict(rows, default_family=family)[0], rb)
+    knn.close()
