@@ -727,6 +727,9 @@ __device__ __forceinline__ void sorted_insert(float (&a)[K], float v) {
 #ifndef KNN_LAYOUT
 #define KNN_LAYOUT 0
 #endif
+#ifndef KNN_SPLIT
+#define KNN_SPLIT 4
+#endif
 #ifndef KNN_F32_CTAS
 #define KNN_F32_CTAS 4
 #endif
@@ -1278,7 +1281,10 @@ struct KnnHandle {
     carma_bit_schema schema{};
     int path = 0;  // 0 auto (fp32 pre-filter when every model allows it), 1 exact fp64 blocks, 2 fp32 pre-filter
     uint64_t last_visits = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // pipeline start, search start / end, pipeline end
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // pipeline start, (unused), (unused), pipeline end
+    static constexpr int kTimedChunks = 8;
+    cudaEvent_t sev[kTimedChunks][2] = {};  // search start / end per chunk of the last device call
+    int timed_chunks = 0;
     bool timed = false;
     uint64_t last_launches = 0, last_evals = 0;
     uint64_t last_h2d = 0;  // bytes copied host -> device by the last host-buffer call
@@ -1397,7 +1403,8 @@ bool use_f32(const KnnHandle& h) {
 uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, int32_t format,
                       const int8_t* family, int32_t default_family, uint64_t q,
                       int32_t* bucket, uint64_t* bytes, double* d2, int64_t* idx,
-                      unsigned long long* evals, cudaStream_t s) {
+                      unsigned long long* evals, cudaStream_t s, int chunk = 0,
+                      bool outer = true) {
     uint32_t n_bins = 0;
     KnnParams p = make_params(h, &n_bins);
     p.rows = rows;
@@ -1411,10 +1418,12 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
     sc.perm.ensure(q * 4);
     sc.hist.ensure(static_cast<size_t>(n_bins) * ctas * 4);
     const size_t shmem = n_bins * 4;
-    const bool timed = h.timed && h.ev[0];
+    const bool timed = h.timed && h.ev[0] && chunk < KnnHandle::kTimedChunks;
+    if (timed) h.timed_chunks = std::max(h.timed_chunks, chunk + 1);
+    cudaEvent_t* se = timed ? h.sev[chunk] : nullptr;
     if (max_k(h) > kMaxK) {  // exact brute force, query chunks bounded by the scratch
-        if (timed) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
-        if (timed) CARMA_CUDA(cudaEventRecord(h.ev[1], s));
+        if (timed && outer) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
+        if (timed) CARMA_CUDA(cudaEventRecord(se[0], s));
         const uint64_t kc = static_cast<uint64_t>(max_k(h));
         const uint64_t chunk = std::max<uint64_t>(1024, (256ull << 20) / (kc * 12));
         uint64_t launches = 0;
@@ -1441,8 +1450,8 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
             CARMA_CUDA(cudaGetLastError());
             ++launches;
         }
-        if (timed) CARMA_CUDA(cudaEventRecord(h.ev[2], s));
-        if (timed) CARMA_CUDA(cudaEventRecord(h.ev[3], s));
+        if (timed) CARMA_CUDA(cudaEventRecord(se[1], s));
+        if (timed && outer) CARMA_CUDA(cudaEventRecord(h.ev[3], s));
         return launches;
     }
     const bool f32 = use_f32(h);
@@ -1462,7 +1471,7 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
     }();
     const bool sorted = f32 && layout >= 1;
     const bool sorted_out = sorted && layout == 2 && (bucket || bytes);
-    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
+    if (timed && outer) CARMA_CUDA(cudaEventRecord(h.ev[0], s));
     if (f32 && !sorted) {
         uint64_t nkeys = 0;
         for (const auto& m : h.model)
@@ -1534,16 +1543,16 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
             sby = sc.sbytes.as<uint64_t>();
         }
     }
-    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[1], s));
+    if (timed) CARMA_CUDA(cudaEventRecord(se[0], s));
     launch_search(p, max_k(h), f32, sc.perm.as<uint32_t>(), sc.qpos.as<uint32_t>(), sb, sby, d2,
                   idx, evals, s);
-    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[2], s));
+    if (timed) CARMA_CUDA(cudaEventRecord(se[1], s));
     if (sorted_out) {
         knn_unpermute<<<static_cast<unsigned>((q + 255) / 256), 256, 0, s>>>(q, sc.perm.as<uint32_t>(), sb, sby,
                                                                           bucket, bytes);
         ++extra;
     }
-    if (timed) CARMA_CUDA(cudaEventRecord(h.ev[3], s));
+    if (timed && outer) CARMA_CUDA(cudaEventRecord(h.ev[3], s));
     CARMA_CUDA(cudaGetLastError());
     return 6 + extra;
 }
@@ -1692,6 +1701,8 @@ carma_status carma_knn_create(int device, carma_knn** out) {
         CARMA_CUDA(cudaStreamCreateWithFlags(&h->pipe[0], cudaStreamNonBlocking));
         CARMA_CUDA(cudaStreamCreateWithFlags(&h->pipe[1], cudaStreamNonBlocking));
         for (auto& e : h->ev) CARMA_CUDA(cudaEventCreate(&e));
+        for (auto& pr : h->sev)
+            for (auto& e : pr) CARMA_CUDA(cudaEventCreate(&e));
         *out = reinterpret_cast<carma_knn*>(h);
     });
 }
@@ -1721,6 +1732,9 @@ carma_status carma_knn_destroy(carma_knn* hh) {
             h->fence.destroy();
             for (auto& e : h->ev)
                 if (e) cudaEventDestroy(e);
+            for (auto& pr : h->sev)
+                for (auto& e : pr)
+                    if (e) cudaEventDestroy(e);
             cudaStreamDestroy(h->stream);
             cudaStreamDestroy(h->pipe[0]);
             cudaStreamDestroy(h->pipe[1]);
@@ -1890,9 +1904,46 @@ carma_status carma_knn_predict_device(carma_knn* hh, const void* rows, int32_t f
         h->fence.acquire(s);  // scratch[0] / evals may be in use on another stream
         CARMA_CUDA(cudaMemsetAsync(h->evals.ptr, 0, 16, s));
         h->timed = true;
-        h->last_launches = run_pipeline(*h, h->scratch[0], rows, format, family, default_family, q,
-                                        bucket_out, bytes_out, topk_d2, topk_idx,
-                                        h->evals.as<unsigned long long>(), s);
+        h->timed_chunks = 0;
+        // KNN_SPLIT chunks on the two pipeline streams: a chunk's bucketing
+        // pre-pass overlaps the previous chunk's search (CARMA_KNN_SPLIT)
+        static const int split = [] {
+            const char* e = std::getenv("CARMA_KNN_SPLIT");
+            return e ? std::atoi(e) : KNN_SPLIT;
+        }();
+        const size_t rb = format == CARMA_ROWS_FEATURES ? sizeof(carma_feature_row)
+                          : format == CARMA_ROWS_PACKED ? sizeof(carma_feature_packed)
+                          : format == CARMA_ROWS_SCALAR ? sizeof(double) * kDims
+                                                        : 0;
+        if (split > 1 && rb && q >= (uint64_t{1} << 22) && !topk_d2 && !topk_idx) {
+            cudaEvent_t ev_in, ev_out[2];
+            CARMA_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+            for (auto& e : ev_out) CARMA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CARMA_CUDA(cudaEventRecord(h->ev[0], s));
+            CARMA_CUDA(cudaEventRecord(ev_in, s));
+            for (auto ps : h->pipe) CARMA_CUDA(cudaStreamWaitEvent(ps, ev_in, 0));
+            uint64_t launches = 0;
+            for (int c = 0; c < split; ++c) {
+                const uint64_t b = q * c / split, e = q * (c + 1) / split;
+                launches += run_pipeline(*h, h->scratch[c & 1], static_cast<const char*>(rows) + b * rb, format,
+                                         family ? family + b : nullptr, default_family, e - b,
+                                         bucket_out ? bucket_out + b : nullptr, bytes_out ? bytes_out + b : nullptr,
+                                         nullptr, nullptr, h->evals.as<unsigned long long>(), h->pipe[c & 1], c,
+                                         false);
+            }
+            for (int k = 0; k < 2; ++k) {
+                CARMA_CUDA(cudaEventRecord(ev_out[k], h->pipe[k]));
+                CARMA_CUDA(cudaStreamWaitEvent(s, ev_out[k], 0));
+            }
+            CARMA_CUDA(cudaEventRecord(h->ev[3], s));
+            cudaEventDestroy(ev_in);
+            for (auto e : ev_out) cudaEventDestroy(e);
+            h->last_launches = launches;
+        } else {
+            h->last_launches = run_pipeline(*h, h->scratch[0], rows, format, family, default_family, q,
+                                            bucket_out, bytes_out, topk_d2, topk_idx,
+                                            h->evals.as<unsigned long long>(), s);
+        }
         h->fence.release(s);
     });
 }
@@ -2038,7 +2089,11 @@ carma_status carma_knn_last_timing(carma_knn* hh, double* search_ms, double* pip
         DeviceGuard g(h->device);
         CARMA_CUDA(cudaEventSynchronize(h->ev[3]));
         float a = 0.f, b = 0.f;
-        CARMA_CUDA(cudaEventElapsedTime(&a, h->ev[1], h->ev[2]));
+        for (int c = 0; c < h->timed_chunks; ++c) {  // the search kernels of every chunk
+            float x = 0.f;
+            CARMA_CUDA(cudaEventElapsedTime(&x, h->sev[c][0], h->sev[c][1]));
+            a += x;
+        }
         CARMA_CUDA(cudaEventElapsedTime(&b, h->ev[0], h->ev[3]));
         if (search_ms) *search_ms = a;
         if (pipeline_ms) *pipeline_ms = b;
