@@ -990,4 +990,10 @@ extern "C" int carma_debug_replay_prof(unsigned long long* out) {
     const unsigned long long z[16] = {};
     return cudaMemcpyToSymbol(carma_b200::replay::g_replay_prof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
 }
+extern "C" int carma_debug_replay_sub(unsigned long long* out) {
+    if (cudaMemcpyFromSymbol(out, carma_b200::replay::g_replay_sub, 8 * sizeof(unsigned long long)) != cudaSuccess)
+        return 1;
+    const unsigned long long z[8] = {};
+    return cudaMemcpyToSymbol(carma_b200::replay::g_replay_sub, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
 #endif

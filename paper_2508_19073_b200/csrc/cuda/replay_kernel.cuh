@@ -67,11 +67,18 @@ namespace replay {
 // region, summed over jobs: 0 next event, 1 integrate, 2 handle, 3 refresh,
 // 4 decide, 5 place, 6 push, 7 events.
 __device__ unsigned long long g_replay_prof[16];
+// sub-regions: 0 refresh_gpu, 1 affected list + sort, 2 re-push loop,
+// 3 decide gate / head, 4 decide inputs (free, SMACT), 5 decide pick
+__device__ unsigned long long g_replay_sub[8];
+#define RSUB_T(v) const long long v = clock64()
+#define RSUB_ADD(r, a, b) if ((threadIdx.x & 31) == 0) atomicAdd(&g_replay_sub[r], static_cast<unsigned long long>((b) - (a)))
 #define RPROF_T(v) const long long v = clock64()
 #define RPROF_ADD(r, t0) prof[r] += static_cast<unsigned long long>(clock64() - (t0))
 #else
 #define RPROF_T(v)
 #define RPROF_ADD(r, t0)
+#define RSUB_T(v)
+#define RSUB_ADD(r, a, b)
 #endif
 
 constexpr uint32_t kNone = 0xffffffffu;
@@ -612,12 +619,38 @@ __device__ __forceinline__ int inst_of(const char* b, uint32_t slot, int g) {
 }
 
 // ----------------------------------------------------------------- SMACT
+// Drops ring entries no window from `begin` on can need (an entry whose
+// successor is at or before begin only sets a level the successor
+// overrides): the rule record_smact applies, applied here too so a GPU that
+// is not touched for a while is not rescanned over its stale steps at every
+// decision. begin never decreases, so the result is unchanged. Owner lane.
+template <class L>
+__device__ __forceinline__ void prune_ring(char* b, int g, double begin) {
+    uint32_t* rh = RP_U32(rhead);
+    uint32_t* rc = RP_U32(rcnt);
+    const double* rt = RP_F64(ring_t) + g * L::RG;
+    uint32_t h = rh[g], n = rc[g];
+    const uint32_t n_in = n;
+#pragma unroll 1
+    while (n >= 2) {
+        const uint32_t second = h + 1 == static_cast<uint32_t>(L::RG) ? 0 : h + 1;
+        if (!(rt[second] <= begin)) break;
+        h = second;
+        --n;
+    }
+    if (n != n_in) {
+        rh[g] = h;
+        rc[g] = n;
+    }
+}
+
 // windowed_smact (gpu.cpp:244-267) over the ring of recent steps.
 template <class L>
 __device__ __forceinline__ double windowed(char* b, int g, double now, double window) {
     const double begin = dmax0(now - window);
     const double span = now - begin;
     if (span <= 0.0) return RP_F64(inst)[g];
+    if constexpr (L::SQ) prune_ring<L>(b, g, begin);  // long-trace tiers (measured slower on c4's)
     const double* rt = RP_F64(ring_t) + g * L::RG;
     const double* rv = RP_F64(ring_v) + g * L::RG;
     double integral = 0.0, level = 0.0, cursor = begin;
@@ -652,6 +685,10 @@ __device__ __forceinline__ void windowed2(char* b, int g0, int g1, bool v1, doub
         o0 = RP_F64(inst)[g0];
         o1 = v1 ? RP_F64(inst)[g1] : 0.0;
         return;
+    }
+    if constexpr (L::SQ) {  // long-trace tiers (measured slower on c4's)
+        prune_ring<L>(b, g0, begin);
+        if (v1) prune_ring<L>(b, g1, begin);
     }
     const double* rt0 = RP_F64(ring_t) + g0 * L::RG;
     const double* rv0 = RP_F64(ring_v) + g0 * L::RG;
@@ -791,6 +828,7 @@ __device__ __forceinline__ bool refresh_gpu(char* b, int g, double now, double w
 // World::refresh_rates (world.cpp:157-186) for the touched GPUs tg[0, nt).
 template <class L>
 __device__ __forceinline__ void refresh_rates(char* b, Sc& c, const int (&tg)[L::WM], int nt, unsigned lane) {
+    RSUB_T(ra);
     const int t0 = tg[0], t1 = tg[1];
     bool ok = true;
     if constexpr (L::MG) {
@@ -811,6 +849,8 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, const int (&tg)[L:
         c.status = kStatusRetry;
         return;
     }
+    RSUB_T(rb);
+    RSUB_ADD(0, ra, rb);
     // Affected tasks: residents of the touched GPUs, deduplicated, ordered by
     // id (std::set<std::string>) == by rank.
     const uint32_t* nres = RP_U32(nres);
@@ -881,6 +921,8 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, const int (&tg)[L:
         aff2[pos] = key;
     }
     __syncwarp();
+    RSUB_T(rc);
+    RSUB_ADD(1, rb, rc);
     const double* grate = RP_F64(rate);
     double* s_rate = RP_F64(s_rate);
     double* s_last = RP_F64(s_last);
@@ -928,6 +970,8 @@ __device__ __forceinline__ void refresh_rates(char* b, Sc& c, const int (&tg)[L:
         s_seq[slot] = seq;
     }
     __syncwarp();
+    RSUB_T(rd);
+    RSUB_ADD(2, rc, rd);
 }
 
 // World::place (world.cpp:73-130) without the trailing refresh_rates:
@@ -1172,6 +1216,7 @@ template <class L>
 __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, const uint64_t* est,
                                       uint32_t& head, bool& from_recovery, int (&gl)[L::WM], int (&il)[L::WM],
                                       uint64_t& est_bytes, unsigned lane, bool seg_mode = false) {
+    RSUB_T(da);
     const carma_replay_config& cf = RP_CFG;
     const int G = cf.gpu_count;
     const uint32_t* nres = RP_U32(nres);
@@ -1198,6 +1243,8 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
             if (need > floor) floor = need;
         }
     }
+    RSUB_T(db);
+    RSUB_ADD(3, da, db);
     constexpr bool mig = L::MIG;
     // pick_instance's bar (manager.cpp:125-134): max(need, 1) bytes; 1 for exclusive
     const uint64_t inst_need = need > 1 ? need : 1;
@@ -1244,7 +1291,11 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
             if (j + 1 < L::GPL) in[j + 1].smact = s1;
         }
     }
+    RSUB_T(dc);
+    RSUB_ADD(4, db, dc);
     const int got = pick_gpus<L::GPL>(cf, policy, tasks[head].gpus, floor, in, lane, 0, 32, c.rr_cursor, gl);
+    RSUB_T(dd);
+    RSUB_ADD(5, dc, dd);
     const int g0 = gl[0], g1 = gl[1];
 #pragma unroll
     for (int k = 0; k < L::WM; ++k) il[k] = 0;

@@ -125,6 +125,11 @@ def fused(args):
         print(f"  heap pops {v[9]}, mean heap size {v[8] / max(v[9], 1):.1f}; decides {v[11]}, with a head {v[10]}; "
               f"refreshes {v[13]}, mean residents on touched GPUs {v[12] / max(v[13], 1):.2f}, "
               f"mean ring entries {v[14] / max(v[13], 1):.2f}; pushes {v[15]}")
+        u = (ctypes.c_ulonglong * 8)()
+        abi.lib.carma_debug_replay_sub(u)
+        for n, x in zip(["refresh_gpu", "affected+sort", "re-push loop", "decide gate/head", "decide inputs",
+                         "decide pick"], u):
+            print(f"    {n:16s} {x / max(v[7], 1):8.1f} cyc/event")
 
 
 def scoring(args):
