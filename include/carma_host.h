@@ -94,6 +94,11 @@ carma_status carma_host_check_log1p(uint64_t n, uint64_t seed, uint64_t* mismatc
 /* scalar_features for n feature rows -> n x 19 doubles. */
 carma_status carma_host_scalar_features(const carma_feature_row* rows, uint64_t n, double* out);
 
+/* Self-check of the device dataset generator's mt19937_64 jump-ahead tables
+ * (characteristic polynomial by Berlekamp-Massey, x^(156 2^(13+b)) mod P): the
+ * jumped window vs stepping the recurrence; *mismatches = differing words. */
+carma_status carma_host_check_mt_jump(uint64_t seed, int32_t b, uint64_t* mismatches);
+
 #ifdef __cplusplus
 }
 #endif

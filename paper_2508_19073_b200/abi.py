@@ -207,6 +207,7 @@ SIGNATURES = {
     "carma_knn_load_snapshot_file": (c_int, [c_void_p, c_char_p, POINTER(c_int32), P]),
     # carma_host.h
     "carma_host_check_log1p": (c_int, [c_uint64, c_uint64, POINTER(c_uint64)]),
+    "carma_host_check_mt_jump": (c_int, [c_uint64, c_int32, POINTER(c_uint64)]),
     "carma_host_parse_snapshot": (c_int, [c_char_p, c_uint64, POINTER(c_int32), POINTER(c_uint64),
                                           POINTER(c_uint64), POINTER(c_uint64), P, P, P, P, c_uint64,
                                           POINTER(c_uint64), P]),

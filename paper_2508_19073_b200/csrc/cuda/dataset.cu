@@ -206,12 +206,19 @@ __device__ __forceinline__ bool eval_row(const DsConst& c, const uint64_t* __res
 // neighbour's word of two steps back (thread 155: thread 0's of one step
 // back). st[0..311] holds the 312 state words preceding the call and is
 // updated to the 312 words following it. out[k] = temper(x[312 + k]).
-__global__ void __launch_bounds__(kHalf) ds_mt_gen(uint64_t* __restrict__ st, uint64_t* __restrict__ out,
-                                                   uint32_t steps) {
+// Multi-segment form: CTA c starts from the window starts[c] (the state
+// jumped c * seg_steps * 156 words ahead, ds_mt_jump) and emits its segment
+// out[c * seg_steps * 156 ...]; the last CTA's final window goes to st.
+__global__ void __launch_bounds__(kHalf) ds_mt_gen(uint64_t* __restrict__ st, const uint64_t* __restrict__ starts,
+                                                   uint64_t* __restrict__ out, uint32_t seg_steps, uint32_t last_steps) {
     constexpr uint64_t kUpper = 0xFFFFFFFF80000000ull, kLower = 0x7FFFFFFFull, kA = 0xB5026F5AA96619E9ull;
     __shared__ uint64_t ring[3][kHalf];
     const int t = threadIdx.x;
-    uint64_t p2 = st[t], p1 = st[kHalf + t];  // own words of steps s-2, s-1
+    const bool last = blockIdx.x + 1 == gridDim.x;
+    const uint32_t steps = last ? last_steps : seg_steps;
+    const uint64_t* w0 = starts ? starts + static_cast<uint64_t>(blockIdx.x) * kMt : st;
+    out += static_cast<uint64_t>(blockIdx.x) * seg_steps * kHalf;
+    uint64_t p2 = w0[t], p1 = w0[kHalf + t];  // own words of steps s-2, s-1
     ring[1][t] = p2;                          // slot (s mod 3) holds step s; s = -2 -> 1, -1 -> 2
     ring[2][t] = p1;
     __syncthreads();
@@ -231,8 +238,58 @@ __global__ void __launch_bounds__(kHalf) ds_mt_gen(uint64_t* __restrict__ st, ui
         p1 = v;
         __syncthreads();
     }
-    st[t] = p2;
-    st[kHalf + t] = p1;
+    if (last) {
+        st[t] = p2;
+        st[kHalf + t] = p1;
+    }
+}
+
+// Jump-ahead (the engine is F2-linear: the window after k words is g(A)
+// applied to the window, g = x^k mod the characteristic polynomial). CTA c
+// composes the jumps of the set bits of c (polys[b] = x^(J 2^b) mod P) with
+// Horner's rule on a 312-word circular window in shared memory: per bit of
+// g, advance the accumulator one word (one thread: x[j+312] = x[j+156] ^
+// f(x[j], x[j+1])), then add the input window if the bit is set (all
+// threads). One warp: __syncwarp is the only barrier.
+constexpr int kPolyWords = 312;  // 19968 bits >= deg P + 1 = 19938
+__global__ void __launch_bounds__(32) ds_mt_jump(const uint64_t* __restrict__ st, const uint64_t* __restrict__ polys,
+                                                 const int32_t* __restrict__ degs, int n_polys,
+                                                 uint64_t* __restrict__ starts) {
+    constexpr uint64_t kUpper = 0xFFFFFFFF80000000ull, kLower = 0x7FFFFFFFull, kA = 0xB5026F5AA96619E9ull;
+    __shared__ uint64_t R[kMt], T[kMt];
+    const unsigned lane = threadIdx.x;
+    const uint32_t c = blockIdx.x;
+    for (int k = lane; k < kMt; k += 32) R[k] = st[k];
+    __syncwarp();
+    for (int b = 0; b < n_polys; ++b) {
+        if (!((c >> b) & 1u)) continue;
+        const uint64_t* g = polys + static_cast<uint64_t>(b) * kPolyWords;
+        for (int k = lane; k < kMt; k += 32) T[k] = 0;
+        uint32_t h = 0;  // T's first word
+        __syncwarp();
+        for (int i = degs[b]; i >= 0; --i) {
+            if (lane == 0) {  // T = A T
+                const uint32_t h1 = h + 1 == kMt ? 0 : h + 1, hm = h + 156 >= kMt ? h + 156 - kMt : h + 156;
+                const uint64_t y = (T[h] & kUpper) | (T[h1] & kLower);
+                T[h] = T[hm] ^ (y >> 1) ^ ((y & 1ull) ? kA : 0ull);
+            }
+            h = h + 1 == kMt ? 0 : h + 1;
+            __syncwarp();
+            if ((g[i >> 6] >> (i & 63)) & 1ull) {  // T += R
+                for (int k = lane; k < kMt; k += 32) {
+                    const uint32_t x = h + k >= kMt ? h + k - kMt : h + k;
+                    T[x] ^= R[k];
+                }
+                __syncwarp();
+            }
+        }
+        for (int k = lane; k < kMt; k += 32) {
+            const uint32_t x = h + k >= kMt ? h + k - kMt : h + k;
+            R[k] = T[x];
+        }
+        __syncwarp();
+    }
+    for (int k = lane; k < kMt; k += 32) starts[static_cast<uint64_t>(c) * kMt + k] = R[k];
 }
 
 // ---------------------------------------------------------------- row boundaries
@@ -353,6 +410,141 @@ __global__ void ds_carry(uint64_t* w, const DsRound* res, uint64_t V) {
     for (uint64_t i = threadIdx.x; tail + i < V; i += blockDim.x) w[i] = w[tail + i];
 }
 
+// ------------------------------------------------ jump-ahead (host side)
+// The characteristic polynomial of the mt19937_64 transition (degree 19937)
+// by Berlekamp-Massey over one bit of the raw state sequence, and the jump
+// polynomials x^(J 2^b) mod P (J = 156 * 2^kSegLog2 words), by squaring.
+using Poly = std::vector<uint64_t>;  // bit i = coefficient of x^i
+
+int poly_deg(const Poly& p) {
+    for (size_t w = p.size(); w-- > 0;)
+        if (p[w]) return static_cast<int>(w * 64 + 63 - __builtin_clzll(p[w]));
+    return -1;
+}
+
+// The raw window sequence from a seed (the host twin of the device recurrence).
+void mt_raw_words(uint64_t seed, std::vector<uint64_t>& x, size_t n) {
+    constexpr uint64_t kUpper = 0xFFFFFFFF80000000ull, kLower = 0x7FFFFFFFull, kA = 0xB5026F5AA96619E9ull;
+    x.assign(n, 0);
+    x[0] = seed;
+    for (size_t i = 1; i < kMt; ++i) x[i] = 6364136223846793005ull * (x[i - 1] ^ (x[i - 1] >> 62)) + i;
+    for (size_t j = kMt; j < n; ++j) {
+        const uint64_t y = (x[j - kMt] & kUpper) | (x[j - kMt + 1] & kLower);
+        x[j] = x[j - kHalf] ^ (y >> 1) ^ ((y & 1ull) ? kA : 0ull);
+    }
+}
+
+// Berlekamp-Massey over GF(2): the connection polynomial C of the bit
+// sequence s (C(x) = 1 + c1 x + ... ; the characteristic polynomial is its
+// reciprocal).
+Poly berlekamp_massey(const std::vector<uint8_t>& s) {
+    const size_t n = s.size(), W = (n + 64) / 64 + 1;
+    Poly C(W, 0), B(W, 0);
+    C[0] = B[0] = 1;
+    int L = 0;
+    long m = -1;
+    for (size_t N = 0; N < n; ++N) {
+        uint8_t d = s[N];
+        for (int i = 1; i <= L; ++i) d ^= static_cast<uint8_t>((C[i >> 6] >> (i & 63)) & 1ull) & s[N - i];
+        if (!d) continue;
+        const Poly T = C;
+        const size_t sh = N - static_cast<size_t>(m);  // C ^= B << sh
+        const size_t ws = sh / 64, bs = sh % 64;
+        for (size_t w = W; w-- > ws;) {
+            uint64_t v = B[w - ws] << bs;
+            if (bs && w - ws > 0) v |= B[w - ws - 1] >> (64 - bs);
+            C[w] ^= v;
+        }
+        if (2 * L <= static_cast<int>(N)) {
+            L = static_cast<int>(N) + 1 - L;
+            m = static_cast<long>(N);
+            B = T;
+        }
+    }
+    // characteristic polynomial = x^L C(1/x): reverse the first L + 1 coefficients
+    Poly P(kPolyWords, 0);
+    for (int i = 0; i <= L; ++i)
+        if ((C[i >> 6] >> (i & 63)) & 1ull) {
+            const int j = L - i;
+            P[j >> 6] |= 1ull << (j & 63);
+        }
+    return P;
+}
+
+// a * a mod P (deg a < deg P).
+Poly poly_sqr_mod(const Poly& a, const Poly& P, int dp) {
+    Poly r(2 * kPolyWords + 1, 0);
+    for (int i = 0; i <= poly_deg(a); ++i)
+        if ((a[i >> 6] >> (i & 63)) & 1ull) {
+            const int j = 2 * i;
+            r[j >> 6] |= 1ull << (j & 63);
+        }
+    for (int i = poly_deg(r); i >= dp; --i) {
+        if (!((r[i >> 6] >> (i & 63)) & 1ull)) continue;
+        const int sh = i - dp;  // r ^= P << sh
+        const int ws = sh / 64, bs = sh % 64;
+        for (int w = kPolyWords - 1; w >= 0; --w) {
+            if (!P[w]) continue;
+            r[w + ws] ^= P[w] << bs;
+            if (bs && w + ws + 1 < static_cast<int>(r.size())) r[w + ws + 1] ^= P[w] >> (64 - bs);
+        }
+    }
+    r.resize(kPolyWords);
+    return r;
+}
+
+constexpr int kSegLog2 = 13;    // segment = 156 * 2^13 = 1,277,952 words
+constexpr int kJumpPolys = 9;   // up to 512 segments per round
+
+struct JumpTables {
+    Poly P;
+    int deg = 0;
+    std::vector<uint64_t> polys;  // kJumpPolys x kPolyWords: x^(156 * 2^(kSegLog2 + b)) mod P
+    std::vector<int32_t> degs;
+};
+
+const JumpTables& jump_tables() {
+    static const JumpTables t = [] {
+        JumpTables j;
+        std::vector<uint64_t> x;
+        const size_t nb = 2 * 19937 + 64;
+        mt_raw_words(5489, x, kMt + nb);
+        std::vector<uint8_t> bits(nb);
+        for (size_t i = 0; i < nb; ++i) bits[i] = static_cast<uint8_t>(x[kMt + i] & 1ull);
+        j.P = berlekamp_massey(bits);
+        j.deg = poly_deg(j.P);
+        if (j.deg != 19937) throw CudaFailure("mt19937_64 characteristic polynomial: unexpected degree");
+        Poly g(kPolyWords, 0);
+        g[156 >> 6] |= 1ull << (156 & 63);  // x^156
+        for (int k = 0; k < kSegLog2; ++k) g = poly_sqr_mod(g, j.P, j.deg);
+        for (int b = 0; b < kJumpPolys; ++b) {
+            if (b > 0) g = poly_sqr_mod(g, j.P, j.deg);
+            j.polys.insert(j.polys.end(), g.begin(), g.end());
+            j.degs.push_back(poly_deg(g));
+        }
+        return j;
+    }();
+    return t;
+}
+
+// Host Horner: the window w advanced by the jump g (for the self-check).
+std::vector<uint64_t> host_jump(const std::vector<uint64_t>& w, const uint64_t* g, int deg) {
+    constexpr uint64_t kUpper = 0xFFFFFFFF80000000ull, kLower = 0x7FFFFFFFull, kA = 0xB5026F5AA96619E9ull;
+    std::vector<uint64_t> T(kMt, 0);
+    uint32_t h = 0;
+    for (int i = deg; i >= 0; --i) {
+        const uint32_t h1 = h + 1 == kMt ? 0 : h + 1, hm = h + 156 >= kMt ? h + 156 - kMt : h + 156;
+        const uint64_t y = (T[h] & kUpper) | (T[h1] & kLower);
+        T[h] = T[hm] ^ (y >> 1) ^ ((y & 1ull) ? kA : 0ull);
+        h = h1;
+        if ((g[i >> 6] >> (i & 63)) & 1ull)
+            for (uint32_t k = 0; k < kMt; ++k) T[(h + k) % kMt] ^= w[k];
+    }
+    std::vector<uint64_t> r(kMt);
+    for (uint32_t k = 0; k < kMt; ++k) r[k] = T[(h + k) % kMt];
+    return r;
+}
+
 DsConst make_const(int32_t family) {
     if (family < 0 || family > 2) throw InvalidArg("unknown model family");
     const Bounds b = Bounds::for_family(static_cast<Family>(family));
@@ -410,6 +602,7 @@ void generate_dataset_device(int32_t family, uint64_t n, uint64_t seed, carma_fe
     for (int i = 1; i < kMt; ++i) init[i] = 6364136223846793005ull * (init[i - 1] ^ (init[i - 1] >> 62)) + i;
 
     DeviceBuffer d_state, d_w, d_maps, d_entry, d_counts, d_roff, d_starts, d_flags, d_aidx, d_res, d_tmp;
+    DeviceBuffer d_polys, d_degs, d_seg;  // jump-ahead tables, segment start windows
     PinnedBuffer h_res;
     h_res.ensure(sizeof(DsRound));
     d_state.ensure(kMt * 8);
@@ -455,7 +648,29 @@ void generate_dataset_device(int32_t family, uint64_t n, uint64_t seed, carma_fe
         d_tmp.ensure(std::max(tmp1, tmp2));
 
         uint64_t* w = d_w.as<uint64_t>();
-        ds_mt_gen<<<1, kHalf, 0, s>>>(d_state.as<uint64_t>(), w + carried, static_cast<uint32_t>(steps));
+        // the stream: segments of 156 * 2^kSegLog2 words, one CTA each, from
+        // windows jumped ahead on the device
+        constexpr uint64_t seg_steps = 1ull << kSegLog2;
+        const uint64_t n_seg = (steps + seg_steps - 1) / seg_steps;
+        const uint32_t last_steps = static_cast<uint32_t>(steps - (n_seg - 1) * seg_steps);
+        if (n_seg > 1) {
+            if (n_seg > (1ull << kJumpPolys)) throw CudaFailure("dataset generator: too many stream segments");
+            const JumpTables& jt = jump_tables();
+            if (!d_polys.ptr) {
+                d_polys.ensure(jt.polys.size() * 8);
+                d_degs.ensure(jt.degs.size() * 4);
+                CARMA_CUDA(cudaMemcpyAsync(d_polys.ptr, jt.polys.data(), jt.polys.size() * 8, cudaMemcpyHostToDevice, s));
+                CARMA_CUDA(cudaMemcpyAsync(d_degs.ptr, jt.degs.data(), jt.degs.size() * 4, cudaMemcpyHostToDevice, s));
+            }
+            d_seg.ensure(n_seg * kMt * 8);
+            ds_mt_jump<<<static_cast<unsigned>(n_seg), 32, 0, s>>>(d_state.as<uint64_t>(), d_polys.as<uint64_t>(),
+                                                                   d_degs.as<int32_t>(), kJumpPolys, d_seg.as<uint64_t>());
+            ds_mt_gen<<<static_cast<unsigned>(n_seg), kHalf, 0, s>>>(d_state.as<uint64_t>(), d_seg.as<uint64_t>(),
+                                                                     w + carried, static_cast<uint32_t>(seg_steps),
+                                                                     last_steps);
+        } else {
+            ds_mt_gen<<<1, kHalf, 0, s>>>(d_state.as<uint64_t>(), nullptr, w + carried, last_steps, last_steps);
+        }
         CARMA_CUDA(cudaGetLastError());
         // boundary maps and the composition tree
         std::vector<uint8_t*> lmap(level_n.size()), lent(level_n.size());
@@ -566,3 +781,26 @@ carma_status carma_dataset_generate(int32_t device, int32_t family, uint64_t n, 
 }
 
 }  // extern "C"
+
+// Self-check of the jump-ahead math on the host (tests): the window jumped by
+// polynomial b of the device tables equals the window reached by stepping
+// 156 * 2^(kSegLog2 + b) words (the first word's low 31 bits, which no later
+// word depends on, excluded). *mismatches = differing words.
+extern "C" carma_status carma_host_check_mt_jump(uint64_t seed, int32_t b, uint64_t* mismatches) {
+    return carma_b200::guarded([&] {
+        using namespace carma_b200;
+        if (!mismatches || b < 0 || b > 2) throw InvalidArg("bad argument");
+        const JumpTables& jt = jump_tables();
+        const uint64_t k = 156ull << (kSegLog2 + b);
+        std::vector<uint64_t> x;
+        mt_raw_words(seed, x, kMt + k + 1);
+        const std::vector<uint64_t> w0(x.begin(), x.begin() + kMt);
+        const std::vector<uint64_t> wj = host_jump(w0, jt.polys.data() + static_cast<size_t>(b) * kPolyWords, jt.degs[b]);
+        uint64_t bad = 0;
+        for (int i = 0; i < kMt; ++i) {
+            const uint64_t mask = i == 0 ? 0xFFFFFFFF80000000ull : ~0ull;
+            bad += ((wj[i] ^ x[k + i]) & mask) != 0;
+        }
+        *mismatches = bad;
+    });
+}

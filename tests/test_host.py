@@ -219,3 +219,16 @@ def test_device_log1p_is_glibc_bit_for_bit():
     bad = ctypes.c_uint64()
     abi.check(abi.lib.carma_host_check_log1p(6_000_000, 12345, ctypes.byref(bad)))
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("b", [0, 1, 2])
+def test_mt_jump_ahead_tables(b):
+    """The device dataset generator's jump-ahead (csrc/cuda/dataset.cu): the
+    characteristic polynomial of mt19937_64 (Berlekamp-Massey) and
+    x^(156 * 2^(13+b)) mod P applied by Horner's rule give exactly the window
+    that stepping the recurrence reaches."""
+    import ctypes
+    for seed in (1, 2**63 + 5):
+        m = ctypes.c_uint64()
+        abi.check(abi.lib.carma_host_check_mt_jump(seed, b, ctypes.byref(m)))
+        assert m.value == 0
