@@ -390,7 +390,13 @@ typedef struct carma_replay_config {
      * the host. They do not change the run. */
     int32_t log_flags;
     int32_t log_reserved;
-} carma_replay_config; /* 216 bytes */
+    /* CARMA_MODE_MIG: the same instance table in bytes (carma_mig_layout
+     * fills both); the replay uses it on byte-granular devices (alloc_block
+     * = 0 or a capacity that is not a block multiple, where instance
+     * boundaries need not fall on blocks). */
+    uint64_t mig_base_bytes[CARMA_MAX_MIG];
+    uint64_t mig_cap_bytes[CARMA_MAX_MIG];
+} carma_replay_config; /* 344 bytes */
 
 /* One materialised task (TaskSpec, task.hpp:63-80) as the replay sees it. */
 typedef struct carma_task {

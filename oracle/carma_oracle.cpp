@@ -155,8 +155,8 @@ struct Sim {
         return s;
     }
     bool mig() const { return c.mode == CARMA_MODE_MIG; }
-    uint64_t inst_base(int i) const { return static_cast<uint64_t>(c.mig_base[i]) * c.alloc_block; }
-    uint64_t inst_cap(int i) const { return static_cast<uint64_t>(c.mig_blocks[i]) * c.alloc_block; }
+    uint64_t inst_base(int i) const { return c.mig_base_bytes[i]; }
+    uint64_t inst_cap(int i) const { return c.mig_cap_bytes[i]; }
     // gpu.cpp:72-114
     bool allocate_range(Gpu& g, uint64_t range_begin, uint64_t range_end, uint64_t bytes, uint64_t* off,
                         uint64_t* size) {

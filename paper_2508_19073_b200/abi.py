@@ -59,6 +59,7 @@ replay_config_dtype = np.dtype([
     ("mig_count", "<i4"), ("mig_reserved", "<i4"), ("mig_fraction", "<f8", (8,)),
     ("mig_base", "<u2", (8,)), ("mig_blocks", "<u2", (8,)), ("sample_interval", "<f8"),
     ("log_flags", "<i4"), ("log_reserved", "<i4"),
+    ("mig_base_bytes", "<u8", (8,)), ("mig_cap_bytes", "<u8", (8,)),
 ], align=True)
 
 dataset_stats_dtype = np.dtype([
@@ -124,7 +125,7 @@ assert nn_spec_dtype.itemsize == 464
 assert feature_row_dtype.itemsize == 136
 assert feature_packed_dtype.itemsize == 64
 assert task_outcome_dtype.itemsize == 24
-assert replay_config_dtype.itemsize == 216
+assert replay_config_dtype.itemsize == 344
 assert task_dtype.itemsize == 48
 assert task_result_dtype.itemsize == 64
 assert trace_result_dtype.itemsize == 80

@@ -264,22 +264,25 @@ void validate_config(const carma_replay_config& c) {
     // alloc_block = 0, capacities that are not a block multiple and more than
     // 4096 blocks run on the byte-granular segment allocator of the generic
     // instantiations (needs_segments); MIG instance tables stay block-based.
-    if (c.mode == CARMA_MODE_MIG && needs_segments(c))
-        throw Unsupported("MIG needs alloc_block > 0, a block-multiple capacity and <= 4096 blocks");
+    // (MIG on a byte-granular device uses the byte instance table)
     if (!(c.sample_interval >= 0.0)) throw InvalidArg("ConfigError: sample_interval must be >= 0");
     if (c.log_flags & ~(CARMA_LOG_EVENTS | CARMA_LOG_DECISIONS)) throw InvalidArg("unknown log_flags bits");
     if (c.mode == CARMA_MODE_MIG) {
         // the table carma_mig_layout builds (gpu.cpp:29-51)
         if (c.mig_count < 1 || c.mig_count > CARMA_MAX_MIG)
             throw InvalidArg("ConfigError: MIG mode needs 1..8 instances (carma_mig_layout)");
-        uint64_t end = 0;
+        uint64_t end = 0, end_b = 0;
+        const bool seg = needs_segments(c);
         for (int i = 0; i < c.mig_count; ++i) {
             if (!(c.mig_fraction[i] > 0.0) || c.mig_fraction[i] > 1.0)
                 throw InvalidArg("ConfigError: mig instance fraction out of (0, 1]");
-            if (c.mig_base[i] != end) throw InvalidArg("ConfigError: MIG instances must tile the device in order");
+            if (c.mig_base_bytes[i] != end_b || (!seg && c.mig_base[i] != end))
+                throw InvalidArg("ConfigError: MIG instances must tile the device in order (carma_mig_layout)");
             end += c.mig_blocks[i];
+            end_b += c.mig_cap_bytes[i];
         }
-        if (end > c.gpu_capacity / c.alloc_block) throw InvalidArg("ConfigError: mig instances exceed capacity");
+        if (end_b > c.gpu_capacity || (!seg && end > c.gpu_capacity / c.alloc_block))
+            throw InvalidArg("ConfigError: mig instances exceed capacity");
     }
 }
 

@@ -531,6 +531,22 @@ __device__ __forceinline__ bool seg_alloc(char* b, int g, uint64_t capacity, uin
     return false;
 }
 
+// Free bytes of the segments clipped to [r0, r1) (instance_free, gpu.cpp:151-160).
+template <class L>
+__device__ __forceinline__ uint64_t seg_free_in_range(const char* b, int g, uint64_t r0, uint64_t r1) {
+    const uint64_t* so = reinterpret_cast<const uint64_t*>(b + L::seg_off) + g * L::NSEG;
+    const uint64_t* sl = reinterpret_cast<const uint64_t*>(b + L::seg_len) + g * L::NSEG;
+    const uint32_t n = reinterpret_cast<const uint32_t*>(b + L::seg_n)[g];
+    uint64_t f = 0;
+#pragma unroll 1
+    for (uint32_t i = 0; i < n; ++i) {
+        if (sl[i] & kSegUsed) continue;
+        const uint64_t lo = so[i] > r0 ? so[i] : r0, end = so[i] + sl[i], hi = end < r1 ? end : r1;
+        if (lo < hi) f += hi - lo;
+    }
+    return f;
+}
+
 // free_region (gpu.cpp:116-130): mark free, coalesce right then left.
 template <class L>
 __device__ __forceinline__ void seg_release(char* b, int g, uint64_t off, uint64_t size) {
@@ -1013,8 +1029,9 @@ __device__ __forceinline__ bool place(char* b, Sc& c, const carma_task& tk, uint
             if (seg) {
                 uint64_t o = 0, f = 0, lg = 0;
                 bool okk = false, ovf = false;
-                if ((g & 31) == static_cast<int>(lane))
-                    okk = seg_alloc<L>(b, g, cf.gpu_capacity, 0, cf.gpu_capacity, want_b, o, f, lg, ovf);
+                const uint64_t r0 = mig ? cf.mig_base_bytes[il[k]] : 0;
+                const uint64_t r1 = mig ? r0 + cf.mig_cap_bytes[il[k]] : cf.gpu_capacity;
+                if ((g & 31) == static_cast<int>(lane)) okk = seg_alloc<L>(b, g, cf.gpu_capacity, r0, r1, want_b, o, f, lg, ovf);
                 okk = __shfl_sync(0xffffffffu, okk, g & 31);
                 ovf = __shfl_sync(0xffffffffu, ovf, g & 31);
                 o = __shfl_sync(0xffffffffu, o, g & 31);
@@ -1270,8 +1287,11 @@ __device__ __forceinline__ int decide(char* b, Sc& c, const carma_task* tasks, c
             for (int i = 0; i < cf.mig_count; ++i) {
                 if ((busy >> i) & 1u) continue;
                 const int r0 = cf.mig_base[i];
-                const uint64_t fb = static_cast<uint64_t>(free_in_range<L>(used, g, r0, r0 + cf.mig_blocks[i])) *
-                                    cf.alloc_block;
+                uint64_t fb;
+                if (L::MG && seg_mode)
+                    fb = seg_free_in_range<L>(b, g, cf.mig_base_bytes[i], cf.mig_base_bytes[i] + cf.mig_cap_bytes[i]);
+                else
+                    fb = static_cast<uint64_t>(free_in_range<L>(used, g, r0, r0 + cf.mig_blocks[i])) * cf.alloc_block;
                 if (fb < inst_need) continue;
                 inst[j] = i;
                 break;
@@ -1333,8 +1353,8 @@ __device__ __noinline__ void init_job(char* b, const Params& p, uint32_t j, unsi
                                       const carma_task*& tasks, carma_task_result*& out, int& nblk) {
     const carma_replay_job job = p.jobs[j];
     const carma_replay_config* src = p.cfgs + job.config;
-    if (lane < sizeof(carma_replay_config) / 8)
-        reinterpret_cast<uint64_t*>(b + L::cfg)[lane] = reinterpret_cast<const uint64_t*>(src)[lane];
+    for (uint32_t k = lane; k < sizeof(carma_replay_config) / 8; k += 32)  // 43 words
+        reinterpret_cast<uint64_t*>(b + L::cfg)[k] = reinterpret_cast<const uint64_t*>(src)[k];
     __syncwarp();
     const carma_replay_config& cf = RP_CFG;
     const uint64_t tb = p.trace_off[job.trace];

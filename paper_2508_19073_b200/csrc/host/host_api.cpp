@@ -282,20 +282,28 @@ carma_status carma_mig_layout(const double* fractions, uint32_t n, carma_replay_
         }
         if (sum > 1.0 + 1e-9) throw InvalidArg("ConfigError: mig instance fractions exceed the device");
         const uint64_t capacity = cfg->gpu_capacity, block = cfg->alloc_block;
-        if (block == 0 || capacity % block != 0) throw Unsupported("MIG needs gpu_capacity to be a multiple of alloc_block");
-        auto round_up = [&](uint64_t b) { return (b + block - 1) / block * block; };
+        // gpu.cpp:58-61: round_up is the identity for alloc_block = 0
+        auto round_up = [&](uint64_t b) { return block == 0 ? b : (b + block - 1) / block * block; };
+        // block tables (mig_base / mig_blocks) only where the bitmap applies
+        const bool blocks = block != 0 && capacity % block == 0 && capacity / block <= 4096;
         uint64_t base = 0;
         carma_replay_config c = *cfg;
         std::memset(c.mig_fraction, 0, sizeof(c.mig_fraction));
         std::memset(c.mig_base, 0, sizeof(c.mig_base));
         std::memset(c.mig_blocks, 0, sizeof(c.mig_blocks));
+        std::memset(c.mig_base_bytes, 0, sizeof(c.mig_base_bytes));
+        std::memset(c.mig_cap_bytes, 0, sizeof(c.mig_cap_bytes));
         for (std::size_t i = 0; i < f.size(); ++i) {
             uint64_t cap = round_up(static_cast<uint64_t>(f[i] * static_cast<double>(capacity)));
             cap = std::min(cap, capacity - base);
             if (i + 1 == f.size() && sum > 1.0 - 1e-9) cap = capacity - base;
             c.mig_fraction[i] = f[i];
-            c.mig_base[i] = static_cast<uint16_t>(base / block);
-            c.mig_blocks[i] = static_cast<uint16_t>(cap / block);
+            if (blocks) {
+                c.mig_base[i] = static_cast<uint16_t>(base / block);
+                c.mig_blocks[i] = static_cast<uint16_t>(cap / block);
+            }
+            c.mig_base_bytes[i] = base;
+            c.mig_cap_bytes[i] = cap;
             base += cap;
         }
         if (base > capacity) throw InvalidArg("ConfigError: mig instances exceed capacity");

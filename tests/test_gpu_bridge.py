@@ -39,6 +39,7 @@ RUNS = [
     dict(policy="rr", block=0, seed=10),
     dict(policy="magm", capacity=40 * GiB + 100 * MiB, seed=11, estimator="learned"),
     dict(policy="magm", gpu_count=100, seed=12, estimator="oracle"),
+    dict(policy="magm", mode="mig", mig=(0.75, 0.25), block=0, seed=13),
 ]
 
 

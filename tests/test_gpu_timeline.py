@@ -19,7 +19,10 @@ CASES = [dict(policy="magm", interval=10.0), dict(policy="rr", interval=7.3),
          dict(policy="magm", interval=10.0, mode="mig", mig=(0.75, 0.25)),
          # byte-granular allocator (generic instantiations): alloc_block 0, non-multiple capacity
          dict(policy="rr", interval=7.3, block=0),
-         dict(policy="magm", interval=10.0, capacity=40 * 2**30 + 100 * 2**20)]
+         dict(policy="magm", interval=10.0, capacity=40 * 2**30 + 100 * 2**20),
+         # MIG on a byte-granular device: instance boundaries in bytes
+         dict(policy="magm", interval=10.0, mode="mig", mig=(0.7, 0.3), block=0),
+         dict(policy="lug", interval=7.3, mode="mig", mig=(0.75, 0.25), capacity=40 * 2**30 + 100 * 2**20)]
 
 
 @pytest.mark.parametrize("case", CASES, ids=[str(i) for i in range(len(CASES))])
@@ -57,7 +60,8 @@ def test_timeline_off_is_unchanged(gpu):
 
 LOG_CASES = [dict(policy="magm"), dict(policy="rr"), dict(policy="lug", estimator="oracle"),
              dict(policy="magm", mode="mig", mig=(0.75, 0.25)), dict(policy="exclusive", gpu_count=8),
-             dict(policy="rr", block=0), dict(policy="rr", capacity=40 * 2**30 + 100 * 2**20)]
+             dict(policy="rr", block=0), dict(policy="rr", capacity=40 * 2**30 + 100 * 2**20),
+             dict(policy="magm", mode="mig", mig=(0.75, 0.25), block=0)]
 
 
 @pytest.mark.parametrize("case", LOG_CASES, ids=[str(i) for i in range(len(LOG_CASES))])

@@ -234,3 +234,17 @@ def test_oracle_byte_granular_allocator_matches_reference(ref, olib, capacity, b
             assert np.array_equal(ot["complete"], tout["complete"]) and np.array_equal(ot["ooms"], tout["ooms"])
             assert otr["energy_mj"] == rout["energy_mj"] and otr["avg_jct"] == rout["avg_jct"]
             assert np.array_equal(og["peak_used"], gp)
+
+
+@pytest.mark.parametrize("block,capacity", [(0, 40 * GiB), (512 * MiB, 40 * GiB + 100 * MiB)])
+def test_oracle_mig_byte_instances_match_reference(ref, olib, block, capacity):
+    """MIG on a byte-granular device (instance tables in bytes, carma_mig_layout)."""
+    for mig in ((0.7, 0.3), (0.75, 0.125, 0.125)):  # the largest instance holds every catalog task
+        cfg = ref_config(policy="magm", mode="mig", mig=mig, capacity=capacity, block=block)
+        for seed in (1, 2):
+            tout, rout, ge, gs, gp = ref_run(ref, cfg, mix="t90", seed=seed)
+            m = cb.materialize_trace(cb.generate_trace("t90", seed))
+            rc, ot, otr, og = oracle_replay(olib, replay_config_from(cfg), m.tasks)
+            assert rc == 0
+            assert np.array_equal(ot["complete"], tout["complete"]) and np.array_equal(ot["ooms"], tout["ooms"])
+            assert otr["energy_mj"] == rout["energy_mj"] and np.array_equal(og["peak_used"], gp)
