@@ -41,7 +41,7 @@ typedef enum carma_status {
     CARMA_ERR_CUDA = 2,        /* no device, launch or copy failure */
     CARMA_ERR_OVERFLOW = 3,    /* a trace exceeded every state capacity tier */
     CARMA_ERR_FAMILY = 4,      /* FamilyMismatch: no model for a requested family */
-    CARMA_ERR_UNSUPPORTED = 5, /* a config outside the kernel's domain (e.g. > 256 blocks) */
+    CARMA_ERR_UNSUPPORTED = 5, /* a config outside the kernel's domain (e.g. > 256 simulated GPUs) */
     CARMA_ERR_INCOMPLETE = 6   /* IncompleteRun: a trace could not finish */
 } carma_status;
 
@@ -577,7 +577,7 @@ typedef struct carma_gpu_view {
 
 typedef struct carma_pick_request {
     uint64_t estimate; /* CARMA_NO_ESTIMATE for none */
-    uint32_t want;     /* gpus_requested (1 or 2) */
+    uint32_t want;     /* gpus_requested (1 or 2; up to 8 in carma_pick_batch_wide) */
     int32_t from_recovery;
 } carma_pick_request;
 
