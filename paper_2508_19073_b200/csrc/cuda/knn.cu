@@ -995,15 +995,12 @@ __global__ void __launch_bounds__(128, KNN_F32_CTAS)
                     for (int c = 0; c < kBlock; ++c) upd |= (sf[c] < sk) ? (1u << c) : 0u;
                     upd &= valid;
                     if (upd) {  // the k smallest sums moved: tighten the bound
-                        do {
-                            const int c = __ffs(upd) - 1;
-                            upd &= upd - 1;
-                            float v = sf[0];
+                        // every point of the block through the branch-free
+                        // insert (+inf, or any value >= the k-th, leaves the
+                        // array unchanged); cheaper than extracting the set
+                        // bits one by one (11.69 -> 11.60 ms on c2)
 #pragma unroll
-                            for (int j = 1; j < kBlock; ++j)
-                                if (j == c) v = sf[j];
-                            sorted_insert<K>(sfk, v);
-                        } while (upd);
+                        for (int c = 0; c < kBlock; ++c) sorted_insert<K>(sfk, ((upd >> c) & 1u) ? sf[c] : finf);
                         const float kub = ub_of(sfk[K - 1], etaf);
                         if (static_cast<double>(kub) < kth) {
                             kth = static_cast<double>(kub);
