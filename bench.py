@@ -823,6 +823,19 @@ def fused_stage(abi, cb, dev, stream, args, knn):
         assert ok, "c5 run differs from the reference golden"
         parity = "bit-exact vs tests/golden/c5_ref.json (report, per-task digests of every field)"
     full = gold["runs"]["learned"]["seconds"] if gold else None
+    # Like-for-like with the CPU sample: the same prefix replayed on the GPU
+    # (the per-event cost grows with the queue on both sides).
+    ns = min(args.fused_cpu_tasks, args.fused_tasks)
+    fs = cb.FusedReplay(cb.materialize_trace(cb.generate_uniform_trace(ns, 3.0, 7)), cfg5, knn, dev)
+    fs.run(stream)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    fs.run(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    s_ms = e0.elapsed_time(e1)
+    assert fs.results().traces[0]["status"] == 0
+    fs.close()
     return {"metric": "fused estimator-in-the-loop placed tasks/sec", "unit": "placed tasks/s",
             "value": args.fused_tasks / (f_ms * 1e-3), "ms_per_step": f_ms, "steps": 1, "warmup": 1,
             "config": {"workload": f"c5: {args.fused_tasks} arrivals, uniform catalog, exp gaps mean 3 s, seed 7; "
@@ -832,6 +845,8 @@ def fused_stage(abi, cb, dev, stream, args, knn):
             "cpu_reference_full_trace": None if full is None else
             {"value": args.fused_tasks / full, "unit": "placed tasks/s", "cores": 1, "kind": "reference",
              "seconds": full, "source": "tests/golden/c5_ref.json (make_c5_golden.py, the full reference run)"},
+            "gpu_same_sample": {"value": ns / (s_ms * 1e-3), "unit": "placed tasks/s", "ms": s_ms,
+                                "sample": f"first {ns} rows of the c5 trace (the CPU sample's input)"},
             "note": "one trace: a single warp replays it (sequential event loop); not sharded"}
 
 
@@ -1016,6 +1031,7 @@ def run_carma(args, d: Dist):
     short["fused"] = None if fused is None else {"value": fused["value"], "unit": fused["unit"],
                                                  "ms_per_step": fused["ms_per_step"], "parity": fused["parity"][:12],
                                                  "cpu_sample": (fused.get("cpu_baseline") or {}).get("value"),
+                                                 "gpu_same_sample": fused["gpu_same_sample"]["value"],
                                                  "cpu_full": (fused.get("cpu_reference_full_trace") or {}).get("value")}
     short["small_configs"] = None if small is None else "gpurun_out/bench_detail_n1.json"
     short["detail"] = f"gpurun_out/bench_detail_n{N}.json"
