@@ -51,11 +51,11 @@ FLOPS_PER_EVAL = 58                # 19 x (sub, mul, add) + 1 weight mul, FMA-fr
 FLOPS_PER_F32_EVAL = 48            # fp32 pre-filter: 16 dims x (sub + fma)
 FEATURE_ROW_BYTES = 136
 # host-buffer calls re-encode every other chunk of 136-B rows (+ 1-B family)
-# into 64-B packed rows on host threads while the copy engine ships the
+# into 40-B compact rows on host threads while the copy engine ships the
 # other chunks raw, so PCIe and host memory bandwidth overlap
 # (csrc/host/stage.cpp); h2d_bytes_per_step is the call's own count
 E2E_API = ("{fn} (pinned 136-B carma_feature_row + family in, bucket + bytes out; half the chunks re-encoded to "
-           "64-B packed rows by the host thread pool inside the call, overlapped with the raw chunks' H2D)")
+           "40-B compact rows by the host thread pool inside the call, overlapped with the raw chunks' H2D)")
 
 
 def log(*a):

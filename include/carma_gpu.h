@@ -129,6 +129,15 @@ typedef struct carma_bit_schema {
 carma_status carma_pack_features_bits(const carma_feature_row* rows, const int8_t* family,
                                       int32_t default_family, uint64_t n, carma_bit_schema* schema,
                                       uint32_t* words, uint64_t* n_words);
+/* The fixed 40-byte bit-packed encoding (ten words per row, every base 0;
+ * field widths: 32 for the six tuple counts and the two totals, 8 per layer
+ * tally, 12 batch, 3 activation code, 4 per kind, 1 has_layers, 4 family with
+ * 15 = none) that carma_knn_predict / carma_nn_predict ship for chunks whose
+ * rows all fit. Fills *schema; words holds n * 10 + 2 (padding) words.
+ * CARMA_ERR_UNSUPPORTED if a row does not fit. */
+carma_status carma_pack_features_compact(const carma_feature_row* rows, const int8_t* family,
+                                         int32_t default_family, uint64_t n, carma_bit_schema* schema,
+                                         uint32_t* words);
 
 carma_status carma_knn_create(int device, carma_knn** out);
 carma_status carma_knn_destroy(carma_knn* h);

@@ -150,6 +150,7 @@ SIGNATURES = {
     "carma_knn_set_act_table": (c_int, [c_void_p, P]),
     "carma_pack_features": (c_int, [P, P, c_int32, c_uint64, P, P]),
     "carma_pack_features_bits": (c_int, [P, P, c_int32, c_uint64, P, P, POINTER(c_uint64)]),
+    "carma_pack_features_compact": (c_int, [P, P, c_int32, c_uint64, P, P]),
     "carma_knn_predict_bitpacked": (c_int, [c_void_p, P, P, c_uint64, P, P]),
     "carma_knn_set_bit_schema": (c_int, [c_void_p, P]),
     "carma_replay_plan_upload_tasks": (c_int, [c_void_p, P]),

@@ -191,6 +191,17 @@ def pack_features_bits(rows: np.ndarray, family=None, default_family: int = 0):
     return words, schema
 
 
+def pack_features_compact(rows: np.ndarray, family=None, default_family: int = 0):
+    """The fixed-schema 40-byte rows the host-buffer predicts ship: (u32 words
+    incl. 2 padding words, schema); CarmaError(UNSUPPORTED) if a row does not fit."""
+    rows = np.ascontiguousarray(rows, abi.feature_row_dtype)
+    fam = None if family is None else np.ascontiguousarray(family, np.int8)
+    schema = np.zeros(1, abi.bit_schema_dtype)
+    words = np.zeros(len(rows) * 10 + 2, np.uint32)
+    check(lib.carma_pack_features_compact(ptr(rows), ptr(fam), default_family, len(rows), ptr(schema), ptr(words)))
+    return words, schema
+
+
 def scalar_features(rows: np.ndarray) -> np.ndarray:
     out = np.zeros((len(rows), 19), np.float64)
     rows = np.ascontiguousarray(rows)

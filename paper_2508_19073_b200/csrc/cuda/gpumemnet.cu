@@ -1469,8 +1469,16 @@ void launch_partition(const NnParams& p, uint64_t q, uint32_t present, uint32_t*
 // One predict on device-resident rows. Returns the number of launches.
 uint64_t run_predict(NnHandle& h, NnHandle::Scratch& sc, const void* rows, int32_t format, const int8_t* family,
                      int32_t default_family, uint64_t q, int32_t* bucket, uint64_t* bytes, float* probs,
-                     float* logits, cudaStream_t s) {
+                     float* logits, cudaStream_t s, const carma_bit_schema* bits = nullptr) {
     NnParams p = base_params(h);
+    if (bits) {  // this call's bit-packed schema instead of the handle's
+        for (int f = 0; f < CARMA_BIT_FIELDS; ++f) {
+            p.bbase[f] = bits->base[f];
+            p.boff[f] = bits->offset[f];
+            p.bw[f] = bits->width[f];
+        }
+        p.bwpr = bits->words_per_row;
+    }
     p.rows = rows;
     p.family = family;
     p.default_family = default_family;
@@ -1604,6 +1612,21 @@ carma_status predict_host(carma_nn* hh, const void* rows, size_t row_bytes, int3
                 if (!sc.staged) CARMA_CUDA(cudaEventCreateWithFlags(&sc.staged, cudaEventDisableTiming));
                 CARMA_CUDA(cudaEventSynchronize(sc.staged));
                 auto* pk = sc.stage_packed.as<carma_feature_packed>();
+                // 40-byte compact rows first (bit-packed, fixed schema), then
+                // the 64-byte packed format, else the raw rows
+                if (compact_rows() &&
+                    pack_rows_compact(static_cast<const carma_feature_row*>(rows) + beg, family ? family + beg : nullptr,
+                                      default_family, cnt, reinterpret_cast<uint64_t*>(pk))) {
+                    const uint64_t nb = cnt * 4ull * kCompactWords;
+                    CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, pk, nb, cudaMemcpyHostToDevice, s));
+                    h2d += nb;
+                    CARMA_CUDA(cudaEventRecord(sc.staged, s));
+                    launches += run_predict(*h, sc, sc.rows.ptr, CARMA_ROWS_BITPACKED, nullptr, default_family, cnt,
+                                            sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(), nullptr, nullptr, s,
+                                            &compact_schema());
+                    copy_out(sc, s, beg, cnt);
+                    continue;
+                }
                 if (pack_rows_canonical(static_cast<const carma_feature_row*>(rows) + beg, family ? family + beg : nullptr,
                                         default_family, cnt, pk)) {
                     CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, pk, cnt * sizeof(carma_feature_packed),

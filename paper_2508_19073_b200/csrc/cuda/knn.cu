@@ -1401,9 +1401,17 @@ uint64_t run_pipeline(KnnHandle& h, KnnHandle::Scratch& sc, const void* rows, in
                       const int8_t* family, int32_t default_family, uint64_t q,
                       int32_t* bucket, uint64_t* bytes, double* d2, int64_t* idx,
                       unsigned long long* evals, cudaStream_t s, int chunk = 0,
-                      bool outer = true) {
+                      bool outer = true, const carma_bit_schema* bits = nullptr) {
     uint32_t n_bins = 0;
     KnnParams p = make_params(h, &n_bins);
+    if (bits) {  // this call's bit-packed schema instead of the handle's
+        for (int f = 0; f < CARMA_BIT_FIELDS; ++f) {
+            p.bbase[f] = bits->base[f];
+            p.boff[f] = bits->offset[f];
+            p.bw[f] = bits->width[f];
+        }
+        p.bwpr = bits->words_per_row;
+    }
     p.rows = rows;
     p.format = format;
     p.family = family;
@@ -1626,6 +1634,21 @@ carma_status predict_host(carma_knn* hh, const void* rows, size_t row_bytes, int
                 if (!sc.staged) CARMA_CUDA(cudaEventCreateWithFlags(&sc.staged, cudaEventDisableTiming));
                 CARMA_CUDA(cudaEventSynchronize(sc.staged));  // the previous copy out of this stage buffer
                 auto* pk = sc.stage_packed.as<carma_feature_packed>();
+                // 40-byte compact rows first (bit-packed, fixed schema), then
+                // the 64-byte packed format, else the raw rows
+                if (compact_rows() &&
+                    pack_rows_compact(static_cast<const carma_feature_row*>(rows) + beg, family ? family + beg : nullptr,
+                                      default_family, cnt, reinterpret_cast<uint64_t*>(pk))) {
+                    const uint64_t nb = cnt * 4ull * kCompactWords;
+                    CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, pk, nb, cudaMemcpyHostToDevice, s));
+                    h2d += nb;
+                    CARMA_CUDA(cudaEventRecord(sc.staged, s));
+                    launches += run_pipeline(*h, sc, sc.rows.ptr, CARMA_ROWS_BITPACKED, nullptr, default_family, cnt,
+                                             sc.bucket.as<int32_t>(), sc.bytes.as<uint64_t>(), nullptr, nullptr,
+                                             h->evals.as<unsigned long long>(), s, 0, true, &compact_schema());
+                    copy_out(sc, s, beg, cnt);
+                    continue;
+                }
                 if (pack_rows_canonical(static_cast<const carma_feature_row*>(rows) + beg, family ? family + beg : nullptr,
                                         default_family, cnt, pk)) {
                     CARMA_CUDA(cudaMemcpyAsync(sc.rows.ptr, pk, cnt * sizeof(carma_feature_packed),

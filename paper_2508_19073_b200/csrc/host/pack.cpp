@@ -5,6 +5,7 @@
 #include <cstring>
 
 #include "../../../include/carma_gpu.h"
+#include "stage.hpp"
 #include "status.hpp"
 
 using namespace carma_b200;
@@ -140,5 +141,23 @@ extern "C" carma_status carma_pack_features_bits(const carma_feature_row* rows, 
                 }
             }
         }
+    });
+}
+
+// The compact 40-byte encoding the host-buffer predicts ship (stage.hpp):
+// bit-packed rows with one fixed schema, so no pass over the batch is needed
+// to size the fields. Rows that do not fit report UNSUPPORTED.
+extern "C" carma_status carma_pack_features_compact(const carma_feature_row* rows, const int8_t* family,
+                                                    int32_t default_family, uint64_t n, carma_bit_schema* schema,
+                                                    uint32_t* words) {
+    return guarded([&] {
+        if (!schema) throw InvalidArg("null argument");
+        *schema = compact_schema();
+        if (n == 0) return;
+        if (!rows || !words) throw InvalidArg("null argument");
+        words[n * kCompactWords] = 0;
+        words[n * kCompactWords + 1] = 0;
+        if (!pack_rows_compact(rows, family, default_family, n, reinterpret_cast<uint64_t*>(words)))
+            throw Unsupported("a row does not fit the compact format");
     });
 }

@@ -132,11 +132,88 @@ inline bool pack_one(const carma_feature_row& r, uint64_t f, const uint64_t* can
     return true;
 }
 
+// One row in the compact encoding (stage.hpp): five u64 words.
+inline bool pack_one_compact(const carma_feature_row& r, uint64_t f, const uint64_t* canon, long long* o) {
+    constexpr uint64_t k32 = 1ull << 32;
+    const uint64_t big = r.total_params | r.total_activations | r.tuple_acts[0] | r.tuple_params[0] |
+                         r.tuple_acts[1] | r.tuple_params[1] | r.tuple_acts[2] | r.tuple_params[2];
+    const uint64_t tally = r.n_linear | r.n_batchnorm | r.n_dropout | r.n_conv;
+    const uint32_t kinds = static_cast<uint32_t>(r.kind[0]) | static_cast<uint32_t>(r.kind[1]) |
+                           static_cast<uint32_t>(r.kind[2]);
+    uint64_t cb, sb;
+    std::memcpy(&cb, &r.act_cos, 8);
+    std::memcpy(&sb, &r.act_sin, 8);
+    uint64_t code = 8;
+    for (uint64_t k = 0; k < 8; ++k)
+        if (cb == canon[2 * k] && sb == canon[2 * k + 1]) code = k;
+    if (big >= k32 || tally > 255 || r.batch_size >= 4096 || kinds > 15 || code == 8) return false;
+    const uint64_t w[5] = {
+        r.total_params | (r.total_activations << 32),
+        r.tuple_acts[0] | (r.tuple_params[0] << 32),
+        r.tuple_acts[1] | (r.tuple_params[1] << 32),
+        r.tuple_acts[2] | (r.tuple_params[2] << 32),
+        r.n_linear | (r.n_batchnorm << 8) | (r.n_dropout << 16) | (r.n_conv << 24) | (r.batch_size << 32) |
+            (code << 44) | (static_cast<uint64_t>(r.kind[0]) << 47) | (static_cast<uint64_t>(r.kind[1]) << 51) |
+            (static_cast<uint64_t>(r.kind[2]) << 55) | (static_cast<uint64_t>(r.has_layers ? 1 : 0) << 59) |
+            (f << 60)};
+    for (int k = 0; k < 5; ++k) _mm_stream_si64(o + k, static_cast<long long>(w[k]));
+    return true;
+}
+
 }  // namespace
+
+const carma_bit_schema& compact_schema() {
+    static const carma_bit_schema s = [] {
+        carma_bit_schema c{};
+        c.words_per_row = kCompactWords;
+        // field order of featurize_bits: 0-6 tallies / batch / totals, 7 act
+        // code, 8-10 kinds, 11 has_layers, 12-17 (acts, params) per tuple, 18 family
+        const struct { int f, off, w; } lay[] = {
+            {5, 0, 32},   {6, 32, 32},  {12, 64, 32},  {13, 96, 32},  {14, 128, 32}, {15, 160, 32}, {16, 192, 32},
+            {17, 224, 32}, {0, 256, 8}, {1, 264, 8},   {2, 272, 8},   {3, 280, 8},   {4, 288, 12},  {7, 300, 3},
+            {8, 303, 4},  {9, 307, 4},  {10, 311, 4},  {11, 315, 1},  {18, 316, 4}};
+        for (const auto& l : lay) {
+            c.offset[l.f] = static_cast<uint16_t>(l.off);
+            c.width[l.f] = static_cast<uint8_t>(l.w);
+        }
+        std::memcpy(c.act_table, canonical_act_table(), sizeof(c.act_table));
+        return c;
+    }();
+    return s;
+}
+
+bool pack_rows_compact(const carma_feature_row* rows, const int8_t* family, int32_t default_family, uint64_t n,
+                       uint64_t* out) {
+    uint64_t canon[16];
+    std::memcpy(canon, canonical_act_table(), sizeof(canon));
+    std::atomic<bool> ok{true};
+    const uint32_t parts = static_cast<uint32_t>(std::min<uint64_t>(host_workers(), (n + 16383) / 16384));
+    host_parallel(parts, [&](uint32_t p, uint32_t np) {
+        const uint64_t b = n * p / np, e = n * (p + 1) / np;
+        bool good = true;
+        for (uint64_t i = b; i < e && good; ++i) {
+            // a negative, absent or unknown family decodes to "no model" (15)
+            const int fi = family ? family[i] : default_family;
+            const uint64_t f = fi >= 0 && fi < 15 ? static_cast<uint64_t>(fi) : 15u;
+            good = pack_one_compact(rows[i], f, canon, reinterpret_cast<long long*>(out + 5 * i));
+        }
+        _mm_sfence();
+        if (!good) ok.store(false, std::memory_order_relaxed);
+    });
+    return ok.load();
+}
 
 void host_parallel(uint32_t parts, const std::function<void(uint32_t, uint32_t)>& fn) { pool().run(parts, fn); }
 
 uint32_t host_workers() { return pool().size(); }
+
+bool compact_rows() {
+    static const bool on = [] {
+        const char* e = std::getenv("CARMA_E2E_COMPACT");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
 
 bool raw_chunk(uint64_t c, bool inputs_pinned) {
     static const uint64_t every = [] {

@@ -296,14 +296,23 @@ def _mixed_rows():
 
 
 def test_host_api_packed_staging_and_raw_fallback(gpu, models):
-    """carma_knn_predict re-encodes host feature rows as 64-byte packed rows per
-    chunk (csrc/host/stage.cpp) and falls back to raw rows for a chunk that
-    does not fit; results equal the device-resident raw-row path bit for bit."""
+    """carma_knn_predict re-encodes host feature rows per chunk
+    (csrc/host/stage.cpp): 40-byte compact rows (bit-packed, fixed schema)
+    when every row fits, else 64-byte packed rows, else the raw rows.
+    Chunks here: [0, 2^18) compact, [2^18, 2^19) raw (a non-registry
+    activation), the rest 64-byte packed (a total_params >= 2^32). Results
+    equal the device-resident raw-row path bit for bit."""
+    import ctypes
     rows, fam = _mixed_rows()
+    rows["total_params"][600_000] = 2**33 + 5
     knn = cb.GpuKnn(gpu)
     for f in models:
         knn.set_model(models[f])
     hb, hby = knn.predict(rows, family=fam, default_family=0)
+    n = ctypes.c_uint64()
+    abi.check(abi.lib.carma_knn_last_h2d_bytes(knn.handle, ctypes.byref(n)))
+    c = 1 << 18
+    assert n.value == 40 * c + 137 * c + 64 * (len(rows) - 2 * c)
     db, dby, _, _ = _device_predict(knn, rows, family=fam, default_family=0)
     assert np.array_equal(hb, db) and np.array_equal(hby, dby)
     assert (hb[fam == -1] == -1).all() and (hby[fam == 7] == np.uint64(2**64 - 1)).all()
@@ -329,6 +338,6 @@ def test_host_api_pinned_rows_mix_raw_and_packed_chunks(gpu, models):
     import ctypes
     n = ctypes.c_uint64()
     abi.check(abi.lib.carma_knn_last_h2d_bytes(knn.handle, ctypes.byref(n)))
-    assert 64 * len(rows) < n.value < 137 * len(rows)  # a mix of packed and raw chunks
+    assert 40 * len(rows) < n.value < 137 * len(rows)  # a mix of compact and raw chunks
     db, dby, _, _ = _device_predict(knn, rows, family=fam, default_family=0)
     assert np.array_equal(hb, db) and np.array_equal(hby, dby)

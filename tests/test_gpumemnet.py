@@ -383,11 +383,16 @@ def test_host_api_packed_staging_and_raw_fallback(gpu, models, path):
     rows, fams = rows[order].copy(), fams[order].copy()
     fams[::991] = -1
     rows["act_cos"][350_001] = 0.3
+    rows["total_params"][590_000] = 2**33 + 5  # that chunk: 64-byte rows, not the 40-byte compact ones
     net = gm.GpuMemNet(gpu)
     net.set_path(path)
     for f in (0, 1, 2):
         net.set_model(models[f])
     hb, hby = net.predict(rows, family=fams, default_family=0)
+    import ctypes
+    n = ctypes.c_uint64()
+    abi.check(abi.lib.carma_nn_last_h2d_bytes(net.handle, ctypes.byref(n)))
+    assert 40 * len(rows) < n.value < 137 * len(rows)  # compact, 64-byte and raw chunks
     db, dby, _, _ = _predict_device(net, rows, abi.ROWS_FEATURES, len(rows), family=fams)
     assert np.array_equal(hb, db) and np.array_equal(hby, dby)
     assert (hb[fams == -1] == -1).all()

@@ -177,6 +177,41 @@ def test_bitpacked_format_is_lossless(families):
     assert int(schema["words_per_row"][0]) * 4 < 64  # denser than the fixed 64-byte packing
 
 
+def test_compact_format_is_lossless_and_rejects_wide_rows():
+    """The fixed-schema 40-byte rows the host-buffer predicts ship (stage.cpp)."""
+    rows, fams = [], []
+    for f in (0, 1, 2):
+        ds = cb.generate_synthetic_dataset(f, 2000, 31 + f)
+        rows.append(ds.rows)
+        fams.append(np.full(2000, f, np.int8))
+    rows, fams = np.concatenate(rows), np.concatenate(fams)
+    fams[::7] = -1
+    fams[3::11] = 9
+    words, schema = cb.pack_features_compact(rows, fams)
+    n = len(rows)
+    assert int(schema["words_per_row"][0]) == 10 and len(words) == 10 * n + 2
+    v = unpack_bits(words, schema, n)
+    for f, name in enumerate(("n_linear", "n_batchnorm", "n_dropout", "n_conv", "batch_size", "total_params",
+                              "total_activations")):
+        assert np.array_equal(v[:, f], rows[name])
+    table = schema["act_table"][0]
+    assert np.array_equal(table[2 * v[:, 7].astype(np.int64)], rows["act_cos"])
+    assert np.array_equal(table[2 * v[:, 7].astype(np.int64) + 1], rows["act_sin"])
+    for k in range(3):
+        assert np.array_equal(v[:, 8 + k].astype(np.int32), rows["kind"][:, k])
+        assert np.array_equal(v[:, 12 + 2 * k], rows["tuple_acts"][:, k])
+        assert np.array_equal(v[:, 13 + 2 * k], rows["tuple_params"][:, k])
+    assert np.array_equal(v[:, 11], (rows["has_layers"] != 0).astype(np.uint64))
+    want_f = np.where((fams >= 0) & (fams < 15), fams, 15).astype(np.uint64)
+    assert np.array_equal(v[:, 18], want_f)
+    for field, value in (("total_params", 2**32), ("batch_size", 4096), ("tuple_acts", 2**32)):
+        bad = rows[:3].copy()
+        bad[field][1] = value
+        with pytest.raises(abi.CarmaError) as e:
+            cb.pack_features_compact(bad, default_family=0)
+        assert e.value.status == 5
+
+
 def test_mig_layout_matches_gpudevice():
     c = cb.make_config(cb.PolicyConfig(collocation_mode="mig"), cb.SimConstants(), None)
     assert c["mig_count"][0] == 2 and list(c["mig_blocks"][0, :2]) == [40, 40]
