@@ -2120,6 +2120,23 @@ carma_status carma_knn_last_timing(carma_knn* hh, double* search_ms, double* pip
     });
 }
 
+// Diagnostic: per chunk of the last timed device call, the search kernel's
+// start and end in ms from the pipeline start (out[2c], out[2c+1]); *n gets
+// the chunk count (at most cap / 2 written).
+extern "C" carma_status carma_debug_knn_chunk_times(carma_knn* hh, float* out, int32_t cap, int32_t* n) {
+    return guarded([&] {
+        KnnHandle* h = reinterpret_cast<KnnHandle*>(hh);
+        if (!h || !out || !n) throw InvalidArg("null argument");
+        DeviceGuard g(h->device);
+        CARMA_CUDA(cudaEventSynchronize(h->ev[3]));
+        *n = h->timed_chunks;
+        for (int c = 0; c < h->timed_chunks && 2 * c + 1 < cap; ++c) {
+            CARMA_CUDA(cudaEventElapsedTime(out + 2 * c, h->ev[0], h->sev[c][0]));
+            CARMA_CUDA(cudaEventElapsedTime(out + 2 * c + 1, h->ev[0], h->sev[c][1]));
+        }
+    });
+}
+
 carma_status carma_knn_last_stats(carma_knn* hh, uint64_t* launches, uint64_t* evaluations) {
     uint64_t visits = 0;
     return carma_knn_last_work(hh, launches, evaluations, &visits);

@@ -69,6 +69,14 @@ def knn(args):
         abi.check(abi.lib.carma_knn_last_timing(k.handle, ctypes.byref(sm), ctypes.byref(pm)))
         print(f"knn {len(rows)} rows: search {sm.value:.2f} ms pipeline {pm.value:.2f} ms stats {k.last_stats()}",
               flush=True)
+    fn = getattr(abi.lib, "carma_debug_knn_chunk_times", None)
+    if fn is not None:
+        fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
+        out = np.zeros(16, np.float32)
+        n = ctypes.c_int32()
+        abi.check(fn(k.handle, out.ctypes.data, 16, ctypes.byref(n)))
+        print("chunk search windows (ms from pipeline start):",
+              [(round(float(out[2 * c]), 3), round(float(out[2 * c + 1]), 3)) for c in range(min(n.value, 8))])
 
 
 def nn(args):
