@@ -49,14 +49,16 @@
 namespace carma_b200 {
 namespace replay {
 
-// Shared-memory tiers: 64 registers, 8 CTAs x 4 warps resident (throughput
-// of many jobs). The large tier (one long trace per warp, latency bound)
-// and the global tier take all the registers they want.
+// Shared-memory tiers: 72 registers, 7 CTAs x 4 warps resident (throughput
+// of many jobs; c4 on B200: 8 CTAs / 64 registers 139.1 ms, 7 / 72 125.5,
+// 6 / 74 125.9, 5 / 81 134.4, 4 / 91 133.5, 9 / 56 (spills) 153.3). The large
+// tier (one long trace per warp, latency bound) and the global tier take all
+// the registers they want.
 #ifndef REPLAY_KLATER_CHAIN
 #define REPLAY_KLATER_CHAIN 1
 #endif
 #ifndef REPLAY_MIN_CTAS
-#define REPLAY_MIN_CTAS 8
+#define REPLAY_MIN_CTAS 7
 #endif
 
 #ifndef REPLAY_PROF
