@@ -281,7 +281,10 @@ __global__ void __launch_bounds__(256) knn_unpermute(uint64_t q, const uint32_t*
 constexpr uint32_t kPrepKeysMax = 8192;
 
 template <int FMT>
-__global__ void __launch_bounds__(512, 2) knn_prep(KnnParams p, uint32_t n_bins, uint32_t* __restrict__ qbin, uint32_t* __restrict__ qpos,
+#ifndef KNN_PREP_MINB
+#define KNN_PREP_MINB 2
+#endif
+__global__ void __launch_bounds__(512, KNN_PREP_MINB) knn_prep(KnnParams p, uint32_t n_bins, uint32_t* __restrict__ qbin, uint32_t* __restrict__ qpos,
                          uint32_t* __restrict__ hist, int keys_in_smem) {
     extern __shared__ __align__(16) uint32_t sh[];
     double* skeys = reinterpret_cast<double*>(sh + ((n_bins + 3) & ~3u));
