@@ -805,8 +805,11 @@ constexpr int kFfIn = 20;
 #define NN_FFMA_ROWS 2
 #endif
 
+#ifndef NN_FFMA_MINB
+#define NN_FFMA_MINB 1
+#endif
 template <int FMT, int R, int CP, bool DIAG>
-__global__ void __launch_bounds__(128) mlp_ffma(const __grid_constant__ NnParams p) {
+__global__ void __launch_bounds__(128, NN_FFMA_MINB) mlp_ffma(const __grid_constant__ NnParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const NnModelDev& m = p.m;
     {
