@@ -805,11 +805,17 @@ constexpr int kFfIn = 20;
 #define NN_FFMA_ROWS 2
 #endif
 
+// NN_FFMA_MINB > 0 caps the registers (A/B knob; uncapped measured fastest)
 #ifndef NN_FFMA_MINB
-#define NN_FFMA_MINB 1
+#define NN_FFMA_MINB 0
+#endif
+#if NN_FFMA_MINB > 0
+#define NN_FFMA_BOUNDS __launch_bounds__(128, NN_FFMA_MINB)
+#else
+#define NN_FFMA_BOUNDS __launch_bounds__(128)
 #endif
 template <int FMT, int R, int CP, bool DIAG>
-__global__ void __launch_bounds__(128, NN_FFMA_MINB) mlp_ffma(const __grid_constant__ NnParams p) {
+__global__ void NN_FFMA_BOUNDS mlp_ffma(const __grid_constant__ NnParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const NnModelDev& m = p.m;
     {
