@@ -220,7 +220,13 @@ bool raw_chunk(uint64_t c, bool inputs_pinned) {
         const char* e = std::getenv("CARMA_E2E_RAW_EVERY");
         return e ? std::strtoull(e, nullptr, 10) : 2ull;
     }();
-    return inputs_pinned && every > 0 && c % every == every - 1;
+    // CARMA_E2E_RAW_FIRST=1: the raw chunks are 0, k, 2k, ... (the copy
+    // engine starts at once while the pool packs chunk 1)
+    static const uint64_t phase = [] {
+        const char* e = std::getenv("CARMA_E2E_RAW_FIRST");
+        return e && std::atoi(e) != 0 ? 0ull : 1ull;
+    }();
+    return inputs_pinned && every > 0 && (c + phase) % every == 0;
 }
 
 bool pack_rows_canonical(const carma_feature_row* rows, const int8_t* family, int32_t default_family, uint64_t n,
